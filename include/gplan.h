@@ -1,0 +1,234 @@
+/* gplan.h — C ABI of the B200 plan-evaluation engine (libgplan.so).
+ *
+ * Drop-in boundary for the hot path of the rlsched reference scheduler
+ * (arXiv 2511.00796, /root/reference/proj). The reference has no plugin
+ * registry: its seam is the C++ free-function API that
+ * `evaluate_partition` / `partition_with_widening` call
+ * (src/scheduler.cpp:77-131). Each entry point below replaces exactly one of
+ * those functions; the C++ shim in paper_2511_00796_b200/shim/ re-exposes them
+ * under the reference signatures so the reference scheduler.cpp links
+ * unchanged.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; caller owns every input buffer (borrowed
+ *     for the duration of the call) and every output buffer.
+ *   - No exceptions cross the ABI. Every function returns a gp_status; the
+ *     C++ shim rethrows the matching rlsched exception (inc/common.hpp:11-39).
+ *   - Calls are synchronous and blocking; one host thread per context.
+ *   - All arithmetic is IEEE fp64 without contraction and reproduces the
+ *     reference bit-for-bit.
+ *   - A context owns its CUDA device buffers and stream; there is no CPU
+ *     fallback: if the CUDA device or the kernels are unavailable,
+ *     gp_ctx_create fails with GP_CUDA_ERROR.
+ */
+#ifndef GPLAN_H_
+#define GPLAN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GP_ABI_VERSION 1
+
+/* Limits of the fixed-size result records. */
+#define GP_MAX_TYPES 8           /* gpu types in one cluster                          */
+#define GP_MAX_STAGES 32         /* pipeline stages of a train plan (4 per type run)  */
+#define GP_MAX_ROLLOUT_STAGES 8  /* pipeline stages of one rollout replica config     */
+
+typedef enum {
+  GP_OK = 0,
+  GP_INFEASIBLE = 1,       /* rlsched::InfeasibleError       */
+  GP_BAND_INFEASIBLE = 2,  /* rlsched::BandInfeasibleError   */
+  GP_INVALID = 3,          /* rlsched::ValidationError       */
+  GP_CUDA_ERROR = 4,       /* device/runtime failure (no fallback) */
+  GP_CAPACITY = 5          /* caller-provided output buffer too small */
+} gp_status;
+
+/* ---- inputs (mirror inc/cluster.hpp:16-59, inc/workload.hpp:43-66,
+ *      inc/calibration.hpp:15-33) ---------------------------------------- */
+
+/* ClusterGraph (inc/cluster.hpp:40-63) flattened to SoA. SI units. */
+typedef struct {
+  int32_t n_devices;
+  int32_t n_types;
+  int32_t n_machines;
+  const int32_t* device_type;     /* [n_devices] GpuDevice::gpu_type            */
+  const int32_t* device_machine;  /* [n_devices] GpuDevice::machine_id          */
+  const double* device_flops;     /* [n_devices] GpuDevice::flops               */
+  const double* device_hbm_bw;    /* [n_devices] GpuDevice::hbm_bandwidth       */
+  const double* device_hbm_cap;   /* [n_devices] GpuDevice::hbm_capacity        */
+  const double* type_flops;       /* [n_types]   GpuTypeInfo::flops             */
+  const double* type_hbm_bw;      /* [n_types]   GpuTypeInfo::hbm_bandwidth     */
+  const double* type_hbm_cap;     /* [n_types]   GpuTypeInfo::hbm_capacity      */
+  const double* links;            /* [n_devices^2] row-major, bytes/s           */
+} gp_cluster;
+
+/* WorkloadSpec scalars (inc/workload.hpp:43-66). */
+typedef struct {
+  double model_params_b;
+  int32_t num_layers;
+  int32_t hidden_dim;
+  int32_t batch_rollouts;
+  int32_t prompt_len;
+  double mean_len;                /* LengthDistribution::mean()                 */
+  double bytes_per_param_train;
+  double bytes_per_param_infer;
+  double reward_cost_const;
+  int32_t micro_batches;
+  int32_t staleness;
+} gp_workload;
+
+/* Calibration (inc/calibration.hpp:15-33), per-type efficiencies by type index. */
+typedef struct {
+  const double* compute_eff;      /* [n_types] */
+  const double* io_eff;           /* [n_types] */
+  double sync_latency_s;
+  double stage_latency_penalty;
+  int32_t max_concurrency;
+  double activation_coeff;
+  double tp_allreduce_coeff;
+  double grad_bytes_per_param;
+} gp_calib;
+
+/* ---- options (inc/train_search.hpp:12-17, inc/rollout_milp.hpp:14-16,
+ *      inc/partition.hpp:10-30) ---------------------------------------------- */
+typedef struct {
+  int32_t max_stages_per_type;       /* default 4  */
+  int32_t device_granularity_limit;  /* default 16 */
+} gp_train_opts;
+
+typedef struct {
+  int32_t max_stages;                /* default 4 (<= GP_MAX_ROLLOUT_STAGES) */
+} gp_rollout_opts;
+
+typedef struct {
+  double q, r, gamma_l, gamma_h;     /* GammaState */
+} gp_gamma;
+
+typedef struct {
+  int32_t exact_threshold;           /* default 12     */
+  int32_t restarts;                  /* default 16     */
+  uint64_t seed;                     /* default 0x5eed */
+  double band_epsilon;               /* default 1e-9   */
+  int32_t force_local_search;
+  int32_t machine_granularity;
+} gp_part_opts;
+
+/* ---- results --------------------------------------------------------------- */
+
+typedef struct {
+  int32_t first;   /* offset into the caller's stage_devices buffer */
+  int32_t count;   /* tp * dp                                       */
+  int32_t tp, dp, layers;
+} gp_stage;
+
+/* std::optional<TrainSearchResult> (inc/train_search.hpp:19-33). */
+typedef struct {
+  int32_t found;          /* 0 == std::nullopt: no memory-feasible layout   */
+  int32_t n_stages;
+  double cost;            /* C_T = window * per_step (TrainSearchResult::cost) */
+  int64_t rank;           /* rank of the winner in the reference enumeration order */
+  int64_t layouts;        /* candidate layouts evaluated (the range size)   */
+  int64_t feasible;       /* memory-feasible layouts among them             */
+  gp_stage stage[GP_MAX_STAGES];
+} gp_train_result;
+
+/* ReplicaConfig (inc/plans.hpp:47-66); machine_footprint == tp_per_stage. */
+typedef struct {
+  int32_t type_counts[GP_MAX_TYPES];
+  int32_t n_stages;
+  int32_t tp[GP_MAX_ROLLOUT_STAGES];
+  double throughput;
+} gp_config;
+
+typedef struct {
+  int32_t config;         /* index into the config list passed to gp_solve_milp */
+  int32_t replicas;       /* y */
+  double workload;        /* x */
+} gp_rollout_entry;
+
+/* RolloutPlan (inc/plans.hpp:75-85). entries is caller-provided. */
+typedef struct {
+  int32_t n_entries;
+  double makespan;
+  double total_rollouts;
+  double aggregate;       /* best[full state] */
+  int64_t states;         /* lattice size */
+} gp_rollout_result;
+
+/* PartitionResult (inc/partition.hpp:32-36); train ids are written to a
+ * caller buffer at train_offset. */
+typedef struct {
+  int32_t train_offset;
+  int32_t train_count;
+  double objective;
+  double compute_fraction;
+} gp_partition;
+
+typedef struct gp_ctx gp_ctx;
+
+/* ---- lifecycle ------------------------------------------------------------- */
+
+/* Validates and uploads the cluster/workload/calibration to `device`
+ * (CUDA ordinal). Fails with GP_CUDA_ERROR when no usable sm_100 device or
+ * kernel image exists. */
+int gp_ctx_create(const gp_cluster* cluster, const gp_workload* work, const gp_calib* calib,
+                  int device, gp_ctx** out);
+void gp_ctx_destroy(gp_ctx* ctx);
+/* Message of the last failing call on this thread. */
+const char* gp_last_error(void);
+int gp_abi_version(void);
+/* Kernel launches issued by this context so far (diagnostics / bench claim). */
+long long gp_ctx_launches(gp_ctx* ctx);
+
+/* ---- training side: replaces constrained_search (src/train_search.cpp:268-325) */
+
+/* Number of layouts constrained_search would enumerate for `ids`
+ * (enumerate_block_lists, src/train_search.cpp:176-192), without materialising. */
+int gp_train_space(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* opts,
+                   int64_t* layouts);
+
+/* constrained_search(train_set, cluster, work, calib, window, options)
+ * (inc/train_search.hpp:29-33). stage_devices must hold n ints; stage s owns
+ * stage_devices[stage[s].first .. +count). Empty train set -> GP_INVALID. */
+int gp_constrained_search(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
+                          const gp_train_opts* opts, gp_train_result* out,
+                          int32_t* stage_devices);
+
+/* Same search restricted to layout ranks [lo, hi): the shard one GPU scans in
+ * the multi-GPU split. The global winner is the lexicographic
+ * min of (cost, rank) over shards. */
+int gp_constrained_search_range(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
+                                const gp_train_opts* opts, int64_t lo, int64_t hi,
+                                gp_train_result* out, int32_t* stage_devices);
+
+/* ---- rollout side: replaces enumerate_configs / rollout_capacities / solve_milp
+ *      (src/rollout_milp.cpp:113-254) ------------------------------------- */
+
+int gp_enumerate_configs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_rollout_opts* opts,
+                         gp_config* out, int32_t cap, int32_t* n_out);
+int gp_rollout_capacities(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t* caps);
+/* Exact makespan DP. entries must hold n_configs records. B <= 0 -> empty plan. */
+int gp_solve_milp(gp_ctx* ctx, const gp_config* configs, int32_t n_configs, const int32_t* caps,
+                  int32_t dims, double total_rollouts, double mean_len, gp_rollout_result* out,
+                  gp_rollout_entry* entries);
+
+/* ---- weight sync: replaces weight_sync_cost (src/cost_model.cpp:255-277) ---- */
+int gp_weight_sync_cost(gp_ctx* ctx, const int32_t* train, int32_t n_train, const int32_t* rollout,
+                        int32_t n_rollout, const int32_t* entry_types,
+                        const int32_t* entry_replicas, int32_t n_entries, int32_t window,
+                        double* out);
+
+/* ---- repartition: replaces graph_partition_candidates (src/partition.cpp:426-463) */
+/* out holds up to k records; train_ids holds up to k * n_devices ints. */
+int gp_partition_candidates(gp_ctx* ctx, const gp_gamma* gamma, const gp_part_opts* opts,
+                            int32_t k, gp_partition* out, int32_t* train_ids, int32_t* n_out);
+int gp_partition_objective(gp_ctx* ctx, const int32_t* train, int32_t n_train, double* objective,
+                           double* fraction);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPLAN_H_ */

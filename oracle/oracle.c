@@ -1,0 +1,733 @@
+/* oracle.c — TEST INFRASTRUCTURE ONLY: plain-C restatement of the rlsched hot path.
+ *
+ * Each function cites the reference file:line it restates (paths relative to
+ * /root/reference/proj). This file is the parity checker for the CUDA engine;
+ * it is never linked into libgplan.so and the product never calls it.
+ * Floating point: every expression keeps the reference's association order
+ * and is compiled with -ffp-contract=off (no FMA), like the reference's
+ * SSE2 scalar object code.
+ */
+#include "oracle.h"
+
+#include <limits.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define K_INF 1e30            /* inc/common.hpp:41 */
+#define K_ACT_BYTES 2.0       /* src/cost_model.cpp:10 */
+
+static _Thread_local char g_err[512];
+
+int or__fail(int code, const char* fmt, ...);
+#define fail or__fail
+int or__fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+const char* or_last_error(void) { return g_err; }
+void or_free(void* p) { free(p); }
+
+/* ---------------------------------------------------------------- workload */
+/* inc/workload.hpp:51-58 */
+static double w_params(const gp_workload* w) { return w->model_params_b * 1e9; }
+static double w_mean_total_len(const gp_workload* w) { return w->prompt_len + w->mean_len; }
+static double w_tokens(const gp_workload* w) {
+  return w->batch_rollouts * w_mean_total_len(w);
+}
+static double w_model_bytes_infer(const gp_workload* w) {
+  return w_params(w) * w->bytes_per_param_infer;
+}
+static double w_kv_bytes_per_token(const gp_workload* w) {
+  return 4.0 * w->hidden_dim * w->num_layers;
+}
+
+static double link(const gp_cluster* c, int a, int b) {
+  return c->links[(size_t)a * (size_t)c->n_devices + (size_t)b];
+}
+
+/* x86 cvttsd2si: out-of-range / NaN -> INT_MIN (SURVEY 8a rule 4). */
+static int trunc_i32_x86(double x) {
+  if (!(x > -2147483649.0 && x < 2147483648.0)) return INT_MIN;
+  return (int)x;
+}
+
+/* ================================================================ training */
+
+/* stage descriptor used while scoring one layout */
+typedef struct {
+  const int32_t* dev;  /* devices of the block, canonical order */
+  int n;
+} block_t;
+
+/* min_link_within_groups (src/cost_model.cpp:12-36) */
+static double min_link_groups(const gp_cluster* c, const int32_t* dev, int n, int gsize,
+                              int strided, int stride) {
+  double m = K_INF;
+  int groups = n / gsize;
+  for (int g = 0; g < groups; ++g)
+    for (int i = 0; i < gsize; ++i)
+      for (int j = i + 1; j < gsize; ++j) {
+        int a = strided ? dev[i * stride + g] : dev[g * gsize + i];
+        int b = strided ? dev[j * stride + g] : dev[g * gsize + j];
+        double l = link(c, a, b);
+        if (l < m) m = l;
+      }
+  return m;
+}
+
+/* min_link_between (src/cost_model.cpp:38-47) */
+static double min_link_between(const gp_cluster* c, block_t a, block_t b) {
+  double m = K_INF;
+  for (int i = 0; i < a.n; ++i)
+    for (int j = 0; j < b.n; ++j) {
+      double l = link(c, a.dev[i], b.dev[j]);
+      if (l < m) m = l;
+    }
+  return m;
+}
+
+typedef struct {
+  double compute, tp_comm, dp_comm;
+} stage_cost_t;
+
+/* train_stage_cost (src/cost_model.cpp:57-91) */
+static stage_cost_t train_stage_cost(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                                     block_t b, int tp, int dp, int layers, int total_layers) {
+  stage_cost_t sc = {0, 0, 0};
+  const double tokens = w_tokens(w);
+  const int type = c->device_type[b.dev[0]];
+  double cap = 0;
+  for (int i = 0; i < b.n; ++i) cap += c->device_flops[b.dev[i]];
+  double lf = total_layers > 0 ? (double)layers / total_layers : 0;
+  double need = 6.0 * w_params(w) * tokens * lf;
+  sc.compute = need / (k->compute_eff[type] * cap);
+  if (tp > 1 && tokens > 0) {
+    double beta = min_link_groups(c, b.dev, b.n, tp, 0, 0);
+    double prt = tokens / dp;
+    double vol = k->tp_allreduce_coeff * layers * prt * w->hidden_dim * K_ACT_BYTES * 2.0 *
+                 (tp - 1) / tp;
+    sc.tp_comm = vol / beta;
+  }
+  if (dp > 1) {
+    double beta = min_link_groups(c, b.dev, b.n, dp, 1, tp);
+    double shard = w_params(w) * lf * k->grad_bytes_per_param / tp;
+    double vol = 2.0 * shard * (dp - 1) / dp;
+    sc.dp_comm = vol / beta;
+  }
+  return sc;
+}
+
+/* mem_cumsum_train (src/cost_model.cpp:198-207) */
+static double mem_train_gb(const gp_workload* w, const gp_calib* k, int tp, int dp, int layers) {
+  double lf = (double)layers / w->num_layers;
+  double weight = w_params(w) * lf * w->bytes_per_param_train / tp;
+  double tpm = w_tokens(w) / dp / w->micro_batches;
+  double act = k->activation_coeff * tpm * w->hidden_dim * K_ACT_BYTES * layers / tp;
+  return (weight + act) / 1e9;
+}
+
+/* allocate_layers (src/train_search.cpp:146-177). Returns 0 or GP_INVALID. */
+static int allocate_layers(int L, const double* f, int S, int* layers) {
+  if (S < 1 || L < S) return fail(GP_INVALID, "cannot allocate %d layers to %d stages", L, S);
+  double total = 0.0;
+  for (int s = 0; s < S; ++s) total += f[s];
+  double rem[GP_MAX_STAGES];
+  int order[GP_MAX_STAGES];
+  int assigned = 0;
+  for (int s = 0; s < S; ++s) {
+    double share = L * f[s] / total;
+    layers[s] = (int)share;
+    assigned += layers[s];
+    rem[s] = share - layers[s];
+  }
+  /* stable sort by remainder, descending (insertion sort is stable) */
+  for (int s = 0; s < S; ++s) {
+    int j = s;
+    while (j > 0 && rem[order[j - 1]] < rem[s]) {
+      order[j] = order[j - 1];
+      --j;
+    }
+    order[j] = s;
+  }
+  for (int i = 0; i < L - assigned; ++i) layers[order[i % S]]++;
+  for (int s = 0; s < S; ++s) {
+    while (layers[s] == 0) {
+      int donor = 0;
+      for (int t = 1; t < S; ++t)
+        if (layers[t] > layers[donor]) donor = t;
+      layers[donor]--;
+      layers[s]++;
+    }
+  }
+  return 0;
+}
+
+typedef struct {
+  const gp_cluster* c;
+  int32_t* ordered;      /* canonical order (src/train_search.cpp:13-22) */
+  int n;
+  int n_runs;
+  int run_start[GP_MAX_TYPES + 1];
+  int run_len[GP_MAX_TYPES];
+  int* cuts[GP_MAX_TYPES];   /* cut positions per run (local indices) */
+  int n_cuts[GP_MAX_TYPES];
+  int max_stages, max_per_run;
+} layout_space_t;
+
+static const gp_cluster* g_sort_cluster;
+static int cmp_canonical(const void* pa, const void* pb) {
+  int a = *(const int32_t*)pa, b = *(const int32_t*)pb;
+  const gp_cluster* c = g_sort_cluster;
+  if (c->device_type[a] != c->device_type[b]) return c->device_type[a] < c->device_type[b] ? -1 : 1;
+  if (c->device_machine[a] != c->device_machine[b])
+    return c->device_machine[a] < c->device_machine[b] ? -1 : 1;
+  return a < b ? -1 : (a > b);
+}
+
+static void space_free(layout_space_t* sp) {
+  free(sp->ordered);
+  for (int r = 0; r < sp->n_runs; ++r) free(sp->cuts[r]);
+}
+
+/* canonical_order + build_runs + enumerate_block_lists setup
+ * (src/train_search.cpp:13-50,126-142) */
+static int space_build(layout_space_t* sp, const gp_cluster* c, const gp_workload* w,
+                       const int32_t* ids, int n, const gp_train_opts* o) {
+  memset(sp, 0, sizeof *sp);
+  sp->c = c;
+  sp->n = n;
+  sp->ordered = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  for (int i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= c->n_devices) {
+      free(sp->ordered);
+      sp->ordered = NULL;
+      return fail(GP_INVALID, "unknown device id %d", ids[i]);
+    }
+    sp->ordered[i] = ids[i];
+  }
+  g_sort_cluster = c;
+  qsort(sp->ordered, (size_t)n, sizeof(int32_t), cmp_canonical);
+  int dev_gran = n <= o->device_granularity_limit;
+  for (int i = 0; i < n; ++i) {
+    int t = c->device_type[sp->ordered[i]];
+    if (i == 0 || c->device_type[sp->ordered[i - 1]] != t) {
+      if (sp->n_runs == GP_MAX_TYPES) return fail(GP_INVALID, "too many runs");
+      sp->run_start[sp->n_runs++] = i;
+    }
+  }
+  sp->run_start[sp->n_runs] = n;
+  for (int r = 0; r < sp->n_runs; ++r) {
+    int s0 = sp->run_start[r], len = sp->run_start[r + 1] - s0;
+    sp->run_len[r] = len;
+    sp->cuts[r] = (int*)malloc(sizeof(int) * (size_t)(len > 0 ? len : 1));
+    sp->n_cuts[r] = 0;
+    for (int i = 1; i < len; ++i) {
+      int edge = c->device_machine[sp->ordered[s0 + i]] != c->device_machine[sp->ordered[s0 + i - 1]];
+      if (dev_gran || edge) sp->cuts[r][sp->n_cuts[r]++] = i;
+    }
+  }
+  sp->max_per_run = o->max_stages_per_type;
+  int ms = sp->n_runs * o->max_stages_per_type;
+  sp->max_stages = w->num_layers < ms ? w->num_layers : ms;
+  if (sp->max_stages > GP_MAX_STAGES) return fail(GP_INVALID, "max_stages exceeds GP_MAX_STAGES");
+  return 0;
+}
+
+typedef struct {
+  layout_space_t* sp;
+  const gp_workload* w;
+  const gp_calib* k;
+  int window;
+  int64_t rank, lo, hi;
+  int64_t feasible;
+  int have_best;
+  double best_cost;
+  int64_t best_rank;
+  int n_blocks;
+  int blk_start[GP_MAX_STAGES];  /* absolute offsets into ordered */
+  int blk_len[GP_MAX_STAGES];
+  int best_n;
+  int best_start[GP_MAX_STAGES], best_len[GP_MAX_STAGES];
+  int best_tp[GP_MAX_STAGES], best_dp[GP_MAX_STAGES], best_layers[GP_MAX_STAGES];
+  int scoring;  /* 0: count only */
+  int err;
+} search_t;
+
+/* max_devices_per_machine (src/train_search.cpp:124-131). A block lies inside one
+ * type run of the canonical order, so equal machine ids are contiguous. */
+static int max_per_machine(const gp_cluster* c, const int32_t* dev, int n) {
+  int best = 0, run = 0;
+  for (int i = 0; i < n; ++i) {
+    run = (i > 0 && c->device_machine[dev[i]] == c->device_machine[dev[i - 1]]) ? run + 1 : 1;
+    if (run > best) best = run;
+  }
+  return best;
+}
+
+/* one layout: constrained_search loop body (src/train_search.cpp:277-322) */
+static void score_layout(search_t* st) {
+  const gp_cluster* c = st->sp->c;
+  const gp_workload* w = st->w;
+  const int S = st->n_blocks;
+  double f[GP_MAX_STAGES];
+  int layers[GP_MAX_STAGES], tps[GP_MAX_STAGES], dps[GP_MAX_STAGES];
+  block_t blk[GP_MAX_STAGES];
+  for (int s = 0; s < S; ++s) {
+    blk[s].dev = st->sp->ordered + st->blk_start[s];
+    blk[s].n = st->blk_len[s];
+    double acc = 0;
+    for (int i = 0; i < blk[s].n; ++i) acc += c->device_flops[blk[s].dev[i]];
+    f[s] = acc;
+  }
+  if (allocate_layers(w->num_layers, f, S, layers)) {
+    st->err = GP_INVALID;
+    return;
+  }
+  for (int s = 0; s < S; ++s) {
+    double best_comm = -1;
+    int per_machine = max_per_machine(c, blk[s].dev, blk[s].n);
+    static const int tp_opts[4] = {1, 2, 4, 8};
+    for (int o = 0; o < 4; ++o) {
+      int tp = tp_opts[o];
+      if (tp > per_machine || blk[s].n % tp != 0) continue;
+      int dp = blk[s].n / tp;
+      double need_gb = mem_train_gb(w, st->k, tp, dp, layers[s]);
+      if (need_gb * 1e9 > c->device_hbm_cap[blk[s].dev[0]]) continue;
+      stage_cost_t sc = train_stage_cost(c, w, st->k, blk[s], tp, dp, layers[s], w->num_layers);
+      double comm = sc.tp_comm + sc.dp_comm;
+      if (best_comm < 0 || comm < best_comm) {
+        best_comm = comm;
+        tps[s] = tp;
+        dps[s] = dp;
+      }
+    }
+    if (best_comm < 0) return; /* dead layout */
+  }
+  st->feasible++;
+  /* train_step_cost -> train_cost_breakdown (src/cost_model.cpp:93-126) */
+  int total_layers = 0;
+  for (int s = 0; s < S; ++s) total_layers += layers[s];
+  double max_stage = 0, max_compute = 0;
+  for (int s = 0; s < S; ++s) {
+    stage_cost_t sc = train_stage_cost(c, w, st->k, blk[s], tps[s], dps[s], layers[s], total_layers);
+    double tot = sc.compute + sc.tp_comm + sc.dp_comm;
+    if (tot > max_stage) max_stage = tot;   /* std::max(max, v): v only if max < v */
+    if (sc.compute > max_compute) max_compute = sc.compute;
+  }
+  double fill = 0, transfers = 0;
+  const double tokens = w_tokens(w);
+  if (S > 1) {
+    fill = (double)(S - 1) / w->micro_batches * max_compute;
+    if (tokens > 0) {
+      for (int s = 0; s + 1 < S; ++s) {
+        double beta = min_link_between(c, blk[s], blk[s + 1]);
+        transfers += tokens * w->hidden_dim * K_ACT_BYTES / beta;
+      }
+    }
+  }
+  double per_step = max_stage + fill + transfers;
+  double cost = st->window * per_step;
+  if (!st->have_best || cost < st->best_cost) {
+    st->have_best = 1;
+    st->best_cost = cost;
+    st->best_rank = st->rank;
+    st->best_n = S;
+    for (int s = 0; s < S; ++s) {
+      st->best_start[s] = st->blk_start[s];
+      st->best_len[s] = st->blk_len[s];
+      st->best_tp[s] = tps[s];
+      st->best_dp[s] = dps[s];
+      st->best_layers[s] = layers[s];
+    }
+  }
+}
+
+static void visit_leaf(search_t* st) {
+  if (st->scoring && st->rank >= st->lo && st->rank < st->hi && !st->err) score_layout(st);
+  st->rank++;
+}
+
+static void recurse_runs(search_t* st, int r, int used);
+
+/* run_compositions (src/train_search.cpp:53-72): choose k-1 cuts in lexicographic order */
+static void recurse_cuts(search_t* st, int r, int used, int k, int chosen, int next_cut, int prev) {
+  layout_space_t* sp = st->sp;
+  int base = sp->run_start[r];
+  if (chosen == k - 1) {
+    st->blk_start[used + chosen] = base + prev;
+    st->blk_len[used + chosen] = sp->run_len[r] - prev;
+    st->n_blocks = used + k;
+    recurse_runs(st, r + 1, used + k);
+    return;
+  }
+  int remaining = k - 1 - chosen;
+  for (int ci = next_cut; ci + remaining <= sp->n_cuts[r]; ++ci) {
+    int cut = sp->cuts[r][ci];
+    st->blk_start[used + chosen] = base + prev;
+    st->blk_len[used + chosen] = cut - prev;
+    recurse_cuts(st, r, used, k, chosen + 1, ci + 1, cut);
+  }
+}
+
+/* Enumerator::recurse (src/train_search.cpp:95-124) */
+static void recurse_runs(search_t* st, int r, int used) {
+  layout_space_t* sp = st->sp;
+  if (r == sp->n_runs) {
+    visit_leaf(st);
+    return;
+  }
+  int remaining_runs = sp->n_runs - r - 1;
+  int kmax = sp->max_per_run < sp->run_len[r] ? sp->max_per_run : sp->run_len[r];
+  for (int k = 1; k <= kmax; ++k) {
+    if (used + k + remaining_runs > sp->max_stages) break;
+    recurse_cuts(st, r, used, k, 0, 0, 0);
+  }
+}
+
+/* Layout count without enumeration: cnt[r][u] recurrence. */
+static int64_t binom(int n, int k) {
+  if (k < 0 || k > n) return 0;
+  int64_t v = 1;
+  for (int i = 1; i <= k; ++i) v = v * (n - k + i) / i;
+  return v;
+}
+
+static int64_t count_layouts(const layout_space_t* sp) {
+  if (sp->max_stages < sp->n_runs) return 0;
+  int64_t cnt[GP_MAX_TYPES + 1][GP_MAX_STAGES + 2];
+  memset(cnt, 0, sizeof cnt);
+  for (int u = 0; u <= sp->max_stages; ++u) cnt[sp->n_runs][u] = 1;
+  for (int r = sp->n_runs - 1; r >= 0; --r) {
+    int remaining_runs = sp->n_runs - r - 1;
+    for (int u = 0; u <= sp->max_stages; ++u) {
+      int64_t acc = 0;
+      int kmax = sp->max_per_run < sp->run_len[r] ? sp->max_per_run : sp->run_len[r];
+      for (int k = 1; k <= kmax; ++k) {
+        if (u + k + remaining_runs > sp->max_stages) break;
+        acc += binom(sp->n_cuts[r], k - 1) * cnt[r + 1][u + k];
+      }
+      cnt[r][u] = acc;
+    }
+  }
+  return cnt[0][0];
+}
+
+int or_train_space(const gp_cluster* c, const gp_workload* w, const int32_t* ids, int32_t n,
+                   const gp_train_opts* opts, int64_t* layouts) {
+  layout_space_t sp;
+  int rc = space_build(&sp, c, w, ids, n, opts);
+  if (rc) return rc;
+  *layouts = count_layouts(&sp);
+  space_free(&sp);
+  return GP_OK;
+}
+
+/* constrained_search (src/train_search.cpp:268-325), restricted to ranks [lo, hi). */
+int or_constrained_search(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                          const int32_t* ids, int32_t n, int32_t window, const gp_train_opts* opts,
+                          int64_t lo, int64_t hi, gp_train_result* out, int32_t* stage_devices) {
+  memset(out, 0, sizeof *out);
+  if (n <= 0) return fail(GP_INVALID, "constrained_search requires a non-empty train set");
+  layout_space_t sp;
+  int rc = space_build(&sp, c, w, ids, n, opts);
+  if (rc) return rc;
+  int64_t total = count_layouts(&sp);
+  if (hi < 0 || hi > total) hi = total;
+  if (lo < 0) lo = 0;
+  search_t st;
+  memset(&st, 0, sizeof st);
+  st.sp = &sp;
+  st.w = w;
+  st.k = k;
+  st.window = window;
+  st.lo = lo;
+  st.hi = hi;
+  st.scoring = 1;
+  if (sp.max_stages >= sp.n_runs && lo < hi) recurse_runs(&st, 0, 0);
+  out->layouts = hi > lo ? hi - lo : 0;
+  out->feasible = st.feasible;
+  if (st.err) {
+    space_free(&sp);
+    return st.err;
+  }
+  if (st.have_best) {
+    out->found = 1;
+    out->cost = st.best_cost;
+    out->rank = st.best_rank;
+    out->n_stages = st.best_n;
+    int off = 0;
+    for (int s = 0; s < st.best_n; ++s) {
+      out->stage[s].first = off;
+      out->stage[s].count = st.best_len[s];
+      out->stage[s].tp = st.best_tp[s];
+      out->stage[s].dp = st.best_dp[s];
+      out->stage[s].layers = st.best_layers[s];
+      for (int i = 0; i < st.best_len[s]; ++i)
+        stage_devices[off++] = sp.ordered[st.best_start[s] + i];
+    }
+  }
+  space_free(&sp);
+  return GP_OK;
+}
+
+/* ================================================================ rollout */
+
+int or_rollout_capacities(const gp_cluster* c, const int32_t* ids, int32_t n, int32_t* caps) {
+  /* src/rollout_milp.cpp:113-120 */
+  for (int t = 0; t < c->n_types; ++t) caps[t] = 0;
+  for (int i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= c->n_devices) return fail(GP_INVALID, "unknown device id %d", ids[i]);
+    caps[c->device_type[ids[i]]]++;
+  }
+  return GP_OK;
+}
+
+static int config_type(const gp_config* cfg, int n_types) {
+  for (int t = 0; t < n_types; ++t)
+    if (cfg->type_counts[t] > 0) return t;
+  return -1;
+}
+
+/* layers_for_stage (src/cost_model.cpp:51-55) */
+static int layers_for_stage(int layers, int stages, int index) {
+  return layers / stages + (index < layers % stages ? 1 : 0);
+}
+
+/* replica_concurrency (src/cost_model.cpp:128-148) */
+static int replica_concurrency(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                               const gp_config* cfg) {
+  int type = config_type(cfg, c->n_types);
+  if (type < 0) return 0;
+  int S = cfg->n_stages;
+  int best = k->max_concurrency;
+  for (int s = 0; s < S; ++s) {
+    int layers = layers_for_stage(w->num_layers, S, s);
+    int tp = cfg->tp[s];
+    double lf = (double)layers / w->num_layers;
+    double weight = w_params(w) * lf * w->bytes_per_param_infer / tp;
+    double free_b = c->type_hbm_cap[type] - weight;
+    if (free_b < 0) return 0;
+    double kv = w_kv_bytes_per_token(w) * w_mean_total_len(w) * lf / tp;
+    if (kv > 0) {
+      int v = trunc_i32_x86(free_b / kv);
+      if (v < best) best = v;
+    }
+  }
+  return best > 0 ? best : 0;
+}
+
+/* replica_rate_at (src/cost_model.cpp:150-165) */
+static double replica_rate_at(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                              const gp_config* cfg, double conc) {
+  double agg_bw = 0, agg_flops = 0;
+  for (int t = 0; t < c->n_types; ++t) {
+    if (cfg->type_counts[t] == 0) continue;
+    agg_bw += cfg->type_counts[t] * c->type_hbm_bw[t] * k->io_eff[t];
+    agg_flops += cfg->type_counts[t] * c->type_flops[t] * k->compute_eff[t];
+  }
+  double io = conc * agg_bw / w_model_bytes_infer(w);
+  double comp = agg_flops / (2.0 * w_params(w));
+  double pen = 1.0 + k->stage_latency_penalty * (cfg->n_stages - 1);
+  double m = comp < io ? comp : io;
+  return m / pen;
+}
+
+static void tp_multisets(int stages, int max_tp, int* acc, int depth, gp_config* tmpl,
+                         int (*emit)(void*, const int*), void* ud) {
+  if (depth == stages) {
+    emit(ud, acc);
+    return;
+  }
+  static const int tps[4] = {8, 4, 2, 1};
+  for (int i = 0; i < 4; ++i) {
+    if (tps[i] > max_tp) continue;
+    acc[depth] = tps[i];
+    tp_multisets(stages, tps[i], acc, depth + 1, tmpl, emit, ud);
+  }
+}
+
+typedef struct {
+  const gp_cluster* c;
+  const gp_workload* w;
+  const gp_calib* k;
+  int type, stages;
+  const int* avail;
+  gp_config* out;
+  int cap, n, overflow;
+} cfg_emit_t;
+
+static int emit_cfg(void* ud, const int* tps) {
+  cfg_emit_t* e = (cfg_emit_t*)ud;
+  for (int s = 0; s < e->stages; ++s)
+    if (tps[s] > e->avail[s]) return 0;
+  gp_config cfg;
+  memset(&cfg, 0, sizeof cfg);
+  for (int s = 0; s < e->stages; ++s) {
+    cfg.type_counts[e->type] += tps[s];
+    cfg.tp[s] = tps[s];
+  }
+  cfg.n_stages = e->stages;
+  int conc = replica_concurrency(e->c, e->w, e->k, &cfg);
+  if (conc < 1) return 0;
+  cfg.throughput = replica_rate_at(e->c, e->w, e->k, &cfg, (double)conc);
+  if (e->n < e->cap) e->out[e->n] = cfg;
+  else e->overflow = 1;
+  e->n++;
+  return 0;
+}
+
+static int cmp_desc_int(const void* a, const void* b) {
+  int x = *(const int*)a, y = *(const int*)b;
+  return (x < y) - (x > y);
+}
+
+/* enumerate_configs (src/rollout_milp.cpp:122-172) */
+int or_enumerate_configs(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                         const int32_t* ids, int32_t n, const gp_rollout_opts* opts,
+                         gp_config* out, int32_t cap, int32_t* n_out) {
+  if (n <= 0) return fail(GP_INVALID, "enumerate_configs requires a non-empty rollout set");
+  if (opts->max_stages > GP_MAX_ROLLOUT_STAGES)
+    return fail(GP_INVALID, "max_stages exceeds GP_MAX_ROLLOUT_STAGES");
+  int* per_machine = (int*)calloc((size_t)c->n_machines, sizeof(int));
+  int* avail = (int*)malloc(sizeof(int) * (size_t)c->n_machines);
+  cfg_emit_t e = {c, w, k, 0, 0, avail, out, cap, 0, 0};
+  for (int i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= c->n_devices) {
+      free(per_machine);
+      free(avail);
+      return fail(GP_INVALID, "unknown device id %d", ids[i]);
+    }
+  for (int t = 0; t < c->n_types; ++t) {
+    memset(per_machine, 0, sizeof(int) * (size_t)c->n_machines);
+    for (int i = 0; i < n; ++i)
+      if (c->device_type[ids[i]] == t) per_machine[c->device_machine[ids[i]]]++;
+    int na = 0;
+    for (int m = 0; m < c->n_machines; ++m)
+      if (per_machine[m] > 0) avail[na++] = per_machine[m];
+    if (na == 0) continue;
+    qsort(avail, (size_t)na, sizeof(int), cmp_desc_int);
+    int ms = opts->max_stages;
+    if (na < ms) ms = na;
+    if (w->num_layers < ms) ms = w->num_layers;
+    e.type = t;
+    for (int s = 1; s <= ms; ++s) {
+      int acc[GP_MAX_ROLLOUT_STAGES];
+      e.stages = s;
+      tp_multisets(s, 8, acc, 0, NULL, emit_cfg, &e);
+    }
+  }
+  free(per_machine);
+  free(avail);
+  *n_out = e.n;
+  if (e.overflow) return fail(GP_CAPACITY, "config buffer too small (%d needed)", e.n);
+  return GP_OK;
+}
+
+/* solve_milp (src/rollout_milp.cpp:174-254) */
+int or_solve_milp(const gp_config* cfg, int32_t nc, const int32_t* caps, int32_t dims, double B,
+                  double len, gp_rollout_result* out, gp_rollout_entry* entries) {
+  memset(out, 0, sizeof *out);
+  out->total_rollouts = B;
+  if (B <= 0) return GP_OK;
+  if (nc == 0) return fail(GP_INFEASIBLE, "no replica configuration available");
+  int64_t stride[GP_MAX_TYPES];
+  int64_t states = 1;
+  for (int t = 0; t < dims; ++t) {
+    stride[t] = states;
+    states *= caps[t] + 1;
+    if (states > 50000000) return fail(GP_INVALID, "capacity lattice too large for the exact solver");
+  }
+  out->states = states;
+  double* best = (double*)malloc(sizeof(double) * (size_t)states);
+  int* choice = (int*)malloc(sizeof(int) * (size_t)states);
+  for (int64_t s = 0; s < states; ++s) {
+    best[s] = 0.0;
+    choice[s] = -1;
+  }
+  int sv[GP_MAX_TYPES];
+  for (int64_t s = 0; s < states; ++s) {
+    int64_t rem = s;
+    for (int t = dims - 1; t >= 0; --t) {
+      sv[t] = (int)(rem / stride[t]);
+      rem %= stride[t];
+    }
+    for (int ci = 0; ci < nc; ++ci) {
+      int64_t prev = s;
+      int ok = 1;
+      for (int t = 0; t < dims; ++t) {
+        int need = cfg[ci].type_counts[t];
+        if (sv[t] < need) {
+          ok = 0;
+          break;
+        }
+        prev -= (int64_t)need * stride[t];
+      }
+      if (!ok) continue;
+      double cand = best[prev] + cfg[ci].throughput;
+      if (cand > best[s]) {
+        best[s] = cand;
+        choice[s] = ci;
+      }
+    }
+  }
+  int64_t full = states - 1;
+  double agg = best[full];
+  out->aggregate = agg;
+  if (agg <= 0) {
+    free(best);
+    free(choice);
+    return fail(GP_INFEASIBLE, "rollout capacity cannot host any replica");
+  }
+  int* counts = (int*)calloc((size_t)nc, sizeof(int));
+  int64_t cur = full;
+  while (choice[cur] >= 0) {
+    int ci = choice[cur];
+    counts[ci]++;
+    for (int t = 0; t < dims; ++t) cur -= (int64_t)cfg[ci].type_counts[t] * stride[t];
+  }
+  out->makespan = B * len / agg;
+  int ne = 0;
+  for (int ci = 0; ci < nc; ++ci) {
+    if (counts[ci] == 0) continue;
+    entries[ne].config = ci;
+    entries[ne].replicas = counts[ci];
+    entries[ne].workload = B * counts[ci] * cfg[ci].throughput / agg;
+    ne++;
+  }
+  out->n_entries = ne;
+  free(counts);
+  free(best);
+  free(choice);
+  return GP_OK;
+}
+
+/* weight_sync_cost (src/cost_model.cpp:255-277) */
+int or_weight_sync_cost(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                        const int32_t* train, int32_t nt, const int32_t* roll, int32_t nr,
+                        const int32_t* etype, const int32_t* erep, int32_t ne, int32_t window,
+                        double* out) {
+  double bottleneck = K_INF;
+  for (int e = 0; e < ne; ++e) {
+    if (erep[e] < 1) continue;
+    int type = etype[e];
+    double best = 0;
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j < nr; ++j) {
+        if (c->device_type[roll[j]] != type) continue;
+        double l = link(c, train[i], roll[j]);
+        if (best < l) best = l;
+      }
+    if (best > 0 && best < bottleneck) bottleneck = best;
+  }
+  double transfer = 0;
+  if (bottleneck < K_INF && w_model_bytes_infer(w) > 0) transfer = w_model_bytes_infer(w) / bottleneck;
+  *out = window * transfer + k->sync_latency_s;
+  return GP_OK;
+}

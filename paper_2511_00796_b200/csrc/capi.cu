@@ -1,0 +1,236 @@
+// capi.cu — extern "C" entry points of libgplan.so (include/gplan.h) and the
+// engine context: validation, device upload, scratch management, error state.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "gp_internal.h"
+
+namespace gp {
+
+int train_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int64_t* layouts);
+int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_train_opts* o,
+                 long long lo, long long hi, gp_train_result* out, int32_t* stage_devices);
+
+static thread_local std::string g_error;
+
+int set_error(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return set_error(GP_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void* ctx_scratch(gp_ctx* ctx, size_t bytes) {
+  if (bytes > ctx->scratch_bytes) {
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    ctx->scratch = nullptr;
+    size_t want = bytes + bytes / 4;
+    cudaError_t e = cudaMalloc(&ctx->scratch, want);
+    if (e != cudaSuccess) {
+      ctx->scratch_bytes = 0;
+      cuda_fail(e, "cudaMalloc(scratch)");
+      return nullptr;
+    }
+    ctx->scratch_bytes = want;
+  }
+  return ctx->scratch;
+}
+
+void* ctx_pinned(gp_ctx* ctx, size_t bytes) {
+  if (bytes > ctx->h_pinned_bytes) {
+    if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+    ctx->h_pinned = nullptr;
+    size_t want = bytes + bytes / 4 + 4096;
+    cudaError_t e = cudaMallocHost(&ctx->h_pinned, want);
+    if (e != cudaSuccess) {
+      ctx->h_pinned_bytes = 0;
+      cuda_fail(e, "cudaMallocHost(staging)");
+      return nullptr;
+    }
+    ctx->h_pinned_bytes = want;
+  }
+  return ctx->h_pinned;
+}
+
+__global__ void k_probe(int* flag) { *flag = 0x5eed; }
+
+// Every device of a type carries the same capabilities in the reference loader
+// (src/cluster.cpp:127-137); the engine's rollout side relies on it.
+static int validate(const gp_cluster* c, const gp_workload* w, const gp_calib* k) {
+  if (!c || !w || !k) return set_error(GP_INVALID, "null input");
+  if (c->n_devices < 1) return set_error(GP_INVALID, "cluster has no devices");
+  if (c->n_types < 1 || c->n_types > GP_MAX_TYPES)
+    return set_error(GP_INVALID, "n_types must lie in [1, GP_MAX_TYPES]");
+  if (c->n_machines < 1) return set_error(GP_INVALID, "cluster has no machines");
+  for (int d = 0; d < c->n_devices; ++d) {
+    if (c->device_type[d] < 0 || c->device_type[d] >= c->n_types)
+      return set_error(GP_INVALID, "device " + std::to_string(d) + " has an unknown gpu_type");
+    if (c->device_machine[d] < 0 || c->device_machine[d] >= c->n_machines)
+      return set_error(GP_INVALID, "device " + std::to_string(d) + " has an unknown machine");
+  }
+  // WorkloadSpec::validate (src/workload.cpp:58-69)
+  if (!(w->model_params_b > 0)) return set_error(GP_INVALID, "model.params_billion must be > 0");
+  if (w->num_layers < 1) return set_error(GP_INVALID, "model.num_layers must be >= 1");
+  if (w->hidden_dim < 1) return set_error(GP_INVALID, "model.hidden_dim must be >= 1");
+  if (w->batch_rollouts < 1) return set_error(GP_INVALID, "batch_rollouts must be >= 1");
+  if (w->prompt_len < 0) return set_error(GP_INVALID, "prompt_len must be >= 0");
+  if (!(w->bytes_per_param_train > 0)) return set_error(GP_INVALID, "bytes_per_param_train must be > 0");
+  if (!(w->bytes_per_param_infer > 0)) return set_error(GP_INVALID, "bytes_per_param_infer must be > 0");
+  if (w->micro_batches < 1) return set_error(GP_INVALID, "micro_batches must be >= 1");
+  return GP_OK;
+}
+
+}  // namespace gp
+
+using namespace gp;
+
+extern "C" {
+
+int gp_abi_version(void) { return GP_ABI_VERSION; }
+const char* gp_last_error(void) { return g_error.c_str(); }
+
+int gp_ctx_create(const gp_cluster* c, const gp_workload* w, const gp_calib* k, int device,
+                  gp_ctx** out) {
+  *out = nullptr;
+  int rc = validate(c, w, k);
+  if (rc) return rc;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return set_error(GP_CUDA_ERROR, std::string("no CUDA device available (") +
+                                        (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices") +
+                                        "); the engine has no CPU fallback");
+  if (device < 0 || device >= ndev) return set_error(GP_CUDA_ERROR, "CUDA ordinal out of range");
+  GP_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  GP_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return set_error(GP_CUDA_ERROR, std::string("device ") + prop.name +
+                                        " is not sm_100 (Blackwell); libgplan is built for sm_100a only");
+  gp_ctx* ctx = new gp_ctx();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  const int N = c->n_devices, T = c->n_types;
+  ctx->N = N;
+  ctx->T = T;
+  ctx->M = c->n_machines;
+  ctx->h_type.assign(c->device_type, c->device_type + N);
+  ctx->h_machine.assign(c->device_machine, c->device_machine + N);
+  ctx->h_flops.assign(c->device_flops, c->device_flops + N);
+  ctx->h_hbm_bw.assign(c->device_hbm_bw, c->device_hbm_bw + N);
+  ctx->h_hbm_cap.assign(c->device_hbm_cap, c->device_hbm_cap + N);
+  ctx->h_tflops.assign(c->type_flops, c->type_flops + T);
+  ctx->h_thbm.assign(c->type_hbm_bw, c->type_hbm_bw + T);
+  ctx->h_tcap.assign(c->type_hbm_cap, c->type_hbm_cap + T);
+  ctx->h_ceff.assign(k->compute_eff, k->compute_eff + T);
+  ctx->h_ioeff.assign(k->io_eff, k->io_eff + T);
+  ctx->work = *w;
+  ctx->calib = *k;
+  ctx->calib.compute_eff = nullptr;
+  ctx->calib.io_eff = nullptr;
+  // derived scalars, same expressions as inc/workload.hpp:51-58
+  Scalars& s = ctx->sc;
+  s.P = w->model_params_b * 1e9;
+  s.mtl = w->prompt_len + w->mean_len;
+  s.tokens = w->batch_rollouts * s.mtl;
+  s.tfpt_tokens = 6.0 * s.P * s.tokens;
+  s.mbi = s.P * w->bytes_per_param_infer;
+  s.ifpt = 2.0 * s.P;
+  s.kvbpt = 4.0 * w->hidden_dim * w->num_layers;
+  s.act_tok_h2 = s.tokens * w->hidden_dim * kActBytes;
+  s.bpp_train = w->bytes_per_param_train;
+  s.bpp_infer = w->bytes_per_param_infer;
+  s.act_coeff = k->activation_coeff;
+  s.tp_coeff = k->tp_allreduce_coeff;
+  s.grad_bpp = k->grad_bytes_per_param;
+  s.stage_pen = k->stage_latency_penalty;
+  s.sync_latency = k->sync_latency_s;
+  s.reward = w->reward_cost_const;
+  s.L = w->num_layers;
+  s.H = w->hidden_dim;
+  s.mb = w->micro_batches;
+  s.max_conc = k->max_concurrency;
+  s.batch = w->batch_rollouts;
+  s.mean_len = w->mean_len;
+
+  auto fail = [&](int code) {
+    gp_ctx_destroy(ctx);
+    return code;
+  };
+#define UP(dst, src, count, T_)                                                           \
+  do {                                                                                     \
+    if (cudaMalloc(&dst, sizeof(T_) * (count)) != cudaSuccess)                             \
+      return fail(set_error(GP_CUDA_ERROR, "cudaMalloc failed"));                          \
+    if (cudaMemcpy(dst, src, sizeof(T_) * (count), cudaMemcpyHostToDevice) != cudaSuccess) \
+      return fail(set_error(GP_CUDA_ERROR, "cudaMemcpy failed"));                          \
+  } while (0)
+  UP(ctx->d_type, c->device_type, N, int);
+  UP(ctx->d_machine, c->device_machine, N, int);
+  UP(ctx->d_flops, c->device_flops, N, double);
+  UP(ctx->d_hbm_bw, c->device_hbm_bw, N, double);
+  UP(ctx->d_hbm_cap, c->device_hbm_cap, N, double);
+  UP(ctx->d_links, c->links, (size_t)N * N, double);
+  UP(ctx->d_ceff, k->compute_eff, T, double);
+  UP(ctx->d_ioeff, k->io_eff, T, double);
+  UP(ctx->d_tflops, c->type_flops, T, double);
+  UP(ctx->d_thbm, c->type_hbm_bw, T, double);
+  UP(ctx->d_tcap, c->type_hbm_cap, T, double);
+#undef UP
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(set_error(GP_CUDA_ERROR, "cudaStreamCreate failed"));
+  // kernel-image probe: fails loudly if this build has no sm_100a code for the device
+  int* flag = static_cast<int*>(ctx_scratch(ctx, 1 << 20));
+  if (!flag) return fail(GP_CUDA_ERROR);
+  k_probe<<<1, 1, 0, ctx->stream>>>(flag);
+  int hflag = 0;
+  cudaError_t pe = cudaGetLastError();
+  if (pe == cudaSuccess) pe = cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+  if (pe == cudaSuccess) pe = cudaStreamSynchronize(ctx->stream);
+  if (pe != cudaSuccess || hflag != 0x5eed)
+    return fail(set_error(GP_CUDA_ERROR, std::string("kernel probe failed: ") + cudaGetErrorString(pe)));
+  *out = ctx;
+  return GP_OK;
+}
+
+void gp_ctx_destroy(gp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  void* ptrs[] = {ctx->d_type, ctx->d_machine, ctx->d_flops, ctx->d_hbm_bw, ctx->d_hbm_cap,
+                  ctx->d_links, ctx->d_ceff, ctx->d_ioeff, ctx->d_tflops, ctx->d_thbm,
+                  ctx->d_tcap, ctx->scratch};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+long long gp_ctx_launches(gp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+void* gp_ctx_stream(gp_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int gp_train_space(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* o,
+                   int64_t* layouts) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  return train_space(ctx, ids, n, o, layouts);
+}
+
+int gp_constrained_search(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
+                          const gp_train_opts* o, gp_train_result* out, int32_t* stage_devices) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return train_search(ctx, ids, n, window, o, 0, -1, out, stage_devices);
+}
+
+int gp_constrained_search_range(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
+                                const gp_train_opts* o, int64_t lo, int64_t hi,
+                                gp_train_result* out, int32_t* stage_devices) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return train_search(ctx, ids, n, window, o, lo, hi, out, stage_devices);
+}
+
+}  // extern "C"

@@ -1,0 +1,142 @@
+// gp_internal.h — shared host/device definitions of the B200 plan-evaluation engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gplan.h"
+
+namespace gp {
+
+constexpr double kInf = 1e30;       // inc/common.hpp:41
+constexpr double kActBytes = 2.0;   // src/cost_model.cpp:10
+constexpr int kMaxPerRun = 4;       // K1 kernel instantiations support <= 4 blocks per type run
+
+// Derived workload/calibration scalars, computed on the host exactly as the
+// reference's inline accessors do (inc/workload.hpp:51-58) and passed by value.
+struct Scalars {
+  double P;             // params()
+  double tokens;        // tokens_per_step()
+  double mtl;           // mean_total_len()
+  double tfpt_tokens;   // train_flops_per_token() * tokens
+  double mbi;           // model_bytes_infer()
+  double ifpt;          // infer_flops_per_token()
+  double kvbpt;         // kv_bytes_per_token()
+  double act_tok_h2;    // tokens * hidden * 2.0 (stage transfer numerator)
+  double bpp_train, bpp_infer;
+  double act_coeff, tp_coeff, grad_bpp;
+  double stage_pen, sync_latency, reward;
+  int L, H, mb, max_conc, batch;
+  double mean_len;
+};
+
+// Per train-set block record (one contiguous block of a type run).
+struct BlockRec {
+  int start;        // offset into the canonical order
+  int n;            // devices
+  int type;
+  int per_machine;  // max_devices_per_machine
+  double flops;     // sequential fold of device flops (src/train_search.cpp:279-282)
+  double lf_num;    // num_layers * flops (allocate_layers numerator)
+  double cap_front; // hbm_capacity of devices.front()
+  double beta_tp[4];  // min link within TP groups for tp = 1,2,4,8 (index 0 unused)
+  double beta_dp[4];  // min link within DP groups (stride tp)
+};
+
+// Launch-parameter view of one train set (fits in the kernel param space).
+struct TrainSpace {
+  int R;                 // type runs
+  int max_stages;        // min(L, R * max_per_run)
+  int max_per_run;
+  int n;                 // devices in the train set
+  int len[GP_MAX_TYPES];
+  int nc[GP_MAX_TYPES];        // cut count per run
+  int kmax[GP_MAX_TYPES];      // min(max_per_run, len)
+  int blk_off[GP_MAX_TYPES];   // first block index of run r
+  int tin_off[GP_MAX_TYPES];   // offset of run r's (nc+2)^3 within-run transfer cube
+  int tx_off[GP_MAX_TYPES];    // offset of the (r, r+1) cross-run transfer matrix
+  int64_t cnt[GP_MAX_TYPES + 1][GP_MAX_STAGES + 1];  // completions of runs r.. with u used
+};
+
+// Device-side training tables of one train set.
+struct TrainTables {
+  const int* ordered;
+  const int* pos;        // per run: positions [0, cuts..., len], offsets = pos_off
+  const BlockRec* blk;
+  const double2* stage;  // [nblk * L] (total, compute); total < 0 => memory-infeasible
+  const int8_t* opt;     // [nblk * L] chosen tp option index
+  const double* tin;
+  const double* tx;
+  const double* fd_coef; // [S] = (double)(S-1) / micro_batches
+  int pos_off[GP_MAX_TYPES];
+};
+
+struct Best {
+  double cost;
+  long long rank;
+  long long feasible;
+};
+
+__host__ __device__ inline int blk_index(int nc, int a, int b) {
+  // blocks (a, b), 0 <= a < b <= nc+1, row-major by a
+  return a * (nc + 1) - (a * (a - 1)) / 2 + (b - a - 1);
+}
+__host__ __device__ inline int64_t binom_small(int n, int j) {
+  switch (j) {
+    case 0: return 1;
+    case 1: return n > 0 ? n : 0;
+    case 2: return n > 1 ? (int64_t)n * (n - 1) / 2 : 0;
+    case 3: return n > 2 ? (int64_t)n * (n - 1) * (n - 2) / 6 : 0;
+  }
+  return 0;
+}
+
+}  // namespace gp
+
+// Engine context (opaque in the C ABI).
+struct gp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  // cluster
+  int N = 0, T = 0, M = 0;
+  std::vector<int> h_type, h_machine;
+  std::vector<double> h_flops, h_hbm_bw, h_hbm_cap, h_tflops, h_thbm, h_tcap, h_ceff, h_ioeff;
+  int* d_type = nullptr;
+  int* d_machine = nullptr;
+  double* d_flops = nullptr;
+  double* d_hbm_bw = nullptr;
+  double* d_hbm_cap = nullptr;
+  double* d_links = nullptr;
+  double* d_ceff = nullptr;
+  double* d_ioeff = nullptr;
+  double* d_tflops = nullptr;
+  double* d_thbm = nullptr;
+  double* d_tcap = nullptr;
+  gp::Scalars sc{};
+  gp_workload work{};
+  gp_calib calib{};
+  // grow-only scratch for the train search
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  void* h_pinned = nullptr;
+  size_t h_pinned_bytes = 0;
+  int num_sms = 148;
+  // kernel launches issued by this context (bench.py's gpu_launches claim)
+  long long launches = 0;
+};
+
+namespace gp {
+int set_error(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+void* ctx_scratch(gp_ctx* ctx, size_t bytes);
+void* ctx_pinned(gp_ctx* ctx, size_t bytes);
+}  // namespace gp
+
+#define GP_CUDA(call)                                          \
+  do {                                                         \
+    cudaError_t e_ = (call);                                   \
+    if (e_ != cudaSuccess) return gp::cuda_fail(e_, #call);    \
+  } while (0)

@@ -1,0 +1,880 @@
+// train.cu — sm_100a kernels for the training-side hot loop:
+//   constrained_search (src/train_search.cpp:268-325) over the layout space of
+//   enumerate_block_lists (src/train_search.cpp:145-192), scored with
+//   train_stage_cost / train_cost_breakdown / mem_cumsum_train
+//   (src/cost_model.cpp:57-126,198-207).
+//
+// Design:
+//   K2a  block_stats   one CTA per contiguous block of a type run: sequential
+//                      FLOPS fold, per-machine count, exact min-link over the TP
+//                      (chunked) and DP (strided) groups of every tp option.
+//   K2b  transfers     one warp per adjacent block pair: exact min-link over the
+//                      block x block rectangle -> stage-transfer term.
+//   K2c  stage_table   one thread per (block, layer_count): memory filter +
+//                      comm-minimal (tp, dp) pick -> (total, compute).
+//   K1   layout_scan   persistent grid; each thread unranks a chunk start of the
+//                      layout rank space and walks the chunk with an odometer
+//                      (no plan list is materialised); allocate_layers + table
+//                      gathers + fill/drain + transfers; lexicographic
+//                      (cost, rank) argmin via warp shuffles -> CTA -> grid.
+//   K1f  finalize      reduce CTA partials, decode the winning rank.
+// Every fp64 expression keeps the reference's association order; the library
+// is compiled with --fmad=false, so results are bit-identical to the CPU.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <numeric>
+
+#include "gp_internal.h"
+
+namespace gp {
+
+struct TrainOut {
+  Best best;
+  int n_stages;
+  int pad;
+  int first[GP_MAX_STAGES];
+  int count[GP_MAX_STAGES];
+  int tp[GP_MAX_STAGES];
+  int dp[GP_MAX_STAGES];
+  int layers[GP_MAX_STAGES];
+};
+
+struct BlockMeta {
+  int run, a, b, start_global;
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = dmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// CTA-wide min; every thread gets the result.
+__device__ double block_min(double v, double* sm) {
+  v = warp_min(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sm[wid] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  double r = lane < nw ? sm[lane] : kInf;
+  r = warp_min(r);
+  return r;
+}
+
+__device__ __forceinline__ bool better(double c1, long long r1, double c2, long long r2) {
+  return c1 < c2 || (c1 == c2 && r1 < r2);
+}
+
+// ---------------------------------------------------------------- K2a blocks
+// min_link_within_groups (src/cost_model.cpp:12-36), exact, for every option.
+__global__ void __launch_bounds__(256) k2a_block_stats(const int* __restrict__ ordered,
+                                                       const BlockMeta* __restrict__ meta,
+                                                       const int* __restrict__ pos,
+                                                       TrainTables tb, BlockRec* __restrict__ out,
+                                                       const int* __restrict__ dtype,
+                                                       const int* __restrict__ dmachine,
+                                                       const double* __restrict__ dflops,
+                                                       const double* __restrict__ dcap,
+                                                       const double* __restrict__ links, int N,
+                                                       int L, int mb, double* fd_coef) {
+  __shared__ double red[32];
+  __shared__ BlockRec rec;
+  const BlockMeta m = meta[blockIdx.x];
+  const int* P = pos + tb.pos_off[m.run];
+  const int start = m.start_global + P[m.a];
+  const int n = P[m.b] - P[m.a];
+  const int* dev = ordered + start;
+  if (threadIdx.x == 0) {
+    rec.start = start;
+    rec.n = n;
+    rec.type = dtype[dev[0]];
+    double f = 0;
+    int best = 0, run = 0;
+    for (int i = 0; i < n; ++i) {
+      f += dflops[dev[i]];
+      run = (i > 0 && dmachine[dev[i]] == dmachine[dev[i - 1]]) ? run + 1 : 1;
+      best = run > best ? run : best;
+    }
+    rec.flops = f;
+    rec.lf_num = L * f;
+    rec.per_machine = best;
+    rec.cap_front = dcap[dev[0]];
+    for (int o = 0; o < 4; ++o) rec.beta_tp[o] = rec.beta_dp[o] = kInf;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < GP_MAX_STAGES + 1) {
+    const int S = threadIdx.x;
+    fd_coef[S] = S > 0 ? static_cast<double>(S - 1) / mb : 0.0;
+  }
+  __syncthreads();
+  const int per_machine = rec.per_machine;
+#pragma unroll 1
+  for (int o = 0; o < 4; ++o) {
+    const int tp = 1 << o;
+    if (tp > per_machine || n % tp != 0) continue;  // tp_dp_options (src/train_search.cpp:74-93)
+    const int dp = n / tp;
+    if (tp > 1) {  // consecutive chunks of tp devices
+      double mn = kInf;
+      const int pairs_per = tp * (tp - 1) / 2;
+      const int total = (n / tp) * pairs_per;
+      for (int p = threadIdx.x; p < total; p += blockDim.x) {
+        const int g = p / pairs_per;
+        int q = p - g * pairs_per, i = 0;
+        while (q >= tp - 1 - i) {
+          q -= tp - 1 - i;
+          ++i;
+        }
+        const int j = i + 1 + q;
+        mn = dmin(mn, links[(size_t)dev[g * tp + i] * N + dev[g * tp + j]]);
+      }
+      mn = block_min(mn, red);
+      if (threadIdx.x == 0) rec.beta_tp[o] = mn;
+    }
+    if (dp > 1) {  // stride-tp groups of dp devices
+      double mn = kInf;
+      const long long sq = (long long)dp * dp;
+      for (long long p = threadIdx.x; p < sq; p += blockDim.x) {
+        const int i = (int)(p / dp), j = (int)(p - (long long)i * dp);
+        if (i >= j) continue;
+        for (int g = 0; g < tp; ++g)
+          mn = dmin(mn, links[(size_t)dev[i * tp + g] * N + dev[j * tp + g]]);
+      }
+      mn = block_min(mn, red);
+      if (threadIdx.x == 0) rec.beta_dp[o] = mn;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = rec;
+}
+
+// ------------------------------------------------------------ K2b transfers
+// min_link_between (src/cost_model.cpp:38-47) over adjacent blocks; one warp per item.
+// item = (run, a, b, c): within-run blocks [a,b) -> [b,c); c < 0 marks a cross-run item
+// (run r's block [a, nc+1) -> run r+1's block [0, -c)).
+__global__ void __launch_bounds__(256) k2b_transfers(const int* __restrict__ ordered,
+                                                     const int4* __restrict__ items, int n_items,
+                                                     const int* __restrict__ pos, TrainTables tb,
+                                                     TrainSpace sp, const int* __restrict__ run_start,
+                                                     const double* __restrict__ links, int N,
+                                                     double numer, double* tin, double* tx) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n_items) return;
+  const int4 it = items[warp];
+  const int r = it.x;
+  const int* P = pos + tb.pos_off[r];
+  int s1, n1, s2, n2;
+  if (it.w >= 0) {
+    s1 = run_start[r] + P[it.y];
+    n1 = P[it.z] - P[it.y];
+    s2 = run_start[r] + P[it.z];
+    n2 = P[it.w] - P[it.z];
+  } else {
+    const int* P2 = pos + tb.pos_off[r + 1];
+    s1 = run_start[r] + P[it.y];
+    n1 = sp.len[r] - P[it.y];
+    s2 = run_start[r + 1];
+    n2 = P2[-it.w];
+  }
+  double mn = kInf;
+  const long long tot = (long long)n1 * n2;
+  for (long long p = lane; p < tot; p += 32) {
+    const int i = (int)(p / n2), j = (int)(p - (long long)i * n2);
+    mn = dmin(mn, links[(size_t)ordered[s1 + i] * N + ordered[s2 + j]]);
+  }
+  mn = warp_min(mn);
+  if (lane == 0) {
+    // tokens * hidden * kActivationBytes / beta; skipped entirely when tokens <= 0
+    const double t = numer > 0 ? numer / mn : 0.0;
+    if (it.w >= 0) {
+      const int e = sp.nc[r] + 2;
+      tin[sp.tin_off[r] + ((size_t)it.y * e + it.z) * e + it.w] = t;
+    } else {
+      const int e2 = sp.nc[r + 1] + 2;
+      tx[sp.tx_off[r] + (size_t)it.y * e2 + (-it.w)] = t;
+    }
+  }
+}
+
+// ------------------------------------------------------------ K2c stage table
+// Per (block, layer_count): the option loop of constrained_search
+// (src/train_search.cpp:289-315) with mem_cumsum_train and train_stage_cost.
+__global__ void __launch_bounds__(256) k2c_stage_table(const BlockRec* __restrict__ blk, int nblk,
+                                                       Scalars sc, const double* __restrict__ ceff,
+                                                       double2* __restrict__ stage,
+                                                       int8_t* __restrict__ opt) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)nblk * sc.L) return;
+  const int bi = (int)(idx / sc.L);
+  const int lc = (int)(idx - (long long)bi * sc.L) + 1;
+  const BlockRec& b = blk[bi];
+  const double lf = static_cast<double>(lc) / sc.L;  // layer_frac (total_layers == num_layers)
+  const double compute = sc.tfpt_tokens * lf / (ceff[b.type] * b.flops);
+  double best_comm = -1, best_tp_comm = 0, best_dp_comm = 0;
+  int best_o = -1;
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    const int tp = 1 << o;
+    if (tp > b.per_machine || b.n % tp != 0) continue;
+    const int dp = b.n / tp;
+    // mem_cumsum_train (src/cost_model.cpp:198-207)
+    const double weight = sc.P * lf * sc.bpp_train / tp;
+    const double tpm = sc.tokens / dp / sc.mb;
+    const double act = sc.act_coeff * tpm * sc.H * kActBytes * lc / tp;
+    const double need_gb = (weight + act) / 1e9;
+    if (need_gb * 1e9 > b.cap_front) continue;
+    double tp_comm = 0, dp_comm = 0;
+    if (tp > 1 && sc.tokens > 0) {
+      const double prt = sc.tokens / dp;
+      const double vol = sc.tp_coeff * lc * prt * sc.H * kActBytes * 2.0 * (tp - 1) / tp;
+      tp_comm = vol / b.beta_tp[o];
+    }
+    if (dp > 1) {
+      const double shard = sc.P * lf * sc.grad_bpp / tp;
+      const double vol = 2.0 * shard * (dp - 1) / dp;
+      dp_comm = vol / b.beta_dp[o];
+    }
+    const double comm = tp_comm + dp_comm;
+    if (best_comm < 0 || comm < best_comm) {
+      best_comm = comm;
+      best_tp_comm = tp_comm;
+      best_dp_comm = dp_comm;
+      best_o = o;
+    }
+  }
+  double2 e;
+  e.x = best_o < 0 ? -1.0 : compute + best_tp_comm + best_dp_comm;  // TrainStageCost::total()
+  e.y = compute;
+  stage[idx] = e;
+  opt[idx] = (int8_t)best_o;
+}
+
+// ------------------------------------------------------------- K1 layout scan
+template <int MAXR>
+struct Layout {
+  int k[MAXR];
+  int used[MAXR];
+  int b[MAXR][kMaxPerRun + 1];  // position-index boundaries; b[r][0] = 0, b[r][k] = nc+1
+};
+
+// Unrank `x` in the enumeration order of Enumerator::recurse (src/train_search.cpp:95-124)
+// with run_compositions' lexicographic cut order (src/train_search.cpp:53-72).
+template <int MAXR>
+__device__ __forceinline__ void unrank(const TrainSpace& sp, long long x, Layout<MAXR>& L) {
+  int u = 0;
+#pragma unroll
+  for (int r = 0; r < MAXR; ++r) {
+    if (r >= sp.R) break;
+    L.used[r] = u;
+    const int nc = sp.nc[r];
+    const int rem_runs = sp.R - 1 - r;
+#pragma unroll 1
+    for (int k = 1; k <= sp.kmax[r]; ++k) {
+      if (u + k + rem_runs > sp.max_stages) break;
+      const long long sub = sp.cnt[r + 1][u + k];
+      const long long size = binom_small(nc, k - 1) * sub;
+      if (x < size) {
+        long long q = x / sub;
+        x -= q * sub;
+        L.k[r] = k;
+        const int m = k - 1;
+        int v = 0;
+#pragma unroll
+        for (int j = 1; j < kMaxPerRun; ++j) {
+          if (j <= m) {
+#pragma unroll 1
+            while (true) {
+              const long long c = binom_small(nc - v - 1, m - j);
+              if (q < c) break;
+              q -= c;
+              ++v;
+            }
+            L.b[r][j] = v + 1;
+            ++v;
+          }
+        }
+#pragma unroll
+        for (int j = 1; j <= kMaxPerRun; ++j)
+          if (j == k) L.b[r][j] = nc + 1;
+        u += k;
+        break;
+      }
+      x -= size;
+    }
+    L.b[r][0] = 0;
+  }
+}
+
+// Next layout in enumeration order (odometer over runs, last run fastest).
+template <int MAXR>
+__device__ __forceinline__ void advance(const TrainSpace& sp, Layout<MAXR>& L) {
+  bool carry = true;
+#pragma unroll
+  for (int rr = MAXR - 1; rr >= 0; --rr) {
+    if (carry && rr < sp.R) {
+      const int nc = sp.nc[rr];
+      const int m = L.k[rr] - 1;
+      int jf = 0;
+#pragma unroll
+      for (int j = kMaxPerRun - 1; j >= 1; --j)
+        if (jf == 0 && j <= m && L.b[rr][j] < nc - (m - j)) jf = j;
+      bool ok = false;
+      if (jf) {
+#pragma unroll
+        for (int j = 1; j < kMaxPerRun; ++j) {
+          if (j == jf) L.b[rr][j] += 1;
+          else if (j > jf && j <= m) L.b[rr][j] = L.b[rr][j - 1] + 1;
+        }
+        ok = true;
+      } else if (L.k[rr] < sp.kmax[rr] && L.used[rr] + L.k[rr] + 1 + (sp.R - 1 - rr) <= sp.max_stages &&
+                 nc >= L.k[rr]) {
+        const int k = ++L.k[rr];
+#pragma unroll
+        for (int j = 1; j <= kMaxPerRun; ++j) {
+          if (j < k) L.b[rr][j] = j;
+          else if (j == k) L.b[rr][j] = nc + 1;
+        }
+        ok = true;
+      }
+      if (ok) {
+        carry = false;
+#pragma unroll
+        for (int r2 = rr + 1; r2 < MAXR; ++r2) {
+          if (r2 < sp.R) {
+            L.used[r2] = L.used[r2 - 1] + L.k[r2 - 1];
+            L.k[r2] = 1;
+            L.b[r2][1] = sp.nc[r2] + 1;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Scores one layout. Returns false when some stage has no memory-feasible option.
+// Also returns the per-slot layer counts / block ids when `out_layers` is set (decode).
+template <int MAXR>
+__device__ __forceinline__ bool score(const TrainSpace& sp, const TrainTables& tb,
+                                      const double2* __restrict__ blkf, int L, int window,
+                                      const Layout<MAXR>& Y, double& cost, int* out_layers,
+                                      int* out_bi) {
+  constexpr int NS = MAXR * kMaxPerRun;
+  int bi[NS];
+  double lfn[NS];
+  int lay[NS];
+  long long remb[NS];
+  bool act[NS];
+  double total = 0.0;
+  int S = 0;
+  // stage flops + allocate_layers total (src/train_search.cpp:146-152)
+#pragma unroll
+  for (int r = 0; r < MAXR; ++r) {
+#pragma unroll
+    for (int j = 0; j < kMaxPerRun; ++j) {
+      const int q = r * kMaxPerRun + j;
+      act[q] = (r < sp.R) && (j < Y.k[r]);
+      if (act[q]) {
+        bi[q] = sp.blk_off[r] + blk_index(sp.nc[r], Y.b[r][j], Y.b[r][j + 1]);
+        const double2 fl = blkf[bi[q]];
+        total += fl.x;
+        lfn[q] = fl.y;
+        ++S;
+      }
+    }
+  }
+  int assigned = 0;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    if (act[q]) {
+      const double share = lfn[q] / total;
+      lay[q] = static_cast<int>(share);
+      assigned += lay[q];
+      remb[q] = __double_as_longlong(share - lay[q]);  // >= +0: integer order == fp order
+    }
+  }
+  // stable_sort by remainder desc -> position; extra layers round-robin over positions
+  const int extra = L - assigned;
+  const int ex_div = extra / S, ex_mod = extra % S;
+  int pos[NS];
+#pragma unroll
+  for (int q = 0; q < NS; ++q) pos[q] = 0;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+#pragma unroll
+    for (int q2 = q + 1; q2 < NS; ++q2) {
+      if (act[q] && act[q2]) {
+        if (remb[q] >= remb[q2]) pos[q2]++;
+        else pos[q]++;
+      }
+    }
+  }
+  bool zero = false;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    if (act[q]) {
+      lay[q] += ex_div + (pos[q] < ex_mod ? 1 : 0);
+      zero |= lay[q] == 0;
+    }
+  }
+  if (zero) {  // every stage needs at least one layer (src/train_search.cpp:217-225)
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      if (act[q] && lay[q] == 0) {
+        int dv = -1, dq = 0;
+#pragma unroll
+        for (int q2 = 0; q2 < NS; ++q2)
+          if (act[q2] && lay[q2] > dv) {
+            dv = lay[q2];
+            dq = q2;
+          }
+#pragma unroll
+        for (int q2 = 0; q2 < NS; ++q2)
+          if (q2 == dq) lay[q2]--;
+        lay[q] = 1;
+      }
+    }
+  }
+  // gather stage entries (train_cost_breakdown, src/cost_model.cpp:93-126)
+  double max_total = 0, max_comp = 0;
+  bool feasible = true;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    if (act[q]) {
+      const double2 e = tb.stage[(size_t)bi[q] * L + (lay[q] - 1)];
+      feasible &= e.x >= 0;
+      max_total = max_total < e.x ? e.x : max_total;
+      max_comp = max_comp < e.y ? e.y : max_comp;
+    }
+  }
+  if (out_layers) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      out_layers[q] = act[q] ? lay[q] : 0;
+      out_bi[q] = act[q] ? bi[q] : -1;
+    }
+  }
+  if (!feasible) return false;
+  double fill = 0, transfers = 0;
+  if (S > 1) {
+    fill = tb.fd_coef[S] * max_comp;
+#pragma unroll
+    for (int r = 0; r < MAXR; ++r) {
+#pragma unroll
+      for (int j = 0; j < kMaxPerRun; ++j) {
+        if (r < sp.R && j < Y.k[r]) {
+          if (j + 1 < Y.k[r]) {
+            const int e = sp.nc[r] + 2;
+            transfers += tb.tin[sp.tin_off[r] + ((size_t)Y.b[r][j] * e + Y.b[r][j + 1]) * e +
+                                Y.b[r][j + 2 <= kMaxPerRun ? j + 2 : kMaxPerRun]];
+          } else if (r + 1 < MAXR && r + 1 < sp.R) {
+            const int e2 = sp.nc[r + 1 < MAXR ? r + 1 : r] + 2;
+            transfers += tb.tx[sp.tx_off[r] + (size_t)Y.b[r][j] * e2 + Y.b[r + 1 < MAXR ? r + 1 : r][1]];
+          }
+        }
+      }
+    }
+  }
+  const double per_step = max_total + fill + transfers;
+  cost = window * per_step;
+  return true;
+}
+
+template <int MAXR>
+__global__ void __launch_bounds__(256) k1_layout_scan(TrainSpace sp, TrainTables tb,
+                                                      const double2* __restrict__ blkf, int L,
+                                                      int window, long long lo, long long hi,
+                                                      long long chunk, Best* __restrict__ partial) {
+  double best_cost = kInf * 10;
+  long long best_rank = LLONG_MAX;
+  long long feasible = 0;
+  const long long n_chunks = (hi - lo + chunk - 1) / chunk;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long ci = (long long)blockIdx.x * blockDim.x + threadIdx.x; ci < n_chunks; ci += stride) {
+    const long long r0 = lo + ci * chunk;
+    const long long r1 = r0 + chunk < hi ? r0 + chunk : hi;
+    Layout<MAXR> Y;
+    unrank<MAXR>(sp, r0, Y);
+    for (long long rank = r0; rank < r1; ++rank) {
+      double cost;
+      if (score<MAXR>(sp, tb, blkf, L, window, Y, cost, nullptr, nullptr)) {
+        ++feasible;
+        if (cost < best_cost) {  // strict <: first rank wins among equal costs
+          best_cost = cost;
+          best_rank = rank;
+        }
+      }
+      if (rank + 1 < r1) advance<MAXR>(sp, Y);
+    }
+  }
+  // warp -> CTA reduction of (cost, rank) lexicographic min and feasible count
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double c2 = __shfl_xor_sync(0xffffffffu, best_cost, o);
+    const long long r2 = __shfl_xor_sync(0xffffffffu, best_rank, o);
+    feasible += __shfl_xor_sync(0xffffffffu, feasible, o);
+    if (better(c2, r2, best_cost, best_rank)) {
+      best_cost = c2;
+      best_rank = r2;
+    }
+  }
+  __shared__ Best sb[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sb[wid] = Best{best_cost, best_rank, feasible};
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    Best b = lane < nw ? sb[lane] : Best{kInf * 10, LLONG_MAX, 0};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double c2 = __shfl_xor_sync(0xffffffffu, b.cost, o);
+      const long long r2 = __shfl_xor_sync(0xffffffffu, b.rank, o);
+      b.feasible += __shfl_xor_sync(0xffffffffu, b.feasible, o);
+      if (better(c2, r2, b.cost, b.rank)) {
+        b.cost = c2;
+        b.rank = r2;
+      }
+    }
+    if (lane == 0) partial[blockIdx.x] = b;
+  }
+}
+
+// Reduce CTA partials and decode the winner's plan.
+template <int MAXR>
+__global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb,
+                                                   const double2* __restrict__ blkf,
+                                                   const BlockRec* __restrict__ blk, int L,
+                                                   int window, const Best* __restrict__ partial,
+                                                   int n_partial, TrainOut* __restrict__ out) {
+  Best b{kInf * 10, LLONG_MAX, 0};
+  for (int i = threadIdx.x; i < n_partial; i += blockDim.x) {
+    const Best p = partial[i];
+    b.feasible += p.feasible;
+    if (better(p.cost, p.rank, b.cost, b.rank)) {
+      b.cost = p.cost;
+      b.rank = p.rank;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double c2 = __shfl_xor_sync(0xffffffffu, b.cost, o);
+    const long long r2 = __shfl_xor_sync(0xffffffffu, b.rank, o);
+    b.feasible += __shfl_xor_sync(0xffffffffu, b.feasible, o);
+    if (better(c2, r2, b.cost, b.rank)) {
+      b.cost = c2;
+      b.rank = r2;
+    }
+  }
+  __shared__ Best sb[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sb[wid] = b;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  b = sb[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+    b.feasible += sb[w].feasible;
+    if (better(sb[w].cost, sb[w].rank, b.cost, b.rank)) {
+      b.cost = sb[w].cost;
+      b.rank = sb[w].rank;
+    }
+  }
+  out->best = b;
+  out->n_stages = 0;
+  if (b.rank == LLONG_MAX) return;
+  Layout<MAXR> Y;
+  unrank<MAXR>(sp, b.rank, Y);
+  constexpr int NS = MAXR * kMaxPerRun;
+  int lay[NS], bis[NS];
+  double cost;
+  score<MAXR>(sp, tb, blkf, L, window, Y, cost, lay, bis);
+  int s = 0;
+  for (int q = 0; q < NS; ++q) {
+    if (bis[q] < 0) continue;
+    const BlockRec& br = blk[bis[q]];
+    const int o = tb.opt[(size_t)bis[q] * L + (lay[q] - 1)];
+    const int tp = 1 << o;
+    out->first[s] = br.start;
+    out->count[s] = br.n;
+    out->tp[s] = tp;
+    out->dp[s] = br.n / tp;
+    out->layers[s] = lay[q];
+    ++s;
+  }
+  out->n_stages = s;
+}
+
+// ===================================================================== host
+
+namespace {
+
+struct HostSpace {
+  TrainSpace sp{};
+  std::vector<int> ordered;
+  std::vector<int> run_start;  // global offset of each run
+  std::vector<int> pos;        // concatenated positions
+  std::vector<int> pos_off;
+  std::vector<BlockMeta> meta;
+  std::vector<int4> items;
+  int nblk = 0, tin_size = 0, tx_size = 0;
+  long long total = 0;
+};
+
+int build_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, HostSpace& h) {
+  if (n <= 0) return set_error(GP_INVALID, "constrained_search requires a non-empty train set");
+  if (o->max_stages_per_type < 1 || o->max_stages_per_type > kMaxPerRun)
+    return set_error(GP_INVALID, "max_stages_per_type must lie in [1, 4] for the sm_100a kernel");
+  h.ordered.assign(ids, ids + n);
+  for (int id : h.ordered)
+    if (id < 0 || id >= ctx->N) return set_error(GP_INVALID, "unknown device id " + std::to_string(id));
+  // canonical_order (src/train_search.cpp:13-22)
+  std::sort(h.ordered.begin(), h.ordered.end(), [&](int a, int b) {
+    if (ctx->h_type[a] != ctx->h_type[b]) return ctx->h_type[a] < ctx->h_type[b];
+    if (ctx->h_machine[a] != ctx->h_machine[b]) return ctx->h_machine[a] < ctx->h_machine[b];
+    return a < b;
+  });
+  for (int i = 1; i < n; ++i)
+    if (h.ordered[i] == h.ordered[i - 1])
+      return set_error(GP_INVALID, "duplicate device id " + std::to_string(h.ordered[i]));
+  // build_runs (src/train_search.cpp:30-50)
+  const bool dev_gran = n <= o->device_granularity_limit;
+  TrainSpace& sp = h.sp;
+  sp.R = 0;
+  for (int i = 0; i < n; ++i) {
+    if (i == 0 || ctx->h_type[h.ordered[i]] != ctx->h_type[h.ordered[i - 1]]) {
+      if (sp.R == GP_MAX_TYPES) return set_error(GP_INVALID, "too many gpu types");
+      h.run_start.push_back(i);
+      sp.R++;
+    }
+  }
+  h.run_start.push_back(n);
+  sp.n = n;
+  sp.max_per_run = o->max_stages_per_type;
+  sp.max_stages = std::min(ctx->sc.L, sp.R * o->max_stages_per_type);
+  if (sp.max_stages > GP_MAX_STAGES) return set_error(GP_INVALID, "max_stages exceeds GP_MAX_STAGES");
+  for (int r = 0; r < sp.R; ++r) {
+    const int s0 = h.run_start[r], len = h.run_start[r + 1] - s0;
+    sp.len[r] = len;
+    h.pos_off.push_back((int)h.pos.size());
+    h.pos.push_back(0);
+    for (int i = 1; i < len; ++i) {
+      const bool edge = ctx->h_machine[h.ordered[s0 + i]] != ctx->h_machine[h.ordered[s0 + i - 1]];
+      if (dev_gran || edge) h.pos.push_back(i);
+    }
+    h.pos.push_back(len);
+    sp.nc[r] = (int)(h.pos.size() - h.pos_off[r]) - 2;
+    sp.kmax[r] = std::min(sp.max_per_run, len);
+  }
+  // completion counts cnt[r][u]
+  std::memset(sp.cnt, 0, sizeof sp.cnt);
+  for (int u = 0; u <= sp.max_stages; ++u) sp.cnt[sp.R][u] = 1;
+  for (int r = sp.R - 1; r >= 0; --r) {
+    const int rem = sp.R - 1 - r;
+    for (int u = 0; u <= sp.max_stages; ++u) {
+      long long acc = 0;
+      for (int k = 1; k <= sp.kmax[r]; ++k) {
+        if (u + k + rem > sp.max_stages) break;
+        acc += binom_small(sp.nc[r], k - 1) * sp.cnt[r + 1][u + k];
+      }
+      sp.cnt[r][u] = acc;
+    }
+  }
+  h.total = sp.max_stages >= sp.R ? sp.cnt[0][0] : 0;
+  // blocks, transfer items
+  h.nblk = 0;
+  h.tin_size = 0;
+  h.tx_size = 0;
+  for (int r = 0; r < sp.R; ++r) {
+    const int nc = sp.nc[r], e = nc + 2;
+    sp.blk_off[r] = h.nblk;
+    for (int a = 0; a <= nc; ++a)
+      for (int b = a + 1; b <= nc + 1; ++b) h.meta.push_back(BlockMeta{r, a, b, h.run_start[r]});
+    h.nblk += (nc + 2) * (nc + 1) / 2;
+    sp.tin_off[r] = h.tin_size;
+    h.tin_size += e * e * e;
+    for (int a = 0; a <= nc - 1; ++a)
+      for (int b = a + 1; b <= nc; ++b)
+        for (int c = b + 1; c <= nc + 1; ++c) h.items.push_back(make_int4(r, a, b, c));
+    sp.tx_off[r] = h.tx_size;
+    if (r + 1 < sp.R) {
+      const int e2 = sp.nc[r + 1] + 2;
+      h.tx_size += e * e2;
+      for (int a = 0; a <= nc; ++a)
+        for (int c = 1; c <= sp.nc[r + 1] + 1; ++c) h.items.push_back(make_int4(r, a, 0, -c));
+    }
+  }
+  return GP_OK;
+}
+
+template <typename T>
+T* carve(char*& p, size_t count) {
+  p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+  T* r = reinterpret_cast<T*>(p);
+  p += sizeof(T) * count;
+  return r;
+}
+
+template <int MAXR>
+int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const double2* blkf,
+                const BlockRec* blk, int window, long long lo, long long hi, Best* partial,
+                int max_blocks, TrainOut* d_out) {
+  const long long span = hi - lo;
+  const int threads = 256;
+  long long chunk = span / ((long long)ctx->num_sms * 2048 * 4);
+  chunk = std::max(8LL, std::min(chunk, 512LL));
+  const long long n_chunks = (span + chunk - 1) / chunk;
+  long long blocks = (n_chunks + threads - 1) / threads;
+  blocks = std::max(1LL, std::min(blocks, (long long)max_blocks));
+  if (span > 0) {
+    k1_layout_scan<MAXR><<<(int)blocks, threads, 0, ctx->stream>>>(h.sp, tb, blkf, ctx->sc.L, window,
+                                                                    lo, hi, chunk, partial);
+    ctx->launches++;
+  } else {
+    blocks = 0;
+  }
+  k1_finalize<MAXR><<<1, 256, 0, ctx->stream>>>(h.sp, tb, blkf, blk, ctx->sc.L, window, partial,
+                                                 (int)blocks, d_out);
+  ctx->launches++;
+  GP_CUDA(cudaGetLastError());
+  return GP_OK;
+}
+
+}  // namespace
+
+int train_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int64_t* layouts) {
+  HostSpace h;
+  int rc = build_space(ctx, ids, n, o, h);
+  if (rc) return rc;
+  *layouts = h.total;
+  return GP_OK;
+}
+
+__global__ void k_extract_blkf(const BlockRec* __restrict__ blk, int nblk, double2* __restrict__ blkf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nblk) blkf[i] = make_double2(blk[i].flops, blk[i].lf_num);
+}
+
+int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_train_opts* o,
+                 long long lo, long long hi, gp_train_result* out, int32_t* stage_devices) {
+  std::memset(out, 0, sizeof *out);
+  HostSpace h;
+  int rc = build_space(ctx, ids, n, o, h);
+  if (rc) return rc;
+  if (lo < 0) lo = 0;
+  if (hi < 0 || hi > h.total) hi = h.total;
+  if (lo > hi) lo = hi;
+  out->layouts = hi - lo;
+  if (h.total == 0 || lo == hi) return GP_OK;  // std::nullopt
+
+  const int L = ctx->sc.L;
+  const int max_blocks = ctx->num_sms * 8;
+  // ---- device scratch layout
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+  add(sizeof(int) * n);                      // ordered
+  add(sizeof(int) * h.pos.size());           // pos
+  add(sizeof(int) * h.run_start.size());     // run_start
+  add(sizeof(BlockMeta) * h.meta.size());    // meta
+  add(sizeof(int4) * h.items.size());        // items
+  add(sizeof(BlockRec) * h.nblk);            // blk
+  add(sizeof(double2) * h.nblk);             // blkf
+  add(sizeof(double2) * (size_t)h.nblk * L); // stage
+  add(sizeof(int8_t) * (size_t)h.nblk * L);  // opt
+  add(sizeof(double) * (h.tin_size + 1));
+  add(sizeof(double) * (h.tx_size + 1));
+  add(sizeof(double) * (GP_MAX_STAGES + 1)); // fd_coef
+  add(sizeof(Best) * max_blocks);
+  add(sizeof(TrainOut));
+  char* base = static_cast<char*>(ctx_scratch(ctx, bytes));
+  if (!base) return GP_CUDA_ERROR;
+  char* p = base;
+  int* d_ordered = carve<int>(p, n);
+  int* d_pos = carve<int>(p, h.pos.size());
+  int* d_run_start = carve<int>(p, h.run_start.size());
+  BlockMeta* d_meta = carve<BlockMeta>(p, h.meta.size());
+  int4* d_items = carve<int4>(p, h.items.size());
+  BlockRec* d_blk = carve<BlockRec>(p, h.nblk);
+  double2* d_blkf = carve<double2>(p, h.nblk);
+  double2* d_stage = carve<double2>(p, (size_t)h.nblk * L);
+  int8_t* d_opt = carve<int8_t>(p, (size_t)h.nblk * L);
+  double* d_tin = carve<double>(p, h.tin_size + 1);
+  double* d_tx = carve<double>(p, h.tx_size + 1);
+  double* d_fd = carve<double>(p, GP_MAX_STAGES + 1);
+  Best* d_partial = carve<Best>(p, max_blocks);
+  TrainOut* d_out = carve<TrainOut>(p, 1);
+  // ---- one pinned staging buffer -> one H2D copy of the enumeration metadata
+  const size_t in_bytes = (size_t)(d_items + h.items.size()) - (size_t)d_ordered;
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(TrainOut))));
+  if (!hp) return GP_CUDA_ERROR;
+  auto stage_in = [&](const void* src, size_t sz, void* dptr) {
+    std::memcpy(hp + ((char*)dptr - (char*)d_ordered), src, sz);
+  };
+  stage_in(h.ordered.data(), sizeof(int) * n, d_ordered);
+  stage_in(h.pos.data(), sizeof(int) * h.pos.size(), d_pos);
+  stage_in(h.run_start.data(), sizeof(int) * h.run_start.size(), d_run_start);
+  stage_in(h.meta.data(), sizeof(BlockMeta) * h.meta.size(), d_meta);
+  if (!h.items.empty()) stage_in(h.items.data(), sizeof(int4) * h.items.size(), d_items);
+  GP_CUDA(cudaMemcpyAsync(d_ordered, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+
+  TrainTables tb{};
+  tb.ordered = d_ordered;
+  tb.pos = d_pos;
+  tb.blk = d_blk;
+  tb.stage = d_stage;
+  tb.opt = d_opt;
+  tb.tin = d_tin;
+  tb.tx = d_tx;
+  tb.fd_coef = d_fd;
+  for (int r = 0; r < h.sp.R; ++r) tb.pos_off[r] = h.pos_off[r];
+
+  k2a_block_stats<<<h.nblk, 256, 0, ctx->stream>>>(d_ordered, d_meta, d_pos, tb, d_blk, ctx->d_type,
+                                                   ctx->d_machine, ctx->d_flops, ctx->d_hbm_cap,
+                                                   ctx->d_links, ctx->N, L, ctx->sc.mb, d_fd);
+  ctx->launches++;
+  if (!h.items.empty()) {
+    const int warps_per_block = 8;
+    const int grid = (int)((h.items.size() + warps_per_block - 1) / warps_per_block);
+    k2b_transfers<<<grid, 32 * warps_per_block, 0, ctx->stream>>>(
+        d_ordered, d_items, (int)h.items.size(), d_pos, tb, h.sp, d_run_start, ctx->d_links, ctx->N,
+        ctx->sc.tokens > 0 ? ctx->sc.act_tok_h2 : 0.0, d_tin, d_tx);
+    ctx->launches++;
+  }
+  {
+    const long long cnt = (long long)h.nblk * L;
+    k2c_stage_table<<<(int)((cnt + 255) / 256), 256, 0, ctx->stream>>>(d_blk, h.nblk, ctx->sc,
+                                                                      ctx->d_ceff, d_stage, d_opt);
+    k_extract_blkf<<<(h.nblk + 255) / 256, 256, 0, ctx->stream>>>(d_blk, h.nblk, d_blkf);
+    ctx->launches += 2;
+  }
+  GP_CUDA(cudaGetLastError());
+  const int R = h.sp.R;
+  if (R == 1) rc = launch_scan<1>(ctx, h, tb, d_blkf, d_blk, window, lo, hi, d_partial, max_blocks, d_out);
+  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, d_blkf, d_blk, window, lo, hi, d_partial, max_blocks, d_out);
+  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, d_blkf, d_blk, window, lo, hi, d_partial, max_blocks, d_out);
+  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, d_blkf, d_blk, window, lo, hi, d_partial, max_blocks, d_out);
+  else rc = launch_scan<8>(ctx, h, tb, d_blkf, d_blk, window, lo, hi, d_partial, max_blocks, d_out);
+  if (rc) return rc;
+  TrainOut* ho = reinterpret_cast<TrainOut*>(hp);
+  GP_CUDA(cudaMemcpyAsync(ho, d_out, sizeof(TrainOut), cudaMemcpyDeviceToHost, ctx->stream));
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  out->feasible = ho->best.feasible;
+  if (ho->best.rank != LLONG_MAX) {
+    out->found = 1;
+    out->cost = ho->best.cost;
+    out->rank = ho->best.rank;
+    out->n_stages = ho->n_stages;
+    for (int s = 0; s < ho->n_stages; ++s) {
+      out->stage[s].first = ho->first[s];
+      out->stage[s].count = ho->count[s];
+      out->stage[s].tp = ho->tp[s];
+      out->stage[s].dp = ho->dp[s];
+      out->stage[s].layers = ho->layers[s];
+    }
+    if (stage_devices) std::memcpy(stage_devices, h.ordered.data(), sizeof(int32_t) * n);
+  }
+  return GP_OK;
+}
+
+}  // namespace gp

@@ -1,0 +1,156 @@
+"""Python host binding of libgplan.so — mirrors the reference's free-function API
+(inc/train_search.hpp:29, inc/rollout_milp.hpp:22-37, inc/cost_model.hpp:63,
+inc/partition.hpp:40-55) with the same argument meaning and error behaviour:
+ValidationError / InfeasibleError / BandInfeasibleError are raised where the
+reference throws them, and `constrained_search` returns None for std::nullopt.
+
+There is no CPU fallback: constructing an Engine without the built library or
+without an sm_100 GPU raises EngineUnavailable.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+from .inputs import Problem
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgplan.so")
+_lib = None
+
+
+class EngineUnavailable(RuntimeError):
+    pass
+
+
+class ValidationError(ValueError):
+    pass
+
+
+class InfeasibleError(RuntimeError):
+    pass
+
+
+class BandInfeasibleError(InfeasibleError):
+    pass
+
+
+class CapacityError(RuntimeError):
+    pass
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise EngineUnavailable(
+                f"{_LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        _lib = C.CDLL(_LIB_PATH)
+        abi.declare(_lib, "gp")
+        _lib.gp_ctx_destroy.argtypes = [C.c_void_p]
+        _lib.gp_ctx_launches.argtypes = [C.c_void_p]
+        _lib.gp_ctx_launches.restype = C.c_longlong
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == abi.GP_OK:
+        return
+    msg = lib().gp_last_error().decode()
+    if rc == abi.GP_INVALID:
+        raise ValidationError(msg)
+    if rc == abi.GP_BAND_INFEASIBLE:
+        raise BandInfeasibleError(msg)
+    if rc == abi.GP_INFEASIBLE:
+        raise InfeasibleError(msg)
+    if rc == abi.GP_CAPACITY:
+        raise CapacityError(msg)
+    raise EngineUnavailable(f"CUDA error: {msg}")
+
+
+def _ids(ids) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
+
+
+@dataclass
+class Stage:
+    devices: list
+    tp: int
+    dp: int
+    layers: int
+
+
+@dataclass
+class TrainSearchResult:
+    stages: list
+    cost: float
+    rank: int
+    layouts: int
+    feasible: int
+
+
+class Engine:
+    """One engine context (cluster + workload + calibration uploaded to one GPU)."""
+
+    def __init__(self, problem: Problem, device: int = 0):
+        self.problem = problem
+        self.n_devices = problem.cluster.n
+        c, w, k = problem.structs()
+        self._structs = (c, w, k)
+        h = C.c_void_p()
+        _check(lib().gp_ctx_create(C.byref(c), C.byref(w), C.byref(k), device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().gp_ctx_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def launches(self) -> int:
+        return int(lib().gp_ctx_launches(self._h))
+
+    # ---- training side ------------------------------------------------------
+    def train_space(self, train_set, opts: abi.gp_train_opts | None = None) -> int:
+        ids = _ids(train_set)
+        out = C.c_int64()
+        _check(lib().gp_train_space(self._h, ids.ctypes.data_as(abi.i32p), len(ids),
+                                    C.byref(opts or abi.default_train_opts()), C.byref(out)))
+        return out.value
+
+    def constrained_search_raw(self, train_set, window: int, opts=None, lo: int = 0, hi: int = -1):
+        ids = _ids(train_set)
+        res = abi.gp_train_result()
+        devs = np.zeros(max(len(ids), 1), dtype=np.int32)
+        o = opts or abi.default_train_opts()
+        if lo == 0 and hi < 0:
+            rc = lib().gp_constrained_search(self._h, ids.ctypes.data_as(abi.i32p), len(ids), window,
+                                             C.byref(o), C.byref(res), devs.ctypes.data_as(abi.i32p))
+        else:
+            rc = lib().gp_constrained_search_range(self._h, ids.ctypes.data_as(abi.i32p), len(ids),
+                                                   window, C.byref(o), lo, hi, C.byref(res),
+                                                   devs.ctypes.data_as(abi.i32p))
+        _check(rc)
+        return res, devs
+
+    def constrained_search(self, train_set, window: int, opts=None, lo: int = 0, hi: int = -1):
+        """constrained_search (inc/train_search.hpp:29-33); None == std::nullopt."""
+        res, devs = self.constrained_search_raw(train_set, window, opts, lo, hi)
+        if not res.found:
+            return None
+        stages = []
+        for s in range(res.n_stages):
+            st = res.stage[s]
+            stages.append(Stage(devs[st.first:st.first + st.count].tolist(), st.tp, st.dp, st.layers))
+        return TrainSearchResult(stages, res.cost, res.rank, res.layouts, res.feasible)
