@@ -179,6 +179,7 @@ typedef struct {
   int* cuts[GP_MAX_TYPES];   /* cut positions per run (local indices) */
   int n_cuts[GP_MAX_TYPES];
   int max_stages, max_per_run;
+  int64_t cnt[GP_MAX_TYPES + 1][GP_MAX_STAGES + 2];  /* completions of runs r.. after u stages */
 } layout_space_t;
 
 static const gp_cluster* g_sort_cluster;
@@ -364,6 +365,12 @@ static void recurse_cuts(search_t* st, int r, int used, int k, int chosen, int n
     st->blk_start[used + chosen] = base + prev;
     st->blk_len[used + chosen] = sp->run_len[r] - prev;
     st->n_blocks = used + k;
+    /* skip whole subtrees outside [lo, hi): their size is cnt[r+1][used+k] */
+    int64_t size = sp->cnt[r + 1][used + k];
+    if (st->rank + size <= st->lo || st->rank >= st->hi) {
+      st->rank += size;
+      return;
+    }
     recurse_runs(st, r + 1, used + k);
     return;
   }
@@ -399,11 +406,10 @@ static int64_t binom(int n, int k) {
   return v;
 }
 
-static int64_t count_layouts(const layout_space_t* sp) {
+static int64_t count_layouts(layout_space_t* sp) {
   if (sp->max_stages < sp->n_runs) return 0;
-  int64_t cnt[GP_MAX_TYPES + 1][GP_MAX_STAGES + 2];
-  memset(cnt, 0, sizeof cnt);
-  for (int u = 0; u <= sp->max_stages; ++u) cnt[sp->n_runs][u] = 1;
+  memset(sp->cnt, 0, sizeof sp->cnt);
+  for (int u = 0; u <= sp->max_stages; ++u) sp->cnt[sp->n_runs][u] = 1;
   for (int r = sp->n_runs - 1; r >= 0; --r) {
     int remaining_runs = sp->n_runs - r - 1;
     for (int u = 0; u <= sp->max_stages; ++u) {
@@ -411,12 +417,12 @@ static int64_t count_layouts(const layout_space_t* sp) {
       int kmax = sp->max_per_run < sp->run_len[r] ? sp->max_per_run : sp->run_len[r];
       for (int k = 1; k <= kmax; ++k) {
         if (u + k + remaining_runs > sp->max_stages) break;
-        acc += binom(sp->n_cuts[r], k - 1) * cnt[r + 1][u + k];
+        acc += binom(sp->n_cuts[r], k - 1) * sp->cnt[r + 1][u + k];
       }
-      cnt[r][u] = acc;
+      sp->cnt[r][u] = acc;
     }
   }
-  return cnt[0][0];
+  return sp->cnt[0][0];
 }
 
 int or_train_space(const gp_cluster* c, const gp_workload* w, const int32_t* ids, int32_t n,

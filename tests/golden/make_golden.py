@@ -1,0 +1,78 @@
+"""Generates the committed golden vectors from the UNMODIFIED reference.
+
+Run in the build container (needs oracle/_ref/libref.so, i.e. `make -C oracle ref`
+with /root/reference present):  python tests/golden/make_golden.py
+Every fixture records the reference's own output on inputs under data/, so the
+GPU box (no /root/reference) can check the oracle and the engine against it.
+"""
+import json
+import os
+import shutil
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from common import CONFIGS, ETA, problem, random_train_sets, type_prefix_sets  # noqa: E402
+from oracles import Oracle, Ref  # noqa: E402
+
+REF_PLAN = "/root/reference/proj/out/desk/plan.json"
+
+
+def dump(name, obj):
+    with open(os.path.join(HERE, name), "w") as f:
+        json.dump(obj, f, separators=(",", ":"))
+        f.write("\n")
+
+
+def main():
+    shutil.copy(REF_PLAN, os.path.join(HERE, "desk_plan.json"))
+    # ---- full schedules (plan_to_json + trace)
+    sched = {}
+    for name, etas in (("c1_desk_mixed", [1, -1]), ("c2_16gpu", [-1]), ("c3_64gpu", [1, 2, 3, 4])):
+        ref = Ref(problem(name))
+        for eta in etas:
+            t = time.time()
+            out = ref.schedule(eta=eta)
+            sched[f"{name}/eta={eta}"] = {"plan": json.loads(out["plan_json"]), "trace": out["trace"],
+                                          "ref_seconds": time.time() - t}
+    dump("schedules.json", sched)
+    # ---- constrained_search on sampled + probe train sets
+    ts = {}
+    for name in CONFIGS:
+        p = problem(name)
+        ref, orc = Ref(p), Oracle(p)
+        n = p.cluster.n
+        sets = random_train_sets(n, 24, seed=77 + n)
+        for lead in range(len(p.cluster.type_names)):
+            sets += type_prefix_sets(p, lead, sorted({1, 2, 3, n // 4, n // 2, n - 1}))
+        cases = []
+        for ids in sets:
+            if orc.train_space(ids) > 300_000:  # keep the reference run bounded
+                continue
+            for window in (ETA[name] + 1, 2 * ETA[name] + 2):
+                r = ref.constrained_search(ids, window)
+                r.pop("seconds")
+                cases.append({"ids": ids, "window": window, "ref": r, "layouts": orc.train_space(ids)})
+        ts[name] = cases
+        print(name, len(cases), "train-search cases")
+    dump("train_search.json", ts)
+    # ---- full candidate lists (enumeration order pin) on small sets
+    cand = {}
+    p = problem("c2_16gpu")
+    ref = Ref(p)
+    for ids in ([0, 1, 2, 3], [0, 1, 2, 8, 9], [4, 5, 6, 7, 12, 13, 14, 15], list(range(16))[::3]):
+        lst = ref.train_candidates(ids, 3)
+        blocks = []
+        for c in lst:
+            key = [s["devices"] for s in c["stages"]]
+            if not blocks or blocks[-1] != key:
+                blocks.append(key)
+        cand[json.dumps(ids)] = {"block_lists": blocks, "candidates": lst}
+    dump("train_candidates.json", cand)
+
+
+if __name__ == "__main__":
+    main()

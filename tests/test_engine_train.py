@@ -1,0 +1,112 @@
+"""GPU parity: the sm_100a layout search vs the oracle / the reference's golden vectors.
+
+Bar (BASELINE.json north_star): selected plan, feasible-set size and cost
+bit-exact (cost compared with ==, not a tolerance).
+"""
+import pytest
+
+from common import CONFIGS, ETA, golden, problem, random_train_sets, type_prefix_sets
+from oracles import Oracle, train_result_dict
+
+pytestmark = pytest.mark.gpu
+
+_engines = {}
+
+
+def engine(name):
+    from paper_2511_00796_b200.engine import Engine
+    if name not in _engines:
+        _engines[name] = Engine(problem(name))
+    return _engines[name]
+
+
+def run(name, ids, window, lo=0, hi=-1):
+    res, devs = engine(name).constrained_search_raw(ids, window, lo=lo, hi=hi)
+    return train_result_dict(res, devs)
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_golden_train_search(name):
+    for case in golden("train_search.json")[name]:
+        got = run(name, case["ids"], case["window"])
+        ref = case["ref"]
+        assert got["found"] == ref["found"], case["ids"]
+        assert got["layouts"] == case["layouts"]
+        if ref["found"]:
+            assert got["cost"] == ref["cost"], case["ids"]
+            assert got["stages"] == ref["stages"], case["ids"]
+
+
+@pytest.mark.parametrize("name", CONFIGS[:4])
+def test_random_sets_vs_oracle(name):
+    p = problem(name)
+    orc = Oracle(p)
+    sets = random_train_sets(p.cluster.n, 40, seed=1000 + p.cluster.n)
+    for lead in range(len(p.cluster.type_names)):
+        sets += type_prefix_sets(p, lead, range(1, p.cluster.n, max(1, p.cluster.n // 12)))
+    checked = 0
+    for ids in sets:
+        if orc.train_space(ids) > 200_000:
+            continue
+        for window in (1, ETA[name] + 1, 64):
+            want = orc.constrained_search(ids, window)
+            got = run(name, ids, window)
+            assert got == want, (ids, window)
+            checked += 1
+    assert checked >= 40
+
+
+def test_ranges_recombine_exactly():
+    """Rank-range sharding (multi-GPU split): lexicographic (cost, rank) min over shards == full."""
+    name = "c4_256gpu"
+    p = problem(name)
+    eng = engine(name)
+    ids = list(range(1, p.cluster.n))
+    total = eng.train_space(ids)
+    assert total > 1_000_000
+    full = run(name, ids, 3)
+    shards = [(total * i) // 8 for i in range(9)]
+    parts = [run(name, ids, 3, lo=a, hi=b) for a, b in zip(shards, shards[1:])]
+    assert sum(x["feasible"] for x in parts) == full["feasible"]
+    assert sum(x["layouts"] for x in parts) == total
+    win = min((x for x in parts if x["found"]), key=lambda x: (x["cost"], x["rank"]))
+    assert win == {**full, "layouts": win["layouts"], "feasible": win["feasible"]}
+    # a window of the space deep inside, checked against the oracle restricted to it
+    lo, hi = total // 3, total // 3 + 50_000
+    assert run(name, ids, 3, lo=lo, hi=hi) == Oracle(p).constrained_search(ids, 3, lo=lo, hi=hi)
+
+
+def test_c5_full_space_slices_vs_oracle():
+    """C5 (1024 GPUs, 3 types): a 2.4e9-layout train set; slices checked against the oracle."""
+    name = "c5_1024gpu"
+    p = problem(name)
+    ids = list(range(p.cluster.n))[:-1]
+    eng = engine(name)
+    total = eng.train_space(ids)
+    assert total == Oracle(p).train_space(ids)
+    assert total > 2_000_000_000
+    orc = Oracle(p)
+    for lo in (0, total // 7, total // 2, total - 40_000):
+        hi = min(total, lo + 40_000)
+        assert run(name, ids, 3, lo=lo, hi=hi) == orc.constrained_search(ids, 3, lo=lo, hi=hi)
+
+
+def test_edge_cases():
+    from paper_2511_00796_b200 import abi
+    from paper_2511_00796_b200.engine import ValidationError
+    eng = engine("c5_1024gpu")
+    with pytest.raises(ValidationError):
+        eng.constrained_search([], 3)
+    with pytest.raises(ValidationError):
+        eng.constrained_search([0, 0], 3)
+    with pytest.raises(ValidationError):
+        eng.constrained_search([5000], 3)
+    with pytest.raises(ValidationError):
+        eng.constrained_search([0, 1], 3, opts=abi.gp_train_opts(5, 16))
+    # 70B on one H800: nothing fits -> std::nullopt, same as the oracle
+    assert eng.constrained_search([0], 3) is None
+    orc = Oracle(problem("c5_1024gpu"))
+    assert orc.constrained_search([0], 3)["found"] is False
+    # single device that fits
+    got = run("c1_desk_mixed", [3], 2)
+    assert got == Oracle(problem("c1_desk_mixed")).constrained_search([3], 2)
