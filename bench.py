@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""bench.py — candidate plans evaluated/sec of the B200 plan-evaluation engine.
+
+Workload (BASELINE.json configs[4], the largest; fits one GPU because no plan
+list is materialised): constrained_search over the C5 1024-GPU cluster
+(24x16 H800 + 24x16 H20 + 16x16 PCIe-class, 70B policy, L=80) for the 1023-device
+three-type train set -> 2,427,584,512 candidate layouts per step, window 3.
+One step = one full pass over that candidate space (stage-table build + layout
+scan + argmin). At N GPUs the rank space is split into N contiguous shards
+(strong scaling), and the per-shard (cost, rank) winners are all-gathered over
+NCCL and reduced lexicographically (the only collective).
+
+value : candidates/s with the train set resident on the device (device time of
+        the stage tables + scan, CUDA events on the engine's stream, max over ranks)
+e2e   : the same metric through the public C ABI with host buffers:
+        gp_constrained_search_range (host prep + H2D + kernels + D2H) + the NCCL
+        all-gather, timed on the device.
+Inputs are tiny (~0.5 MB of tables), so L2 is flushed (a 512 MiB write)
+between timed steps.
+
+--impl reference: the reference's own constrained_search (oracle/_ref, compiled
+from /root/reference by oracle/Makefile) on the host cores, one thread per core
+(cap 32), on bounded C5 train sets (its plan list is materialised in RAM).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+CONFIG = "c5_1024gpu"
+WINDOW = 3
+METRIC = "candidate plans evaluated/sec"
+UNIT = "plans/s"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), \
+        int(os.environ.get("WORLD_SIZE", 1))
+
+
+def problem():
+    from common import problem as load
+    return load(CONFIG)
+
+
+def bench_train_set(p):
+    return list(range(p.cluster.n - 1))
+
+
+def cpu_sample_sets(p, count):
+    """Bounded C5 train sets for the reference (which materialises every layout):
+    16 H800 machines + 8 H20 machines -> 36,864 layouts, 384 devices each,
+    rotated over the cluster's machines."""
+    cl = p.cluster
+    by_type = {}
+    for m, t in enumerate(cl.machine_type.tolist()):
+        by_type.setdefault(t, []).append(m)
+    sets = []
+    for i in range(count):
+        h800 = by_type[0][i % 8: i % 8 + 16]
+        h20 = by_type[1][(3 * i) % 16: (3 * i) % 16 + 8]
+        ms = set(h800 + h20)
+        sets.append([d for d in range(cl.n) if cl.device_machine[d] in ms])
+    return sets
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu_index: int):
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- reference
+def ref_rate(p, sets, threads, window=WINDOW):
+    import ctypes as C
+
+    import numpy as np
+    from oracles import Ref, ref_available
+    if not ref_available():
+        return None
+    ref = Ref(p)
+    lib = ref.lib
+    lib.ref_bench_constrained_search.argtypes = [C.c_void_p, C.POINTER(C.c_int32),
+                                                 C.POINTER(C.c_int32), C.c_int, C.c_int, C.c_int,
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(s, dtype=np.int32) for s in sets]))
+    lens = np.asarray([len(s) for s in sets], dtype=np.int32)
+    secs, chk = C.c_double(), C.c_double()
+    rc = lib.ref_bench_constrained_search(ref.h, flat.ctypes.data_as(C.POINTER(C.c_int32)),
+                                          lens.ctypes.data_as(C.POINTER(C.c_int32)), len(sets),
+                                          window, threads, C.byref(secs), C.byref(chk))
+    if rc:
+        raise RuntimeError(lib.ref_last_error().decode())
+    return secs.value
+
+
+def cpu_baseline(p, threads=1, n_sets=3):
+    """Reference (oracle/_ref) on the host cores, bounded sample; port (oracle/) if absent."""
+    from oracles import Oracle, ref_available
+    sets = cpu_sample_sets(p, n_sets)
+    orc = Oracle(p)
+    layouts = sum(orc.train_space(s) for s in sets)
+    sample = f"{n_sets} C5 train sets x 36,864 layouts (16 H800 + 8 H20 machines, 384 devices), window {WINDOW}"
+    if ref_available():
+        secs = ref_rate(p, sets, threads)
+        kind = "reference"
+    else:
+        t = time.perf_counter()
+        for s in sets:
+            orc.constrained_search(s, WINDOW)
+        secs = time.perf_counter() - t
+        kind = "port"
+        threads = 1
+    return {"value": layouts / secs, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": sample, "seconds": secs, "cpu": cpu_model(), "nproc": os.cpu_count()}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    p = problem()
+    threads = max(1, min(os.cpu_count() or 1, 32))
+    sets = cpu_sample_sets(p, threads)
+    from oracles import Oracle, ref_available
+    orc = Oracle(p)
+    layouts = sum(orc.train_space(s) for s in sets)
+    kind = "reference" if ref_available() else "port"
+    times = []
+    for i in range(args.warmup + args.steps):
+        if kind == "reference":
+            secs = ref_rate(p, sets, threads)
+        else:
+            t = time.perf_counter()
+            for s in sets:
+                orc.constrained_search(s, WINDOW)
+            secs = time.perf_counter() - t
+        if i >= args.warmup:
+            times.append(secs)
+    total = sum(times)
+    value = layouts * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{CONFIG}: reference constrained_search, bounded sample of "
+                               f"{len(sets)} train sets x 36,864 layouts (one per host thread)",
+                   "window": WINDOW},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads if kind == "reference" else 1,
+                         "kind": kind, "sample": f"{len(sets)} C5 train sets x 36,864 layouts per step",
+                         "cpu": cpu_model(), "nproc": os.cpu_count()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------- B200
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_00796_b200.engine import Engine
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    p = problem()
+    ids = bench_train_set(p)
+    eng = Engine(p, device=local_rank)
+    total = eng.train_space(ids)
+    lo, hi = total * rank // world, total * (rank + 1) // world
+    stream = torch.cuda.ExternalStream(eng.stream_ptr, device=dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def gather(res):
+        """All-gather (cost, rank, feasible) of every shard; lexicographic min."""
+        t = torch.tensor([res.cost if res.found else float("inf"), float(res.rank if res.found else -1),
+                          float(res.feasible)], dtype=torch.float64, device=dev)
+        if world == 1:
+            return t.view(1, 3)
+        out = torch.empty(world, 3, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(out, t)
+        return out
+
+    # ---- device-resident timing (value) ------------------------------------
+    eng.set_timing(True)
+    eng.train_prepare(ids)
+    for _ in range(args.warmup):
+        eng.train_launch(WINDOW, lo, hi)
+        eng.train_collect()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    dev_ms, k1_ms, k2_ms = [], [], []
+    res = None
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.train_launch(WINDOW, lo, hi)
+        b.record(stream)
+        res, _ = eng.train_collect()
+        dev_ms.append(a.elapsed_time(b))
+        k2, k1 = eng.train_timing()
+        k2_ms.append(k2)
+        k1_ms.append(k1)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    win = gather(res)
+    # ---- end-to-end through the public C ABI with host buffers (e2e) --------
+    h2d0, d2h0, _ = eng.io_bytes()
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        r2, _ = eng.constrained_search_raw(ids, WINDOW, lo=lo, hi=hi)
+        g = gather(r2)
+        b.record(torch.cuda.current_stream(dev))
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b))
+    h2d1, d2h1, sum_stages = eng.io_bytes()
+    steps_e2e = args.warmup + args.steps
+    h2d_step = (h2d1 - h2d0) / steps_e2e
+    d2h_step = (d2h1 - d2h0) / steps_e2e + 24 * world
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    t_dev = max_over_ranks(sum(dev_ms))
+    t_e2e = max_over_ranks(sum(e2e_ms))
+    t_k1 = max_over_ranks(sum(k1_ms))
+    t_k2 = max_over_ranks(sum(k2_ms))
+    launches = eng.launches
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    # argmin sanity: every rank's winner reduced lexicographically
+    best = min((tuple(x) for x in win.tolist() if x[1] >= 0), default=None)
+    value = total * args.steps / (t_dev / 1e3)
+    e2e = total * args.steps / (t_e2e / 1e3)
+    # ---- roofline of the dominant kernel (K1 layout scan) -------------------
+    # algorithmic fp64 pipe work per candidate, counted on the K1 source as written
+    # (DESIGN.md "K1 roofline"): S-1 DADD (total fold) + S DDIV (shares, 8 pipe
+    # instructions each on sm_100: MUFU.RCP64H + 7 DFMA/DMUL) + S DADD (remainders)
+    # + S-1 DADD (transfers) + 1 DMUL (fill/drain) + 2 DADD (per_step) + 1 DMUL (window)
+    avg_S = sum_stages / total
+    ops_per_cand = (avg_S - 1) + 8 * avg_S + avg_S + (avg_S - 1) + 1 + 2 + 1
+    peak_ops = eng.fp64_peak()
+    k1_s = t_k1 / 1e3 / args.steps
+    shard = hi - lo
+    achieved = ops_per_cand * shard / k1_s
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_dev / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{CONFIG}: constrained_search over the 1023-device 3-type train set "
+                               f"(24x16 H800 + 24x16 H20 + 15x16+15 PCIe), 70B L=80, window {WINDOW}",
+                   "candidates_per_step": total, "parallelism": f"rank-range shards x{world}",
+                   "l2": "flushed (512 MiB write) between timed steps"},
+        "time_to_best_plan_ms": t_dev / args.steps,
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d_step),
+                "d2h_bytes_per_step": int(d2h_step), "ms_per_step": t_e2e / args.steps},
+        "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
+                     "unit": "TFLOP/s", "frac": achieved / peak_ops, "traffic": None,
+                     "kernel": "k1_layout_scan", "ops_per_candidate": ops_per_cand,
+                     "avg_stages": avg_S, "k1_ms_per_step": t_k1 / args.steps,
+                     "k2_ms_per_step": t_k2 / args.steps,
+                     "peak_source": "measured on this GPU by gp_fp64_peak (independent DADD chains)"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "winner": {"cost": best[0], "rank": int(best[1])} if best else None,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(p)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

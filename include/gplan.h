@@ -204,6 +204,25 @@ int gp_constrained_search_range(gp_ctx* ctx, const int32_t* ids, int32_t n, int3
                                 const gp_train_opts* opts, int64_t lo, int64_t hi,
                                 gp_train_result* out, int32_t* stage_devices);
 
+/* Split form of gp_constrained_search_range for callers that overlap work or
+ * time the device part alone (bench.py): prepare uploads the train set's
+ * enumeration metadata (one H2D copy), launch enqueues the stage-table build
+ * and the layout scan on the context's stream without blocking, collect
+ * copies the result back and synchronises. */
+int gp_train_prepare(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* opts);
+int gp_train_launch(gp_ctx* ctx, int32_t window, int64_t lo, int64_t hi);
+int gp_train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices);
+/* The context's CUDA stream (cudaStream_t), for event timing by the caller. */
+void* gp_ctx_stream(gp_ctx* ctx);
+/* Measurement hooks (bench.py): device time of the last launch's stage-table
+ * build (K2) and layout scan (K1 + finalize); bytes moved host<->device by API
+ * calls so far; sum over the prepared space of the stage count; FP64 pipe
+ * throughput probe (DADD/s) used as the roofline denominator. */
+int gp_ctx_set_timing(gp_ctx* ctx, int on);
+int gp_train_timing(gp_ctx* ctx, float* k2_ms, float* k1_ms);
+void gp_ctx_io_bytes(gp_ctx* ctx, long long* h2d, long long* d2h, double* sum_stages);
+int gp_fp64_peak(gp_ctx* ctx, double* dadd_per_s);
+
 /* ---- rollout side: replaces enumerate_configs / rollout_capacities / solve_milp
  *      (src/rollout_milp.cpp:113-254) ------------------------------------- */
 

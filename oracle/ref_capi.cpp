@@ -12,6 +12,7 @@
 // nlohmann, which prints with 17 significant digits -> lossless).
 
 #include <chrono>
+#include <thread>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -309,6 +310,38 @@ int ref_partition_objective(void* h, const int* train, int nt, double* objective
     auto* ctx = static_cast<RefCtx*>(h);
     *objective = partition_objective(ctx->cluster, ids_vec(train, nt));
     *fraction = compute_fraction(ctx->cluster, ids_vec(train, nt));
+  });
+}
+
+// CPU baseline: `threads` host threads each run the reference's constrained_search
+// on train sets taken round-robin from `sets` (concatenated ids, set_len[i] each).
+// Returns wall seconds; layouts are counted by the caller.
+int ref_bench_constrained_search(void* h, const int* ids, const int* set_len, int n_sets,
+                                 int window, int threads, double* seconds, double* checksum) {
+  return guarded([&] {
+    auto* ctx = static_cast<RefCtx*>(h);
+    std::vector<std::vector<int>> sets;
+    int off = 0;
+    for (int i = 0; i < n_sets; ++i) {
+      sets.emplace_back(ids + off, ids + off + set_len[i]);
+      off += set_len[i];
+    }
+    std::vector<double> costs(sets.size(), 0.0);
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) {
+      pool.emplace_back([&, t] {
+        for (size_t i = t; i < sets.size(); i += threads) {
+          auto r = constrained_search(sets[i], ctx->cluster, ctx->work, ctx->calib, window);
+          costs[i] = r ? r->cost : -1.0;
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    double cs = 0;
+    for (double c : costs) cs += c;
+    *checksum = cs;
   });
 }
 

@@ -11,6 +11,10 @@ namespace gp {
 int train_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int64_t* layouts);
 int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_train_opts* o,
                  long long lo, long long hi, gp_train_result* out, int32_t* stage_devices);
+int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o);
+int train_launch(gp_ctx* ctx, int window, long long lo, long long hi);
+int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices);
+void train_state_free(gp_ctx* ctx);
 
 static thread_local std::string g_error;
 
@@ -42,6 +46,7 @@ void* ctx_scratch(gp_ctx* ctx, size_t bytes) {
 void* ctx_pinned(gp_ctx* ctx, size_t bytes) {
   if (bytes > ctx->h_pinned_bytes) {
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  train_state_free(ctx);
     ctx->h_pinned = nullptr;
     size_t want = bytes + bytes / 4 + 4096;
     cudaError_t e = cudaMallocHost(&ctx->h_pinned, want);
@@ -205,6 +210,9 @@ void gp_ctx_destroy(gp_ctx* ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  train_state_free(ctx);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -231,6 +239,83 @@ int gp_constrained_search_range(gp_ctx* ctx, const int32_t* ids, int32_t n, int3
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return train_search(ctx, ids, n, window, o, lo, hi, out, stage_devices);
+}
+
+int gp_train_prepare(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* o) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return train_prepare(ctx, ids, n, o);
+}
+
+int gp_train_launch(gp_ctx* ctx, int32_t window, int64_t lo, int64_t hi) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return train_launch(ctx, window, lo, hi);
+}
+
+int gp_train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return train_collect(ctx, out, stage_devices);
+}
+
+int gp_ctx_set_timing(gp_ctx* ctx, int on) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  for (auto& e : ctx->ev)
+    if (!e) GP_CUDA(cudaEventCreate(&e));
+  ctx->timing = on != 0;
+  return GP_OK;
+}
+
+// Device time of the last gp_train_launch: stage tables (K2) and layout scan (K1 + finalize).
+int gp_train_timing(gp_ctx* ctx, float* k2_ms, float* k1_ms) {
+  if (!ctx || !ctx->timing) return set_error(GP_INVALID, "timing not enabled");
+  GP_CUDA(cudaEventElapsedTime(k2_ms, ctx->ev[0], ctx->ev[1]));
+  GP_CUDA(cudaEventElapsedTime(k1_ms, ctx->ev[1], ctx->ev[2]));
+  return GP_OK;
+}
+
+void gp_ctx_io_bytes(gp_ctx* ctx, long long* h2d, long long* d2h, double* sum_stages) {
+  *h2d = ctx->h2d_bytes;
+  *d2h = ctx->d2h_bytes;
+  *sum_stages = ctx->sum_stages;
+}
+
+// FP64 pipe throughput probe (bench.py roofline denominator): independent DADD chains.
+__global__ void __launch_bounds__(256) k_fp64_peak(double* out, int iters, double y) {
+  double a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+         a6 = a0 + 6, a7 = a0 + 7;
+  for (int i = 0; i < iters; ++i) {
+    a0 += y; a1 += y; a2 += y; a3 += y; a4 += y; a5 += y; a6 += y; a7 += y;
+  }
+  if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == -1.0) out[0] = a0;
+}
+
+int gp_fp64_peak(gp_ctx* ctx, double* dadd_per_s) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  double* d = static_cast<double*>(ctx_scratch(ctx, 1 << 20));
+  if (!d) return GP_CUDA_ERROR;
+  cudaEvent_t a, b;
+  GP_CUDA(cudaEventCreate(&a));
+  GP_CUDA(cudaEventCreate(&b));
+  const int blocks = ctx->num_sms * 8, iters = 1 << 14;
+  k_fp64_peak<<<blocks, 256, 0, ctx->stream>>>(d, iters, 1e-300);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    GP_CUDA(cudaEventRecord(a, ctx->stream));
+    k_fp64_peak<<<blocks, 256, 0, ctx->stream>>>(d, iters, 1e-300);
+    GP_CUDA(cudaEventRecord(b, ctx->stream));
+    GP_CUDA(cudaEventSynchronize(b));
+    float ms;
+    GP_CUDA(cudaEventElapsedTime(&ms, a, b));
+    best = ms < best ? ms : best;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *dadd_per_s = (double)blocks * 256 * iters * 8 / (best * 1e-3);
+  return GP_OK;
 }
 
 }  // extern "C"

@@ -126,6 +126,15 @@ struct gp_ctx {
   int num_sms = 148;
   // kernel launches issued by this context (bench.py's gpu_launches claim)
   long long launches = 0;
+  // prepared train set (train.cu)
+  void* train_state = nullptr;
+  // optional device timing of the train phases (bench.py): events around K2 and K1
+  bool timing = false;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // host<->device bytes moved by API calls (bench.py's e2e accounting)
+  long long h2d_bytes = 0, d2h_bytes = 0;
+  // sum over the prepared train set's layouts of the stage count (roofline accounting)
+  double sum_stages = 0;
 };
 
 namespace gp {

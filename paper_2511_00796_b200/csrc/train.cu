@@ -756,108 +756,188 @@ __global__ void k_extract_blkf(const BlockRec* __restrict__ blk, int nblk, doubl
   if (i < nblk) blkf[i] = make_double2(blk[i].flops, blk[i].lf_num);
 }
 
-int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_train_opts* o,
-                 long long lo, long long hi, gp_train_result* out, int32_t* stage_devices) {
-  std::memset(out, 0, sizeof *out);
+// A train set whose enumeration metadata is resident on the device
+// (gp_train_prepare); gp_train_launch builds the K2 tables and scans a range.
+struct PreparedTrain {
   HostSpace h;
-  int rc = build_space(ctx, ids, n, o, h);
-  if (rc) return rc;
-  if (lo < 0) lo = 0;
-  if (hi < 0 || hi > h.total) hi = h.total;
-  if (lo > hi) lo = hi;
-  out->layouts = hi - lo;
-  if (h.total == 0 || lo == hi) return GP_OK;  // std::nullopt
+  int* d_ordered = nullptr;
+  int* d_pos = nullptr;
+  int* d_run_start = nullptr;
+  BlockMeta* d_meta = nullptr;
+  int4* d_items = nullptr;
+  BlockRec* d_blk = nullptr;
+  double2* d_blkf = nullptr;
+  double2* d_stage = nullptr;
+  int8_t* d_opt = nullptr;
+  double* d_tin = nullptr;
+  double* d_tx = nullptr;
+  double* d_fd = nullptr;
+  Best* d_partial = nullptr;
+  TrainOut* d_out = nullptr;
+  int max_blocks = 0;
+  long long lo = 0, hi = 0;
+  bool launched = false;
+};
 
+static PreparedTrain*& prepared(gp_ctx* ctx) {
+  return reinterpret_cast<PreparedTrain*&>(ctx->train_state);
+}
+
+void train_state_free(gp_ctx* ctx) {
+  delete prepared(ctx);
+  prepared(ctx) = nullptr;
+}
+
+int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o) {
+  if (!prepared(ctx)) prepared(ctx) = new PreparedTrain();
+  PreparedTrain& P = *prepared(ctx);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer / scratch may be reused
+  P.launched = false;
+  P.h = HostSpace();
+  int rc = build_space(ctx, ids, n, o, P.h);
+  if (rc) return rc;
+  HostSpace& h = P.h;
   const int L = ctx->sc.L;
-  const int max_blocks = ctx->num_sms * 8;
-  // ---- device scratch layout
+  P.max_blocks = ctx->num_sms * 8;
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
-  add(sizeof(int) * n);                      // ordered
-  add(sizeof(int) * h.pos.size());           // pos
-  add(sizeof(int) * h.run_start.size());     // run_start
-  add(sizeof(BlockMeta) * h.meta.size());    // meta
-  add(sizeof(int4) * h.items.size());        // items
-  add(sizeof(BlockRec) * h.nblk);            // blk
-  add(sizeof(double2) * h.nblk);             // blkf
-  add(sizeof(double2) * (size_t)h.nblk * L); // stage
-  add(sizeof(int8_t) * (size_t)h.nblk * L);  // opt
+  add(sizeof(int) * n);
+  add(sizeof(int) * h.pos.size());
+  add(sizeof(int) * h.run_start.size());
+  add(sizeof(BlockMeta) * h.meta.size());
+  add(sizeof(int4) * h.items.size());
+  add(sizeof(BlockRec) * h.nblk);
+  add(sizeof(double2) * h.nblk);
+  add(sizeof(double2) * (size_t)h.nblk * L);
+  add(sizeof(int8_t) * (size_t)h.nblk * L);
   add(sizeof(double) * (h.tin_size + 1));
   add(sizeof(double) * (h.tx_size + 1));
-  add(sizeof(double) * (GP_MAX_STAGES + 1)); // fd_coef
-  add(sizeof(Best) * max_blocks);
+  add(sizeof(double) * (GP_MAX_STAGES + 1));
+  add(sizeof(Best) * P.max_blocks);
   add(sizeof(TrainOut));
   char* base = static_cast<char*>(ctx_scratch(ctx, bytes));
   if (!base) return GP_CUDA_ERROR;
   char* p = base;
-  int* d_ordered = carve<int>(p, n);
-  int* d_pos = carve<int>(p, h.pos.size());
-  int* d_run_start = carve<int>(p, h.run_start.size());
-  BlockMeta* d_meta = carve<BlockMeta>(p, h.meta.size());
-  int4* d_items = carve<int4>(p, h.items.size());
-  BlockRec* d_blk = carve<BlockRec>(p, h.nblk);
-  double2* d_blkf = carve<double2>(p, h.nblk);
-  double2* d_stage = carve<double2>(p, (size_t)h.nblk * L);
-  int8_t* d_opt = carve<int8_t>(p, (size_t)h.nblk * L);
-  double* d_tin = carve<double>(p, h.tin_size + 1);
-  double* d_tx = carve<double>(p, h.tx_size + 1);
-  double* d_fd = carve<double>(p, GP_MAX_STAGES + 1);
-  Best* d_partial = carve<Best>(p, max_blocks);
-  TrainOut* d_out = carve<TrainOut>(p, 1);
-  // ---- one pinned staging buffer -> one H2D copy of the enumeration metadata
-  const size_t in_bytes = (size_t)(d_items + h.items.size()) - (size_t)d_ordered;
+  P.d_ordered = carve<int>(p, n);
+  P.d_pos = carve<int>(p, h.pos.size());
+  P.d_run_start = carve<int>(p, h.run_start.size());
+  P.d_meta = carve<BlockMeta>(p, h.meta.size());
+  P.d_items = carve<int4>(p, h.items.size());
+  P.d_blk = carve<BlockRec>(p, h.nblk);
+  P.d_blkf = carve<double2>(p, h.nblk);
+  P.d_stage = carve<double2>(p, (size_t)h.nblk * L);
+  P.d_opt = carve<int8_t>(p, (size_t)h.nblk * L);
+  P.d_tin = carve<double>(p, h.tin_size + 1);
+  P.d_tx = carve<double>(p, h.tx_size + 1);
+  P.d_fd = carve<double>(p, GP_MAX_STAGES + 1);
+  P.d_partial = carve<Best>(p, P.max_blocks);
+  P.d_out = carve<TrainOut>(p, 1);
+  // one pinned staging buffer -> one H2D copy of the enumeration metadata
+  const size_t in_bytes = (size_t)(P.d_items + h.items.size()) - (size_t)P.d_ordered;
   char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(TrainOut))));
   if (!hp) return GP_CUDA_ERROR;
   auto stage_in = [&](const void* src, size_t sz, void* dptr) {
-    std::memcpy(hp + ((char*)dptr - (char*)d_ordered), src, sz);
+    if (sz) std::memcpy(hp + ((char*)dptr - (char*)P.d_ordered), src, sz);
   };
-  stage_in(h.ordered.data(), sizeof(int) * n, d_ordered);
-  stage_in(h.pos.data(), sizeof(int) * h.pos.size(), d_pos);
-  stage_in(h.run_start.data(), sizeof(int) * h.run_start.size(), d_run_start);
-  stage_in(h.meta.data(), sizeof(BlockMeta) * h.meta.size(), d_meta);
-  if (!h.items.empty()) stage_in(h.items.data(), sizeof(int4) * h.items.size(), d_items);
-  GP_CUDA(cudaMemcpyAsync(d_ordered, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  stage_in(h.ordered.data(), sizeof(int) * n, P.d_ordered);
+  stage_in(h.pos.data(), sizeof(int) * h.pos.size(), P.d_pos);
+  stage_in(h.run_start.data(), sizeof(int) * h.run_start.size(), P.d_run_start);
+  stage_in(h.meta.data(), sizeof(BlockMeta) * h.meta.size(), P.d_meta);
+  stage_in(h.items.data(), sizeof(int4) * h.items.size(), P.d_items);
+  GP_CUDA(cudaMemcpyAsync(P.d_ordered, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)in_bytes;
+  // sum over layouts of S (roofline accounting only): tot[r][u] = sum of stages of runs r..
+  {
+    double tot[GP_MAX_TYPES + 1][GP_MAX_STAGES + 1] = {};
+    const TrainSpace& sp = h.sp;
+    for (int r = sp.R - 1; r >= 0; --r)
+      for (int u = 0; u <= sp.max_stages; ++u) {
+        double acc = 0;
+        for (int k = 1; k <= sp.kmax[r]; ++k) {
+          if (u + k + (sp.R - 1 - r) > sp.max_stages) break;
+          const double c = (double)binom_small(sp.nc[r], k - 1);
+          acc += c * ((double)k * (double)sp.cnt[r + 1][u + k] + tot[r + 1][u + k]);
+        }
+        tot[r][u] = acc;
+      }
+    ctx->sum_stages = h.total ? tot[0][0] : 0;
+  }
+  return GP_OK;
+}
 
+int train_launch(gp_ctx* ctx, int window, long long lo, long long hi) {
+  PreparedTrain* PP = prepared(ctx);
+  if (!PP) return set_error(GP_INVALID, "gp_train_launch without gp_train_prepare");
+  PreparedTrain& P = *PP;
+  const HostSpace& h = P.h;
+  if (lo < 0) lo = 0;
+  if (hi < 0 || hi > h.total) hi = h.total;
+  if (lo > hi) lo = hi;
+  P.lo = lo;
+  P.hi = hi;
+  P.launched = true;
+  if (h.total == 0 || lo == hi) return GP_OK;  // std::nullopt
+  const int L = ctx->sc.L;
   TrainTables tb{};
-  tb.ordered = d_ordered;
-  tb.pos = d_pos;
-  tb.blk = d_blk;
-  tb.stage = d_stage;
-  tb.opt = d_opt;
-  tb.tin = d_tin;
-  tb.tx = d_tx;
-  tb.fd_coef = d_fd;
+  tb.ordered = P.d_ordered;
+  tb.pos = P.d_pos;
+  tb.blk = P.d_blk;
+  tb.stage = P.d_stage;
+  tb.opt = P.d_opt;
+  tb.tin = P.d_tin;
+  tb.tx = P.d_tx;
+  tb.fd_coef = P.d_fd;
   for (int r = 0; r < h.sp.R; ++r) tb.pos_off[r] = h.pos_off[r];
-
-  k2a_block_stats<<<h.nblk, 256, 0, ctx->stream>>>(d_ordered, d_meta, d_pos, tb, d_blk, ctx->d_type,
-                                                   ctx->d_machine, ctx->d_flops, ctx->d_hbm_cap,
-                                                   ctx->d_links, ctx->N, L, ctx->sc.mb, d_fd);
+  if (ctx->timing) GP_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  // ---- K2: per-train-set tables
+  k2a_block_stats<<<h.nblk, 256, 0, ctx->stream>>>(P.d_ordered, P.d_meta, P.d_pos, tb, P.d_blk,
+                                                   ctx->d_type, ctx->d_machine, ctx->d_flops,
+                                                   ctx->d_hbm_cap, ctx->d_links, ctx->N, L,
+                                                   ctx->sc.mb, P.d_fd);
   ctx->launches++;
   if (!h.items.empty()) {
     const int warps_per_block = 8;
     const int grid = (int)((h.items.size() + warps_per_block - 1) / warps_per_block);
     k2b_transfers<<<grid, 32 * warps_per_block, 0, ctx->stream>>>(
-        d_ordered, d_items, (int)h.items.size(), d_pos, tb, h.sp, d_run_start, ctx->d_links, ctx->N,
-        ctx->sc.tokens > 0 ? ctx->sc.act_tok_h2 : 0.0, d_tin, d_tx);
+        P.d_ordered, P.d_items, (int)h.items.size(), P.d_pos, tb, h.sp, P.d_run_start, ctx->d_links,
+        ctx->N, ctx->sc.tokens > 0 ? ctx->sc.act_tok_h2 : 0.0, P.d_tin, P.d_tx);
     ctx->launches++;
   }
   {
     const long long cnt = (long long)h.nblk * L;
-    k2c_stage_table<<<(int)((cnt + 255) / 256), 256, 0, ctx->stream>>>(d_blk, h.nblk, ctx->sc,
-                                                                      ctx->d_ceff, d_stage, d_opt);
-    k_extract_blkf<<<(h.nblk + 255) / 256, 256, 0, ctx->stream>>>(d_blk, h.nblk, d_blkf);
+    k2c_stage_table<<<(int)((cnt + 255) / 256), 256, 0, ctx->stream>>>(P.d_blk, h.nblk, ctx->sc,
+                                                                      ctx->d_ceff, P.d_stage, P.d_opt);
+    k_extract_blkf<<<(h.nblk + 255) / 256, 256, 0, ctx->stream>>>(P.d_blk, h.nblk, P.d_blkf);
     ctx->launches += 2;
   }
   GP_CUDA(cudaGetLastError());
+  if (ctx->timing) GP_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  // ---- K1: layout scan over [lo, hi)
   const int R = h.sp.R;
-  if (R == 1) rc = launch_scan<1>(ctx, h, tb, d_blkf, d_blk, window, lo, hi, d_partial, max_blocks, d_out);
-  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, d_blkf, d_blk, window, lo, hi, d_partial, max_blocks, d_out);
-  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, d_blkf, d_blk, window, lo, hi, d_partial, max_blocks, d_out);
-  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, d_blkf, d_blk, window, lo, hi, d_partial, max_blocks, d_out);
-  else rc = launch_scan<8>(ctx, h, tb, d_blkf, d_blk, window, lo, hi, d_partial, max_blocks, d_out);
-  if (rc) return rc;
-  TrainOut* ho = reinterpret_cast<TrainOut*>(hp);
-  GP_CUDA(cudaMemcpyAsync(ho, d_out, sizeof(TrainOut), cudaMemcpyDeviceToHost, ctx->stream));
+  int rc;
+  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
+  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
+  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
+  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
+  else rc = launch_scan<8>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
+  if (!rc && ctx->timing) GP_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+  return rc;
+}
+
+int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices) {
+  std::memset(out, 0, sizeof *out);
+  PreparedTrain* PP = prepared(ctx);
+  if (!PP || !PP->launched) return set_error(GP_INVALID, "gp_train_collect without gp_train_launch");
+  PreparedTrain& P = *PP;
+  const HostSpace& h = P.h;
+  out->layouts = P.hi - P.lo;
+  if (h.total == 0 || P.lo == P.hi) {
+    GP_CUDA(cudaStreamSynchronize(ctx->stream));
+    return GP_OK;
+  }
+  TrainOut* ho = reinterpret_cast<TrainOut*>(ctx_pinned(ctx, sizeof(TrainOut)));
+  GP_CUDA(cudaMemcpyAsync(ho, P.d_out, sizeof(TrainOut), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += (long long)sizeof(TrainOut);
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
   out->feasible = ho->best.feasible;
   if (ho->best.rank != LLONG_MAX) {
@@ -872,9 +952,18 @@ int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_tr
       out->stage[s].dp = ho->dp[s];
       out->stage[s].layers = ho->layers[s];
     }
-    if (stage_devices) std::memcpy(stage_devices, h.ordered.data(), sizeof(int32_t) * n);
+    if (stage_devices) std::memcpy(stage_devices, h.ordered.data(), sizeof(int32_t) * h.sp.n);
   }
   return GP_OK;
+}
+
+int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_train_opts* o,
+                 long long lo, long long hi, gp_train_result* out, int32_t* stage_devices) {
+  std::memset(out, 0, sizeof *out);
+  int rc = train_prepare(ctx, ids, n, o);
+  if (!rc) rc = train_launch(ctx, window, lo, hi);
+  if (!rc) rc = train_collect(ctx, out, stage_devices);
+  return rc;
 }
 
 }  // namespace gp

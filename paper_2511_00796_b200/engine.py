@@ -53,6 +53,18 @@ def lib() -> C.CDLL:
         _lib.gp_ctx_destroy.argtypes = [C.c_void_p]
         _lib.gp_ctx_launches.argtypes = [C.c_void_p]
         _lib.gp_ctx_launches.restype = C.c_longlong
+        vp = C.c_void_p
+        _lib.gp_ctx_stream.argtypes = [vp]
+        _lib.gp_ctx_stream.restype = vp
+        _lib.gp_train_prepare.argtypes = [vp, abi.i32p, C.c_int32, C.POINTER(abi.gp_train_opts)]
+        _lib.gp_train_launch.argtypes = [vp, C.c_int32, C.c_int64, C.c_int64]
+        _lib.gp_train_collect.argtypes = [vp, C.POINTER(abi.gp_train_result), abi.i32p]
+        _lib.gp_ctx_set_timing.argtypes = [vp, C.c_int]
+        _lib.gp_train_timing.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]
+        _lib.gp_ctx_io_bytes.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                                         C.POINTER(C.c_double)]
+        _lib.gp_ctx_io_bytes.restype = None
+        _lib.gp_fp64_peak.argtypes = [vp, C.POINTER(C.c_double)]
     return _lib
 
 
@@ -154,3 +166,40 @@ class Engine:
             st = res.stage[s]
             stages.append(Stage(devs[st.first:st.first + st.count].tolist(), st.tp, st.dp, st.layers))
         return TrainSearchResult(stages, res.cost, res.rank, res.layouts, res.feasible)
+
+    # ---- split form + measurement hooks (bench.py) -------------------------
+    @property
+    def stream_ptr(self) -> int:
+        return int(lib().gp_ctx_stream(self._h))
+
+    def train_prepare(self, train_set, opts=None):
+        self._prep_ids = _ids(train_set)
+        _check(lib().gp_train_prepare(self._h, self._prep_ids.ctypes.data_as(abi.i32p),
+                                      len(self._prep_ids), C.byref(opts or abi.default_train_opts())))
+
+    def train_launch(self, window: int, lo: int = 0, hi: int = -1):
+        _check(lib().gp_train_launch(self._h, window, lo, hi))
+
+    def train_collect(self):
+        res = abi.gp_train_result()
+        devs = np.zeros(max(len(self._prep_ids), 1), dtype=np.int32)
+        _check(lib().gp_train_collect(self._h, C.byref(res), devs.ctypes.data_as(abi.i32p)))
+        return res, devs
+
+    def set_timing(self, on: bool = True):
+        _check(lib().gp_ctx_set_timing(self._h, int(on)))
+
+    def train_timing(self):
+        k2, k1 = C.c_float(), C.c_float()
+        _check(lib().gp_train_timing(self._h, C.byref(k2), C.byref(k1)))
+        return k2.value, k1.value
+
+    def io_bytes(self):
+        h2d, d2h, ss = C.c_longlong(), C.c_longlong(), C.c_double()
+        lib().gp_ctx_io_bytes(self._h, C.byref(h2d), C.byref(d2h), C.byref(ss))
+        return h2d.value, d2h.value, ss.value
+
+    def fp64_peak(self) -> float:
+        v = C.c_double()
+        _check(lib().gp_fp64_peak(self._h, C.byref(v)))
+        return v.value
