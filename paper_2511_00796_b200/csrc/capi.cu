@@ -1,6 +1,11 @@
 // capi.cu — extern "C" entry points of libgplan.so (include/gplan.h) and the
 // engine context: validation, device upload, scratch management, error state.
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
+
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -46,7 +51,6 @@ void* ctx_scratch(gp_ctx* ctx, size_t bytes) {
 void* ctx_pinned(gp_ctx* ctx, size_t bytes) {
   if (bytes > ctx->h_pinned_bytes) {
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
-  train_state_free(ctx);
     ctx->h_pinned = nullptr;
     size_t want = bytes + bytes / 4 + 4096;
     cudaError_t e = cudaMallocHost(&ctx->h_pinned, want);
@@ -61,6 +65,17 @@ void* ctx_pinned(gp_ctx* ctx, size_t bytes) {
 }
 
 __global__ void k_probe(int* flag) { *flag = 0x5eed; }
+
+// GP_SEGV_TRACE=1: print a native backtrace on SIGSEGV (debug aid on GPU boxes without gdb).
+static void segv_handler(int sig) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  const char msg[] = "libgplan: fatal signal, native backtrace:\n";
+  (void)!write(2, msg, sizeof msg - 1);
+  backtrace_symbols_fd(frames, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
 
 // Every device of a type carries the same capabilities in the reference loader
 // (src/cluster.cpp:127-137); the engine's rollout side relies on it.
@@ -100,6 +115,7 @@ const char* gp_last_error(void) { return g_error.c_str(); }
 int gp_ctx_create(const gp_cluster* c, const gp_workload* w, const gp_calib* k, int device,
                   gp_ctx** out) {
   *out = nullptr;
+  if (std::getenv("GP_SEGV_TRACE")) signal(SIGSEGV, segv_handler);
   int rc = validate(c, w, k);
   if (rc) return rc;
   int ndev = 0;

@@ -59,6 +59,17 @@ struct TrainSpace {
   int tin_off[GP_MAX_TYPES];   // offset of run r's (nc+2)^3 within-run transfer cube
   int tx_off[GP_MAX_TYPES];    // offset of the (r, r+1) cross-run transfer matrix
   int64_t cnt[GP_MAX_TYPES + 1][GP_MAX_STAGES + 1];  // completions of runs r.. with u used
+  int64_t cntP[GP_MAX_TYPES + 1][GP_MAX_STAGES + 1]; // same over the prefix runs 0..R-2 only
+  int n_suf;             // suffix table size (all (k, cuts) choices of the last run)
+};
+
+// One choice of the last type run (the "suffix" of a layout), in enumeration order:
+// its block ids, its internal stage-transfer terms and the end of its first block.
+struct SufEnt {
+  int bi[4];
+  double t[3];
+  int k;
+  int b1;
 };
 
 // Device-side training tables of one train set.
@@ -71,6 +82,7 @@ struct TrainTables {
   const double* tin;
   const double* tx;
   const double* fd_coef; // [S] = (double)(S-1) / micro_batches
+  const SufEnt* suf;     // [n_suf]
   int pos_off[GP_MAX_TYPES];
 };
 

@@ -253,152 +253,249 @@ __global__ void __launch_bounds__(256) k2c_stage_table(const BlockRec* __restric
   opt[idx] = (int8_t)best_o;
 }
 
+
+// --------------------------------------------------------- K2d suffix table
+// One entry per choice (k, cuts) of the LAST type run, in run_compositions order
+// (src/train_search.cpp:53-72, k ascending): block ids, internal transfers.
+__global__ void k2d_suffix_table(const int4* __restrict__ choices, int n, TrainSpace sp,
+                                 const double* __restrict__ tin, SufEnt* __restrict__ suf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int r = sp.R - 1, nc = sp.nc[r], e = nc + 2;
+  const int4 c = choices[i];  // (k, b1, b2, b3) position-index boundaries
+  const int k = c.x;
+  int b[5] = {0, c.y, c.z, c.w, 0};
+  b[k] = nc + 1;
+  SufEnt out;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) out.bi[j] = j < k ? sp.blk_off[r] + blk_index(nc, b[j], b[j + 1]) : 0;
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    out.t[j] = j + 1 < k ? tin[sp.tin_off[r] + ((size_t)b[j] * e + b[j + 1]) * e + b[j + 2]] : 0.0;
+  out.k = k;
+  out.b1 = b[1];
+  suf[i] = out;
+}
+
 // ------------------------------------------------------------- K1 layout scan
-template <int MAXR>
-struct Layout {
-  int k[MAXR];
-  int used[MAXR];
-  int b[MAXR][kMaxPerRun + 1];  // position-index boundaries; b[r][0] = 0, b[r][k] = nc+1
+// Rank space = concatenation over prefixes p (choices of runs 0..R-2, in
+// enumeration order) of the suffix choices s < ns(u_p) of the last run. A warp
+// owns a range of prefixes; its lanes stride over the suffixes of each prefix.
+// The prefix's stage data are warp-uniform; per lane only the suffix differs.
+template <int R>
+struct Prefix {
+  int k[R > 1 ? R - 1 : 1];
+  int b[R > 1 ? R - 1 : 1][kMaxPerRun + 1];
+  int u;
 };
 
-// Unrank `x` in the enumeration order of Enumerator::recurse (src/train_search.cpp:95-124)
-// with run_compositions' lexicographic cut order (src/train_search.cpp:53-72).
-template <int MAXR>
-__device__ __forceinline__ void unrank(const TrainSpace& sp, long long x, Layout<MAXR>& L) {
+// Decode prefix index x over runs 0..R-2 (Enumerator::recurse order). Returns the
+// full-space rank of the prefix's first layout (its base).
+template <int R>
+__host__ __device__ __forceinline__ long long prefix_decode(const TrainSpace& sp, long long x,
+                                                            Prefix<R>& P) {
   int u = 0;
+  long long base = 0;
 #pragma unroll
-  for (int r = 0; r < MAXR; ++r) {
-    if (r >= sp.R) break;
-    L.used[r] = u;
+  for (int r = 0; r + 1 < R; ++r) {
     const int nc = sp.nc[r];
-    const int rem_runs = sp.R - 1 - r;
-#pragma unroll 1
+    const int rem_runs = R - 1 - r;
     for (int k = 1; k <= sp.kmax[r]; ++k) {
       if (u + k + rem_runs > sp.max_stages) break;
+      const long long c = binom_small(nc, k - 1);
+      const long long subP = sp.cntP[r + 1][u + k];
       const long long sub = sp.cnt[r + 1][u + k];
-      const long long size = binom_small(nc, k - 1) * sub;
-      if (x < size) {
-        long long q = x / sub;
-        x -= q * sub;
-        L.k[r] = k;
+      if (x < c * subP) {
+        long long q = x / subP;
+        x -= q * subP;
+        base += q * sub;
+        P.k[r] = k;
         const int m = k - 1;
         int v = 0;
 #pragma unroll
         for (int j = 1; j < kMaxPerRun; ++j) {
           if (j <= m) {
-#pragma unroll 1
             while (true) {
-              const long long c = binom_small(nc - v - 1, m - j);
-              if (q < c) break;
-              q -= c;
+              const long long cc = binom_small(nc - v - 1, m - j);
+              if (q < cc) break;
+              q -= cc;
               ++v;
             }
-            L.b[r][j] = v + 1;
+            P.b[r][j] = v + 1;
             ++v;
           }
         }
 #pragma unroll
         for (int j = 1; j <= kMaxPerRun; ++j)
-          if (j == k) L.b[r][j] = nc + 1;
+          if (j == k) P.b[r][j] = nc + 1;
+        P.b[r][0] = 0;
         u += k;
         break;
       }
-      x -= size;
+      x -= c * subP;
+      base += c * sub;
     }
-    L.b[r][0] = 0;
   }
+  P.u = u;
+  return base;
 }
 
-// Next layout in enumeration order (odometer over runs, last run fastest).
-template <int MAXR>
-__device__ __forceinline__ void advance(const TrainSpace& sp, Layout<MAXR>& L) {
+// Next prefix in enumeration order (odometer over runs 0..R-2).
+template <int R>
+__device__ __forceinline__ void prefix_advance(const TrainSpace& sp, Prefix<R>& P) {
   bool carry = true;
+  int used[R > 1 ? R - 1 : 1];
+  int acc = 0;
 #pragma unroll
-  for (int rr = MAXR - 1; rr >= 0; --rr) {
-    if (carry && rr < sp.R) {
+  for (int r = 0; r + 1 < R; ++r) {
+    used[r] = acc;
+    acc += P.k[r];
+  }
+#pragma unroll
+  for (int rr = R - 2; rr >= 0; --rr) {
+    if (carry) {
       const int nc = sp.nc[rr];
-      const int m = L.k[rr] - 1;
+      const int m = P.k[rr] - 1;
       int jf = 0;
 #pragma unroll
       for (int j = kMaxPerRun - 1; j >= 1; --j)
-        if (jf == 0 && j <= m && L.b[rr][j] < nc - (m - j)) jf = j;
+        if (jf == 0 && j <= m && P.b[rr][j] < nc - (m - j)) jf = j;
       bool ok = false;
       if (jf) {
 #pragma unroll
         for (int j = 1; j < kMaxPerRun; ++j) {
-          if (j == jf) L.b[rr][j] += 1;
-          else if (j > jf && j <= m) L.b[rr][j] = L.b[rr][j - 1] + 1;
+          if (j == jf) P.b[rr][j] += 1;
+          else if (j > jf && j <= m) P.b[rr][j] = P.b[rr][j - 1] + 1;
         }
         ok = true;
-      } else if (L.k[rr] < sp.kmax[rr] && L.used[rr] + L.k[rr] + 1 + (sp.R - 1 - rr) <= sp.max_stages &&
-                 nc >= L.k[rr]) {
-        const int k = ++L.k[rr];
+      } else if (P.k[rr] < sp.kmax[rr] && used[rr] + P.k[rr] + 1 + (R - 1 - rr) <= sp.max_stages &&
+                 nc >= P.k[rr]) {
+        const int k = ++P.k[rr];
 #pragma unroll
         for (int j = 1; j <= kMaxPerRun; ++j) {
-          if (j < k) L.b[rr][j] = j;
-          else if (j == k) L.b[rr][j] = nc + 1;
+          if (j < k) P.b[rr][j] = j;
+          else if (j == k) P.b[rr][j] = nc + 1;
         }
         ok = true;
       }
       if (ok) {
         carry = false;
 #pragma unroll
-        for (int r2 = rr + 1; r2 < MAXR; ++r2) {
-          if (r2 < sp.R) {
-            L.used[r2] = L.used[r2 - 1] + L.k[r2 - 1];
-            L.k[r2] = 1;
-            L.b[r2][1] = sp.nc[r2] + 1;
-          }
+        for (int r2 = rr + 1; r2 + 1 < R; ++r2) {
+          P.k[r2] = 1;
+          P.b[r2][1] = sp.nc[r2] + 1;
+        }
+      }
+    }
+  }
+  int u = 0;
+#pragma unroll
+  for (int r = 0; r + 1 < R; ++r) u += P.k[r];
+  P.u = u;
+}
+
+// Warp-uniform data of one prefix.
+template <int R>
+struct PrefixData {
+  static constexpr int NP = (R - 1) * kMaxPerRun;
+  int bi[NP > 0 ? NP : 1];
+  double lfn[NP > 0 ? NP : 1];
+  bool act[NP > 0 ? NP : 1];
+  double total;      // left fold of the prefix stages' FLOPS (allocate_layers total, first part)
+  double transfers;  // left fold of the prefix-internal stage transfers
+  int a_last;        // start position of the prefix's last block (junction transfer)
+  int u;             // prefix stage count
+};
+
+template <int R>
+__device__ __forceinline__ void prefix_data(const TrainSpace& sp, const TrainTables& tb,
+                                            const double2* __restrict__ blkf, const Prefix<R>& P,
+                                            PrefixData<R>& D) {
+  D.total = 0.0;
+  D.transfers = 0.0;
+  D.a_last = 0;
+  D.u = P.u;
+#pragma unroll
+  for (int r = 0; r + 1 < R; ++r) {
+#pragma unroll
+    for (int j = 0; j < kMaxPerRun; ++j) {
+      const int q = r * kMaxPerRun + j;
+      D.act[q] = j < P.k[r];
+      D.bi[q] = 0;
+      D.lfn[q] = 0;
+      if (D.act[q]) {
+        D.bi[q] = sp.blk_off[r] + blk_index(sp.nc[r], P.b[r][j], P.b[r][j + 1]);
+        const double2 fl = blkf[D.bi[q]];
+        D.total += fl.x;
+        D.lfn[q] = fl.y;
+        if (j + 1 < P.k[r]) {
+          const int e = sp.nc[r] + 2;
+          D.transfers += tb.tin[sp.tin_off[r] + ((size_t)P.b[r][j] * e + P.b[r][j + 1]) * e +
+                                P.b[r][j + 2 <= kMaxPerRun ? j + 2 : kMaxPerRun]];
+        } else if (r + 2 < R) {
+          const int e2 = sp.nc[r + 1] + 2;
+          D.transfers += tb.tx[sp.tx_off[r] + (size_t)P.b[r][j] * e2 + P.b[r + 2 < R ? r + 1 : r][1]];
+        } else {
+          D.a_last = P.b[r][j];
         }
       }
     }
   }
 }
 
-// Scores one layout. Returns false when some stage has no memory-feasible option.
-// Also returns the per-slot layer counts / block ids when `out_layers` is set (decode).
-template <int MAXR>
-__device__ __forceinline__ bool score(const TrainSpace& sp, const TrainTables& tb,
-                                      const double2* __restrict__ blkf, int L, int window,
-                                      const Layout<MAXR>& Y, double& cost, int* out_layers,
-                                      int* out_bi) {
-  constexpr int NS = MAXR * kMaxPerRun;
+// a / b correctly rounded, given y = RN(1/b): Markstein's theorem (q within one ulp,
+// y within half an ulp -> one FMA residual correction yields RN(a/b)); operands are
+// positive normals far from the exponent limits. Pinned by tests/test_engine_train.py.
+__device__ __forceinline__ double div_rn_recip(double a, double b, double y) {
+  const double q = __dmul_rn(a, y);
+  const double r = __fma_rn(-q, b, a);
+  return __fma_rn(r, y, q);
+}
+
+// Score (prefix, suffix). Returns false when some stage has no memory-feasible option.
+template <int R, bool DECODE>
+__device__ __forceinline__ bool eval_layout(const TrainSpace& sp, const TrainTables& tb,
+                                            const double2* __restrict__ blkf, int L, int window,
+                                            const PrefixData<R>& D, const SufEnt& e, double& cost,
+                                            int* out_lay, int* out_bi) {
+  constexpr int NP = (R - 1) * kMaxPerRun;
+  constexpr int NS = NP + kMaxPerRun;
   int bi[NS];
   double lfn[NS];
-  int lay[NS];
-  long long remb[NS];
   bool act[NS];
-  double total = 0.0;
-  int S = 0;
-  // stage flops + allocate_layers total (src/train_search.cpp:146-152)
+  int lay[NS];
+  long long key[NS];
+  double total = D.total;
 #pragma unroll
-  for (int r = 0; r < MAXR; ++r) {
+  for (int q = 0; q < NP; ++q) {
+    bi[q] = D.bi[q];
+    lfn[q] = D.lfn[q];
+    act[q] = D.act[q];
+  }
+  const int k = e.k;
 #pragma unroll
-    for (int j = 0; j < kMaxPerRun; ++j) {
-      const int q = r * kMaxPerRun + j;
-      act[q] = (r < sp.R) && (j < Y.k[r]);
-      if (act[q]) {
-        bi[q] = sp.blk_off[r] + blk_index(sp.nc[r], Y.b[r][j], Y.b[r][j + 1]);
-        const double2 fl = blkf[bi[q]];
-        total += fl.x;
-        lfn[q] = fl.y;
-        ++S;
-      }
+  for (int j = 0; j < kMaxPerRun; ++j) {
+    const int q = NP + j;
+    act[q] = j < k;
+    bi[q] = e.bi[j];
+    lfn[q] = 0;
+    if (act[q]) {
+      const double2 fl = blkf[bi[q]];
+      total += fl.x;  // allocate_layers total: left fold in stage order
+      lfn[q] = fl.y;
     }
   }
+  const int S = D.u + k;
+  const double y = 1.0 / total;
   int assigned = 0;
 #pragma unroll
   for (int q = 0; q < NS; ++q) {
-    if (act[q]) {
-      const double share = lfn[q] / total;
-      lay[q] = static_cast<int>(share);
-      assigned += lay[q];
-      remb[q] = __double_as_longlong(share - lay[q]);  // >= +0: integer order == fp order
-    }
+    const double share = div_rn_recip(lfn[q], total, y);  // num_layers * f / total
+    lay[q] = static_cast<int>(share);
+    key[q] = act[q] ? __double_as_longlong(share - lay[q]) : -1LL;  // rem >= +0
+    assigned += act[q] ? lay[q] : 0;
   }
-  // stable_sort by remainder desc -> position; extra layers round-robin over positions
-  const int extra = L - assigned;
-  const int ex_div = extra / S, ex_mod = extra % S;
+  // std::stable_sort of remainders (desc) -> position; extra layers round-robin
   int pos[NS];
 #pragma unroll
   for (int q = 0; q < NS; ++q) pos[q] = 0;
@@ -406,19 +503,20 @@ __device__ __forceinline__ bool score(const TrainSpace& sp, const TrainTables& t
   for (int q = 0; q < NS; ++q) {
 #pragma unroll
     for (int q2 = q + 1; q2 < NS; ++q2) {
-      if (act[q] && act[q2]) {
-        if (remb[q] >= remb[q2]) pos[q2]++;
-        else pos[q]++;
-      }
+      if (key[q] >= key[q2]) pos[q2]++;
+      else pos[q]++;
     }
+  }
+  int extra = L - assigned, ex_div = 0, ex_mod = extra;
+  if (extra < 0 || extra >= S) {
+    ex_div = extra / S;
+    ex_mod = extra % S;
   }
   bool zero = false;
 #pragma unroll
   for (int q = 0; q < NS; ++q) {
-    if (act[q]) {
-      lay[q] += ex_div + (pos[q] < ex_mod ? 1 : 0);
-      zero |= lay[q] == 0;
-    }
+    lay[q] += ex_div + (pos[q] < ex_mod ? 1 : 0);
+    zero |= act[q] && lay[q] == 0;
   }
   if (zero) {  // every stage needs at least one layer (src/train_search.cpp:217-225)
 #pragma unroll
@@ -444,86 +542,93 @@ __device__ __forceinline__ bool score(const TrainSpace& sp, const TrainTables& t
 #pragma unroll
   for (int q = 0; q < NS; ++q) {
     if (act[q]) {
-      const double2 e = tb.stage[(size_t)bi[q] * L + (lay[q] - 1)];
-      feasible &= e.x >= 0;
-      max_total = max_total < e.x ? e.x : max_total;
-      max_comp = max_comp < e.y ? e.y : max_comp;
+      const double2 st = tb.stage[(size_t)bi[q] * L + (lay[q] - 1)];
+      feasible &= st.x >= 0;
+      max_total = max_total < st.x ? st.x : max_total;
+      max_comp = max_comp < st.y ? st.y : max_comp;
     }
   }
-  if (out_layers) {
+  if (DECODE) {
 #pragma unroll
     for (int q = 0; q < NS; ++q) {
-      out_layers[q] = act[q] ? lay[q] : 0;
+      out_lay[q] = act[q] ? lay[q] : 0;
       out_bi[q] = act[q] ? bi[q] : -1;
     }
   }
   if (!feasible) return false;
-  double fill = 0, transfers = 0;
-  if (S > 1) {
-    fill = tb.fd_coef[S] * max_comp;
-#pragma unroll
-    for (int r = 0; r < MAXR; ++r) {
-#pragma unroll
-      for (int j = 0; j < kMaxPerRun; ++j) {
-        if (r < sp.R && j < Y.k[r]) {
-          if (j + 1 < Y.k[r]) {
-            const int e = sp.nc[r] + 2;
-            transfers += tb.tin[sp.tin_off[r] + ((size_t)Y.b[r][j] * e + Y.b[r][j + 1]) * e +
-                                Y.b[r][j + 2 <= kMaxPerRun ? j + 2 : kMaxPerRun]];
-          } else if (r + 1 < MAXR && r + 1 < sp.R) {
-            const int e2 = sp.nc[r + 1 < MAXR ? r + 1 : r] + 2;
-            transfers += tb.tx[sp.tx_off[r] + (size_t)Y.b[r][j] * e2 + Y.b[r + 1 < MAXR ? r + 1 : r][1]];
-          }
-        }
-      }
-    }
+  // stage transfers in stage order: prefix-internal, junction, suffix-internal
+  double transfers = D.transfers;
+  if (R > 1) {
+    const int e2 = sp.nc[R - 1] + 2;
+    transfers += tb.tx[sp.tx_off[R > 1 ? R - 2 : 0] + (size_t)D.a_last * e2 + e.b1];
   }
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    if (j + 1 < k) transfers += e.t[j];
+  const double fill = tb.fd_coef[S] * max_comp;
   const double per_step = max_total + fill + transfers;
   cost = window * per_step;
   return true;
 }
 
-template <int MAXR>
+
+struct ScanRange {
+  long long p_lo, s_lo, p_hi, s_hi;  // candidates (p, s) with (p_lo,s_lo) <= (p,s) < (p_hi,s_hi)
+  long long n_pref;                  // prefixes touched
+  long long chunk;                   // prefixes per warp work item
+};
+
+template <int R>
 __global__ void __launch_bounds__(256) k1_layout_scan(TrainSpace sp, TrainTables tb,
                                                       const double2* __restrict__ blkf, int L,
-                                                      int window, long long lo, long long hi,
-                                                      long long chunk, Best* __restrict__ partial) {
+                                                      int window, ScanRange rg,
+                                                      Best* __restrict__ partial) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
+  const long long n_suf = sp.n_suf;
   double best_cost = kInf * 10;
-  long long best_rank = LLONG_MAX;
+  long long best_key = LLONG_MAX;
   long long feasible = 0;
-  const long long n_chunks = (hi - lo + chunk - 1) / chunk;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long ci = (long long)blockIdx.x * blockDim.x + threadIdx.x; ci < n_chunks; ci += stride) {
-    const long long r0 = lo + ci * chunk;
-    const long long r1 = r0 + chunk < hi ? r0 + chunk : hi;
-    Layout<MAXR> Y;
-    unrank<MAXR>(sp, r0, Y);
-    for (long long rank = r0; rank < r1; ++rank) {
-      double cost;
-      if (score<MAXR>(sp, tb, blkf, L, window, Y, cost, nullptr, nullptr)) {
-        ++feasible;
-        if (cost < best_cost) {  // strict <: first rank wins among equal costs
-          best_cost = cost;
-          best_rank = rank;
+  for (long long it = warp; it < n_items; it += n_warps) {
+    long long p = rg.p_lo + it * rg.chunk;
+    const long long p_end = min(p + rg.chunk, rg.p_lo + rg.n_pref);
+    Prefix<R> P;
+    prefix_decode<R>(sp, p, P);
+    for (; p < p_end; ++p) {
+      PrefixData<R> D;
+      prefix_data<R>(sp, tb, blkf, P, D);
+      const long long ns = sp.cnt[R - 1][P.u];
+      const long long s0 = p == rg.p_lo ? rg.s_lo : 0;
+      const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
+      for (long long s = s0 + lane; s < s1; s += 32) {
+        const SufEnt e = tb.suf[s];
+        double cost;
+        if (eval_layout<R, false>(sp, tb, blkf, L, window, D, e, cost, nullptr, nullptr)) {
+          ++feasible;
+          if (cost < best_cost) {  // strict <: first in enumeration order wins ties
+            best_cost = cost;
+            best_key = p * n_suf + s;
+          }
         }
       }
-      if (rank + 1 < r1) advance<MAXR>(sp, Y);
+      if (p + 1 < p_end) prefix_advance<R>(sp, P);
     }
   }
-  // warp -> CTA reduction of (cost, rank) lexicographic min and feasible count
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const double c2 = __shfl_xor_sync(0xffffffffu, best_cost, o);
-    const long long r2 = __shfl_xor_sync(0xffffffffu, best_rank, o);
+    const long long k2 = __shfl_xor_sync(0xffffffffu, best_key, o);
     feasible += __shfl_xor_sync(0xffffffffu, feasible, o);
-    if (better(c2, r2, best_cost, best_rank)) {
+    if (better(c2, k2, best_cost, best_key)) {
       best_cost = c2;
-      best_rank = r2;
+      best_key = k2;
     }
   }
   __shared__ Best sb[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) sb[wid] = Best{best_cost, best_rank, feasible};
+  const int wid = threadIdx.x >> 5;
+  if (lane == 0) sb[wid] = Best{best_cost, best_key, feasible};
   __syncthreads();
   if (wid == 0) {
     const int nw = blockDim.x >> 5;
@@ -531,19 +636,19 @@ __global__ void __launch_bounds__(256) k1_layout_scan(TrainSpace sp, TrainTables
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double c2 = __shfl_xor_sync(0xffffffffu, b.cost, o);
-      const long long r2 = __shfl_xor_sync(0xffffffffu, b.rank, o);
+      const long long k2 = __shfl_xor_sync(0xffffffffu, b.rank, o);
       b.feasible += __shfl_xor_sync(0xffffffffu, b.feasible, o);
-      if (better(c2, r2, b.cost, b.rank)) {
+      if (better(c2, k2, b.cost, b.rank)) {
         b.cost = c2;
-        b.rank = r2;
+        b.rank = k2;
       }
     }
     if (lane == 0) partial[blockIdx.x] = b;
   }
 }
 
-// Reduce CTA partials and decode the winner's plan.
-template <int MAXR>
+// Reduce CTA partials and decode the winner (prefix, suffix) -> rank + plan.
+template <int R>
 __global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb,
                                                    const double2* __restrict__ blkf,
                                                    const BlockRec* __restrict__ blk, int L,
@@ -561,11 +666,11 @@ __global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const double c2 = __shfl_xor_sync(0xffffffffu, b.cost, o);
-    const long long r2 = __shfl_xor_sync(0xffffffffu, b.rank, o);
+    const long long k2 = __shfl_xor_sync(0xffffffffu, b.rank, o);
     b.feasible += __shfl_xor_sync(0xffffffffu, b.feasible, o);
-    if (better(c2, r2, b.cost, b.rank)) {
+    if (better(c2, k2, b.cost, b.rank)) {
       b.cost = c2;
-      b.rank = r2;
+      b.rank = k2;
     }
   }
   __shared__ Best sb[32];
@@ -584,26 +689,30 @@ __global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb
   out->best = b;
   out->n_stages = 0;
   if (b.rank == LLONG_MAX) return;
-  Layout<MAXR> Y;
-  unrank<MAXR>(sp, b.rank, Y);
-  constexpr int NS = MAXR * kMaxPerRun;
+  const long long p = b.rank / sp.n_suf, s = b.rank % sp.n_suf;
+  Prefix<R> P;
+  const long long base = prefix_decode<R>(sp, p, P);
+  out->best.rank = base + s;
+  PrefixData<R> D;
+  prefix_data<R>(sp, tb, blkf, P, D);
+  constexpr int NS = R * kMaxPerRun;
   int lay[NS], bis[NS];
   double cost;
-  score<MAXR>(sp, tb, blkf, L, window, Y, cost, lay, bis);
-  int s = 0;
+  eval_layout<R, true>(sp, tb, blkf, L, window, D, tb.suf[s], cost, lay, bis);
+  int n = 0;
   for (int q = 0; q < NS; ++q) {
     if (bis[q] < 0) continue;
     const BlockRec& br = blk[bis[q]];
     const int o = tb.opt[(size_t)bis[q] * L + (lay[q] - 1)];
     const int tp = 1 << o;
-    out->first[s] = br.start;
-    out->count[s] = br.n;
-    out->tp[s] = tp;
-    out->dp[s] = br.n / tp;
-    out->layers[s] = lay[q];
-    ++s;
+    out->first[n] = br.start;
+    out->count[n] = br.n;
+    out->tp[n] = tp;
+    out->dp[n] = br.n / tp;
+    out->layers[n] = lay[q];
+    ++n;
   }
-  out->n_stages = s;
+  out->n_stages = n;
 }
 
 // ===================================================================== host
@@ -618,8 +727,10 @@ struct HostSpace {
   std::vector<int> pos_off;
   std::vector<BlockMeta> meta;
   std::vector<int4> items;
+  std::vector<int4> choices;   // last-run choices (k, b1, b2, b3)
   int nblk = 0, tin_size = 0, tx_size = 0;
   long long total = 0;
+  long long n_prefix = 0;
 };
 
 int build_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, HostSpace& h) {
@@ -667,21 +778,29 @@ int build_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, 
     sp.nc[r] = (int)(h.pos.size() - h.pos_off[r]) - 2;
     sp.kmax[r] = std::min(sp.max_per_run, len);
   }
-  // completion counts cnt[r][u]
+  // completion counts: cnt over all runs, cntP over the prefix runs
   std::memset(sp.cnt, 0, sizeof sp.cnt);
-  for (int u = 0; u <= sp.max_stages; ++u) sp.cnt[sp.R][u] = 1;
+  std::memset(sp.cntP, 0, sizeof sp.cntP);
+  for (int u = 0; u <= sp.max_stages; ++u) {
+    sp.cnt[sp.R][u] = 1;
+    sp.cntP[sp.R - 1][u] = 1;
+  }
   for (int r = sp.R - 1; r >= 0; --r) {
     const int rem = sp.R - 1 - r;
     for (int u = 0; u <= sp.max_stages; ++u) {
-      long long acc = 0;
+      long long acc = 0, accP = 0;
       for (int k = 1; k <= sp.kmax[r]; ++k) {
         if (u + k + rem > sp.max_stages) break;
         acc += binom_small(sp.nc[r], k - 1) * sp.cnt[r + 1][u + k];
+        if (r + 1 < sp.R) accP += binom_small(sp.nc[r], k - 1) * sp.cntP[r + 1][u + k];
       }
       sp.cnt[r][u] = acc;
+      if (r + 1 < sp.R) sp.cntP[r][u] = accP;
     }
   }
-  h.total = sp.max_stages >= sp.R ? sp.cnt[0][0] : 0;
+  const bool any = sp.max_stages >= sp.R;
+  h.total = any ? sp.cnt[0][0] : 0;
+  h.n_prefix = any ? sp.cntP[0][0] : 0;
   // blocks, transfer items
   h.nblk = 0;
   h.tin_size = 0;
@@ -705,7 +824,63 @@ int build_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, 
         for (int c = 1; c <= sp.nc[r + 1] + 1; ++c) h.items.push_back(make_int4(r, a, 0, -c));
     }
   }
+  // last-run choices in run_compositions order: k ascending, cut indices lexicographic
+  {
+    const int r = sp.R - 1, nc = sp.nc[r];
+    for (int k = 1; k <= sp.kmax[r]; ++k) {
+      const int m = k - 1;
+      if (nc < m) break;
+      int c[3] = {0, 1, 2};
+      while (true) {
+        int4 ch = make_int4(k, 0, 0, 0);
+        if (m > 0) ch.y = c[0] + 1;
+        if (m > 1) ch.z = c[1] + 1;
+        if (m > 2) ch.w = c[2] + 1;
+        h.choices.push_back(ch);
+        int j = m - 1;
+        while (j >= 0 && c[j] == nc - m + j) --j;
+        if (j < 0) break;
+        ++c[j];
+        for (int t = j + 1; t < m; ++t) c[t] = c[t - 1] + 1;
+      }
+    }
+    sp.n_suf = (int)h.choices.size();
+  }
   return GP_OK;
+}
+
+// Host twin of prefix_decode's base (rank of a prefix's first layout).
+template <int R>
+long long prefix_base_host(const TrainSpace& sp, long long p) {
+  Prefix<R> P;
+  return prefix_decode<R>(sp, p, P);
+}
+
+long long prefix_base(const TrainSpace& sp, long long p) {
+  switch (sp.R) {
+    case 1: return 0;
+    case 2: return prefix_base_host<2>(sp, p);
+    case 3: return prefix_base_host<3>(sp, p);
+    case 4: return prefix_base_host<4>(sp, p);
+    default: return prefix_base_host<8>(sp, p);
+  }
+}
+
+// rank -> (prefix, suffix): the last prefix whose base <= rank.
+void rank_split(const HostSpace& h, long long rank, long long& p, long long& s) {
+  if (rank >= h.total) {
+    p = h.n_prefix;
+    s = 0;
+    return;
+  }
+  long long lo = 0, hi = h.n_prefix - 1;
+  while (lo < hi) {
+    const long long mid = lo + (hi - lo + 1) / 2;
+    if (prefix_base(h.sp, mid) <= rank) lo = mid;
+    else hi = mid - 1;
+  }
+  p = lo;
+  s = rank - prefix_base(h.sp, lo);
 }
 
 template <typename T>
@@ -716,26 +891,34 @@ T* carve(char*& p, size_t count) {
   return r;
 }
 
-template <int MAXR>
+template <int R>
 int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const double2* blkf,
                 const BlockRec* blk, int window, long long lo, long long hi, Best* partial,
                 int max_blocks, TrainOut* d_out) {
-  const long long span = hi - lo;
+  ScanRange rg{};
+  rank_split(h, lo, rg.p_lo, rg.s_lo);
+  rank_split(h, hi, rg.p_hi, rg.s_hi);
+  rg.n_pref = rg.p_hi - rg.p_lo + (rg.s_hi > 0 ? 1 : 0);
   const int threads = 256;
-  long long chunk = span / ((long long)ctx->num_sms * 2048 * 4);
-  chunk = std::max(8LL, std::min(chunk, 512LL));
-  const long long n_chunks = (span + chunk - 1) / chunk;
-  long long blocks = (n_chunks + threads - 1) / threads;
-  blocks = std::max(1LL, std::min(blocks, (long long)max_blocks));
-  if (span > 0) {
-    k1_layout_scan<MAXR><<<(int)blocks, threads, 0, ctx->stream>>>(h.sp, tb, blkf, ctx->sc.L, window,
-                                                                    lo, hi, chunk, partial);
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_layout_scan<R>, threads, 0);
+    occ = std::max(1, occ);
+  }
+  const long long warps_total = (long long)ctx->num_sms * occ * (threads / 32);
+  rg.chunk = std::max(1LL, rg.n_pref / (warps_total * 6));
+  const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
+  long long blocks = (n_items + (threads / 32) - 1) / (threads / 32);
+  blocks = std::max(1LL, std::min(blocks, std::min((long long)max_blocks, (long long)ctx->num_sms * occ)));
+  if (hi > lo) {
+    k1_layout_scan<R><<<(int)blocks, threads, 0, ctx->stream>>>(h.sp, tb, blkf, ctx->sc.L, window, rg,
+                                                                 partial);
     ctx->launches++;
   } else {
     blocks = 0;
   }
-  k1_finalize<MAXR><<<1, 256, 0, ctx->stream>>>(h.sp, tb, blkf, blk, ctx->sc.L, window, partial,
-                                                 (int)blocks, d_out);
+  k1_finalize<R><<<1, 256, 0, ctx->stream>>>(h.sp, tb, blkf, blk, ctx->sc.L, window, partial,
+                                              (int)blocks, d_out);
   ctx->launches++;
   GP_CUDA(cudaGetLastError());
   return GP_OK;
@@ -765,6 +948,7 @@ struct PreparedTrain {
   int* d_run_start = nullptr;
   BlockMeta* d_meta = nullptr;
   int4* d_items = nullptr;
+  int4* d_choices = nullptr;
   BlockRec* d_blk = nullptr;
   double2* d_blkf = nullptr;
   double2* d_stage = nullptr;
@@ -772,6 +956,7 @@ struct PreparedTrain {
   double* d_tin = nullptr;
   double* d_tx = nullptr;
   double* d_fd = nullptr;
+  SufEnt* d_suf = nullptr;
   Best* d_partial = nullptr;
   TrainOut* d_out = nullptr;
   int max_blocks = 0;
@@ -806,6 +991,7 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
   add(sizeof(int) * h.run_start.size());
   add(sizeof(BlockMeta) * h.meta.size());
   add(sizeof(int4) * h.items.size());
+  add(sizeof(int4) * h.choices.size());
   add(sizeof(BlockRec) * h.nblk);
   add(sizeof(double2) * h.nblk);
   add(sizeof(double2) * (size_t)h.nblk * L);
@@ -813,6 +999,7 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
   add(sizeof(double) * (h.tin_size + 1));
   add(sizeof(double) * (h.tx_size + 1));
   add(sizeof(double) * (GP_MAX_STAGES + 1));
+  add(sizeof(SufEnt) * (h.choices.size() + 1));
   add(sizeof(Best) * P.max_blocks);
   add(sizeof(TrainOut));
   char* base = static_cast<char*>(ctx_scratch(ctx, bytes));
@@ -823,6 +1010,7 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
   P.d_run_start = carve<int>(p, h.run_start.size());
   P.d_meta = carve<BlockMeta>(p, h.meta.size());
   P.d_items = carve<int4>(p, h.items.size());
+  P.d_choices = carve<int4>(p, h.choices.size());
   P.d_blk = carve<BlockRec>(p, h.nblk);
   P.d_blkf = carve<double2>(p, h.nblk);
   P.d_stage = carve<double2>(p, (size_t)h.nblk * L);
@@ -830,10 +1018,11 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
   P.d_tin = carve<double>(p, h.tin_size + 1);
   P.d_tx = carve<double>(p, h.tx_size + 1);
   P.d_fd = carve<double>(p, GP_MAX_STAGES + 1);
+  P.d_suf = carve<SufEnt>(p, h.choices.size() + 1);
   P.d_partial = carve<Best>(p, P.max_blocks);
   P.d_out = carve<TrainOut>(p, 1);
   // one pinned staging buffer -> one H2D copy of the enumeration metadata
-  const size_t in_bytes = (size_t)(P.d_items + h.items.size()) - (size_t)P.d_ordered;
+  const size_t in_bytes = (size_t)(P.d_choices + h.choices.size()) - (size_t)P.d_ordered;
   char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(TrainOut))));
   if (!hp) return GP_CUDA_ERROR;
   auto stage_in = [&](const void* src, size_t sz, void* dptr) {
@@ -844,6 +1033,7 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
   stage_in(h.run_start.data(), sizeof(int) * h.run_start.size(), P.d_run_start);
   stage_in(h.meta.data(), sizeof(BlockMeta) * h.meta.size(), P.d_meta);
   stage_in(h.items.data(), sizeof(int4) * h.items.size(), P.d_items);
+  stage_in(h.choices.data(), sizeof(int4) * h.choices.size(), P.d_choices);
   GP_CUDA(cudaMemcpyAsync(P.d_ordered, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h2d_bytes += (long long)in_bytes;
   // sum over layouts of S (roofline accounting only): tot[r][u] = sum of stages of runs r..
@@ -887,6 +1077,7 @@ int train_launch(gp_ctx* ctx, int window, long long lo, long long hi) {
   tb.tin = P.d_tin;
   tb.tx = P.d_tx;
   tb.fd_coef = P.d_fd;
+  tb.suf = P.d_suf;
   for (int r = 0; r < h.sp.R; ++r) tb.pos_off[r] = h.pos_off[r];
   if (ctx->timing) GP_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   // ---- K2: per-train-set tables
@@ -908,7 +1099,10 @@ int train_launch(gp_ctx* ctx, int window, long long lo, long long hi) {
     k2c_stage_table<<<(int)((cnt + 255) / 256), 256, 0, ctx->stream>>>(P.d_blk, h.nblk, ctx->sc,
                                                                       ctx->d_ceff, P.d_stage, P.d_opt);
     k_extract_blkf<<<(h.nblk + 255) / 256, 256, 0, ctx->stream>>>(P.d_blk, h.nblk, P.d_blkf);
-    ctx->launches += 2;
+    const int ns = (int)h.choices.size();
+    k2d_suffix_table<<<(ns + 255) / 256, 256, 0, ctx->stream>>>(P.d_choices, ns, h.sp, P.d_tin,
+                                                                P.d_suf);
+    ctx->launches += 3;
   }
   GP_CUDA(cudaGetLastError());
   if (ctx->timing) GP_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
@@ -919,7 +1113,7 @@ int train_launch(gp_ctx* ctx, int window, long long lo, long long hi) {
   else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
   else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
   else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
-  else rc = launch_scan<8>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
+  else rc = set_error(GP_INVALID, "train sets spanning more than 4 gpu types are not supported");
   if (!rc && ctx->timing) GP_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
   return rc;
 }
