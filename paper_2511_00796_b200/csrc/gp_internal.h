@@ -65,7 +65,7 @@ struct TrainSpace {
 
 // One choice of the last type run (the "suffix" of a layout), in enumeration order:
 // its block ids, its internal stage-transfer terms and the end of its first block.
-struct SufEnt {
+struct __align__(16) SufEnt {
   int bi[4];
   double t[3];
   int k;
@@ -77,7 +77,7 @@ struct TrainTables {
   const int* ordered;
   const int* pos;        // per run: positions [0, cuts..., len], offsets = pos_off
   const BlockRec* blk;
-  const double2* stage;  // [nblk * L] (total, compute); total < 0 => memory-infeasible
+  const double2* stage;  // [nblk * L] (total, compute); total = +inf => memory-infeasible
   const int8_t* opt;     // [nblk * L] chosen tp option index
   const double* tin;
   const double* tx;

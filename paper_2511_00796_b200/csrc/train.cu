@@ -247,7 +247,9 @@ __global__ void __launch_bounds__(256) k2c_stage_table(const BlockRec* __restric
     }
   }
   double2 e;
-  e.x = best_o < 0 ? -1.0 : compute + best_tp_comm + best_dp_comm;  // TrainStageCost::total()
+  // TrainStageCost::total(); +inf marks "no memory-feasible option" so that the layout
+  // maximum becomes +inf and the layout is rejected without a per-stage test in K1
+  e.x = best_o < 0 ? __longlong_as_double(0x7ff0000000000000LL) : compute + best_tp_comm + best_dp_comm;
   e.y = compute;
   stage[idx] = e;
   opt[idx] = (int8_t)best_o;
@@ -460,29 +462,27 @@ __device__ __forceinline__ bool eval_layout(const TrainSpace& sp, const TrainTab
                                             int* out_lay, int* out_bi) {
   constexpr int NP = (R - 1) * kMaxPerRun;
   constexpr int NS = NP + kMaxPerRun;
-  int bi[NS];
-  double lfn[NS];
+  // Prefix fields are re-read from the warp's shared-memory copy where they are used
+  // (volatile: keeps them out of registers across the phases below).
+  auto vbi = [&](int q) { return *(const volatile int*)&D.bi[q]; };
+  auto vlfn = [&](int q) { return *(const volatile double*)&D.lfn[q]; };
   bool act[NS];
   int lay[NS];
-  long long key[NS];
+  double rem[NS];
   double total = D.total;
 #pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    bi[q] = D.bi[q];
-    lfn[q] = D.lfn[q];
-    act[q] = D.act[q];
-  }
+  for (int q = 0; q < NP; ++q) act[q] = D.act[q];
   const int k = e.k;
+  double lfn_s[kMaxPerRun];
 #pragma unroll
   for (int j = 0; j < kMaxPerRun; ++j) {
     const int q = NP + j;
     act[q] = j < k;
-    bi[q] = e.bi[j];
-    lfn[q] = 0;
+    lfn_s[j] = 0;
     if (act[q]) {
-      const double2 fl = blkf[bi[q]];
+      const double2 fl = blkf[e.bi[j]];
       total += fl.x;  // allocate_layers total: left fold in stage order
-      lfn[q] = fl.y;
+      lfn_s[j] = fl.y;
     }
   }
   const int S = D.u + k;
@@ -490,12 +490,13 @@ __device__ __forceinline__ bool eval_layout(const TrainSpace& sp, const TrainTab
   int assigned = 0;
 #pragma unroll
   for (int q = 0; q < NS; ++q) {
-    const double share = div_rn_recip(lfn[q], total, y);  // num_layers * f / total
+    const double share = div_rn_recip(q < NP ? vlfn(q) : lfn_s[q - NP], total, y);  // L * f / total
     lay[q] = static_cast<int>(share);
-    key[q] = act[q] ? __double_as_longlong(share - lay[q]) : -1LL;  // rem >= +0
+    rem[q] = act[q] ? share - lay[q] : -1.0;  // remainder >= +0 for active slots
     assigned += act[q] ? lay[q] : 0;
   }
-  // std::stable_sort of remainders (desc) -> position; extra layers round-robin
+  // std::stable_sort of remainders (desc) -> position of each slot; equal remainders
+  // keep slot (stage) order. One DSETP + two predicated adds per pair.
   int pos[NS];
 #pragma unroll
   for (int q = 0; q < NS; ++q) pos[q] = 0;
@@ -503,19 +504,25 @@ __device__ __forceinline__ bool eval_layout(const TrainSpace& sp, const TrainTab
   for (int q = 0; q < NS; ++q) {
 #pragma unroll
     for (int q2 = q + 1; q2 < NS; ++q2) {
-      if (key[q] >= key[q2]) pos[q2]++;
-      else pos[q]++;
+      asm("{\n\t.reg .pred p;\n\tsetp.ge.f64 p, %2, %3;\n\t@p add.s32 %1, %1, 1;\n\t"
+          "@!p add.s32 %0, %0, 1;\n\t}"
+          : "+r"(pos[q]), "+r"(pos[q2])
+          : "d"(rem[q]), "d"(rem[q2]));
     }
   }
-  int extra = L - assigned, ex_div = 0, ex_mod = extra;
-  if (extra < 0 || extra >= S) {
-    ex_div = extra / S;
+  int extra = L - assigned, ex_mod = extra;
+  if (extra < 0 || extra >= S) {  // rare: more than one round of the round-robin
+    const int ex_div = extra / S;
     ex_mod = extra % S;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) lay[q] += ex_div;
   }
   bool zero = false;
 #pragma unroll
   for (int q = 0; q < NS; ++q) {
-    lay[q] += ex_div + (pos[q] < ex_mod ? 1 : 0);
+    asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+        : "+r"(lay[q])
+        : "r"(pos[q]), "r"(ex_mod));
     zero |= act[q] && lay[q] == 0;
   }
   if (zero) {  // every stage needs at least one layer (src/train_search.cpp:217-225)
@@ -536,25 +543,29 @@ __device__ __forceinline__ bool eval_layout(const TrainSpace& sp, const TrainTab
       }
     }
   }
-  // gather stage entries (train_cost_breakdown, src/cost_model.cpp:93-126)
+  // gather stage entries (train_cost_breakdown, src/cost_model.cpp:93-126). Totals and
+  // computes are >= 0, infeasible entries hold +inf: plain ordered compares suffice.
+  const double2* __restrict__ stage = tb.stage;
   double max_total = 0, max_comp = 0;
-  bool feasible = true;
 #pragma unroll
   for (int q = 0; q < NS; ++q) {
     if (act[q]) {
-      const double2 st = tb.stage[(size_t)bi[q] * L + (lay[q] - 1)];
-      feasible &= st.x >= 0;
-      max_total = max_total < st.x ? st.x : max_total;
-      max_comp = max_comp < st.y ? st.y : max_comp;
+      const int b = q < NP ? vbi(q) : e.bi[q - NP];
+      const double2 st = stage[(unsigned)(b * L + (lay[q] - 1))];
+      asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %2, %0;\n\t@p mov.b64 %0, %2;\n\t"
+          "setp.gt.f64 p, %3, %1;\n\t@p mov.b64 %1, %3;\n\t}"
+          : "+d"(max_total), "+d"(max_comp)
+          : "d"(st.x), "d"(st.y));
     }
   }
   if (DECODE) {
 #pragma unroll
     for (int q = 0; q < NS; ++q) {
       out_lay[q] = act[q] ? lay[q] : 0;
-      out_bi[q] = act[q] ? bi[q] : -1;
+      out_bi[q] = act[q] ? (q < NP ? vbi(q) : e.bi[q - NP]) : -1;
     }
   }
+  const bool feasible = max_total < __longlong_as_double(0x7ff0000000000000LL);
   if (!feasible) return false;
   // stage transfers in stage order: prefix-internal, junction, suffix-internal
   double transfers = D.transfers;
@@ -578,8 +589,10 @@ struct ScanRange {
   long long chunk;                   // prefixes per warp work item
 };
 
+constexpr int kK1Threads = 128;
+
 template <int R>
-__global__ void __launch_bounds__(256) k1_layout_scan(TrainSpace sp, TrainTables tb,
+__global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(TrainSpace sp, TrainTables tb,
                                                       const double2* __restrict__ blkf, int L,
                                                       int window, ScanRange rg,
                                                       Best* __restrict__ partial) {
@@ -591,15 +604,21 @@ __global__ void __launch_bounds__(256) k1_layout_scan(TrainSpace sp, TrainTables
   double best_cost = kInf * 10;
   long long best_key = LLONG_MAX;
   long long feasible = 0;
+  // the warp's current prefix lives in shared memory (lane 0 owns it; lanes read broadcasts)
+  __shared__ Prefix<R> sP[kK1Threads / 32];
+  __shared__ PrefixData<R> sD[kK1Threads / 32];
+  Prefix<R>& P = sP[threadIdx.x >> 5];
+  PrefixData<R>& D = sD[threadIdx.x >> 5];
   for (long long it = warp; it < n_items; it += n_warps) {
     long long p = rg.p_lo + it * rg.chunk;
     const long long p_end = min(p + rg.chunk, rg.p_lo + rg.n_pref);
-    Prefix<R> P;
-    prefix_decode<R>(sp, p, P);
+    __syncwarp();
+    if (lane == 0) prefix_decode<R>(sp, p, P);
     for (; p < p_end; ++p) {
-      PrefixData<R> D;
-      prefix_data<R>(sp, tb, blkf, P, D);
-      const long long ns = sp.cnt[R - 1][P.u];
+      __syncwarp();
+      if (lane == 0) prefix_data<R>(sp, tb, blkf, P, D);
+      __syncwarp();
+      const long long ns = sp.cnt[R - 1][D.u];
       const long long s0 = p == rg.p_lo ? rg.s_lo : 0;
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
       for (long long s = s0 + lane; s < s1; s += 32) {
@@ -613,7 +632,8 @@ __global__ void __launch_bounds__(256) k1_layout_scan(TrainSpace sp, TrainTables
           }
         }
       }
-      if (p + 1 < p_end) prefix_advance<R>(sp, P);
+      __syncwarp();
+      if (lane == 0 && p + 1 < p_end) prefix_advance<R>(sp, P);
     }
   }
 #pragma unroll
@@ -899,7 +919,7 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   rank_split(h, lo, rg.p_lo, rg.s_lo);
   rank_split(h, hi, rg.p_hi, rg.s_hi);
   rg.n_pref = rg.p_hi - rg.p_lo + (rg.s_hi > 0 ? 1 : 0);
-  const int threads = 256;
+  const int threads = kK1Threads;
   static int occ = 0;
   if (!occ) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_layout_scan<R>, threads, 0);

@@ -18,7 +18,8 @@ import numpy as np
 from . import abi
 from .inputs import Problem
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgplan.so")
+_LIB_PATH = os.environ.get("GPLAN_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                       "libgplan.so")
 _lib = None
 
 
