@@ -20,6 +20,13 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
 int train_launch(gp_ctx* ctx, int window, long long lo, long long hi);
 int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices);
 void train_state_free(gp_ctx* ctx);
+int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opts* o, gp_config* out,
+                    int cap, int* n_out);
+int rollout_capacities(gp_ctx* ctx, const int32_t* ids, int n, int32_t* caps);
+int solve_milp(gp_ctx* ctx, const gp_config* cfg, int nc, const int32_t* caps, int dims, double B,
+               double len, gp_rollout_result* out, gp_rollout_entry* entries);
+int weight_sync(gp_ctx* ctx, const int32_t* train, int nt, const int32_t* roll, int nr,
+                const int32_t* etype, const int32_t* erep, int ne, int window, double* out);
 
 static thread_local std::string g_error;
 
@@ -32,20 +39,22 @@ int cuda_fail(cudaError_t e, const char* what) {
   return set_error(GP_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-void* ctx_scratch(gp_ctx* ctx, size_t bytes) {
-  if (bytes > ctx->scratch_bytes) {
-    if (ctx->scratch) cudaFree(ctx->scratch);
-    ctx->scratch = nullptr;
+void* ctx_scratch(gp_ctx* ctx, size_t bytes, int arena) {
+  void*& buf = ctx->scratch_arena[arena];
+  size_t& have = ctx->scratch_arena_bytes[arena];
+  if (bytes > have) {
+    if (buf) cudaFree(buf);
+    buf = nullptr;
     size_t want = bytes + bytes / 4;
-    cudaError_t e = cudaMalloc(&ctx->scratch, want);
+    cudaError_t e = cudaMalloc(&buf, want);
     if (e != cudaSuccess) {
-      ctx->scratch_bytes = 0;
+      have = 0;
       cuda_fail(e, "cudaMalloc(scratch)");
       return nullptr;
     }
-    ctx->scratch_bytes = want;
+    have = want;
   }
-  return ctx->scratch;
+  return buf;
 }
 
 void* ctx_pinned(gp_ctx* ctx, size_t bytes) {
@@ -222,7 +231,8 @@ void gp_ctx_destroy(gp_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* ptrs[] = {ctx->d_type, ctx->d_machine, ctx->d_flops, ctx->d_hbm_bw, ctx->d_hbm_cap,
                   ctx->d_links, ctx->d_ceff, ctx->d_ioeff, ctx->d_tflops, ctx->d_thbm,
-                  ctx->d_tcap, ctx->scratch};
+                  ctx->d_tcap,   ctx->scratch_arena[0], ctx->scratch_arena[1],
+                  ctx->scratch_arena[2], ctx->scratch_arena[3]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
@@ -273,6 +283,35 @@ int gp_train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices) 
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return train_collect(ctx, out, stage_devices);
+}
+
+int gp_enumerate_configs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_rollout_opts* o,
+                         gp_config* out, int32_t cap, int32_t* n_out) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return rollout_configs(ctx, ids, n, o, out, cap, n_out);
+}
+
+int gp_rollout_capacities(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t* caps) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  return rollout_capacities(ctx, ids, n, caps);
+}
+
+int gp_solve_milp(gp_ctx* ctx, const gp_config* configs, int32_t n_configs, const int32_t* caps,
+                  int32_t dims, double total_rollouts, double mean_len, gp_rollout_result* out,
+                  gp_rollout_entry* entries) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return solve_milp(ctx, configs, n_configs, caps, dims, total_rollouts, mean_len, out, entries);
+}
+
+int gp_weight_sync_cost(gp_ctx* ctx, const int32_t* train, int32_t n_train, const int32_t* rollout,
+                        int32_t n_rollout, const int32_t* entry_types, const int32_t* entry_replicas,
+                        int32_t n_entries, int32_t window, double* out) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return weight_sync(ctx, train, n_train, rollout, n_rollout, entry_types, entry_replicas, n_entries,
+                     window, out);
 }
 
 int gp_ctx_set_timing(gp_ctx* ctx, int on) {

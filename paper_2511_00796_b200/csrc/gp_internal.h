@@ -130,9 +130,9 @@ struct gp_ctx {
   gp::Scalars sc{};
   gp_workload work{};
   gp_calib calib{};
-  // grow-only scratch for the train search
-  void* scratch = nullptr;
-  size_t scratch_bytes = 0;
+  // grow-only device scratch, one arena per subsystem (0 train, 1 rollout, 2 partition)
+  void* scratch_arena[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t scratch_arena_bytes[4] = {0, 0, 0, 0};
   void* h_pinned = nullptr;
   size_t h_pinned_bytes = 0;
   int num_sms = 148;
@@ -152,7 +152,8 @@ struct gp_ctx {
 namespace gp {
 int set_error(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
-void* ctx_scratch(gp_ctx* ctx, size_t bytes);
+enum { kArenaTrain = 0, kArenaRollout = 1, kArenaPartition = 2, kArenaMisc = 3 };
+void* ctx_scratch(gp_ctx* ctx, size_t bytes, int arena = kArenaMisc);
 void* ctx_pinned(gp_ctx* ctx, size_t bytes);
 }  // namespace gp
 

@@ -1,0 +1,606 @@
+// rollout.cu — sm_100a kernels for the rollout side of the hot path:
+//   K3  enumerate_configs + replica_concurrency/replica_rate_at
+//       (src/rollout_milp.cpp:122-172, src/cost_model.cpp:209-253)
+//   K4  solve_milp: exact unbounded-knapsack DP over the type-capacity lattice
+//       (src/rollout_milp.cpp:174-254), level-synchronous wavefront
+//   K6  weight_sync_cost (src/cost_model.cpp:255-277)
+//
+// K4 design. best[s] = max_c best[s - v_c] + h_c with strict '>' in config order
+// (first maximal config wins). Every config is type-pure and uses >= 1 device,
+// so a state at level l = sum_t s_t depends only on lower levels: one level is
+// one parallel step. Configs sharing (type, devices) read the same predecessor,
+// and fp addition is monotone, so the value is max over groups of
+// best[prev_g] + hmax_g (exact); the choice is the smallest config index c with
+// best[prev_g(c)] + h_c == that value, found by scanning only the groups that
+// reach it. The value and the choice are therefore identical to the reference's
+// sequential scan; the backtracking walk runs on one device thread.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <vector>
+
+#include "gp_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace gp {
+
+// ------------------------------------------------------------------ K3 configs
+struct CfgCand {
+  int type;
+  int stages;
+  int tp[4];
+};
+
+__device__ __forceinline__ int trunc_i32_x86(double x) {
+  // static_cast<int>(double) on x86-64 (cvttsd2si): out of range / NaN -> INT_MIN
+  if (!(x > -2147483649.0 && x < 2147483648.0)) return INT_MIN;
+  return static_cast<int>(x);
+}
+
+// One thread per (type, tp-multiset) candidate; the caller compacts in order.
+__global__ void k3_configs(const CfgCand* __restrict__ cands, int n_cands,
+                           const int* __restrict__ avail /* [T][4] top-4 machine counts */,
+                           const int* __restrict__ n_machines /* [T] */, int max_stages,
+                           Scalars sc, const double* __restrict__ tcap,
+                           const double* __restrict__ thbm, const double* __restrict__ tflops,
+                           const double* __restrict__ ceff, const double* __restrict__ ioeff,
+                           int T, gp_config* __restrict__ out, int* __restrict__ keep) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_cands) return;
+  const CfgCand c = cands[i];
+  const int t = c.type, S = c.stages;
+  int ms = max_stages < n_machines[t] ? max_stages : n_machines[t];
+  ms = ms < sc.L ? ms : sc.L;
+  bool ok = n_machines[t] > 0 && S <= ms;
+  for (int s = 0; s < S && ok; ++s) ok = c.tp[s] <= avail[t * 4 + s];  // stage k on k-th largest machine
+  int conc = 0;
+  if (ok) {
+    // replica_concurrency (src/cost_model.cpp:209-229)
+    int best = sc.max_conc;
+    for (int s = 0; s < S; ++s) {
+      const int layers = sc.L / S + (s < sc.L % S ? 1 : 0);  // layers_for_stage
+      const int tp = c.tp[s];
+      const double lf = static_cast<double>(layers) / sc.L;
+      const double weight = sc.P * lf * sc.bpp_infer / tp;
+      const double free_b = tcap[t] - weight;
+      if (free_b < 0) {
+        best = 0;
+        break;
+      }
+      const double kv = sc.kvbpt * sc.mtl * lf / tp;
+      if (kv > 0) {
+        const int v = trunc_i32_x86(free_b / kv);
+        best = v < best ? v : best;
+      }
+    }
+    conc = best > 0 ? best : 0;
+  }
+  keep[i] = ok && conc >= 1;
+  if (!keep[i]) return;
+  gp_config cfg;
+  for (int u = 0; u < GP_MAX_TYPES; ++u) cfg.type_counts[u] = 0;
+  for (int u = 0; u < GP_MAX_ROLLOUT_STAGES; ++u) cfg.tp[u] = 0;
+  int n = 0;
+  for (int s = 0; s < S; ++s) {
+    cfg.tp[s] = c.tp[s];
+    n += c.tp[s];
+  }
+  cfg.type_counts[t] = n;
+  cfg.n_stages = S;
+  // replica_rate_at (src/cost_model.cpp:231-246): only type t contributes
+  double agg_bw = 0, agg_flops = 0;
+  for (int u = 0; u < T; ++u) {
+    if (cfg.type_counts[u] == 0) continue;
+    agg_bw += cfg.type_counts[u] * thbm[u] * ioeff[u];
+    agg_flops += cfg.type_counts[u] * tflops[u] * ceff[u];
+  }
+  const double io_rate = static_cast<double>(conc) * agg_bw / sc.mbi;
+  const double compute_rate = agg_flops / sc.ifpt;
+  const double penalty = 1.0 + sc.stage_pen * (S - 1);
+  const double m = compute_rate < io_rate ? compute_rate : io_rate;
+  cfg.throughput = m / penalty;
+  out[i] = cfg;
+}
+
+// ---------------------------------------------------------------- K4 MILP DP
+struct MilpDims {
+  int T;
+  long long states;
+  long long stride[GP_MAX_TYPES];
+  int cap[GP_MAX_TYPES];
+  int levels;  // sum cap + 1
+};
+
+struct Group {
+  int type;
+  int n;            // devices of the type used by each member
+  double hmax;      // max member throughput
+  int first, count; // members[first .. first+count) = config indices, ascending
+};
+
+__device__ __forceinline__ int state_level(const MilpDims& d, long long s, int* coord) {
+  int l = 0;
+  for (int t = d.T - 1; t >= 0; --t) {
+    coord[t] = (int)(s / d.stride[t]);
+    s -= (long long)coord[t] * d.stride[t];
+    l += coord[t];
+  }
+  return l;
+}
+
+__global__ void k4_level_hist(MilpDims d, int* __restrict__ hist) {
+  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < d.states;
+       s += (long long)gridDim.x * blockDim.x) {
+    int coord[GP_MAX_TYPES];
+    atomicAdd(&hist[state_level(d, s, coord)], 1);
+  }
+}
+
+// exclusive scan of level counts (levels <= N+1, one CTA)
+__global__ void k4_level_scan(const int* __restrict__ hist, int levels, long long* __restrict__ off,
+                              int* __restrict__ cursor) {
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int l = 0; l < levels; ++l) {
+      off[l] = acc;
+      cursor[l] = 0;
+      acc += hist[l];
+    }
+    off[levels] = acc;
+  }
+}
+
+__global__ void k4_level_scatter(MilpDims d, const long long* __restrict__ off,
+                                 int* __restrict__ cursor, unsigned* __restrict__ order) {
+  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < d.states;
+       s += (long long)gridDim.x * blockDim.x) {
+    int coord[GP_MAX_TYPES];
+    const int l = state_level(d, s, coord);
+    const int slot = atomicAdd(&cursor[l], 1);
+    order[off[l] + slot] = (unsigned)s;
+  }
+}
+
+__device__ __forceinline__ void relax_state(const MilpDims& d, const Group* __restrict__ groups,
+                                            int n_groups, const int* __restrict__ members,
+                                            const double* __restrict__ h, double* __restrict__ best,
+                                            int* __restrict__ choice, long long s) {
+  int coord[GP_MAX_TYPES];
+  state_level(d, s, coord);
+  double m = 0.0;  // best[s] starts at 0.0 and only a strictly larger candidate replaces it
+  for (int g = 0; g < n_groups; ++g) {
+    const Group G = groups[g];
+    if (coord[G.type] < G.n) continue;
+    const double v = best[s - (long long)G.n * d.stride[G.type]] + G.hmax;
+    m = v > m ? v : m;
+  }
+  int ch = -1;
+  if (m > 0.0) {
+    ch = INT_MAX;
+    for (int g = 0; g < n_groups; ++g) {
+      const Group G = groups[g];
+      if (coord[G.type] < G.n) continue;
+      const double bp = best[s - (long long)G.n * d.stride[G.type]];
+      if (bp + G.hmax != m) continue;
+      for (int i = 0; i < G.count; ++i) {  // members ascending: first reaching m wins
+        const int c = members[G.first + i];
+        if (c >= ch) break;
+        if (bp + h[c] == m) {
+          ch = c;
+          break;
+        }
+      }
+    }
+  }
+  best[s] = m;
+  choice[s] = ch;
+}
+
+// Persistent cooperative kernel: one grid barrier per lattice level.
+__global__ void __launch_bounds__(256) k4_dp_levels(MilpDims d, const Group* __restrict__ groups,
+                                                    int n_groups, const int* __restrict__ members,
+                                                    const double* __restrict__ h,
+                                                    const long long* __restrict__ off,
+                                                    const unsigned* __restrict__ order,
+                                                    double* __restrict__ best,
+                                                    int* __restrict__ choice) {
+  cg::grid_group grid = cg::this_grid();
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  for (int l = 0; l < d.levels; ++l) {
+    for (long long i = off[l] + tid; i < off[l + 1]; i += nth)
+      relax_state(d, groups, n_groups, members, h, best, choice, order[i]);
+    grid.sync();
+  }
+}
+
+struct MilpOut {
+  double aggregate;
+  double makespan;
+  int n_entries;
+  int pad;
+};
+
+// Backtracking + plan assembly on one thread (src/rollout_milp.cpp:227-253).
+__global__ void k4_backtrack(MilpDims d, const gp_config* __restrict__ cfg, int n_cfg,
+                             const double* __restrict__ best, const int* __restrict__ choice,
+                             double B, double len, int* __restrict__ counts,
+                             gp_rollout_entry* __restrict__ entries, MilpOut* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const long long full = d.states - 1;
+  const double agg = best[full];
+  out->aggregate = agg;
+  out->n_entries = -1;
+  if (agg <= 0) return;
+  for (int c = 0; c < n_cfg; ++c) counts[c] = 0;
+  long long cur = full;
+  while (choice[cur] >= 0) {
+    const int c = choice[cur];
+    counts[c]++;
+    for (int t = 0; t < d.T; ++t) cur -= (long long)cfg[c].type_counts[t] * d.stride[t];
+  }
+  out->makespan = B * len / agg;
+  int ne = 0;
+  for (int c = 0; c < n_cfg; ++c) {
+    if (counts[c] == 0) continue;
+    entries[ne].config = c;
+    entries[ne].replicas = counts[c];
+    entries[ne].workload = B * counts[c] * cfg[c].throughput / agg;
+    ++ne;
+  }
+  out->n_entries = ne;
+}
+
+// ------------------------------------------------------------ K6 weight sync
+// For each rollout entry type: max link from any train device into any rollout
+// device of that type; bottleneck = min over entries (src/cost_model.cpp:255-277).
+__global__ void k6_type_maxlink(const int* __restrict__ train, int nt, const int* __restrict__ roll,
+                                int nr, const int* __restrict__ dtype, const double* __restrict__ links,
+                                int N, double* __restrict__ type_max /* [T] */) {
+  const int t = blockIdx.x;
+  double m = 0;
+  const long long tot = (long long)nt * nr;
+  for (long long p = threadIdx.x; p < tot; p += blockDim.x) {
+    const int i = (int)(p / nr), j = (int)(p - (long long)i * nr);
+    const int di = roll[j];
+    if (dtype[di] != t) continue;
+    const double l = links[(size_t)train[i] * N + di];
+    m = m < l ? l : m;
+  }
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const double x = __shfl_xor_sync(0xffffffffu, m, o);
+    m = m < x ? x : m;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = m < red[w] ? red[w] : m;
+    type_max[t] = m;
+  }
+}
+
+__global__ void k6_combine(const double* __restrict__ type_max, const int* __restrict__ etype,
+                           const int* __restrict__ erep, int ne, int window, double mbi,
+                           double sync_latency, double* __restrict__ out) {
+  double bottleneck = kInf;
+  for (int e = 0; e < ne; ++e) {
+    if (erep[e] < 1) continue;
+    const double best = etype[e] >= 0 ? type_max[etype[e]] : 0.0;
+    if (best > 0) bottleneck = best < bottleneck ? best : bottleneck;
+  }
+  double transfer = 0;
+  if (bottleneck < kInf && mbi > 0) transfer = mbi / bottleneck;
+  *out = window * transfer + sync_latency;
+}
+
+// ===================================================================== host
+
+template <typename T>
+static T* carve2(char*& p, size_t count) {
+  p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+  T* r = reinterpret_cast<T*>(p);
+  p += sizeof(T) * count;
+  return r;
+}
+
+int rollout_capacities(gp_ctx* ctx, const int32_t* ids, int n, int32_t* caps) {
+  for (int t = 0; t < ctx->T; ++t) caps[t] = 0;
+  for (int i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= ctx->N) return set_error(GP_INVALID, "unknown device id " + std::to_string(ids[i]));
+    caps[ctx->h_type[ids[i]]]++;
+  }
+  return GP_OK;
+}
+
+// enumerate_configs (src/rollout_milp.cpp:122-172)
+int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opts* o, gp_config* out,
+                    int cap, int* n_out) {
+  *n_out = 0;
+  if (n <= 0) return set_error(GP_INVALID, "enumerate_configs requires a non-empty rollout set");
+  if (o->max_stages < 0 || o->max_stages > 4)
+    return set_error(GP_INVALID, "rollout max_stages must lie in [0, 4] for the sm_100a kernel");
+  const int T = ctx->T;
+  // per type: machines with available devices and the 4 largest counts (stage k
+  // is placed on the k-th largest machine) — enumeration metadata only
+  std::vector<int> per_machine(ctx->M, 0), avail(T * 4, 0), nm(T, 0);
+  std::vector<char> seen(ctx->N, 0);
+  for (int i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= ctx->N) return set_error(GP_INVALID, "unknown device id " + std::to_string(ids[i]));
+    if (seen[ids[i]]++) return set_error(GP_INVALID, "duplicate device id " + std::to_string(ids[i]));
+    per_machine[ctx->h_machine[ids[i]]]++;
+  }
+  std::vector<std::vector<int>> by_type(T);
+  for (int m = 0; m < ctx->M; ++m) {
+    if (!per_machine[m]) continue;
+    // machines are type-pure in the reference loader; take the type of any device on it
+    int t = -1;
+    for (int i = 0; i < n && t < 0; ++i)
+      if (ctx->h_machine[ids[i]] == m) t = ctx->h_type[ids[i]];
+    by_type[t].push_back(per_machine[m]);
+  }
+  for (int t = 0; t < T; ++t) {
+    auto& v = by_type[t];
+    std::sort(v.rbegin(), v.rend());
+    nm[t] = (int)v.size();
+    for (int k = 0; k < 4 && k < (int)v.size(); ++k) avail[t * 4 + k] = v[k];
+  }
+  // candidate list in reference order: type, stages, tp_multisets({8,4,2,1})
+  std::vector<CfgCand> cands;
+  for (int t = 0; t < T; ++t) {
+    if (nm[t] == 0) continue;
+    for (int S = 1; S <= std::min(o->max_stages, 4); ++S) {
+      int tp[4];
+      // non-increasing sequences of length S over {8,4,2,1}
+      std::function<void(int, int)> rec = [&](int d, int mx) {
+        if (d == S) {
+          CfgCand c{t, S, {0, 0, 0, 0}};
+          for (int s = 0; s < S; ++s) c.tp[s] = tp[s];
+          cands.push_back(c);
+          return;
+        }
+        for (int v : {8, 4, 2, 1}) {
+          if (v > mx) continue;
+          tp[d] = v;
+          rec(d + 1, v);
+        }
+      };
+      rec(0, 8);
+    }
+  }
+  const int nc = (int)cands.size();
+  if (nc == 0) return GP_OK;
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+  add(sizeof(CfgCand) * nc);
+  add(sizeof(int) * T * 4);
+  add(sizeof(int) * T);
+  add(sizeof(gp_config) * nc);
+  add(sizeof(int) * nc);
+  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaRollout));
+  if (!base) return GP_CUDA_ERROR;
+  char* p = base;
+  CfgCand* d_c = carve2<CfgCand>(p, nc);
+  int* d_av = carve2<int>(p, T * 4);
+  int* d_nm = carve2<int>(p, T);
+  gp_config* d_out = carve2<gp_config>(p, nc);
+  int* d_keep = carve2<int>(p, nc);
+  const size_t in_bytes = (size_t)((char*)(d_nm + T) - (char*)d_c);
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(gp_config) * nc + sizeof(int) * nc + 512)));
+  if (!hp) return GP_CUDA_ERROR;
+  std::memcpy(hp, cands.data(), sizeof(CfgCand) * nc);
+  std::memcpy(hp + ((char*)d_av - (char*)d_c), avail.data(), sizeof(int) * T * 4);
+  std::memcpy(hp + ((char*)d_nm - (char*)d_c), nm.data(), sizeof(int) * T);
+  GP_CUDA(cudaMemcpyAsync(d_c, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)in_bytes;
+  k3_configs<<<(nc + 127) / 128, 128, 0, ctx->stream>>>(d_c, nc, d_av, d_nm, o->max_stages, ctx->sc,
+                                                      ctx->d_tcap, ctx->d_thbm, ctx->d_tflops,
+                                                      ctx->d_ceff, ctx->d_ioeff, T, d_out, d_keep);
+  ctx->launches++;
+  GP_CUDA(cudaGetLastError());
+  gp_config* h_cfg = reinterpret_cast<gp_config*>(hp);
+  int* h_keep = reinterpret_cast<int*>(hp + sizeof(gp_config) * nc);
+  GP_CUDA(cudaMemcpyAsync(h_cfg, d_out, sizeof(gp_config) * nc, cudaMemcpyDeviceToHost, ctx->stream));
+  GP_CUDA(cudaMemcpyAsync(h_keep, d_keep, sizeof(int) * nc, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += (long long)(sizeof(gp_config) + sizeof(int)) * nc;
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  int k = 0;
+  for (int i = 0; i < nc; ++i) {
+    if (!h_keep[i]) continue;
+    if (k < cap) out[k] = h_cfg[i];
+    ++k;
+  }
+  *n_out = k;
+  if (k > cap) return set_error(GP_CAPACITY, "config buffer too small (" + std::to_string(k) + " needed)");
+  return GP_OK;
+}
+
+// solve_milp (src/rollout_milp.cpp:174-254)
+int solve_milp(gp_ctx* ctx, const gp_config* cfg, int nc, const int32_t* caps, int dims, double B,
+               double len, gp_rollout_result* out, gp_rollout_entry* entries) {
+  std::memset(out, 0, sizeof *out);
+  out->total_rollouts = B;
+  if (B <= 0) return GP_OK;
+  if (nc == 0) return set_error(GP_INFEASIBLE, "no replica configuration available");
+  if (dims < 1 || dims > GP_MAX_TYPES) return set_error(GP_INVALID, "dims must lie in [1, GP_MAX_TYPES]");
+  MilpDims d{};
+  d.T = dims;
+  long long states = 1;
+  int levels = 1;
+  for (int t = 0; t < dims; ++t) {
+    if (caps[t] < 0) return set_error(GP_INVALID, "negative capacity");
+    d.stride[t] = states;
+    d.cap[t] = caps[t];
+    states *= caps[t] + 1;
+    levels += caps[t];
+    if (states > 50000000) return set_error(GP_INVALID, "capacity lattice too large for the exact solver");
+  }
+  d.states = states;
+  d.levels = levels;
+  out->states = states;
+  // groups of configs with the same (type, device count): one predecessor each
+  std::vector<Group> groups;
+  std::vector<int> members;
+  {
+    std::vector<std::pair<long long, int>> key;  // (type * 1e6 + n, index)
+    for (int c = 0; c < nc; ++c) {
+      int t = -1, n = 0, used = 0;
+      for (int u = 0; u < dims; ++u)
+        if (cfg[c].type_counts[u] > 0) {
+          if (t < 0) t = u;
+          ++used;
+          n = cfg[c].type_counts[u];
+        }
+      if (used != 1 || n <= 0)
+        return set_error(GP_INVALID, "solve_milp on the GPU requires type-pure configs using >= 1 device");
+      key.push_back({(long long)t * 1000000 + n, c});
+    }
+    std::stable_sort(key.begin(), key.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (size_t i = 0; i < key.size();) {
+      size_t j = i;
+      Group G{(int)(key[i].first / 1000000), (int)(key[i].first % 1000000), 0.0, (int)members.size(), 0};
+      double hmax = cfg[key[i].second].throughput;
+      while (j < key.size() && key[j].first == key[i].first) {
+        members.push_back(key[j].second);
+        const double h = cfg[key[j].second].throughput;
+        hmax = hmax < h ? h : hmax;
+        ++j;
+      }
+      G.hmax = hmax;
+      G.count = (int)(j - i);
+      groups.push_back(G);
+      i = j;
+    }
+  }
+  const int ng = (int)groups.size();
+  std::vector<double> hs(nc);
+  for (int c = 0; c < nc; ++c) hs[c] = cfg[c].throughput;
+  // device buffers
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+  add(sizeof(gp_config) * nc);
+  add(sizeof(Group) * ng);
+  add(sizeof(int) * nc);
+  add(sizeof(double) * nc);
+  add(sizeof(int) * levels);
+  add(sizeof(long long) * (levels + 1));
+  add(sizeof(int) * levels);
+  add(sizeof(unsigned) * states);
+  add(sizeof(double) * states);
+  add(sizeof(int) * states);
+  add(sizeof(int) * nc);
+  add(sizeof(gp_rollout_entry) * nc);
+  add(sizeof(MilpOut));
+  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaRollout));
+  if (!base) return GP_CUDA_ERROR;
+  char* p = base;
+  gp_config* d_cfg = carve2<gp_config>(p, nc);
+  Group* d_groups = carve2<Group>(p, ng);
+  int* d_members = carve2<int>(p, nc);
+  double* d_h = carve2<double>(p, nc);
+  int* d_hist = carve2<int>(p, levels);
+  long long* d_off = carve2<long long>(p, levels + 1);
+  int* d_cursor = carve2<int>(p, levels);
+  unsigned* d_order = carve2<unsigned>(p, states);
+  double* d_best = carve2<double>(p, states);
+  int* d_choice = carve2<int>(p, states);
+  int* d_counts = carve2<int>(p, nc);
+  gp_rollout_entry* d_entries = carve2<gp_rollout_entry>(p, nc);
+  MilpOut* d_mo = carve2<MilpOut>(p, 1);
+  const size_t in_bytes = (size_t)((char*)(d_h + nc) - (char*)d_cfg);
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(MilpOut) + sizeof(gp_rollout_entry) * nc + 256)));
+  if (!hp) return GP_CUDA_ERROR;
+  std::memcpy(hp, cfg, sizeof(gp_config) * nc);
+  std::memcpy(hp + ((char*)d_groups - (char*)d_cfg), groups.data(), sizeof(Group) * ng);
+  std::memcpy(hp + ((char*)d_members - (char*)d_cfg), members.data(), sizeof(int) * nc);
+  std::memcpy(hp + ((char*)d_h - (char*)d_cfg), hs.data(), sizeof(double) * nc);
+  GP_CUDA(cudaMemcpyAsync(d_cfg, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)in_bytes;
+  GP_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int) * levels, ctx->stream));
+  const int sweep_blocks = (int)std::min<long long>((states + 255) / 256, (long long)ctx->num_sms * 16);
+  k4_level_hist<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_hist);
+  k4_level_scan<<<1, 32, 0, ctx->stream>>>(d_hist, levels, d_off, d_cursor);
+  k4_level_scatter<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_off, d_cursor, d_order);
+  ctx->launches += 3;
+  // cooperative persistent DP over levels
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_dp_levels, 256, 0);
+    occ = std::max(1, occ);
+  }
+  int dp_blocks = (int)std::min<long long>((long long)ctx->num_sms * occ, (states + 255) / 256);
+  dp_blocks = std::max(1, dp_blocks);
+  void* args[] = {&d, &d_groups, (void*)&ng, &d_members, &d_h, &d_off, &d_order, &d_best, &d_choice};
+  int ng_arg = ng;
+  args[2] = &ng_arg;
+  GP_CUDA(cudaLaunchCooperativeKernel((void*)k4_dp_levels, dp_blocks, 256, args, 0, ctx->stream));
+  k4_backtrack<<<1, 32, 0, ctx->stream>>>(d, d_cfg, nc, d_best, d_choice, B, len, d_counts, d_entries, d_mo);
+  ctx->launches += 2;
+  GP_CUDA(cudaGetLastError());
+  MilpOut* ho = reinterpret_cast<MilpOut*>(hp);
+  gp_rollout_entry* he = reinterpret_cast<gp_rollout_entry*>(hp + 256);
+  GP_CUDA(cudaMemcpyAsync(ho, d_mo, sizeof(MilpOut), cudaMemcpyDeviceToHost, ctx->stream));
+  GP_CUDA(cudaMemcpyAsync(he, d_entries, sizeof(gp_rollout_entry) * nc, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += (long long)(sizeof(MilpOut) + sizeof(gp_rollout_entry) * nc);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  out->aggregate = ho->aggregate;
+  if (ho->n_entries < 0) return set_error(GP_INFEASIBLE, "rollout capacity cannot host any replica");
+  out->makespan = ho->makespan;
+  out->n_entries = ho->n_entries;
+  std::memcpy(entries, he, sizeof(gp_rollout_entry) * ho->n_entries);
+  return GP_OK;
+}
+
+int weight_sync(gp_ctx* ctx, const int32_t* train, int nt, const int32_t* roll, int nr,
+                const int32_t* etype, const int32_t* erep, int ne, int window, double* out) {
+  for (int i = 0; i < nt; ++i)
+    if (train[i] < 0 || train[i] >= ctx->N) return set_error(GP_INVALID, "unknown device id");
+  for (int i = 0; i < nr; ++i)
+    if (roll[i] < 0 || roll[i] >= ctx->N) return set_error(GP_INVALID, "unknown device id");
+  const int T = ctx->T;
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+  add(sizeof(int) * (nt + 1));
+  add(sizeof(int) * (nr + 1));
+  add(sizeof(int) * (ne + 1));
+  add(sizeof(int) * (ne + 1));
+  add(sizeof(double) * T);
+  add(sizeof(double));
+  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaRollout));
+  if (!base) return GP_CUDA_ERROR;
+  char* p = base;
+  int* d_t = carve2<int>(p, nt + 1);
+  int* d_r = carve2<int>(p, nr + 1);
+  int* d_et = carve2<int>(p, ne + 1);
+  int* d_er = carve2<int>(p, ne + 1);
+  double* d_tm = carve2<double>(p, T);
+  double* d_out = carve2<double>(p, 1);
+  const size_t in_bytes = (size_t)((char*)(d_er + ne + 1) - (char*)d_t);
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, (size_t)64)));
+  if (!hp) return GP_CUDA_ERROR;
+  std::memcpy(hp, train, sizeof(int) * nt);
+  std::memcpy(hp + ((char*)d_r - (char*)d_t), roll, sizeof(int) * nr);
+  if (ne) std::memcpy(hp + ((char*)d_et - (char*)d_t), etype, sizeof(int) * ne);
+  if (ne) std::memcpy(hp + ((char*)d_er - (char*)d_t), erep, sizeof(int) * ne);
+  GP_CUDA(cudaMemcpyAsync(d_t, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)in_bytes;
+  k6_type_maxlink<<<T, 256, 0, ctx->stream>>>(d_t, nt, d_r, nr, ctx->d_type, ctx->d_links, ctx->N, d_tm);
+  k6_combine<<<1, 1, 0, ctx->stream>>>(d_tm, d_et, d_er, ne, window, ctx->sc.mbi, ctx->sc.sync_latency,
+                                       d_out);
+  ctx->launches += 2;
+  GP_CUDA(cudaGetLastError());
+  double* ho = reinterpret_cast<double*>(hp);
+  GP_CUDA(cudaMemcpyAsync(ho, d_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += sizeof(double);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  *out = *ho;
+  return GP_OK;
+}
+
+}  // namespace gp

@@ -1022,7 +1022,7 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
   add(sizeof(SufEnt) * (h.choices.size() + 1));
   add(sizeof(Best) * P.max_blocks);
   add(sizeof(TrainOut));
-  char* base = static_cast<char*>(ctx_scratch(ctx, bytes));
+  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaTrain));
   if (!base) return GP_CUDA_ERROR;
   char* p = base;
   P.d_ordered = carve<int>(p, n);

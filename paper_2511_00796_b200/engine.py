@@ -204,3 +204,41 @@ class Engine:
         v = C.c_double()
         _check(lib().gp_fp64_peak(self._h, C.byref(v)))
         return v.value
+
+    # ---- rollout side ---------------------------------------------------------
+    def enumerate_configs(self, rollout_set, opts=None, cap: int = 4096):
+        """enumerate_configs (inc/rollout_milp.hpp:22-25) -> list of gp_config."""
+        ids = _ids(rollout_set)
+        out = (abi.gp_config * cap)()
+        n = C.c_int32()
+        _check(lib().gp_enumerate_configs(self._h, ids.ctypes.data_as(abi.i32p), len(ids),
+                                          C.byref(opts or abi.default_rollout_opts()), out, cap,
+                                          C.byref(n)))
+        return [out[i] for i in range(n.value)]
+
+    def rollout_capacities(self, rollout_set):
+        ids = _ids(rollout_set)
+        caps = np.zeros(len(self.problem.cluster.type_names), dtype=np.int32)
+        _check(lib().gp_rollout_capacities(self._h, ids.ctypes.data_as(abi.i32p), len(ids),
+                                           caps.ctypes.data_as(abi.i32p)))
+        return caps.tolist()
+
+    def solve_milp(self, configs, caps, total_rollouts: float, mean_len: float):
+        """solve_milp (inc/rollout_milp.hpp:35-37) -> (gp_rollout_result, [gp_rollout_entry])."""
+        arr = (abi.gp_config * max(len(configs), 1))(*configs)
+        caps = _ids(caps)
+        res = abi.gp_rollout_result()
+        ent = (abi.gp_rollout_entry * max(len(configs), 1))()
+        _check(lib().gp_solve_milp(self._h, arr, len(configs), caps.ctypes.data_as(abi.i32p),
+                                   len(caps), total_rollouts, mean_len, C.byref(res), ent))
+        return res, [ent[i] for i in range(res.n_entries)]
+
+    def weight_sync_cost(self, train, rollout, entry_types, entry_replicas, window: int) -> float:
+        t, r = _ids(train), _ids(rollout)
+        et, er = _ids(entry_types), _ids(entry_replicas)
+        out = C.c_double()
+        _check(lib().gp_weight_sync_cost(self._h, t.ctypes.data_as(abi.i32p), len(t),
+                                         r.ctypes.data_as(abi.i32p), len(r),
+                                         et.ctypes.data_as(abi.i32p), er.ctypes.data_as(abi.i32p),
+                                         len(et), window, C.byref(out)))
+        return out.value

@@ -16,7 +16,7 @@ sys.path.insert(0, os.path.dirname(HERE))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 from common import CONFIGS, ETA, problem, random_train_sets, type_prefix_sets  # noqa: E402
-from oracles import Oracle, Ref  # noqa: E402
+from oracles import Oracle, Ref, RefError  # noqa: E402
 
 REF_PLAN = "/root/reference/proj/out/desk/plan.json"
 
@@ -28,7 +28,7 @@ def dump(name, obj):
 
 
 def main():
-    shutil.copy(REF_PLAN, os.path.join(HERE, "desk_plan.json"))
+    shutil.copyfile(REF_PLAN, os.path.join(HERE, "desk_plan.json"))
     # ---- full schedules (plan_to_json + trace)
     sched = {}
     for name, etas in (("c1_desk_mixed", [1, -1]), ("c2_16gpu", [-1]), ("c3_64gpu", [1, 2, 3, 4])):
@@ -72,6 +72,36 @@ def main():
                 blocks.append(key)
         cand[json.dumps(ids)] = {"block_lists": blocks, "candidates": lst}
     dump("train_candidates.json", cand)
+    # ---- rollout side: enumerate_configs + solve_milp + weight_sync_cost on sampled rollout sets
+    ro = {}
+    for name in CONFIGS:
+        p = problem(name)
+        ref = Ref(p)
+        n = p.cluster.n
+        cases = []
+        for train in random_train_sets(n, 30, seed=500 + n):
+            roll = sorted(set(range(n)) - set(train))
+            window = ETA[name] + 1
+            cfg = ref.enumerate_configs(roll)
+            states = 1
+            for c in cfg["capacities"]:
+                states *= c + 1
+            if states > 400_000:
+                continue
+            case = {"train": train, "rollout": roll, "window": window, "configs": cfg["configs"],
+                    "capacities": cfg["capacities"]}
+            B = float(p.workload.batch_rollouts * window)
+            try:
+                plan = ref.solve_milp(cfg["configs"], cfg["capacities"], B, p.workload.mean_len)
+                plan.pop("seconds")
+                case["milp"] = plan
+                case["weight_sync"] = ref.weight_sync(train, roll, window, plan)
+            except RefError as e:
+                case["milp_error"] = e.code
+            cases.append(case)
+        ro[name] = cases
+        print(name, len(cases), "rollout cases")
+    dump("rollout.json", ro)
 
 
 if __name__ == "__main__":

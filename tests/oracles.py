@@ -208,3 +208,46 @@ def train_result_dict(res, devs):
         d["stages"] = [{"devices": devs[s.first:s.first + s.count].tolist(), "tp": s.tp, "dp": s.dp,
                         "layers": s.layers} for s in res.stage[:res.n_stages]]
     return d
+
+
+def config_dict(c, n_types):
+    return {"type_counts": list(c.type_counts[:n_types]), "tp_per_stage": list(c.tp[:c.n_stages]),
+            "throughput": c.throughput}
+
+
+def oracle_configs(orc, ids, max_stages=4):
+    import ctypes as C
+    ids = _ids(ids)
+    out = (abi.gp_config * 4096)()
+    n = C.c_int32()
+    rc = orc.lib.or_enumerate_configs(C.byref(orc.c), C.byref(orc.w), C.byref(orc.k),
+                                      ids.ctypes.data_as(abi.i32p), len(ids),
+                                      C.byref(abi.gp_rollout_opts(max_stages)), out, 4096, C.byref(n))
+    if rc:
+        orc.err(rc)
+    return [out[i] for i in range(n.value)]
+
+
+def oracle_milp(orc, configs, caps, B, mean_len):
+    """Returns (rc, result, entries) of the C restatement of solve_milp."""
+    import ctypes as C
+    arr = (abi.gp_config * max(len(configs), 1))(*configs)
+    caps = _ids(caps)
+    res = abi.gp_rollout_result()
+    ent = (abi.gp_rollout_entry * max(len(configs), 1))()
+    rc = orc.lib.or_solve_milp(arr, len(configs), caps.ctypes.data_as(abi.i32p), len(caps), B,
+                               mean_len, C.byref(res), ent)
+    return rc, res, [ent[i] for i in range(res.n_entries)] if rc == 0 else []
+
+
+def oracle_weight_sync(orc, train, roll, etypes, ereps, window):
+    import ctypes as C
+    t, r, et, er = _ids(train), _ids(roll), _ids(etypes), _ids(ereps)
+    v = C.c_double()
+    rc = orc.lib.or_weight_sync_cost(C.byref(orc.c), C.byref(orc.w), C.byref(orc.k),
+                                     t.ctypes.data_as(abi.i32p), len(t), r.ctypes.data_as(abi.i32p),
+                                     len(r), et.ctypes.data_as(abi.i32p), er.ctypes.data_as(abi.i32p),
+                                     len(et), window, C.byref(v))
+    if rc:
+        orc.err(rc)
+    return v.value

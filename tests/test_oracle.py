@@ -75,3 +75,31 @@ def test_ranges_partition_the_space():
     assert sum(p["feasible"] for p in parts) == full["feasible"]
     win = min((p for p in parts if p["found"]), key=lambda p: (p["cost"], p["rank"]))
     assert (win["cost"], win["rank"], win["stages"]) == (full["cost"], full["rank"], full["stages"])
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_rollout_side_matches_reference(name):
+    """enumerate_configs / solve_milp / weight_sync_cost restated in C == reference."""
+    from oracles import config_dict, oracle_configs, oracle_milp, oracle_weight_sync
+    p = problem(name)
+    orc = Oracle(p)
+    T = len(p.cluster.type_names)
+    for case in golden("rollout.json")[name]:
+        cfgs = oracle_configs(orc, case["rollout"])
+        got = [config_dict(c, T) for c in cfgs]
+        want = [{k: c[k] for k in ("type_counts", "tp_per_stage", "throughput")} for c in case["configs"]]
+        assert got == want
+        B = float(p.workload.batch_rollouts * case["window"])
+        rc, res, ents = oracle_milp(orc, cfgs, case["capacities"], B, p.workload.mean_len)
+        if "milp_error" in case:
+            assert rc != 0
+            continue
+        m = case["milp"]
+        assert rc == 0
+        assert res.makespan == m["makespan"]
+        assert [(e.replicas, e.workload) for e in ents] == [(e["replicas"], e["workload"]) for e in m["entries"]]
+        assert [config_dict(cfgs[e.config], T) for e in ents] == \
+            [{k: e[k] for k in ("type_counts", "tp_per_stage", "throughput")} for e in m["entries"]]
+        et = [next(t for t, v in enumerate(e["type_counts"]) if v > 0) for e in m["entries"]]
+        er = [e["replicas"] for e in m["entries"]]
+        assert oracle_weight_sync(orc, case["train"], case["rollout"], et, er, case["window"]) == case["weight_sync"]
