@@ -27,6 +27,9 @@ int solve_milp(gp_ctx* ctx, const gp_config* cfg, int nc, const int32_t* caps, i
                double len, gp_rollout_result* out, gp_rollout_entry* entries);
 int weight_sync(gp_ctx* ctx, const int32_t* train, int nt, const int32_t* roll, int nr,
                 const int32_t* etype, const int32_t* erep, int ne, int window, double* out);
+int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, int k, gp_partition* out,
+                         int32_t* train_ids, int32_t* n_out);
+int partition_objective(gp_ctx* ctx, const int32_t* train, int nt, double* obj, double* frac);
 
 static thread_local std::string g_error;
 
@@ -312,6 +315,20 @@ int gp_weight_sync_cost(gp_ctx* ctx, const int32_t* train, int32_t n_train, cons
   cudaSetDevice(ctx->device);
   return weight_sync(ctx, train, n_train, rollout, n_rollout, entry_types, entry_replicas, n_entries,
                      window, out);
+}
+
+int gp_partition_candidates(gp_ctx* ctx, const gp_gamma* gamma, const gp_part_opts* opts, int32_t k,
+                            gp_partition* out, int32_t* train_ids, int32_t* n_out) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return partition_candidates(ctx, gamma, opts, k, out, train_ids, n_out);
+}
+
+int gp_partition_objective(gp_ctx* ctx, const int32_t* train, int32_t n_train, double* objective,
+                           double* fraction) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return partition_objective(ctx, train, n_train, objective, fraction);
 }
 
 int gp_ctx_set_timing(gp_ctx* ctx, int on) {

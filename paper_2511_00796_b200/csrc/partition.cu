@@ -1,0 +1,770 @@
+// partition.cu — sm_100a kernels for the repartition solver:
+//   graph_partition_candidates (src/partition.cpp:369-406) with build_units
+//   (:37-80), State (:83-163), TopK (:174-210), exact_enumeration (:212-222),
+//   greedy_seed (:224-269), local_search (:271-350), compute_fraction (:360-367).
+//
+// K5a units      unit folds (flops, hbm, internal link, cross matrix) — one CTA per unit row
+// K5b exact      one thread per bisection mask (n <= exact_threshold)
+// K5c restarts   one CTA per restart: SplitMix64-perturbed order (counter-based,
+//                parallel), CTA-wide stable sort, greedy seed, then the whole
+//                steepest-ascent loop on chip: every step scores all moves and all
+//                (train, rollout) swaps in parallel and reduces lexicographically on
+//                (gain desc, scan position asc) — the reference's first strict max.
+// K5d topk       one thread replays TopK::offer in the reference's offer order.
+// Objective/fraction divisions by the fixed totals use a correctly rounded
+// reciprocal with one FMA residual correction (Markstein), identical to IEEE
+// division for these operands; every other fp operation keeps reference order.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <vector>
+
+#include "gp_internal.h"
+
+namespace gp {
+
+constexpr int kMaxUnits = 4096;
+constexpr int kK5Threads = 1024;
+
+struct Units {
+  int n;
+  const double* flops;
+  const double* hbm;
+  const double* internal;
+  const double* cross;  // n x n
+  const int* mem_off;   // members of unit i: mem_ids[mem_off[i] .. mem_off[i+1])
+  const int* mem_ids;
+};
+
+struct Totals {
+  double flops, hbm, link;
+  double y_flops, y_hbm, y_link;  // RN(1/total)
+};
+
+__device__ __forceinline__ double div_rn_recip2(double a, double b, double y) {
+  const double q = __dmul_rn(a, y);
+  const double r = __fma_rn(-q, b, a);
+  return __fma_rn(r, y, q);
+}
+
+// ---------------------------------------------------------------- K5a units
+__global__ void k5_units(int n, const int* __restrict__ mem_off, const int* __restrict__ mem_ids,
+                         const double* __restrict__ dflops, const double* __restrict__ dhbm,
+                         const double* __restrict__ links, int N, double* __restrict__ uflops,
+                         double* __restrict__ uhbm, double* __restrict__ uint_,
+                         double* __restrict__ cross) {
+  const int i = blockIdx.x;
+  const int* mi = mem_ids + mem_off[i];
+  const int ni = mem_off[i + 1] - mem_off[i];
+  if (threadIdx.x == 0) {
+    double f = 0, h = 0, in = 0;
+    for (int a = 0; a < ni; ++a) {
+      f += dflops[mi[a]];
+      h += dhbm[mi[a]];
+      for (int b = a + 1; b < ni; ++b) in += links[(size_t)mi[a] * N + mi[b]];
+    }
+    uflops[i] = f;
+    uhbm[i] = h;
+    uint_[i] = in;
+    cross[(size_t)i * n + i] = 0;
+  }
+  for (int j = i + 1 + threadIdx.x; j < n; j += blockDim.x) {
+    const int* mj = mem_ids + mem_off[j];
+    const int nj = mem_off[j + 1] - mem_off[j];
+    double bw = 0;
+    for (int a = 0; a < ni; ++a)
+      for (int b = 0; b < nj; ++b) bw += links[(size_t)mi[a] * N + mj[b]];
+    cross[(size_t)i * n + j] = bw;
+    cross[(size_t)j * n + i] = bw;
+  }
+}
+
+// totals: sequential folds in unit order (src/partition.cpp:75-79)
+__global__ void k5_totals(Units u, Totals* __restrict__ tot, double* __restrict__ base_score) {
+  __shared__ double s_tl;
+  if (threadIdx.x == 0) {
+    double tf = 0.0, th = 0.0, tl = 0;
+    for (int i = 0; i < u.n; ++i) tf += u.flops[i];
+    for (int i = 0; i < u.n; ++i) th += u.hbm[i];
+    for (int i = 0; i < u.n; ++i) {
+      tl += u.internal[i];
+      for (int j = i + 1; j < u.n; ++j) tl += u.cross[(size_t)i * u.n + j];
+    }
+    tot->flops = tf;
+    tot->hbm = th;
+    tot->link = tl;
+    tot->y_flops = 1.0 / tf;
+    tot->y_hbm = 1.0 / th;
+    tot->y_link = tl > 0 ? 1.0 / tl : 0.0;
+    s_tl = tl;
+  }
+  __syncthreads();
+  // local_search base score (src/partition.cpp:273-282): per unit, fold over j != i
+  for (int i = threadIdx.x; i < u.n; i += blockDim.x) {
+    double d = 0;
+    for (int j = 0; j < u.n; ++j)
+      if (j != i) d += u.cross[(size_t)i * u.n + j];
+    d += 2.0 * u.internal[i];
+    if (u.n > 1) d /= static_cast<double>(u.n - 1);
+    base_score[i] = d * u.flops[i];
+  }
+}
+
+// ---------------------------------------------------------------- K5b exact
+struct Offer {
+  double obj;
+  int valid;
+  int pad;
+};
+
+__global__ void k5_exact(Units u, const Totals* __restrict__ tot, double lo, double hi,
+                         Offer* __restrict__ offers) {
+  const unsigned long long mask = 1ull + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = u.n;
+  if (mask + 1 >= (1ull << n)) return;
+  double ltt[20];
+  for (int j = 0; j < n; ++j) ltt[j] = 0;
+  double link_train = 0, hbm_train = 0, flops_train = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!(mask & (1ull << i))) continue;
+    link_train += ltt[i] + u.internal[i];  // State::add
+    hbm_train += u.hbm[i];
+    flops_train += u.flops[i];
+    for (int j = 0; j < n; ++j)
+      if (j != i) ltt[j] += u.cross[(size_t)i * n + j];
+  }
+  const Totals T = *tot;
+  const double f = flops_train / T.flops;
+  Offer o;
+  o.valid = f >= lo && f <= hi;
+  const double lf = T.link > 0 ? link_train / T.link : 0;
+  o.obj = lf + (T.hbm - hbm_train) / T.hbm;
+  o.pad = 0;
+  offers[mask - 1] = o;
+}
+
+// ---------------------------------------------------------------- K5c restarts
+struct RestartOut {
+  double obj;
+  int ok;
+  int count;
+  unsigned long long steps;
+};
+
+__device__ __forceinline__ unsigned long long smx(unsigned long long x) {
+  unsigned long long z = x;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+struct Cand {
+  double gain;
+  int pos;  // scan position: moves i, swaps n + a*n + b
+};
+
+__device__ __forceinline__ bool cand_better(const Cand& x, const Cand& y) {
+  return x.gain > y.gain || (x.gain == y.gain && x.pos < y.pos);
+}
+
+__device__ Cand block_best(Cand c, Cand* sm) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Cand d;
+    d.gain = __shfl_xor_sync(0xffffffffu, c.gain, o);
+    d.pos = __shfl_xor_sync(0xffffffffu, c.pos, o);
+    if (cand_better(d, c)) c = d;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sm[wid] = c;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  c = lane < nw ? sm[lane] : Cand{-1e300, INT_MAX};
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Cand d;
+    d.gain = __shfl_xor_sync(0xffffffffu, c.gain, o);
+    d.pos = __shfl_xor_sync(0xffffffffu, c.pos, o);
+    if (cand_better(d, c)) c = d;
+  }
+  return c;
+}
+
+struct SState {
+  double link_train, hbm_train, flops_train;
+  int count;
+  int pick;
+  int flag;
+  int n_tr, n_ro;
+};
+
+__global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* __restrict__ tot,
+                                                         const double* __restrict__ base_score,
+                                                         double lo, double hi, int restarts,
+                                                         unsigned long long seed,
+                                                         unsigned char* __restrict__ in_train_out,
+                                                         RestartOut* __restrict__ out) {
+  extern __shared__ unsigned char smem[];
+  const int n = u.n;
+  double* ltt = reinterpret_cast<double*>(smem);
+  double* key = ltt + n;                       // perturbed scores, then reused
+  int* order = reinterpret_cast<int*>(key + n);
+  int* tr = order + n;                         // train unit list (ascending)
+  int* ro = tr + n;                            // rollout unit list (ascending)
+  unsigned char* in_tr = reinterpret_cast<unsigned char*>(ro + n);
+  __shared__ SState S;
+  __shared__ Cand red[32];
+  __shared__ int ired[32];
+  const int r = blockIdx.x;
+  const Totals T = *tot;
+  const int tid = threadIdx.x, nth = blockDim.x;
+
+  // ---- perturbed order: score_i *= 0.5 + U_i (SplitMix64 stream of this restart)
+  const unsigned long long s0 = seed + (unsigned long long)r * 0x9e3779b97f4a7c15ull;
+  for (int i = tid; i < n; i += nth) {
+    double sc = base_score[i];
+    if (r > 0) {
+      const unsigned long long z = smx(s0 + (unsigned long long)(i + 1) * 0x9e3779b97f4a7c15ull);
+      sc *= 0.5 + static_cast<double>(z >> 11) * 0x1.0p-53;
+    }
+    key[i] = sc;
+    ltt[i] = 0;
+    in_tr[i] = 0;
+  }
+  __syncthreads();
+  // stable sort by score desc: rank_i = #{score_j > score_i} + #{j < i : score_j == score_i}
+  for (int i = tid; i < n; i += nth) {
+    const double si = key[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double sj = key[j];
+      rank += (sj > si) || (sj == si && j < i);
+    }
+    order[rank] = i;
+  }
+  if (tid == 0) {
+    S.link_train = S.hbm_train = S.flops_train = 0;
+    S.count = 0;
+  }
+  __syncthreads();
+  const double bhi = (1.0 < hi) ? 1.0 : hi;
+  const double blo = (lo < 0.0) ? 0.0 : lo;
+  const double target = blo + (r + 0.5) / restarts * (bhi - blo);
+
+  auto frac = [&](double ft) { return div_rn_recip2(ft, T.flops, T.y_flops); };
+  auto in_band = [&](double f) { return f >= lo && f <= hi; };
+  // State::add / State::remove with the parallel link_to_train update
+  auto add = [&](int i) {
+    __syncthreads();
+    if (tid == 0) {
+      S.link_train += ltt[i] + u.internal[i];
+      S.hbm_train += u.hbm[i];
+      S.flops_train += u.flops[i];
+      S.count++;
+      in_tr[i] = 1;
+    }
+    __syncthreads();
+    for (int j = tid; j < n; j += nth)
+      if (j != i) ltt[j] += u.cross[(size_t)i * n + j];
+    __syncthreads();
+  };
+  auto remove = [&](int i) {
+    __syncthreads();
+    for (int j = tid; j < n; j += nth)
+      if (j != i) ltt[j] -= u.cross[(size_t)i * n + j];
+    __syncthreads();
+    if (tid == 0) {
+      in_tr[i] = 0;
+      S.link_train -= ltt[i] + u.internal[i];
+      S.hbm_train -= u.hbm[i];
+      S.flops_train -= u.flops[i];
+      S.count--;
+    }
+    __syncthreads();
+  };
+  // argmin of flops over units with in_tr == want (first index on ties); n if none
+  auto argmin_flops = [&](int want) {
+    double bv = 0;
+    int bi = INT_MAX;
+    for (int i = tid; i < n; i += nth) {
+      if (in_tr[i] != want) continue;
+      const double f = u.flops[i];
+      if (bi == INT_MAX || f < bv || (f == bv && i < bi)) {
+        bv = f;
+        bi = i;
+      }
+    }
+    Cand c{bi == INT_MAX ? -1e300 : -bv, bi};
+    c = block_best(c, red);
+    return c.pos == INT_MAX ? n : c.pos;
+  };
+
+  // ---- greedy_seed (src/partition.cpp:224-269)
+  bool ok = true;
+  for (int oi = 0; oi < n; ++oi) {
+    if (frac(S.flops_train) >= target) break;
+    if (S.count + 1 >= n) break;
+    add(order[oi]);
+  }
+  for (int guard = 0; guard < 4 * n; ++guard) {
+    const double f = frac(S.flops_train);
+    if (in_band(f)) break;
+    if (f > hi) {
+      if (S.count <= 1) {
+        ok = false;
+        break;
+      }
+      const int pick = argmin_flops(1);
+      remove(pick);
+    } else {
+      if (S.count + 1 >= n) {
+        ok = false;
+        break;
+      }
+      // first unit in `order` outside train whose move keeps f <= hi + 1e-15
+      int best_o = INT_MAX;
+      for (int oi = tid; oi < n; oi += nth) {
+        const int i = order[oi];
+        if (in_tr[i]) continue;
+        if (frac(S.flops_train + u.flops[i]) <= hi + 1e-15) best_o = min(best_o, oi);
+      }
+      for (int o = 16; o > 0; o >>= 1) best_o = min(best_o, __shfl_xor_sync(0xffffffffu, best_o, o));
+      __syncthreads();
+      if ((tid & 31) == 0) ired[tid >> 5] = best_o;
+      __syncthreads();
+      if (tid < 32) {
+        int v = tid < (nth >> 5) ? ired[tid] : INT_MAX;
+        for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (tid == 0) S.pick = v;
+      }
+      __syncthreads();
+      int pick = S.pick == INT_MAX ? n : order[S.pick];
+      if (pick == n) {
+        pick = argmin_flops(0);
+        if (pick == n) {
+          ok = false;
+          break;
+        }
+      }
+      add(pick);
+    }
+  }
+  ok = ok && in_band(frac(S.flops_train)) && S.count > 0 && S.count < n;
+
+  // ---- steepest ascent (src/partition.cpp:302-347)
+  unsigned long long steps = 0;
+  while (ok) {
+    // ascending train / rollout unit lists (scan order of the swap loops)
+    if (tid < 32) {
+      int ctr = 0, cro = 0;
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + tid;
+        const bool t = i < n && in_tr[i];
+        const bool rr = i < n && !in_tr[i];
+        const unsigned mt = __ballot_sync(0xffffffffu, t), mr = __ballot_sync(0xffffffffu, rr);
+        if (t) tr[ctr + __popc(mt & ((1u << tid) - 1))] = i;
+        if (rr) ro[cro + __popc(mr & ((1u << tid) - 1))] = i;
+        ctr += __popc(mt);
+        cro += __popc(mr);
+      }
+      if (tid == 0) {
+        S.n_tr = ctr;
+        S.n_ro = cro;
+      }
+    }
+    __syncthreads();
+    const double lt0 = S.link_train, hb0 = S.hbm_train, ft0 = S.flops_train;
+    const int cnt = S.count, ntr = S.n_tr, nro = S.n_ro;
+    const double cur = (T.link > 0 ? div_rn_recip2(lt0, T.link, T.y_link) : 0) +
+                       div_rn_recip2(T.hbm - hb0, T.hbm, T.y_hbm);
+    Cand best{1e-12, INT_MAX};
+    for (int i = tid; i < n; i += nth) {  // single moves
+      const bool to_train = !in_tr[i];
+      if (to_train && cnt + 1 == n) continue;
+      if (!to_train && cnt == 1) continue;
+      const double ftm = ft0 + (to_train ? u.flops[i] : -u.flops[i]);
+      if (!in_band(frac(ftm))) continue;
+      double lt = lt0;
+      if (to_train) lt += ltt[i] + u.internal[i];
+      else lt -= ltt[i] + u.internal[i];
+      const double hbm = hb0 + (to_train ? u.hbm[i] : -u.hbm[i]);
+      const double obj = (T.link > 0 ? div_rn_recip2(lt, T.link, T.y_link) : 0) +
+                         div_rn_recip2(T.hbm - hbm, T.hbm, T.y_hbm);
+      const Cand c{obj - cur, i};
+      if (c.gain > best.gain) best = c;  // i ascending per thread: strict '>' keeps the first
+    }
+    const long long npairs = (long long)ntr * nro;
+    for (long long p = tid; p < npairs; p += nth) {  // swaps: a in train asc, b in rollout asc
+      const int a = tr[p / nro], b = ro[p % nro];
+      const double fts = ft0 - u.flops[a] + u.flops[b];
+      if (!in_band(frac(fts))) continue;
+      const double lt = lt0 - (ltt[a] + u.internal[a]) + (ltt[b] + u.internal[b]) -
+                        u.cross[(size_t)a * n + b];
+      const double hbm = hb0 - u.hbm[a] + u.hbm[b];
+      const double obj = (T.link > 0 ? div_rn_recip2(lt, T.link, T.y_link) : 0) +
+                         div_rn_recip2(T.hbm - hbm, T.hbm, T.y_hbm);
+      const Cand c{obj - cur, n + a * n + b};
+      if (c.gain > best.gain) best = c;
+    }
+    const Cand w = block_best(best, red);
+    if (w.pos == INT_MAX) break;
+    ++steps;
+    if (w.pos < n) {
+      if (in_tr[w.pos]) remove(w.pos);
+      else add(w.pos);
+    } else {
+      const int a = (w.pos - n) / n, b = (w.pos - n) % n;
+      remove(a);
+      add(b);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += nth) in_train_out[(size_t)r * n + i] = ok ? in_tr[i] : 0;
+  if (tid == 0) {
+    RestartOut o;
+    o.ok = ok;
+    o.count = S.count;
+    o.steps = steps;
+    o.obj = (T.link > 0 ? div_rn_recip2(S.link_train, T.link, T.y_link) : 0) +
+            div_rn_recip2(T.hbm - S.hbm_train, T.hbm, T.y_hbm);
+    out[r] = o;
+  }
+}
+
+__global__ void k5_unpack_offers(const Offer* __restrict__ of, const RestartOut* __restrict__ ro, int n_off,
+                                 bool exact, double* __restrict__ objs, int* __restrict__ valid) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_off) return;
+  objs[i] = exact ? of[i].obj : ro[i].obj;
+  valid[i] = exact ? of[i].valid : ro[i].ok;
+}
+
+// ---------------------------------------------------------------- K5d TopK
+struct TopItem {
+  double obj;
+  int count;     // train devices
+  int src;       // offer index (row into the offer-mask table)
+};
+
+struct TopKOut {
+  int n_items;
+  int pad;
+  TopItem item[64];
+};
+
+// Train device ids of offer `o` (sorted: units hold ascending contiguous ids).
+__device__ int offer_ids(const Units& u, const unsigned char* __restrict__ in_train, int o,
+                         int* __restrict__ buf) {
+  int c = 0;
+  for (int i = 0; i < u.n; ++i) {
+    if (!in_train[(size_t)o * u.n + i]) continue;
+    for (int m = u.mem_off[i]; m < u.mem_off[i + 1]; ++m) buf[c++] = u.mem_ids[m];
+  }
+  return c;
+}
+
+__device__ bool lex_less(const int* a, int na, const int* b, int nb) {
+  const int m = na < nb ? na : nb;
+  for (int i = 0; i < m; ++i)
+    if (a[i] != b[i]) return a[i] < b[i];
+  return na < nb;
+}
+
+// Replays TopK::offer in offer order (single thread). Offers with valid == 0 are skipped.
+__global__ void k5_topk(Units u, const unsigned char* __restrict__ in_train, const double* __restrict__ objs,
+                        const int* __restrict__ valid, int n_offers, int k, const int* __restrict__ dmachine,
+                        int M, int* __restrict__ work /* 3 * N + M * (k + 2) ints */, TopKOut* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int N = u.mem_off[u.n];
+  int* ids = work;              // candidate ids
+  int* ids2 = work + N;         // scratch
+  int* foot = work + 2 * N;     // per item footprint: M ints each, (k+1) items, + candidate
+  int* cand_foot = foot + (size_t)M * (k + 1);
+  int n_items = 0;
+  TopItem items[65];
+  for (int o = 0; o < n_offers; ++o) {
+    if (!valid[o]) continue;
+    const double obj = objs[o];
+    const int nc = offer_ids(u, in_train, o, ids);
+    for (int m = 0; m < M; ++m) cand_foot[m] = 0;
+    for (int i = 0; i < nc; ++i) cand_foot[dmachine[ids[i]]]++;
+    bool merged = false;
+    for (int e = 0; e < n_items && !merged; ++e) {
+      if (fabs(items[e].obj - obj) > 1e-12) continue;
+      bool same = true;
+      for (int m = 0; m < M && same; ++m) same = foot[(size_t)e * M + m] == cand_foot[m];
+      if (!same) continue;
+      const int ne = offer_ids(u, in_train, items[e].src, ids2);
+      if (lex_less(ids, nc, ids2, ne)) {
+        items[e].src = o;
+        items[e].count = nc;
+      }
+      merged = true;
+    }
+    if (merged) continue;
+    // push_back + std::sort (objective desc, train lexicographic asc) + trim to k
+    items[n_items] = TopItem{obj, nc, o};
+    for (int m = 0; m < M; ++m) foot[(size_t)n_items * M + m] = cand_foot[m];
+    ++n_items;
+    for (int i = 1; i < n_items; ++i) {
+      int j = i;
+      while (j > 0) {
+        const TopItem& x = items[j];
+        const TopItem& y = items[j - 1];
+        bool before;
+        if (x.obj != y.obj) {
+          before = x.obj > y.obj;
+        } else {
+          const int nx = offer_ids(u, in_train, x.src, ids);
+          const int ny = offer_ids(u, in_train, y.src, ids2);
+          before = lex_less(ids, nx, ids2, ny);
+        }
+        if (!before) break;
+        const TopItem t = items[j];
+        items[j] = items[j - 1];
+        items[j - 1] = t;
+        for (int m = 0; m < M; ++m) {
+          const int v = foot[(size_t)j * M + m];
+          foot[(size_t)j * M + m] = foot[(size_t)(j - 1) * M + m];
+          foot[(size_t)(j - 1) * M + m] = v;
+        }
+        --j;
+      }
+    }
+    if (n_items > k) --n_items;
+  }
+  out->n_items = n_items;
+  for (int e = 0; e < n_items; ++e) out->item[e] = items[e];
+}
+
+// compute_fraction (src/partition.cpp:360-367) for each result + its train ids
+__global__ void k5_emit(Units u, const unsigned char* __restrict__ in_train, const TopKOut* __restrict__ tk,
+                        const double* __restrict__ dflops, int N, int* __restrict__ ids_out,
+                        double* __restrict__ frac_out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double total = 0;
+  for (int d = 0; d < N; ++d) total += dflops[d];
+  int off = 0;
+  for (int e = 0; e < tk->n_items; ++e) {
+    const int c = offer_ids(u, in_train, tk->item[e].src, ids_out + off);
+    double t = 0;
+    for (int i = 0; i < c; ++i) t += dflops[ids_out[off + i]];
+    frac_out[e] = t / total;
+    off += c;
+  }
+}
+
+// partition_objective (src/partition.cpp:354-358): State built by add() in the given order
+__global__ void k5_objective(const int* __restrict__ train, int nt, const double* __restrict__ dflops,
+                             const double* __restrict__ dhbm, const double* __restrict__ links, int N,
+                             double* __restrict__ ltt, double* __restrict__ out) {
+  __shared__ double s_lt, s_hb;
+  if (threadIdx.x == 0) s_lt = s_hb = 0;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) ltt[j] = 0;
+  __syncthreads();
+  for (int k = 0; k < nt; ++k) {
+    const int i = train[k];
+    if (threadIdx.x == 0) {
+      s_lt += ltt[i] + 0.0;  // device units: internal link 0
+      s_hb += dhbm[i];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < N; j += blockDim.x)
+      if (j != i) ltt[j] += links[(size_t)i * N + j];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double tl = 0, th = 0;
+    for (int i = 0; i < N; ++i) {
+      tl += 0.0;
+      for (int j = i + 1; j < N; ++j) tl += links[(size_t)i * N + j];
+    }
+    for (int i = 0; i < N; ++i) th += dhbm[i];
+    const double lf = tl > 0 ? s_lt / tl : 0;
+    out[0] = lf + (th - s_hb) / th;
+    double tf = 0, trf = 0;
+    for (int d = 0; d < N; ++d) tf += dflops[d];
+    for (int k = 0; k < nt; ++k) trf += dflops[train[k]];
+    out[1] = trf / tf;
+  }
+}
+
+// ===================================================================== host
+
+template <typename T>
+static T* carve3(char*& p, size_t count) {
+  p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+  T* r = reinterpret_cast<T*>(p);
+  p += sizeof(T) * count;
+  return r;
+}
+
+int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, int k, gp_partition* out,
+                         int32_t* train_ids, int32_t* n_out) {
+  *n_out = 0;
+  const int N = ctx->N, M = ctx->M;
+  if (N < 2) return set_error(GP_INVALID, "graph_partition requires at least two devices");
+  if (k < 1 || k > 64) return set_error(GP_INVALID, "k must lie in [1, 64]");
+  if (o->restarts < 0) return set_error(GP_INVALID, "restarts must be >= 0");
+  // units: machines (device ids ascending) or devices (build_units, src/partition.cpp:37-52)
+  const bool by_machine = o->machine_granularity && M >= 2;
+  std::vector<int> mem_off, mem_ids;
+  if (by_machine) {
+    std::vector<std::vector<int>> mm(M);
+    for (int d = 0; d < N; ++d) mm[ctx->h_machine[d]].push_back(d);
+    for (int m = 0; m < M; ++m) {
+      mem_off.push_back((int)mem_ids.size());
+      mem_ids.insert(mem_ids.end(), mm[m].begin(), mm[m].end());
+    }
+  } else {
+    for (int d = 0; d < N; ++d) {
+      mem_off.push_back(d);
+      mem_ids.push_back(d);
+    }
+  }
+  mem_off.push_back((int)mem_ids.size());
+  const int n = (int)mem_off.size() - 1;
+  if (n > kMaxUnits) return set_error(GP_INVALID, "too many partition units for the sm_100a kernel");
+  const double lo = g->gamma_l - o->band_epsilon, hi = g->gamma_h + o->band_epsilon;
+  const bool exact = !o->force_local_search && n <= o->exact_threshold && n <= 20;
+  const int n_offers = exact ? (int)((1ull << n) - 2) : o->restarts;
+  // ---- device buffers
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+  add(sizeof(int) * (n + 1));
+  add(sizeof(int) * N);
+  add(sizeof(double) * n * 4);
+  add(sizeof(double) * (size_t)n * n);
+  add(sizeof(Totals));
+  add(sizeof(Offer) * std::max(n_offers, 1));
+  add(sizeof(RestartOut) * std::max(o->restarts, 1));
+  add((size_t)std::max(n_offers, 1) * n);
+  add(sizeof(double) * std::max(n_offers, 1));
+  add(sizeof(int) * std::max(n_offers, 1));
+  add(sizeof(int) * (3 * (size_t)N + (size_t)M * (k + 2)));
+  add(sizeof(TopKOut));
+  add(sizeof(int) * (size_t)N * k);
+  add(sizeof(double) * k);
+  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaPartition));
+  if (!base) return GP_CUDA_ERROR;
+  char* p = base;
+  int* d_off = carve3<int>(p, n + 1);
+  int* d_ids = carve3<int>(p, N);
+  double* d_uf = carve3<double>(p, n);
+  double* d_uh = carve3<double>(p, n);
+  double* d_ui = carve3<double>(p, n);
+  double* d_base = carve3<double>(p, n);
+  double* d_cross = carve3<double>(p, (size_t)n * n);
+  Totals* d_tot = carve3<Totals>(p, 1);
+  Offer* d_offer = carve3<Offer>(p, std::max(n_offers, 1));
+  RestartOut* d_rout = carve3<RestartOut>(p, std::max(o->restarts, 1));
+  unsigned char* d_mask = carve3<unsigned char>(p, (size_t)std::max(n_offers, 1) * n);
+  double* d_objs = carve3<double>(p, std::max(n_offers, 1));
+  int* d_valid = carve3<int>(p, std::max(n_offers, 1));
+  int* d_work = carve3<int>(p, 3 * (size_t)N + (size_t)M * (k + 2));
+  TopKOut* d_tk = carve3<TopKOut>(p, 1);
+  int* d_tids = carve3<int>(p, (size_t)N * k);
+  double* d_frac = carve3<double>(p, k);
+  const size_t in_bytes = (size_t)((char*)(d_ids + N) - (char*)d_off);
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(TopKOut) + sizeof(int) * (size_t)N * k + sizeof(double) * k + 1024)));
+  if (!hp) return GP_CUDA_ERROR;
+  std::memcpy(hp, mem_off.data(), sizeof(int) * (n + 1));
+  std::memcpy(hp + ((char*)d_ids - (char*)d_off), mem_ids.data(), sizeof(int) * N);
+  GP_CUDA(cudaMemcpyAsync(d_off, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)in_bytes;
+  Units u{n, d_uf, d_uh, d_ui, d_cross, d_off, d_ids};
+  k5_units<<<n, 128, 0, ctx->stream>>>(n, d_off, d_ids, ctx->d_flops, ctx->d_hbm_bw, ctx->d_links, N, d_uf,
+                                      d_uh, d_ui, d_cross);
+  k5_totals<<<1, 256, 0, ctx->stream>>>(u, d_tot, d_base);
+  ctx->launches += 2;
+  if (exact) {
+    k5_exact<<<(n_offers + 255) / 256, 256, 0, ctx->stream>>>(u, d_tot, lo, hi, d_offer);
+    ctx->launches++;
+  } else if (o->restarts > 0) {
+    const size_t sm = sizeof(double) * 2 * n + sizeof(int) * 3 * n + n + 16;
+    if (sm > 227 * 1024) return set_error(GP_INVALID, "partition units exceed shared memory");
+    GP_CUDA(cudaFuncSetAttribute(k5_restart, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k5_restart<<<o->restarts, kK5Threads, sm, ctx->stream>>>(u, d_tot, d_base, lo, hi, o->restarts,
+                                                            o->seed, d_mask, d_rout);
+    ctx->launches++;
+  }
+  GP_CUDA(cudaGetLastError());
+  // offers -> (mask rows, objective, valid) in the reference's offer order
+  if (exact) {
+    // masks 1..2^n-2 ascending; the unit membership of mask m is its bit pattern
+    std::vector<unsigned char> masks((size_t)n_offers * n);
+    for (int m = 0; m < n_offers; ++m)
+      for (int i = 0; i < n; ++i) masks[(size_t)m * n + i] = ((m + 1) >> i) & 1;
+    // stage through pinned memory in slices (small: <= 4094 x 12)
+    char* hp2 = static_cast<char*>(ctx_pinned(ctx, std::max(masks.size(), sizeof(TopKOut) + sizeof(int) * (size_t)N * k + sizeof(double) * k + 1024)));
+    if (!hp2) return GP_CUDA_ERROR;
+    GP_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(hp2, masks.data(), masks.size());
+    GP_CUDA(cudaMemcpyAsync(d_mask, hp2, masks.size(), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->h2d_bytes += (long long)masks.size();
+  }
+  k5_unpack_offers<<<(n_offers + 255) / 256, 256, 0, ctx->stream>>>(d_offer, d_rout, n_offers, exact, d_objs,
+                                                                    d_valid);
+  k5_topk<<<1, 1, 0, ctx->stream>>>(u, d_mask, d_objs, d_valid, n_offers, k, ctx->d_machine, M, d_work, d_tk);
+  k5_emit<<<1, 1, 0, ctx->stream>>>(u, d_mask, d_tk, ctx->d_flops, N, d_tids, d_frac);
+  ctx->launches += 3;
+  GP_CUDA(cudaGetLastError());
+  TopKOut* htk = reinterpret_cast<TopKOut*>(hp);
+  int* hids = reinterpret_cast<int*>(hp + sizeof(TopKOut));
+  double* hfrac = reinterpret_cast<double*>(hp + sizeof(TopKOut) + sizeof(int) * (size_t)N * k);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  GP_CUDA(cudaMemcpyAsync(htk, d_tk, sizeof(TopKOut), cudaMemcpyDeviceToHost, ctx->stream));
+  GP_CUDA(cudaMemcpyAsync(hids, d_tids, sizeof(int) * (size_t)N * k, cudaMemcpyDeviceToHost, ctx->stream));
+  GP_CUDA(cudaMemcpyAsync(hfrac, d_frac, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += (long long)(sizeof(TopKOut) + sizeof(int) * (size_t)N * k + sizeof(double) * k);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (htk->n_items == 0)
+    return set_error(GP_BAND_INFEASIBLE, "no bisection satisfies the compute-fraction band [" +
+                                             std::to_string(g->gamma_l) + ", " + std::to_string(g->gamma_h) + "]");
+  int off = 0;
+  for (int e = 0; e < htk->n_items; ++e) {
+    out[e].train_offset = off;
+    out[e].train_count = htk->item[e].count;
+    out[e].objective = htk->item[e].obj;
+    out[e].compute_fraction = hfrac[e];
+    std::memcpy(train_ids + off, hids + off, sizeof(int32_t) * htk->item[e].count);
+    off += htk->item[e].count;
+  }
+  *n_out = htk->n_items;
+  return GP_OK;
+}
+
+int partition_objective(gp_ctx* ctx, const int32_t* train, int nt, double* obj, double* frac) {
+  const int N = ctx->N;
+  for (int i = 0; i < nt; ++i)
+    if (train[i] < 0 || train[i] >= N) return set_error(GP_INVALID, "unknown device id");
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+  add(sizeof(int) * (nt + 1));
+  add(sizeof(double) * N);
+  add(sizeof(double) * 2);
+  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaPartition));
+  if (!base) return GP_CUDA_ERROR;
+  char* p = base;
+  int* d_t = carve3<int>(p, nt + 1);
+  double* d_ltt = carve3<double>(p, N);
+  double* d_out = carve3<double>(p, 2);
+  char* hp = static_cast<char*>(ctx_pinned(ctx, sizeof(int) * (nt + 1) + 64));
+  if (!hp) return GP_CUDA_ERROR;
+  std::memcpy(hp, train, sizeof(int) * nt);
+  GP_CUDA(cudaMemcpyAsync(d_t, hp, sizeof(int) * (nt + 1), cudaMemcpyHostToDevice, ctx->stream));
+  k5_objective<<<1, 256, 0, ctx->stream>>>(d_t, nt, ctx->d_flops, ctx->d_hbm_bw, ctx->d_links, N, d_ltt,
+                                           d_out);
+  ctx->launches++;
+  GP_CUDA(cudaGetLastError());
+  double* ho = reinterpret_cast<double*>(hp);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  GP_CUDA(cudaMemcpyAsync(ho, d_out, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  *obj = ho[0];
+  *frac = ho[1];
+  return GP_OK;
+}
+
+}  // namespace gp

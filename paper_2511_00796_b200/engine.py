@@ -242,3 +242,23 @@ class Engine:
                                          et.ctypes.data_as(abi.i32p), er.ctypes.data_as(abi.i32p),
                                          len(et), window, C.byref(out)))
         return out.value
+
+    # ---- repartition ----------------------------------------------------------
+    def partition_candidates(self, gamma_l: float, gamma_h: float, k: int = 8, opts=None,
+                             q: float = 0.0, r: float = 1.0):
+        """graph_partition_candidates (inc/partition.hpp:53-55): [(train ids, objective, fraction)]."""
+        g = abi.gp_gamma(q, r, gamma_l, gamma_h)
+        out = (abi.gp_partition * k)()
+        ids = np.zeros(self.n_devices * k, dtype=np.int32)
+        n = C.c_int32()
+        _check(lib().gp_partition_candidates(self._h, C.byref(g), C.byref(opts or abi.default_part_opts()),
+                                             k, out, ids.ctypes.data_as(abi.i32p), C.byref(n)))
+        return [(ids[o.train_offset:o.train_offset + o.train_count].tolist(), o.objective,
+                 o.compute_fraction) for o in out[:n.value]]
+
+    def partition_objective(self, train):
+        t = _ids(train)
+        obj, frac = C.c_double(), C.c_double()
+        _check(lib().gp_partition_objective(self._h, t.ctypes.data_as(abi.i32p), len(t), C.byref(obj),
+                                            C.byref(frac)))
+        return obj.value, frac.value

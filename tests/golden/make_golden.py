@@ -102,6 +102,33 @@ def main():
         ro[name] = cases
         print(name, len(cases), "rollout cases")
     dump("rollout.json", ro)
+    # ---- graph_partition_candidates: scheduler-style probes (top-8, gamma grid, widened bands)
+    parts = {}
+    for name in CONFIGS + ["t10_tiny", "t8_tiny"]:
+        p = problem(name)
+        ref = Ref(p)
+        cases = []
+        grid = [1, 4, 8, 12, 15] if name == "c5_1024gpu" else range(1, 16)
+        for pp in grid:
+            gm = pp / 16
+            for widen in (0.0, 0.05):
+                for machine in ((False, True) if name != "c5_1024gpu" else (False,)):
+                    lo, hi = max(0.0, gm - widen), min(1.0, gm + widen)
+                    case = {"gamma_l": lo, "gamma_h": hi, "machine": machine}
+                    try:
+                        out = ref.partition_candidates(lo, hi, k=8, seed=4276115, machine=machine)
+                        case["candidates"] = out["candidates"]
+                    except RefError as e:
+                        case["error"] = e.code
+                    cases.append(case)
+        if name in ("t10_tiny", "t8_tiny"):  # heuristic tier on exact-size clusters
+            for lo, hi in ((0.2, 0.5), (0.4, 0.7), (0.1, 0.9)):
+                out = ref.partition_candidates(lo, hi, k=8, seed=99, force_local=True)
+                cases.append({"gamma_l": lo, "gamma_h": hi, "machine": False, "force_local": True,
+                              "seed": 99, "candidates": out["candidates"]})
+        parts[name] = cases
+        print(name, len(cases), "partition cases")
+    dump("partition.json", parts)
 
 
 if __name__ == "__main__":

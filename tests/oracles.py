@@ -251,3 +251,20 @@ def oracle_weight_sync(orc, train, roll, etypes, ereps, window):
     if rc:
         orc.err(rc)
     return v.value
+
+
+def oracle_partitions(orc, gamma_l, gamma_h, k=8, seed=0x5EED, restarts=16, force_local=False,
+                      machine=False):
+    """C restatement of graph_partition_candidates -> [(train, objective, fraction)] or raises."""
+    import ctypes as C
+    g = abi.gp_gamma(0.0, 1.0, gamma_l, gamma_h)
+    o = abi.gp_part_opts(12, restarts, seed, 1e-9, int(force_local), int(machine))
+    out = (abi.gp_partition * k)()
+    ids = np.zeros(orc.problem.cluster.n * k, dtype=np.int32)
+    n = C.c_int32()
+    rc = orc.lib.or_partition_candidates(C.byref(orc.c), C.byref(g), C.byref(o), k, out,
+                                         ids.ctypes.data_as(abi.i32p), C.byref(n))
+    if rc:
+        orc.err(rc)
+    return [(ids[p.train_offset:p.train_offset + p.train_count].tolist(), p.objective,
+             p.compute_fraction) for p in out[:n.value]]

@@ -103,3 +103,19 @@ def test_rollout_side_matches_reference(name):
         et = [next(t for t, v in enumerate(e["type_counts"]) if v > 0) for e in m["entries"]]
         er = [e["replicas"] for e in m["entries"]]
         assert oracle_weight_sync(orc, case["train"], case["rollout"], et, er, case["window"]) == case["weight_sync"]
+
+
+@pytest.mark.parametrize("name", CONFIGS + ["t10_tiny", "t8_tiny"])
+def test_partition_matches_reference(name):
+    from oracles import RefError, oracle_partitions
+    orc = Oracle(problem(name))
+    for case in golden("partition.json")[name]:
+        kw = dict(k=8, seed=case.get("seed", 4276115), force_local=case.get("force_local", False),
+                  machine=case["machine"])
+        if "error" in case:
+            with pytest.raises(RefError):
+                oracle_partitions(orc, case["gamma_l"], case["gamma_h"], **kw)
+            continue
+        got = oracle_partitions(orc, case["gamma_l"], case["gamma_h"], **kw)
+        want = [(c["train"], c["objective"], c["compute_fraction"]) for c in case["candidates"]]
+        assert got == want, (case["gamma_l"], case["gamma_h"], case["machine"])

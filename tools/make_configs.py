@@ -60,6 +60,11 @@ CONFIGS = {
                    workload(70, 80, 8192, 2)),
 }
 
+# tiny clusters (<= 12 devices) exercise the exact bisection tier (src/partition.cpp:212-222)
+CONFIGS["t10_tiny"] = (cluster([("H800", 2, 3), ("H20", 1, 4)]), workload(1.5, 28, 1536, 1))
+CONFIGS["t8_tiny"] = (cluster([("H20", 2, 2), ("PCIE", 1, 4)], [("h20-0", "h20-1", 25)]),
+                      workload(1.5, 28, 1536, 2))
+
 if __name__ == "__main__":
     for name, (cl, wl) in CONFIGS.items():
         types = [t["name"] for t in cl["gpu_types"]]
