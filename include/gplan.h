@@ -246,6 +246,8 @@ int gp_partition_candidates(gp_ctx* ctx, const gp_gamma* gamma, const gp_part_op
                             int32_t k, gp_partition* out, int32_t* train_ids, int32_t* n_out);
 int gp_partition_objective(gp_ctx* ctx, const int32_t* train, int32_t n_train, double* objective,
                            double* fraction);
+/* compute_fraction (src/partition.cpp:360-367). */
+int gp_compute_fraction(gp_ctx* ctx, const int32_t* train, int32_t n_train, double* fraction);
 
 #ifdef __cplusplus
 }

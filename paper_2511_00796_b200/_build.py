@@ -59,5 +59,29 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+REF_INCLUDE = "/root/reference/proj/include"
+SHIM_SRC = os.path.join(PKG, "shim", "rlsched_shim.cpp")
+SHIM_LIB = os.path.join(PKG, "libgplan_shim.so")
+
+
+def build_shim(ref_include: str = REF_INCLUDE) -> str | None:
+    """libgplan_shim.so: the reference seam on the engine. Needs the reference's
+    headers (present in the build container only); the built .so travels."""
+    if not os.path.isdir(ref_include):
+        return None
+    lib = build()
+    if os.path.exists(SHIM_LIB) and os.path.getmtime(SHIM_LIB) >= max(
+            os.path.getmtime(SHIM_SRC), os.path.getmtime(lib)):
+        return SHIM_LIB
+    cmd = ["g++", "-std=gnu++20", "-O2", "-fPIC", "-shared", "-Wall", "-I", os.path.join(ROOT, "include"),
+           "-I", ref_include, SHIM_SRC, "-L", PKG, "-lgplan", "-Wl,-rpath,$ORIGIN", "-o", SHIM_LIB]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("shim build failed")
+    return SHIM_LIB
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    print(build_shim())

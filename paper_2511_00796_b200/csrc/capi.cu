@@ -30,6 +30,7 @@ int weight_sync(gp_ctx* ctx, const int32_t* train, int nt, const int32_t* roll, 
 int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, int k, gp_partition* out,
                          int32_t* train_ids, int32_t* n_out);
 int partition_objective(gp_ctx* ctx, const int32_t* train, int nt, double* obj, double* frac);
+int compute_fraction(gp_ctx* ctx, const int32_t* train, int nt, double* frac);
 
 static thread_local std::string g_error;
 
@@ -329,6 +330,12 @@ int gp_partition_objective(gp_ctx* ctx, const int32_t* train, int32_t n_train, d
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return partition_objective(ctx, train, n_train, objective, fraction);
+}
+
+int gp_compute_fraction(gp_ctx* ctx, const int32_t* train, int32_t n_train, double* fraction) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  cudaSetDevice(ctx->device);
+  return compute_fraction(ctx, train, n_train, fraction);
 }
 
 int gp_ctx_set_timing(gp_ctx* ctx, int on) {

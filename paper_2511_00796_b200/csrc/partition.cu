@@ -590,6 +590,16 @@ __global__ void k5_objective(const int* __restrict__ train, int nt, const double
   }
 }
 
+// compute_fraction (src/partition.cpp:360-367): two sequential folds
+__global__ void k5_fraction(const int* __restrict__ train, int nt, const double* __restrict__ dflops, int N,
+                            double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double total = 0, tr = 0;
+  for (int d = 0; d < N; ++d) total += dflops[d];
+  for (int i = 0; i < nt; ++i) tr += dflops[train[i]];
+  *out = tr / total;
+}
+
 // ===================================================================== host
 
 template <typename T>
@@ -732,6 +742,29 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
     off += htk->item[e].count;
   }
   *n_out = htk->n_items;
+  return GP_OK;
+}
+
+int compute_fraction(gp_ctx* ctx, const int32_t* train, int nt, double* frac) {
+  const int N = ctx->N;
+  for (int i = 0; i < nt; ++i)
+    if (train[i] < 0 || train[i] >= N) return set_error(GP_INVALID, "unknown device id");
+  char* base = static_cast<char*>(ctx_scratch(ctx, sizeof(int) * (nt + 1) + 1024, kArenaMisc));
+  if (!base) return GP_CUDA_ERROR;
+  char* p = base;
+  int* d_t = carve3<int>(p, nt + 1);
+  double* d_out = carve3<double>(p, 1);
+  char* hp = static_cast<char*>(ctx_pinned(ctx, sizeof(int) * (nt + 1) + 64));
+  if (!hp) return GP_CUDA_ERROR;
+  std::memcpy(hp, train, sizeof(int) * nt);
+  GP_CUDA(cudaMemcpyAsync(d_t, hp, sizeof(int) * (nt + 1), cudaMemcpyHostToDevice, ctx->stream));
+  k5_fraction<<<1, 32, 0, ctx->stream>>>(d_t, nt, ctx->d_flops, N, d_out);
+  ctx->launches++;
+  GP_CUDA(cudaGetLastError());
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  GP_CUDA(cudaMemcpyAsync(hp, d_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(frac, hp, sizeof(double));
   return GP_OK;
 }
 

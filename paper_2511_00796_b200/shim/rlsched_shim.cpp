@@ -1,0 +1,315 @@
+// rlsched_shim.cpp — the drop-in: the reference's hot-path free functions
+// (the seam scheduler.cpp calls, src/scheduler.cpp:21-75,150-151,196) with their
+// EXACT signatures, implemented on the B200 engine through the C ABI (include/gplan.h).
+//
+// Built against the reference's own headers (-I proj/include), into
+// libgplan_shim.so. Linking/loading it ahead of the reference library
+// (`-lgplan_shim -lrlsched`, or LD_PRELOAD=libgplan_shim.so) makes the UNMODIFIED
+// reference scheduler.cpp resolve these calls to the engine: its cross-TU calls
+// go through the PLT, so the first definition in load order wins. See
+// INTEGRATION.md. Errors come back as gp_status codes and are rethrown as the
+// reference's exception types (inc/common.hpp:11-39).
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gplan.h"
+#include "rlsched/calibration.hpp"
+#include "rlsched/cluster.hpp"
+#include "rlsched/cost_model.hpp"
+#include "rlsched/partition.hpp"
+#include "rlsched/plans.hpp"
+#include "rlsched/rollout_milp.hpp"
+#include "rlsched/train_search.hpp"
+#include "rlsched/workload.hpp"
+
+namespace {
+
+using namespace rlsched;
+
+long long g_calls = 0;
+
+[[noreturn]] void rethrow(int rc) {
+  const std::string msg = gp_last_error();
+  switch (rc) {
+    case GP_INVALID: throw ValidationError(msg);
+    case GP_BAND_INFEASIBLE: throw BandInfeasibleError(msg);
+    case GP_INFEASIBLE: throw InfeasibleError(msg);
+    default: throw std::runtime_error("libgplan: " + msg);
+  }
+}
+
+inline void check(int rc) {
+  ++g_calls;
+  if (rc != GP_OK) rethrow(rc);
+}
+
+// One engine context per (cluster, workload, calibration) content. The reference
+// passes the same ClusterGraph object for a whole schedule() run and a copy of the
+// workload (scheduler.cpp:265-267), so the key is the cluster's address and
+// fingerprint plus every workload/calibration scalar the engine consumes.
+struct Key {
+  const ClusterGraph* cluster = nullptr;
+  std::string fingerprint;
+  int n = 0;
+  std::vector<double> scalars;
+  bool operator==(const Key& o) const {
+    return cluster == o.cluster && fingerprint == o.fingerprint && n == o.n && scalars == o.scalars;
+  }
+};
+
+struct Ctx {
+  Key key;
+  gp_ctx* ctx = nullptr;
+  ~Ctx() { gp_ctx_destroy(ctx); }
+};
+
+std::mutex g_mu;
+std::vector<std::unique_ptr<Ctx>> g_ctx;
+
+std::vector<double> scalars_of(const WorkloadSpec& w, const Calibration& k, const ClusterGraph& g) {
+  std::vector<double> s = {w.model_params_b, (double)w.num_layers, (double)w.hidden_dim,
+                           (double)w.batch_rollouts, (double)w.prompt_len, w.length_dist.mean(),
+                           w.bytes_per_param_train, w.bytes_per_param_infer, w.reward_cost_const,
+                           (double)w.micro_batches, k.params.sync_latency_s,
+                           k.params.stage_latency_penalty, (double)k.params.max_concurrency,
+                           k.params.activation_coeff, k.params.tp_allreduce_coeff,
+                           k.params.grad_bytes_per_param};
+  for (const auto& t : g.types) {
+    auto it = k.per_type.find(t.name);
+    s.push_back(it == k.per_type.end() ? -1.0 : it->second.compute_efficiency);
+    s.push_back(it == k.per_type.end() ? -1.0 : it->second.io_efficiency);
+  }
+  return s;
+}
+
+gp_ctx* context(const ClusterGraph& g, const WorkloadSpec& w, const Calibration& k) {
+  Key key{&g, g.fingerprint, g.size(), scalars_of(w, k, g)};
+  std::lock_guard<std::mutex> lock(g_mu);
+  for (auto& c : g_ctx)
+    if (c->key == key) return c->ctx;
+  const int N = g.size(), T = (int)g.types.size();
+  std::vector<int32_t> dtype(N), dmach(N);
+  std::vector<double> dfl(N), dbw(N), dcap(N), tfl(T), tbw(T), tcap(T), ce(T), io(T);
+  for (int d = 0; d < N; ++d) {
+    dtype[d] = g.devices[d].gpu_type;
+    dmach[d] = g.devices[d].machine_id;
+    dfl[d] = g.devices[d].flops;
+    dbw[d] = g.devices[d].hbm_bandwidth;
+    dcap[d] = g.devices[d].hbm_capacity;
+  }
+  for (int t = 0; t < T; ++t) {
+    tfl[t] = g.types[t].flops;
+    tbw[t] = g.types[t].hbm_bandwidth;
+    tcap[t] = g.types[t].hbm_capacity;
+    const TypeEfficiency& e = k.for_type(g.types[t].name);  // throws like the reference
+    ce[t] = e.compute_efficiency;
+    io[t] = e.io_efficiency;
+  }
+  gp_cluster c{N, T, (int32_t)g.machines.size(), dtype.data(), dmach.data(), dfl.data(), dbw.data(),
+               dcap.data(), tfl.data(), tbw.data(), tcap.data(), g.links.data()};
+  gp_workload wl{w.model_params_b, w.num_layers, w.hidden_dim, w.batch_rollouts, w.prompt_len,
+                 w.length_dist.mean(), w.bytes_per_param_train, w.bytes_per_param_infer,
+                 w.reward_cost_const, w.micro_batches, w.staleness};
+  gp_calib kc{ce.data(), io.data(), k.params.sync_latency_s, k.params.stage_latency_penalty,
+              k.params.max_concurrency, k.params.activation_coeff, k.params.tp_allreduce_coeff,
+              k.params.grad_bytes_per_param};
+  const char* dev = std::getenv("GPLAN_DEVICE");
+  gp_ctx* h = nullptr;
+  check(gp_ctx_create(&c, &wl, &kc, dev ? std::atoi(dev) : 0, &h));
+  if (g_ctx.size() >= 8) g_ctx.erase(g_ctx.begin());
+  g_ctx.push_back(std::make_unique<Ctx>());
+  g_ctx.back()->key = key;
+  g_ctx.back()->ctx = h;
+  return h;
+}
+
+// Partition objective needs no workload; any context for this cluster serves.
+gp_ctx* any_context(const ClusterGraph& g) {
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (auto& c : g_ctx)
+      if (c->key.cluster == &g && c->key.fingerprint == g.fingerprint && c->key.n == g.size())
+        return c->ctx;
+  }
+  WorkloadSpec w;  // placeholder scalars: the partition kernels read only the cluster
+  w.model_params_b = 1;
+  w.num_layers = 1;
+  w.hidden_dim = 1;
+  w.batch_rollouts = 1;
+  w.length_dist = LengthDistribution::point(1);
+  Calibration k = default_calibration(g);
+  return context(g, w, k);
+}
+
+ReplicaConfig to_config(const gp_config& c, int T) {
+  ReplicaConfig r;
+  r.type_counts.assign(c.type_counts, c.type_counts + T);
+  r.tp_per_stage.assign(c.tp, c.tp + c.n_stages);
+  r.throughput = c.throughput;
+  r.machine_footprint = r.tp_per_stage;
+  return r;
+}
+
+gp_config from_config(const ReplicaConfig& r) {
+  gp_config c;
+  std::memset(&c, 0, sizeof c);
+  if (r.type_counts.size() > GP_MAX_TYPES || r.tp_per_stage.size() > GP_MAX_ROLLOUT_STAGES)
+    throw ValidationError("replica config exceeds the engine's fixed limits");
+  for (size_t t = 0; t < r.type_counts.size(); ++t) c.type_counts[t] = r.type_counts[t];
+  for (size_t s = 0; s < r.tp_per_stage.size(); ++s) c.tp[s] = r.tp_per_stage[s];
+  c.n_stages = (int32_t)r.tp_per_stage.size();
+  c.throughput = r.throughput;
+  return c;
+}
+
+}  // namespace
+
+// ============================================================== the seam
+namespace rlsched {
+
+std::optional<TrainSearchResult> constrained_search(const std::vector<int>& train_set,
+                                                    const ClusterGraph& cluster,
+                                                    const WorkloadSpec& work,
+                                                    const Calibration& calib, int window,
+                                                    const TrainSearchOptions& options) {
+  gp_ctx* h = context(cluster, work, calib);
+  gp_train_opts o{options.max_stages_per_type, options.device_granularity_limit};
+  gp_train_result res;
+  std::vector<int32_t> devs(train_set.size() + 1);
+  check(gp_constrained_search(h, train_set.data(), (int32_t)train_set.size(), window, &o, &res,
+                              devs.data()));
+  if (!res.found) return std::nullopt;
+  TrainSearchResult out;
+  for (int s = 0; s < res.n_stages; ++s) {
+    PipelineStage st;
+    st.devices.assign(devs.begin() + res.stage[s].first,
+                      devs.begin() + res.stage[s].first + res.stage[s].count);
+    st.tp_degree = res.stage[s].tp;
+    st.dp_degree = res.stage[s].dp;
+    st.layer_count = res.stage[s].layers;
+    out.plan.stages.push_back(std::move(st));
+  }
+  out.cost = res.cost;
+  out.plan.predicted_cost = res.cost;
+  return out;
+}
+
+std::vector<ReplicaConfig> enumerate_configs(const std::vector<int>& rollout_set,
+                                             const ClusterGraph& cluster, const WorkloadSpec& work,
+                                             const Calibration& calib,
+                                             const RolloutSearchOptions& options) {
+  gp_ctx* h = context(cluster, work, calib);
+  gp_rollout_opts o{options.max_stages};
+  std::vector<gp_config> buf(70 * cluster.types.size() + 8);
+  int32_t n = 0;
+  check(gp_enumerate_configs(h, rollout_set.data(), (int32_t)rollout_set.size(), &o, buf.data(),
+                             (int32_t)buf.size(), &n));
+  std::vector<ReplicaConfig> out;
+  for (int i = 0; i < n; ++i) out.push_back(to_config(buf[i], (int)cluster.types.size()));
+  return out;
+}
+
+std::vector<int> rollout_capacities(const std::vector<int>& rollout_set, const ClusterGraph& cluster) {
+  std::vector<int> caps(cluster.types.size(), 0);
+  for (int id : rollout_set) caps[static_cast<size_t>(cluster.device(id).gpu_type)]++;
+  return caps;
+}
+
+RolloutPlan solve_milp(const std::vector<ReplicaConfig>& configs, const std::vector<int>& capacities,
+                       double total_rollouts, double mean_len) {
+  // solve_milp carries no cluster: use the most recent engine context (every
+  // scheduler call site follows enumerate_configs on the same context).
+  gp_ctx* h = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    if (!g_ctx.empty()) h = g_ctx.back()->ctx;
+  }
+  if (!h) throw std::runtime_error("libgplan: solve_milp before any engine context exists");
+  std::vector<gp_config> cfg;
+  for (const auto& c : configs) cfg.push_back(from_config(c));
+  std::vector<gp_rollout_entry> ent(configs.size() + 1);
+  gp_rollout_result res;
+  check(gp_solve_milp(h, cfg.data(), (int32_t)cfg.size(), capacities.data(), (int32_t)capacities.size(),
+                      total_rollouts, mean_len, &res, ent.data()));
+  RolloutPlan plan;
+  plan.total_rollouts = total_rollouts;
+  plan.makespan = res.makespan;
+  for (int e = 0; e < res.n_entries; ++e) {
+    RolloutEntry entry;
+    entry.config = configs[static_cast<size_t>(ent[e].config)];
+    entry.replicas = ent[e].replicas;
+    entry.workload = ent[e].workload;
+    plan.entries.push_back(std::move(entry));
+  }
+  return plan;
+}
+
+double weight_sync_cost(const TrainPlan& /*train_plan*/, const RolloutPlan& rollout_plan,
+                        const DevicePartition& partition, const ClusterGraph& cluster,
+                        const WorkloadSpec& work, const Calibration& calib, int window) {
+  gp_ctx* h = context(cluster, work, calib);
+  std::vector<int32_t> et, er;
+  for (const auto& e : rollout_plan.entries) {
+    et.push_back(e.config.gpu_type());
+    er.push_back(e.replicas);
+  }
+  double out = 0;
+  check(gp_weight_sync_cost(h, partition.train_set.data(), (int32_t)partition.train_set.size(),
+                            partition.rollout_set.data(), (int32_t)partition.rollout_set.size(),
+                            et.data(), er.data(), (int32_t)et.size(), window, &out));
+  return out;
+}
+
+std::vector<PartitionResult> graph_partition_candidates(const ClusterGraph& cluster,
+                                                        const GammaState& gamma,
+                                                        const PartitionOptions& options, int k) {
+  if (cluster.size() < 2) throw ValidationError("graph_partition requires at least two devices");
+  gp_ctx* h = any_context(cluster);
+  gp_gamma g{gamma.q, gamma.r, gamma.gamma_l, gamma.gamma_h};
+  gp_part_opts o{options.exact_threshold, options.restarts, options.seed, options.band_epsilon,
+                 options.force_local_search, options.machine_granularity};
+  std::vector<gp_partition> parts(static_cast<size_t>(k));
+  std::vector<int32_t> ids(static_cast<size_t>(k) * cluster.size() + 1);
+  int32_t n = 0;
+  check(gp_partition_candidates(h, &g, &o, k, parts.data(), ids.data(), &n));
+  std::vector<PartitionResult> results;
+  for (int i = 0; i < n; ++i) {
+    PartitionResult r;
+    r.objective = parts[i].objective;
+    r.compute_fraction = parts[i].compute_fraction;
+    r.partition.train_set.assign(ids.begin() + parts[i].train_offset,
+                                 ids.begin() + parts[i].train_offset + parts[i].train_count);
+    std::vector<char> in(static_cast<size_t>(cluster.size()), 0);
+    for (int id : r.partition.train_set) in[static_cast<size_t>(id)] = 1;
+    for (const auto& d : cluster.devices)
+      if (!in[static_cast<size_t>(d.id)]) r.partition.rollout_set.push_back(d.id);
+    r.partition.validate(cluster);
+    results.push_back(std::move(r));
+  }
+  return results;
+}
+
+double partition_objective(const ClusterGraph& cluster, const std::vector<int>& train_set) {
+  gp_ctx* h = any_context(cluster);
+  double obj = 0, frac = 0;
+  check(gp_partition_objective(h, train_set.data(), (int32_t)train_set.size(), &obj, &frac));
+  return obj;
+}
+
+double compute_fraction(const ClusterGraph& cluster, const std::vector<int>& train_set) {
+  gp_ctx* h = any_context(cluster);
+  double frac = 0;
+  check(gp_compute_fraction(h, train_set.data(), (int32_t)train_set.size(), &frac));
+  return frac;
+}
+
+}  // namespace rlsched
+
+extern "C" long long gplan_shim_calls() { return g_calls; }
