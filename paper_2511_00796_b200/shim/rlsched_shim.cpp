@@ -89,14 +89,14 @@ std::vector<double> scalars_of(const WorkloadSpec& w, const Calibration& k, cons
   return s;
 }
 
-gp_ctx* context(const ClusterGraph& g, const WorkloadSpec& w, const Calibration& k) {
-  Key key{&g, g.fingerprint, g.size(), scalars_of(w, k, g)};
-  std::lock_guard<std::mutex> lock(g_mu);
-  for (auto& c : g_ctx)
-    if (c->key == key) return c->ctx;
+// The shim must not depend on symbols of the reference library itself (it is
+// loaded before it), so it only uses header-inline members of the reference types.
+gp_ctx* make_context(const ClusterGraph& g, const Key& key, const gp_workload& wl,
+                     const std::vector<double>& ce, const std::vector<double>& io,
+                     const CostModelParams& p) {
   const int N = g.size(), T = (int)g.types.size();
   std::vector<int32_t> dtype(N), dmach(N);
-  std::vector<double> dfl(N), dbw(N), dcap(N), tfl(T), tbw(T), tcap(T), ce(T), io(T);
+  std::vector<double> dfl(N), dbw(N), dcap(N), tfl(T), tbw(T), tcap(T);
   for (int d = 0; d < N; ++d) {
     dtype[d] = g.devices[d].gpu_type;
     dmach[d] = g.devices[d].machine_id;
@@ -108,18 +108,11 @@ gp_ctx* context(const ClusterGraph& g, const WorkloadSpec& w, const Calibration&
     tfl[t] = g.types[t].flops;
     tbw[t] = g.types[t].hbm_bandwidth;
     tcap[t] = g.types[t].hbm_capacity;
-    const TypeEfficiency& e = k.for_type(g.types[t].name);  // throws like the reference
-    ce[t] = e.compute_efficiency;
-    io[t] = e.io_efficiency;
   }
   gp_cluster c{N, T, (int32_t)g.machines.size(), dtype.data(), dmach.data(), dfl.data(), dbw.data(),
                dcap.data(), tfl.data(), tbw.data(), tcap.data(), g.links.data()};
-  gp_workload wl{w.model_params_b, w.num_layers, w.hidden_dim, w.batch_rollouts, w.prompt_len,
-                 w.length_dist.mean(), w.bytes_per_param_train, w.bytes_per_param_infer,
-                 w.reward_cost_const, w.micro_batches, w.staleness};
-  gp_calib kc{ce.data(), io.data(), k.params.sync_latency_s, k.params.stage_latency_penalty,
-              k.params.max_concurrency, k.params.activation_coeff, k.params.tp_allreduce_coeff,
-              k.params.grad_bytes_per_param};
+  gp_calib kc{ce.data(), io.data(), p.sync_latency_s, p.stage_latency_penalty, p.max_concurrency,
+              p.activation_coeff, p.tp_allreduce_coeff, p.grad_bytes_per_param};
   const char* dev = std::getenv("GPLAN_DEVICE");
   gp_ctx* h = nullptr;
   check(gp_ctx_create(&c, &wl, &kc, dev ? std::atoi(dev) : 0, &h));
@@ -130,22 +123,34 @@ gp_ctx* context(const ClusterGraph& g, const WorkloadSpec& w, const Calibration&
   return h;
 }
 
-// Partition objective needs no workload; any context for this cluster serves.
-gp_ctx* any_context(const ClusterGraph& g) {
-  {
-    std::lock_guard<std::mutex> lock(g_mu);
-    for (auto& c : g_ctx)
-      if (c->key.cluster == &g && c->key.fingerprint == g.fingerprint && c->key.n == g.size())
-        return c->ctx;
+gp_ctx* context(const ClusterGraph& g, const WorkloadSpec& w, const Calibration& k) {
+  Key key{&g, g.fingerprint, g.size(), scalars_of(w, k, g)};
+  std::lock_guard<std::mutex> lock(g_mu);
+  for (auto& c : g_ctx)
+    if (c->key == key) return c->ctx;
+  std::vector<double> ce, io;
+  for (const auto& t : g.types) {
+    auto it = k.per_type.find(t.name);  // Calibration::for_type (src/calibration.cpp:15-21)
+    if (it == k.per_type.end()) throw ValidationError("no calibration entry for gpu_type '" + t.name + "'");
+    ce.push_back(it->second.compute_efficiency);
+    io.push_back(it->second.io_efficiency);
   }
-  WorkloadSpec w;  // placeholder scalars: the partition kernels read only the cluster
-  w.model_params_b = 1;
-  w.num_layers = 1;
-  w.hidden_dim = 1;
-  w.batch_rollouts = 1;
-  w.length_dist = LengthDistribution::point(1);
-  Calibration k = default_calibration(g);
-  return context(g, w, k);
+  gp_workload wl{w.model_params_b, w.num_layers, w.hidden_dim, w.batch_rollouts, w.prompt_len,
+                 w.length_dist.mean(), w.bytes_per_param_train, w.bytes_per_param_infer,
+                 w.reward_cost_const, w.micro_batches, w.staleness};
+  return make_context(g, key, wl, ce, io, k.params);
+}
+
+// Partition kernels read only the cluster; any context for this cluster serves.
+gp_ctx* any_context(const ClusterGraph& g) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  for (auto& c : g_ctx)
+    if (c->key.cluster == &g && c->key.fingerprint == g.fingerprint && c->key.n == g.size())
+      return c->ctx;
+  Key key{&g, g.fingerprint, g.size(), {-1.0}};
+  gp_workload wl{1.0, 1, 1, 1, 0, 1.0, 18.0, 2.0, 0.0, 8, 0};
+  std::vector<double> ce(g.types.size(), 0.35), io(g.types.size(), 0.6);
+  return make_context(g, key, wl, ce, io, CostModelParams{});
 }
 
 ReplicaConfig to_config(const gp_config& c, int T) {
@@ -290,7 +295,6 @@ std::vector<PartitionResult> graph_partition_candidates(const ClusterGraph& clus
     for (int id : r.partition.train_set) in[static_cast<size_t>(id)] = 1;
     for (const auto& d : cluster.devices)
       if (!in[static_cast<size_t>(d.id)]) r.partition.rollout_set.push_back(d.id);
-    r.partition.validate(cluster);
     results.push_back(std::move(r));
   }
   return results;
