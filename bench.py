@@ -226,7 +226,8 @@ def run_b200(args):
     ids = bench_train_set(p)
     eng = Engine(p, device=local_rank)
     total = eng.train_space(ids)
-    lo, hi = total * rank // world, total * (rank + 1) // world
+    from paper_2511_00796_b200.shard import gather_winner, shard_range
+    lo, hi = shard_range(total, rank, world)
     stream = torch.cuda.ExternalStream(eng.stream_ptr, device=dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
@@ -235,14 +236,8 @@ def run_b200(args):
             dist.barrier()
 
     def gather(res):
-        """All-gather (cost, rank, feasible) of every shard; lexicographic min."""
-        t = torch.tensor([res.cost if res.found else float("inf"), float(res.rank if res.found else -1),
-                          float(res.feasible)], dtype=torch.float64, device=dev)
-        if world == 1:
-            return t.view(1, 3)
-        out = torch.empty(world, 3, dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(out, t)
-        return out
+        """All-gather (cost, rank, feasible) of every shard; lexicographic min (shard.py)."""
+        return gather_winner(bool(res.found), res.cost, res.rank, res.feasible, device=dev)
 
     # ---- device-resident timing (value) ------------------------------------
     eng.set_timing(True)
@@ -305,8 +300,7 @@ def run_b200(args):
         dist.destroy_process_group()
     if rank != 0:
         return 0
-    # argmin sanity: every rank's winner reduced lexicographically
-    best = min((tuple(x) for x in win.tolist() if x[1] >= 0), default=None)
+    best = win if win[1] >= 0 else None
     value = total * args.steps / (t_dev / 1e3)
     e2e = total * args.steps / (t_e2e / 1e3)
     # ---- roofline of the dominant kernel (K1 layout scan) -------------------
