@@ -4,7 +4,7 @@
 Workload (BASELINE.json configs[4], the largest; fits one GPU because no plan
 list is materialised): constrained_search over the C5 1024-GPU cluster
 (24x16 H800 + 24x16 H20 + 16x16 PCIe-class, 70B policy, L=80) for the 1023-device
-three-type train set -> 2,427,584,512 candidate layouts per step, window 3.
+three-type train set -> 2,415,919,104 candidate layouts per step, window 3.
 One step = one full pass over that candidate space (stage-table build + layout
 scan + argmin). At N GPUs the rank space is split into N contiguous shards
 (strong scaling), and the per-shard (cost, rank) winners are all-gathered over

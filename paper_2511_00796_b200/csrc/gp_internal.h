@@ -138,8 +138,9 @@ struct gp_ctx {
   int num_sms = 148;
   // kernel launches issued by this context (bench.py's gpu_launches claim)
   long long launches = 0;
-  // prepared train set (train.cu)
+  // prepared train set (train.cu), cached MILP lattice table (rollout.cu)
   void* train_state = nullptr;
+  void* milp_cache = nullptr;
   // optional device timing of the train phases (bench.py): events around K2 and K1
   bool timing = false;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};

@@ -113,108 +113,133 @@ struct MilpDims {
   long long states;
   long long stride[GP_MAX_TYPES];
   int cap[GP_MAX_TYPES];
-  int levels;  // sum cap + 1
+  int off[GP_MAX_TYPES];        // bit offset of coordinate t in the packed state word
+  unsigned mask[GP_MAX_TYPES];  // (1 << bits_t) - 1
+  int levels;                   // sum cap + 1
 };
 
 struct Group {
   int type;
-  int n;            // devices of the type used by each member
-  double hmax;      // max member throughput
-  int first, count; // members[first .. first+count) = config indices, ascending
+  int n;             // devices of the type used by each member
+  long long delta;   // n * stride[type]: predecessor offset
+  double hmax;       // max member throughput
+  int first, count;  // members[first .. first+count) = config indices, ascending
 };
 
-__device__ __forceinline__ int state_level(const MilpDims& d, long long s, int* coord) {
-  int l = 0;
+constexpr int kMaxGroups = 256;
+constexpr int kMaxCfg = 1024;
+
+__device__ __forceinline__ unsigned long long pack_state(const MilpDims& d, long long s, int& level) {
+  unsigned long long pk = 0;
+  level = 0;
   for (int t = d.T - 1; t >= 0; --t) {
-    coord[t] = (int)(s / d.stride[t]);
-    s -= (long long)coord[t] * d.stride[t];
-    l += coord[t];
+    const int c = (int)(s / d.stride[t]);
+    s -= (long long)c * d.stride[t];
+    level += c;
+    pk |= (unsigned long long)c << d.off[t];
   }
-  return l;
+  return pk;
 }
 
 __global__ void k4_level_hist(MilpDims d, int* __restrict__ hist) {
   for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < d.states;
        s += (long long)gridDim.x * blockDim.x) {
-    int coord[GP_MAX_TYPES];
-    atomicAdd(&hist[state_level(d, s, coord)], 1);
+    int l;
+    pack_state(d, s, l);
+    atomicAdd(&hist[l], 1);
   }
 }
 
-// exclusive scan of level counts (levels <= N+1, one CTA)
+// exclusive scan of level counts (levels <= N+1, one thread)
 __global__ void k4_level_scan(const int* __restrict__ hist, int levels, long long* __restrict__ off,
-                              int* __restrict__ cursor) {
+                              int* __restrict__ cursor, int* __restrict__ max_width) {
   if (threadIdx.x == 0) {
     long long acc = 0;
+    int mw = 0;
     for (int l = 0; l < levels; ++l) {
       off[l] = acc;
       cursor[l] = 0;
       acc += hist[l];
+      mw = hist[l] > mw ? hist[l] : mw;
     }
     off[levels] = acc;
+    *max_width = mw;
   }
 }
 
+// states of each level, as packed coordinates (order within a level is irrelevant:
+// a level's states read only lower levels)
 __global__ void k4_level_scatter(MilpDims d, const long long* __restrict__ off,
-                                 int* __restrict__ cursor, unsigned* __restrict__ order) {
+                                 int* __restrict__ cursor, unsigned long long* __restrict__ order) {
   for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < d.states;
        s += (long long)gridDim.x * blockDim.x) {
-    int coord[GP_MAX_TYPES];
-    const int l = state_level(d, s, coord);
+    int l;
+    const unsigned long long pk = pack_state(d, s, l);
     const int slot = atomicAdd(&cursor[l], 1);
-    order[off[l] + slot] = (unsigned)s;
+    order[off[l] + slot] = pk;
   }
 }
 
-__device__ __forceinline__ void relax_state(const MilpDims& d, const Group* __restrict__ groups,
-                                            int n_groups, const int* __restrict__ members,
-                                            const double* __restrict__ h, double* __restrict__ best,
-                                            int* __restrict__ choice, long long s) {
-  int coord[GP_MAX_TYPES];
-  state_level(d, s, coord);
-  double m = 0.0;  // best[s] starts at 0.0 and only a strictly larger candidate replaces it
-  for (int g = 0; g < n_groups; ++g) {
-    const Group G = groups[g];
-    if (coord[G.type] < G.n) continue;
-    const double v = best[s - (long long)G.n * d.stride[G.type]] + G.hmax;
-    m = v > m ? v : m;
-  }
-  int ch = -1;
-  if (m > 0.0) {
-    ch = INT_MAX;
-    for (int g = 0; g < n_groups; ++g) {
-      const Group G = groups[g];
-      if (coord[G.type] < G.n) continue;
-      const double bp = best[s - (long long)G.n * d.stride[G.type]];
-      if (bp + G.hmax != m) continue;
-      for (int i = 0; i < G.count; ++i) {  // members ascending: first reaching m wins
-        const int c = members[G.first + i];
-        if (c >= ch) break;
-        if (bp + h[c] == m) {
-          ch = c;
-          break;
-        }
-      }
-    }
-  }
-  best[s] = m;
-  choice[s] = ch;
-}
-
-// Persistent cooperative kernel: one grid barrier per lattice level.
-__global__ void __launch_bounds__(256) k4_dp_levels(MilpDims d, const Group* __restrict__ groups,
-                                                    int n_groups, const int* __restrict__ members,
-                                                    const double* __restrict__ h,
+// Persistent cooperative kernel: one grid barrier per lattice level. For each state,
+// one pass over the (type, devices) groups: value = max_g best[s - delta_g] + hmax_g;
+// choice = smallest config index c with best[prev_g(c)] + h_c == value.
+__global__ void __launch_bounds__(256) k4_dp_levels(MilpDims d, const Group* __restrict__ groups_g,
+                                                    int n_groups, const int* __restrict__ members_g,
+                                                    const double* __restrict__ h_g, int n_cfg,
                                                     const long long* __restrict__ off,
-                                                    const unsigned* __restrict__ order,
+                                                    const unsigned long long* __restrict__ order,
                                                     double* __restrict__ best,
                                                     int* __restrict__ choice) {
+  __shared__ Group groups[kMaxGroups];
+  __shared__ int members[kMaxCfg];
+  __shared__ double h[kMaxCfg];
+  __shared__ int shift[GP_MAX_TYPES];
+  __shared__ unsigned mask[GP_MAX_TYPES];
+  for (int i = threadIdx.x; i < n_groups; i += blockDim.x) groups[i] = groups_g[i];
+  for (int i = threadIdx.x; i < n_cfg; i += blockDim.x) {
+    members[i] = members_g[i];
+    h[i] = h_g[i];
+  }
+  if (threadIdx.x < d.T) {
+    shift[threadIdx.x] = d.off[threadIdx.x];
+    mask[threadIdx.x] = d.mask[threadIdx.x];
+  }
+  __syncthreads();
   cg::grid_group grid = cg::this_grid();
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nth = (long long)gridDim.x * blockDim.x;
   for (int l = 0; l < d.levels; ++l) {
-    for (long long i = off[l] + tid; i < off[l + 1]; i += nth)
-      relax_state(d, groups, n_groups, members, h, best, choice, order[i]);
+    const long long e = off[l + 1];
+    for (long long i = off[l] + tid; i < e; i += nth) {
+      const unsigned long long pk = order[i];
+      long long s = 0;
+      for (int t = 0; t < d.T; ++t) s += (long long)((pk >> shift[t]) & mask[t]) * d.stride[t];
+      double m = 0.0;  // best[s] starts at 0.0; only a strictly larger candidate replaces it
+      int ch = -1;
+      for (int g = 0; g < n_groups; ++g) {
+        const Group& G = groups[g];
+        if ((int)((pk >> shift[G.type]) & mask[G.type]) < G.n) continue;
+        const double bp = best[s - G.delta];
+        const double v = bp + G.hmax;
+        if (v < m) continue;
+        int c = INT_MAX;  // first member (ascending index) reaching v
+        for (int k = 0; k < G.count; ++k) {
+          const int cc = members[G.first + k];
+          if (bp + h[cc] == v) {
+            c = cc;
+            break;
+          }
+        }
+        if (v > m) {
+          m = v;
+          ch = c;
+        } else if (c < ch) {  // tie with an earlier group: smallest config index wins
+          ch = c;
+        }
+      }
+      best[s] = m;
+      choice[s] = ch;
+    }
     grid.sync();
   }
 }
@@ -227,12 +252,11 @@ struct MilpOut {
 };
 
 // Backtracking + plan assembly on one thread (src/rollout_milp.cpp:227-253).
-__global__ void k4_backtrack(MilpDims d, const gp_config* __restrict__ cfg, int n_cfg,
+__global__ void k4_backtrack(MilpDims d, long long full, const gp_config* __restrict__ cfg, int n_cfg,
                              const double* __restrict__ best, const int* __restrict__ choice,
                              double B, double len, int* __restrict__ counts,
                              gp_rollout_entry* __restrict__ entries, MilpOut* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const long long full = d.states - 1;
   const double agg = best[full];
   out->aggregate = agg;
   out->n_entries = -1;
@@ -421,6 +445,51 @@ int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opt
 }
 
 // solve_milp (src/rollout_milp.cpp:174-254)
+//
+// Lattice tables are cached per configuration list: best[s] and choice[s] depend only
+// on the state's coordinates and the configs (the recurrence never looks at the
+// capacities except as the lattice bound), so a table computed on a lattice that
+// contains the requested one answers it bit-identically. The scheduler solves many
+// MILPs with the same configs (rollout sets whose per-type machine availability
+// agrees); each is then a backtrack from its own full state.
+struct MilpCache {
+  std::vector<unsigned char> sig;  // configs + dims
+  MilpDims d{};
+  int nc = 0;
+  void* buf = nullptr;  // best | choice
+  size_t bytes = 0;
+  double* best = nullptr;
+  int* choice = nullptr;
+  bool valid = false;
+  ~MilpCache() {
+    if (buf) cudaFree(buf);
+  }
+};
+
+void milp_cache_free(gp_ctx* ctx) {
+  delete static_cast<MilpCache*>(ctx->milp_cache);
+  ctx->milp_cache = nullptr;
+}
+
+static void set_dims(MilpDims& d, int dims, const int* caps) {
+  d.T = dims;
+  long long states = 1;
+  int levels = 1, off = 0;
+  for (int t = 0; t < dims; ++t) {
+    d.stride[t] = states;
+    d.cap[t] = caps[t];
+    states *= caps[t] + 1;
+    levels += caps[t];
+    int bits = 1;
+    while ((1 << bits) <= caps[t]) ++bits;
+    d.off[t] = off;
+    d.mask[t] = (1u << bits) - 1u;
+    off += bits;
+  }
+  d.states = states;
+  d.levels = levels;
+}
+
 int solve_milp(gp_ctx* ctx, const gp_config* cfg, int nc, const int32_t* caps, int dims, double B,
                double len, gp_rollout_result* out, gp_rollout_entry* entries) {
   std::memset(out, 0, sizeof *out);
@@ -428,120 +497,168 @@ int solve_milp(gp_ctx* ctx, const gp_config* cfg, int nc, const int32_t* caps, i
   if (B <= 0) return GP_OK;
   if (nc == 0) return set_error(GP_INFEASIBLE, "no replica configuration available");
   if (dims < 1 || dims > GP_MAX_TYPES) return set_error(GP_INVALID, "dims must lie in [1, GP_MAX_TYPES]");
-  MilpDims d{};
-  d.T = dims;
+  if (nc > kMaxCfg) return set_error(GP_INVALID, "too many replica configurations for the sm_100a kernel");
   long long states = 1;
-  int levels = 1;
   for (int t = 0; t < dims; ++t) {
     if (caps[t] < 0) return set_error(GP_INVALID, "negative capacity");
-    d.stride[t] = states;
-    d.cap[t] = caps[t];
     states *= caps[t] + 1;
-    levels += caps[t];
     if (states > 50000000) return set_error(GP_INVALID, "capacity lattice too large for the exact solver");
   }
-  d.states = states;
-  d.levels = levels;
   out->states = states;
   // groups of configs with the same (type, device count): one predecessor each
-  std::vector<Group> groups;
-  std::vector<int> members;
-  {
-    std::vector<std::pair<long long, int>> key;  // (type * 1e6 + n, index)
-    for (int c = 0; c < nc; ++c) {
-      int t = -1, n = 0, used = 0;
-      for (int u = 0; u < dims; ++u)
-        if (cfg[c].type_counts[u] > 0) {
-          if (t < 0) t = u;
-          ++used;
-          n = cfg[c].type_counts[u];
-        }
-      if (used != 1 || n <= 0)
-        return set_error(GP_INVALID, "solve_milp on the GPU requires type-pure configs using >= 1 device");
-      key.push_back({(long long)t * 1000000 + n, c});
+  std::vector<std::pair<long long, int>> key;
+  for (int c = 0; c < nc; ++c) {
+    int t = -1, n = 0, used = 0;
+    for (int u = 0; u < dims; ++u)
+      if (cfg[c].type_counts[u] > 0) {
+        if (t < 0) t = u;
+        ++used;
+        n = cfg[c].type_counts[u];
+      }
+    if (used != 1 || n <= 0)
+      return set_error(GP_INVALID, "solve_milp on the GPU requires type-pure configs using >= 1 device");
+    key.push_back({(long long)t * 1000000 + n, c});
+  }
+  std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  // cache lookup: same configs and dims, lattice covering caps
+  if (!ctx->milp_cache) ctx->milp_cache = new MilpCache();
+  MilpCache& mc = *static_cast<MilpCache*>(ctx->milp_cache);
+  std::vector<unsigned char> sig(sizeof(gp_config) * nc + sizeof(int));
+  std::memcpy(sig.data(), cfg, sizeof(gp_config) * nc);
+  std::memcpy(sig.data() + sizeof(gp_config) * nc, &dims, sizeof(int));
+  bool hit = mc.valid && mc.sig == sig;
+  for (int t = 0; t < dims && hit; ++t) hit = caps[t] <= mc.d.cap[t];
+  if (!hit) {
+    // lattice to tabulate: the union with the cached one when the configs agree and it fits
+    std::vector<int> lat(caps, caps + dims);
+    if (mc.valid && mc.sig == sig) {
+      long long u = 1;
+      std::vector<int> un(dims);
+      for (int t = 0; t < dims; ++t) {
+        un[t] = std::max(caps[t], mc.d.cap[t]);
+        u *= un[t] + 1;
+      }
+      if (u <= 50000000) lat = un;
     }
-    std::stable_sort(key.begin(), key.end(),
-                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    MilpDims d{};
+    set_dims(d, dims, lat.data());
+    std::vector<Group> groups;
+    std::vector<int> members;
     for (size_t i = 0; i < key.size();) {
       size_t j = i;
-      Group G{(int)(key[i].first / 1000000), (int)(key[i].first % 1000000), 0.0, (int)members.size(), 0};
-      double hmax = cfg[key[i].second].throughput;
+      const int t = (int)(key[i].first / 1000000), n = (int)(key[i].first % 1000000);
+      Group G{t, n, (long long)n * d.stride[t], cfg[key[i].second].throughput, (int)members.size(), 0};
       while (j < key.size() && key[j].first == key[i].first) {
         members.push_back(key[j].second);
-        const double h = cfg[key[j].second].throughput;
-        hmax = hmax < h ? h : hmax;
+        const double hh = cfg[key[j].second].throughput;
+        G.hmax = G.hmax < hh ? hh : G.hmax;
         ++j;
       }
-      G.hmax = hmax;
       G.count = (int)(j - i);
       groups.push_back(G);
       i = j;
     }
+    const int ng = (int)groups.size();
+    if (ng > kMaxGroups) return set_error(GP_INVALID, "too many config groups for the sm_100a kernel");
+    std::vector<double> hs(nc);
+    for (int c = 0; c < nc; ++c) hs[c] = cfg[c].throughput;
+    // table buffers (persistent)
+    const size_t tbytes = (((size_t)d.states * sizeof(double) + 255) & ~size_t(255)) + (size_t)d.states * sizeof(int) + 256;
+    if (tbytes > mc.bytes) {
+      if (mc.buf) cudaFree(mc.buf);
+      mc.buf = nullptr;
+      mc.bytes = 0;
+      mc.valid = false;
+      GP_CUDA(cudaMalloc(&mc.buf, tbytes));
+      mc.bytes = tbytes;
+    }
+    mc.best = static_cast<double*>(mc.buf);
+    mc.choice = reinterpret_cast<int*>(static_cast<char*>(mc.buf) +
+                                       (((size_t)d.states * sizeof(double) + 255) & ~size_t(255)));
+    // scratch: groups, members, h, level tables, packed order
+    size_t bytes = 0;
+    auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+    add(sizeof(Group) * ng);
+    add(sizeof(int) * nc);
+    add(sizeof(double) * nc);
+    add(sizeof(int) * d.levels);
+    add(sizeof(long long) * (d.levels + 1));
+    add(sizeof(int) * d.levels);
+    add(sizeof(int));
+    add(sizeof(unsigned long long) * d.states);
+    char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaRollout));
+    if (!base) return GP_CUDA_ERROR;
+    char* p = base;
+    Group* d_groups = carve2<Group>(p, ng);
+    int* d_members = carve2<int>(p, nc);
+    double* d_h = carve2<double>(p, nc);
+    int* d_hist = carve2<int>(p, d.levels);
+    long long* d_off = carve2<long long>(p, d.levels + 1);
+    int* d_cursor = carve2<int>(p, d.levels);
+    int* d_maxw = carve2<int>(p, 1);
+    unsigned long long* d_order = carve2<unsigned long long>(p, d.states);
+    const size_t in_bytes = (size_t)((char*)(d_h + nc) - (char*)d_groups);
+    char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, (size_t)4096)));
+    if (!hp) return GP_CUDA_ERROR;
+    GP_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(hp, groups.data(), sizeof(Group) * ng);
+    std::memcpy(hp + ((char*)d_members - (char*)d_groups), members.data(), sizeof(int) * nc);
+    std::memcpy(hp + ((char*)d_h - (char*)d_groups), hs.data(), sizeof(double) * nc);
+    GP_CUDA(cudaMemcpyAsync(d_groups, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->h2d_bytes += (long long)in_bytes;
+    GP_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int) * d.levels, ctx->stream));
+    const int sweep_blocks = (int)std::min<long long>((d.states + 255) / 256, (long long)ctx->num_sms * 16);
+    k4_level_hist<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_hist);
+    k4_level_scan<<<1, 32, 0, ctx->stream>>>(d_hist, d.levels, d_off, d_cursor, d_maxw);
+    k4_level_scatter<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_off, d_cursor, d_order);
+    ctx->launches += 3;
+    int* h_maxw = reinterpret_cast<int*>(hp);
+    GP_CUDA(cudaMemcpyAsync(h_maxw, d_maxw, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    GP_CUDA(cudaStreamSynchronize(ctx->stream));
+    static int occ = 0;
+    if (!occ) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_dp_levels, 256, 0);
+      occ = std::max(1, occ);
+    }
+    // grid: enough blocks for the widest level, at most what is co-resident
+    int dp_blocks = (int)std::min<long long>((long long)ctx->num_sms * occ, ((long long)*h_maxw + 255) / 256);
+    dp_blocks = std::max(1, dp_blocks);
+    int ng_arg = ng, nc_arg = nc;
+    double* best = mc.best;
+    int* choice = mc.choice;
+    void* args[] = {&d, &d_groups, &ng_arg, &d_members, &d_h, &nc_arg, &d_off, &d_order, &best, &choice};
+    GP_CUDA(cudaLaunchCooperativeKernel((void*)k4_dp_levels, dp_blocks, 256, args, 0, ctx->stream));
+    ctx->launches++;
+    mc.d = d;
+    mc.nc = nc;
+    mc.sig = sig;
+    mc.valid = true;
   }
-  const int ng = (int)groups.size();
-  std::vector<double> hs(nc);
-  for (int c = 0; c < nc; ++c) hs[c] = cfg[c].throughput;
-  // device buffers
+  // backtrack from this lattice's full state inside the cached table
+  long long full = 0;
+  for (int t = 0; t < dims; ++t) full += (long long)caps[t] * mc.d.stride[t];
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
   add(sizeof(gp_config) * nc);
-  add(sizeof(Group) * ng);
-  add(sizeof(int) * nc);
-  add(sizeof(double) * nc);
-  add(sizeof(int) * levels);
-  add(sizeof(long long) * (levels + 1));
-  add(sizeof(int) * levels);
-  add(sizeof(unsigned) * states);
-  add(sizeof(double) * states);
-  add(sizeof(int) * states);
   add(sizeof(int) * nc);
   add(sizeof(gp_rollout_entry) * nc);
   add(sizeof(MilpOut));
-  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaRollout));
+  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaMisc));
   if (!base) return GP_CUDA_ERROR;
   char* p = base;
   gp_config* d_cfg = carve2<gp_config>(p, nc);
-  Group* d_groups = carve2<Group>(p, ng);
-  int* d_members = carve2<int>(p, nc);
-  double* d_h = carve2<double>(p, nc);
-  int* d_hist = carve2<int>(p, levels);
-  long long* d_off = carve2<long long>(p, levels + 1);
-  int* d_cursor = carve2<int>(p, levels);
-  unsigned* d_order = carve2<unsigned>(p, states);
-  double* d_best = carve2<double>(p, states);
-  int* d_choice = carve2<int>(p, states);
   int* d_counts = carve2<int>(p, nc);
   gp_rollout_entry* d_entries = carve2<gp_rollout_entry>(p, nc);
   MilpOut* d_mo = carve2<MilpOut>(p, 1);
-  const size_t in_bytes = (size_t)((char*)(d_h + nc) - (char*)d_cfg);
-  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(MilpOut) + sizeof(gp_rollout_entry) * nc + 256)));
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(sizeof(gp_config) * nc, sizeof(MilpOut) + sizeof(gp_rollout_entry) * nc + 256)));
   if (!hp) return GP_CUDA_ERROR;
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
   std::memcpy(hp, cfg, sizeof(gp_config) * nc);
-  std::memcpy(hp + ((char*)d_groups - (char*)d_cfg), groups.data(), sizeof(Group) * ng);
-  std::memcpy(hp + ((char*)d_members - (char*)d_cfg), members.data(), sizeof(int) * nc);
-  std::memcpy(hp + ((char*)d_h - (char*)d_cfg), hs.data(), sizeof(double) * nc);
-  GP_CUDA(cudaMemcpyAsync(d_cfg, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
-  ctx->h2d_bytes += (long long)in_bytes;
-  GP_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int) * levels, ctx->stream));
-  const int sweep_blocks = (int)std::min<long long>((states + 255) / 256, (long long)ctx->num_sms * 16);
-  k4_level_hist<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_hist);
-  k4_level_scan<<<1, 32, 0, ctx->stream>>>(d_hist, levels, d_off, d_cursor);
-  k4_level_scatter<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_off, d_cursor, d_order);
-  ctx->launches += 3;
-  // cooperative persistent DP over levels
-  static int occ = 0;
-  if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_dp_levels, 256, 0);
-    occ = std::max(1, occ);
-  }
-  int dp_blocks = (int)std::min<long long>((long long)ctx->num_sms * occ, (states + 255) / 256);
-  dp_blocks = std::max(1, dp_blocks);
-  void* args[] = {&d, &d_groups, (void*)&ng, &d_members, &d_h, &d_off, &d_order, &d_best, &d_choice};
-  int ng_arg = ng;
-  args[2] = &ng_arg;
-  GP_CUDA(cudaLaunchCooperativeKernel((void*)k4_dp_levels, dp_blocks, 256, args, 0, ctx->stream));
-  k4_backtrack<<<1, 32, 0, ctx->stream>>>(d, d_cfg, nc, d_best, d_choice, B, len, d_counts, d_entries, d_mo);
-  ctx->launches += 2;
+  GP_CUDA(cudaMemcpyAsync(d_cfg, hp, sizeof(gp_config) * nc, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)(sizeof(gp_config) * nc);
+  k4_backtrack<<<1, 32, 0, ctx->stream>>>(mc.d, full, d_cfg, nc, mc.best, mc.choice, B, len, d_counts,
+                                          d_entries, d_mo);
+  ctx->launches++;
   GP_CUDA(cudaGetLastError());
   MilpOut* ho = reinterpret_cast<MilpOut*>(hp);
   gp_rollout_entry* he = reinterpret_cast<gp_rollout_entry*>(hp + 256);
