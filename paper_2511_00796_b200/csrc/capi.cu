@@ -21,6 +21,7 @@ int train_launch(gp_ctx* ctx, int window, long long lo, long long hi);
 int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices);
 void train_state_free(gp_ctx* ctx);
 void milp_cache_free(gp_ctx* ctx);
+void part_cache_free(gp_ctx* ctx);
 int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opts* o, gp_config* out,
                     int cap, int* n_out);
 int rollout_capacities(gp_ctx* ctx, const int32_t* ids, int n, int32_t* caps);
@@ -243,6 +244,7 @@ void gp_ctx_destroy(gp_ctx* ctx) {
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   train_state_free(ctx);
   milp_cache_free(ctx);
+  part_cache_free(ctx);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -141,6 +141,7 @@ struct gp_ctx {
   // prepared train set (train.cu), cached MILP lattice table (rollout.cu)
   void* train_state = nullptr;
   void* milp_cache = nullptr;
+  void* part_cache[2] = {nullptr, nullptr};  // partition unit tables per granularity (partition.cu)
   // optional device timing of the train phases (bench.py): events around K2 and K1
   bool timing = false;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};

@@ -80,23 +80,36 @@ __global__ void k5_units(int n, const int* __restrict__ mem_off, const int* __re
 }
 
 // totals: sequential folds in unit order (src/partition.cpp:75-79)
+// The total-link fold is inherently sequential (fp order); the CTA streams each row of
+// the cross matrix into shared memory (double-buffered) so the folding thread only
+// waits on DADD latency, not on L2.
 __global__ void k5_totals(Units u, Totals* __restrict__ tot, double* __restrict__ base_score) {
-  __shared__ double s_tl;
+  constexpr int kChunk = 2048;
+  __shared__ double row[2][kChunk];
+  double tl = 0;
+  int buf = 0;
+  for (int i = 0; i < u.n; ++i) {
+    if (threadIdx.x == 0) tl += u.internal[i];
+    for (int c0 = i + 1; c0 < u.n; c0 += kChunk) {
+      const int c1 = min(u.n, c0 + kChunk);
+      for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) row[buf][j - c0] = u.cross[(size_t)i * u.n + j];
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int j = 0; j < c1 - c0; ++j) tl += row[buf][j];
+      buf ^= 1;  // the next chunk fills the other buffer while thread 0 folds this one
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    double tf = 0.0, th = 0.0, tl = 0;
+    double tf = 0.0, th = 0.0;
     for (int i = 0; i < u.n; ++i) tf += u.flops[i];
     for (int i = 0; i < u.n; ++i) th += u.hbm[i];
-    for (int i = 0; i < u.n; ++i) {
-      tl += u.internal[i];
-      for (int j = i + 1; j < u.n; ++j) tl += u.cross[(size_t)i * u.n + j];
-    }
     tot->flops = tf;
     tot->hbm = th;
     tot->link = tl;
     tot->y_flops = 1.0 / tf;
     tot->y_hbm = 1.0 / th;
     tot->y_link = tl > 0 ? 1.0 / tl : 0.0;
-    s_tl = tl;
   }
   __syncthreads();
   // local_search base score (src/partition.cpp:273-282): per unit, fold over j != i
@@ -212,7 +225,10 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
   int* order = reinterpret_cast<int*>(key + n);
   int* tr = order + n;                         // train unit list (ascending)
   int* ro = tr + n;                            // rollout unit list (ascending)
-  unsigned char* in_tr = reinterpret_cast<unsigned char*>(ro + n);
+  double* uf = reinterpret_cast<double*>(ro + n + (n & 1));  // unit flops / hbm / internal (smem copies)
+  double* uh = uf + n;
+  double* ui = uh + n;
+  unsigned char* in_tr = reinterpret_cast<unsigned char*>(ui + n);
   __shared__ SState S;
   __shared__ Cand red[32];
   __shared__ int ired[32];
@@ -231,6 +247,9 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
     key[i] = sc;
     ltt[i] = 0;
     in_tr[i] = 0;
+    uf[i] = u.flops[i];
+    uh[i] = u.hbm[i];
+    ui[i] = u.internal[i];
   }
   __syncthreads();
   // stable sort by score desc: rank_i = #{score_j > score_i} + #{j < i : score_j == score_i}
@@ -258,9 +277,9 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
   auto add = [&](int i) {
     __syncthreads();
     if (tid == 0) {
-      S.link_train += ltt[i] + u.internal[i];
-      S.hbm_train += u.hbm[i];
-      S.flops_train += u.flops[i];
+      S.link_train += ltt[i] + ui[i];
+      S.hbm_train += uh[i];
+      S.flops_train += uf[i];
       S.count++;
       in_tr[i] = 1;
     }
@@ -276,9 +295,9 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
     __syncthreads();
     if (tid == 0) {
       in_tr[i] = 0;
-      S.link_train -= ltt[i] + u.internal[i];
-      S.hbm_train -= u.hbm[i];
-      S.flops_train -= u.flops[i];
+      S.link_train -= ltt[i] + ui[i];
+      S.hbm_train -= uh[i];
+      S.flops_train -= uf[i];
       S.count--;
     }
     __syncthreads();
@@ -289,7 +308,7 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
     int bi = INT_MAX;
     for (int i = tid; i < n; i += nth) {
       if (in_tr[i] != want) continue;
-      const double f = u.flops[i];
+      const double f = uf[i];
       if (bi == INT_MAX || f < bv || (f == bv && i < bi)) {
         bv = f;
         bi = i;
@@ -327,7 +346,7 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
       for (int oi = tid; oi < n; oi += nth) {
         const int i = order[oi];
         if (in_tr[i]) continue;
-        if (frac(S.flops_train + u.flops[i]) <= hi + 1e-15) best_o = min(best_o, oi);
+        if (frac(S.flops_train + uf[i]) <= hi + 1e-15) best_o = min(best_o, oi);
       }
       for (int o = 16; o > 0; o >>= 1) best_o = min(best_o, __shfl_xor_sync(0xffffffffu, best_o, o));
       __syncthreads();
@@ -383,29 +402,39 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
       const bool to_train = !in_tr[i];
       if (to_train && cnt + 1 == n) continue;
       if (!to_train && cnt == 1) continue;
-      const double ftm = ft0 + (to_train ? u.flops[i] : -u.flops[i]);
+      const double ftm = ft0 + (to_train ? uf[i] : -uf[i]);
       if (!in_band(frac(ftm))) continue;
       double lt = lt0;
-      if (to_train) lt += ltt[i] + u.internal[i];
-      else lt -= ltt[i] + u.internal[i];
-      const double hbm = hb0 + (to_train ? u.hbm[i] : -u.hbm[i]);
+      if (to_train) lt += ltt[i] + ui[i];
+      else lt -= ltt[i] + ui[i];
+      const double hbm = hb0 + (to_train ? uh[i] : -uh[i]);
       const double obj = (T.link > 0 ? div_rn_recip2(lt, T.link, T.y_link) : 0) +
                          div_rn_recip2(T.hbm - hbm, T.hbm, T.y_hbm);
       const Cand c{obj - cur, i};
       if (c.gain > best.gain) best = c;  // i ascending per thread: strict '>' keeps the first
     }
-    const long long npairs = (long long)ntr * nro;
-    for (long long p = tid; p < npairs; p += nth) {  // swaps: a in train asc, b in rollout asc
-      const int a = tr[p / nro], b = ro[p % nro];
-      const double fts = ft0 - u.flops[a] + u.flops[b];
-      if (!in_band(frac(fts))) continue;
-      const double lt = lt0 - (ltt[a] + u.internal[a]) + (ltt[b] + u.internal[b]) -
-                        u.cross[(size_t)a * n + b];
-      const double hbm = hb0 - u.hbm[a] + u.hbm[b];
-      const double obj = (T.link > 0 ? div_rn_recip2(lt, T.link, T.y_link) : 0) +
-                         div_rn_recip2(T.hbm - hbm, T.hbm, T.y_hbm);
-      const Cand c{obj - cur, n + a * n + b};
-      if (c.gain > best.gain) best = c;
+    // swaps, scan order a in train ascending, b in rollout ascending: one warp per row a,
+    // lanes over b; lb = link_to_train + internal per unit for this step
+    double* lb = key;  // free after the ordering
+    for (int i = tid; i < n; i += nth) lb[i] = ltt[i] + ui[i];
+    __syncthreads();
+    const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
+    for (int ia = warp; ia < ntr; ia += nwarps) {
+      const int a = tr[ia];
+      const double Fa = ft0 - uf[a];  // (flops_train - f[a]) + f[b]
+      const double Xa = lt0 - lb[a];  // ((link_train - (ltt[a]+int[a])) + (ltt[b]+int[b])) - cross
+      const double Ha = hb0 - uh[a];  // (hbm_train - hbm[a]) + hbm[b]
+      const double* crow = u.cross + (size_t)a * n;
+      for (int ib = lane; ib < nro; ib += 32) {
+        const int b = ro[ib];
+        if (!in_band(frac(Fa + uf[b]))) continue;
+        const double lt = Xa + lb[b] - crow[b];
+        const double hbm = Ha + uh[b];
+        const double obj = (T.link > 0 ? div_rn_recip2(lt, T.link, T.y_link) : 0) +
+                           div_rn_recip2(T.hbm - hbm, T.hbm, T.y_hbm);
+        const Cand c{obj - cur, n + a * n + b};
+        if (c.gain > best.gain) best = c;
+      }
     }
     const Cand w = block_best(best, red);
     if (w.pos == INT_MAX) break;
@@ -610,6 +639,26 @@ static T* carve3(char*& p, size_t count) {
   return r;
 }
 
+// Unit tables of one granularity (device or machine units): cluster-only data.
+struct PartCache {
+  int n = 0;
+  void* buf = nullptr;
+  int* off = nullptr;
+  int* ids = nullptr;
+  double *uf = nullptr, *uh = nullptr, *ui = nullptr, *base = nullptr, *cross = nullptr;
+  Totals* tot = nullptr;
+  ~PartCache() {
+    if (buf) cudaFree(buf);
+  }
+};
+
+void part_cache_free(gp_ctx* ctx) {
+  for (auto& p : ctx->part_cache) {
+    delete static_cast<PartCache*>(p);
+    p = nullptr;
+  }
+}
+
 int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, int k, gp_partition* out,
                          int32_t* train_ids, int32_t* n_out) {
   *n_out = 0;
@@ -639,14 +688,49 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
   const double lo = g->gamma_l - o->band_epsilon, hi = g->gamma_h + o->band_epsilon;
   const bool exact = !o->force_local_search && n <= o->exact_threshold && n <= 20;
   const int n_offers = exact ? (int)((1ull << n) - 2) : o->restarts;
-  // ---- device buffers
+  // ---- unit tables: built once per (context, granularity) — they depend only on the cluster
+  PartCache*& pc = reinterpret_cast<PartCache**>(ctx->part_cache)[by_machine ? 1 : 0];
+  if (!pc) {
+    pc = new PartCache();
+    pc->n = n;
+    size_t ub = 0;
+    auto uadd = [&](size_t b) { ub += ((b + 255) & ~size_t(255)) + 256; };
+    uadd(sizeof(int) * (n + 1));
+    uadd(sizeof(int) * N);
+    uadd(sizeof(double) * n * 4);
+    uadd(sizeof(double) * (size_t)n * n);
+    uadd(sizeof(Totals));
+    GP_CUDA(cudaMalloc(&pc->buf, ub));
+    char* q = static_cast<char*>(pc->buf);
+    pc->off = carve3<int>(q, n + 1);
+    pc->ids = carve3<int>(q, N);
+    pc->uf = carve3<double>(q, n);
+    pc->uh = carve3<double>(q, n);
+    pc->ui = carve3<double>(q, n);
+    pc->base = carve3<double>(q, n);
+    pc->cross = carve3<double>(q, (size_t)n * n);
+    pc->tot = carve3<Totals>(q, 1);
+    const size_t in_bytes = (size_t)((char*)(pc->ids + N) - (char*)pc->off);
+    char* hp0 = static_cast<char*>(ctx_pinned(ctx, in_bytes + 64));
+    if (!hp0) return GP_CUDA_ERROR;
+    GP_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(hp0, mem_off.data(), sizeof(int) * (n + 1));
+    std::memcpy(hp0 + ((char*)pc->ids - (char*)pc->off), mem_ids.data(), sizeof(int) * N);
+    GP_CUDA(cudaMemcpyAsync(pc->off, hp0, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->h2d_bytes += (long long)in_bytes;
+    const Units u0{n, pc->uf, pc->uh, pc->ui, pc->cross, pc->off, pc->ids};
+    k5_units<<<n, 128, 0, ctx->stream>>>(n, pc->off, pc->ids, ctx->d_flops, ctx->d_hbm_bw, ctx->d_links, N,
+                                        pc->uf, pc->uh, pc->ui, pc->cross);
+    k5_totals<<<1, 256, 0, ctx->stream>>>(u0, pc->tot, pc->base);
+    ctx->launches += 2;
+    GP_CUDA(cudaGetLastError());
+  }
+  const Units u{n, pc->uf, pc->uh, pc->ui, pc->cross, pc->off, pc->ids};
+  Totals* d_tot = pc->tot;
+  double* d_base = pc->base;
+  // ---- per-call buffers
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
-  add(sizeof(int) * (n + 1));
-  add(sizeof(int) * N);
-  add(sizeof(double) * n * 4);
-  add(sizeof(double) * (size_t)n * n);
-  add(sizeof(Totals));
   add(sizeof(Offer) * std::max(n_offers, 1));
   add(sizeof(RestartOut) * std::max(o->restarts, 1));
   add((size_t)std::max(n_offers, 1) * n);
@@ -659,14 +743,6 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
   char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaPartition));
   if (!base) return GP_CUDA_ERROR;
   char* p = base;
-  int* d_off = carve3<int>(p, n + 1);
-  int* d_ids = carve3<int>(p, N);
-  double* d_uf = carve3<double>(p, n);
-  double* d_uh = carve3<double>(p, n);
-  double* d_ui = carve3<double>(p, n);
-  double* d_base = carve3<double>(p, n);
-  double* d_cross = carve3<double>(p, (size_t)n * n);
-  Totals* d_tot = carve3<Totals>(p, 1);
   Offer* d_offer = carve3<Offer>(p, std::max(n_offers, 1));
   RestartOut* d_rout = carve3<RestartOut>(p, std::max(o->restarts, 1));
   unsigned char* d_mask = carve3<unsigned char>(p, (size_t)std::max(n_offers, 1) * n);
@@ -676,23 +752,13 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
   TopKOut* d_tk = carve3<TopKOut>(p, 1);
   int* d_tids = carve3<int>(p, (size_t)N * k);
   double* d_frac = carve3<double>(p, k);
-  const size_t in_bytes = (size_t)((char*)(d_ids + N) - (char*)d_off);
-  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(TopKOut) + sizeof(int) * (size_t)N * k + sizeof(double) * k + 1024)));
+  char* hp = static_cast<char*>(ctx_pinned(ctx, sizeof(TopKOut) + sizeof(int) * (size_t)N * k + sizeof(double) * k + 1024));
   if (!hp) return GP_CUDA_ERROR;
-  std::memcpy(hp, mem_off.data(), sizeof(int) * (n + 1));
-  std::memcpy(hp + ((char*)d_ids - (char*)d_off), mem_ids.data(), sizeof(int) * N);
-  GP_CUDA(cudaMemcpyAsync(d_off, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
-  ctx->h2d_bytes += (long long)in_bytes;
-  Units u{n, d_uf, d_uh, d_ui, d_cross, d_off, d_ids};
-  k5_units<<<n, 128, 0, ctx->stream>>>(n, d_off, d_ids, ctx->d_flops, ctx->d_hbm_bw, ctx->d_links, N, d_uf,
-                                      d_uh, d_ui, d_cross);
-  k5_totals<<<1, 256, 0, ctx->stream>>>(u, d_tot, d_base);
-  ctx->launches += 2;
   if (exact) {
     k5_exact<<<(n_offers + 255) / 256, 256, 0, ctx->stream>>>(u, d_tot, lo, hi, d_offer);
     ctx->launches++;
   } else if (o->restarts > 0) {
-    const size_t sm = sizeof(double) * 2 * n + sizeof(int) * 3 * n + n + 16;
+    const size_t sm = sizeof(double) * 5 * n + sizeof(int) * (3 * n + 2) + n + 64;
     if (sm > 227 * 1024) return set_error(GP_INVALID, "partition units exceed shared memory");
     GP_CUDA(cudaFuncSetAttribute(k5_restart, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k5_restart<<<o->restarts, kK5Threads, sm, ctx->stream>>>(u, d_tot, d_base, lo, hi, o->restarts,

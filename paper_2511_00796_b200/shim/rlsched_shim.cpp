@@ -317,3 +317,10 @@ double compute_fraction(const ClusterGraph& cluster, const std::vector<int>& tra
 }  // namespace rlsched
 
 extern "C" long long gplan_shim_calls() { return g_calls; }
+
+// Drops every engine context (and with them the cached MILP lattice tables); the CUDA
+// runtime stays initialised. Used to time "warm process, cold caches" runs.
+extern "C" void gplan_shim_reset() {
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_ctx.clear();
+}

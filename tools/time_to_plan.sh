@@ -4,8 +4,8 @@
 KEYS=${1:-"c1_desk_mixed/eta=1 c2_16gpu/eta=2 c3_64gpu/eta=1"}
 echo "== engine (drop-in)"
 for k in $KEYS; do
-  LD_PRELOAD=$PWD/paper_2511_00796_b200/libgplan_shim.so timeout ${TTP_TIMEOUT:-900} python tests/dropin_driver.py $k | \
-    python -c "import json,sys; [print(d['key'], 'seconds %.3f'%d['seconds'], 'calls', d['engine_calls'], 'window', d['plan']['window_steps'], 'obj', max(d['plan']['costs']['train_s'], d['plan']['costs']['infer_total_s'])) for d in map(json.loads, sys.stdin)]"
+  DROPIN_RUNS=2 LD_PRELOAD=$PWD/paper_2511_00796_b200/libgplan_shim.so timeout ${TTP_TIMEOUT:-900} python tests/dropin_driver.py $k | \
+    python -c "import json,sys; [print(d['key'], 'cold %.3f s'%d['seconds'], 'warm %.3f s'%d['warm_seconds'], 'calls', d['engine_calls'], 'window', d['plan']['window_steps'], 'obj', max(d['plan']['costs']['train_s'], d['plan']['costs']['infer_total_s'])) for d in map(json.loads, sys.stdin)]"
 done
 if [ "$2" == "cpu" ]; then
   echo "== reference on host CPU"
