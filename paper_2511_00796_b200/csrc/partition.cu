@@ -473,7 +473,7 @@ __global__ void k5_unpack_offers(const Offer* __restrict__ of, const RestartOut*
 struct TopItem {
   double obj;
   int count;     // train devices
-  int src;       // offer index (row into the offer-mask table)
+  int src;       // offer index
 };
 
 struct TopKOut {
@@ -482,103 +482,140 @@ struct TopKOut {
   TopItem item[64];
 };
 
-// Train device ids of offer `o` (sorted: units hold ascending contiguous ids).
-__device__ int offer_ids(const Units& u, const unsigned char* __restrict__ in_train, int o,
-                         int* __restrict__ buf) {
-  int c = 0;
-  for (int i = 0; i < u.n; ++i) {
-    if (!in_train[(size_t)o * u.n + i]) continue;
-    for (int m = u.mem_off[i]; m < u.mem_off[i + 1]; ++m) buf[c++] = u.mem_ids[m];
+// One warp per offer: its train device ids (sorted: units hold ascending, contiguous
+// ids) and its per-machine footprint (TopK's equivalence key, src/partition.cpp:186-190).
+__global__ void k5_offer_lists(Units u, const unsigned char* __restrict__ in_train,
+                               const int* __restrict__ valid, int n_offers, const int* __restrict__ dmachine,
+                               int M, int N, int* __restrict__ ids, int* __restrict__ counts,
+                               int* __restrict__ foot) {
+  const int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (o >= n_offers) return;
+  int* f = foot + (size_t)o * M;
+  for (int m = lane; m < M; m += 32) f[m] = 0;
+  __syncwarp();
+  if (!valid[o]) {
+    if (lane == 0) counts[o] = 0;
+    return;
   }
-  return c;
+  int base = 0;
+  for (int c = 0; c < u.n; c += 32) {
+    const int i = c + lane;
+    const bool t = i < u.n && in_train[(size_t)o * u.n + i];
+    const int nm = t ? u.mem_off[i + 1] - u.mem_off[i] : 0;
+    int incl = nm;  // inclusive prefix sum of member counts
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int excl = base + incl - nm;
+    for (int k = 0; k < nm; ++k) {
+      const int id = u.mem_ids[u.mem_off[i] + k];
+      ids[(size_t)o * N + excl + k] = id;
+      atomicAdd(&f[dmachine[id]], 1);
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) counts[o] = base;
 }
 
-__device__ bool lex_less(const int* a, int na, const int* b, int nb) {
+// warp-cooperative lexicographic a < b
+__device__ bool warp_lex_less(const int* a, int na, const int* b, int nb) {
+  const int lane = threadIdx.x & 31;
   const int m = na < nb ? na : nb;
-  for (int i = 0; i < m; ++i)
-    if (a[i] != b[i]) return a[i] < b[i];
+  for (int c = 0; c < m; c += 32) {
+    const int i = c + lane;
+    const bool diff = i < m && a[i] != b[i];
+    const unsigned bal = __ballot_sync(0xffffffffu, diff);
+    if (bal) {
+      const int j = c + __ffs(bal) - 1;
+      return a[j] < b[j];
+    }
+  }
   return na < nb;
 }
 
-// Replays TopK::offer in offer order (single thread). Offers with valid == 0 are skipped.
-__global__ void k5_topk(Units u, const unsigned char* __restrict__ in_train, const double* __restrict__ objs,
-                        const int* __restrict__ valid, int n_offers, int k, const int* __restrict__ dmachine,
-                        int M, int* __restrict__ work /* 3 * N + M * (k + 2) ints */, TopKOut* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const int N = u.mem_off[u.n];
-  int* ids = work;              // candidate ids
-  int* ids2 = work + N;         // scratch
-  int* foot = work + 2 * N;     // per item footprint: M ints each, (k+1) items, + candidate
-  int* cand_foot = foot + (size_t)M * (k + 1);
+__device__ bool warp_equal(const int* a, const int* b, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int c = 0; c < n; c += 32) {
+    const int i = c + lane;
+    if (__any_sync(0xffffffffu, i < n && a[i] != b[i])) return false;
+  }
+  return true;
+}
+
+// Replays TopK::offer (src/partition.cpp:183-201) in offer order with one warp:
+// merge into an equivalent entry (|dobj| <= 1e-12 and same footprint) keeping the
+// lexicographically smaller train set (no re-sort), else push_back + sort + trim.
+__global__ void k5_topk(const double* __restrict__ objs, const int* __restrict__ valid, int n_offers, int k,
+                        int M, int N, const int* __restrict__ ids, const int* __restrict__ counts,
+                        const int* __restrict__ foot, TopKOut* __restrict__ out) {
+  __shared__ TopItem items[65];
   int n_items = 0;
-  TopItem items[65];
   for (int o = 0; o < n_offers; ++o) {
     if (!valid[o]) continue;
     const double obj = objs[o];
-    const int nc = offer_ids(u, in_train, o, ids);
-    for (int m = 0; m < M; ++m) cand_foot[m] = 0;
-    for (int i = 0; i < nc; ++i) cand_foot[dmachine[ids[i]]]++;
+    const int* oid = ids + (size_t)o * N;
+    const int nc = counts[o];
     bool merged = false;
     for (int e = 0; e < n_items && !merged; ++e) {
       if (fabs(items[e].obj - obj) > 1e-12) continue;
-      bool same = true;
-      for (int m = 0; m < M && same; ++m) same = foot[(size_t)e * M + m] == cand_foot[m];
-      if (!same) continue;
-      const int ne = offer_ids(u, in_train, items[e].src, ids2);
-      if (lex_less(ids, nc, ids2, ne)) {
-        items[e].src = o;
-        items[e].count = nc;
+      if (!warp_equal(foot + (size_t)items[e].src * M, foot + (size_t)o * M, M)) continue;
+      if (warp_lex_less(oid, nc, ids + (size_t)items[e].src * N, items[e].count)) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+          items[e].src = o;
+          items[e].count = nc;
+        }
+        __syncwarp();
       }
       merged = true;
     }
     if (merged) continue;
-    // push_back + std::sort (objective desc, train lexicographic asc) + trim to k
-    items[n_items] = TopItem{obj, nc, o};
-    for (int m = 0; m < M; ++m) foot[(size_t)n_items * M + m] = cand_foot[m];
+    if ((threadIdx.x & 31) == 0) items[n_items] = TopItem{obj, nc, o};
+    __syncwarp();
     ++n_items;
-    for (int i = 1; i < n_items; ++i) {
+    for (int i = 1; i < n_items; ++i) {  // std::sort: (objective desc, train asc) is a strict total order
       int j = i;
       while (j > 0) {
-        const TopItem& x = items[j];
-        const TopItem& y = items[j - 1];
+        const TopItem x = items[j], y = items[j - 1];
         bool before;
-        if (x.obj != y.obj) {
-          before = x.obj > y.obj;
-        } else {
-          const int nx = offer_ids(u, in_train, x.src, ids);
-          const int ny = offer_ids(u, in_train, y.src, ids2);
-          before = lex_less(ids, nx, ids2, ny);
-        }
+        if (x.obj != y.obj) before = x.obj > y.obj;
+        else before = warp_lex_less(ids + (size_t)x.src * N, x.count, ids + (size_t)y.src * N, y.count);
         if (!before) break;
-        const TopItem t = items[j];
-        items[j] = items[j - 1];
-        items[j - 1] = t;
-        for (int m = 0; m < M; ++m) {
-          const int v = foot[(size_t)j * M + m];
-          foot[(size_t)j * M + m] = foot[(size_t)(j - 1) * M + m];
-          foot[(size_t)(j - 1) * M + m] = v;
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+          items[j] = y;
+          items[j - 1] = x;
         }
+        __syncwarp();
         --j;
       }
     }
     if (n_items > k) --n_items;
   }
-  out->n_items = n_items;
-  for (int e = 0; e < n_items; ++e) out->item[e] = items[e];
+  if ((threadIdx.x & 31) == 0) {
+    out->n_items = n_items;
+    for (int e = 0; e < n_items; ++e) out->item[e] = items[e];
+  }
 }
 
 // compute_fraction (src/partition.cpp:360-367) for each result + its train ids
-__global__ void k5_emit(Units u, const unsigned char* __restrict__ in_train, const TopKOut* __restrict__ tk,
-                        const double* __restrict__ dflops, int N, int* __restrict__ ids_out,
+__global__ void k5_emit(const TopKOut* __restrict__ tk, const int* __restrict__ ids, int N,
+                        const double* __restrict__ dflops, int* __restrict__ ids_out,
                         double* __restrict__ frac_out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double total = 0;
   for (int d = 0; d < N; ++d) total += dflops[d];
   int off = 0;
   for (int e = 0; e < tk->n_items; ++e) {
-    const int c = offer_ids(u, in_train, tk->item[e].src, ids_out + off);
+    const int src = tk->item[e].src, c = tk->item[e].count;
     double t = 0;
-    for (int i = 0; i < c; ++i) t += dflops[ids_out[off + i]];
+    for (int i = 0; i < c; ++i) {
+      const int id = ids[(size_t)src * N + i];
+      ids_out[off + i] = id;
+      t += dflops[id];
+    }
     frac_out[e] = t / total;
     off += c;
   }
@@ -736,7 +773,9 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
   add((size_t)std::max(n_offers, 1) * n);
   add(sizeof(double) * std::max(n_offers, 1));
   add(sizeof(int) * std::max(n_offers, 1));
-  add(sizeof(int) * (3 * (size_t)N + (size_t)M * (k + 2)));
+  add(sizeof(int) * (size_t)std::max(n_offers, 1) * N);  // train id lists per offer
+  add(sizeof(int) * (size_t)std::max(n_offers, 1));      // counts
+  add(sizeof(int) * (size_t)std::max(n_offers, 1) * M);  // footprints
   add(sizeof(TopKOut));
   add(sizeof(int) * (size_t)N * k);
   add(sizeof(double) * k);
@@ -748,7 +787,9 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
   unsigned char* d_mask = carve3<unsigned char>(p, (size_t)std::max(n_offers, 1) * n);
   double* d_objs = carve3<double>(p, std::max(n_offers, 1));
   int* d_valid = carve3<int>(p, std::max(n_offers, 1));
-  int* d_work = carve3<int>(p, 3 * (size_t)N + (size_t)M * (k + 2));
+  int* d_lists = carve3<int>(p, (size_t)std::max(n_offers, 1) * N);
+  int* d_counts = carve3<int>(p, (size_t)std::max(n_offers, 1));
+  int* d_foot = carve3<int>(p, (size_t)std::max(n_offers, 1) * M);
   TopKOut* d_tk = carve3<TopKOut>(p, 1);
   int* d_tids = carve3<int>(p, (size_t)N * k);
   double* d_frac = carve3<double>(p, k);
@@ -782,9 +823,11 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
   }
   k5_unpack_offers<<<(n_offers + 255) / 256, 256, 0, ctx->stream>>>(d_offer, d_rout, n_offers, exact, d_objs,
                                                                     d_valid);
-  k5_topk<<<1, 1, 0, ctx->stream>>>(u, d_mask, d_objs, d_valid, n_offers, k, ctx->d_machine, M, d_work, d_tk);
-  k5_emit<<<1, 1, 0, ctx->stream>>>(u, d_mask, d_tk, ctx->d_flops, N, d_tids, d_frac);
-  ctx->launches += 3;
+  k5_offer_lists<<<(n_offers + 7) / 8, 256, 0, ctx->stream>>>(u, d_mask, d_valid, n_offers, ctx->d_machine, M, N,
+                                                              d_lists, d_counts, d_foot);
+  k5_topk<<<1, 32, 0, ctx->stream>>>(d_objs, d_valid, n_offers, k, M, N, d_lists, d_counts, d_foot, d_tk);
+  k5_emit<<<1, 1, 0, ctx->stream>>>(d_tk, d_lists, N, ctx->d_flops, d_tids, d_frac);
+  ctx->launches += 4;
   GP_CUDA(cudaGetLastError());
   TopKOut* htk = reinterpret_cast<TopKOut*>(hp);
   int* hids = reinterpret_cast<int*>(hp + sizeof(TopKOut));
