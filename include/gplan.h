@@ -176,6 +176,12 @@ typedef struct gp_ctx gp_ctx;
  * kernel image exists. */
 int gp_ctx_create(const gp_cluster* cluster, const gp_workload* work, const gp_calib* calib,
                   int device, gp_ctx** out);
+/* Multi-GPU context: the same inputs on every listed CUDA ordinal. Searches whose
+ * layout range is large are split into contiguous rank shards, one per device, run
+ * concurrently and reduced lexicographically inside the call; every other entry point
+ * runs on devices[0]. */
+int gp_ctx_create_multi(const gp_cluster* cluster, const gp_workload* work, const gp_calib* calib,
+                        const int* devices, int n_devices, gp_ctx** out);
 void gp_ctx_destroy(gp_ctx* ctx);
 /* Message of the last failing call on this thread. */
 const char* gp_last_error(void);

@@ -233,6 +233,8 @@ int gp_ctx_create(const gp_cluster* c, const gp_workload* w, const gp_calib* k, 
 
 void gp_ctx_destroy(gp_ctx* ctx) {
   if (!ctx) return;
+  for (gp_ctx* peer : ctx->peers) gp_ctx_destroy(peer);
+  ctx->peers.clear();
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* ptrs[] = {ctx->d_type, ctx->d_machine, ctx->d_flops, ctx->d_hbm_bw, ctx->d_hbm_cap,
@@ -260,19 +262,86 @@ int gp_train_space(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_op
   return train_space(ctx, ids, n, o, layouts);
 }
 
+// In-call multi-GPU fan-out: a multi-device context splits the rank
+// range of one search into contiguous shards, one per device; every device builds its
+// tables and scans its shard on its own stream concurrently; the (cost, rank) winners
+// are reduced lexicographically on the host (first rank among equal costs).
+static int search_fanout(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
+                         const gp_train_opts* o, int64_t lo, int64_t hi, gp_train_result* out,
+                         int32_t* stage_devices) {
+  int64_t total = 0;
+  int rc = train_space(ctx, ids, n, o, &total);
+  if (rc) return rc;
+  if (lo < 0) lo = 0;
+  if (hi < 0 || hi > total) hi = total;
+  if (lo > hi) lo = hi;
+  const int P = 1 + (int)ctx->peers.size();
+  if (ctx->peers.empty() || hi - lo < kFanoutMinLayouts) {
+    cudaSetDevice(ctx->device);
+    return train_search(ctx, ids, n, window, o, lo, hi, out, stage_devices);
+  }
+  std::vector<gp_ctx*> devs{ctx};
+  devs.insert(devs.end(), ctx->peers.begin(), ctx->peers.end());
+  for (int i = 0; i < P; ++i) {  // enqueue everything first: shards run concurrently
+    cudaSetDevice(devs[i]->device);
+    const int64_t a = lo + (hi - lo) * i / P, b = lo + (hi - lo) * (i + 1) / P;
+    rc = train_prepare(devs[i], ids, n, o);
+    if (!rc) rc = train_launch(devs[i], window, a, b);
+    if (rc) return rc;
+  }
+  std::memset(out, 0, sizeof *out);
+  out->layouts = hi - lo;
+  std::vector<int32_t> tmp(n > 0 ? n : 1);
+  for (int i = 0; i < P; ++i) {
+    cudaSetDevice(devs[i]->device);
+    gp_train_result r;
+    rc = train_collect(devs[i], &r, tmp.data());
+    if (rc) return rc;
+    out->feasible += r.feasible;
+    if (r.found && (!out->found || r.cost < out->cost || (r.cost == out->cost && r.rank < out->rank))) {
+      const int64_t layouts = out->layouts, feasible = out->feasible;
+      *out = r;
+      out->layouts = layouts;
+      out->feasible = feasible;
+      if (stage_devices) std::memcpy(stage_devices, tmp.data(), sizeof(int32_t) * n);
+    }
+  }
+  cudaSetDevice(ctx->device);
+  return GP_OK;
+}
+
 int gp_constrained_search(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
                           const gp_train_opts* o, gp_train_result* out, int32_t* stage_devices) {
   if (!ctx) return set_error(GP_INVALID, "null context");
-  cudaSetDevice(ctx->device);
-  return train_search(ctx, ids, n, window, o, 0, -1, out, stage_devices);
+  return search_fanout(ctx, ids, n, window, o, 0, -1, out, stage_devices);
 }
 
 int gp_constrained_search_range(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
                                 const gp_train_opts* o, int64_t lo, int64_t hi,
                                 gp_train_result* out, int32_t* stage_devices) {
   if (!ctx) return set_error(GP_INVALID, "null context");
-  cudaSetDevice(ctx->device);
-  return train_search(ctx, ids, n, window, o, lo, hi, out, stage_devices);
+  return search_fanout(ctx, ids, n, window, o, lo, hi, out, stage_devices);
+}
+
+int gp_ctx_create_multi(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                        const int* devices, int n_devices, gp_ctx** out) {
+  *out = nullptr;
+  if (!devices || n_devices < 1) return set_error(GP_INVALID, "need at least one device");
+  gp_ctx* primary = nullptr;
+  int rc = gp_ctx_create(c, w, k, devices[0], &primary);
+  if (rc) return rc;
+  for (int i = 1; i < n_devices; ++i) {
+    gp_ctx* peer = nullptr;
+    rc = gp_ctx_create(c, w, k, devices[i], &peer);
+    if (rc) {
+      gp_ctx_destroy(primary);
+      return rc;
+    }
+    primary->peers.push_back(peer);
+  }
+  cudaSetDevice(primary->device);
+  *out = primary;
+  return GP_OK;
 }
 
 int gp_train_prepare(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* o) {

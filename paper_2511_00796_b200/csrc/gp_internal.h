@@ -14,6 +14,7 @@ namespace gp {
 constexpr double kInf = 1e30;       // inc/common.hpp:41
 constexpr double kActBytes = 2.0;   // src/cost_model.cpp:10
 constexpr int kMaxPerRun = 4;       // K1 kernel instantiations support <= 4 blocks per type run
+constexpr long long kFanoutMinLayouts = 20000000;  // below this a search stays on one GPU
 
 // Derived workload/calibration scalars, computed on the host exactly as the
 // reference's inline accessors do (inc/workload.hpp:51-58) and passed by value.
@@ -142,6 +143,8 @@ struct gp_ctx {
   void* train_state = nullptr;
   void* milp_cache = nullptr;
   void* part_cache[2] = {nullptr, nullptr};  // partition unit tables per granularity (partition.cu)
+  // peer contexts on other GPUs (gp_ctx_create_multi): constrained_search fans out over them
+  std::vector<gp_ctx*> peers;
   // optional device timing of the train phases (bench.py): events around K2 and K1
   bool timing = false;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};

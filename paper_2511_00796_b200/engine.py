@@ -108,13 +108,22 @@ class TrainSearchResult:
 class Engine:
     """One engine context (cluster + workload + calibration uploaded to one GPU)."""
 
-    def __init__(self, problem: Problem, device: int = 0):
+    def __init__(self, problem: Problem, device: int = 0, devices=None):
+        """devices: list of CUDA ordinals for an in-call multi-GPU context (searches fan out)."""
         self.problem = problem
         self.n_devices = problem.cluster.n
         c, w, k = problem.structs()
         self._structs = (c, w, k)
         h = C.c_void_p()
-        _check(lib().gp_ctx_create(C.byref(c), C.byref(w), C.byref(k), device, C.byref(h)))
+        if devices:
+            arr = (C.c_int * len(devices))(*devices)
+            lib().gp_ctx_create_multi.argtypes = [C.POINTER(abi.gp_cluster), C.POINTER(abi.gp_workload),
+                                                  C.POINTER(abi.gp_calib), C.POINTER(C.c_int), C.c_int,
+                                                  C.POINTER(C.c_void_p)]
+            _check(lib().gp_ctx_create_multi(C.byref(c), C.byref(w), C.byref(k), arr, len(devices),
+                                             C.byref(h)))
+        else:
+            _check(lib().gp_ctx_create(C.byref(c), C.byref(w), C.byref(k), device, C.byref(h)))
         self._h = h
 
     def close(self):

@@ -113,9 +113,21 @@ gp_ctx* make_context(const ClusterGraph& g, const Key& key, const gp_workload& w
                dcap.data(), tfl.data(), tbw.data(), tcap.data(), g.links.data()};
   gp_calib kc{ce.data(), io.data(), p.sync_latency_s, p.stage_latency_penalty, p.max_concurrency,
               p.activation_coeff, p.tp_allreduce_coeff, p.grad_bytes_per_param};
-  const char* dev = std::getenv("GPLAN_DEVICE");
+  // GPLAN_DEVICES=0,1,... : multi-GPU context (searches fan out); else GPLAN_DEVICE or 0
+  std::vector<int> devs;
+  if (const char* list = std::getenv("GPLAN_DEVICES")) {
+    for (const char* q = list; *q;) {
+      devs.push_back(std::atoi(q));
+      while (*q && *q != ',') ++q;
+      if (*q == ',') ++q;
+    }
+  }
+  if (devs.empty()) {
+    const char* dev = std::getenv("GPLAN_DEVICE");
+    devs.push_back(dev ? std::atoi(dev) : 0);
+  }
   gp_ctx* h = nullptr;
-  check(gp_ctx_create(&c, &wl, &kc, dev ? std::atoi(dev) : 0, &h));
+  check(gp_ctx_create_multi(&c, &wl, &kc, devs.data(), (int)devs.size(), &h));
   if (g_ctx.size() >= 8) g_ctx.erase(g_ctx.begin());
   g_ctx.push_back(std::make_unique<Ctx>());
   g_ctx.back()->key = key;

@@ -110,3 +110,20 @@ def test_edge_cases():
     # single device that fits
     got = run("c1_desk_mixed", [3], 2)
     assert got == Oracle(problem("c1_desk_mixed")).constrained_search([3], 2)
+
+
+def test_multi_gpu_context_fanout():
+    """gp_ctx_create_multi: one search split over every visible GPU == the single-GPU result."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    from paper_2511_00796_b200.engine import Engine
+    p = problem("c5_1024gpu")
+    multi = Engine(p, devices=list(range(n)))
+    ids = list(range(p.cluster.n))[:-1]
+    # a 1.8e8-layout sub-range, large enough to fan out
+    lo, hi = 100_000_000, 280_000_000
+    r1, d1 = engine("c5_1024gpu").constrained_search_raw(ids, 3, lo=lo, hi=hi)
+    r2, d2 = multi.constrained_search_raw(ids, 3, lo=lo, hi=hi)
+    assert train_result_dict(r1, d1) == train_result_dict(r2, d2)
