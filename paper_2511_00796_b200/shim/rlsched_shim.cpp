@@ -9,7 +9,9 @@
 // go through the PLT, so the first definition in load order wins. See
 // INTEGRATION.md. Errors come back as gp_status codes and are rethrown as the
 // reference's exception types (inc/common.hpp:11-39).
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -34,6 +36,29 @@ namespace {
 using namespace rlsched;
 
 long long g_calls = 0;
+
+// GPLAN_PROFILE=1: wall time per seam function, printed at exit (stderr)
+struct Prof {
+  double sec[8] = {};
+  long long n[8] = {};
+  ~Prof() {
+    if (!std::getenv("GPLAN_PROFILE")) return;
+    static const char* names[8] = {"constrained_search", "enumerate_configs", "solve_milp", "weight_sync_cost",
+                                   "graph_partition_candidates", "partition_objective", "compute_fraction", "-"};
+    for (int i = 0; i < 7; ++i)
+      if (n[i]) std::fprintf(stderr, "gplan_shim %-28s %8lld calls %10.3f s\n", names[i], n[i], sec[i]);
+  }
+} g_prof;
+
+struct Timer {
+  int id;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit Timer(int i) : id(i) {}
+  ~Timer() {
+    g_prof.sec[id] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    g_prof.n[id]++;
+  }
+};
 
 [[noreturn]] void rethrow(int rc) {
   const std::string msg = gp_last_error();
@@ -196,6 +221,7 @@ std::optional<TrainSearchResult> constrained_search(const std::vector<int>& trai
                                                     const WorkloadSpec& work,
                                                     const Calibration& calib, int window,
                                                     const TrainSearchOptions& options) {
+  Timer _t(0);
   gp_ctx* h = context(cluster, work, calib);
   gp_train_opts o{options.max_stages_per_type, options.device_granularity_limit};
   gp_train_result res;
@@ -222,6 +248,7 @@ std::vector<ReplicaConfig> enumerate_configs(const std::vector<int>& rollout_set
                                              const ClusterGraph& cluster, const WorkloadSpec& work,
                                              const Calibration& calib,
                                              const RolloutSearchOptions& options) {
+  Timer _t(1);
   gp_ctx* h = context(cluster, work, calib);
   gp_rollout_opts o{options.max_stages};
   std::vector<gp_config> buf(70 * cluster.types.size() + 8);
@@ -241,6 +268,7 @@ std::vector<int> rollout_capacities(const std::vector<int>& rollout_set, const C
 
 RolloutPlan solve_milp(const std::vector<ReplicaConfig>& configs, const std::vector<int>& capacities,
                        double total_rollouts, double mean_len) {
+  Timer _t(2);
   // solve_milp carries no cluster: use the most recent engine context (every
   // scheduler call site follows enumerate_configs on the same context).
   gp_ctx* h = nullptr;
@@ -271,6 +299,7 @@ RolloutPlan solve_milp(const std::vector<ReplicaConfig>& configs, const std::vec
 double weight_sync_cost(const TrainPlan& /*train_plan*/, const RolloutPlan& rollout_plan,
                         const DevicePartition& partition, const ClusterGraph& cluster,
                         const WorkloadSpec& work, const Calibration& calib, int window) {
+  Timer _t(3);
   gp_ctx* h = context(cluster, work, calib);
   std::vector<int32_t> et, er;
   for (const auto& e : rollout_plan.entries) {
@@ -287,6 +316,7 @@ double weight_sync_cost(const TrainPlan& /*train_plan*/, const RolloutPlan& roll
 std::vector<PartitionResult> graph_partition_candidates(const ClusterGraph& cluster,
                                                         const GammaState& gamma,
                                                         const PartitionOptions& options, int k) {
+  Timer _t(4);
   if (cluster.size() < 2) throw ValidationError("graph_partition requires at least two devices");
   gp_ctx* h = any_context(cluster);
   gp_gamma g{gamma.q, gamma.r, gamma.gamma_l, gamma.gamma_h};
@@ -313,6 +343,7 @@ std::vector<PartitionResult> graph_partition_candidates(const ClusterGraph& clus
 }
 
 double partition_objective(const ClusterGraph& cluster, const std::vector<int>& train_set) {
+  Timer _t(5);
   gp_ctx* h = any_context(cluster);
   double obj = 0, frac = 0;
   check(gp_partition_objective(h, train_set.data(), (int32_t)train_set.size(), &obj, &frac));
@@ -320,6 +351,7 @@ double partition_objective(const ClusterGraph& cluster, const std::vector<int>& 
 }
 
 double compute_fraction(const ClusterGraph& cluster, const std::vector<int>& train_set) {
+  Timer _t(6);
   gp_ctx* h = any_context(cluster);
   double frac = 0;
   check(gp_compute_fraction(h, train_set.data(), (int32_t)train_set.size(), &frac));
