@@ -255,6 +255,48 @@ int gp_partition_objective(gp_ctx* ctx, const int32_t* train, int32_t n_train, d
 /* compute_fraction (src/partition.cpp:360-367). */
 int gp_compute_fraction(gp_ctx* ctx, const int32_t* train, int32_t n_train, double* fraction);
 
+/* ---- Algorithm-1 driver on the engine: schedule() (src/scheduler.cpp:259-292) ----- */
+
+/* SchedulerOptions (inc/scheduler.hpp:15-34) + the solver options it carries. */
+typedef struct {
+  int32_t eta_override;        /* < 0: the workload's staleness */
+  int32_t stable_iters;        /* 20 */
+  int32_t iteration_cap;       /* 200 */
+  double stability_tol;        /* 0.005 */
+  double balance_tol;          /* 0.02 */
+  double interval_min;         /* 1e-3 */
+  double band_widen_step;      /* 0.05 */
+  int32_t delta_cap;           /* 64 */
+  int32_t expand_window;       /* 1 */
+  int32_t candidate_width;     /* 8 */
+  int32_t grid_probes;         /* 15 */
+  gp_train_opts train;
+  gp_rollout_opts rollout;
+  int32_t exact_threshold;     /* PartitionOptions: 12 */
+  int32_t restarts;            /* 16 */
+  uint64_t seed;               /* 0x5eed (the CLI passes 4276115) */
+  double band_epsilon;         /* 1e-9 */
+  int32_t force_local_search;
+  int32_t machine_granularity;
+} gp_sched_opts;
+
+typedef struct {
+  int32_t window, staleness, iterations_run, converged;
+  int32_t n_trace;             /* IterationTrace rows (gamma_mid, c_train, c_infer, objective) */
+  int32_t n_train, n_rollout;  /* partition sizes (ids in the caller's buffers) */
+  gp_train_result train;       /* stage devices in the caller's stage_devices buffer */
+  gp_rollout_result rollout;   /* entries[i].config indexes entry_configs */
+  double c_train, c_rollout, c_reward, c_update, c_infer_total;
+  int64_t evaluated_partitions, evaluated_layouts;
+} gp_schedule_result;
+
+void gp_default_sched_opts(gp_sched_opts* o);
+/* train_ids, rollout_ids, stage_devices: n_devices ints each; entry_configs/entries:
+ * entry_cap records; trace: 4 * iteration_cap doubles. */
+int gp_schedule(gp_ctx* ctx, const gp_sched_opts* opts, gp_schedule_result* out, int32_t* train_ids,
+                int32_t* rollout_ids, int32_t* stage_devices, gp_config* entry_configs,
+                gp_rollout_entry* entries, int32_t entry_cap, double* trace);
+
 #ifdef __cplusplus
 }
 #endif

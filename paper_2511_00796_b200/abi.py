@@ -164,3 +164,26 @@ def declare(lib: C.CDLL, prefix: str) -> None:
     err = getattr(lib, f"{prefix}_last_error")
     err.restype = C.c_char_p
     err.argtypes = []
+
+
+class gp_sched_opts(C.Structure):
+    _fields_ = [
+        ("eta_override", C.c_int32), ("stable_iters", C.c_int32), ("iteration_cap", C.c_int32),
+        ("stability_tol", C.c_double), ("balance_tol", C.c_double), ("interval_min", C.c_double),
+        ("band_widen_step", C.c_double), ("delta_cap", C.c_int32), ("expand_window", C.c_int32),
+        ("candidate_width", C.c_int32), ("grid_probes", C.c_int32), ("train", gp_train_opts),
+        ("rollout", gp_rollout_opts), ("exact_threshold", C.c_int32), ("restarts", C.c_int32),
+        ("seed", C.c_uint64), ("band_epsilon", C.c_double), ("force_local_search", C.c_int32),
+        ("machine_granularity", C.c_int32),
+    ]
+
+
+class gp_schedule_result(C.Structure):
+    _fields_ = [
+        ("window", C.c_int32), ("staleness", C.c_int32), ("iterations_run", C.c_int32),
+        ("converged", C.c_int32), ("n_trace", C.c_int32), ("n_train", C.c_int32),
+        ("n_rollout", C.c_int32), ("train", gp_train_result), ("rollout", gp_rollout_result),
+        ("c_train", C.c_double), ("c_rollout", C.c_double), ("c_reward", C.c_double),
+        ("c_update", C.c_double), ("c_infer_total", C.c_double),
+        ("evaluated_partitions", C.c_int64), ("evaluated_layouts", C.c_int64),
+    ]

@@ -33,6 +33,9 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
                          int32_t* train_ids, int32_t* n_out);
 int partition_objective(gp_ctx* ctx, const int32_t* train, int nt, double* obj, double* frac);
 int compute_fraction(gp_ctx* ctx, const int32_t* train, int nt, double* frac);
+int schedule(gp_ctx* ctx, const gp_sched_opts* o, gp_schedule_result* res, int32_t* train_ids,
+             int32_t* rollout_ids, int32_t* stage_devices, gp_config* entry_configs, gp_rollout_entry* entries,
+             int32_t entry_cap, double* trace);
 
 static thread_local std::string g_error;
 
@@ -409,6 +412,36 @@ int gp_compute_fraction(gp_ctx* ctx, const int32_t* train, int32_t n_train, doub
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return compute_fraction(ctx, train, n_train, fraction);
+}
+
+void gp_default_sched_opts(gp_sched_opts* o) {
+  std::memset(o, 0, sizeof *o);
+  o->eta_override = -1;
+  o->stable_iters = 20;
+  o->iteration_cap = 200;
+  o->stability_tol = 0.005;
+  o->balance_tol = 0.02;
+  o->interval_min = 1e-3;
+  o->band_widen_step = 0.05;
+  o->delta_cap = 64;
+  o->expand_window = 1;
+  o->candidate_width = 8;
+  o->grid_probes = 15;
+  o->train.max_stages_per_type = 4;
+  o->train.device_granularity_limit = 16;
+  o->rollout.max_stages = 4;
+  o->exact_threshold = 12;
+  o->restarts = 16;
+  o->seed = 0x5eedULL;
+  o->band_epsilon = 1e-9;
+}
+
+int gp_schedule(gp_ctx* ctx, const gp_sched_opts* opts, gp_schedule_result* out, int32_t* train_ids,
+                int32_t* rollout_ids, int32_t* stage_devices, gp_config* entry_configs,
+                gp_rollout_entry* entries, int32_t entry_cap, double* trace) {
+  if (!ctx || !opts) return set_error(GP_INVALID, "null argument");
+  cudaSetDevice(ctx->device);
+  return schedule(ctx, opts, out, train_ids, rollout_ids, stage_devices, entry_configs, entries, entry_cap, trace);
 }
 
 int gp_ctx_set_timing(gp_ctx* ctx, int on) {

@@ -20,6 +20,7 @@
 #include <climits>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <numeric>
 #include <vector>
 
@@ -34,6 +35,7 @@ struct CfgCand {
   int type;
   int stages;
   int tp[4];
+  int set;  // rollout set of this candidate (batched enumeration)
 };
 
 __device__ __forceinline__ int trunc_i32_x86(double x) {
@@ -54,10 +56,12 @@ __global__ void k3_configs(const CfgCand* __restrict__ cands, int n_cands,
   if (i >= n_cands) return;
   const CfgCand c = cands[i];
   const int t = c.type, S = c.stages;
-  int ms = max_stages < n_machines[t] ? max_stages : n_machines[t];
+  const int* nm = n_machines + c.set * T;
+  const int* av = avail + c.set * T * 4;
+  int ms = max_stages < nm[t] ? max_stages : nm[t];
   ms = ms < sc.L ? ms : sc.L;
-  bool ok = n_machines[t] > 0 && S <= ms;
-  for (int s = 0; s < S && ok; ++s) ok = c.tp[s] <= avail[t * 4 + s];  // stage k on k-th largest machine
+  bool ok = nm[t] > 0 && S <= ms;
+  for (int s = 0; s < S && ok; ++s) ok = c.tp[s] <= av[t * 4 + s];  // stage k on k-th largest machine
   int conc = 0;
   if (ok) {
     // replica_concurrency (src/cost_model.cpp:209-229)
@@ -251,12 +255,19 @@ struct MilpOut {
   int pad;
 };
 
-// Backtracking + plan assembly on one thread (src/rollout_milp.cpp:227-253).
-__global__ void k4_backtrack(MilpDims d, long long full, const gp_config* __restrict__ cfg, int n_cfg,
-                             const double* __restrict__ best, const int* __restrict__ choice,
-                             double B, double len, int* __restrict__ counts,
-                             gp_rollout_entry* __restrict__ entries, MilpOut* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Backtracking + plan assembly, one thread per query (src/rollout_milp.cpp:227-253).
+__global__ void k4_backtrack(MilpDims d, int q, const long long* __restrict__ full_idx,
+                             const gp_config* __restrict__ cfg, int n_cfg, const double* __restrict__ best,
+                             const int* __restrict__ choice, const double* __restrict__ Bs, double len,
+                             int* __restrict__ counts_all, gp_rollout_entry* __restrict__ entries_all,
+                             MilpOut* __restrict__ outs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= q) return;
+  const long long full = full_idx[i];
+  const double B = Bs[i];
+  int* counts = counts_all + (size_t)i * n_cfg;
+  gp_rollout_entry* entries = entries_all + (size_t)i * n_cfg;
+  MilpOut* out = outs + i;
   const double agg = best[full];
   out->aggregate = agg;
   out->n_entries = -1;
@@ -323,6 +334,54 @@ __global__ void k6_combine(const double* __restrict__ type_max, const int* __res
   *out = window * transfer + sync_latency;
 }
 
+// Batched weight sync: block (set, type) -> max link train(set) x rollout(set, type);
+// then one thread per set combines its entries (bottleneck, window transfer + latency).
+__global__ void k6_batch_maxlink(const int* __restrict__ ids, const int* __restrict__ t_off,
+                                 const int* __restrict__ r_off, int T, const int* __restrict__ dtype,
+                                 const double* __restrict__ links, int N, double* __restrict__ type_max) {
+  const int set = blockIdx.x / T, t = blockIdx.x % T;
+  const int* train = ids + t_off[set];
+  const int nt = r_off[set] - t_off[set];
+  const int* roll = ids + r_off[set];
+  const int nr = t_off[set + 1] - r_off[set];
+  double m = 0;
+  const long long tot = (long long)nt * nr;
+  for (long long p = threadIdx.x; p < tot; p += blockDim.x) {
+    const int i = (int)(p / nr), j = (int)(p - (long long)i * nr);
+    const int di = roll[j];
+    if (dtype[di] != t) continue;
+    const double l = links[(size_t)train[i] * N + di];
+    m = m < l ? l : m;
+  }
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const double x = __shfl_xor_sync(0xffffffffu, m, o);
+    m = m < x ? x : m;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = m < red[w] ? red[w] : m;
+    type_max[blockIdx.x] = m;
+  }
+}
+
+__global__ void k6_batch_combine(int q, int T, const double* __restrict__ type_max, const int* __restrict__ e_off,
+                                 const int* __restrict__ etype, const int* __restrict__ erep, int window,
+                                 double mbi, double sync_latency, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= q) return;
+  double bottleneck = kInf;
+  for (int e = e_off[i]; e < e_off[i + 1]; ++e) {
+    if (erep[e] < 1) continue;
+    const double best = etype[e] >= 0 ? type_max[(size_t)i * T + etype[e]] : 0.0;
+    if (best > 0) bottleneck = best < bottleneck ? best : bottleneck;
+  }
+  double transfer = 0;
+  if (bottleneck < kInf && mbi > 0) transfer = mbi / bottleneck;
+  out[i] = window * transfer + sync_latency;
+}
+
 // ===================================================================== host
 
 template <typename T>
@@ -342,59 +401,62 @@ int rollout_capacities(gp_ctx* ctx, const int32_t* ids, int n, int32_t* caps) {
   return GP_OK;
 }
 
-// enumerate_configs (src/rollout_milp.cpp:122-172)
-int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opts* o, gp_config* out,
-                    int cap, int* n_out) {
-  *n_out = 0;
-  if (n <= 0) return set_error(GP_INVALID, "enumerate_configs requires a non-empty rollout set");
+// enumerate_configs (src/rollout_milp.cpp:122-172), batched over rollout sets: the
+// host derives each set's per-type machine availability (enumeration metadata), one
+// K3 launch scores every (set, type, TP multiset) candidate, one copy brings them back.
+int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* ns, const gp_rollout_opts* o,
+                  std::vector<std::vector<gp_config>>& out) {
+  out.assign(q, {});
   if (o->max_stages < 0 || o->max_stages > 4)
     return set_error(GP_INVALID, "rollout max_stages must lie in [0, 4] for the sm_100a kernel");
   const int T = ctx->T;
-  // per type: machines with available devices and the 4 largest counts (stage k
-  // is placed on the k-th largest machine) — enumeration metadata only
-  std::vector<int> per_machine(ctx->M, 0), avail(T * 4, 0), nm(T, 0);
-  std::vector<char> seen(ctx->N, 0);
-  for (int i = 0; i < n; ++i) {
-    if (ids[i] < 0 || ids[i] >= ctx->N) return set_error(GP_INVALID, "unknown device id " + std::to_string(ids[i]));
-    if (seen[ids[i]]++) return set_error(GP_INVALID, "duplicate device id " + std::to_string(ids[i]));
-    per_machine[ctx->h_machine[ids[i]]]++;
-  }
-  std::vector<std::vector<int>> by_type(T);
-  for (int m = 0; m < ctx->M; ++m) {
-    if (!per_machine[m]) continue;
-    // machines are type-pure in the reference loader; take the type of any device on it
-    int t = -1;
-    for (int i = 0; i < n && t < 0; ++i)
-      if (ctx->h_machine[ids[i]] == m) t = ctx->h_type[ids[i]];
-    by_type[t].push_back(per_machine[m]);
-  }
-  for (int t = 0; t < T; ++t) {
-    auto& v = by_type[t];
-    std::sort(v.rbegin(), v.rend());
-    nm[t] = (int)v.size();
-    for (int k = 0; k < 4 && k < (int)v.size(); ++k) avail[t * 4 + k] = v[k];
-  }
-  // candidate list in reference order: type, stages, tp_multisets({8,4,2,1})
+  std::vector<int> avail((size_t)q * T * 4, 0), nm((size_t)q * T, 0);
   std::vector<CfgCand> cands;
-  for (int t = 0; t < T; ++t) {
-    if (nm[t] == 0) continue;
-    for (int S = 1; S <= std::min(o->max_stages, 4); ++S) {
-      int tp[4];
-      // non-increasing sequences of length S over {8,4,2,1}
-      std::function<void(int, int)> rec = [&](int d, int mx) {
-        if (d == S) {
-          CfgCand c{t, S, {0, 0, 0, 0}};
-          for (int s = 0; s < S; ++s) c.tp[s] = tp[s];
-          cands.push_back(c);
-          return;
-        }
-        for (int v : {8, 4, 2, 1}) {
-          if (v > mx) continue;
-          tp[d] = v;
-          rec(d + 1, v);
-        }
-      };
-      rec(0, 8);
+  std::vector<int> per_machine(ctx->M, 0), mtype(ctx->M, -1);
+  std::vector<char> seen(ctx->N, 0);
+  for (int si = 0; si < q; ++si) {
+    const int32_t* id = ids[si];
+    const int n = ns[si];
+    if (n <= 0) return set_error(GP_INVALID, "enumerate_configs requires a non-empty rollout set");
+    std::fill(per_machine.begin(), per_machine.end(), 0);
+    for (int i = 0; i < n; ++i) {
+      if (id[i] < 0 || id[i] >= ctx->N) return set_error(GP_INVALID, "unknown device id " + std::to_string(id[i]));
+      if (seen[id[i]]) {
+        for (int j = 0; j < i; ++j) seen[id[j]] = 0;
+        return set_error(GP_INVALID, "duplicate device id " + std::to_string(id[i]));
+      }
+      seen[id[i]] = 1;
+      per_machine[ctx->h_machine[id[i]]]++;
+      mtype[ctx->h_machine[id[i]]] = ctx->h_type[id[i]];  // machines are type-pure (loader)
+    }
+    for (int i = 0; i < n; ++i) seen[id[i]] = 0;
+    std::vector<std::vector<int>> by_type(T);
+    for (int m = 0; m < ctx->M; ++m)
+      if (per_machine[m]) by_type[mtype[m]].push_back(per_machine[m]);
+    for (int t = 0; t < T; ++t) {
+      auto& v = by_type[t];
+      std::sort(v.rbegin(), v.rend());
+      nm[(size_t)si * T + t] = (int)v.size();
+      for (int k = 0; k < 4 && k < (int)v.size(); ++k) avail[((size_t)si * T + t) * 4 + k] = v[k];
+      if (v.empty()) continue;
+      // candidates in reference order: stages, then tp_multisets over {8,4,2,1}
+      for (int S = 1; S <= std::min(o->max_stages, 4); ++S) {
+        int tp[4];
+        std::function<void(int, int)> rec = [&](int d, int mx) {
+          if (d == S) {
+            CfgCand c{t, S, {0, 0, 0, 0}, si};
+            for (int u = 0; u < S; ++u) c.tp[u] = tp[u];
+            cands.push_back(c);
+            return;
+          }
+          for (int v2 : {8, 4, 2, 1}) {
+            if (v2 > mx) continue;
+            tp[d] = v2;
+            rec(d + 1, v2);
+          }
+        };
+        rec(0, 8);
+      }
     }
   }
   const int nc = (int)cands.size();
@@ -402,43 +464,52 @@ int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opt
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
   add(sizeof(CfgCand) * nc);
-  add(sizeof(int) * T * 4);
-  add(sizeof(int) * T);
+  add(sizeof(int) * avail.size());
+  add(sizeof(int) * nm.size());
   add(sizeof(gp_config) * nc);
   add(sizeof(int) * nc);
   char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaRollout));
   if (!base) return GP_CUDA_ERROR;
   char* p = base;
   CfgCand* d_c = carve2<CfgCand>(p, nc);
-  int* d_av = carve2<int>(p, T * 4);
-  int* d_nm = carve2<int>(p, T);
+  int* d_av = carve2<int>(p, avail.size());
+  int* d_nm = carve2<int>(p, nm.size());
   gp_config* d_out = carve2<gp_config>(p, nc);
   int* d_keep = carve2<int>(p, nc);
-  const size_t in_bytes = (size_t)((char*)(d_nm + T) - (char*)d_c);
-  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(gp_config) * nc + sizeof(int) * nc + 512)));
+  const size_t in_bytes = (size_t)((char*)(d_nm + nm.size()) - (char*)d_c);
+  const size_t out_bytes = (size_t)((char*)(d_keep + nc) - (char*)d_out);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, out_bytes) + 512));
   if (!hp) return GP_CUDA_ERROR;
   std::memcpy(hp, cands.data(), sizeof(CfgCand) * nc);
-  std::memcpy(hp + ((char*)d_av - (char*)d_c), avail.data(), sizeof(int) * T * 4);
-  std::memcpy(hp + ((char*)d_nm - (char*)d_c), nm.data(), sizeof(int) * T);
+  std::memcpy(hp + ((char*)d_av - (char*)d_c), avail.data(), sizeof(int) * avail.size());
+  std::memcpy(hp + ((char*)d_nm - (char*)d_c), nm.data(), sizeof(int) * nm.size());
   GP_CUDA(cudaMemcpyAsync(d_c, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h2d_bytes += (long long)in_bytes;
-  k3_configs<<<(nc + 127) / 128, 128, 0, ctx->stream>>>(d_c, nc, d_av, d_nm, o->max_stages, ctx->sc,
-                                                      ctx->d_tcap, ctx->d_thbm, ctx->d_tflops,
-                                                      ctx->d_ceff, ctx->d_ioeff, T, d_out, d_keep);
+  k3_configs<<<(nc + 127) / 128, 128, 0, ctx->stream>>>(d_c, nc, d_av, d_nm, o->max_stages, ctx->sc, ctx->d_tcap,
+                                                      ctx->d_thbm, ctx->d_tflops, ctx->d_ceff, ctx->d_ioeff, T,
+                                                      d_out, d_keep);
   ctx->launches++;
   GP_CUDA(cudaGetLastError());
-  gp_config* h_cfg = reinterpret_cast<gp_config*>(hp);
-  int* h_keep = reinterpret_cast<int*>(hp + sizeof(gp_config) * nc);
-  GP_CUDA(cudaMemcpyAsync(h_cfg, d_out, sizeof(gp_config) * nc, cudaMemcpyDeviceToHost, ctx->stream));
-  GP_CUDA(cudaMemcpyAsync(h_keep, d_keep, sizeof(int) * nc, cudaMemcpyDeviceToHost, ctx->stream));
-  ctx->d2h_bytes += (long long)(sizeof(gp_config) + sizeof(int)) * nc;
+  GP_CUDA(cudaMemcpyAsync(hp, d_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += (long long)out_bytes;
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
-  int k = 0;
-  for (int i = 0; i < nc; ++i) {
-    if (!h_keep[i]) continue;
-    if (k < cap) out[k] = h_cfg[i];
-    ++k;
-  }
+  const gp_config* h_cfg = reinterpret_cast<const gp_config*>(hp);
+  const int* h_keep = reinterpret_cast<const int*>(hp + ((char*)d_keep - (char*)d_out));
+  for (int i = 0; i < nc; ++i)
+    if (h_keep[i]) out[cands[i].set].push_back(h_cfg[i]);
+  return GP_OK;
+}
+
+int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opts* o, gp_config* out,
+                    int cap, int* n_out) {
+  *n_out = 0;
+  if (n <= 0) return set_error(GP_INVALID, "enumerate_configs requires a non-empty rollout set");
+  std::vector<std::vector<gp_config>> res;
+  int rc = configs_batch(ctx, 1, &ids, &n, o, res);
+  if (rc) return rc;
+  const int k = (int)res[0].size();
+  for (int i = 0; i < k && i < cap; ++i) out[i] = res[0][i];
   *n_out = k;
   if (k > cap) return set_error(GP_CAPACITY, "config buffer too small (" + std::to_string(k) + " needed)");
   return GP_OK;
@@ -452,18 +523,22 @@ int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opt
 // contains the requested one answers it bit-identically. The scheduler solves many
 // MILPs with the same configs (rollout sets whose per-type machine availability
 // agrees); each is then a backtrack from its own full state.
-struct MilpCache {
+struct MilpTable {
   std::vector<unsigned char> sig;  // configs + dims
   MilpDims d{};
-  int nc = 0;
-  void* buf = nullptr;  // best | choice
+  void* buf = nullptr;             // best | choice
   size_t bytes = 0;
   double* best = nullptr;
   int* choice = nullptr;
-  bool valid = false;
-  ~MilpCache() {
+  long long last_use = 0;
+  ~MilpTable() {
     if (buf) cudaFree(buf);
   }
+};
+
+struct MilpCache {
+  std::vector<std::unique_ptr<MilpTable>> tables;  // small LRU
+  long long clock = 0;
 };
 
 void milp_cache_free(gp_ctx* ctx) {
@@ -490,23 +565,16 @@ static void set_dims(MilpDims& d, int dims, const int* caps) {
   d.levels = levels;
 }
 
-int solve_milp(gp_ctx* ctx, const gp_config* cfg, int nc, const int32_t* caps, int dims, double B,
-               double len, gp_rollout_result* out, gp_rollout_entry* entries) {
-  std::memset(out, 0, sizeof *out);
-  out->total_rollouts = B;
-  if (B <= 0) return GP_OK;
-  if (nc == 0) return set_error(GP_INFEASIBLE, "no replica configuration available");
-  if (dims < 1 || dims > GP_MAX_TYPES) return set_error(GP_INVALID, "dims must lie in [1, GP_MAX_TYPES]");
-  if (nc > kMaxCfg) return set_error(GP_INVALID, "too many replica configurations for the sm_100a kernel");
-  long long states = 1;
-  for (int t = 0; t < dims; ++t) {
-    if (caps[t] < 0) return set_error(GP_INVALID, "negative capacity");
-    states *= caps[t] + 1;
-    if (states > 50000000) return set_error(GP_INVALID, "capacity lattice too large for the exact solver");
-  }
-  out->states = states;
-  // groups of configs with the same (type, device count): one predecessor each
-  std::vector<std::pair<long long, int>> key;
+static std::vector<unsigned char> milp_sig(const gp_config* cfg, int nc, int dims) {
+  std::vector<unsigned char> sig(sizeof(gp_config) * nc + sizeof(int));
+  std::memcpy(sig.data(), cfg, sizeof(gp_config) * nc);
+  std::memcpy(sig.data() + sizeof(gp_config) * nc, &dims, sizeof(int));
+  return sig;
+}
+
+// Validates configs (type-pure, >= 1 device) and returns the (type, devices) grouping key.
+static int milp_groups(const gp_config* cfg, int nc, int dims, std::vector<std::pair<long long, int>>& key) {
+  key.clear();
   for (int c = 0; c < nc; ++c) {
     int t = -1, n = 0, used = 0;
     for (int u = 0; u < dims; ++u)
@@ -520,157 +588,377 @@ int solve_milp(gp_ctx* ctx, const gp_config* cfg, int nc, const int32_t* caps, i
     key.push_back({(long long)t * 1000000 + n, c});
   }
   std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-  // cache lookup: same configs and dims, lattice covering caps
+  return GP_OK;
+}
+
+// A table for `cfg` covering `caps` (computes the lattice DP when no cached table does).
+static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, const int* caps, MilpTable** out) {
   if (!ctx->milp_cache) ctx->milp_cache = new MilpCache();
   MilpCache& mc = *static_cast<MilpCache*>(ctx->milp_cache);
-  std::vector<unsigned char> sig(sizeof(gp_config) * nc + sizeof(int));
-  std::memcpy(sig.data(), cfg, sizeof(gp_config) * nc);
-  std::memcpy(sig.data() + sizeof(gp_config) * nc, &dims, sizeof(int));
-  bool hit = mc.valid && mc.sig == sig;
-  for (int t = 0; t < dims && hit; ++t) hit = caps[t] <= mc.d.cap[t];
-  if (!hit) {
-    // lattice to tabulate: the union with the cached one when the configs agree and it fits
-    std::vector<int> lat(caps, caps + dims);
-    if (mc.valid && mc.sig == sig) {
-      long long u = 1;
-      std::vector<int> un(dims);
-      for (int t = 0; t < dims; ++t) {
-        un[t] = std::max(caps[t], mc.d.cap[t]);
-        u *= un[t] + 1;
-      }
-      if (u <= 50000000) lat = un;
+  const std::vector<unsigned char> sig = milp_sig(cfg, nc, dims);
+  MilpTable* same = nullptr;
+  for (auto& t : mc.tables) {
+    if (t->sig != sig) continue;
+    same = t.get();
+    bool covers = true;
+    for (int u = 0; u < dims && covers; ++u) covers = caps[u] <= t->d.cap[u];
+    if (covers) {
+      t->last_use = ++mc.clock;
+      *out = t.get();
+      return GP_OK;
     }
-    MilpDims d{};
-    set_dims(d, dims, lat.data());
-    std::vector<Group> groups;
-    std::vector<int> members;
-    for (size_t i = 0; i < key.size();) {
-      size_t j = i;
-      const int t = (int)(key[i].first / 1000000), n = (int)(key[i].first % 1000000);
-      Group G{t, n, (long long)n * d.stride[t], cfg[key[i].second].throughput, (int)members.size(), 0};
-      while (j < key.size() && key[j].first == key[i].first) {
-        members.push_back(key[j].second);
-        const double hh = cfg[key[j].second].throughput;
-        G.hmax = G.hmax < hh ? hh : G.hmax;
-        ++j;
-      }
-      G.count = (int)(j - i);
-      groups.push_back(G);
-      i = j;
-    }
-    const int ng = (int)groups.size();
-    if (ng > kMaxGroups) return set_error(GP_INVALID, "too many config groups for the sm_100a kernel");
-    std::vector<double> hs(nc);
-    for (int c = 0; c < nc; ++c) hs[c] = cfg[c].throughput;
-    // table buffers (persistent)
-    const size_t tbytes = (((size_t)d.states * sizeof(double) + 255) & ~size_t(255)) + (size_t)d.states * sizeof(int) + 256;
-    if (tbytes > mc.bytes) {
-      if (mc.buf) cudaFree(mc.buf);
-      mc.buf = nullptr;
-      mc.bytes = 0;
-      mc.valid = false;
-      GP_CUDA(cudaMalloc(&mc.buf, tbytes));
-      mc.bytes = tbytes;
-    }
-    mc.best = static_cast<double*>(mc.buf);
-    mc.choice = reinterpret_cast<int*>(static_cast<char*>(mc.buf) +
-                                       (((size_t)d.states * sizeof(double) + 255) & ~size_t(255)));
-    // scratch: groups, members, h, level tables, packed order
-    size_t bytes = 0;
-    auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
-    add(sizeof(Group) * ng);
-    add(sizeof(int) * nc);
-    add(sizeof(double) * nc);
-    add(sizeof(int) * d.levels);
-    add(sizeof(long long) * (d.levels + 1));
-    add(sizeof(int) * d.levels);
-    add(sizeof(int));
-    add(sizeof(unsigned long long) * d.states);
-    char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaRollout));
-    if (!base) return GP_CUDA_ERROR;
-    char* p = base;
-    Group* d_groups = carve2<Group>(p, ng);
-    int* d_members = carve2<int>(p, nc);
-    double* d_h = carve2<double>(p, nc);
-    int* d_hist = carve2<int>(p, d.levels);
-    long long* d_off = carve2<long long>(p, d.levels + 1);
-    int* d_cursor = carve2<int>(p, d.levels);
-    int* d_maxw = carve2<int>(p, 1);
-    unsigned long long* d_order = carve2<unsigned long long>(p, d.states);
-    const size_t in_bytes = (size_t)((char*)(d_h + nc) - (char*)d_groups);
-    char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, (size_t)4096)));
-    if (!hp) return GP_CUDA_ERROR;
-    GP_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::memcpy(hp, groups.data(), sizeof(Group) * ng);
-    std::memcpy(hp + ((char*)d_members - (char*)d_groups), members.data(), sizeof(int) * nc);
-    std::memcpy(hp + ((char*)d_h - (char*)d_groups), hs.data(), sizeof(double) * nc);
-    GP_CUDA(cudaMemcpyAsync(d_groups, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
-    ctx->h2d_bytes += (long long)in_bytes;
-    GP_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int) * d.levels, ctx->stream));
-    const int sweep_blocks = (int)std::min<long long>((d.states + 255) / 256, (long long)ctx->num_sms * 16);
-    k4_level_hist<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_hist);
-    k4_level_scan<<<1, 32, 0, ctx->stream>>>(d_hist, d.levels, d_off, d_cursor, d_maxw);
-    k4_level_scatter<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_off, d_cursor, d_order);
-    ctx->launches += 3;
-    int* h_maxw = reinterpret_cast<int*>(hp);
-    GP_CUDA(cudaMemcpyAsync(h_maxw, d_maxw, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    GP_CUDA(cudaStreamSynchronize(ctx->stream));
-    static int occ = 0;
-    if (!occ) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_dp_levels, 256, 0);
-      occ = std::max(1, occ);
-    }
-    // grid: enough blocks for the widest level, at most what is co-resident
-    int dp_blocks = (int)std::min<long long>((long long)ctx->num_sms * occ, ((long long)*h_maxw + 255) / 256);
-    dp_blocks = std::max(1, dp_blocks);
-    int ng_arg = ng, nc_arg = nc;
-    double* best = mc.best;
-    int* choice = mc.choice;
-    void* args[] = {&d, &d_groups, &ng_arg, &d_members, &d_h, &nc_arg, &d_off, &d_order, &best, &choice};
-    GP_CUDA(cudaLaunchCooperativeKernel((void*)k4_dp_levels, dp_blocks, 256, args, 0, ctx->stream));
-    ctx->launches++;
-    mc.d = d;
-    mc.nc = nc;
-    mc.sig = sig;
-    mc.valid = true;
   }
-  // backtrack from this lattice's full state inside the cached table
-  long long full = 0;
-  for (int t = 0; t < dims; ++t) full += (long long)caps[t] * mc.d.stride[t];
+  std::vector<std::pair<long long, int>> key;
+  int rc = milp_groups(cfg, nc, dims, key);
+  if (rc) return rc;
+  // lattice to tabulate: the union with a cached table of the same configs when it fits
+  std::vector<int> lat(caps, caps + dims);
+  if (same) {
+    long long u = 1;
+    std::vector<int> un(dims);
+    for (int t = 0; t < dims; ++t) {
+      un[t] = std::max(caps[t], same->d.cap[t]);
+      u *= un[t] + 1;
+    }
+    if (u <= 50000000) lat = un;
+  }
+  MilpTable* tab = same;
+  if (!tab) {
+    if (mc.tables.size() >= 4) {  // evict the least recently used
+      auto lru = std::min_element(mc.tables.begin(), mc.tables.end(),
+                                  [](const auto& a, const auto& b) { return a->last_use < b->last_use; });
+      mc.tables.erase(lru);
+    }
+    mc.tables.push_back(std::make_unique<MilpTable>());
+    tab = mc.tables.back().get();
+    tab->sig = sig;
+  }
+  MilpDims d{};
+  set_dims(d, dims, lat.data());
+  std::vector<Group> groups;
+  std::vector<int> members;
+  for (size_t i = 0; i < key.size();) {
+    size_t j = i;
+    const int t = (int)(key[i].first / 1000000), n = (int)(key[i].first % 1000000);
+    Group G{t, n, (long long)n * d.stride[t], cfg[key[i].second].throughput, (int)members.size(), 0};
+    while (j < key.size() && key[j].first == key[i].first) {
+      members.push_back(key[j].second);
+      const double hh = cfg[key[j].second].throughput;
+      G.hmax = G.hmax < hh ? hh : G.hmax;
+      ++j;
+    }
+    G.count = (int)(j - i);
+    groups.push_back(G);
+    i = j;
+  }
+  const int ng = (int)groups.size();
+  if (ng > kMaxGroups) return set_error(GP_INVALID, "too many config groups for the sm_100a kernel");
+  std::vector<double> hs(nc);
+  for (int c = 0; c < nc; ++c) hs[c] = cfg[c].throughput;
+  const size_t best_bytes = ((size_t)d.states * sizeof(double) + 255) & ~size_t(255);
+  const size_t tbytes = best_bytes + (size_t)d.states * sizeof(int) + 256;
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (tbytes > tab->bytes) {
+    if (tab->buf) cudaFree(tab->buf);
+    tab->buf = nullptr;
+    tab->bytes = 0;
+    GP_CUDA(cudaMalloc(&tab->buf, tbytes));
+    tab->bytes = tbytes;
+  }
+  tab->best = static_cast<double*>(tab->buf);
+  tab->choice = reinterpret_cast<int*>(static_cast<char*>(tab->buf) + best_bytes);
+  // scratch: groups, members, h, level tables, packed order
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+  add(sizeof(Group) * ng);
+  add(sizeof(int) * nc);
+  add(sizeof(double) * nc);
+  add(sizeof(int) * d.levels);
+  add(sizeof(long long) * (d.levels + 1));
+  add(sizeof(int) * d.levels);
+  add(sizeof(int));
+  add(sizeof(unsigned long long) * d.states);
+  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaRollout));
+  if (!base) return GP_CUDA_ERROR;
+  char* p = base;
+  Group* d_groups = carve2<Group>(p, ng);
+  int* d_members = carve2<int>(p, nc);
+  double* d_h = carve2<double>(p, nc);
+  int* d_hist = carve2<int>(p, d.levels);
+  long long* d_off = carve2<long long>(p, d.levels + 1);
+  int* d_cursor = carve2<int>(p, d.levels);
+  int* d_maxw = carve2<int>(p, 1);
+  unsigned long long* d_order = carve2<unsigned long long>(p, d.states);
+  const size_t in_bytes = (size_t)((char*)(d_h + nc) - (char*)d_groups);
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, (size_t)4096)));
+  if (!hp) return GP_CUDA_ERROR;
+  std::memcpy(hp, groups.data(), sizeof(Group) * ng);
+  std::memcpy(hp + ((char*)d_members - (char*)d_groups), members.data(), sizeof(int) * nc);
+  std::memcpy(hp + ((char*)d_h - (char*)d_groups), hs.data(), sizeof(double) * nc);
+  GP_CUDA(cudaMemcpyAsync(d_groups, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)in_bytes;
+  GP_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int) * d.levels, ctx->stream));
+  const int sweep_blocks = (int)std::min<long long>((d.states + 255) / 256, (long long)ctx->num_sms * 16);
+  k4_level_hist<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_hist);
+  k4_level_scan<<<1, 32, 0, ctx->stream>>>(d_hist, d.levels, d_off, d_cursor, d_maxw);
+  k4_level_scatter<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_off, d_cursor, d_order);
+  ctx->launches += 3;
+  int* h_maxw = reinterpret_cast<int*>(hp);
+  GP_CUDA(cudaMemcpyAsync(h_maxw, d_maxw, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_dp_levels, 256, 0);
+    occ = std::max(1, occ);
+  }
+  // grid: enough blocks for the widest level, at most what is co-resident
+  int dp_blocks = (int)std::min<long long>((long long)ctx->num_sms * occ, ((long long)*h_maxw + 255) / 256);
+  dp_blocks = std::max(1, dp_blocks);
+  int ng_arg = ng, nc_arg = nc;
+  double* best = tab->best;
+  int* choice = tab->choice;
+  void* args[] = {&d, &d_groups, &ng_arg, &d_members, &d_h, &nc_arg, &d_off, &d_order, &best, &choice};
+  GP_CUDA(cudaLaunchCooperativeKernel((void*)k4_dp_levels, dp_blocks, 256, args, 0, ctx->stream));
+  ctx->launches++;
+  tab->d = d;
+  tab->last_use = ++mc.clock;
+  *out = tab;
+  return GP_OK;
+}
+
+// Backtracks q queries (caps, B, len) of the same configs from `tab` in one launch.
+static int backtrack_many(gp_ctx* ctx, MilpTable* tab, const gp_config* cfg, int nc, int q,
+                          const int* const* caps, const double* Bs, double len, gp_rollout_result* outs,
+                          gp_rollout_entry* const* entries) {
+  std::vector<long long> full(q);
+  std::vector<double> Bv(Bs, Bs + q);
+  for (int i = 0; i < q; ++i) {
+    full[i] = 0;
+    for (int t = 0; t < tab->d.T; ++t) full[i] += (long long)caps[i][t] * tab->d.stride[t];
+  }
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
   add(sizeof(gp_config) * nc);
-  add(sizeof(int) * nc);
-  add(sizeof(gp_rollout_entry) * nc);
-  add(sizeof(MilpOut));
+  add(sizeof(long long) * q);
+  add(sizeof(double) * q);
+  add(sizeof(int) * (size_t)nc * q);
+  add(sizeof(gp_rollout_entry) * (size_t)nc * q);
+  add(sizeof(MilpOut) * q);
   char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaMisc));
   if (!base) return GP_CUDA_ERROR;
   char* p = base;
   gp_config* d_cfg = carve2<gp_config>(p, nc);
-  int* d_counts = carve2<int>(p, nc);
-  gp_rollout_entry* d_entries = carve2<gp_rollout_entry>(p, nc);
-  MilpOut* d_mo = carve2<MilpOut>(p, 1);
-  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(sizeof(gp_config) * nc, sizeof(MilpOut) + sizeof(gp_rollout_entry) * nc + 256)));
+  long long* d_full = carve2<long long>(p, q);
+  double* d_B = carve2<double>(p, q);
+  int* d_counts = carve2<int>(p, (size_t)nc * q);
+  gp_rollout_entry* d_entries = carve2<gp_rollout_entry>(p, (size_t)nc * q);
+  MilpOut* d_mo = carve2<MilpOut>(p, q);
+  const size_t in_bytes = (size_t)((char*)(d_B + q) - (char*)d_cfg);
+  const size_t out_bytes = (size_t)((char*)(d_mo + q) - (char*)d_entries);
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, out_bytes) + 512));
   if (!hp) return GP_CUDA_ERROR;
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
   std::memcpy(hp, cfg, sizeof(gp_config) * nc);
-  GP_CUDA(cudaMemcpyAsync(d_cfg, hp, sizeof(gp_config) * nc, cudaMemcpyHostToDevice, ctx->stream));
-  ctx->h2d_bytes += (long long)(sizeof(gp_config) * nc);
-  k4_backtrack<<<1, 32, 0, ctx->stream>>>(mc.d, full, d_cfg, nc, mc.best, mc.choice, B, len, d_counts,
-                                          d_entries, d_mo);
+  std::memcpy(hp + ((char*)d_full - (char*)d_cfg), full.data(), sizeof(long long) * q);
+  std::memcpy(hp + ((char*)d_B - (char*)d_cfg), Bv.data(), sizeof(double) * q);
+  GP_CUDA(cudaMemcpyAsync(d_cfg, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)in_bytes;
+  k4_backtrack<<<(q + 31) / 32, 32, 0, ctx->stream>>>(tab->d, q, d_full, d_cfg, nc, tab->best, tab->choice, d_B,
+                                                     len, d_counts, d_entries, d_mo);
   ctx->launches++;
   GP_CUDA(cudaGetLastError());
-  MilpOut* ho = reinterpret_cast<MilpOut*>(hp);
-  gp_rollout_entry* he = reinterpret_cast<gp_rollout_entry*>(hp + 256);
-  GP_CUDA(cudaMemcpyAsync(ho, d_mo, sizeof(MilpOut), cudaMemcpyDeviceToHost, ctx->stream));
-  GP_CUDA(cudaMemcpyAsync(he, d_entries, sizeof(gp_rollout_entry) * nc, cudaMemcpyDeviceToHost, ctx->stream));
-  ctx->d2h_bytes += (long long)(sizeof(MilpOut) + sizeof(gp_rollout_entry) * nc);
+  GP_CUDA(cudaMemcpyAsync(hp, d_entries, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += (long long)out_bytes;
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
-  out->aggregate = ho->aggregate;
-  if (ho->n_entries < 0) return set_error(GP_INFEASIBLE, "rollout capacity cannot host any replica");
-  out->makespan = ho->makespan;
-  out->n_entries = ho->n_entries;
-  std::memcpy(entries, he, sizeof(gp_rollout_entry) * ho->n_entries);
+  const gp_rollout_entry* he = reinterpret_cast<const gp_rollout_entry*>(hp);
+  const MilpOut* ho = reinterpret_cast<const MilpOut*>(hp + ((char*)d_mo - (char*)d_entries));
+  for (int i = 0; i < q; ++i) {
+    gp_rollout_result& o = outs[i];
+    std::memset(&o, 0, sizeof o);
+    o.total_rollouts = Bs[i];
+    o.aggregate = ho[i].aggregate;
+    long long states = 1;
+    for (int t = 0; t < tab->d.T; ++t) states *= caps[i][t] + 1;
+    o.states = states;
+    o.n_entries = ho[i].n_entries;  // -1: infeasible (aggregate <= 0)
+    if (ho[i].n_entries >= 0) {
+      o.makespan = ho[i].makespan;
+      std::memcpy(entries[i], he + (size_t)nc * i, sizeof(gp_rollout_entry) * ho[i].n_entries);
+    }
+  }
+  return GP_OK;
+}
+
+static int milp_check(int nc, const int32_t* caps, int dims) {
+  if (dims < 1 || dims > GP_MAX_TYPES) return set_error(GP_INVALID, "dims must lie in [1, GP_MAX_TYPES]");
+  if (nc > kMaxCfg) return set_error(GP_INVALID, "too many replica configurations for the sm_100a kernel");
+  long long states = 1;
+  for (int t = 0; t < dims; ++t) {
+    if (caps[t] < 0) return set_error(GP_INVALID, "negative capacity");
+    states *= caps[t] + 1;
+    if (states > 50000000) return set_error(GP_INVALID, "capacity lattice too large for the exact solver");
+  }
+  return GP_OK;
+}
+
+int solve_milp(gp_ctx* ctx, const gp_config* cfg, int nc, const int32_t* caps, int dims, double B,
+               double len, gp_rollout_result* out, gp_rollout_entry* entries) {
+  std::memset(out, 0, sizeof *out);
+  out->total_rollouts = B;
+  if (B <= 0) return GP_OK;
+  if (nc == 0) return set_error(GP_INFEASIBLE, "no replica configuration available");
+  int rc = milp_check(nc, caps, dims);
+  if (rc) return rc;
+  MilpTable* tab = nullptr;
+  rc = ensure_table(ctx, cfg, nc, dims, caps, &tab);
+  if (rc) return rc;
+  const int* cp = caps;
+  rc = backtrack_many(ctx, tab, cfg, nc, 1, &cp, &B, len, out, &entries);
+  if (rc) return rc;
+  if (out->n_entries < 0) {
+    out->n_entries = 0;
+    return set_error(GP_INFEASIBLE, "rollout capacity cannot host any replica");
+  }
+  return GP_OK;
+}
+
+// Many MILPs (one scheduler evaluation batch). Results per query: GP_OK with a plan,
+// GP_INFEASIBLE (no configs / aggregate <= 0), or GP_INVALID (lattice > 5e7) in rcs[i].
+int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs, const int32_t* const* caps,
+               int dims, const double* Bs, double len, gp_rollout_result* outs, gp_rollout_entry* const* entries,
+               int* rcs) {
+  // group queries with identical config lists
+  std::vector<int> order(q);
+  std::vector<std::vector<unsigned char>> sigs(q);
+  for (int i = 0; i < q; ++i) {
+    order[i] = i;
+    sigs[i] = milp_sig(cfgs[i], ncs[i], dims);
+    std::memset(&outs[i], 0, sizeof outs[i]);
+    outs[i].total_rollouts = Bs[i];
+    rcs[i] = GP_OK;
+    if (Bs[i] <= 0) { rcs[i] = -1; continue; }  // empty plan
+    if (ncs[i] == 0) { rcs[i] = GP_INFEASIBLE; continue; }
+    if (milp_check(ncs[i], caps[i], dims)) rcs[i] = GP_INVALID;
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sigs[a] < sigs[b]; });
+  for (size_t g0 = 0; g0 < order.size();) {
+    size_t g1 = g0;
+    while (g1 < order.size() && sigs[order[g1]] == sigs[order[g0]]) ++g1;
+    std::vector<int> live;
+    for (size_t j = g0; j < g1; ++j)
+      if (rcs[order[j]] == GP_OK) live.push_back(order[j]);
+    if (!live.empty()) {
+      // union lattice of the group (split into single queries if it would exceed 5e7)
+      std::vector<int> un(dims, 0);
+      long long u = 1;
+      for (int t = 0; t < dims; ++t) {
+        for (int i : live) un[t] = std::max(un[t], (int)caps[i][t]);
+        u *= un[t] + 1;
+      }
+      std::vector<std::vector<int>> parts;
+      if (u <= 50000000) parts.push_back(live);
+      else for (int i : live) parts.push_back({i});
+      for (auto& part : parts) {
+        std::vector<int> pc(dims, 0);
+        for (int t = 0; t < dims; ++t)
+          for (int i : part) pc[t] = std::max(pc[t], (int)caps[i][t]);
+        const int i0 = part[0];
+        MilpTable* tab = nullptr;
+        int rc = ensure_table(ctx, cfgs[i0], ncs[i0], dims, pc.data(), &tab);
+        if (rc) return rc;
+        std::vector<const int*> cp;
+        std::vector<double> bb;
+        std::vector<gp_rollout_result> ro(part.size());
+        std::vector<gp_rollout_entry*> ep;
+        for (int i : part) {
+          cp.push_back(caps[i]);
+          bb.push_back(Bs[i]);
+          ep.push_back(entries[i]);
+        }
+        rc = backtrack_many(ctx, tab, cfgs[i0], ncs[i0], (int)part.size(), cp.data(), bb.data(), len, ro.data(),
+                            ep.data());
+        if (rc) return rc;
+        for (size_t j = 0; j < part.size(); ++j) {
+          outs[part[j]] = ro[j];
+          if (ro[j].n_entries < 0) {
+            outs[part[j]].n_entries = 0;
+            rcs[part[j]] = GP_INFEASIBLE;
+          }
+        }
+      }
+    }
+    g0 = g1;
+  }
+  for (int i = 0; i < q; ++i)
+    if (rcs[i] == -1) rcs[i] = GP_OK;
+  return GP_OK;
+}
+
+int weight_sync_batch(gp_ctx* ctx, int q, const int32_t* const* train, const int32_t* nt,
+                      const int32_t* const* roll, const int32_t* nr, const int32_t* const* etype,
+                      const int32_t* const* erep, const int32_t* ne, int window, double* out) {
+  if (q <= 0) return GP_OK;
+  const int T = ctx->T;
+  std::vector<int> ids, t_off, r_off, e_off, et, er;
+  for (int i = 0; i < q; ++i) {
+    t_off.push_back((int)ids.size());
+    ids.insert(ids.end(), train[i], train[i] + nt[i]);
+    r_off.push_back((int)ids.size());
+    ids.insert(ids.end(), roll[i], roll[i] + nr[i]);
+    e_off.push_back((int)et.size());
+    et.insert(et.end(), etype[i], etype[i] + ne[i]);
+    er.insert(er.end(), erep[i], erep[i] + ne[i]);
+  }
+  t_off.push_back((int)ids.size());
+  e_off.push_back((int)et.size());
+  for (int id : ids)
+    if (id < 0 || id >= ctx->N) return set_error(GP_INVALID, "unknown device id");
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+  add(sizeof(int) * (ids.size() + 1));
+  add(sizeof(int) * t_off.size());
+  add(sizeof(int) * r_off.size());
+  add(sizeof(int) * e_off.size());
+  add(sizeof(int) * (et.size() + 1));
+  add(sizeof(int) * (er.size() + 1));
+  add(sizeof(double) * (size_t)q * T);
+  add(sizeof(double) * q);
+  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaMisc));
+  if (!base) return GP_CUDA_ERROR;
+  char* p = base;
+  int* d_ids = carve2<int>(p, ids.size() + 1);
+  int* d_toff = carve2<int>(p, t_off.size());
+  int* d_roff = carve2<int>(p, r_off.size());
+  int* d_eoff = carve2<int>(p, e_off.size());
+  int* d_et = carve2<int>(p, et.size() + 1);
+  int* d_er = carve2<int>(p, er.size() + 1);
+  double* d_tm = carve2<double>(p, (size_t)q * T);
+  double* d_out = carve2<double>(p, q);
+  const size_t in_bytes = (size_t)((char*)(d_er + er.size() + 1) - (char*)d_ids);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(double) * q) + 256));
+  if (!hp) return GP_CUDA_ERROR;
+  auto put = [&](const std::vector<int>& v, void* dptr) {
+    if (!v.empty()) std::memcpy(hp + ((char*)dptr - (char*)d_ids), v.data(), sizeof(int) * v.size());
+  };
+  put(ids, d_ids);
+  put(t_off, d_toff);
+  put(r_off, d_roff);
+  put(e_off, d_eoff);
+  put(et, d_et);
+  put(er, d_er);
+  GP_CUDA(cudaMemcpyAsync(d_ids, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)in_bytes;
+  k6_batch_maxlink<<<q * T, 256, 0, ctx->stream>>>(d_ids, d_toff, d_roff, T, ctx->d_type, ctx->d_links, ctx->N,
+                                                   d_tm);
+  k6_batch_combine<<<(q + 127) / 128, 128, 0, ctx->stream>>>(q, T, d_tm, d_eoff, d_et, d_er, window, ctx->sc.mbi,
+                                                            ctx->sc.sync_latency, d_out);
+  ctx->launches += 2;
+  GP_CUDA(cudaGetLastError());
+  GP_CUDA(cudaMemcpyAsync(hp, d_out, sizeof(double) * q, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += (long long)(sizeof(double) * q);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(out, hp, sizeof(double) * q);
   return GP_OK;
 }
 

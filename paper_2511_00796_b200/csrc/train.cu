@@ -914,7 +914,7 @@ T* carve(char*& p, size_t count) {
 template <int R>
 int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const double2* blkf,
                 const BlockRec* blk, int window, long long lo, long long hi, Best* partial,
-                int max_blocks, TrainOut* d_out) {
+                int max_blocks, TrainOut* d_out, cudaStream_t stream) {
   ScanRange rg{};
   rank_split(h, lo, rg.p_lo, rg.s_lo);
   rank_split(h, hi, rg.p_hi, rg.s_hi);
@@ -931,14 +931,12 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   long long blocks = (n_items + (threads / 32) - 1) / (threads / 32);
   blocks = std::max(1LL, std::min(blocks, std::min((long long)max_blocks, (long long)ctx->num_sms * occ)));
   if (hi > lo) {
-    k1_layout_scan<R><<<(int)blocks, threads, 0, ctx->stream>>>(h.sp, tb, blkf, ctx->sc.L, window, rg,
-                                                                 partial);
+    k1_layout_scan<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, window, rg, partial);
     ctx->launches++;
   } else {
     blocks = 0;
   }
-  k1_finalize<R><<<1, 256, 0, ctx->stream>>>(h.sp, tb, blkf, blk, ctx->sc.L, window, partial,
-                                              (int)blocks, d_out);
+  k1_finalize<R><<<1, 256, 0, stream>>>(h.sp, tb, blkf, blk, ctx->sc.L, window, partial, (int)blocks, d_out);
   ctx->launches++;
   GP_CUDA(cudaGetLastError());
   return GP_OK;
@@ -980,6 +978,7 @@ struct PreparedTrain {
   Best* d_partial = nullptr;
   TrainOut* d_out = nullptr;
   int max_blocks = 0;
+  int L = 0;
   long long lo = 0, hi = 0;
   bool launched = false;
 };
@@ -993,25 +992,23 @@ void train_state_free(gp_ctx* ctx) {
   prepared(ctx) = nullptr;
 }
 
-int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o) {
-  if (!prepared(ctx)) prepared(ctx) = new PreparedTrain();
-  PreparedTrain& P = *prepared(ctx);
-  GP_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer / scratch may be reused
-  P.launched = false;
-  P.h = HostSpace();
-  int rc = build_space(ctx, ids, n, o, P.h);
-  if (rc) return rc;
-  HostSpace& h = P.h;
-  const int L = ctx->sc.L;
-  P.max_blocks = ctx->num_sms * 8;
+// ---- layout of one prepared train set in a device arena: the inputs section
+// (copied from host) first, then the tables the kernels build.
+static size_t input_bytes(const HostSpace& h) {
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
-  add(sizeof(int) * n);
+  add(sizeof(int) * h.sp.n);
   add(sizeof(int) * h.pos.size());
   add(sizeof(int) * h.run_start.size());
   add(sizeof(BlockMeta) * h.meta.size());
   add(sizeof(int4) * h.items.size());
   add(sizeof(int4) * h.choices.size());
+  return bytes;
+}
+
+static size_t table_bytes(const HostSpace& h, int L, int max_blocks) {
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
   add(sizeof(BlockRec) * h.nblk);
   add(sizeof(double2) * h.nblk);
   add(sizeof(double2) * (size_t)h.nblk * L);
@@ -1020,65 +1017,59 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
   add(sizeof(double) * (h.tx_size + 1));
   add(sizeof(double) * (GP_MAX_STAGES + 1));
   add(sizeof(SufEnt) * (h.choices.size() + 1));
-  add(sizeof(Best) * P.max_blocks);
-  add(sizeof(TrainOut));
-  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaTrain));
-  if (!base) return GP_CUDA_ERROR;
-  char* p = base;
-  P.d_ordered = carve<int>(p, n);
-  P.d_pos = carve<int>(p, h.pos.size());
-  P.d_run_start = carve<int>(p, h.run_start.size());
-  P.d_meta = carve<BlockMeta>(p, h.meta.size());
-  P.d_items = carve<int4>(p, h.items.size());
-  P.d_choices = carve<int4>(p, h.choices.size());
-  P.d_blk = carve<BlockRec>(p, h.nblk);
-  P.d_blkf = carve<double2>(p, h.nblk);
-  P.d_stage = carve<double2>(p, (size_t)h.nblk * L);
-  P.d_opt = carve<int8_t>(p, (size_t)h.nblk * L);
-  P.d_tin = carve<double>(p, h.tin_size + 1);
-  P.d_tx = carve<double>(p, h.tx_size + 1);
-  P.d_fd = carve<double>(p, GP_MAX_STAGES + 1);
-  P.d_suf = carve<SufEnt>(p, h.choices.size() + 1);
-  P.d_partial = carve<Best>(p, P.max_blocks);
-  P.d_out = carve<TrainOut>(p, 1);
-  // one pinned staging buffer -> one H2D copy of the enumeration metadata
-  const size_t in_bytes = (size_t)(P.d_choices + h.choices.size()) - (size_t)P.d_ordered;
-  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, sizeof(TrainOut))));
-  if (!hp) return GP_CUDA_ERROR;
-  auto stage_in = [&](const void* src, size_t sz, void* dptr) {
-    if (sz) std::memcpy(hp + ((char*)dptr - (char*)P.d_ordered), src, sz);
-  };
-  stage_in(h.ordered.data(), sizeof(int) * n, P.d_ordered);
-  stage_in(h.pos.data(), sizeof(int) * h.pos.size(), P.d_pos);
-  stage_in(h.run_start.data(), sizeof(int) * h.run_start.size(), P.d_run_start);
-  stage_in(h.meta.data(), sizeof(BlockMeta) * h.meta.size(), P.d_meta);
-  stage_in(h.items.data(), sizeof(int4) * h.items.size(), P.d_items);
-  stage_in(h.choices.data(), sizeof(int4) * h.choices.size(), P.d_choices);
-  GP_CUDA(cudaMemcpyAsync(P.d_ordered, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
-  ctx->h2d_bytes += (long long)in_bytes;
-  // sum over layouts of S (roofline accounting only): tot[r][u] = sum of stages of runs r..
-  {
-    double tot[GP_MAX_TYPES + 1][GP_MAX_STAGES + 1] = {};
-    const TrainSpace& sp = h.sp;
-    for (int r = sp.R - 1; r >= 0; --r)
-      for (int u = 0; u <= sp.max_stages; ++u) {
-        double acc = 0;
-        for (int k = 1; k <= sp.kmax[r]; ++k) {
-          if (u + k + (sp.R - 1 - r) > sp.max_stages) break;
-          const double c = (double)binom_small(sp.nc[r], k - 1);
-          acc += c * ((double)k * (double)sp.cnt[r + 1][u + k] + tot[r + 1][u + k]);
-        }
-        tot[r][u] = acc;
-      }
-    ctx->sum_stages = h.total ? tot[0][0] : 0;
-  }
-  return GP_OK;
+  add(sizeof(Best) * max_blocks);
+  return bytes;
 }
 
-int train_launch(gp_ctx* ctx, int window, long long lo, long long hi) {
-  PreparedTrain* PP = prepared(ctx);
-  if (!PP) return set_error(GP_INVALID, "gp_train_launch without gp_train_prepare");
-  PreparedTrain& P = *PP;
+// Carves the inputs at *in (device) and stages them into *hst (pinned host) at the same
+// offsets relative to `in_base`/`h_base`; then carves the tables at *tab.
+static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_base, char* h_base) {
+  const HostSpace& h = P.h;
+  auto stage = [&](const void* src, size_t sz, void* dptr) {
+    if (sz) std::memcpy(h_base + ((char*)dptr - in_base), src, sz);
+  };
+  P.d_ordered = carve<int>(in, h.sp.n);
+  stage(h.ordered.data(), sizeof(int) * h.sp.n, P.d_ordered);
+  P.d_pos = carve<int>(in, h.pos.size());
+  stage(h.pos.data(), sizeof(int) * h.pos.size(), P.d_pos);
+  P.d_run_start = carve<int>(in, h.run_start.size());
+  stage(h.run_start.data(), sizeof(int) * h.run_start.size(), P.d_run_start);
+  P.d_meta = carve<BlockMeta>(in, h.meta.size());
+  stage(h.meta.data(), sizeof(BlockMeta) * h.meta.size(), P.d_meta);
+  P.d_items = carve<int4>(in, h.items.size());
+  stage(h.items.data(), sizeof(int4) * h.items.size(), P.d_items);
+  P.d_choices = carve<int4>(in, h.choices.size());
+  stage(h.choices.data(), sizeof(int4) * h.choices.size(), P.d_choices);
+  P.d_blk = carve<BlockRec>(tab, h.nblk);
+  P.d_blkf = carve<double2>(tab, h.nblk);
+  P.d_stage = carve<double2>(tab, (size_t)h.nblk * P.L);
+  P.d_opt = carve<int8_t>(tab, (size_t)h.nblk * P.L);
+  P.d_tin = carve<double>(tab, h.tin_size + 1);
+  P.d_tx = carve<double>(tab, h.tx_size + 1);
+  P.d_fd = carve<double>(tab, GP_MAX_STAGES + 1);
+  P.d_suf = carve<SufEnt>(tab, h.choices.size() + 1);
+  P.d_partial = carve<Best>(tab, P.max_blocks);
+}
+
+static double sum_stages(const HostSpace& h) {
+  double tot[GP_MAX_TYPES + 1][GP_MAX_STAGES + 1] = {};
+  const TrainSpace& sp = h.sp;
+  for (int r = sp.R - 1; r >= 0; --r)
+    for (int u = 0; u <= sp.max_stages; ++u) {
+      double acc = 0;
+      for (int k = 1; k <= sp.kmax[r]; ++k) {
+        if (u + k + (sp.R - 1 - r) > sp.max_stages) break;
+        const double c = (double)binom_small(sp.nc[r], k - 1);
+        acc += c * ((double)k * (double)sp.cnt[r + 1][u + k] + tot[r + 1][u + k]);
+      }
+      tot[r][u] = acc;
+    }
+  return h.total ? tot[0][0] : 0;
+}
+
+// Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
+static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long lo, long long hi,
+                           cudaStream_t stream, bool timing) {
   const HostSpace& h = P.h;
   if (lo < 0) lo = 0;
   if (hi < 0 || hi > h.total) hi = h.total;
@@ -1099,60 +1090,47 @@ int train_launch(gp_ctx* ctx, int window, long long lo, long long hi) {
   tb.fd_coef = P.d_fd;
   tb.suf = P.d_suf;
   for (int r = 0; r < h.sp.R; ++r) tb.pos_off[r] = h.pos_off[r];
-  if (ctx->timing) GP_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  if (timing) GP_CUDA(cudaEventRecord(ctx->ev[0], stream));
   // ---- K2: per-train-set tables
-  k2a_block_stats<<<h.nblk, 256, 0, ctx->stream>>>(P.d_ordered, P.d_meta, P.d_pos, tb, P.d_blk,
-                                                   ctx->d_type, ctx->d_machine, ctx->d_flops,
-                                                   ctx->d_hbm_cap, ctx->d_links, ctx->N, L,
-                                                   ctx->sc.mb, P.d_fd);
+  k2a_block_stats<<<h.nblk, 256, 0, stream>>>(P.d_ordered, P.d_meta, P.d_pos, tb, P.d_blk, ctx->d_type,
+                                              ctx->d_machine, ctx->d_flops, ctx->d_hbm_cap, ctx->d_links,
+                                              ctx->N, L, ctx->sc.mb, P.d_fd);
   ctx->launches++;
   if (!h.items.empty()) {
     const int warps_per_block = 8;
     const int grid = (int)((h.items.size() + warps_per_block - 1) / warps_per_block);
-    k2b_transfers<<<grid, 32 * warps_per_block, 0, ctx->stream>>>(
-        P.d_ordered, P.d_items, (int)h.items.size(), P.d_pos, tb, h.sp, P.d_run_start, ctx->d_links,
-        ctx->N, ctx->sc.tokens > 0 ? ctx->sc.act_tok_h2 : 0.0, P.d_tin, P.d_tx);
+    k2b_transfers<<<grid, 32 * warps_per_block, 0, stream>>>(
+        P.d_ordered, P.d_items, (int)h.items.size(), P.d_pos, tb, h.sp, P.d_run_start, ctx->d_links, ctx->N,
+        ctx->sc.tokens > 0 ? ctx->sc.act_tok_h2 : 0.0, P.d_tin, P.d_tx);
     ctx->launches++;
   }
   {
     const long long cnt = (long long)h.nblk * L;
-    k2c_stage_table<<<(int)((cnt + 255) / 256), 256, 0, ctx->stream>>>(P.d_blk, h.nblk, ctx->sc,
-                                                                      ctx->d_ceff, P.d_stage, P.d_opt);
-    k_extract_blkf<<<(h.nblk + 255) / 256, 256, 0, ctx->stream>>>(P.d_blk, h.nblk, P.d_blkf);
+    k2c_stage_table<<<(int)((cnt + 255) / 256), 256, 0, stream>>>(P.d_blk, h.nblk, ctx->sc, ctx->d_ceff,
+                                                                 P.d_stage, P.d_opt);
+    k_extract_blkf<<<(h.nblk + 255) / 256, 256, 0, stream>>>(P.d_blk, h.nblk, P.d_blkf);
     const int ns = (int)h.choices.size();
-    k2d_suffix_table<<<(ns + 255) / 256, 256, 0, ctx->stream>>>(P.d_choices, ns, h.sp, P.d_tin,
-                                                                P.d_suf);
+    k2d_suffix_table<<<(ns + 255) / 256, 256, 0, stream>>>(P.d_choices, ns, h.sp, P.d_tin, P.d_suf);
     ctx->launches += 3;
   }
   GP_CUDA(cudaGetLastError());
-  if (ctx->timing) GP_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  if (timing) GP_CUDA(cudaEventRecord(ctx->ev[1], stream));
   // ---- K1: layout scan over [lo, hi)
   const int R = h.sp.R;
   int rc;
-  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
-  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
-  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
-  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out);
+  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream);
+  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream);
+  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream);
+  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream);
   else rc = set_error(GP_INVALID, "train sets spanning more than 4 gpu types are not supported");
-  if (!rc && ctx->timing) GP_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+  if (!rc && timing) GP_CUDA(cudaEventRecord(ctx->ev[2], stream));
   return rc;
 }
 
-int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices) {
+static void fill_result(const PreparedTrain& P, const TrainOut* ho, gp_train_result* out, int32_t* stage_devices) {
   std::memset(out, 0, sizeof *out);
-  PreparedTrain* PP = prepared(ctx);
-  if (!PP || !PP->launched) return set_error(GP_INVALID, "gp_train_collect without gp_train_launch");
-  PreparedTrain& P = *PP;
-  const HostSpace& h = P.h;
   out->layouts = P.hi - P.lo;
-  if (h.total == 0 || P.lo == P.hi) {
-    GP_CUDA(cudaStreamSynchronize(ctx->stream));
-    return GP_OK;
-  }
-  TrainOut* ho = reinterpret_cast<TrainOut*>(ctx_pinned(ctx, sizeof(TrainOut)));
-  GP_CUDA(cudaMemcpyAsync(ho, P.d_out, sizeof(TrainOut), cudaMemcpyDeviceToHost, ctx->stream));
-  ctx->d2h_bytes += (long long)sizeof(TrainOut);
-  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (!ho) return;
   out->feasible = ho->best.feasible;
   if (ho->best.rank != LLONG_MAX) {
     out->found = 1;
@@ -1166,8 +1144,57 @@ int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices) {
       out->stage[s].dp = ho->dp[s];
       out->stage[s].layers = ho->layers[s];
     }
-    if (stage_devices) std::memcpy(stage_devices, h.ordered.data(), sizeof(int32_t) * h.sp.n);
+    if (stage_devices) std::memcpy(stage_devices, P.h.ordered.data(), sizeof(int32_t) * P.h.sp.n);
   }
+}
+
+int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o) {
+  if (!prepared(ctx)) prepared(ctx) = new PreparedTrain();
+  PreparedTrain& P = *prepared(ctx);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer / scratch may be reused
+  P.launched = false;
+  P.h = HostSpace();
+  int rc = build_space(ctx, ids, n, o, P.h);
+  if (rc) return rc;
+  P.L = ctx->sc.L;
+  P.max_blocks = ctx->num_sms * 8;
+  const size_t ib = input_bytes(P.h), tbytes = table_bytes(P.h, P.L, P.max_blocks);
+  char* base = static_cast<char*>(ctx_scratch(ctx, ib + tbytes + sizeof(TrainOut) + 512, kArenaTrain));
+  if (!base) return GP_CUDA_ERROR;
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(ib, sizeof(TrainOut)) + 256));
+  if (!hp) return GP_CUDA_ERROR;
+  char* in = base;
+  char* tab = base + ib;
+  carve_prepared(P, in, tab, base, hp);
+  P.d_out = carve<TrainOut>(tab, 1);
+  const size_t in_bytes = (size_t)(in - base);
+  GP_CUDA(cudaMemcpyAsync(base, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)in_bytes;
+  ctx->sum_stages = sum_stages(P.h);
+  return GP_OK;
+}
+
+int train_launch(gp_ctx* ctx, int window, long long lo, long long hi) {
+  PreparedTrain* PP = prepared(ctx);
+  if (!PP) return set_error(GP_INVALID, "gp_train_launch without gp_train_prepare");
+  return launch_prepared(ctx, *PP, window, lo, hi, ctx->stream, ctx->timing);
+}
+
+int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices) {
+  std::memset(out, 0, sizeof *out);
+  PreparedTrain* PP = prepared(ctx);
+  if (!PP || !PP->launched) return set_error(GP_INVALID, "gp_train_collect without gp_train_launch");
+  PreparedTrain& P = *PP;
+  if (P.h.total == 0 || P.lo == P.hi) {
+    GP_CUDA(cudaStreamSynchronize(ctx->stream));
+    fill_result(P, nullptr, out, stage_devices);
+    return GP_OK;
+  }
+  TrainOut* ho = reinterpret_cast<TrainOut*>(ctx_pinned(ctx, sizeof(TrainOut)));
+  GP_CUDA(cudaMemcpyAsync(ho, P.d_out, sizeof(TrainOut), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += (long long)sizeof(TrainOut);
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  fill_result(P, ho, out, stage_devices);
   return GP_OK;
 }
 
@@ -1178,6 +1205,51 @@ int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_tr
   if (!rc) rc = train_launch(ctx, window, lo, hi);
   if (!rc) rc = train_collect(ctx, out, stage_devices);
   return rc;
+}
+
+// Batched constrained_search over many train sets (the scheduler's evaluation batches):
+// every set's inputs travel in ONE H2D copy, all tables + scans are enqueued back to back,
+// the results come back in ONE D2H copy with ONE synchronisation.
+int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
+                const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices) {
+  if (n_sets <= 0) return GP_OK;
+  std::vector<PreparedTrain> Ps(n_sets);
+  size_t ib = 0, tbytes = 0;
+  for (int i = 0; i < n_sets; ++i) {
+    int rc = build_space(ctx, ids[i], ns[i], o, Ps[i].h);
+    if (rc) return rc;
+    Ps[i].L = ctx->sc.L;
+    Ps[i].max_blocks = std::min(ctx->num_sms * 8, (int)std::max<long long>(1, Ps[i].h.total / 4096));
+    ib += input_bytes(Ps[i].h);
+    tbytes += table_bytes(Ps[i].h, Ps[i].L, Ps[i].max_blocks);
+  }
+  const size_t out_bytes = sizeof(TrainOut) * n_sets;
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  char* base = static_cast<char*>(ctx_scratch(ctx, ib + tbytes + out_bytes + 1024, kArenaTrain));
+  if (!base) return GP_CUDA_ERROR;
+  char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(ib, out_bytes) + 1024));
+  if (!hp) return GP_CUDA_ERROR;
+  char* in = base;
+  char* tab = base + ib;
+  for (int i = 0; i < n_sets; ++i) carve_prepared(Ps[i], in, tab, base, hp);
+  TrainOut* d_out = carve<TrainOut>(tab, n_sets);
+  for (int i = 0; i < n_sets; ++i) Ps[i].d_out = d_out + i;
+  const size_t in_bytes = (size_t)(in - base);
+  GP_CUDA(cudaMemcpyAsync(base, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)in_bytes;
+  for (int i = 0; i < n_sets; ++i) {
+    int rc = launch_prepared(ctx, Ps[i], window, 0, -1, ctx->stream, false);
+    if (rc) return rc;
+  }
+  TrainOut* ho = reinterpret_cast<TrainOut*>(hp);
+  GP_CUDA(cudaMemcpyAsync(ho, d_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += (long long)out_bytes;
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n_sets; ++i) {
+    const bool ran = Ps[i].h.total > 0;
+    fill_result(Ps[i], ran ? ho + i : nullptr, outs + i, stage_devices ? stage_devices[i] : nullptr);
+  }
+  return GP_OK;
 }
 
 }  // namespace gp

@@ -271,3 +271,54 @@ class Engine:
         _check(lib().gp_partition_objective(self._h, t.ctypes.data_as(abi.i32p), len(t), C.byref(obj),
                                             C.byref(frac)))
         return obj.value, frac.value
+
+    # ---- Algorithm-1 driver -----------------------------------------------------
+    def schedule(self, eta: int = -1, seed: int = 0x5EED, expand_window: bool = True, restarts: int = 16,
+                 with_stats: bool = False):
+        """schedule() (inc/scheduler.hpp:53-54) on the engine. Returns the plan_to_json fields
+        (src/plan_io.cpp:43-75, values only, no fingerprints) plus the iteration trace."""
+        L = lib()
+        L.gp_default_sched_opts.argtypes = [C.POINTER(abi.gp_sched_opts)]
+        L.gp_default_sched_opts.restype = None
+        o = abi.gp_sched_opts()
+        L.gp_default_sched_opts(C.byref(o))
+        o.eta_override, o.seed, o.expand_window, o.restarts = eta, seed, int(expand_window), restarts
+        N = self.n_devices
+        res = abi.gp_schedule_result()
+        tr = np.zeros(N, dtype=np.int32)
+        ro = np.zeros(N, dtype=np.int32)
+        sd = np.zeros(N, dtype=np.int32)
+        cap = 8 * 70
+        cfg = (abi.gp_config * cap)()
+        ent = (abi.gp_rollout_entry * cap)()
+        trace = np.zeros(4 * o.iteration_cap, dtype=np.float64)
+        L.gp_schedule.argtypes = [C.c_void_p, C.POINTER(abi.gp_sched_opts), C.POINTER(abi.gp_schedule_result),
+                                  abi.i32p, abi.i32p, abi.i32p, C.POINTER(abi.gp_config),
+                                  C.POINTER(abi.gp_rollout_entry), C.c_int32, abi.f64p]
+        _check(L.gp_schedule(self._h, C.byref(o), C.byref(res), tr.ctypes.data_as(abi.i32p),
+                             ro.ctypes.data_as(abi.i32p), sd.ctypes.data_as(abi.i32p), cfg, ent, cap,
+                             trace.ctypes.data_as(abi.f64p)))
+        T = len(self.problem.cluster.type_names)
+        t = res.train
+        plan = {
+            "window_steps": res.window, "staleness": res.staleness, "iterations_run": res.iterations_run,
+            "converged": bool(res.converged),
+            "partition": {"train": tr[:res.n_train].tolist(), "rollout": ro[:res.n_rollout].tolist()},
+            "train_plan": {"stages": [{"devices": sd[s.first:s.first + s.count].tolist(), "tp": s.tp,
+                                       "dp": s.dp, "layers": s.layers} for s in t.stage[:t.n_stages]],
+                           "cost_s": t.cost},
+            "rollout_plan": {"entries": [{"type_counts": list(cfg[i].type_counts[:T]),
+                                          "tp_per_stage": list(cfg[i].tp[:cfg[i].n_stages]),
+                                          "throughput_tps": cfg[i].throughput,
+                                          "machine_footprint": list(cfg[i].tp[:cfg[i].n_stages]),
+                                          "replicas": ent[i].replicas, "workload_rollouts": ent[i].workload}
+                                         for i in range(res.rollout.n_entries)],
+                             "makespan_s": res.rollout.makespan, "total_rollouts": res.rollout.total_rollouts},
+            "costs": {"train_s": res.c_train, "rollout_s": res.c_rollout, "reward_s": res.c_reward,
+                      "update_s": res.c_update, "infer_total_s": res.c_infer_total, "window_steps": res.window},
+        }
+        tr_rows = trace[:4 * res.n_trace].reshape(-1, 4).tolist()
+        if with_stats:
+            return plan, tr_rows, {"evaluated_partitions": res.evaluated_partitions,
+                                   "evaluated_layouts": res.evaluated_layouts}
+        return plan, tr_rows
