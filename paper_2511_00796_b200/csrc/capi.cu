@@ -4,6 +4,7 @@
 #include <signal.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -54,7 +55,9 @@ void* ctx_scratch(gp_ctx* ctx, size_t bytes, int arena) {
   if (bytes > have) {
     if (buf) cudaFree(buf);
     buf = nullptr;
-    size_t want = bytes + bytes / 4;
+    // 1.5x headroom with a 4 MiB floor: the scheduler's batches vary in size and a
+    // cudaMalloc/cudaFree pair costs more than the kernels of a small batch
+    size_t want = std::max(bytes + bytes / 2, (size_t)4 << 20);
     cudaError_t e = cudaMalloc(&buf, want);
     if (e != cudaSuccess) {
       have = 0;
@@ -70,7 +73,7 @@ void* ctx_pinned(gp_ctx* ctx, size_t bytes) {
   if (bytes > ctx->h_pinned_bytes) {
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
     ctx->h_pinned = nullptr;
-    size_t want = bytes + bytes / 4 + 4096;
+    size_t want = std::max(bytes + bytes / 2 + 4096, (size_t)4 << 20);
     cudaError_t e = cudaMallocHost(&ctx->h_pinned, want);
     if (e != cudaSuccess) {
       ctx->h_pinned_bytes = 0;

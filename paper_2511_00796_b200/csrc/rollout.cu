@@ -611,16 +611,19 @@ static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, con
   std::vector<std::pair<long long, int>> key;
   int rc = milp_groups(cfg, nc, dims, key);
   if (rc) return rc;
-  // lattice to tabulate: the union with a cached table of the same configs when it fits
+  // lattice to tabulate: the union with a cached table of the same configs when that
+  // grows the state count by at most 2x (a union of unlike lattices multiplies states)
   std::vector<int> lat(caps, caps + dims);
   if (same) {
-    long long u = 1;
+    long long u = 1, own = 1;
     std::vector<int> un(dims);
     for (int t = 0; t < dims; ++t) {
       un[t] = std::max(caps[t], same->d.cap[t]);
       u *= un[t] + 1;
+      own *= caps[t] + 1;
     }
-    if (u <= 50000000) lat = un;
+    if (u <= 50000000 && u <= 2 * std::max(own, same->d.states)) lat = un;
+    else same = nullptr;  // keep the cached table; tabulate this lattice separately
   }
   MilpTable* tab = same;
   if (!tab) {
@@ -848,20 +851,35 @@ int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs,
     for (size_t j = g0; j < g1; ++j)
       if (rcs[order[j]] == GP_OK) live.push_back(order[j]);
     if (!live.empty()) {
-      // union lattice of the group (split into single queries if it would exceed 5e7)
-      std::vector<int> un(dims, 0);
-      long long u = 1;
-      for (int t = 0; t < dims; ++t) {
-        for (int i : live) un[t] = std::max(un[t], (int)caps[i][t]);
-        u *= un[t] + 1;
+      // largest lattices first: each later query whose capacities are covered by an
+      // already tabulated lattice of the group is answered from that table
+      std::sort(live.begin(), live.end(), [&](int a, int b) {
+        long long sa = 1, sb = 1;
+        for (int t = 0; t < dims; ++t) {
+          sa *= caps[a][t] + 1;
+          sb *= caps[b][t] + 1;
+        }
+        return sa > sb || (sa == sb && a < b);
+      });
+      std::vector<std::vector<int>> parts;      // queries per table
+      std::vector<std::vector<int>> part_caps;  // the table's lattice
+      for (int i : live) {
+        int hit = -1;
+        for (size_t pidx = 0; pidx < parts.size() && hit < 0; ++pidx) {
+          bool cov = true;
+          for (int t = 0; t < dims && cov; ++t) cov = caps[i][t] <= part_caps[pidx][t];
+          if (cov) hit = (int)pidx;
+        }
+        if (hit < 0) {
+          parts.push_back({});
+          part_caps.emplace_back(caps[i], caps[i] + dims);
+          hit = (int)parts.size() - 1;
+        }
+        parts[hit].push_back(i);
       }
-      std::vector<std::vector<int>> parts;
-      if (u <= 50000000) parts.push_back(live);
-      else for (int i : live) parts.push_back({i});
-      for (auto& part : parts) {
-        std::vector<int> pc(dims, 0);
-        for (int t = 0; t < dims; ++t)
-          for (int i : part) pc[t] = std::max(pc[t], (int)caps[i][t]);
+      for (size_t pidx = 0; pidx < parts.size(); ++pidx) {
+        const std::vector<int>& part = parts[pidx];
+        const std::vector<int>& pc = part_caps[pidx];
         const int i0 = part[0];
         MilpTable* tab = nullptr;
         int rc = ensure_table(ctx, cfgs[i0], ncs[i0], dims, pc.data(), &tab);

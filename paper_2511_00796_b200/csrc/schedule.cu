@@ -10,7 +10,10 @@
 // exactly as SearchPhase (src/scheduler.cpp:106-120); graph_partition_candidates is
 // a pure function of the band, so its results are reused across passes.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -34,6 +37,25 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
                          int32_t* train_ids, int32_t* n_out);
 
 namespace {
+
+// GPLAN_PROFILE=1: host wall time per driver phase (stderr)
+struct Phase {
+  double sec[6] = {};
+  ~Phase() {
+    if (!std::getenv("GPLAN_PROFILE")) return;
+    static const char* n[6] = {"partition", "train_batch", "configs_batch", "milp_batch", "weight_sync", "host"};
+    for (int i = 0; i < 6; ++i) std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", n[i], sec[i]);
+  }
+} g_phase;
+
+struct PhaseTimer {
+  int id;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit PhaseTimer(int i) : id(i) {}
+  ~PhaseTimer() {
+    g_phase.sec[id] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
 
 struct Eval {  // IterationResult (src/scheduler.cpp:11-17)
   std::vector<int> train, roll;
@@ -103,11 +125,15 @@ struct Driver {
     }
     // train side: constrained_search
     std::vector<gp_train_result> tr(q);
+    PhaseTimer* pt = new PhaseTimer(1);
     int rc = train_batch(ctx, q, tids.data(), tn.data(), window, &o.train, tr.data(), sdev.data());
+    delete pt;
     if (rc) return rc;
     // rollout side: enumerate_configs + solve_milp
     std::vector<std::vector<gp_config>> cfgs;
+    pt = new PhaseTimer(2);
     rc = configs_batch(ctx, q, rids.data(), rn.data(), &o.rollout, cfgs);
+    delete pt;
     if (rc) return rc;
     const int T = ctx->T;
     std::vector<int> mq;  // sets with configs
@@ -134,8 +160,10 @@ struct Driver {
         ent[j].assign(nc[j], gp_rollout_entry{});
         ep[j] = ent[j].data();
       }
+      pt = new PhaseTimer(3);
       rc = milp_batch(ctx, m, cp.data(), nc.data(), capp.data(), T, Bs.data(), ctx->work.mean_len, rr.data(),
                       ep.data(), rcs.data());
+      delete pt;
       if (rc) return rc;
       for (int j = 0; j < m; ++j) {
         const int i = mq[j];
@@ -191,8 +219,10 @@ struct Driver {
         wer[j] = er[j].data();
         wne[j] = (int32_t)et[j].size();
       }
+      pt = new PhaseTimer(4);
       rc = weight_sync_batch(ctx, w, wt.data(), wtn.data(), wr.data(), wrn.data(), wet.data(), wer.data(),
                              wne.data(), window, upd.data());
+      delete pt;
       if (rc) return rc;
       for (int j = 0; j < w; ++j) {
         Eval& e = *ev[wq[j]];
@@ -216,6 +246,7 @@ struct Driver {
       out = it->second;
       return GP_OK;
     }
+    PhaseTimer pt(0);
     const int k = std::max(1, o.candidate_width);
     gp_part_opts po{o.exact_threshold, o.restarts, o.seed, o.band_epsilon, o.force_local_search,
                     o.machine_granularity};
