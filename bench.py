@@ -337,8 +337,44 @@ def run_b200(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(p)
+    if not args.no_ttp:
+        line["time_to_best_plan"] = time_to_best_plan(local_rank)
     print(json.dumps(line), flush=True)
     return 0
+
+
+def time_to_best_plan(device, keys=("c3_64gpu/eta=1", "c4_256gpu/eta=2")):
+    """schedule() wall time (all window passes, up to the final plan) through the native
+    batched driver (gp_schedule) on a freshly created context (context setup excluded,
+    like the reference's input loading); the reference's own schedule() on one host core
+    for the configs it can finish, with the plans compared field by field."""
+    from common import problem as load
+    from oracles import Ref, ref_available
+
+    from paper_2511_00796_b200.engine import Engine
+    out = {}
+    for key in keys:
+        name, eta = key.split("/eta=")
+        prob = load(name)
+        with Engine(prob, device=device) as eng:  # warm-up run: CUDA module load, first allocations
+            eng.schedule(eta=int(eta), seed=4276115)
+        with Engine(prob, device=device) as eng:
+            t = time.perf_counter()
+            plan, _ = eng.schedule(eta=int(eta), seed=4276115)
+            b200_s = time.perf_counter() - t
+        row = {"b200_s": b200_s, "window": plan["window_steps"],
+               "objective": max(plan["costs"]["train_s"], plan["costs"]["infer_total_s"])}
+        if name in ("c1_desk_mixed", "c2_16gpu", "c3_64gpu") and ref_available():
+            t = time.perf_counter()
+            ref = json.loads(Ref(prob).schedule(eta=int(eta))["plan_json"])
+            row["reference_cpu_s"] = time.perf_counter() - t
+            for k in ("format", "cluster_fingerprint", "calibration_fingerprint", "workload_fingerprint"):
+                ref.pop(k, None)
+            row["plan_identical"] = ref == plan
+        elif name == "c4_256gpu":
+            row["reference_cpu_s"] = "did not finish in 25 min (SURVEY.md 6)"
+        out[key] = row
+    return out
 
 
 def main():
@@ -348,6 +384,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ttp", action="store_true", help="skip the time-to-best-plan runs")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
