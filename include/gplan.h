@@ -198,7 +198,10 @@ int gp_train_space(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_op
 
 /* constrained_search(train_set, cluster, work, calib, window, options)
  * (inc/train_search.hpp:29-33). stage_devices must hold n ints; stage s owns
- * stage_devices[stage[s].first .. +count). Empty train set -> GP_INVALID. */
+ * stage_devices[stage[s].first .. +count). Empty train set -> GP_INVALID.
+ * The scan is window-independent: each train set's near-minimum summary is
+ * memoised on the context, and a later call for the same set with another
+ * window is answered from it bit-exactly (gp_ctx_set_memo(ctx, 0) disables). */
 int gp_constrained_search(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
                           const gp_train_opts* opts, gp_train_result* out,
                           int32_t* stage_devices);
@@ -225,6 +228,8 @@ void* gp_ctx_stream(gp_ctx* ctx);
  * calls so far; sum over the prepared space of the stage count; FP64 pipe
  * throughput probe (DADD/s) used as the roofline denominator. */
 int gp_ctx_set_timing(gp_ctx* ctx, int on);
+/* Enable (default) / disable + drop the constrained_search memo. */
+int gp_ctx_set_memo(gp_ctx* ctx, int on);
 int gp_train_timing(gp_ctx* ctx, float* k2_ms, float* k1_ms);
 void gp_ctx_io_bytes(gp_ctx* ctx, long long* h2d, long long* d2h, double* sum_stages);
 int gp_fp64_peak(gp_ctx* ctx, double* dadd_per_s);

@@ -5,6 +5,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +22,13 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
 int train_launch(gp_ctx* ctx, int window, long long lo, long long hi);
 int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices);
 void train_state_free(gp_ctx* ctx);
+void train_last_nm(gp_ctx* ctx, long long nm[4]);
+void train_nm_merge(long long a[4], const long long b[4]);
+void train_memo_free(gp_ctx* ctx);
+std::string train_memo_key(const int32_t* ids, int n, const gp_train_opts* o);
+bool train_memo_get(gp_ctx* ctx, const std::string& key, int window, gp_train_result* out,
+                    int32_t* stage_devices);
+void train_memo_put_last(gp_ctx* ctx, const std::string& key, const gp_train_result& r, const long long nm[4]);
 void milp_cache_free(gp_ctx* ctx);
 void part_cache_free(gp_ctx* ctx);
 int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opts* o, gp_config* out,
@@ -251,6 +259,7 @@ void gp_ctx_destroy(gp_ctx* ctx) {
     if (p) cudaFree(p);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   train_state_free(ctx);
+  train_memo_free(ctx);
   milp_cache_free(ctx);
   part_cache_free(ctx);
   for (auto& e : ctx->ev)
@@ -274,7 +283,7 @@ int gp_train_space(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_op
 // are reduced lexicographically on the host (first rank among equal costs).
 static int search_fanout(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
                          const gp_train_opts* o, int64_t lo, int64_t hi, gp_train_result* out,
-                         int32_t* stage_devices) {
+                         int32_t* stage_devices, long long nm[4]) {
   int64_t total = 0;
   int rc = train_space(ctx, ids, n, o, &total);
   if (rc) return rc;
@@ -284,7 +293,9 @@ static int search_fanout(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t win
   const int P = 1 + (int)ctx->peers.size();
   if (ctx->peers.empty() || hi - lo < kFanoutMinLayouts) {
     cudaSetDevice(ctx->device);
-    return train_search(ctx, ids, n, window, o, lo, hi, out, stage_devices);
+    rc = train_search(ctx, ids, n, window, o, lo, hi, out, stage_devices);
+    if (!rc) train_last_nm(ctx, nm);
+    return rc;
   }
   std::vector<gp_ctx*> devs{ctx};
   devs.insert(devs.end(), ctx->peers.begin(), ctx->peers.end());
@@ -297,12 +308,17 @@ static int search_fanout(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t win
   }
   std::memset(out, 0, sizeof *out);
   out->layouts = hi - lo;
+  nm[0] = 0x7ff0000000000000LL;
+  nm[1] = nm[2] = nm[3] = LLONG_MAX;
   std::vector<int32_t> tmp(n > 0 ? n : 1);
   for (int i = 0; i < P; ++i) {
     cudaSetDevice(devs[i]->device);
     gp_train_result r;
     rc = train_collect(devs[i], &r, tmp.data());
     if (rc) return rc;
+    long long nmi[4];
+    train_last_nm(devs[i], nmi);
+    train_nm_merge(nm, nmi);
     out->feasible += r.feasible;
     if (r.found && (!out->found || r.cost < out->cost || (r.cost == out->cost && r.rank < out->rank))) {
       const int64_t layouts = out->layouts, feasible = out->feasible;
@@ -319,14 +335,23 @@ static int search_fanout(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t win
 int gp_constrained_search(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
                           const gp_train_opts* o, gp_train_result* out, int32_t* stage_devices) {
   if (!ctx) return set_error(GP_INVALID, "null context");
-  return search_fanout(ctx, ids, n, window, o, 0, -1, out, stage_devices);
+  std::string key;
+  if (ids && o && n > 0) {
+    key = train_memo_key(ids, n, o);
+    if (train_memo_get(ctx, key, window, out, stage_devices)) return GP_OK;
+  }
+  long long nm[4];
+  const int rc = search_fanout(ctx, ids, n, window, o, 0, -1, out, stage_devices, nm);
+  if (!rc && !key.empty()) train_memo_put_last(ctx, key, *out, nm);
+  return rc;
 }
 
 int gp_constrained_search_range(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
                                 const gp_train_opts* o, int64_t lo, int64_t hi,
                                 gp_train_result* out, int32_t* stage_devices) {
   if (!ctx) return set_error(GP_INVALID, "null context");
-  return search_fanout(ctx, ids, n, window, o, lo, hi, out, stage_devices);
+  long long nm[4];  // explicit ranges are never memoised: every call scans its range
+  return search_fanout(ctx, ids, n, window, o, lo, hi, out, stage_devices, nm);
 }
 
 int gp_ctx_create_multi(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
@@ -445,6 +470,13 @@ int gp_schedule(gp_ctx* ctx, const gp_sched_opts* opts, gp_schedule_result* out,
   if (!ctx || !opts) return set_error(GP_INVALID, "null argument");
   cudaSetDevice(ctx->device);
   return schedule(ctx, opts, out, train_ids, rollout_ids, stage_devices, entry_configs, entries, entry_cap, trace);
+}
+
+int gp_ctx_set_memo(gp_ctx* ctx, int on) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  ctx->memo = on != 0;
+  if (!ctx->memo) train_memo_free(ctx);
+  return GP_OK;
 }
 
 int gp_ctx_set_timing(gp_ctx* ctx, int on) {

@@ -143,6 +143,9 @@ struct gp_ctx {
   void* train_state = nullptr;
   void* milp_cache = nullptr;
   void* part_cache[2] = {nullptr, nullptr};  // partition unit tables per granularity (partition.cu)
+  // constrained_search results per train set, window-independent (train.cu TrainMemo)
+  void* train_memo = nullptr;
+  bool memo = true;
   // peer contexts on other GPUs (gp_ctx_create_multi): constrained_search fans out over them
   std::vector<gp_ctx*> peers;
   // optional device timing of the train phases (bench.py): events around K2 and K1

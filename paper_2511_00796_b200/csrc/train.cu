@@ -24,6 +24,8 @@
 #include <climits>
 #include <cstring>
 #include <numeric>
+#include <string>
+#include <unordered_map>
 
 #include "gp_internal.h"
 
@@ -31,6 +33,8 @@ namespace gp {
 
 struct TrainOut {
   Best best;
+  long long nm_b0;       // near-minimum summary of the scanned range (NearMin), keys decoded to ranks
+  long long nm_rank[3];
   int n_stages;
   int pad;
   int first[GP_MAX_STAGES];
@@ -68,6 +72,67 @@ __device__ double block_min(double v, double* sm) {
 
 __device__ __forceinline__ bool better(double c1, long long r1, double c2, long long r2) {
   return c1 < c2 || (c1 == c2 && r1 < r2);
+}
+
+// Window-independent argmin summary. The reference scores a layout by
+// cost = window * per_step (src/train_search.cpp, oracle/oracle.c:337) and keeps the first
+// rank of minimal cost. fl(window * x) is monotone in x, so the minimal cost is
+// fl(window * x_min), and a layout ties with it only if fl(window * x) == fl(window * x_min),
+// which needs x < x_min + 2 ulp(x_min) (|w x - w x_min| < ulp(w x_min) <= 2 w ulp(x_min)).
+// Positive doubles order like their bit patterns, so it suffices to keep, for the three bit
+// patterns b0, b0+1, b0+2 above the smallest per-step time b0, the first key reaching each:
+// the argmin for ANY window is then the first key among the patterns whose scaled cost equals
+// the smallest one. One scan therefore answers every window of the scheduler's passes.
+struct NearMin {
+  long long b0;      // bit pattern of the smallest feasible per-step time (kInfBits when none)
+  long long key[3];  // first key whose per-step time has bit pattern b0 + i (LLONG_MAX if none)
+  long long feasible;
+};
+
+constexpr long long kInfBits = 0x7ff0000000000000LL;
+
+__host__ __device__ __forceinline__ void nm_init(NearMin& m) {
+  m.b0 = kInfBits;
+  m.key[0] = m.key[1] = m.key[2] = LLONG_MAX;
+  m.feasible = 0;
+}
+
+// key of pattern b0 + j (selects, not a dynamic index: keeps summaries in registers)
+__host__ __device__ __forceinline__ long long nm_at(const NearMin& m, long long j) {
+  return j == 0 ? m.key[0] : j == 1 ? m.key[1] : j == 2 ? m.key[2] : LLONG_MAX;
+}
+
+// m := merge(m, o); both summaries are exact for disjoint key sets.
+__host__ __device__ __forceinline__ void nm_merge(NearMin& m, const NearMin& o) {
+  m.feasible += o.feasible;
+  const long long base = o.b0 < m.b0 ? o.b0 : m.b0;
+  const long long dm = m.b0 - base, dn = o.b0 - base;
+  long long k[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const long long a = nm_at(m, i - dm), b = nm_at(o, i - dn);
+    k[i] = a < b ? a : b;
+  }
+  m.b0 = base;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) m.key[i] = k[i];
+}
+
+// First key among the near-minimum patterns whose window-scaled cost is the minimum.
+__host__ __device__ __forceinline__ long long nm_winner(const NearMin& m, int window, double& cost) {
+  long long bits = m.b0;
+  double x0;
+  memcpy(&x0, &bits, sizeof x0);
+  cost = window * x0;
+  long long win = LLONG_MAX;
+  for (int i = 0; i < 3; ++i) {
+    if (m.key[i] == LLONG_MAX) continue;
+    bits = m.b0 + i;
+    double x;
+    memcpy(&x, &bits, sizeof x);
+    if (window * x == cost && m.key[i] < win) win = m.key[i];
+  }
+  return win;
 }
 
 // ---------------------------------------------------------------- K2a blocks
@@ -457,8 +522,8 @@ __device__ __forceinline__ double div_rn_recip(double a, double b, double y) {
 // Score (prefix, suffix). Returns false when some stage has no memory-feasible option.
 template <int R, bool DECODE>
 __device__ __forceinline__ bool eval_layout(const TrainSpace& sp, const TrainTables& tb,
-                                            const double2* __restrict__ blkf, int L, int window,
-                                            const PrefixData<R>& D, const SufEnt& e, double& cost,
+                                            const double2* __restrict__ blkf, int L,
+                                            const PrefixData<R>& D, const SufEnt& e, double& per_step,
                                             int* out_lay, int* out_bi) {
   constexpr int NP = (R - 1) * kMaxPerRun;
   constexpr int NS = NP + kMaxPerRun;
@@ -577,8 +642,7 @@ __device__ __forceinline__ bool eval_layout(const TrainSpace& sp, const TrainTab
   for (int j = 0; j < 3; ++j)
     if (j + 1 < k) transfers += e.t[j];
   const double fill = tb.fd_coef[S] * max_comp;
-  const double per_step = max_total + fill + transfers;
-  cost = window * per_step;
+  per_step = max_total + fill + transfers;
   return true;
 }
 
@@ -591,19 +655,47 @@ struct ScanRange {
 
 constexpr int kK1Threads = 128;
 
+__device__ __forceinline__ NearMin nm_shfl_xor(const NearMin& m, int o) {
+  NearMin r;
+  r.b0 = __shfl_xor_sync(0xffffffffu, m.b0, o);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r.key[i] = __shfl_xor_sync(0xffffffffu, m.key[i], o);
+  r.feasible = __shfl_xor_sync(0xffffffffu, m.feasible, o);
+  return r;
+}
+
+// CTA-wide merge; the result is valid in thread 0.
+__device__ NearMin nm_block_reduce(NearMin m) {
+  __shared__ NearMin sb[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nm_merge(m, nm_shfl_xor(m, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sb[wid] = m;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    if (lane < nw) {
+      m = sb[lane];
+    } else {
+      nm_init(m);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nm_merge(m, nm_shfl_xor(m, o));
+  }
+  return m;
+}
+
 template <int R>
 __global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(TrainSpace sp, TrainTables tb,
                                                       const double2* __restrict__ blkf, int L,
-                                                      int window, ScanRange rg,
-                                                      Best* __restrict__ partial) {
+                                                      ScanRange rg, NearMin* __restrict__ partial) {
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
   const long long n_suf = sp.n_suf;
-  double best_cost = kInf * 10;
-  long long best_key = LLONG_MAX;
-  long long feasible = 0;
+  // thread summary in registers: NearMin {b0, k0..k2, feasible}
+  long long b0 = kInfBits, k0 = LLONG_MAX, k1 = LLONG_MAX, k2 = LLONG_MAX, feasible = 0;
   // the warp's current prefix lives in shared memory (lane 0 owns it; lanes read broadcasts)
   __shared__ Prefix<R> sP[kK1Threads / 32];
   __shared__ PrefixData<R> sD[kK1Threads / 32];
@@ -623,12 +715,24 @@ __global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(Tra
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
       for (long long s = s0 + lane; s < s1; s += 32) {
         const SufEnt e = tb.suf[s];
-        double cost;
-        if (eval_layout<R, false>(sp, tb, blkf, L, window, D, e, cost, nullptr, nullptr)) {
+        double x;
+        if (eval_layout<R, false>(sp, tb, blkf, L, D, e, x, nullptr, nullptr)) {
           ++feasible;
-          if (cost < best_cost) {  // strict <: first in enumeration order wins ties
-            best_cost = cost;
-            best_key = p * n_suf + s;
+          // keys grow along a thread's walk: only a new minimum or a pattern within two
+          // ulps of it can change the summary, and a pattern already held keeps its key
+          const long long d = __double_as_longlong(x) - b0;
+          if (d < 3) {
+            const long long key = p * n_suf + s;
+            if (d < 0) {  // new minimum: shift the held patterns up by -d
+              k2 = d == -1 ? k1 : d == -2 ? k0 : LLONG_MAX;
+              k1 = d == -1 ? k0 : LLONG_MAX;
+              k0 = key;
+              b0 += d;
+            } else if (d == 1) {
+              k1 = min(k1, key);
+            } else if (d == 2) {
+              k2 = min(k2, key);
+            }
           }
         }
       }
@@ -636,89 +740,42 @@ __global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(Tra
       if (lane == 0 && p + 1 < p_end) prefix_advance<R>(sp, P);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double c2 = __shfl_xor_sync(0xffffffffu, best_cost, o);
-    const long long k2 = __shfl_xor_sync(0xffffffffu, best_key, o);
-    feasible += __shfl_xor_sync(0xffffffffu, feasible, o);
-    if (better(c2, k2, best_cost, best_key)) {
-      best_cost = c2;
-      best_key = k2;
-    }
-  }
-  __shared__ Best sb[32];
-  const int wid = threadIdx.x >> 5;
-  if (lane == 0) sb[wid] = Best{best_cost, best_key, feasible};
-  __syncthreads();
-  if (wid == 0) {
-    const int nw = blockDim.x >> 5;
-    Best b = lane < nw ? sb[lane] : Best{kInf * 10, LLONG_MAX, 0};
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double c2 = __shfl_xor_sync(0xffffffffu, b.cost, o);
-      const long long k2 = __shfl_xor_sync(0xffffffffu, b.rank, o);
-      b.feasible += __shfl_xor_sync(0xffffffffu, b.feasible, o);
-      if (better(c2, k2, b.cost, b.rank)) {
-        b.cost = c2;
-        b.rank = k2;
-      }
-    }
-    if (lane == 0) partial[blockIdx.x] = b;
-  }
+  NearMin nm{b0, {k0, k1, k2}, feasible};
+  nm = nm_block_reduce(nm);
+  if (threadIdx.x == 0) partial[blockIdx.x] = nm;
 }
 
-// Reduce CTA partials and decode the winner (prefix, suffix) -> rank + plan.
+// Merge CTA summaries, pick the window's winner and decode it (prefix, suffix) -> rank + plan.
 template <int R>
 __global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb,
                                                    const double2* __restrict__ blkf,
                                                    const BlockRec* __restrict__ blk, int L,
-                                                   int window, const Best* __restrict__ partial,
+                                                   int window, const NearMin* __restrict__ partial,
                                                    int n_partial, TrainOut* __restrict__ out) {
-  Best b{kInf * 10, LLONG_MAX, 0};
-  for (int i = threadIdx.x; i < n_partial; i += blockDim.x) {
-    const Best p = partial[i];
-    b.feasible += p.feasible;
-    if (better(p.cost, p.rank, b.cost, b.rank)) {
-      b.cost = p.cost;
-      b.rank = p.rank;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double c2 = __shfl_xor_sync(0xffffffffu, b.cost, o);
-    const long long k2 = __shfl_xor_sync(0xffffffffu, b.rank, o);
-    b.feasible += __shfl_xor_sync(0xffffffffu, b.feasible, o);
-    if (better(c2, k2, b.cost, b.rank)) {
-      b.cost = c2;
-      b.rank = k2;
-    }
-  }
-  __shared__ Best sb[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) sb[wid] = b;
-  __syncthreads();
+  NearMin m;
+  nm_init(m);
+  for (int i = threadIdx.x; i < n_partial; i += blockDim.x) nm_merge(m, partial[i]);
+  m = nm_block_reduce(m);
   if (threadIdx.x != 0) return;
-  b = sb[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-    b.feasible += sb[w].feasible;
-    if (better(sb[w].cost, sb[w].rank, b.cost, b.rank)) {
-      b.cost = sb[w].cost;
-      b.rank = sb[w].rank;
-    }
-  }
-  out->best = b;
-  out->n_stages = 0;
-  if (b.rank == LLONG_MAX) return;
-  const long long p = b.rank / sp.n_suf, s = b.rank % sp.n_suf;
+  double cost;
+  const long long key = nm_winner(m, window, cost);
+  out->best = Best{cost, key, m.feasible};
+  out->nm_b0 = m.b0;
   Prefix<R> P;
+  for (int i = 0; i < 3; ++i)
+    out->nm_rank[i] = m.key[i] == LLONG_MAX ? LLONG_MAX
+                                            : prefix_decode<R>(sp, m.key[i] / sp.n_suf, P) + m.key[i] % sp.n_suf;
+  out->n_stages = 0;
+  if (key == LLONG_MAX) return;
+  const long long p = key / sp.n_suf, s = key % sp.n_suf;
   const long long base = prefix_decode<R>(sp, p, P);
   out->best.rank = base + s;
   PrefixData<R> D;
   prefix_data<R>(sp, tb, blkf, P, D);
   constexpr int NS = R * kMaxPerRun;
   int lay[NS], bis[NS];
-  double cost;
-  eval_layout<R, true>(sp, tb, blkf, L, window, D, tb.suf[s], cost, lay, bis);
+  double x;
+  eval_layout<R, true>(sp, tb, blkf, L, D, tb.suf[s], x, lay, bis);
   int n = 0;
   for (int q = 0; q < NS; ++q) {
     if (bis[q] < 0) continue;
@@ -913,7 +970,7 @@ T* carve(char*& p, size_t count) {
 
 template <int R>
 int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const double2* blkf,
-                const BlockRec* blk, int window, long long lo, long long hi, Best* partial,
+                const BlockRec* blk, int window, long long lo, long long hi, NearMin* partial,
                 int max_blocks, TrainOut* d_out, cudaStream_t stream) {
   ScanRange rg{};
   rank_split(h, lo, rg.p_lo, rg.s_lo);
@@ -931,7 +988,7 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   long long blocks = (n_items + (threads / 32) - 1) / (threads / 32);
   blocks = std::max(1LL, std::min(blocks, std::min((long long)max_blocks, (long long)ctx->num_sms * occ)));
   if (hi > lo) {
-    k1_layout_scan<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, window, rg, partial);
+    k1_layout_scan<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial);
     ctx->launches++;
   } else {
     blocks = 0;
@@ -975,12 +1032,13 @@ struct PreparedTrain {
   double* d_tx = nullptr;
   double* d_fd = nullptr;
   SufEnt* d_suf = nullptr;
-  Best* d_partial = nullptr;
+  NearMin* d_partial = nullptr;
   TrainOut* d_out = nullptr;
   int max_blocks = 0;
   int L = 0;
   long long lo = 0, hi = 0;
   bool launched = false;
+  long long nm[4] = {kInfBits, LLONG_MAX, LLONG_MAX, LLONG_MAX};  // NearMin of the last collect (ranks)
 };
 
 static PreparedTrain*& prepared(gp_ctx* ctx) {
@@ -1017,7 +1075,7 @@ static size_t table_bytes(const HostSpace& h, int L, int max_blocks) {
   add(sizeof(double) * (h.tx_size + 1));
   add(sizeof(double) * (GP_MAX_STAGES + 1));
   add(sizeof(SufEnt) * (h.choices.size() + 1));
-  add(sizeof(Best) * max_blocks);
+  add(sizeof(NearMin) * max_blocks);
   return bytes;
 }
 
@@ -1048,7 +1106,7 @@ static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_bas
   P.d_tx = carve<double>(tab, h.tx_size + 1);
   P.d_fd = carve<double>(tab, GP_MAX_STAGES + 1);
   P.d_suf = carve<SufEnt>(tab, h.choices.size() + 1);
-  P.d_partial = carve<Best>(tab, P.max_blocks);
+  P.d_partial = carve<NearMin>(tab, P.max_blocks);
 }
 
 static double sum_stages(const HostSpace& h) {
@@ -1127,10 +1185,14 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   return rc;
 }
 
-static void fill_result(const PreparedTrain& P, const TrainOut* ho, gp_train_result* out, int32_t* stage_devices) {
+static void fill_result(PreparedTrain& P, const TrainOut* ho, gp_train_result* out, int32_t* stage_devices) {
   std::memset(out, 0, sizeof *out);
   out->layouts = P.hi - P.lo;
+  P.nm[0] = kInfBits;
+  P.nm[1] = P.nm[2] = P.nm[3] = LLONG_MAX;
   if (!ho) return;
+  P.nm[0] = ho->nm_b0;
+  for (int i = 0; i < 3; ++i) P.nm[1 + i] = ho->nm_rank[i];
   out->feasible = ho->best.feasible;
   if (ho->best.rank != LLONG_MAX) {
     out->found = 1;
@@ -1198,6 +1260,89 @@ int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices) {
   return GP_OK;
 }
 
+void train_last_nm(gp_ctx* ctx, long long nm[4]) {
+  PreparedTrain* PP = prepared(ctx);
+  for (int i = 0; i < 4; ++i) nm[i] = PP ? PP->nm[i] : (i ? LLONG_MAX : kInfBits);
+}
+
+// ---- window-independent memo of constrained_search (see NearMin). A full-range search
+// of a train set is stored with its near-minimum summary and the decoded plan of the rank
+// that won; a later call with another window derives its winner from the summary exactly
+// and is answered from the memo when that winner is the stored plan (always, unless a
+// two-ulp near tie resolves differently under the new window — then it is re-scanned).
+struct TrainMemoEntry {
+  gp_train_result res;
+  std::vector<int32_t> ordered;
+  NearMin nm;  // keys = ranks (rank order == key order)
+};
+struct TrainMemo {
+  std::unordered_map<std::string, TrainMemoEntry> map;
+};
+constexpr size_t kMemoCap = 1 << 16;
+
+// host merge of two NearMin summaries held as {b0, rank0, rank1, rank2}
+void train_nm_merge(long long a[4], const long long b[4]) {
+  NearMin x{a[0], {a[1], a[2], a[3]}, 0}, y{b[0], {b[1], b[2], b[3]}, 0};
+  nm_merge(x, y);
+  a[0] = x.b0;
+  for (int i = 0; i < 3; ++i) a[1 + i] = x.key[i];
+}
+
+void train_memo_free(gp_ctx* ctx) {
+  delete static_cast<TrainMemo*>(ctx->train_memo);
+  ctx->train_memo = nullptr;
+}
+
+std::string train_memo_key(const int32_t* ids, int n, const gp_train_opts* o) {
+  std::vector<int32_t> v(ids, ids + n);
+  std::sort(v.begin(), v.end());  // the search canonicalises the order itself
+  v.push_back(o->max_stages_per_type);
+  v.push_back(o->device_granularity_limit);
+  return std::string(reinterpret_cast<const char*>(v.data()), v.size() * sizeof(int32_t));
+}
+
+void train_memo_put(gp_ctx* ctx, const std::string& key, const gp_train_result& r, const int32_t* ordered,
+                    int n, const long long nm[4]);
+
+// stores a search just collected on ctx (the plan's device order is the prepared set's)
+void train_memo_put_last(gp_ctx* ctx, const std::string& key, const gp_train_result& r, const long long nm[4]) {
+  PreparedTrain* PP = prepared(ctx);
+  if (!PP) return;
+  train_memo_put(ctx, key, r, PP->h.ordered.data(), PP->h.sp.n, nm);
+}
+
+bool train_memo_get(gp_ctx* ctx, const std::string& key, int window, gp_train_result* out,
+                    int32_t* stage_devices) {
+  if (!ctx->memo || !ctx->train_memo) return false;
+  auto& map = static_cast<TrainMemo*>(ctx->train_memo)->map;
+  auto it = map.find(key);
+  if (it == map.end()) return false;
+  const TrainMemoEntry& e = it->second;
+  double cost;
+  const long long rank = nm_winner(e.nm, window, cost);
+  if (rank != (e.res.found ? e.res.rank : LLONG_MAX)) return false;
+  *out = e.res;
+  if (out->found) {
+    out->cost = cost;
+    if (stage_devices) std::memcpy(stage_devices, e.ordered.data(), sizeof(int32_t) * e.ordered.size());
+  }
+  return true;
+}
+
+void train_memo_put(gp_ctx* ctx, const std::string& key, const gp_train_result& r, const int32_t* ordered,
+                    int n, const long long nm[4]) {
+  if (!ctx->memo) return;
+  if (!ctx->train_memo) ctx->train_memo = new TrainMemo();
+  auto& map = static_cast<TrainMemo*>(ctx->train_memo)->map;
+  if (map.size() >= kMemoCap) map.clear();
+  TrainMemoEntry& e = map[key];
+  e.res = r;
+  if (r.found) e.ordered.assign(ordered, ordered + n);
+  e.nm.b0 = nm[0];
+  for (int i = 0; i < 3; ++i) e.nm.key[i] = nm[1 + i];
+  e.nm.feasible = r.feasible;
+}
+
 int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_train_opts* o,
                  long long lo, long long hi, gp_train_result* out, int32_t* stage_devices) {
   std::memset(out, 0, sizeof *out);
@@ -1213,6 +1358,31 @@ int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_tr
 int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
                 const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices) {
   if (n_sets <= 0) return GP_OK;
+  // answered from the memo where possible; the rest is scanned in one batch
+  std::vector<std::string> keys(n_sets);
+  std::vector<int> todo;
+  for (int i = 0; i < n_sets; ++i) {
+    keys[i] = train_memo_key(ids[i], ns[i], o);
+    if (!train_memo_get(ctx, keys[i], window, outs + i, stage_devices ? stage_devices[i] : nullptr))
+      todo.push_back(i);
+  }
+  if (todo.empty()) return GP_OK;
+  if ((int)todo.size() < n_sets) {
+    std::vector<const int32_t*> ids2;
+    std::vector<int32_t> ns2;
+    std::vector<gp_train_result> outs2(todo.size());
+    std::vector<int32_t*> sd2;
+    for (int i : todo) {
+      ids2.push_back(ids[i]);
+      ns2.push_back(ns[i]);
+      sd2.push_back(stage_devices ? stage_devices[i] : nullptr);
+    }
+    int rc = train_batch(ctx, (int)todo.size(), ids2.data(), ns2.data(), window, o, outs2.data(),
+                         stage_devices ? sd2.data() : nullptr);
+    if (rc) return rc;
+    for (size_t j = 0; j < todo.size(); ++j) outs[todo[j]] = outs2[j];
+    return GP_OK;
+  }
   std::vector<PreparedTrain> Ps(n_sets);
   size_t ib = 0, tbytes = 0;
   for (int i = 0; i < n_sets; ++i) {
@@ -1248,6 +1418,7 @@ int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_
   for (int i = 0; i < n_sets; ++i) {
     const bool ran = Ps[i].h.total > 0;
     fill_result(Ps[i], ran ? ho + i : nullptr, outs + i, stage_devices ? stage_devices[i] : nullptr);
+    train_memo_put(ctx, keys[i], outs[i], Ps[i].h.ordered.data(), Ps[i].h.sp.n, Ps[i].nm);
   }
   return GP_OK;
 }

@@ -61,6 +61,7 @@ def lib() -> C.CDLL:
         _lib.gp_train_launch.argtypes = [vp, C.c_int32, C.c_int64, C.c_int64]
         _lib.gp_train_collect.argtypes = [vp, C.POINTER(abi.gp_train_result), abi.i32p]
         _lib.gp_ctx_set_timing.argtypes = [vp, C.c_int]
+        _lib.gp_ctx_set_memo.argtypes = [vp, C.c_int]
         _lib.gp_train_timing.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]
         _lib.gp_ctx_io_bytes.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
                                          C.POINTER(C.c_double)]
@@ -195,6 +196,10 @@ class Engine:
         devs = np.zeros(max(len(self._prep_ids), 1), dtype=np.int32)
         _check(lib().gp_train_collect(self._h, C.byref(res), devs.ctypes.data_as(abi.i32p)))
         return res, devs
+
+    def set_memo(self, on: bool = True):
+        """Enable (default) / disable + drop the window-independent constrained_search memo."""
+        _check(lib().gp_ctx_set_memo(self._h, int(on)))
 
     def set_timing(self, on: bool = True):
         _check(lib().gp_ctx_set_timing(self._h, int(on)))

@@ -127,3 +127,22 @@ def test_multi_gpu_context_fanout():
     r1, d1 = engine("c5_1024gpu").constrained_search_raw(ids, 3, lo=lo, hi=hi)
     r2, d2 = multi.constrained_search_raw(ids, 3, lo=lo, hi=hi)
     assert train_result_dict(r1, d1) == train_result_dict(r2, d2)
+
+
+def test_memo_window_sweep_vs_oracle():
+    """One scan per train set answers every window: repeated searches of the same sets
+    with windows 1..70 (memo hits after the first) == the oracle, and == a memo-less context."""
+    from paper_2511_00796_b200.engine import Engine
+    name = "c3_64gpu"
+    p = problem(name)
+    orc = Oracle(p)
+    memo_less = Engine(p)
+    memo_less.set_memo(False)
+    sets = [s for s in random_train_sets(p.cluster.n, 30, seed=77) if orc.train_space(s) <= 60_000][:8]
+    assert len(sets) >= 4
+    for ids in sets:
+        for window in (3, 1, 2, 6, 7, 12, 24, 33, 48, 64, 70):
+            want = orc.constrained_search(ids, window)
+            assert run(name, ids, window) == want, (ids, window)
+            r, d = memo_less.constrained_search_raw(ids, window)
+            assert train_result_dict(r, d) == want, (ids, window)
