@@ -260,6 +260,7 @@ void gp_ctx_destroy(gp_ctx* ctx) {
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   train_state_free(ctx);
   train_memo_free(ctx);
+  if (ctx->d_slow) cudaFree(ctx->d_slow);
   milp_cache_free(ctx);
   part_cache_free(ctx);
   for (auto& e : ctx->ev)

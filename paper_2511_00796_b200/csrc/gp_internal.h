@@ -12,6 +12,7 @@
 namespace gp {
 
 constexpr double kInf = 1e30;       // inc/common.hpp:41
+constexpr long long kSlowQueue = 1 << 21;  // deferred generic candidates per scan (overflow -> rescan)
 constexpr double kActBytes = 2.0;   // src/cost_model.cpp:10
 constexpr int kMaxPerRun = 4;       // K1 kernel instantiations support <= 4 blocks per type run
 constexpr long long kFanoutMinLayouts = 20000000;  // below this a search stays on one GPU
@@ -73,6 +74,26 @@ struct __align__(16) SufEnt {
   int b1;
 };
 
+// Fast-path view of a suffix choice, valid when the layer-allocation total is the same
+// for every layout of the train set (see k1_layout_scan_fast): the suffix stages'
+// remainders in stable descending order and floor sum, and, per promotion count b (its top
+// b stages get one extra layer) and per number d of zero-layer fix-up donations taken from
+// it, its zero-stage count and its largest layer count (k2f_suffix_fast).
+constexpr int kDonations = 4;  // fix-up donations tabulated (more -> generic fallback)
+struct __align__(16) SufFast {
+  // first 32 bytes: everything a candidate reads unconditionally (two 16-byte loads)
+  int fs;        // sum of the floors
+  int kb1;       // k | b1 << 16
+  int rb01;      // run-local block index of the stages in remainder order (desc,
+  int rb23;      //   stage order among equals), 16 bits each
+  int nzs0123;   // zero-layer stage count at promotion b = 0..3 (one byte each)
+  int nzs4_bad;  // byte 0: zero-layer count at b = 4; bits 8..12: stage would exceed L at b
+  int pad[2];
+  double t[3];   // internal stage-transfer terms (as SufEnt::t)
+  signed char ms[5][kDonations + 1];  // largest layer count after d donations (-1: none)
+};
+static_assert(sizeof(SufFast) == 96, "K1-fast reads SufFast as six 16-byte words");
+
 // Device-side training tables of one train set.
 struct TrainTables {
   const int* ordered;
@@ -84,6 +105,11 @@ struct TrainTables {
   const double* tx;
   const double* fd_coef; // [S] = (double)(S-1) / micro_batches
   const SufEnt* suf;     // [n_suf]
+  // fast path (constant allocation total): per block (remainder, floor) of its layer share,
+  // per suffix SufFast + (max total, max compute) of its stages when the top b get +1
+  const double2* blk_sh;  // [nblk]
+  const SufFast* sufx;    // [n_suf]
+  const double2* suf_st;  // [n_suf * 5 * (kDonations + 1)]
   int pos_off[GP_MAX_TYPES];
 };
 
@@ -143,6 +169,8 @@ struct gp_ctx {
   void* train_state = nullptr;
   void* milp_cache = nullptr;
   void* part_cache[2] = {nullptr, nullptr};  // partition unit tables per granularity (partition.cu)
+  // K1-fast's deferred generic candidates: [0] = count, then keys (train.cu)
+  unsigned long long* d_slow = nullptr;
   // constrained_search results per train set, window-independent (train.cu TrainMemo)
   void* train_memo = nullptr;
   bool memo = true;

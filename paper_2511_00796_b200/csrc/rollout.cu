@@ -17,6 +17,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <cstring>
 #include <functional>
@@ -184,12 +187,15 @@ __global__ void k4_level_scatter(MilpDims d, const long long* __restrict__ off,
   }
 }
 
-// Persistent cooperative kernel: one grid barrier per lattice level. For each state,
-// one pass over the (type, devices) groups: value = max_g best[s - delta_g] + hmax_g;
-// choice = smallest config index c with best[prev_g(c)] + h_c == value.
+// Persistent cooperative kernel, one warp per state, lanes over the (type, devices) groups:
+// value = max_g best[s - delta_g] + hmax_g; choice = smallest config index c with
+// best[prev_g(c)] + h_c == value (src/rollout_milp.cpp:197-225). The lanes' partial
+// (max value, min index) pairs merge exactly in any order. A state at level l reads levels
+// <= l - n_min (n_min = fewest devices of any config), so `step` = n_min consecutive levels
+// form one phase between grid barriers.
 __global__ void __launch_bounds__(256) k4_dp_levels(MilpDims d, const Group* __restrict__ groups_g,
                                                     int n_groups, const int* __restrict__ members_g,
-                                                    const double* __restrict__ h_g, int n_cfg,
+                                                    const double* __restrict__ h_g, int n_cfg, int step,
                                                     const long long* __restrict__ off,
                                                     const unsigned long long* __restrict__ order,
                                                     double* __restrict__ best,
@@ -210,17 +216,18 @@ __global__ void __launch_bounds__(256) k4_dp_levels(MilpDims d, const Group* __r
   }
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nth = (long long)gridDim.x * blockDim.x;
-  for (int l = 0; l < d.levels; ++l) {
-    const long long e = off[l + 1];
-    for (long long i = off[l] + tid; i < e; i += nth) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (int l = 0; l < d.levels; l += step) {
+    const long long e = off[min(l + step, d.levels)];
+    for (long long i = off[l] + warp; i < e; i += n_warps) {
       const unsigned long long pk = order[i];
       long long s = 0;
       for (int t = 0; t < d.T; ++t) s += (long long)((pk >> shift[t]) & mask[t]) * d.stride[t];
       double m = 0.0;  // best[s] starts at 0.0; only a strictly larger candidate replaces it
       int ch = -1;
-      for (int g = 0; g < n_groups; ++g) {
+      for (int g = lane; g < n_groups; g += 32) {
         const Group& G = groups[g];
         if ((int)((pk >> shift[G.type]) & mask[G.type]) < G.n) continue;
         const double bp = best[s - G.delta];
@@ -241,8 +248,20 @@ __global__ void __launch_bounds__(256) k4_dp_levels(MilpDims d, const Group* __r
           ch = c;
         }
       }
-      best[s] = m;
-      choice[s] = ch;
+      // (m, ch): ch == -1 exactly when m == 0, so the lexicographic merge is exact
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const int c2 = __shfl_xor_sync(0xffffffffu, ch, o);
+        if (m2 > m || (m2 == m && c2 < ch)) {
+          m = m2;
+          ch = c2;
+        }
+      }
+      if (lane == 0) {
+        best[s] = m;
+        choice[s] = ch;
+      }
     }
     grid.sync();
   }
@@ -541,6 +560,26 @@ struct MilpCache {
   long long clock = 0;
 };
 
+// GPLAN_PROFILE=1: lattice tables built / reused, states tabulated, DP and backtrack wall time
+struct MilpStats {
+  long long built = 0, reused = 0, states = 0, backtracks = 0, queries = 0, mallocs = 0;
+  double dp_s = 0, bt_s = 0, malloc_s = 0, prep_s = 0, kern_s = 0;
+  long long levels = 0, groups = 0;
+  ~MilpStats() {
+    if (std::getenv("GPLAN_PROFILE"))
+      std::fprintf(stderr,
+                   "milp: %lld tables built (%lld states, %lld mallocs, %.3f s), %lld reused, %lld backtrack "
+                   "launches for %lld queries (%.3f s); malloc %.3f s, level sort %.3f s, dp kernel %.3f s, "
+                   "%lld levels, %lld groups\n",
+                   built, states, mallocs, dp_s, reused, backtracks, queries, bt_s, malloc_s, prep_s, kern_s,
+                   levels, groups);
+  }
+} g_milp_stats;
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void milp_cache_free(gp_ctx* ctx) {
   delete static_cast<MilpCache*>(ctx->milp_cache);
   ctx->milp_cache = nullptr;
@@ -605,9 +644,11 @@ static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, con
     if (covers) {
       t->last_use = ++mc.clock;
       *out = t.get();
+      g_milp_stats.reused++;
       return GP_OK;
     }
   }
+  const double t_start = now_s();
   std::vector<std::pair<long long, int>> key;
   int rc = milp_groups(cfg, nc, dims, key);
   if (rc) return rc;
@@ -627,13 +668,14 @@ static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, con
   }
   MilpTable* tab = same;
   if (!tab) {
-    if (mc.tables.size() >= 4) {  // evict the least recently used
+    if (mc.tables.size() >= 4) {  // recycle the least recently used table (and its buffer)
       auto lru = std::min_element(mc.tables.begin(), mc.tables.end(),
                                   [](const auto& a, const auto& b) { return a->last_use < b->last_use; });
-      mc.tables.erase(lru);
+      tab = lru->get();
+    } else {
+      mc.tables.push_back(std::make_unique<MilpTable>());
+      tab = mc.tables.back().get();
     }
-    mc.tables.push_back(std::make_unique<MilpTable>());
-    tab = mc.tables.back().get();
     tab->sig = sig;
   }
   MilpDims d{};
@@ -656,17 +698,23 @@ static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, con
   }
   const int ng = (int)groups.size();
   if (ng > kMaxGroups) return set_error(GP_INVALID, "too many config groups for the sm_100a kernel");
+  int step = INT_MAX;
+  for (const Group& G : groups) step = std::min(step, G.n);
   std::vector<double> hs(nc);
   for (int c = 0; c < nc; ++c) hs[c] = cfg[c].throughput;
   const size_t best_bytes = ((size_t)d.states * sizeof(double) + 255) & ~size_t(255);
   const size_t tbytes = best_bytes + (size_t)d.states * sizeof(int) + 256;
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (tbytes > tab->bytes) {
+  if (tbytes > tab->bytes) {  // grow-only, with headroom: tables of one run vary in size
     if (tab->buf) cudaFree(tab->buf);
     tab->buf = nullptr;
     tab->bytes = 0;
-    GP_CUDA(cudaMalloc(&tab->buf, tbytes));
-    tab->bytes = tbytes;
+    const double t0 = now_s();
+    const size_t want = std::max(tbytes + tbytes / 2, (size_t)1 << 20);
+    GP_CUDA(cudaMalloc(&tab->buf, want));
+    tab->bytes = want;
+    g_milp_stats.mallocs++;
+    g_milp_stats.malloc_s += now_s() - t0;
   }
   tab->best = static_cast<double*>(tab->buf);
   tab->choice = reinterpret_cast<int*>(static_cast<char*>(tab->buf) + best_bytes);
@@ -700,32 +748,44 @@ static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, con
   std::memcpy(hp + ((char*)d_h - (char*)d_groups), hs.data(), sizeof(double) * nc);
   GP_CUDA(cudaMemcpyAsync(d_groups, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h2d_bytes += (long long)in_bytes;
+  const double t_prep = now_s();
   GP_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int) * d.levels, ctx->stream));
   const int sweep_blocks = (int)std::min<long long>((d.states + 255) / 256, (long long)ctx->num_sms * 16);
   k4_level_hist<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_hist);
   k4_level_scan<<<1, 32, 0, ctx->stream>>>(d_hist, d.levels, d_off, d_cursor, d_maxw);
   k4_level_scatter<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_off, d_cursor, d_order);
   ctx->launches += 3;
-  int* h_maxw = reinterpret_cast<int*>(hp);
-  GP_CUDA(cudaMemcpyAsync(h_maxw, d_maxw, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double t_kern = now_s();
+  g_milp_stats.prep_s += t_kern - t_prep;
+  g_milp_stats.levels += d.levels;
+  g_milp_stats.groups += ng;
   static int occ = 0;
   if (!occ) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_dp_levels, 256, 0);
     occ = std::max(1, occ);
   }
-  // grid: enough blocks for the widest level, at most what is co-resident
-  int dp_blocks = (int)std::min<long long>((long long)ctx->num_sms * occ, ((long long)*h_maxw + 255) / 256);
+  // grid: about one warp per state of an average phase (2x for the wider middle levels),
+  // at most what is co-resident
+  const long long phases = (d.levels + step - 1) / step;
+  const long long warps = 2 * ((d.states + phases - 1) / phases);
+  int dp_blocks = (int)std::min<long long>((long long)ctx->num_sms * occ, (warps + 7) / 8);
   dp_blocks = std::max(1, dp_blocks);
   int ng_arg = ng, nc_arg = nc;
   double* best = tab->best;
   int* choice = tab->choice;
-  void* args[] = {&d, &d_groups, &ng_arg, &d_members, &d_h, &nc_arg, &d_off, &d_order, &best, &choice};
+  void* args[] = {&d, &d_groups, &ng_arg, &d_members, &d_h, &nc_arg, &step, &d_off, &d_order, &best, &choice};
   GP_CUDA(cudaLaunchCooperativeKernel((void*)k4_dp_levels, dp_blocks, 256, args, 0, ctx->stream));
   ctx->launches++;
   tab->d = d;
   tab->last_use = ++mc.clock;
   *out = tab;
+  g_milp_stats.built++;
+  g_milp_stats.states += d.states;
+  if (std::getenv("GPLAN_PROFILE")) {
+    cudaStreamSynchronize(ctx->stream);
+    g_milp_stats.dp_s += now_s() - t_start;
+    g_milp_stats.kern_s += now_s() - t_kern;
+  }
   return GP_OK;
 }
 
@@ -733,6 +793,9 @@ static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, con
 static int backtrack_many(gp_ctx* ctx, MilpTable* tab, const gp_config* cfg, int nc, int q,
                           const int* const* caps, const double* Bs, double len, gp_rollout_result* outs,
                           gp_rollout_entry* const* entries) {
+  const double t_start = now_s();
+  g_milp_stats.backtracks++;
+  g_milp_stats.queries += q;
   std::vector<long long> full(q);
   std::vector<double> Bv(Bs, Bs + q);
   for (int i = 0; i < q; ++i) {
@@ -789,6 +852,7 @@ static int backtrack_many(gp_ctx* ctx, MilpTable* tab, const gp_config* cfg, int
       std::memcpy(entries[i], he + (size_t)nc * i, sizeof(gp_rollout_entry) * ho[i].n_entries);
     }
   }
+  g_milp_stats.bt_s += now_s() - t_start;
   return GP_OK;
 }
 

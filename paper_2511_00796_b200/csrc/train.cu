@@ -22,6 +22,9 @@
 // is compiled with --fmad=false, so results are bit-identical to the CPU.
 #include <algorithm>
 #include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -36,7 +39,7 @@ struct TrainOut {
   long long nm_b0;       // near-minimum summary of the scanned range (NearMin), keys decoded to ranks
   long long nm_rank[3];
   int n_stages;
-  int pad;
+  int overflow;  // K1-fast's deferred queue overflowed: the host rescans with the generic K1
   int first[GP_MAX_STAGES];
   int count[GP_MAX_STAGES];
   int tp[GP_MAX_STAGES];
@@ -647,6 +650,263 @@ __device__ __forceinline__ bool eval_layout(const TrainSpace& sp, const TrainTab
 }
 
 
+// ------------------------------------------- fast path: constant allocation total
+// When every partial sum of the train set's device FLOPS is exact (all FLOPS are integer
+// multiples of one power of two and their total stays below 2^53 of it — true for the
+// spec-sheet FLOPS of every benchmark cluster, SURVEY.md 8a rule 2), allocate_layers'
+// total is the same for every layout, so each block's share L*f/total, its floor and its
+// remainder are per-block constants (K2e). A layout's layer counts then follow from the
+// floors and from which stages the remainder ranking promotes by one, and both sides of
+// a layout (prefix stages, suffix stages) can tabulate their stage maxima per promotion
+// count (prefix: per warp, suffix: K2f). K1-fast merges the two sides with a rank count.
+__global__ void k2e_block_shares(const double2* __restrict__ blkf, int nblk, double total,
+                                 double2* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nblk) return;
+  const double y = 1.0 / total;
+  const double share = div_rn_recip(blkf[i].y, total, y);  // as eval_layout
+  const int fl = static_cast<int>(share);
+  out[i] = make_double2(share - fl, (double)fl);
+}
+
+// Per suffix choice: the fast-path tables (SufFast) and, per promotion count b and
+// donation count d, the (max total, max compute) of its stages — zero-layer stages counted
+// with the one layer the fix-up gives them, donors with the layers they keep.
+__global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const double2* __restrict__ blk_sh,
+                                const double2* __restrict__ stage, int L, int blk_off_last,
+                                SufFast* __restrict__ out, double2* __restrict__ st_out) {
+  constexpr int DM = kDonations;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const SufEnt e = suf[i];
+  const int k = e.k;
+  double rem[4];
+  int fl[4], rk[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    rem[j] = -1.0;
+    fl[j] = 0;
+    if (j < k) {
+      const double2 sh = blk_sh[e.bi[j]];
+      rem[j] = sh.x;
+      fl[j] = (int)sh.y;
+    }
+  }
+  int fs = 0;
+  int rbs[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    rk[j] = 0;
+#pragma unroll
+    for (int j2 = 0; j2 < 4; ++j2)
+      if (j2 < k && j2 != j) rk[j] += rem[j2] > rem[j] || (rem[j2] == rem[j] && j2 < j);
+    fs += fl[j];
+  }
+  for (int j = 0; j < k; ++j) rbs[rk[j]] = e.bi[j] - blk_off_last;
+  SufFast f;
+  f.fs = fs;
+  f.kb1 = k | (e.b1 << 16);
+  f.rb01 = rbs[0] | (rbs[1] << 16);
+  f.rb23 = rbs[2] | (rbs[3] << 16);
+  f.pad[0] = f.pad[1] = 0;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) f.t[j] = e.t[j];
+  unsigned nzs = 0, nz4 = 0, bad = 0;
+  for (int b = 0; b <= 4; ++b) {
+    int lay[4];
+    int nz = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      lay[j] = 0;
+      if (j < k) {
+        lay[j] = fl[j] + (rk[j] < b ? 1 : 0);
+        nz += lay[j] == 0;
+        if (lay[j] > L) bad |= 1u << b;
+      }
+    }
+    if (b < 4) nzs |= (unsigned)nz << (8 * b);
+    else nz4 = (unsigned)nz;
+    bool live = true;
+    for (int d = 0; d <= DM; ++d) {
+      int mx = -1, jm = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < k && lay[j] > 0 && lay[j] > mx) {
+          mx = lay[j];
+          jm = j;
+        }
+      double mt = 0, mc = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= k) continue;
+        const int l1 = lay[j] == 0 ? 1 : lay[j];
+        if (l1 < 1 || l1 > L) continue;
+        const double2 st = stage[(unsigned)(e.bi[j] * L + (l1 - 1))];
+        if (st.x > mt) mt = st.x;
+        if (st.y > mc) mc = st.y;
+      }
+      f.ms[b][d] = (signed char)(live ? (mx > 127 ? 127 : mx) : -1);
+      st_out[((size_t)i * 5 + b) * (DM + 1) + d] = make_double2(mt, mc);
+      if (mx < 2) live = false;  // a donor needs >= 2 layers (checked by the scan)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (live && j == jm) lay[j]--;
+    }
+  }
+  f.nzs0123 = (int)nzs;
+  f.nzs4_bad = (int)(nz4 | (bad << 8));
+  out[i] = f;
+}
+
+constexpr int kMaxLastBlocks = 1280;  // last type run blocks tabulated per prefix (else count_ge)
+
+// Warp-uniform fast-path data of one prefix (shared memory).
+template <int R>
+struct PrefixFast {
+  static constexpr int NP = (R - 1) * kMaxPerRun;
+  static constexpr int NPP = NP < 4 ? 4 : (NP < 8 ? 8 : 16);  // > NP, power of two
+  static constexpr int NQ = NP > 0 ? NP : 1;
+  static constexpr int DM = kDonations;
+  double srt[NPP];            // prefix remainders sorted (desc, stage order), padded with -1
+  double2 pt[NP + 1][DM + 1]; // (max total, max compute) of the prefix stages: top a promoted, d donations
+  double2 tc[NQ][DM + 3];     // stage q's (total, compute) at fl+1-o layers (o <= DM+1), o = DM+2: 1 layer
+  double rem[NQ];
+  int fl[NQ];
+  int rk[NQ];
+  short mp[NP + 1][DM + 1];   // largest layer count after d donations (-1: none / invalid)
+  unsigned char nzp[NP + 1];  // zero-layer prefix stages at promotion a
+  int fp;                     // sum of the prefix floors
+  int bad;                    // bit a: a promoted prefix stage would exceed L layers
+  unsigned char cntb[kMaxLastBlocks];  // per last-run block: prefix remainders >= its remainder
+};
+
+// number of entries >= x in the descending, -1-padded srt (x >= 0)
+template <int R>
+__device__ __forceinline__ int count_ge(const double* srt, double x) {
+  constexpr int NPP = PrefixFast<R>::NPP;
+  int pos = 0;
+#pragma unroll
+  for (int step = NPP / 2; step >= 1; step >>= 1)
+    if (srt[pos + step - 1] >= x) pos += step;
+  return pos;
+}
+
+// All lanes: remainder ranks, floor sum, stage-time cache and the (promotion, donation)
+// tables of the warp's prefix.
+template <int R>
+__device__ __forceinline__ void prefix_fast(int lane, const TrainTables& tb, int L, int sp_nc_last,
+                                            int blk_off_last, const PrefixData<R>& D, PrefixFast<R>& F) {
+  constexpr int NP = PrefixData<R>::NP;
+  constexpr int NPP = PrefixFast<R>::NPP;
+  constexpr int DM = kDonations;
+  if (NP == 0) {
+    if (lane <= DM) {
+      F.pt[0][lane] = make_double2(0.0, 0.0);
+      F.mp[0][lane] = -1;
+    }
+    if (lane == 0) {
+      F.fp = 0;
+      F.bad = 0;
+      F.nzp[0] = 0;
+    }
+    __syncwarp();
+    return;
+  }
+  bool aq = false;
+  double rq = -1.0;
+  int fq = 0;
+  if (lane < NP) {
+    aq = D.act[lane];
+    if (aq) {
+      const double2 sh = tb.blk_sh[D.bi[lane]];
+      rq = sh.x;
+      fq = (int)sh.y;
+    }
+    F.rem[lane] = rq;
+    F.fl[lane] = fq;
+  }
+  if (lane < NPP) F.srt[lane] = -1.0;
+  if (lane == 0) F.bad = 0;
+  __syncwarp();
+  if (lane < NP && aq) {
+    int rk = 0;
+#pragma unroll
+    for (int q2 = 0; q2 < NP; ++q2) {
+      const double r2 = F.rem[q2];
+      rk += (D.act[q2] && (r2 > rq || (r2 == rq && q2 < lane))) ? 1 : 0;
+    }
+    F.rk[lane] = rk;
+    F.srt[rk] = rq;
+  }
+  const int fp = __reduce_add_sync(0xffffffffu, fq);
+  // stage-time cache: every layer count a prefix stage can end with
+  for (int idx = lane; idx < NP * (DM + 3); idx += 32) {
+    const int q = idx / (DM + 3), o = idx % (DM + 3);
+    if (!D.act[q]) continue;
+    const int lay = o == DM + 2 ? 1 : F.fl[q] + 1 - o;
+    double2 v = make_double2(kInf, kInf);
+    if (lay >= 1 && lay <= L) v = tb.stage[(unsigned)(D.bi[q] * L + (lay - 1))];
+    F.tc[q][o] = v;
+  }
+  __syncwarp();
+  const int kp = D.u;
+  for (int idx = lane; idx < (kp + 1) * (DM + 1); idx += 32) {
+    const int a = idx / (DM + 1), d = idx % (DM + 1);
+    int lay[PrefixFast<R>::NQ];
+    int nz = 0;
+    bool over = false;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      lay[q] = 0;
+      if (D.act[q]) {
+        lay[q] = F.fl[q] + (F.rk[q] < a ? 1 : 0);
+        nz += lay[q] == 0;
+        over |= lay[q] > L;
+      }
+    }
+    int mx = -1;
+    for (int step = 0; step <= d; ++step) {  // water-filling: d donations from the first maximum
+      int qm = 0;
+      mx = -1;
+#pragma unroll
+      for (int q = 0; q < NP; ++q)
+        if (D.act[q] && lay[q] > 0 && lay[q] > mx) {
+          mx = lay[q];
+          qm = q;
+        }
+      if (step == d) break;
+      if (mx < 2) {
+        mx = -1;
+        break;
+      }
+#pragma unroll
+      for (int q = 0; q < NP; ++q)
+        if (q == qm) lay[q]--;
+    }
+    double mt = 0, mc = 0;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      if (!D.act[q]) continue;
+      const int o = lay[q] == 0 ? DM + 2 : F.fl[q] + 1 - lay[q];
+      const double2 v = F.tc[q][o < 0 ? 0 : (o > DM + 2 ? DM + 2 : o)];
+      if (v.x > mt) mt = v.x;
+      if (v.y > mc) mc = v.y;
+    }
+    F.pt[a][d] = make_double2(mt, mc);
+    F.mp[a][d] = (short)mx;
+    if (d == 0) {
+      F.nzp[a] = (unsigned char)nz;
+      if (over) atomicOr(&F.bad, 1 << a);
+    }
+  }
+  if (lane == 0) F.fp = fp;
+  // rank count of every last-run block's remainder among the prefix remainders
+  const int nlast = (sp_nc_last + 2) * (sp_nc_last + 1) / 2;
+  if (nlast <= kMaxLastBlocks)
+    for (int i = lane; i < nlast; i += 32) F.cntb[i] = (unsigned char)count_ge<R>(F.srt, tb.blk_sh[blk_off_last + i].x);
+  __syncwarp();
+}
+
 struct ScanRange {
   long long p_lo, s_lo, p_hi, s_hi;  // candidates (p, s) with (p_lo,s_lo) <= (p,s) < (p_hi,s_hi)
   long long n_pref;                  // prefixes touched
@@ -654,6 +914,7 @@ struct ScanRange {
 };
 
 constexpr int kK1Threads = 128;
+constexpr int kDeferBlocks = 64;  // CTAs of k1_deferred (their partials follow K1-fast's)
 
 __device__ __forceinline__ NearMin nm_shfl_xor(const NearMin& m, int o) {
   NearMin r;
@@ -745,13 +1006,172 @@ __global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(Tra
   if (threadIdx.x == 0) partial[blockIdx.x] = nm;
 }
 
+// candidates scored by K1-fast's tables / by the deferred generic kernel (GPLAN_PROFILE report)
+__device__ unsigned long long g_k1_fast_cnt[2];
+
+// K1-fast (constant allocation total). Per candidate: the suffix's remainder ranks among
+// the prefix's (cntb) fix how many prefix (a) and suffix (b) stages the round-robin
+// promotes; zero-layer fix-ups are merged from the two sides' donation tables; the stage
+// maxima are then two table reads. Layouts outside the tabulated cases (extra layers
+// outside [0, S), more than kDonations fix-ups, a donor left without layers) are queued
+// for k1_deferred, which scores them with the generic eval_layout — so every candidate's
+// per-step time is the one the reference computes.
+template <int R>
+__global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace sp, TrainTables tb,
+                                                      const double2* __restrict__ blkf, int L,
+                                                      ScanRange rg, NearMin* __restrict__ partial,
+                                                      unsigned long long* __restrict__ slow_q) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
+  const long long n_suf = sp.n_suf;
+  long long b0 = kInfBits, k0 = LLONG_MAX, k1 = LLONG_MAX, k2 = LLONG_MAX, feasible = 0;
+  unsigned n_tab = 0;
+  __shared__ Prefix<R> sP[kK1Threads / 32];
+  __shared__ PrefixData<R> sD[kK1Threads / 32];
+  __shared__ PrefixFast<R> sF[kK1Threads / 32];
+  Prefix<R>& P = sP[threadIdx.x >> 5];
+  PrefixData<R>& D = sD[threadIdx.x >> 5];
+  PrefixFast<R>& F = sF[threadIdx.x >> 5];
+  const int e2 = sp.nc[R - 1] + 2;
+  const int4* __restrict__ sufx = reinterpret_cast<const int4*>(tb.sufx);
+  for (long long it = warp; it < n_items; it += n_warps) {
+    long long p = rg.p_lo + it * rg.chunk;
+    const long long p_end = min(p + rg.chunk, rg.p_lo + rg.n_pref);
+    __syncwarp();
+    if (lane == 0) prefix_decode<R>(sp, p, P);
+    for (; p < p_end; ++p) {
+      __syncwarp();
+      if (lane == 0) prefix_data<R>(sp, tb, blkf, P, D);
+      __syncwarp();
+      prefix_fast<R>(lane, tb, L, sp.nc[R - 1], sp.blk_off[R - 1], D, F);
+      const int kp = D.u;
+      const int fp = F.fp, pbad = F.bad;
+      const double dtr = D.transfers;
+      const double* __restrict__ txrow = tb.tx + (R > 1 ? sp.tx_off[R > 1 ? R - 2 : 0] + (size_t)D.a_last * e2 : 0);
+      const long long ns = sp.cnt[R - 1][kp];
+      const long long s0 = p == rg.p_lo ? rg.s_lo : 0;
+      const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
+      for (long long s = s0 + lane; s < s1; s += 32) {
+        const int4 A = __ldg(sufx + 6 * s);      // fs, k|b1, rb01, rb23
+        const int4 B = __ldg(sufx + 6 * s + 1);  // nzs0123, nzs4|bad
+        const int fk = A.y & 0xffff;
+        const int S = kp + fk;
+        const int extra = L - (fp + A.x);
+        bool slow = (unsigned)extra >= (unsigned)S;
+        int a = 0, b = 0, dP = 0, dS = 0;
+        if (!slow) {
+          if (R > 1) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int rb = ((j < 2 ? A.z : A.w) >> (16 * (j & 1))) & 0xffff;
+              if (j < fk) b += (j + F.cntb[rb] < extra) ? 1 : 0;
+            }
+          } else {
+            b = extra;
+          }
+          a = extra - b;
+          slow = ((pbad >> a) | (B.y >> (8 + b))) & 1;
+          const unsigned long long nzs = ((unsigned long long)(unsigned)B.y << 32) | (unsigned)B.x;
+          const int nz = F.nzp[a] + (int)((nzs >> (8 * b)) & 0xff);
+          if (nz > kDonations) slow = true;
+          // zero-layer fix-up: each donation comes from the side holding the first maximum
+          // (the prefix on ties: its stages come first); a donor must keep >= 1 layer
+          for (int i = 0; i < nz && !slow; ++i) {
+            const int mpv = F.mp[a][dP], msv = tb.sufx[s].ms[b][dS];
+            if ((mpv > msv ? mpv : msv) < 2) slow = true;
+            if (mpv >= msv) ++dP;
+            else ++dS;
+          }
+        }
+        const long long key = p * n_suf + s;
+        if (slow) {
+          const unsigned long long at = atomicAdd(slow_q, 1ULL);
+          if (at < (unsigned long long)kSlowQueue) slow_q[1 + at] = (unsigned long long)key;
+          continue;
+        }
+        ++n_tab;
+        const double2 pa = F.pt[a][dP];
+        const double2 sb = tb.suf_st[(s * 5 + b) * (kDonations + 1) + dS];
+        double mt = pa.x, mc = pa.y;
+        if (sb.x > mt) mt = sb.x;
+        if (sb.y > mc) mc = sb.y;
+        if (!(mt < __longlong_as_double(0x7ff0000000000000LL))) continue;  // memory-infeasible
+        const double* __restrict__ t = tb.sufx[s].t;
+        double tr = dtr;
+        if (R > 1) tr += txrow[(A.y >> 16) & 0xffff];
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          if (j + 1 < fk) tr += t[j];
+        const double x = mt + tb.fd_coef[S] * mc + tr;
+        ++feasible;
+        const long long d = __double_as_longlong(x) - b0;
+        if (d < 3) {
+          if (d < 0) {
+            k2 = d == -1 ? k1 : d == -2 ? k0 : LLONG_MAX;
+            k1 = d == -1 ? k0 : LLONG_MAX;
+            k0 = key;
+            b0 += d;
+          } else if (d == 1) {
+            k1 = min(k1, key);
+          } else if (d == 2) {
+            k2 = min(k2, key);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && p + 1 < p_end) prefix_advance<R>(sp, P);
+    }
+  }
+  n_tab = __reduce_add_sync(0xffffffffu, n_tab);
+  if (lane == 0) atomicAdd(&g_k1_fast_cnt[0], (unsigned long long)n_tab);
+  NearMin nm{b0, {k0, k1, k2}, feasible};
+  nm = nm_block_reduce(nm);
+  if (threadIdx.x == 0) partial[blockIdx.x] = nm;
+}
+
+// The candidates K1-fast deferred, scored by the generic eval_layout (rare; keys arrive
+// in any order, so the summary merges them with nm_merge).
+template <int R>
+__global__ void __launch_bounds__(kK1Threads) k1_deferred(TrainSpace sp, TrainTables tb,
+                                                         const double2* __restrict__ blkf, int L,
+                                                         const unsigned long long* __restrict__ slow_q,
+                                                         NearMin* __restrict__ partial) {
+  const unsigned long long cnt = slow_q[0];
+  const long long n = (long long)min(cnt, (unsigned long long)kSlowQueue);
+  NearMin m;
+  nm_init(m);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long key = (long long)slow_q[1 + i];
+    const long long p = key / sp.n_suf, s = key % sp.n_suf;
+    Prefix<R> P;
+    prefix_decode<R>(sp, p, P);
+    PrefixData<R> D;
+    prefix_data<R>(sp, tb, blkf, P, D);
+    double x;
+    if (eval_layout<R, false>(sp, tb, blkf, L, D, tb.suf[s], x, nullptr, nullptr)) {
+      NearMin o;
+      o.b0 = __double_as_longlong(x);
+      o.key[0] = key;
+      o.key[1] = o.key[2] = LLONG_MAX;
+      o.feasible = 1;
+      nm_merge(m, o);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_k1_fast_cnt[1], (unsigned long long)n);
+  m = nm_block_reduce(m);
+  if (threadIdx.x == 0) partial[blockIdx.x] = m;
+}
+
 // Merge CTA summaries, pick the window's winner and decode it (prefix, suffix) -> rank + plan.
 template <int R>
 __global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb,
                                                    const double2* __restrict__ blkf,
                                                    const BlockRec* __restrict__ blk, int L,
                                                    int window, const NearMin* __restrict__ partial,
-                                                   int n_partial, TrainOut* __restrict__ out) {
+                                                   int n_partial, TrainOut* __restrict__ out,
+                                                   const unsigned long long* __restrict__ slow_q) {
   NearMin m;
   nm_init(m);
   for (int i = threadIdx.x; i < n_partial; i += blockDim.x) nm_merge(m, partial[i]);
@@ -760,6 +1180,7 @@ __global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb
   double cost;
   const long long key = nm_winner(m, window, cost);
   out->best = Best{cost, key, m.feasible};
+  out->overflow = slow_q && slow_q[0] > (unsigned long long)kSlowQueue;  // -> generic rescan
   out->nm_b0 = m.b0;
   Prefix<R> P;
   for (int i = 0; i < 3; ++i)
@@ -808,7 +1229,37 @@ struct HostSpace {
   int nblk = 0, tin_size = 0, tx_size = 0;
   long long total = 0;
   long long n_prefix = 0;
+  bool exact_total = false;  // every partial FLOPS sum exact: K1-fast applies
+  double flops_total = 0;    // allocate_layers' total (the same for every layout when exact)
 };
+
+// True when every partial sum of these devices' FLOPS is exactly representable: all are
+// integer multiples of 2^e (e = the smallest trailing exponent) and sum / 2^e < 2^53.
+static bool exact_flops_total(const gp_ctx* ctx, const std::vector<int>& ids, double* total) {
+  int e_min = INT_MAX;
+  for (int id : ids) {
+    const double f = ctx->h_flops[id];
+    if (!(f >= 0) || !std::isfinite(f)) return false;
+    if (f == 0) continue;
+    int ex;
+    const double m = std::frexp(f, &ex);  // f = m * 2^ex, m in [0.5, 1)
+    const unsigned long long mi = (unsigned long long)std::ldexp(m, 53);
+    e_min = std::min(e_min, ex - 53 + __builtin_ctzll(mi));
+  }
+  double t = 0;
+  if (e_min != INT_MAX) {
+    unsigned long long units = 0;
+    for (int id : ids) {
+      const double q = std::ldexp(ctx->h_flops[id], -e_min);  // exact integer
+      if (q >= 9007199254740992.0) return false;
+      units += (unsigned long long)q;
+      if (units >= (1ULL << 53)) return false;
+    }
+  }
+  for (int id : ids) t += ctx->h_flops[id];
+  *total = t;
+  return true;
+}
 
 int build_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, HostSpace& h) {
   if (n <= 0) return set_error(GP_INVALID, "constrained_search requires a non-empty train set");
@@ -875,6 +1326,7 @@ int build_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, 
       if (r + 1 < sp.R) sp.cntP[r][u] = accP;
     }
   }
+  h.exact_total = exact_flops_total(ctx, h.ordered, &h.flops_total);
   const bool any = sp.max_stages >= sp.R;
   h.total = any ? sp.cnt[0][0] : 0;
   h.n_prefix = any ? sp.cntP[0][0] : 0;
@@ -971,15 +1423,17 @@ T* carve(char*& p, size_t count) {
 template <int R>
 int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const double2* blkf,
                 const BlockRec* blk, int window, long long lo, long long hi, NearMin* partial,
-                int max_blocks, TrainOut* d_out, cudaStream_t stream) {
+                int max_blocks, TrainOut* d_out, cudaStream_t stream, bool fast) {
   ScanRange rg{};
   rank_split(h, lo, rg.p_lo, rg.s_lo);
   rank_split(h, hi, rg.p_hi, rg.s_hi);
   rg.n_pref = rg.p_hi - rg.p_lo + (rg.s_hi > 0 ? 1 : 0);
   const int threads = kK1Threads;
-  static int occ = 0;
+  static int occ_g = 0, occ_f = 0;
+  int& occ = fast ? occ_f : occ_g;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_layout_scan<R>, threads, 0);
+    if (fast) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_layout_scan_fast<R>, threads, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_layout_scan<R>, threads, 0);
     occ = std::max(1, occ);
   }
   const long long warps_total = (long long)ctx->num_sms * occ * (threads / 32);
@@ -987,13 +1441,25 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
   long long blocks = (n_items + (threads / 32) - 1) / (threads / 32);
   blocks = std::max(1LL, std::min(blocks, std::min((long long)max_blocks, (long long)ctx->num_sms * occ)));
+  int n_partial = (int)blocks;
   if (hi > lo) {
-    k1_layout_scan<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial);
-    ctx->launches++;
+    if (fast) {
+      GP_CUDA(cudaMemsetAsync(ctx->d_slow, 0, sizeof(unsigned long long), stream));
+      k1_layout_scan_fast<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial,
+                                                                  ctx->d_slow);
+      k1_deferred<R><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, ctx->d_slow,
+                                                            partial + blocks);
+      n_partial += kDeferBlocks;
+      ctx->launches += 2;
+    } else {
+      k1_layout_scan<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial);
+      ctx->launches++;
+    }
   } else {
-    blocks = 0;
+    n_partial = 0;
   }
-  k1_finalize<R><<<1, 256, 0, stream>>>(h.sp, tb, blkf, blk, ctx->sc.L, window, partial, (int)blocks, d_out);
+  k1_finalize<R><<<1, 256, 0, stream>>>(h.sp, tb, blkf, blk, ctx->sc.L, window, partial, n_partial, d_out,
+                                        fast && hi > lo ? ctx->d_slow : nullptr);
   ctx->launches++;
   GP_CUDA(cudaGetLastError());
   return GP_OK;
@@ -1032,14 +1498,39 @@ struct PreparedTrain {
   double* d_tx = nullptr;
   double* d_fd = nullptr;
   SufEnt* d_suf = nullptr;
+  double2* d_blk_sh = nullptr;
+  SufFast* d_sufx = nullptr;
+  double2* d_suf_st = nullptr;
   NearMin* d_partial = nullptr;
   TrainOut* d_out = nullptr;
   int max_blocks = 0;
   int L = 0;
   long long lo = 0, hi = 0;
+  int window = 0;
   bool launched = false;
   long long nm[4] = {kInfBits, LLONG_MAX, LLONG_MAX, LLONG_MAX};  // NearMin of the last collect (ranks)
 };
+
+// GPLAN_PROFILE=1: memo hits / scanned sets / scanned layouts (stderr at exit)
+struct MemoStats {
+  long long hits = 0, scans = 0, layouts = 0;
+  unsigned long long fast_cnt[2] = {0, 0};
+  void poll() {  // after a synchronisation
+    if (!std::getenv("GPLAN_PROFILE")) return;
+    unsigned long long c[2] = {0, 0};
+    cudaMemcpyFromSymbol(c, g_k1_fast_cnt, sizeof c);
+    fast_cnt[0] = c[0];
+    fast_cnt[1] = c[1];
+  }
+  ~MemoStats() {
+    if (std::getenv("GPLAN_PROFILE"))
+      std::fprintf(stderr, "k1 fast: %llu candidates from tables, %llu by the generic fallback\n", fast_cnt[0],
+                   fast_cnt[1]);
+    if (std::getenv("GPLAN_PROFILE"))
+      std::fprintf(stderr, "train memo: %lld hits, %lld scanned sets, %lld scanned layouts\n", hits, scans,
+                   layouts);
+  }
+} g_memo_stats;
 
 static PreparedTrain*& prepared(gp_ctx* ctx) {
   return reinterpret_cast<PreparedTrain*&>(ctx->train_state);
@@ -1075,7 +1566,10 @@ static size_t table_bytes(const HostSpace& h, int L, int max_blocks) {
   add(sizeof(double) * (h.tx_size + 1));
   add(sizeof(double) * (GP_MAX_STAGES + 1));
   add(sizeof(SufEnt) * (h.choices.size() + 1));
-  add(sizeof(NearMin) * max_blocks);
+  add(sizeof(double2) * h.nblk);
+  add(sizeof(SufFast) * (h.choices.size() + 1));
+  add(sizeof(double2) * 5 * (kDonations + 1) * (h.choices.size() + 1));
+  add(sizeof(NearMin) * (max_blocks + kDeferBlocks));
   return bytes;
 }
 
@@ -1106,7 +1600,10 @@ static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_bas
   P.d_tx = carve<double>(tab, h.tx_size + 1);
   P.d_fd = carve<double>(tab, GP_MAX_STAGES + 1);
   P.d_suf = carve<SufEnt>(tab, h.choices.size() + 1);
-  P.d_partial = carve<NearMin>(tab, P.max_blocks);
+  P.d_blk_sh = carve<double2>(tab, h.nblk);
+  P.d_sufx = carve<SufFast>(tab, h.choices.size() + 1);
+  P.d_suf_st = carve<double2>(tab, 5 * (kDonations + 1) * (h.choices.size() + 1));
+  P.d_partial = carve<NearMin>(tab, P.max_blocks + kDeferBlocks);
 }
 
 static double sum_stages(const HostSpace& h) {
@@ -1127,13 +1624,14 @@ static double sum_stages(const HostSpace& h) {
 
 // Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
 static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long lo, long long hi,
-                           cudaStream_t stream, bool timing) {
+                           cudaStream_t stream, bool timing, bool force_generic = false) {
   const HostSpace& h = P.h;
   if (lo < 0) lo = 0;
   if (hi < 0 || hi > h.total) hi = h.total;
   if (lo > hi) lo = hi;
   P.lo = lo;
   P.hi = hi;
+  P.window = window;
   P.launched = true;
   if (h.total == 0 || lo == hi) return GP_OK;  // std::nullopt
   const int L = ctx->sc.L;
@@ -1147,7 +1645,17 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   tb.tx = P.d_tx;
   tb.fd_coef = P.d_fd;
   tb.suf = P.d_suf;
+  tb.blk_sh = P.d_blk_sh;
+  tb.sufx = P.d_sufx;
+  tb.suf_st = P.d_suf_st;
   for (int r = 0; r < h.sp.R; ++r) tb.pos_off[r] = h.pos_off[r];
+  const char* generic_env = std::getenv("GPLAN_K1_GENERIC");
+  // (layer counts are tabulated as signed bytes: L <= 127)
+  const int nlast = (h.sp.nc[h.sp.R - 1] + 2) * (h.sp.nc[h.sp.R - 1] + 1) / 2;
+  const bool fast = h.exact_total && ctx->sc.L <= 127 && nlast <= kMaxLastBlocks && !force_generic &&
+                    !(generic_env && generic_env[0] == '1');
+  if (fast && !ctx->d_slow)
+    GP_CUDA(cudaMalloc(&ctx->d_slow, sizeof(unsigned long long) * (1 + kSlowQueue)));
   if (timing) GP_CUDA(cudaEventRecord(ctx->ev[0], stream));
   // ---- K2: per-train-set tables
   k2a_block_stats<<<h.nblk, 256, 0, stream>>>(P.d_ordered, P.d_meta, P.d_pos, tb, P.d_blk, ctx->d_type,
@@ -1170,16 +1678,22 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
     const int ns = (int)h.choices.size();
     k2d_suffix_table<<<(ns + 255) / 256, 256, 0, stream>>>(P.d_choices, ns, h.sp, P.d_tin, P.d_suf);
     ctx->launches += 3;
+    if (fast) {
+      k2e_block_shares<<<(h.nblk + 255) / 256, 256, 0, stream>>>(P.d_blkf, h.nblk, h.flops_total, P.d_blk_sh);
+      k2f_suffix_fast<<<(ns + 127) / 128, 128, 0, stream>>>(P.d_suf, ns, P.d_blk_sh, P.d_stage, L,
+                                                           h.sp.blk_off[h.sp.R - 1], P.d_sufx, P.d_suf_st);
+      ctx->launches += 2;
+    }
   }
   GP_CUDA(cudaGetLastError());
   if (timing) GP_CUDA(cudaEventRecord(ctx->ev[1], stream));
   // ---- K1: layout scan over [lo, hi)
   const int R = h.sp.R;
   int rc;
-  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream);
-  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream);
-  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream);
-  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream);
+  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast);
+  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast);
+  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast);
+  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast);
   else rc = set_error(GP_INVALID, "train sets spanning more than 4 gpu types are not supported");
   if (!rc && timing) GP_CUDA(cudaEventRecord(ctx->ev[2], stream));
   return rc;
@@ -1256,7 +1770,14 @@ int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices) {
   GP_CUDA(cudaMemcpyAsync(ho, P.d_out, sizeof(TrainOut), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->d2h_bytes += (long long)sizeof(TrainOut);
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ho->overflow) {  // too many deferred candidates: rescan the range with the generic K1
+    int rc = launch_prepared(ctx, P, P.window, P.lo, P.hi, ctx->stream, false, true);
+    if (rc) return rc;
+    GP_CUDA(cudaMemcpyAsync(ho, P.d_out, sizeof(TrainOut), cudaMemcpyDeviceToHost, ctx->stream));
+    GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   fill_result(P, ho, out, stage_devices);
+  g_memo_stats.poll();
   return GP_OK;
 }
 
@@ -1279,6 +1800,7 @@ struct TrainMemo {
   std::unordered_map<std::string, TrainMemoEntry> map;
 };
 constexpr size_t kMemoCap = 1 << 16;
+
 
 // host merge of two NearMin summaries held as {b0, rank0, rank1, rank2}
 void train_nm_merge(long long a[4], const long long b[4]) {
@@ -1322,6 +1844,7 @@ bool train_memo_get(gp_ctx* ctx, const std::string& key, int window, gp_train_re
   const long long rank = nm_winner(e.nm, window, cost);
   if (rank != (e.res.found ? e.res.rank : LLONG_MAX)) return false;
   *out = e.res;
+  g_memo_stats.hits++;
   if (out->found) {
     out->cost = cost;
     if (stage_devices) std::memcpy(stage_devices, e.ordered.data(), sizeof(int32_t) * e.ordered.size());
@@ -1416,10 +1939,21 @@ int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_
   ctx->d2h_bytes += (long long)out_bytes;
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
   for (int i = 0; i < n_sets; ++i) {
+    if (Ps[i].h.total > 0 && ho[i].overflow) {  // rescan with the generic K1
+      int rc = launch_prepared(ctx, Ps[i], window, 0, -1, ctx->stream, false, true);
+      if (rc) return rc;
+      GP_CUDA(cudaMemcpyAsync(ho + i, d_out + i, sizeof(TrainOut), cudaMemcpyDeviceToHost, ctx->stream));
+      GP_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  for (int i = 0; i < n_sets; ++i) {
     const bool ran = Ps[i].h.total > 0;
     fill_result(Ps[i], ran ? ho + i : nullptr, outs + i, stage_devices ? stage_devices[i] : nullptr);
     train_memo_put(ctx, keys[i], outs[i], Ps[i].h.ordered.data(), Ps[i].h.sp.n, Ps[i].nm);
+    g_memo_stats.scans++;
+    g_memo_stats.layouts += Ps[i].h.total;
   }
+  g_memo_stats.poll();
   return GP_OK;
 }
 

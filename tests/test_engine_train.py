@@ -146,3 +146,42 @@ def test_memo_window_sweep_vs_oracle():
             assert run(name, ids, window) == want, (ids, window)
             r, d = memo_less.constrained_search_raw(ids, window)
             assert train_result_dict(r, d) == want, (ids, window)
+
+
+def test_generic_scan_fractional_flops():
+    """Fractional FLOPS (the reference's random_instance style, tests/test_fixtures.cpp:108):
+    allocate_layers' total then depends on the layout's grouping, K1-fast does not apply,
+    and the generic scan must still equal the oracle."""
+    import json
+
+    from common import read
+    from paper_2511_00796_b200 import load_problem
+    from paper_2511_00796_b200.engine import Engine
+    doc = json.loads(read("clusters", "c3_64gpu"))
+    for i, t in enumerate(doc["gpu_types"]):
+        t["flops_tflops"] = t["flops_tflops"] * (1.0 + 0.0123456789 * (i + 1)) + 0.1
+    p = load_problem(json.dumps(doc), read("workloads", "c3_64gpu"), read("calibration", "c3_64gpu"))
+    orc = Oracle(p)
+    eng = Engine(p)
+    sets = [s for s in random_train_sets(p.cluster.n, 40, seed=4242) if orc.train_space(s) <= 100_000][:12]
+    assert len(sets) >= 6
+    for ids in sets:
+        for window in (1, 2, 33):
+            res, devs = eng.constrained_search_raw(ids, window)
+            assert train_result_dict(res, devs) == orc.constrained_search(ids, window), (ids, window)
+
+
+def test_fast_scan_equals_generic_scan(monkeypatch):
+    """K1-fast vs the generic K1 (GPLAN_K1_GENERIC=1) on large ranges: same winner, cost and
+    feasible count (every candidate is scored, by the tables or by the generic fallback)."""
+    for name, span in (("c4_256gpu", None), ("c5_1024gpu", 30_000_000)):
+        p = problem(name)
+        eng = engine(name)
+        ids = list(range(1, p.cluster.n))
+        total = eng.train_space(ids)
+        lo, hi = (0, total) if span is None else (total // 3, total // 3 + span)
+        fast = run(name, ids, 3, lo=lo, hi=hi)
+        monkeypatch.setenv("GPLAN_K1_GENERIC", "1")
+        generic = run(name, ids, 3, lo=lo, hi=hi)
+        monkeypatch.delenv("GPLAN_K1_GENERIC")
+        assert fast == generic, name
