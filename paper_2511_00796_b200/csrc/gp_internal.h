@@ -80,19 +80,7 @@ struct __align__(16) SufEnt {
 // b stages get one extra layer) and per number d of zero-layer fix-up donations taken from
 // it, its zero-stage count and its largest layer count (k2f_suffix_fast).
 constexpr int kDonations = 4;  // fix-up donations tabulated (more -> generic fallback)
-struct __align__(16) SufFast {
-  // first 32 bytes: everything a candidate reads unconditionally (two 16-byte loads)
-  int fs;        // sum of the floors
-  int kb1;       // k | b1 << 16
-  int rb01;      // run-local block index of the stages in remainder order (desc,
-  int rb23;      //   stage order among equals), 16 bits each
-  int nzs0123;   // zero-layer stage count at promotion b = 0..3 (one byte each)
-  int nzs4_bad;  // byte 0: zero-layer count at b = 4; bits 8..12: stage would exceed L at b
-  int pad[2];
-  double t[3];   // internal stage-transfer terms (as SufEnt::t)
-  signed char ms[5][kDonations + 1];  // largest layer count after d donations (-1: none)
-};
-static_assert(sizeof(SufFast) == 96, "K1-fast reads SufFast as six 16-byte words");
+constexpr int kMsStride = 32;  // bytes per suffix choice in TrainTables::sf_ms
 
 // Device-side training tables of one train set.
 struct TrainTables {
@@ -105,11 +93,17 @@ struct TrainTables {
   const double* tx;
   const double* fd_coef; // [S] = (double)(S-1) / micro_batches
   const SufEnt* suf;     // [n_suf]
-  // fast path (constant allocation total): per block (remainder, floor) of its layer share,
-  // per suffix SufFast + (max total, max compute) of its stages when the top b get +1
-  const double2* blk_sh;  // [nblk]
-  const SufFast* sufx;    // [n_suf]
-  const double2* suf_st;  // [n_suf * 5 * (kDonations + 1)]
+  // fast path (constant allocation total), structure-of-arrays over the suffix choices so
+  // that a warp's 32 consecutive choices are read with coalesced loads (k2f_suffix_fast):
+  const double2* blk_sh;  // [nblk] per block (remainder, floor) of its layer share
+  const int4* sf_hot;     // [n_suf] floor sum, k | b1 << 16, run-local block ids of the stages in
+                          //   remainder order (desc, stage order among equals), 16 bits each
+  const int2* sf_zb;      // [n_suf] zero-layer stage count at promotion b = 0..3 (bytes),
+                          //   b = 4 (byte 0) | stage-would-exceed-L mask << 8
+  const double* sf_t;     // [3][n_suf] internal stage-transfer terms
+  const signed char* sf_ms;  // [n_suf][kMsStride]: largest layer count at (b, d donations), -1: none
+  const double2* sf_st;   // [5 * (kDonations + 1)][n_suf]: (max total, max compute) at (b, d)
+  const int* nzs_max;     // most zero-layer stages of any suffix choice
   int pos_off[GP_MAX_TYPES];
 };
 

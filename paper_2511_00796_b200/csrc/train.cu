@@ -669,12 +669,14 @@ __global__ void k2e_block_shares(const double2* __restrict__ blkf, int nblk, dou
   out[i] = make_double2(share - fl, (double)fl);
 }
 
-// Per suffix choice: the fast-path tables (SufFast) and, per promotion count b and
+// Per suffix choice: the fast-path tables (TrainTables::sf_*) and, per promotion count b and
 // donation count d, the (max total, max compute) of its stages — zero-layer stages counted
 // with the one layer the fix-up gives them, donors with the layers they keep.
 __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const double2* __restrict__ blk_sh,
                                 const double2* __restrict__ stage, int L, int blk_off_last,
-                                SufFast* __restrict__ out, double2* __restrict__ st_out) {
+                                int4* __restrict__ sf_hot, int2* __restrict__ sf_zb, double* __restrict__ sf_t,
+                                signed char* __restrict__ sf_ms, double2* __restrict__ sf_st,
+                                int* __restrict__ nzs_max) {
   constexpr int DM = kDonations;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -703,14 +705,9 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
     fs += fl[j];
   }
   for (int j = 0; j < k; ++j) rbs[rk[j]] = e.bi[j] - blk_off_last;
-  SufFast f;
-  f.fs = fs;
-  f.kb1 = k | (e.b1 << 16);
-  f.rb01 = rbs[0] | (rbs[1] << 16);
-  f.rb23 = rbs[2] | (rbs[3] << 16);
-  f.pad[0] = f.pad[1] = 0;
+  sf_hot[i] = make_int4(fs, k | (e.b1 << 16), rbs[0] | (rbs[1] << 16), rbs[2] | (rbs[3] << 16));
 #pragma unroll
-  for (int j = 0; j < 3; ++j) f.t[j] = e.t[j];
+  for (int j = 0; j < 3; ++j) sf_t[(size_t)j * n + i] = e.t[j];
   unsigned nzs = 0, nz4 = 0, bad = 0;
   for (int b = 0; b <= 4; ++b) {
     int lay[4];
@@ -745,20 +742,23 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
         if (st.x > mt) mt = st.x;
         if (st.y > mc) mc = st.y;
       }
-      f.ms[b][d] = (signed char)(live ? (mx > 127 ? 127 : mx) : -1);
-      st_out[((size_t)i * 5 + b) * (DM + 1) + d] = make_double2(mt, mc);
+      sf_ms[(size_t)i * kMsStride + b * (DM + 1) + d] = (signed char)(live ? (mx > 127 ? 127 : mx) : -1);
+      sf_st[(size_t)(b * (DM + 1) + d) * n + i] = make_double2(mt, mc);
       if (mx < 2) live = false;  // a donor needs >= 2 layers (checked by the scan)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (live && j == jm) lay[j]--;
     }
   }
-  f.nzs0123 = (int)nzs;
-  f.nzs4_bad = (int)(nz4 | (bad << 8));
-  out[i] = f;
+  sf_zb[i] = make_int2((int)nzs, (int)(nz4 | (bad << 8)));
+  int zmax = (int)nz4;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) zmax = max(zmax, (int)((nzs >> (8 * b)) & 0xff));
+  atomicMax(nzs_max, zmax);
 }
 
-constexpr int kMaxLastBlocks = 1280;  // last type run blocks tabulated per prefix (else count_ge)
+constexpr int kK1Threads = 128;
+constexpr int kMaxLastBlocks = 1024;  // last type run blocks with a per-prefix rank count (else generic K1)
 
 // Warp-uniform fast-path data of one prefix (shared memory).
 template <int R>
@@ -773,11 +773,19 @@ struct PrefixFast {
   double rem[NQ];
   int fl[NQ];
   int rk[NQ];
+  double term[NQ];            // per prefix slot: its stage-transfer term (0 if none)
   short mp[NP + 1][DM + 1];   // largest layer count after d donations (-1: none / invalid)
   unsigned char nzp[NP + 1];  // zero-layer prefix stages at promotion a
   int fp;                     // sum of the prefix floors
   int bad;                    // bit a: a promoted prefix stage would exceed L layers
-  unsigned char cntb[kMaxLastBlocks];  // per last-run block: prefix remainders >= its remainder
+};
+
+// K1-fast shared memory per warp beside PrefixFast: the rank count of every last-run
+// block's remainder among the prefix's (cntb) and the prefix's junction-transfer row (txs).
+constexpr int kMaxJunction = 64;  // nc_last + 2 (else generic K1)
+struct PrefixLast {
+  unsigned char cntb[kMaxLastBlocks];
+  double txs[kMaxJunction];
 };
 
 // number of entries >= x in the descending, -1-padded srt (x >= 0)
@@ -791,11 +799,46 @@ __device__ __forceinline__ int count_ge(const double* srt, double x) {
   return pos;
 }
 
+// All lanes: the K1-fast subset of prefix_data (slot activity, block ids, the junction
+// position) computed one slot per lane; the transfer terms go to F.term and are folded
+// in stage order by prefix_fast (adding the 0 terms of the other slots is exact).
+template <int R>
+__device__ __forceinline__ void prefix_data_warp(int lane, const TrainSpace& sp, const TrainTables& tb,
+                                                 const Prefix<R>& P, PrefixData<R>& D, PrefixFast<R>& F) {
+  constexpr int NP = PrefixData<R>::NP;
+  if (lane < NP) {
+    const int r = lane / kMaxPerRun, j = lane % kMaxPerRun;
+    const bool act = j < P.k[r];
+    int bi = 0;
+    double t = 0.0;
+    if (act) {
+      bi = sp.blk_off[r] + blk_index(sp.nc[r], P.b[r][j], P.b[r][j + 1]);
+      if (j + 1 < P.k[r]) {
+        const int e = sp.nc[r] + 2;
+        t = tb.tin[sp.tin_off[r] + ((size_t)P.b[r][j] * e + P.b[r][j + 1]) * e +
+                   P.b[r][j + 2 <= kMaxPerRun ? j + 2 : kMaxPerRun]];
+      } else if (r + 2 < R) {
+        const int e2 = sp.nc[r + 1] + 2;
+        t = tb.tx[sp.tx_off[r] + (size_t)P.b[r][j] * e2 + P.b[r + 2 < R ? r + 1 : r][1]];
+      } else {
+        D.a_last = P.b[r][j];
+      }
+    }
+    D.act[lane] = act;
+    D.bi[lane] = bi;
+    F.term[lane] = t;
+  }
+  if (lane == 0) D.u = P.u;
+  __syncwarp();
+}
+
 // All lanes: remainder ranks, floor sum, stage-time cache and the (promotion, donation)
 // tables of the warp's prefix.
 template <int R>
-__device__ __forceinline__ void prefix_fast(int lane, const TrainTables& tb, int L, int sp_nc_last,
-                                            int blk_off_last, const PrefixData<R>& D, PrefixFast<R>& F) {
+__device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, const TrainTables& tb, int L,
+                                            int nzs_max, PrefixData<R>& D, PrefixFast<R>& F,
+                                            unsigned char* cntb, double* txs) {
+  const int sp_nc_last = sp.nc[R - 1], blk_off_last = sp.blk_off[R - 1];
   constexpr int NP = PrefixData<R>::NP;
   constexpr int NPP = PrefixFast<R>::NPP;
   constexpr int DM = kDonations;
@@ -808,6 +851,8 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainTables& tb, int
       F.fp = 0;
       F.bad = 0;
       F.nzp[0] = 0;
+      D.transfers = 0.0;
+      D.a_last = 0;
     }
     __syncwarp();
     return;
@@ -838,7 +883,6 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainTables& tb, int
     F.rk[lane] = rk;
     F.srt[rk] = rq;
   }
-  const int fp = __reduce_add_sync(0xffffffffu, fq);
   // stage-time cache: every layer count a prefix stage can end with
   for (int idx = lane; idx < NP * (DM + 3); idx += 32) {
     const int q = idx / (DM + 3), o = idx % (DM + 3);
@@ -849,9 +893,12 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainTables& tb, int
     F.tc[q][o] = v;
   }
   __syncwarp();
+  // per promotion count a (one lane each): the layer counts, then up to dm water-filling
+  // donations (dm = the most fix-ups a candidate of this prefix can need), recording the
+  // stage maxima and the largest layer count of every state
   const int kp = D.u;
-  for (int idx = lane; idx < (kp + 1) * (DM + 1); idx += 32) {
-    const int a = idx / (DM + 1), d = idx % (DM + 1);
+  if (lane <= kp) {
+    const int a = lane;
     int lay[PrefixFast<R>::NQ];
     int nz = 0;
     bool over = false;
@@ -864,46 +911,51 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainTables& tb, int
         over |= lay[q] > L;
       }
     }
-    int mx = -1;
-    for (int step = 0; step <= d; ++step) {  // water-filling: d donations from the first maximum
-      int qm = 0;
-      mx = -1;
+    const int dm = min(DM, nz + nzs_max);
+    bool live = true;
+    for (int d = 0; d <= dm; ++d) {
+      int mx = -1, qm = 0;
+      double mt = 0, mc = 0;
 #pragma unroll
-      for (int q = 0; q < NP; ++q)
-        if (D.act[q] && lay[q] > 0 && lay[q] > mx) {
+      for (int q = 0; q < NP; ++q) {
+        if (!D.act[q]) continue;
+        if (lay[q] > 0 && lay[q] > mx) {
           mx = lay[q];
           qm = q;
         }
-      if (step == d) break;
-      if (mx < 2) {
-        mx = -1;
-        break;
+        const int o = lay[q] == 0 ? DM + 2 : F.fl[q] + 1 - lay[q];
+        const double2 v = F.tc[q][o < 0 ? 0 : (o > DM + 2 ? DM + 2 : o)];
+        if (v.x > mt) mt = v.x;
+        if (v.y > mc) mc = v.y;
       }
+      F.pt[a][d] = make_double2(mt, mc);
+      F.mp[a][d] = (short)(live ? mx : -1);
+      if (mx < 2) live = false;  // a donor needs >= 2 layers (checked by the scan)
 #pragma unroll
       for (int q = 0; q < NP; ++q)
-        if (q == qm) lay[q]--;
+        if (live && q == qm) lay[q]--;
     }
-    double mt = 0, mc = 0;
+    F.nzp[a] = (unsigned char)nz;
+    if (over) atomicOr(&F.bad, 1 << a);
+  }
+  if (lane == 0) {
+    int fp = 0;
+    double tr = 0.0;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      if (!D.act[q]) continue;
-      const int o = lay[q] == 0 ? DM + 2 : F.fl[q] + 1 - lay[q];
-      const double2 v = F.tc[q][o < 0 ? 0 : (o > DM + 2 ? DM + 2 : o)];
-      if (v.x > mt) mt = v.x;
-      if (v.y > mc) mc = v.y;
+      fp += F.fl[q];  // inactive slots hold 0
+      tr += F.term[q];
     }
-    F.pt[a][d] = make_double2(mt, mc);
-    F.mp[a][d] = (short)mx;
-    if (d == 0) {
-      F.nzp[a] = (unsigned char)nz;
-      if (over) atomicOr(&F.bad, 1 << a);
-    }
+    F.fp = fp;
+    D.transfers = tr;
   }
-  if (lane == 0) F.fp = fp;
-  // rank count of every last-run block's remainder among the prefix remainders
-  const int nlast = (sp_nc_last + 2) * (sp_nc_last + 1) / 2;
-  if (nlast <= kMaxLastBlocks)
-    for (int i = lane; i < nlast; i += 32) F.cntb[i] = (unsigned char)count_ge<R>(F.srt, tb.blk_sh[blk_off_last + i].x);
+  // rank count of every last-run block's remainder among the prefix remainders, and the
+  // junction-transfer row of the prefix's last block
+  const int e2 = sp_nc_last + 2;
+  const int nlast = e2 * (sp_nc_last + 1) / 2;
+  for (int i = lane; i < nlast; i += 32) cntb[i] = (unsigned char)count_ge<R>(F.srt, tb.blk_sh[blk_off_last + i].x);
+  const double* __restrict__ txrow = tb.tx + sp.tx_off[R > 1 ? R - 2 : 0] + (size_t)D.a_last * e2;
+  for (int i = lane; i < e2; i += 32) txs[i] = txrow[i];
   __syncwarp();
 }
 
@@ -913,7 +965,6 @@ struct ScanRange {
   long long chunk;                   // prefixes per warp work item
 };
 
-constexpr int kK1Threads = 128;
 constexpr int kDeferBlocks = 64;  // CTAs of k1_deferred (their partials follow K1-fast's)
 
 __device__ __forceinline__ NearMin nm_shfl_xor(const NearMin& m, int o) {
@@ -1035,7 +1086,13 @@ __global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace 
   PrefixData<R>& D = sD[threadIdx.x >> 5];
   PrefixFast<R>& F = sF[threadIdx.x >> 5];
   const int e2 = sp.nc[R - 1] + 2;
-  const int4* __restrict__ sufx = reinterpret_cast<const int4*>(tb.sufx);
+  const int nzs_max = *tb.nzs_max;
+  __shared__ PrefixLast sL[kK1Threads / 32];
+  __shared__ double fd[GP_MAX_STAGES + 1];
+  unsigned char* const cntb = sL[threadIdx.x >> 5].cntb;
+  double* const txs = sL[threadIdx.x >> 5].txs;
+  for (int i = threadIdx.x; i <= GP_MAX_STAGES; i += blockDim.x) fd[i] = tb.fd_coef[i];
+  __syncthreads();
   for (long long it = warp; it < n_items; it += n_warps) {
     long long p = rg.p_lo + it * rg.chunk;
     const long long p_end = min(p + rg.chunk, rg.p_lo + rg.n_pref);
@@ -1043,30 +1100,28 @@ __global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace 
     if (lane == 0) prefix_decode<R>(sp, p, P);
     for (; p < p_end; ++p) {
       __syncwarp();
-      if (lane == 0) prefix_data<R>(sp, tb, blkf, P, D);
-      __syncwarp();
-      prefix_fast<R>(lane, tb, L, sp.nc[R - 1], sp.blk_off[R - 1], D, F);
+      prefix_data_warp<R>(lane, sp, tb, P, D, F);
+      prefix_fast<R>(lane, sp, tb, L, nzs_max, D, F, cntb, txs);
       const int kp = D.u;
       const int fp = F.fp, pbad = F.bad;
       const double dtr = D.transfers;
-      const double* __restrict__ txrow = tb.tx + (R > 1 ? sp.tx_off[R > 1 ? R - 2 : 0] + (size_t)D.a_last * e2 : 0);
       const long long ns = sp.cnt[R - 1][kp];
       const long long s0 = p == rg.p_lo ? rg.s_lo : 0;
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
       for (long long s = s0 + lane; s < s1; s += 32) {
-        const int4 A = __ldg(sufx + 6 * s);      // fs, k|b1, rb01, rb23
-        const int4 B = __ldg(sufx + 6 * s + 1);  // nzs0123, nzs4|bad
+        const int4 A = __ldg(tb.sf_hot + s);  // fs, k|b1, rb01, rb23
+        const int2 B = __ldg(tb.sf_zb + s);   // nzs0123, nzs4|bad
         const int fk = A.y & 0xffff;
         const int S = kp + fk;
         const int extra = L - (fp + A.x);
         bool slow = (unsigned)extra >= (unsigned)S;
         int a = 0, b = 0, dP = 0, dS = 0;
         if (!slow) {
-          if (R > 1) {
+          if (R > 1) {  // branch-free: unused stage slots hold block 0 and are masked
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int rb = ((j < 2 ? A.z : A.w) >> (16 * (j & 1))) & 0xffff;
-              if (j < fk) b += (j + F.cntb[rb] < extra) ? 1 : 0;
+              b += ((j < fk) & (j + cntb[rb] < extra)) ? 1 : 0;
             }
           } else {
             b = extra;
@@ -1079,7 +1134,7 @@ __global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace 
           // zero-layer fix-up: each donation comes from the side holding the first maximum
           // (the prefix on ties: its stages come first); a donor must keep >= 1 layer
           for (int i = 0; i < nz && !slow; ++i) {
-            const int mpv = F.mp[a][dP], msv = tb.sufx[s].ms[b][dS];
+            const int mpv = F.mp[a][dP], msv = tb.sf_ms[s * kMsStride + b * (kDonations + 1) + dS];
             if ((mpv > msv ? mpv : msv) < 2) slow = true;
             if (mpv >= msv) ++dP;
             else ++dS;
@@ -1093,18 +1148,17 @@ __global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace 
         }
         ++n_tab;
         const double2 pa = F.pt[a][dP];
-        const double2 sb = tb.suf_st[(s * 5 + b) * (kDonations + 1) + dS];
+        const double2 sb = tb.sf_st[(b * (kDonations + 1) + dS) * n_suf + s];
         double mt = pa.x, mc = pa.y;
         if (sb.x > mt) mt = sb.x;
         if (sb.y > mc) mc = sb.y;
         if (!(mt < __longlong_as_double(0x7ff0000000000000LL))) continue;  // memory-infeasible
-        const double* __restrict__ t = tb.sufx[s].t;
         double tr = dtr;
-        if (R > 1) tr += txrow[(A.y >> 16) & 0xffff];
+        if (R > 1) tr += txs[(A.y >> 16) & 0xffff];
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-          if (j + 1 < fk) tr += t[j];
-        const double x = mt + tb.fd_coef[S] * mc + tr;
+          if (j + 1 < fk) tr += tb.sf_t[j * n_suf + s];
+        const double x = mt + fd[S] * mc + tr;
         ++feasible;
         const long long d = __double_as_longlong(x) - b0;
         if (d < 3) {
@@ -1499,8 +1553,12 @@ struct PreparedTrain {
   double* d_fd = nullptr;
   SufEnt* d_suf = nullptr;
   double2* d_blk_sh = nullptr;
-  SufFast* d_sufx = nullptr;
-  double2* d_suf_st = nullptr;
+  int4* d_sf_hot = nullptr;
+  int2* d_sf_zb = nullptr;
+  double* d_sf_t = nullptr;
+  signed char* d_sf_ms = nullptr;
+  double2* d_sf_st = nullptr;
+  int* d_nzs_max = nullptr;
   NearMin* d_partial = nullptr;
   TrainOut* d_out = nullptr;
   int max_blocks = 0;
@@ -1567,8 +1625,13 @@ static size_t table_bytes(const HostSpace& h, int L, int max_blocks) {
   add(sizeof(double) * (GP_MAX_STAGES + 1));
   add(sizeof(SufEnt) * (h.choices.size() + 1));
   add(sizeof(double2) * h.nblk);
-  add(sizeof(SufFast) * (h.choices.size() + 1));
-  add(sizeof(double2) * 5 * (kDonations + 1) * (h.choices.size() + 1));
+  const size_t nsf = h.choices.size() + 1;
+  add(sizeof(int4) * nsf);
+  add(sizeof(int2) * nsf);
+  add(sizeof(double) * 3 * nsf);
+  add((size_t)kMsStride * nsf);
+  add(sizeof(double2) * 5 * (kDonations + 1) * nsf);
+  add(sizeof(int));
   add(sizeof(NearMin) * (max_blocks + kDeferBlocks));
   return bytes;
 }
@@ -1601,8 +1664,13 @@ static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_bas
   P.d_fd = carve<double>(tab, GP_MAX_STAGES + 1);
   P.d_suf = carve<SufEnt>(tab, h.choices.size() + 1);
   P.d_blk_sh = carve<double2>(tab, h.nblk);
-  P.d_sufx = carve<SufFast>(tab, h.choices.size() + 1);
-  P.d_suf_st = carve<double2>(tab, 5 * (kDonations + 1) * (h.choices.size() + 1));
+  const size_t nsf = h.choices.size() + 1;
+  P.d_sf_hot = carve<int4>(tab, nsf);
+  P.d_sf_zb = carve<int2>(tab, nsf);
+  P.d_sf_t = carve<double>(tab, 3 * nsf);
+  P.d_sf_ms = carve<signed char>(tab, (size_t)kMsStride * nsf);
+  P.d_sf_st = carve<double2>(tab, 5 * (kDonations + 1) * nsf);
+  P.d_nzs_max = carve<int>(tab, 1);
   P.d_partial = carve<NearMin>(tab, P.max_blocks + kDeferBlocks);
 }
 
@@ -1646,13 +1714,18 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   tb.fd_coef = P.d_fd;
   tb.suf = P.d_suf;
   tb.blk_sh = P.d_blk_sh;
-  tb.sufx = P.d_sufx;
-  tb.suf_st = P.d_suf_st;
+  tb.sf_hot = P.d_sf_hot;
+  tb.sf_zb = P.d_sf_zb;
+  tb.sf_t = P.d_sf_t;
+  tb.sf_ms = P.d_sf_ms;
+  tb.sf_st = P.d_sf_st;
+  tb.nzs_max = P.d_nzs_max;
   for (int r = 0; r < h.sp.R; ++r) tb.pos_off[r] = h.pos_off[r];
   const char* generic_env = std::getenv("GPLAN_K1_GENERIC");
   // (layer counts are tabulated as signed bytes: L <= 127)
   const int nlast = (h.sp.nc[h.sp.R - 1] + 2) * (h.sp.nc[h.sp.R - 1] + 1) / 2;
-  const bool fast = h.exact_total && ctx->sc.L <= 127 && nlast <= kMaxLastBlocks && !force_generic &&
+  const bool fast = h.exact_total && ctx->sc.L <= 127 && nlast <= kMaxLastBlocks &&
+                    h.sp.nc[h.sp.R - 1] + 2 <= kMaxJunction && !force_generic &&
                     !(generic_env && generic_env[0] == '1');
   if (fast && !ctx->d_slow)
     GP_CUDA(cudaMalloc(&ctx->d_slow, sizeof(unsigned long long) * (1 + kSlowQueue)));
@@ -1680,8 +1753,10 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
     ctx->launches += 3;
     if (fast) {
       k2e_block_shares<<<(h.nblk + 255) / 256, 256, 0, stream>>>(P.d_blkf, h.nblk, h.flops_total, P.d_blk_sh);
+      GP_CUDA(cudaMemsetAsync(P.d_nzs_max, 0, sizeof(int), stream));
       k2f_suffix_fast<<<(ns + 127) / 128, 128, 0, stream>>>(P.d_suf, ns, P.d_blk_sh, P.d_stage, L,
-                                                           h.sp.blk_off[h.sp.R - 1], P.d_sufx, P.d_suf_st);
+                                                           h.sp.blk_off[h.sp.R - 1], P.d_sf_hot, P.d_sf_zb,
+                                                           P.d_sf_t, P.d_sf_ms, P.d_sf_st, P.d_nzs_max);
       ctx->launches += 2;
     }
   }
