@@ -41,8 +41,8 @@ WINDOW = 3
 METRIC = "candidate plans evaluated/sec"
 # from the committed ncu capture of K1-fast on this workload (profiles/r01/)
 K1_PROFILE = "profiles/r01/k1_layout_scan_fast_ncu_summary.txt"
-K1_WARP_INST_PER_CAND = 8.38    # smsp__inst_executed.sum / candidates
-K1_DRAM_BYTES_PER_LAUNCH = 964864  # dram__bytes_read.sum + dram__bytes_write.sum
+K1_WARP_INST_PER_CAND = 8.481   # smsp__inst_executed.sum / candidates (20,489,721,977 / 2,415,919,104)
+K1_DRAM_BYTES_PER_LAUNCH = 382720  # dram__bytes_read.sum + dram__bytes_write.sum (tables stay in L2)
 UNIT = "plans/s"
 
 
@@ -142,7 +142,7 @@ def ref_rate(p, sets, threads, window=WINDOW):
     return secs.value
 
 
-def cpu_baseline(p, threads=1, n_sets=3):
+def cpu_baseline(p, threads=1, n_sets=12):
     """Reference (oracle/_ref) on the host cores, bounded sample; port (oracle/) if absent."""
     from oracles import Oracle, ref_available
     sets = cpu_sample_sets(p, n_sets)
