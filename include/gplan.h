@@ -302,6 +302,34 @@ int gp_schedule(gp_ctx* ctx, const gp_sched_opts* opts, gp_schedule_result* out,
                 int32_t* rollout_ids, int32_t* stage_devices, gp_config* entry_configs,
                 gp_rollout_entry* entries, int32_t entry_cap, double* trace);
 
+/* ---- exhaustive evaluation -------------------------------- */
+
+/* Product-space training search: every candidate of enumerate_train_candidates
+ * (src/train_search.cpp:179-216; block lists x per-stage (tp, dp) options in odometer
+ * order), filtered by train_plan_fits (src/cost_model.cpp:232-241), ranked by
+ * train_step_cost, first minimum — the loop of tests/oracles.cpp:166-174.
+ * out->layouts = candidates, out->rank = the winner's candidate index; feasible is not
+ * counted (-1). Default TrainSearchOptions. */
+int gp_train_candidates_search(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
+                               gp_train_result* out, int32_t* stage_devices);
+
+typedef struct {
+  int32_t feasible;
+  int32_t n_train;            /* train_ids[0 .. n_train) ascending */
+  double objective;           /* max(C_T, C_I) of the optimum */
+  int64_t partitions;         /* bipartitions evaluated: 2^N - 2 */
+  int64_t train_candidates;   /* product-space training candidates over all partitions */
+  int64_t replica_vectors;    /* integer replica-count vectors enumerated */
+} gp_exhaustive_result;
+
+/* exhaustive_schedule_optimum (tests/oracles.cpp:144-209): over every bipartition of the
+ * cluster, the product-space training optimum, enumerate_configs + brute_milp_unbounded
+ * (tests/oracles.cpp:110-115, every integer replica vector), weight_sync_cost; objective
+ * max(C_T, C_I), first strict minimum in mask order, preferring C_I >= C_T. The
+ * reference refuses N > 10 (tests/oracles.cpp:148-151); the engine takes N <= 20.
+ * train_ids: N ints. */
+int gp_exhaustive_optimum(gp_ctx* ctx, int32_t window, gp_exhaustive_result* out, int32_t* train_ids);
+
 #ifdef __cplusplus
 }
 #endif

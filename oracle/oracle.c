@@ -258,6 +258,8 @@ typedef struct {
   int best_start[GP_MAX_STAGES], best_len[GP_MAX_STAGES];
   int best_tp[GP_MAX_STAGES], best_dp[GP_MAX_STAGES], best_layers[GP_MAX_STAGES];
   int scoring;  /* 0: count only */
+  int product;  /* enumerate_train_candidates product space instead of constrained_search */
+  int64_t cand; /* product-space candidates visited */
   int err;
 } search_t;
 
@@ -270,6 +272,101 @@ static int max_per_machine(const gp_cluster* c, const int32_t* dev, int n) {
     if (run > best) best = run;
   }
   return best;
+}
+
+/* train_step_cost -> train_cost_breakdown (src/cost_model.cpp:93-126) */
+static double plan_step_cost(const search_t* st, const block_t* blk, int S, const int* layers,
+                             const int* tps, const int* dps) {
+  const gp_cluster* c = st->sp->c;
+  const gp_workload* w = st->w;
+  int total_layers = 0;
+  for (int s = 0; s < S; ++s) total_layers += layers[s];
+  double max_stage = 0, max_compute = 0;
+  for (int s = 0; s < S; ++s) {
+    stage_cost_t sc = train_stage_cost(c, w, st->k, blk[s], tps[s], dps[s], layers[s], total_layers);
+    double tot = sc.compute + sc.tp_comm + sc.dp_comm;
+    if (tot > max_stage) max_stage = tot;   /* std::max(max, v): v only if max < v */
+    if (sc.compute > max_compute) max_compute = sc.compute;
+  }
+  double fill = 0, transfers = 0;
+  const double tokens = w_tokens(w);
+  if (S > 1) {
+    fill = (double)(S - 1) / w->micro_batches * max_compute;
+    if (tokens > 0) {
+      for (int s = 0; s + 1 < S; ++s) {
+        double beta = min_link_between(c, blk[s], blk[s + 1]);
+        transfers += tokens * w->hidden_dim * K_ACT_BYTES / beta;
+      }
+    }
+  }
+  double per_step = max_stage + fill + transfers;
+  return st->window * per_step;
+}
+
+/* one block list of enumerate_train_candidates (src/train_search.cpp:179-216): every
+ * (tp, dp) pick in odometer order (pick[0] fastest), train_plan_fits
+ * (src/cost_model.cpp:232-241), train_step_cost, strict < (tests/oracles.cpp:166-174) */
+static void score_layout_product(search_t* st) {
+  const gp_cluster* c = st->sp->c;
+  const gp_workload* w = st->w;
+  const int S = st->n_blocks;
+  double f[GP_MAX_STAGES];
+  int layers[GP_MAX_STAGES], tps[GP_MAX_STAGES], dps[GP_MAX_STAGES];
+  int n_opt[GP_MAX_STAGES], opt_tp[GP_MAX_STAGES][4], pick[GP_MAX_STAGES];
+  block_t blk[GP_MAX_STAGES];
+  for (int s = 0; s < S; ++s) {
+    blk[s].dev = st->sp->ordered + st->blk_start[s];
+    blk[s].n = st->blk_len[s];
+    double acc = 0;
+    for (int i = 0; i < blk[s].n; ++i) acc += c->device_flops[blk[s].dev[i]];
+    f[s] = acc;
+  }
+  if (allocate_layers(w->num_layers, f, S, layers)) {
+    st->err = GP_INVALID;
+    return;
+  }
+  for (int s = 0; s < S; ++s) {  /* tp_dp_options (src/train_search.cpp:74-93) */
+    int per_machine = max_per_machine(c, blk[s].dev, blk[s].n);
+    static const int tp_opts[4] = {1, 2, 4, 8};
+    n_opt[s] = 0;
+    for (int o = 0; o < 4; ++o)
+      if (tp_opts[o] <= per_machine && blk[s].n % tp_opts[o] == 0) opt_tp[s][n_opt[s]++] = tp_opts[o];
+    pick[s] = 0;
+  }
+  for (;;) {
+    int fits = 1;
+    for (int s = 0; s < S; ++s) {
+      tps[s] = opt_tp[s][pick[s]];
+      dps[s] = blk[s].n / tps[s];
+      double need_gb = mem_train_gb(w, st->k, tps[s], dps[s], layers[s]);
+      for (int i = 0; i < blk[s].n; ++i)
+        if (need_gb * 1e9 > c->device_hbm_cap[blk[s].dev[i]]) fits = 0;
+    }
+    if (fits) {
+      st->feasible++;
+      double cost = plan_step_cost(st, blk, S, layers, tps, dps);
+      if (!st->have_best || cost < st->best_cost) {
+        st->have_best = 1;
+        st->best_cost = cost;
+        st->best_rank = st->cand;
+        st->best_n = S;
+        for (int s = 0; s < S; ++s) {
+          st->best_start[s] = st->blk_start[s];
+          st->best_len[s] = st->blk_len[s];
+          st->best_tp[s] = tps[s];
+          st->best_dp[s] = dps[s];
+          st->best_layers[s] = layers[s];
+        }
+      }
+    }
+    st->cand++;
+    int i = 0;
+    while (i < S && ++pick[i] == n_opt[i]) {
+      pick[i] = 0;
+      ++i;
+    }
+    if (i == S) break;
+  }
 }
 
 /* one layout: constrained_search loop body (src/train_search.cpp:277-322) */
@@ -312,29 +409,7 @@ static void score_layout(search_t* st) {
     if (best_comm < 0) return; /* dead layout */
   }
   st->feasible++;
-  /* train_step_cost -> train_cost_breakdown (src/cost_model.cpp:93-126) */
-  int total_layers = 0;
-  for (int s = 0; s < S; ++s) total_layers += layers[s];
-  double max_stage = 0, max_compute = 0;
-  for (int s = 0; s < S; ++s) {
-    stage_cost_t sc = train_stage_cost(c, w, st->k, blk[s], tps[s], dps[s], layers[s], total_layers);
-    double tot = sc.compute + sc.tp_comm + sc.dp_comm;
-    if (tot > max_stage) max_stage = tot;   /* std::max(max, v): v only if max < v */
-    if (sc.compute > max_compute) max_compute = sc.compute;
-  }
-  double fill = 0, transfers = 0;
-  const double tokens = w_tokens(w);
-  if (S > 1) {
-    fill = (double)(S - 1) / w->micro_batches * max_compute;
-    if (tokens > 0) {
-      for (int s = 0; s + 1 < S; ++s) {
-        double beta = min_link_between(c, blk[s], blk[s + 1]);
-        transfers += tokens * w->hidden_dim * K_ACT_BYTES / beta;
-      }
-    }
-  }
-  double per_step = max_stage + fill + transfers;
-  double cost = st->window * per_step;
+  double cost = plan_step_cost(st, blk, S, layers, tps, dps);
   if (!st->have_best || cost < st->best_cost) {
     st->have_best = 1;
     st->best_cost = cost;
@@ -351,7 +426,10 @@ static void score_layout(search_t* st) {
 }
 
 static void visit_leaf(search_t* st) {
-  if (st->scoring && st->rank >= st->lo && st->rank < st->hi && !st->err) score_layout(st);
+  if (st->scoring && st->rank >= st->lo && st->rank < st->hi && !st->err) {
+    if (st->product) score_layout_product(st);
+    else score_layout(st);
+  }
   st->rank++;
 }
 
@@ -477,6 +555,52 @@ int or_constrained_search(const gp_cluster* c, const gp_workload* w, const gp_ca
       out->stage[s].layers = st.best_layers[s];
       for (int i = 0; i < st.best_len[s]; ++i)
         stage_devices[off++] = sp.ordered[st.best_start[s] + i];
+    }
+  }
+  space_free(&sp);
+  return GP_OK;
+}
+
+int or_train_candidates_search(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                               const int32_t* ids, int32_t n, int32_t window, gp_train_result* out,
+                               int32_t* stage_devices) {
+  memset(out, 0, sizeof *out);
+  if (n <= 0) return fail(GP_INVALID, "enumerate_train_candidates requires a non-empty train set");
+  gp_train_opts opts = {4, 16};  /* TrainSearchOptions defaults */
+  layout_space_t sp;
+  int rc = space_build(&sp, c, w, ids, n, &opts);
+  if (rc) return rc;
+  search_t st;
+  memset(&st, 0, sizeof st);
+  st.sp = &sp;
+  st.w = w;
+  st.k = k;
+  st.window = window;
+  st.lo = 0;
+  st.hi = INT64_MAX;
+  st.scoring = 1;
+  st.product = 1;
+  count_layouts(&sp);  /* the enumeration's subtree sizes */
+  if (sp.max_stages >= sp.n_runs) recurse_runs(&st, 0, 0);
+  out->layouts = st.cand;
+  out->feasible = st.feasible;
+  if (st.err) {
+    space_free(&sp);
+    return st.err;
+  }
+  if (st.have_best) {
+    out->found = 1;
+    out->cost = st.best_cost;
+    out->rank = st.best_rank;
+    out->n_stages = st.best_n;
+    int off = 0;
+    for (int s = 0; s < st.best_n; ++s) {
+      out->stage[s].first = off;
+      out->stage[s].count = st.best_len[s];
+      out->stage[s].tp = st.best_tp[s];
+      out->stage[s].dp = st.best_dp[s];
+      out->stage[s].layers = st.best_layers[s];
+      for (int i = 0; i < st.best_len[s]; ++i) stage_devices[off++] = sp.ordered[st.best_start[s] + i];
     }
   }
   space_free(&sp);
@@ -735,5 +859,148 @@ int or_weight_sync_cost(const gp_cluster* c, const gp_workload* w, const gp_cali
   double transfer = 0;
   if (bottleneck < K_INF && w_model_bytes_infer(w) > 0) transfer = w_model_bytes_infer(w) / bottleneck;
   *out = window * transfer + k->sync_latency_s;
+  return GP_OK;
+}
+
+/* ====================================================== exhaustive (tests/oracles.cpp) */
+
+typedef struct {
+  const gp_config* cfg;
+  int nc, dims;
+  int caps[GP_MAX_TYPES];
+  double B, len;
+  int feasible;
+  double theta;
+  int32_t* best;
+  int cur[512];
+  int64_t vectors;
+} brute_t;
+
+/* enumerate_all's Rec::go (tests/oracles.cpp:34-66) */
+static void brute_go(brute_t* b, int idx, double agg) {
+  if (idx == b->nc) {
+    b->vectors++;
+    if (agg <= 0) return;
+    double theta = b->B * b->len / agg;
+    if (!b->feasible || theta < b->theta - 1e-15) {
+      b->feasible = 1;
+      b->theta = theta;
+      for (int i = 0; i < b->nc; ++i) b->best[i] = b->cur[i];
+    }
+    return;
+  }
+  const int32_t* v = b->cfg[idx].type_counts;
+  int bound = INT32_MAX, uses = 0;
+  for (int t = 0; t < b->dims; ++t)
+    if (v[t] > 0) {
+      uses = 1;
+      int q = b->caps[t] / v[t];
+      if (q < bound) bound = q;
+    }
+  if (!uses) bound = 0;
+  for (int y = 0; y <= bound; ++y) {
+    b->cur[idx] = y;
+    for (int t = 0; t < b->dims; ++t) b->caps[t] -= y * v[t];
+    brute_go(b, idx + 1, agg + y * b->cfg[idx].throughput);
+    for (int t = 0; t < b->dims; ++t) b->caps[t] += y * v[t];
+  }
+}
+
+int or_brute_milp(const gp_config* configs, int32_t n_configs, const int32_t* caps, int32_t dims,
+                  double total_rollouts, double mean_len, int32_t* feasible, double* theta,
+                  int32_t* counts, int64_t* vectors) {
+  if (n_configs > 512 || dims > GP_MAX_TYPES) return fail(GP_INVALID, "brute_milp instance too large");
+  for (int i = 0; i < n_configs; ++i) counts[i] = 0;
+  *vectors = 0;
+  if (total_rollouts <= 0) {
+    *feasible = 1;
+    *theta = 0;
+    return GP_OK;
+  }
+  brute_t b;
+  memset(&b, 0, sizeof b);
+  b.cfg = configs;
+  b.nc = n_configs;
+  b.dims = dims;
+  for (int t = 0; t < dims; ++t) b.caps[t] = caps[t];
+  b.B = total_rollouts;
+  b.len = mean_len;
+  b.best = counts;
+  brute_go(&b, 0, 0.0);
+  *feasible = b.feasible;
+  *theta = b.theta;
+  *vectors = b.vectors;
+  return GP_OK;
+}
+
+int or_exhaustive_optimum(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                          int32_t window, gp_exhaustive_result* out, int32_t* train_ids) {
+  memset(out, 0, sizeof *out);
+  const int n = c->n_devices;
+  if (n < 2 || n > 30) return fail(GP_INVALID, "exhaustive optimum needs 2 <= devices <= 30");
+  const double total_rollouts = (double)w->batch_rollouts * window;
+  int have = 0, have_c = 0;
+  double best = 0, best_c = 0;
+  uint32_t best_mask = 0, best_mask_c = 0;
+  int32_t train[32], roll[32], sdev[32], caps[GP_MAX_TYPES], counts[512], et[512], er[512];
+  gp_config cfg[512];
+  for (uint32_t mask = 1; mask + 1 < (1u << n); ++mask) {
+    int nt = 0, nr = 0;
+    for (int d = 0; d < n; ++d) {
+      if (mask & (1u << d)) train[nt++] = d;
+      else roll[nr++] = d;
+    }
+    out->partitions++;
+    gp_train_result tr;
+    int rc = or_train_candidates_search(c, w, k, train, nt, window, &tr, sdev);
+    if (rc) return rc;
+    out->train_candidates += tr.layouts;
+    if (!tr.found) continue;
+    const double c_train = tr.cost;
+    gp_rollout_opts ro = {4};
+    int32_t ncfg = 0;
+    rc = or_enumerate_configs(c, w, k, roll, nr, &ro, cfg, 512, &ncfg);
+    if (rc) return rc;
+    if (ncfg == 0) continue;
+    rc = or_rollout_capacities(c, roll, nr, caps);
+    if (rc) return rc;
+    int32_t feas;
+    double theta;
+    int64_t vec;
+    rc = or_brute_milp(cfg, ncfg, caps, c->n_types, total_rollouts, w->mean_len, &feas, &theta, counts, &vec);
+    if (rc) return rc;
+    out->replica_vectors += vec;
+    if (!feas) continue;
+    int ne = 0;
+    for (int i = 0; i < ncfg; ++i)
+      if (counts[i] > 0) {
+        int t = 0;
+        while (t < c->n_types && cfg[i].type_counts[t] == 0) ++t;
+        et[ne] = t;
+        er[ne] = counts[i];
+        ++ne;
+      }
+    double update;
+    rc = or_weight_sync_cost(c, w, k, train, nt, roll, nr, et, er, ne, window, &update);
+    if (rc) return rc;
+    const double c_infer = theta + w->reward_cost_const + update;
+    const double objective = c_train < c_infer ? c_infer : c_train;  /* std::max */
+    if (!have || objective < best) {
+      have = 1;
+      best = objective;
+      best_mask = mask;
+    }
+    if (c_infer >= c_train && (!have_c || objective < best_c)) {
+      have_c = 1;
+      best_c = objective;
+      best_mask_c = mask;
+    }
+  }
+  const uint32_t m = have_c ? best_mask_c : best_mask;
+  out->feasible = have_c || have;
+  out->objective = have_c ? best_c : best;
+  if (out->feasible)
+    for (int d = 0; d < n; ++d)
+      if (m & (1u << d)) train_ids[out->n_train++] = d;
   return GP_OK;
 }

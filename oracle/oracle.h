@@ -59,6 +59,20 @@ int or_schedule(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
                 const or_sched_opts* opts, char** plan_json);
 void or_free(void* p);
 
+/* product-space training search (tests/oracles.cpp:166-174 over src/train_search.cpp:179-216):
+ * out->layouts = candidates, out->feasible = candidates passing train_plan_fits,
+ * out->rank = winner's candidate index */
+int or_train_candidates_search(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                               const int32_t* ids, int32_t n, int32_t window, gp_train_result* out,
+                               int32_t* stage_devices);
+/* brute_milp_unbounded (tests/oracles.cpp:16-115); counts: n_configs ints */
+int or_brute_milp(const gp_config* configs, int32_t n_configs, const int32_t* caps, int32_t dims,
+                  double total_rollouts, double mean_len, int32_t* feasible, double* theta,
+                  int32_t* counts, int64_t* vectors);
+/* exhaustive_schedule_optimum (tests/oracles.cpp:144-209), no device-count limit */
+int or_exhaustive_optimum(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                          int32_t window, gp_exhaustive_result* out, int32_t* train_ids);
+
 #ifdef __cplusplus
 }
 #endif

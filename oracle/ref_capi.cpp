@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "json.hpp"
+#include "oracles.hpp"
 #include "rlsched/calibration.hpp"
 #include "rlsched/cluster.hpp"
 #include "rlsched/cost_model.hpp"
@@ -224,6 +225,39 @@ int ref_train_candidates(void* h, const int* ids, int n, int window, char** out_
       arr.push_back(ojson{{"fits", fits}, {"cost", cost}, {"stages", st}});
     }
     *out_json = dup_string(arr.dump());
+  });
+}
+
+// The reference's own brute-force optimum (tests/oracles.cpp:144-209): every bipartition,
+// full product-space training search, exhaustive integer replica vectors.
+int ref_exhaustive_optimum(void* h, int window, char** out_json) {
+  return guarded([&] {
+    auto* ctx = static_cast<RefCtx*>(h);
+    auto t0 = std::chrono::steady_clock::now();
+    auto opt = oracle::exhaustive_schedule_optimum(ctx->cluster, ctx->work, ctx->calib, window);
+    double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    ojson doc;
+    doc["feasible"] = opt.feasible;
+    doc["objective"] = opt.objective;
+    doc["train_set"] = opt.train_set;
+    doc["seconds"] = secs;
+    *out_json = dup_string(doc.dump());
+  });
+}
+
+// brute_milp_unbounded (tests/oracles.cpp:110-115): every integer replica vector.
+int ref_brute_milp(const char* configs_json, const int* caps, int dims, double total_rollouts,
+                   double mean_len, char** out_json) {
+  return guarded([&] {
+    auto j = nlohmann::json::parse(configs_json);
+    std::vector<ReplicaConfig> cfgs;
+    for (const auto& c : j) cfgs.push_back(config_from(c));
+    auto r = oracle::brute_milp_unbounded(cfgs, std::vector<int>(caps, caps + dims), total_rollouts, mean_len);
+    ojson doc;
+    doc["feasible"] = r.feasible;
+    doc["theta"] = r.theta;
+    doc["replica_counts"] = r.replica_counts;
+    *out_json = dup_string(doc.dump());
   });
 }
 

@@ -100,6 +100,13 @@ class gp_partition(C.Structure):
                 ("compute_fraction", C.c_double)]
 
 
+class gp_exhaustive_result(C.Structure):
+    _fields_ = [
+        ("feasible", C.c_int32), ("n_train", C.c_int32), ("objective", C.c_double),
+        ("partitions", C.c_int64), ("train_candidates", C.c_int64), ("replica_vectors", C.c_int64),
+    ]
+
+
 def default_train_opts() -> gp_train_opts:
     return gp_train_opts(4, 16)
 
@@ -136,6 +143,8 @@ def declare(lib: C.CDLL, prefix: str) -> None:
                            P(gp_rollout_result), P(gp_rollout_entry)],
             "weight_sync_cost": [vp, i32p, C.c_int32, i32p, C.c_int32, i32p, i32p, C.c_int32,
                                  C.c_int32, f64p],
+            "train_candidates_search": [vp, i32p, C.c_int32, C.c_int32, P(gp_train_result), i32p],
+            "exhaustive_optimum": [vp, C.c_int32, P(gp_exhaustive_result), i32p],
         })
     else:  # oracle: cluster/workload/calib pointers instead of a context
         cw = [P(gp_cluster), P(gp_workload)]
@@ -154,6 +163,10 @@ def declare(lib: C.CDLL, prefix: str) -> None:
             "partition_candidates": [P(gp_cluster), P(gp_gamma), P(gp_part_opts), C.c_int32,
                                      P(gp_partition), i32p, P(C.c_int32)],
             "partition_objective": [P(gp_cluster), i32p, C.c_int32, f64p, f64p],
+            "train_candidates_search": cwk + [i32p, C.c_int32, C.c_int32, P(gp_train_result), i32p],
+            "brute_milp": [P(gp_config), C.c_int32, i32p, C.c_int32, C.c_double, C.c_double, i32p, f64p,
+                           i32p, P(C.c_int64)],
+            "exhaustive_optimum": cwk + [C.c_int32, P(gp_exhaustive_result), i32p],
         }
     for name, args in sigs.items():
         fn = getattr(lib, f"{prefix}_{name}", None)

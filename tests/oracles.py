@@ -55,6 +55,8 @@ def ref_lib():
         _ref.ref_solve_milp.argtypes = [cp, abi.i32p, C.c_int, C.c_double, C.c_double, P(vp)]
         _ref.ref_weight_sync.argtypes = [vp, abi.i32p, C.c_int, abi.i32p, C.c_int, C.c_int, cp,
                                          P(C.c_double)]
+        _ref.ref_exhaustive_optimum.argtypes = [vp, C.c_int, P(vp)]
+        _ref.ref_brute_milp.argtypes = [cp, abi.i32p, C.c_int, C.c_double, C.c_double, P(vp)]
         _ref.ref_partition_candidates.argtypes = [vp, C.c_double, C.c_double, C.c_double, C.c_double,
                                                   C.c_int, C.c_ulonglong, C.c_int, C.c_int, C.c_int,
                                                   P(vp)]
@@ -116,6 +118,17 @@ class Ref:
         out = C.c_void_p()
         return self._json(self.lib.ref_train_candidates(self.h, ids.ctypes.data_as(abi.i32p),
                                                         len(ids), window, C.byref(out)), out)
+
+    def exhaustive(self, window):
+        out = C.c_void_p()
+        return self._json(self.lib.ref_exhaustive_optimum(self.h, window, C.byref(out)), out)
+
+    def brute_milp(self, configs, caps, B, mean_len):
+        caps = _ids(caps)
+        out = C.c_void_p()
+        rc = self.lib.ref_brute_milp(json.dumps(configs).encode(), caps.ctypes.data_as(abi.i32p),
+                                     len(caps), B, mean_len, C.byref(out))
+        return self._json(rc, out)
 
     def enumerate_configs(self, ids, max_stages=4):
         ids = _ids(ids)
@@ -184,6 +197,39 @@ class Oracle:
         res, devs = self.constrained_search_raw(ids, window, opts, lo, hi)
         return train_result_dict(res, devs)
 
+    def train_candidates_search(self, ids, window):
+        ids = _ids(ids)
+        res = abi.gp_train_result()
+        devs = np.zeros(max(len(ids), 1), dtype=np.int32)
+        rc = self.lib.or_train_candidates_search(C.byref(self.c), C.byref(self.w), C.byref(self.k),
+                                                 ids.ctypes.data_as(abi.i32p), len(ids), window,
+                                                 C.byref(res), devs.ctypes.data_as(abi.i32p))
+        if rc:
+            self.err(rc)
+        return train_result_dict(res, devs)
+
+    def brute_milp(self, configs, caps, B, mean_len):
+        arr = (abi.gp_config * max(len(configs), 1))(*configs)
+        caps = _ids(caps)
+        feas, theta, vec = C.c_int32(), C.c_double(), C.c_int64()
+        counts = np.zeros(max(len(configs), 1), dtype=np.int32)
+        rc = self.lib.or_brute_milp(arr, len(configs), caps.ctypes.data_as(abi.i32p), len(caps), B,
+                                   mean_len, C.byref(feas), C.byref(theta),
+                                   counts.ctypes.data_as(abi.i32p), C.byref(vec))
+        if rc:
+            self.err(rc)
+        return {"feasible": bool(feas.value), "theta": theta.value,
+                "replica_counts": counts[:len(configs)].tolist(), "vectors": vec.value}
+
+    def exhaustive(self, window):
+        out = abi.gp_exhaustive_result()
+        ids = np.zeros(self.problem.cluster.n, dtype=np.int32)
+        rc = self.lib.or_exhaustive_optimum(C.byref(self.c), C.byref(self.w), C.byref(self.k), window,
+                                            C.byref(out), ids.ctypes.data_as(abi.i32p))
+        if rc:
+            self.err(rc)
+        return exhaustive_dict(out, ids)
+
     def schedule(self, eta=-1, seed=4276115, expand=True, restarts=16):
         class SchedOpts(C.Structure):
             _fields_ = [("eta_override", C.c_int32), ("seed", C.c_uint64), ("restarts", C.c_int32),
@@ -208,6 +254,12 @@ def train_result_dict(res, devs):
         d["stages"] = [{"devices": devs[s.first:s.first + s.count].tolist(), "tp": s.tp, "dp": s.dp,
                         "layers": s.layers} for s in res.stage[:res.n_stages]]
     return d
+
+
+def exhaustive_dict(out, ids):
+    return {"feasible": bool(out.feasible), "objective": out.objective if out.feasible else None,
+            "train_set": ids[:out.n_train].tolist(), "partitions": out.partitions,
+            "train_candidates": out.train_candidates, "replica_vectors": out.replica_vectors}
 
 
 def config_dict(c, n_types):
