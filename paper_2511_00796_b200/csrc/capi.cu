@@ -17,15 +17,15 @@ namespace gp {
 
 int train_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int64_t* layouts);
 int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_train_opts* o,
-                 long long lo, long long hi, gp_train_result* out, int32_t* stage_devices);
-int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o);
+                 long long lo, long long hi, gp_train_result* out, int32_t* stage_devices, int mode = 0);
+int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int mode = 0);
 int train_launch(gp_ctx* ctx, int window, long long lo, long long hi);
 int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices);
 void train_state_free(gp_ctx* ctx);
 void train_last_nm(gp_ctx* ctx, long long nm[4]);
 void train_nm_merge(long long a[4], const long long b[4]);
 void train_memo_free(gp_ctx* ctx);
-std::string train_memo_key(const int32_t* ids, int n, const gp_train_opts* o);
+std::string train_memo_key(const int32_t* ids, int n, const gp_train_opts* o, int mode = 0);
 bool train_memo_get(gp_ctx* ctx, const std::string& key, int window, gp_train_result* out,
                     int32_t* stage_devices);
 void train_memo_put_last(gp_ctx* ctx, const std::string& key, const gp_train_result& r, const long long nm[4]);

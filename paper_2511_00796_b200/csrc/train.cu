@@ -271,53 +271,72 @@ __global__ void __launch_bounds__(256) k2b_transfers(const int* __restrict__ ord
 // ------------------------------------------------------------ K2c stage table
 // Per (block, layer_count): the option loop of constrained_search
 // (src/train_search.cpp:289-315) with mem_cumsum_train and train_stage_cost.
+// One (tp, dp) option of a stage with lc layers (src/train_search.cpp:241-258 with
+// tp_dp_options :74-93, mem_cumsum_train src/cost_model.cpp:198-207, train_stage_cost
+// :57-91). False when the option is not offered or exceeds the block's memory.
+__device__ __forceinline__ bool stage_option(const BlockRec& b, int lc, int o, const Scalars& sc,
+                                             double ceff, double& compute, double& tp_comm,
+                                             double& dp_comm) {
+  const int tp = 1 << o;
+  if (tp > b.per_machine || b.n % tp != 0) return false;
+  const int dp = b.n / tp;
+  const double lf = static_cast<double>(lc) / sc.L;  // layer_frac (total_layers == num_layers)
+  const double weight = sc.P * lf * sc.bpp_train / tp;
+  const double tpm = sc.tokens / dp / sc.mb;
+  const double act = sc.act_coeff * tpm * sc.H * kActBytes * lc / tp;
+  const double need_gb = (weight + act) / 1e9;
+  if (need_gb * 1e9 > b.cap_front) return false;
+  compute = sc.tfpt_tokens * lf / (ceff * b.flops);
+  tp_comm = 0;
+  dp_comm = 0;
+  if (tp > 1 && sc.tokens > 0) {
+    const double prt = sc.tokens / dp;
+    const double vol = sc.tp_coeff * lc * prt * sc.H * kActBytes * 2.0 * (tp - 1) / tp;
+    tp_comm = vol / b.beta_tp[o];
+  }
+  if (dp > 1) {
+    const double shard = sc.P * lf * sc.grad_bpp / tp;
+    const double vol = 2.0 * shard * (dp - 1) / dp;
+    dp_comm = vol / b.beta_dp[o];
+  }
+  return true;
+}
+
+// mode 0 (constrained_search): per (block, layers) the comm-minimal memory-feasible option
+// (strict <, tp ascending). mode 1 (product space, enumerate_train_candidates): the option of
+// minimal TrainStageCost::total() — the value the product-space argmin reaches per stage.
 __global__ void __launch_bounds__(256) k2c_stage_table(const BlockRec* __restrict__ blk, int nblk,
                                                        Scalars sc, const double* __restrict__ ceff,
-                                                       double2* __restrict__ stage,
+                                                       int mode, double2* __restrict__ stage,
                                                        int8_t* __restrict__ opt) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)nblk * sc.L) return;
   const int bi = (int)(idx / sc.L);
   const int lc = (int)(idx - (long long)bi * sc.L) + 1;
   const BlockRec& b = blk[bi];
-  const double lf = static_cast<double>(lc) / sc.L;  // layer_frac (total_layers == num_layers)
-  const double compute = sc.tfpt_tokens * lf / (ceff[b.type] * b.flops);
-  double best_comm = -1, best_tp_comm = 0, best_dp_comm = 0;
+  double best_key = -1, best_total = 0, compute = 0;
   int best_o = -1;
 #pragma unroll
   for (int o = 0; o < 4; ++o) {
-    const int tp = 1 << o;
-    if (tp > b.per_machine || b.n % tp != 0) continue;
-    const int dp = b.n / tp;
-    // mem_cumsum_train (src/cost_model.cpp:198-207)
-    const double weight = sc.P * lf * sc.bpp_train / tp;
-    const double tpm = sc.tokens / dp / sc.mb;
-    const double act = sc.act_coeff * tpm * sc.H * kActBytes * lc / tp;
-    const double need_gb = (weight + act) / 1e9;
-    if (need_gb * 1e9 > b.cap_front) continue;
-    double tp_comm = 0, dp_comm = 0;
-    if (tp > 1 && sc.tokens > 0) {
-      const double prt = sc.tokens / dp;
-      const double vol = sc.tp_coeff * lc * prt * sc.H * kActBytes * 2.0 * (tp - 1) / tp;
-      tp_comm = vol / b.beta_tp[o];
-    }
-    if (dp > 1) {
-      const double shard = sc.P * lf * sc.grad_bpp / tp;
-      const double vol = 2.0 * shard * (dp - 1) / dp;
-      dp_comm = vol / b.beta_dp[o];
-    }
-    const double comm = tp_comm + dp_comm;
-    if (best_comm < 0 || comm < best_comm) {
-      best_comm = comm;
-      best_tp_comm = tp_comm;
-      best_dp_comm = dp_comm;
+    double cmp, tp_comm, dp_comm;
+    if (!stage_option(b, lc, o, sc, ceff[b.type], cmp, tp_comm, dp_comm)) continue;
+    compute = cmp;  // option-independent
+    const double total = cmp + tp_comm + dp_comm;
+    const double key = mode == 0 ? tp_comm + dp_comm : total;
+    if (best_key < 0 || key < best_key) {
+      best_key = key;
+      best_total = total;
       best_o = o;
     }
+  }
+  if (best_o < 0) {  // still report compute (option-independent) for the fill/drain term
+    const double lf = static_cast<double>(lc) / sc.L;
+    compute = sc.tfpt_tokens * lf / (ceff[b.type] * b.flops);
   }
   double2 e;
   // TrainStageCost::total(); +inf marks "no memory-feasible option" so that the layout
   // maximum becomes +inf and the layout is rejected without a per-stage test in K1
-  e.x = best_o < 0 ? __longlong_as_double(0x7ff0000000000000LL) : compute + best_tp_comm + best_dp_comm;
+  e.x = best_o < 0 ? __longlong_as_double(0x7ff0000000000000LL) : best_total;
   e.y = compute;
   stage[idx] = e;
   opt[idx] = (int8_t)best_o;
@@ -1225,7 +1244,8 @@ __global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb
                                                    const BlockRec* __restrict__ blk, int L,
                                                    int window, const NearMin* __restrict__ partial,
                                                    int n_partial, TrainOut* __restrict__ out,
-                                                   const unsigned long long* __restrict__ slow_q) {
+                                                   const unsigned long long* __restrict__ slow_q,
+                                                   Scalars sc, const double* __restrict__ ceff, int mode) {
   NearMin m;
   nm_init(m);
   for (int i = threadIdx.x; i < n_partial; i += blockDim.x) nm_merge(m, partial[i]);
@@ -1251,11 +1271,29 @@ __global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb
   int lay[NS], bis[NS];
   double x;
   eval_layout<R, true>(sp, tb, blkf, L, D, tb.suf[s], x, lay, bis);
+  // mode 1 (product space): the first option combination in odometer order reaching the
+  // layout's minimum — per stage the lowest tp whose total does not exceed M* = max over the
+  // stages of their minimal totals (any such stage choice keeps the maximum at M*)
+  double mstar = 0;
+  for (int q = 0; q < NS; ++q)
+    if (bis[q] >= 0) {
+      const double v = tb.stage[(size_t)bis[q] * L + (lay[q] - 1)].x;
+      if (v > mstar) mstar = v;
+    }
   int n = 0;
   for (int q = 0; q < NS; ++q) {
     if (bis[q] < 0) continue;
     const BlockRec& br = blk[bis[q]];
-    const int o = tb.opt[(size_t)bis[q] * L + (lay[q] - 1)];
+    int o = tb.opt[(size_t)bis[q] * L + (lay[q] - 1)];
+    if (mode == 1) {
+      for (int oo = 0; oo < 4; ++oo) {
+        double cmp, tpc, dpc;
+        if (stage_option(br, lay[q], oo, sc, ceff[br.type], cmp, tpc, dpc) && cmp + tpc + dpc <= mstar) {
+          o = oo;
+          break;
+        }
+      }
+    }
     const int tp = 1 << o;
     out->first[n] = br.start;
     out->count[n] = br.n;
@@ -1477,7 +1515,7 @@ T* carve(char*& p, size_t count) {
 template <int R>
 int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const double2* blkf,
                 const BlockRec* blk, int window, long long lo, long long hi, NearMin* partial,
-                int max_blocks, TrainOut* d_out, cudaStream_t stream, bool fast) {
+                int max_blocks, TrainOut* d_out, cudaStream_t stream, bool fast, int mode) {
   ScanRange rg{};
   rank_split(h, lo, rg.p_lo, rg.s_lo);
   rank_split(h, hi, rg.p_hi, rg.s_hi);
@@ -1513,13 +1551,129 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
     n_partial = 0;
   }
   k1_finalize<R><<<1, 256, 0, stream>>>(h.sp, tb, blkf, blk, ctx->sc.L, window, partial, n_partial, d_out,
-                                        fast && hi > lo ? ctx->d_slow : nullptr);
+                                        fast && hi > lo ? ctx->d_slow : nullptr, ctx->sc, ctx->d_ceff, mode);
   ctx->launches++;
   GP_CUDA(cudaGetLastError());
   return GP_OK;
 }
 
 }  // namespace
+
+// ---- product-space bookkeeping (enumerate_train_candidates, src/train_search.cpp:179-216):
+// the number of candidates = sum over layouts of prod_s |tp_dp_options(block_s)|, and the
+// candidate index of a (layout, option picks). Pure enumeration metadata (no cost model).
+namespace {
+struct CandMeta {
+  const HostSpace* h;
+  const gp_ctx* ctx;
+  // options of the block [a, b) (position indices) of run r
+  int w(int r, int a, int b, int* tps = nullptr) const {
+    const int* P = h->pos.data() + h->pos_off[r];
+    const int s0 = h->run_start[r] + P[a], s1 = h->run_start[r] + P[b];
+    int per_machine = 0, run = 0;
+    for (int i = s0; i < s1; ++i) {
+      run = (i > s0 && ctx->h_machine[h->ordered[i]] == ctx->h_machine[h->ordered[i - 1]]) ? run + 1 : 1;
+      per_machine = std::max(per_machine, run);
+    }
+    int n = 0;
+    for (int tp = 1; tp <= 8; tp *= 2)
+      if (tp <= per_machine && (s1 - s0) % tp == 0) {
+        if (tps) tps[n] = tp;
+        ++n;
+      }
+    return n;
+  }
+  // sum over cut combinations of run r with k blocks of the product of block weights
+  long long G(int r, int k) const {
+    const int nc = h->sp.nc[r];
+    std::vector<std::vector<long long>> F(k + 1, std::vector<long long>(nc + 2, 0));
+    F[0][0] = 1;
+    for (int j = 0; j < k; ++j)
+      for (int i = 0; i <= nc + 1; ++i) {
+        if (!F[j][i]) continue;
+        for (int i2 = i + 1; i2 <= nc + 1; ++i2) {
+          if (j + 1 < k && i2 == nc + 1) continue;  // only the last block ends at the run end
+          if (j + 1 == k && i2 != nc + 1) continue;
+          F[j + 1][i2] += F[j][i] * w(r, i, i2);
+        }
+      }
+    return F[k][nc + 1];
+  }
+};
+}  // namespace
+
+int train_candidates_meta(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_result* res,
+                          const int32_t* stage_devices, long long* count, long long* index) {
+  HostSpace h;
+  gp_train_opts o{4, 16};
+  int rc = build_space(ctx, ids, n, &o, h);
+  if (rc) return rc;
+  const TrainSpace& sp = h.sp;
+  CandMeta cm{&h, ctx};
+  std::vector<std::vector<long long>> W(sp.R + 1, std::vector<long long>(sp.max_stages + 2, 0));
+  std::vector<std::vector<long long>> Gk(sp.R, std::vector<long long>(kMaxPerRun + 1, 0));
+  for (int r = 0; r < sp.R; ++r)
+    for (int k = 1; k <= sp.kmax[r] && k - 1 <= sp.nc[r]; ++k) Gk[r][k] = cm.G(r, k);
+  for (int u = 0; u <= sp.max_stages; ++u) W[sp.R][u] = 1;
+  for (int r = sp.R - 1; r >= 0; --r)
+    for (int u = 0; u <= sp.max_stages; ++u) {
+      long long acc = 0;
+      for (int k = 1; k <= sp.kmax[r]; ++k) {
+        if (u + k + (sp.R - 1 - r) > sp.max_stages) break;
+        acc += Gk[r][k] * W[r + 1][u + k];
+      }
+      W[r][u] = acc;
+    }
+  *count = sp.max_stages >= sp.R ? W[0][0] : 0;
+  *index = -1;
+  if (!res || !res->found) return GP_OK;
+  // the winner's blocks per run, as position indices
+  long long before = 0, pick_index = 0, radix = 1, pw = 1;  // pw: weight of the chosen earlier runs
+  int u = 0, st = 0;
+  for (int r = 0; r < sp.R; ++r) {
+    const int* P = h.pos.data() + h.pos_off[r];
+    const int nc = sp.nc[r], base = h.run_start[r];
+    std::vector<int> idx{0};
+    while (st < res->n_stages && res->stage[st].first < h.run_start[r + 1]) {
+      const int end = res->stage[st].first + res->stage[st].count - base;
+      int pi = 0;
+      while (pi <= nc + 1 && P[pi] != end) ++pi;
+      idx.push_back(pi);
+      int tps[4];
+      const int nw = cm.w(r, idx[idx.size() - 2], pi, tps);
+      int pk = 0;
+      while (pk < nw && tps[pk] != res->stage[st].tp) ++pk;
+      pick_index += pk * radix;
+      radix *= nw;
+      ++st;
+    }
+    const int k = (int)idx.size() - 1;
+    for (int k2 = 1; k2 < k; ++k2) before += pw * Gk[r][k2] * W[r + 1][u + k2];
+    // combinations of k-1 cut indices before the winner's, lexicographically
+    std::vector<int> c(k + 1);
+    c[0] = 0;
+    c[k] = nc + 1;
+    for (int j = 1; j < k; ++j) c[j] = j;
+    while (true) {
+      bool same = true;
+      for (int j = 1; j < k; ++j) same &= c[j] == idx[j];
+      if (same) break;
+      long long wt = 1;
+      for (int j = 0; j < k; ++j) wt *= cm.w(r, c[j], c[j + 1]);
+      before += pw * wt * W[r + 1][u + k];
+      int j = k - 1;  // next combination (lexicographic over c[1..k-1] in [1, nc])
+      while (j >= 1 && c[j] == nc - (k - 1 - j)) --j;
+      if (j < 1) break;
+      ++c[j];
+      for (int j2 = j + 1; j2 < k; ++j2) c[j2] = c[j2 - 1] + 1;
+    }
+    for (int j = 0; j < k; ++j) pw *= cm.w(r, idx[j], idx[j + 1]);
+    u += k;
+  }
+  (void)stage_devices;
+  *index = before + pick_index;
+  return GP_OK;
+}
 
 int train_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int64_t* layouts) {
   HostSpace h;
@@ -1565,6 +1719,7 @@ struct PreparedTrain {
   int L = 0;
   long long lo = 0, hi = 0;
   int window = 0;
+  int mode = 0;  // 0: constrained_search; 1: product space (enumerate_train_candidates)
   bool launched = false;
   long long nm[4] = {kInfBits, LLONG_MAX, LLONG_MAX, LLONG_MAX};  // NearMin of the last collect (ranks)
 };
@@ -1746,7 +1901,7 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   {
     const long long cnt = (long long)h.nblk * L;
     k2c_stage_table<<<(int)((cnt + 255) / 256), 256, 0, stream>>>(P.d_blk, h.nblk, ctx->sc, ctx->d_ceff,
-                                                                 P.d_stage, P.d_opt);
+                                                                 P.mode, P.d_stage, P.d_opt);
     k_extract_blkf<<<(h.nblk + 255) / 256, 256, 0, stream>>>(P.d_blk, h.nblk, P.d_blkf);
     const int ns = (int)h.choices.size();
     k2d_suffix_table<<<(ns + 255) / 256, 256, 0, stream>>>(P.d_choices, ns, h.sp, P.d_tin, P.d_suf);
@@ -1765,10 +1920,10 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   // ---- K1: layout scan over [lo, hi)
   const int R = h.sp.R;
   int rc;
-  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast);
-  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast);
-  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast);
-  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast);
+  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode);
+  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode);
+  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode);
+  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode);
   else rc = set_error(GP_INVALID, "train sets spanning more than 4 gpu types are not supported");
   if (!rc && timing) GP_CUDA(cudaEventRecord(ctx->ev[2], stream));
   return rc;
@@ -1799,11 +1954,12 @@ static void fill_result(PreparedTrain& P, const TrainOut* ho, gp_train_result* o
   }
 }
 
-int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o) {
+int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int mode) {
   if (!prepared(ctx)) prepared(ctx) = new PreparedTrain();
   PreparedTrain& P = *prepared(ctx);
   GP_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer / scratch may be reused
   P.launched = false;
+  P.mode = mode;
   P.h = HostSpace();
   int rc = build_space(ctx, ids, n, o, P.h);
   if (rc) return rc;
@@ -1890,11 +2046,12 @@ void train_memo_free(gp_ctx* ctx) {
   ctx->train_memo = nullptr;
 }
 
-std::string train_memo_key(const int32_t* ids, int n, const gp_train_opts* o) {
+std::string train_memo_key(const int32_t* ids, int n, const gp_train_opts* o, int mode) {
   std::vector<int32_t> v(ids, ids + n);
   std::sort(v.begin(), v.end());  // the search canonicalises the order itself
   v.push_back(o->max_stages_per_type);
   v.push_back(o->device_granularity_limit);
+  v.push_back(mode);
   return std::string(reinterpret_cast<const char*>(v.data()), v.size() * sizeof(int32_t));
 }
 
@@ -1942,9 +2099,9 @@ void train_memo_put(gp_ctx* ctx, const std::string& key, const gp_train_result& 
 }
 
 int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_train_opts* o,
-                 long long lo, long long hi, gp_train_result* out, int32_t* stage_devices) {
+                 long long lo, long long hi, gp_train_result* out, int32_t* stage_devices, int mode) {
   std::memset(out, 0, sizeof *out);
-  int rc = train_prepare(ctx, ids, n, o);
+  int rc = train_prepare(ctx, ids, n, o, mode);
   if (!rc) rc = train_launch(ctx, window, lo, hi);
   if (!rc) rc = train_collect(ctx, out, stage_devices);
   return rc;
@@ -1954,13 +2111,13 @@ int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_tr
 // every set's inputs travel in ONE H2D copy, all tables + scans are enqueued back to back,
 // the results come back in ONE D2H copy with ONE synchronisation.
 int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
-                const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices) {
+                const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices, int mode) {
   if (n_sets <= 0) return GP_OK;
   // answered from the memo where possible; the rest is scanned in one batch
   std::vector<std::string> keys(n_sets);
   std::vector<int> todo;
   for (int i = 0; i < n_sets; ++i) {
-    keys[i] = train_memo_key(ids[i], ns[i], o);
+    keys[i] = train_memo_key(ids[i], ns[i], o, mode);
     if (!train_memo_get(ctx, keys[i], window, outs + i, stage_devices ? stage_devices[i] : nullptr))
       todo.push_back(i);
   }
@@ -1976,7 +2133,7 @@ int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_
       sd2.push_back(stage_devices ? stage_devices[i] : nullptr);
     }
     int rc = train_batch(ctx, (int)todo.size(), ids2.data(), ns2.data(), window, o, outs2.data(),
-                         stage_devices ? sd2.data() : nullptr);
+                         stage_devices ? sd2.data() : nullptr, mode);
     if (rc) return rc;
     for (size_t j = 0; j < todo.size(); ++j) outs[todo[j]] = outs2[j];
     return GP_OK;
@@ -1986,6 +2143,7 @@ int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_
   for (int i = 0; i < n_sets; ++i) {
     int rc = build_space(ctx, ids[i], ns[i], o, Ps[i].h);
     if (rc) return rc;
+    Ps[i].mode = mode;
     Ps[i].L = ctx->sc.L;
     Ps[i].max_blocks = std::min(ctx->num_sms * 8, (int)std::max<long long>(1, Ps[i].h.total / 4096));
     ib += input_bytes(Ps[i].h);

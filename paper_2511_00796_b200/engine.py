@@ -197,6 +197,26 @@ class Engine:
         _check(lib().gp_train_collect(self._h, C.byref(res), devs.ctypes.data_as(abi.i32p)))
         return res, devs
 
+    def train_candidates_search(self, train_set, window: int):
+        """Product-space training search (enumerate_train_candidates x train_plan_fits x
+        train_step_cost, first minimum; tests/oracles.cpp:166-174) -> (gp_train_result, devices).
+        res.layouts = candidates, res.rank = the winner's candidate index."""
+        ids = _ids(train_set)
+        res = abi.gp_train_result()
+        devs = np.zeros(max(len(ids), 1), dtype=np.int32)
+        _check(lib().gp_train_candidates_search(self._h, ids.ctypes.data_as(abi.i32p), len(ids), window,
+                                                C.byref(res), devs.ctypes.data_as(abi.i32p)))
+        return res, devs
+
+    def exhaustive(self, window: int):
+        """exhaustive_schedule_optimum (tests/oracles.cpp:144-209) over every bipartition."""
+        out = abi.gp_exhaustive_result()
+        ids = np.zeros(self.problem.cluster.n, dtype=np.int32)
+        _check(lib().gp_exhaustive_optimum(self._h, window, C.byref(out), ids.ctypes.data_as(abi.i32p)))
+        return {"feasible": bool(out.feasible), "objective": out.objective if out.feasible else None,
+                "train_set": ids[:out.n_train].tolist(), "partitions": out.partitions,
+                "train_candidates": out.train_candidates, "replica_vectors": out.replica_vectors}
+
     def set_memo(self, on: bool = True):
         """Enable (default) / disable + drop the window-independent constrained_search memo."""
         _check(lib().gp_ctx_set_memo(self._h, int(on)))

@@ -1,0 +1,69 @@
+"""GPU parity of the exhaustive rows: the product-space training
+search and exhaustive_schedule_optimum, against the reference's own outputs
+(tests/golden/exhaustive.json) and, beyond the reference's 10-device limit, the C
+restatement (oracle/)."""
+import pytest
+
+from common import golden, problem, random_train_sets
+from oracles import Oracle, train_result_dict
+
+pytestmark = pytest.mark.gpu
+
+_engines = {}
+
+
+def engine(name):
+    from paper_2511_00796_b200.engine import Engine
+    if name not in _engines:
+        _engines[name] = Engine(problem(name))
+    return _engines[name]
+
+
+@pytest.mark.parametrize("name", ["t8_tiny", "t10_tiny", "c1_desk_mixed", "c2_16gpu"])
+def test_product_space_vs_reference(name):
+    eng = engine(name)
+    for case in golden("exhaustive.json")["train_candidates"][name]:
+        res, devs = eng.train_candidates_search(case["ids"], case["window"])
+        got = train_result_dict(res, devs)
+        assert got["layouts"] == case["candidates"], case["ids"]
+        best = case["best"]
+        assert got["found"] == (best is not None), case["ids"]
+        if best:
+            assert got["cost"] == best["cost"], case["ids"]
+            assert got["rank"] == best["rank"], case["ids"]
+            assert got["stages"] == best["stages"], case["ids"]
+
+
+def test_product_space_vs_oracle_c3():
+    """Larger train sets (machine-granular cuts, three types) against the C restatement."""
+    name = "c3_64gpu"
+    p = problem(name)
+    orc = Oracle(p)
+    eng = engine(name)
+    sets = [s for s in random_train_sets(p.cluster.n, 40, seed=31337) if orc.train_space(s) <= 2000][:12]
+    assert len(sets) >= 6
+    for ids in sets:
+        want = orc.train_candidates_search(ids, 3)
+        res, devs = eng.train_candidates_search(ids, 3)
+        got = train_result_dict(res, devs)
+        want.pop("feasible")
+        got.pop("feasible")
+        assert got == want, ids
+
+
+def test_exhaustive_optimum_vs_reference():
+    for key, want in golden("exhaustive.json")["exhaustive"].items():
+        name, window = key.split("/window=")
+        got = engine(name).exhaustive(int(window))
+        assert got["feasible"] == want["feasible"], key
+        assert got["objective"] == want["objective"], key
+        assert got["train_set"] == want["train_set"], key
+
+
+@pytest.mark.parametrize("name", ["t12_tiny", "c2_16gpu"])
+def test_exhaustive_optimum_beyond_reference_limit(name):
+    """12 and 16 devices (the reference refuses > 10): engine == C restatement, incl. the
+    candidate and replica-vector counts."""
+    want = Oracle(problem(name)).exhaustive(3)
+    got = engine(name).exhaustive(3)
+    assert got == want
