@@ -15,7 +15,10 @@
 //
 // Brute MILP. One thread per rollout set walks the recursion of enumerate_all iteratively
 // (same order, same `agg + y * h` accumulation and `theta < best - 1e-15` improvement rule).
+#include <chrono>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -197,6 +200,11 @@ int exhaustive_optimum(gp_ctx* ctx, int window, gp_exhaustive_result* out, int32
   const gp_rollout_opts ro{4};
   const long long masks = (1LL << N) - 2;
   const int chunk = 8192;
+  double ph[5] = {0, 0, 0, 0, 0};  // GPLAN_PROFILE: train, counts, configs, brute, weight sync
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto since = [&](std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(now() - t0).count();
+  };
   bool have = false, have_c = false;
   double best = 0, best_c = 0;
   long long best_mask = 0, best_mask_c = 0;
@@ -215,8 +223,11 @@ int exhaustive_optimum(gp_ctx* ctx, int window, gp_exhaustive_result* out, int32
     }
     // training side: product-space optimum per train set
     std::vector<gp_train_result> tres(q);
+    auto t0 = now();
     int rc = train_batch(ctx, q, tp.data(), tn.data(), window, &to, tres.data(), nullptr, 1);
     if (rc) return rc;
+    ph[0] += since(t0);
+    t0 = now();
     for (int i = 0; i < q; ++i) {
       long long count = 0, index = 0;
       rc = train_candidates_meta(ctx, tp[i], tn[i], nullptr, nullptr, &count, &index);
@@ -224,9 +235,13 @@ int exhaustive_optimum(gp_ctx* ctx, int window, gp_exhaustive_result* out, int32
       out->train_candidates += count;
     }
     // rollout side: configs, brute MILP, weight sync
+    ph[1] += since(t0);
+    t0 = now();
     std::vector<std::vector<gp_config>> cfgs;
     rc = configs_batch(ctx, q, rp.data(), rn.data(), &ro, cfgs);
     if (rc) return rc;
+    ph[2] += since(t0);
+    t0 = now();
     std::vector<int> live;
     std::vector<const std::vector<gp_config>*> bc;
     std::vector<std::vector<int32_t>> caps;
@@ -249,6 +264,8 @@ int exhaustive_optimum(gp_ctx* ctx, int window, gp_exhaustive_result* out, int32
     std::vector<BruteOut> bo;
     rc = brute_batch(ctx, (int)live.size(), bc, capp, Bs, ctx->work.mean_len, counts, bo);
     if (rc) return rc;
+    ph[3] += since(t0);
+    t0 = now();
     std::vector<int> wl;
     std::vector<const int32_t*> wt, wr, wet, wer;
     std::vector<int32_t> wtn, wrn, wne;
@@ -277,6 +294,7 @@ int exhaustive_optimum(gp_ctx* ctx, int window, gp_exhaustive_result* out, int32
     rc = weight_sync_batch(ctx, (int)wl.size(), wt.data(), wtn.data(), wr.data(), wrn.data(), wet.data(),
                            wer.data(), wne.data(), window, upd.data());
     if (rc) return rc;
+    ph[4] += since(t0);
     // selection in mask order (tests/oracles.cpp:196-207)
     for (size_t k = 0; k < wl.size(); ++k) {
       const int j = wl[k], i = live[j];
@@ -297,6 +315,9 @@ int exhaustive_optimum(gp_ctx* ctx, int window, gp_exhaustive_result* out, int32
     }
     out->partitions += q;
   }
+  if (std::getenv("GPLAN_PROFILE"))
+    std::fprintf(stderr, "exhaustive: train %.3f s, candidate counts %.3f s, configs %.3f s, brute MILP %.3f s, "
+                 "weight sync %.3f s\n", ph[0], ph[1], ph[2], ph[3], ph[4]);
   out->feasible = have_c || have;
   out->objective = have_c ? best_c : best;
   const long long m = have_c ? best_mask_c : best_mask;

@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(256) k2a_block_stats(const int* __restrict__ o
                                                        const double* __restrict__ dflops,
                                                        const double* __restrict__ dcap,
                                                        const double* __restrict__ links, int N,
-                                                       int L, int mb, double* fd_coef) {
+                                                       int L, int mb, double* fd_coef,
+                                                       double2* __restrict__ blkf) {
   __shared__ double red[32];
   __shared__ BlockRec rec;
   const BlockMeta m = meta[blockIdx.x];
@@ -216,7 +217,10 @@ __global__ void __launch_bounds__(256) k2a_block_stats(const int* __restrict__ o
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) out[blockIdx.x] = rec;
+  if (threadIdx.x == 0) {
+    out[blockIdx.x] = rec;
+    blkf[blockIdx.x] = make_double2(rec.flops, rec.lf_num);  // K1's (flops, L*f) view
+  }
 }
 
 // ------------------------------------------------------------ K2b transfers
@@ -1566,21 +1570,42 @@ namespace {
 struct CandMeta {
   const HostSpace* h;
   const gp_ctx* ctx;
-  // options of the block [a, b) (position indices) of run r
-  int w(int r, int a, int b, int* tps = nullptr) const {
-    const int* P = h->pos.data() + h->pos_off[r];
-    const int s0 = h->run_start[r] + P[a], s1 = h->run_start[r] + P[b];
-    int per_machine = 0, run = 0;
-    for (int i = s0; i < s1; ++i) {
-      run = (i > s0 && ctx->h_machine[h->ordered[i]] == ctx->h_machine[h->ordered[i - 1]]) ? run + 1 : 1;
-      per_machine = std::max(per_machine, run);
-    }
-    int n = 0;
-    for (int tp = 1; tp <= 8; tp *= 2)
-      if (tp <= per_machine && (s1 - s0) % tp == 0) {
-        if (tps) tps[n] = tp;
-        ++n;
+  std::vector<std::vector<int>> wt;  // per run: options of block [a, b), (nc+2)^2 table
+  std::vector<std::vector<int>> tps;  // per run: option tp values, 4 per block
+  void init() {
+    const TrainSpace& sp = h->sp;
+    wt.assign(sp.R, {});
+    tps.assign(sp.R, {});
+    for (int r = 0; r < sp.R; ++r) {
+      const int e = sp.nc[r] + 2;
+      const int* P = h->pos.data() + h->pos_off[r];
+      wt[r].assign(e * e, 0);
+      tps[r].assign(e * e * 4, 0);
+      for (int a = 0; a + 1 < e; ++a) {
+        // per-machine run lengths of the blocks starting at a, extended one position at a time
+        int per_machine = 0, run = 0;
+        const int s0 = h->run_start[r] + P[a];
+        int i = s0;
+        for (int b = a + 1; b < e; ++b) {
+          const int s1 = h->run_start[r] + P[b];
+          for (; i < s1; ++i) {
+            run = (i > s0 && ctx->h_machine[h->ordered[i]] == ctx->h_machine[h->ordered[i - 1]]) ? run + 1 : 1;
+            per_machine = std::max(per_machine, run);
+          }
+          int n = 0;
+          for (int tp = 1; tp <= 8; tp *= 2)
+            if (tp <= per_machine && (s1 - s0) % tp == 0) tps[r][(a * e + b) * 4 + n++] = tp;
+          wt[r][a * e + b] = n;
+        }
       }
+    }
+  }
+  // options of the block [a, b) (position indices) of run r
+  int w(int r, int a, int b, int* tp_out = nullptr) const {
+    const int e = h->sp.nc[r] + 2;
+    const int n = wt[r][a * e + b];
+    if (tp_out)
+      for (int j = 0; j < n; ++j) tp_out[j] = tps[r][(a * e + b) * 4 + j];
     return n;
   }
   // sum over cut combinations of run r with k blocks of the product of block weights
@@ -1609,7 +1634,8 @@ int train_candidates_meta(gp_ctx* ctx, const int32_t* ids, int n, const gp_train
   int rc = build_space(ctx, ids, n, &o, h);
   if (rc) return rc;
   const TrainSpace& sp = h.sp;
-  CandMeta cm{&h, ctx};
+  CandMeta cm{&h, ctx, {}, {}};
+  cm.init();
   std::vector<std::vector<long long>> W(sp.R + 1, std::vector<long long>(sp.max_stages + 2, 0));
   std::vector<std::vector<long long>> Gk(sp.R, std::vector<long long>(kMaxPerRun + 1, 0));
   for (int r = 0; r < sp.R; ++r)
@@ -1683,10 +1709,6 @@ int train_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, 
   return GP_OK;
 }
 
-__global__ void k_extract_blkf(const BlockRec* __restrict__ blk, int nblk, double2* __restrict__ blkf) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nblk) blkf[i] = make_double2(blk[i].flops, blk[i].lf_num);
-}
 
 // A train set whose enumeration metadata is resident on the device
 // (gp_train_prepare); gp_train_launch builds the K2 tables and scans a range.
@@ -1879,7 +1901,8 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   const char* generic_env = std::getenv("GPLAN_K1_GENERIC");
   // (layer counts are tabulated as signed bytes: L <= 127)
   const int nlast = (h.sp.nc[h.sp.R - 1] + 2) * (h.sp.nc[h.sp.R - 1] + 1) / 2;
-  const bool fast = h.exact_total && ctx->sc.L <= 127 && nlast <= kMaxLastBlocks &&
+  // (small spaces: the generic scan; the fast path's extra table launches would dominate)
+  const bool fast = h.exact_total && h.total >= (1LL << 20) && ctx->sc.L <= 127 && nlast <= kMaxLastBlocks &&
                     h.sp.nc[h.sp.R - 1] + 2 <= kMaxJunction && !force_generic &&
                     !(generic_env && generic_env[0] == '1');
   if (fast && !ctx->d_slow)
@@ -1888,7 +1911,7 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   // ---- K2: per-train-set tables
   k2a_block_stats<<<h.nblk, 256, 0, stream>>>(P.d_ordered, P.d_meta, P.d_pos, tb, P.d_blk, ctx->d_type,
                                               ctx->d_machine, ctx->d_flops, ctx->d_hbm_cap, ctx->d_links,
-                                              ctx->N, L, ctx->sc.mb, P.d_fd);
+                                              ctx->N, L, ctx->sc.mb, P.d_fd, P.d_blkf);
   ctx->launches++;
   if (!h.items.empty()) {
     const int warps_per_block = 8;
@@ -1902,10 +1925,9 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
     const long long cnt = (long long)h.nblk * L;
     k2c_stage_table<<<(int)((cnt + 255) / 256), 256, 0, stream>>>(P.d_blk, h.nblk, ctx->sc, ctx->d_ceff,
                                                                  P.mode, P.d_stage, P.d_opt);
-    k_extract_blkf<<<(h.nblk + 255) / 256, 256, 0, stream>>>(P.d_blk, h.nblk, P.d_blkf);
     const int ns = (int)h.choices.size();
     k2d_suffix_table<<<(ns + 255) / 256, 256, 0, stream>>>(P.d_choices, ns, h.sp, P.d_tin, P.d_suf);
-    ctx->launches += 3;
+    ctx->launches += 2;
     if (fast) {
       k2e_block_shares<<<(h.nblk + 255) / 256, 256, 0, stream>>>(P.d_blkf, h.nblk, h.flops_total, P.d_blk_sh);
       GP_CUDA(cudaMemsetAsync(P.d_nzs_max, 0, sizeof(int), stream));
