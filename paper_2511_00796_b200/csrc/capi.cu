@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "gp_internal.h"
 
@@ -228,6 +229,27 @@ int gp_ctx_create(const gp_cluster* c, const gp_workload* w, const gp_calib* k, 
   UP(ctx->d_tflops, c->type_flops, T, double);
   UP(ctx->d_thbm, c->type_hbm_bw, T, double);
   UP(ctx->d_tcap, c->type_hbm_cap, T, double);
+  {  // machine-structured links? (exact check over every ordered device pair)
+    const int M = ctx->M;
+    std::vector<double> ml((size_t)M * M, 0.0);
+    std::vector<char> seen((size_t)M * M, 0);
+    const char* dl = std::getenv("GPLAN_DEVICE_LINKS");  // force the device-level path (tests)
+    bool ok = M > 0 && !(dl && dl[0] == '1');
+    for (int a = 0; a < N && ok; ++a)
+      for (int b = 0; b < N; ++b) {
+        if (a == b) continue;
+        const size_t slot = (size_t)c->device_machine[a] * M + c->device_machine[b];
+        const double v = c->links[(size_t)a * N + b];
+        if (!seen[slot]) {
+          seen[slot] = 1;
+          ml[slot] = v;
+        } else if (std::memcmp(&ml[slot], &v, sizeof v) != 0) {
+          ok = false;
+          break;
+        }
+      }
+    if (ok) UP(ctx->d_mlinks, ml.data(), (size_t)M * M, double);
+  }
 #undef UP
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(set_error(GP_CUDA_ERROR, "cudaStreamCreate failed"));
@@ -253,7 +275,7 @@ void gp_ctx_destroy(gp_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* ptrs[] = {ctx->d_type, ctx->d_machine, ctx->d_flops, ctx->d_hbm_bw, ctx->d_hbm_cap,
                   ctx->d_links, ctx->d_ceff, ctx->d_ioeff, ctx->d_tflops, ctx->d_thbm,
-                  ctx->d_tcap,   ctx->scratch_arena[0], ctx->scratch_arena[1],
+                  ctx->d_tcap,   ctx->d_mlinks, ctx->scratch_arena[0], ctx->scratch_arena[1],
                   ctx->scratch_arena[2], ctx->scratch_arena[3]};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -85,6 +85,13 @@ constexpr int kMsStride = 32;  // bytes per suffix choice in TrainTables::sf_ms
 // Device-side training tables of one train set.
 struct TrainTables {
   const int* ordered;
+  // machine groups of the canonical order (consecutive devices on one machine): group of
+  // each position, first position of each group (+ end), machine id of each group
+  const int* mgrp;
+  const int* gstart;
+  const int* gmach;
+  const double* mlinks;  // [M * M] or nullptr (device-level links)
+  int M;
   const int* pos;        // per run: positions [0, cuts..., len], offsets = pos_off
   const BlockRec* blk;
   const double2* stage;  // [nblk * L] (total, compute); total = +inf => memory-infeasible
@@ -143,6 +150,9 @@ struct gp_ctx {
   double* d_hbm_bw = nullptr;
   double* d_hbm_cap = nullptr;
   double* d_links = nullptr;
+  // machine-pair link table, set when every link(a != b) depends only on (machine(a),
+  // machine(b)) — certified at context creation; K2a/K2b then take minima over machines
+  double* d_mlinks = nullptr;
   double* d_ceff = nullptr;
   double* d_ioeff = nullptr;
   double* d_tflops = nullptr;

@@ -186,6 +186,48 @@ __global__ void __launch_bounds__(256) k2a_block_stats(const int* __restrict__ o
     const int tp = 1 << o;
     if (tp > per_machine || n % tp != 0) continue;  // tp_dp_options (src/train_search.cpp:74-93)
     const int dp = n / tp;
+    if (tb.mlinks) {  // machine-structured links: minima over machine-group pairs
+      // a pair (earlier, later) of distinct devices has link mlinks[m(earlier)][m(later)];
+      // groups are in canonical (machine) order, so earlier devices sit in groups <= later
+      if (tp > 1) {
+        double mn = kInf;
+        for (int c = threadIdx.x; c < n / tp; c += blockDim.x) {
+          const int p0 = start + c * tp, p1 = p0 + tp;  // chunk [p0, p1)
+          const int ga = tb.mgrp[p0], gb = tb.mgrp[p1 - 1];
+          for (int g = ga; g <= gb; ++g)
+            for (int h = g; h <= gb; ++h) {
+              if (g == h) {
+                const int cnt = min(p1, tb.gstart[g + 1]) - max(p0, tb.gstart[g]);
+                if (cnt < 2) continue;
+              }
+              mn = dmin(mn, tb.mlinks[(size_t)tb.gmach[g] * tb.M + tb.gmach[h]]);
+            }
+        }
+        mn = block_min(mn, red);
+        if (threadIdx.x == 0) rec.beta_tp[o] = mn;
+      }
+      if (dp > 1) {  // stride-tp groups: devices start + g + i*tp, i < dp
+        double mn = kInf;
+        const int ga = tb.mgrp[start], K = tb.mgrp[start + n - 1] - ga + 1;
+        auto cnt = [&](int g, int k) {  // devices of stride group g on machine group k
+          const int x0 = tb.gstart[k] - start - g, x1 = tb.gstart[k + 1] - start - g;
+          const int lo = x0 <= 0 ? 0 : (x0 + tp - 1) / tp;
+          const int hi = x1 <= 0 ? 0 : min(dp, (x1 + tp - 1) / tp);
+          return hi > lo ? hi - lo : 0;
+        };
+        for (int idx = threadIdx.x; idx < tp * K * K; idx += blockDim.x) {
+          const int g = idx / (K * K), rem = idx % (K * K);
+          const int k = ga + rem / K, k2 = ga + rem % K;
+          if (k2 < k) continue;
+          const int c1 = cnt(g, k);
+          if (k == k2 ? c1 < 2 : (c1 == 0 || cnt(g, k2) == 0)) continue;
+          mn = dmin(mn, tb.mlinks[(size_t)tb.gmach[k] * tb.M + tb.gmach[k2]]);
+        }
+        mn = block_min(mn, red);
+        if (threadIdx.x == 0) rec.beta_dp[o] = mn;
+      }
+      continue;
+    }
     if (tp > 1) {  // consecutive chunks of tp devices
       double mn = kInf;
       const int pairs_per = tp * (tp - 1) / 2;
@@ -253,10 +295,19 @@ __global__ void __launch_bounds__(256) k2b_transfers(const int* __restrict__ ord
     n2 = P2[-it.w];
   }
   double mn = kInf;
-  const long long tot = (long long)n1 * n2;
-  for (long long p = lane; p < tot; p += 32) {
-    const int i = (int)(p / n2), j = (int)(p - (long long)i * n2);
-    mn = dmin(mn, links[(size_t)ordered[s1 + i] * N + ordered[s2 + j]]);
+  if (tb.mlinks) {  // machine-structured links: the minimum over the machine pairs
+    const int ga = tb.mgrp[s1], gb = tb.mgrp[s1 + n1 - 1], ha = tb.mgrp[s2], hb = tb.mgrp[s2 + n2 - 1];
+    const int k2 = hb - ha + 1, tot = (gb - ga + 1) * k2;
+    for (int p = lane; p < tot; p += 32) {
+      const int g = ga + p / k2, h = ha + p % k2;
+      mn = dmin(mn, tb.mlinks[(size_t)tb.gmach[g] * tb.M + tb.gmach[h]]);
+    }
+  } else {
+    const long long tot = (long long)n1 * n2;
+    for (long long p = lane; p < tot; p += 32) {
+      const int i = (int)(p / n2), j = (int)(p - (long long)i * n2);
+      mn = dmin(mn, links[(size_t)ordered[s1 + i] * N + ordered[s2 + j]]);
+    }
   }
   mn = warp_min(mn);
   if (lane == 0) {
@@ -1325,6 +1376,7 @@ struct HostSpace {
   int nblk = 0, tin_size = 0, tx_size = 0;
   long long total = 0;
   long long n_prefix = 0;
+  std::vector<int> mgrp, gstart, gmach;  // machine groups of the canonical order
   bool exact_total = false;  // every partial FLOPS sum exact: K1-fast applies
   double flops_total = 0;    // allocate_layers' total (the same for every layout when exact)
 };
@@ -1423,6 +1475,15 @@ int build_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, 
     }
   }
   h.exact_total = exact_flops_total(ctx, h.ordered, &h.flops_total);
+  h.mgrp.resize(n);
+  for (int i = 0; i < n; ++i) {
+    if (i == 0 || ctx->h_machine[h.ordered[i]] != ctx->h_machine[h.ordered[i - 1]]) {
+      h.gstart.push_back(i);
+      h.gmach.push_back(ctx->h_machine[h.ordered[i]]);
+    }
+    h.mgrp[i] = (int)h.gstart.size() - 1;
+  }
+  h.gstart.push_back(n);
   const bool any = sp.max_stages >= sp.R;
   h.total = any ? sp.cnt[0][0] : 0;
   h.n_prefix = any ? sp.cntP[0][0] : 0;
@@ -1720,6 +1781,9 @@ struct PreparedTrain {
   BlockMeta* d_meta = nullptr;
   int4* d_items = nullptr;
   int4* d_choices = nullptr;
+  int* d_mgrp = nullptr;
+  int* d_gstart = nullptr;
+  int* d_gmach = nullptr;
   BlockRec* d_blk = nullptr;
   double2* d_blkf = nullptr;
   double2* d_stage = nullptr;
@@ -1787,6 +1851,9 @@ static size_t input_bytes(const HostSpace& h) {
   add(sizeof(BlockMeta) * h.meta.size());
   add(sizeof(int4) * h.items.size());
   add(sizeof(int4) * h.choices.size());
+  add(sizeof(int) * h.mgrp.size());
+  add(sizeof(int) * h.gstart.size());
+  add(sizeof(int) * h.gmach.size());
   return bytes;
 }
 
@@ -1832,6 +1899,12 @@ static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_bas
   stage(h.items.data(), sizeof(int4) * h.items.size(), P.d_items);
   P.d_choices = carve<int4>(in, h.choices.size());
   stage(h.choices.data(), sizeof(int4) * h.choices.size(), P.d_choices);
+  P.d_mgrp = carve<int>(in, h.mgrp.size());
+  stage(h.mgrp.data(), sizeof(int) * h.mgrp.size(), P.d_mgrp);
+  P.d_gstart = carve<int>(in, h.gstart.size());
+  stage(h.gstart.data(), sizeof(int) * h.gstart.size(), P.d_gstart);
+  P.d_gmach = carve<int>(in, h.gmach.size());
+  stage(h.gmach.data(), sizeof(int) * h.gmach.size(), P.d_gmach);
   P.d_blk = carve<BlockRec>(tab, h.nblk);
   P.d_blkf = carve<double2>(tab, h.nblk);
   P.d_stage = carve<double2>(tab, (size_t)h.nblk * P.L);
@@ -1882,6 +1955,11 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   const int L = ctx->sc.L;
   TrainTables tb{};
   tb.ordered = P.d_ordered;
+  tb.mgrp = P.d_mgrp;
+  tb.gstart = P.d_gstart;
+  tb.gmach = P.d_gmach;
+  tb.mlinks = ctx->d_mlinks;
+  tb.M = ctx->M;
   tb.pos = P.d_pos;
   tb.blk = P.d_blk;
   tb.stage = P.d_stage;

@@ -185,3 +185,21 @@ def test_fast_scan_equals_generic_scan(monkeypatch):
         generic = run(name, ids, 3, lo=lo, hi=hi)
         monkeypatch.delenv("GPLAN_K1_GENERIC")
         assert fast == generic, name
+
+
+def test_device_level_links_path(monkeypatch):
+    """K2a/K2b over device pairs (GPLAN_DEVICE_LINKS=1) == over machine pairs (default,
+    certified at context creation) == the oracle."""
+    from paper_2511_00796_b200.engine import Engine
+    name = "c3_64gpu"
+    p = problem(name)
+    orc = Oracle(p)
+    monkeypatch.setenv("GPLAN_DEVICE_LINKS", "1")
+    dev_level = Engine(p)
+    monkeypatch.delenv("GPLAN_DEVICE_LINKS")
+    sets = [s for s in random_train_sets(p.cluster.n, 30, seed=2024) if orc.train_space(s) <= 100_000][:8]
+    for ids in sets:
+        want = orc.constrained_search(ids, 3)
+        r, d = dev_level.constrained_search_raw(ids, 3)
+        assert train_result_dict(r, d) == want, ids
+        assert run(name, ids, 3) == want, ids
