@@ -110,7 +110,8 @@ struct TrainTables {
   const double* sf_t;     // [3][n_suf] internal stage-transfer terms
   const signed char* sf_ms;  // [n_suf][kMsStride]: largest layer count at (b, d donations), -1: none
   const double2* sf_st;   // [5 * (kDonations + 1)][n_suf]: (max total, max compute) at (b, d)
-  const int* nzs_max;     // most zero-layer stages of any suffix choice
+  const int* nzs_max;     // suffix stats: [0] most zero-layer stages of any suffix choice,
+                          //   [1] kFsBias - smallest floor sum, [2] largest floor sum
   int pos_off[GP_MAX_TYPES];
 };
 

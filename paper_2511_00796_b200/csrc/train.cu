@@ -743,6 +743,8 @@ __global__ void k2e_block_shares(const double2* __restrict__ blkf, int nblk, dou
   out[i] = make_double2(share - fl, (double)fl);
 }
 
+constexpr int kFsBias = 1 << 20;  // suffix-stats encoding of the smallest floor sum
+
 // Per suffix choice: the fast-path tables (TrainTables::sf_*) and, per promotion count b and
 // donation count d, the (max total, max compute) of its stages — zero-layer stages counted
 // with the one layer the fix-up gives them, donors with the layers they keep.
@@ -829,6 +831,8 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
 #pragma unroll
   for (int b = 0; b < 4; ++b) zmax = max(zmax, (int)((nzs >> (8 * b)) & 0xff));
   atomicMax(nzs_max, zmax);
+  atomicMax(nzs_max + 1, kFsBias - fs);  // suffix floor-sum range: min via the bias
+  atomicMax(nzs_max + 2, fs);
 }
 
 constexpr int kK1Threads = 128;
@@ -910,7 +914,7 @@ __device__ __forceinline__ void prefix_data_warp(int lane, const TrainSpace& sp,
 // tables of the warp's prefix.
 template <int R>
 __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, const TrainTables& tb, int L,
-                                            int nzs_max, PrefixData<R>& D, PrefixFast<R>& F,
+                                            int3 sstat, PrefixData<R>& D, PrefixFast<R>& F,
                                             unsigned char* cntb, double* txs) {
   const int sp_nc_last = sp.nc[R - 1], blk_off_last = sp.blk_off[R - 1];
   constexpr int NP = PrefixData<R>::NP;
@@ -970,9 +974,16 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
   // per promotion count a (one lane each): the layer counts, then up to dm water-filling
   // donations (dm = the most fix-ups a candidate of this prefix can need), recording the
   // stage maxima and the largest layer count of every state
+  // only the promotion counts a candidate can reach: extra = L - fp - fs with the suffix
+  // floor sum fs in [fs_min, fs_max] and a = extra - b, b in [0, 4]
   const int kp = D.u;
-  if (lane <= kp) {
-    const int a = lane;
+  const int nzs_max = sstat.x, fs_min = kFsBias - sstat.y, fs_max = sstat.z;
+  int fp_all = 0;
+#pragma unroll
+  for (int q = 0; q < NP; ++q) fp_all += F.fl[q];
+  const int a_lo = max(0, L - fp_all - fs_max - 4), a_hi = min(kp, L - fp_all - fs_min);
+  if (lane <= a_hi - a_lo) {
+    const int a = a_lo + lane;
     int lay[PrefixFast<R>::NQ];
     int nz = 0;
     bool over = false;
@@ -1160,7 +1171,7 @@ __global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace 
   PrefixData<R>& D = sD[threadIdx.x >> 5];
   PrefixFast<R>& F = sF[threadIdx.x >> 5];
   const int e2 = sp.nc[R - 1] + 2;
-  const int nzs_max = *tb.nzs_max;
+  const int3 sstat = make_int3(tb.nzs_max[0], tb.nzs_max[1], tb.nzs_max[2]);
   __shared__ PrefixLast sL[kK1Threads / 32];
   __shared__ double fd[GP_MAX_STAGES + 1];
   unsigned char* const cntb = sL[threadIdx.x >> 5].cntb;
@@ -1175,7 +1186,7 @@ __global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace 
     for (; p < p_end; ++p) {
       __syncwarp();
       prefix_data_warp<R>(lane, sp, tb, P, D, F);
-      prefix_fast<R>(lane, sp, tb, L, nzs_max, D, F, cntb, txs);
+      prefix_fast<R>(lane, sp, tb, L, sstat, D, F, cntb, txs);
       const int kp = D.u;
       const int fp = F.fp, pbad = F.bad;
       const double dtr = D.transfers;
@@ -1875,7 +1886,7 @@ static size_t table_bytes(const HostSpace& h, int L, int max_blocks) {
   add(sizeof(double) * 3 * nsf);
   add((size_t)kMsStride * nsf);
   add(sizeof(double2) * 5 * (kDonations + 1) * nsf);
-  add(sizeof(int));
+  add(sizeof(int) * 3);
   add(sizeof(NearMin) * (max_blocks + kDeferBlocks));
   return bytes;
 }
@@ -1920,7 +1931,7 @@ static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_bas
   P.d_sf_t = carve<double>(tab, 3 * nsf);
   P.d_sf_ms = carve<signed char>(tab, (size_t)kMsStride * nsf);
   P.d_sf_st = carve<double2>(tab, 5 * (kDonations + 1) * nsf);
-  P.d_nzs_max = carve<int>(tab, 1);
+  P.d_nzs_max = carve<int>(tab, 3);
   P.d_partial = carve<NearMin>(tab, P.max_blocks + kDeferBlocks);
 }
 
@@ -2008,7 +2019,7 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
     ctx->launches += 2;
     if (fast) {
       k2e_block_shares<<<(h.nblk + 255) / 256, 256, 0, stream>>>(P.d_blkf, h.nblk, h.flops_total, P.d_blk_sh);
-      GP_CUDA(cudaMemsetAsync(P.d_nzs_max, 0, sizeof(int), stream));
+      GP_CUDA(cudaMemsetAsync(P.d_nzs_max, 0, 3 * sizeof(int), stream));
       k2f_suffix_fast<<<(ns + 127) / 128, 128, 0, stream>>>(P.d_suf, ns, P.d_blk_sh, P.d_stage, L,
                                                            h.sp.blk_off[h.sp.R - 1], P.d_sf_hot, P.d_sf_zb,
                                                            P.d_sf_t, P.d_sf_ms, P.d_sf_st, P.d_nzs_max);
