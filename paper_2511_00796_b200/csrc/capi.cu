@@ -283,6 +283,12 @@ void gp_ctx_destroy(gp_ctx* ctx) {
   train_state_free(ctx);
   train_memo_free(ctx);
   if (ctx->d_slow) cudaFree(ctx->d_slow);
+  for (int l = 0; l < gp_ctx::kTrainLanes; ++l) {
+    if (ctx->d_slow_lane[l]) cudaFree(ctx->d_slow_lane[l]);
+    if (ctx->lane[l]) cudaStreamDestroy(ctx->lane[l]);
+  }
+  for (auto& e : ctx->ev_lane)
+    if (e) cudaEventDestroy(e);
   milp_cache_free(ctx);
   part_cache_free(ctx);
   for (auto& e : ctx->ev)

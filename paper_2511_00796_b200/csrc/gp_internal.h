@@ -176,6 +176,11 @@ struct gp_ctx {
   void* part_cache[2] = {nullptr, nullptr};  // partition unit tables per granularity (partition.cu)
   // K1-fast's deferred generic candidates: [0] = count, then keys (train.cu)
   unsigned long long* d_slow = nullptr;
+  // train_batch runs its train sets on kTrainLanes streams (each with its own queue)
+  static constexpr int kTrainLanes = 4;
+  cudaStream_t lane[kTrainLanes] = {};
+  unsigned long long* d_slow_lane[kTrainLanes] = {};
+  cudaEvent_t ev_lane[kTrainLanes + 1] = {};
   // constrained_search results per train set, window-independent (train.cu TrainMemo)
   void* train_memo = nullptr;
   bool memo = true;

@@ -1591,7 +1591,8 @@ T* carve(char*& p, size_t count) {
 template <int R>
 int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const double2* blkf,
                 const BlockRec* blk, int window, long long lo, long long hi, NearMin* partial,
-                int max_blocks, TrainOut* d_out, cudaStream_t stream, bool fast, int mode) {
+                int max_blocks, TrainOut* d_out, cudaStream_t stream, bool fast, int mode,
+                unsigned long long* slow_q) {
   ScanRange rg{};
   rank_split(h, lo, rg.p_lo, rg.s_lo);
   rank_split(h, hi, rg.p_hi, rg.s_hi);
@@ -1612,10 +1613,10 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   int n_partial = (int)blocks;
   if (hi > lo) {
     if (fast) {
-      GP_CUDA(cudaMemsetAsync(ctx->d_slow, 0, sizeof(unsigned long long), stream));
+      GP_CUDA(cudaMemsetAsync(slow_q, 0, sizeof(unsigned long long), stream));
       k1_layout_scan_fast<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial,
-                                                                  ctx->d_slow);
-      k1_deferred<R><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, ctx->d_slow,
+                                                                  slow_q);
+      k1_deferred<R><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, slow_q,
                                                             partial + blocks);
       n_partial += kDeferBlocks;
       ctx->launches += 2;
@@ -1627,7 +1628,7 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
     n_partial = 0;
   }
   k1_finalize<R><<<1, 256, 0, stream>>>(h.sp, tb, blkf, blk, ctx->sc.L, window, partial, n_partial, d_out,
-                                        fast && hi > lo ? ctx->d_slow : nullptr, ctx->sc, ctx->d_ceff, mode);
+                                        fast && hi > lo ? slow_q : nullptr, ctx->sc, ctx->d_ceff, mode);
   ctx->launches++;
   GP_CUDA(cudaGetLastError());
   return GP_OK;
@@ -1953,7 +1954,7 @@ static double sum_stages(const HostSpace& h) {
 
 // Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
 static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long lo, long long hi,
-                           cudaStream_t stream, bool timing, bool force_generic = false) {
+                           cudaStream_t stream, bool timing, bool force_generic = false, int lane = -1) {
   const HostSpace& h = P.h;
   if (lo < 0) lo = 0;
   if (hi < 0 || hi > h.total) hi = h.total;
@@ -1994,8 +1995,8 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   const bool fast = h.exact_total && h.total >= (1LL << 20) && ctx->sc.L <= 127 && nlast <= kMaxLastBlocks &&
                     h.sp.nc[h.sp.R - 1] + 2 <= kMaxJunction && !force_generic &&
                     !(generic_env && generic_env[0] == '1');
-  if (fast && !ctx->d_slow)
-    GP_CUDA(cudaMalloc(&ctx->d_slow, sizeof(unsigned long long) * (1 + kSlowQueue)));
+  unsigned long long*& slow_q = lane < 0 ? ctx->d_slow : ctx->d_slow_lane[lane];
+  if (fast && !slow_q) GP_CUDA(cudaMalloc(&slow_q, sizeof(unsigned long long) * (1 + kSlowQueue)));
   if (timing) GP_CUDA(cudaEventRecord(ctx->ev[0], stream));
   // ---- K2: per-train-set tables
   k2a_block_stats<<<h.nblk, 256, 0, stream>>>(P.d_ordered, P.d_meta, P.d_pos, tb, P.d_blk, ctx->d_type,
@@ -2031,10 +2032,10 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   // ---- K1: layout scan over [lo, hi)
   const int R = h.sp.R;
   int rc;
-  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode);
-  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode);
-  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode);
-  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode);
+  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q);
+  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q);
+  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q);
+  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q);
   else rc = set_error(GP_INVALID, "train sets spanning more than 4 gpu types are not supported");
   if (!rc && timing) GP_CUDA(cudaEventRecord(ctx->ev[2], stream));
   return rc;
@@ -2274,9 +2275,22 @@ int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_
   const size_t in_bytes = (size_t)(in - base);
   GP_CUDA(cudaMemcpyAsync(base, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h2d_bytes += (long long)in_bytes;
+  // the sets run on kTrainLanes streams so that small sets overlap on the GPU
+  constexpr int NL = gp_ctx::kTrainLanes;
+  if (!ctx->lane[0]) {
+    for (int l = 0; l < NL; ++l) GP_CUDA(cudaStreamCreateWithFlags(&ctx->lane[l], cudaStreamNonBlocking));
+    for (int l = 0; l <= NL; ++l) GP_CUDA(cudaEventCreateWithFlags(&ctx->ev_lane[l], cudaEventDisableTiming));
+  }
+  GP_CUDA(cudaEventRecord(ctx->ev_lane[NL], ctx->stream));  // inputs are on the device
+  for (int l = 0; l < NL; ++l) GP_CUDA(cudaStreamWaitEvent(ctx->lane[l], ctx->ev_lane[NL], 0));
   for (int i = 0; i < n_sets; ++i) {
-    int rc = launch_prepared(ctx, Ps[i], window, 0, -1, ctx->stream, false);
+    const int l = i % NL;
+    int rc = launch_prepared(ctx, Ps[i], window, 0, -1, ctx->lane[l], false, false, l);
     if (rc) return rc;
+  }
+  for (int l = 0; l < NL; ++l) {
+    GP_CUDA(cudaEventRecord(ctx->ev_lane[l], ctx->lane[l]));
+    GP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_lane[l], 0));
   }
   TrainOut* ho = reinterpret_cast<TrainOut*>(hp);
   GP_CUDA(cudaMemcpyAsync(ho, d_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
