@@ -29,6 +29,8 @@
 #include <numeric>
 #include <string>
 #include <unordered_map>
+#include <thread>
+#include <array>
 
 #include "gp_internal.h"
 
@@ -2222,34 +2224,15 @@ int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_tr
 // Batched constrained_search over many train sets (the scheduler's evaluation batches):
 // every set's inputs travel in ONE H2D copy, all tables + scans are enqueued back to back,
 // the results come back in ONE D2H copy with ONE synchronisation.
-int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
-                const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices, int mode) {
+// Scans every set on ctx (no memo): one H2D, all launches on the lane streams, one D2H.
+// Returns per set the NearMin summary and the canonical device order for the memo.
+static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
+                           const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices,
+                           int mode, std::vector<std::array<long long, 4>>& nms,
+                           std::vector<std::vector<int32_t>>& ordered) {
+  nms.assign(n_sets, {});
+  ordered.assign(n_sets, {});
   if (n_sets <= 0) return GP_OK;
-  // answered from the memo where possible; the rest is scanned in one batch
-  std::vector<std::string> keys(n_sets);
-  std::vector<int> todo;
-  for (int i = 0; i < n_sets; ++i) {
-    keys[i] = train_memo_key(ids[i], ns[i], o, mode);
-    if (!train_memo_get(ctx, keys[i], window, outs + i, stage_devices ? stage_devices[i] : nullptr))
-      todo.push_back(i);
-  }
-  if (todo.empty()) return GP_OK;
-  if ((int)todo.size() < n_sets) {
-    std::vector<const int32_t*> ids2;
-    std::vector<int32_t> ns2;
-    std::vector<gp_train_result> outs2(todo.size());
-    std::vector<int32_t*> sd2;
-    for (int i : todo) {
-      ids2.push_back(ids[i]);
-      ns2.push_back(ns[i]);
-      sd2.push_back(stage_devices ? stage_devices[i] : nullptr);
-    }
-    int rc = train_batch(ctx, (int)todo.size(), ids2.data(), ns2.data(), window, o, outs2.data(),
-                         stage_devices ? sd2.data() : nullptr, mode);
-    if (rc) return rc;
-    for (size_t j = 0; j < todo.size(); ++j) outs[todo[j]] = outs2[j];
-    return GP_OK;
-  }
   std::vector<PreparedTrain> Ps(n_sets);
   size_t ib = 0, tbytes = 0;
   for (int i = 0; i < n_sets; ++i) {
@@ -2307,11 +2290,98 @@ int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_
   for (int i = 0; i < n_sets; ++i) {
     const bool ran = Ps[i].h.total > 0;
     fill_result(Ps[i], ran ? ho + i : nullptr, outs + i, stage_devices ? stage_devices[i] : nullptr);
-    train_memo_put(ctx, keys[i], outs[i], Ps[i].h.ordered.data(), Ps[i].h.sp.n, Ps[i].nm);
+    for (int k = 0; k < 4; ++k) nms[i][k] = Ps[i].nm[k];
+    ordered[i] = Ps[i].h.ordered;
     g_memo_stats.scans++;
     g_memo_stats.layouts += Ps[i].h.total;
   }
   g_memo_stats.poll();
+  return GP_OK;
+}
+
+// Batched constrained_search over many train sets (the scheduler's evaluation batches):
+// memo hits are answered on the host; the rest is scanned by train_batch_run — split over
+// the context's devices (gp_ctx_create_multi) by layout count when it has peers.
+int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
+                const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices, int mode) {
+  if (n_sets <= 0) return GP_OK;
+  std::vector<std::string> keys(n_sets);
+  std::vector<int> todo;
+  for (int i = 0; i < n_sets; ++i) {
+    keys[i] = train_memo_key(ids[i], ns[i], o, mode);
+    if (!train_memo_get(ctx, keys[i], window, outs + i, stage_devices ? stage_devices[i] : nullptr))
+      todo.push_back(i);
+  }
+  if (todo.empty()) return GP_OK;
+  const int q = (int)todo.size();
+  std::vector<std::array<long long, 4>> nms(q);
+  std::vector<std::vector<int32_t>> ordered(q);
+  std::vector<gp_train_result> res(q);
+  std::vector<int> dev_of(q, 0);
+  const int D = 1 + (int)ctx->peers.size();
+  if (D > 1 && q > 1) {  // longest-processing-time assignment by layout count
+    std::vector<std::pair<long long, int>> sz(q);
+    for (int j = 0; j < q; ++j) {
+      int64_t total = 0;
+      int rc = train_space(ctx, ids[todo[j]], ns[todo[j]], o, &total);
+      if (rc) return rc;
+      sz[j] = {(long long)total, j};
+    }
+    std::sort(sz.begin(), sz.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+    std::vector<long long> load(D, 0);
+    for (const auto& e : sz) {
+      const int d = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      dev_of[e.second] = d;
+      load[d] += e.first + 100000;  // + per-set fixed cost
+    }
+  }
+  std::vector<int> rcs(D, GP_OK);
+  std::vector<std::string> errs(D);
+  std::vector<std::vector<int>> part(D);
+  for (int j = 0; j < q; ++j) part[dev_of[j]].push_back(j);
+  auto run = [&](int d) {
+    gp_ctx* c = d == 0 ? ctx : ctx->peers[d - 1];
+    const std::vector<int>& pj = part[d];
+    if (pj.empty()) return;
+    cudaSetDevice(c->device);
+    std::vector<const int32_t*> id2;
+    std::vector<int32_t> n2;
+    std::vector<int32_t*> sd2;
+    for (int j : pj) {
+      id2.push_back(ids[todo[j]]);
+      n2.push_back(ns[todo[j]]);
+      sd2.push_back(stage_devices ? stage_devices[todo[j]] : nullptr);
+    }
+    std::vector<gp_train_result> r2(pj.size());
+    std::vector<std::array<long long, 4>> nm2;
+    std::vector<std::vector<int32_t>> or2;
+    rcs[d] = train_batch_run(c, (int)pj.size(), id2.data(), n2.data(), window, o, r2.data(),
+                             stage_devices ? sd2.data() : nullptr, mode, nm2, or2);
+    if (rcs[d]) {
+      errs[d] = gp_last_error();
+      return;
+    }
+    for (size_t k = 0; k < pj.size(); ++k) {
+      res[pj[k]] = r2[k];
+      nms[pj[k]] = nm2[k];
+      ordered[pj[k]] = std::move(or2[k]);
+    }
+  };
+  if (D == 1 || q == 1) {
+    run(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int d = 1; d < D; ++d) th.emplace_back(run, d);
+    run(0);
+    for (auto& t : th) t.join();
+    cudaSetDevice(ctx->device);
+  }
+  for (int d = 0; d < D; ++d)
+    if (rcs[d]) return set_error(rcs[d], errs[d].empty() ? std::string("train batch failed") : errs[d]);
+  for (int j = 0; j < q; ++j) {
+    outs[todo[j]] = res[j];
+    train_memo_put(ctx, keys[todo[j]], res[j], ordered[j].data(), (int)ordered[j].size(), nms[j].data());
+  }
   return GP_OK;
 }
 
