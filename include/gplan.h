@@ -240,6 +240,13 @@ int gp_fp64_peak(gp_ctx* ctx, double* dadd_per_s);
 int gp_enumerate_configs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_rollout_opts* opts,
                          gp_config* out, int32_t cap, int32_t* n_out);
 int gp_rollout_capacities(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t* caps);
+/* Many solve_milp instances in one call (the scheduler's evaluation batches): query i has
+ * configs[cfg_off[i] .. cfg_off[i+1]), caps[i*dims ..], total_rollouts[i]; results in
+ * out[i], entries at entries[cfg_off[i] ..], status per query in status[i] (GP_OK,
+ * GP_INFEASIBLE, GP_INVALID). The lattice DPs of all queries run batched. */
+int gp_solve_milp_batch(gp_ctx* ctx, int32_t q, const gp_config* configs, const int32_t* cfg_off,
+                        const int32_t* caps, int32_t dims, const double* total_rollouts, double mean_len,
+                        gp_rollout_result* out, gp_rollout_entry* entries, int32_t* status);
 /* Exact makespan DP. entries must hold n_configs records. B <= 0 -> empty plan. */
 int gp_solve_milp(gp_ctx* ctx, const gp_config* configs, int32_t n_configs, const int32_t* caps,
                   int32_t dims, double total_rollouts, double mean_len, gp_rollout_result* out,

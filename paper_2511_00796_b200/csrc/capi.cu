@@ -37,6 +37,9 @@ int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opt
 int rollout_capacities(gp_ctx* ctx, const int32_t* ids, int n, int32_t* caps);
 int solve_milp(gp_ctx* ctx, const gp_config* cfg, int nc, const int32_t* caps, int dims, double B,
                double len, gp_rollout_result* out, gp_rollout_entry* entries);
+int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs, const int32_t* const* caps,
+               int dims, const double* Bs, double len, gp_rollout_result* outs, gp_rollout_entry* const* entries,
+               int* rcs);
 int weight_sync(gp_ctx* ctx, const int32_t* train, int nt, const int32_t* roll, int nr,
                 const int32_t* etype, const int32_t* erep, int ne, int window, double* out);
 int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, int k, gp_partition* out,
@@ -440,6 +443,30 @@ int gp_solve_milp(gp_ctx* ctx, const gp_config* configs, int32_t n_configs, cons
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return solve_milp(ctx, configs, n_configs, caps, dims, total_rollouts, mean_len, out, entries);
+}
+
+int gp_solve_milp_batch(gp_ctx* ctx, int32_t q, const gp_config* configs, const int32_t* cfg_off,
+                        const int32_t* caps, int32_t dims, const double* total_rollouts, double mean_len,
+                        gp_rollout_result* out, gp_rollout_entry* entries, int32_t* status) {
+  if (!ctx) return set_error(GP_INVALID, "null context");
+  if (q < 0 || (q > 0 && (!configs || !cfg_off || !caps || !total_rollouts || !out || !entries || !status)))
+    return set_error(GP_INVALID, "null argument");
+  cudaSetDevice(ctx->device);
+  std::vector<const gp_config*> cp(q);
+  std::vector<int> nc(q);
+  std::vector<const int32_t*> capp(q);
+  std::vector<gp_rollout_entry*> ep(q);
+  std::vector<int> rcs(q);
+  for (int i = 0; i < q; ++i) {
+    cp[i] = configs + cfg_off[i];
+    nc[i] = cfg_off[i + 1] - cfg_off[i];
+    capp[i] = caps + (size_t)i * dims;
+    ep[i] = entries + cfg_off[i];
+  }
+  int rc = milp_batch(ctx, q, cp.data(), nc.data(), capp.data(), dims, total_rollouts, mean_len, out, ep.data(),
+                      rcs.data());
+  for (int i = 0; i < q; ++i) status[i] = rcs[i];
+  return rc;
 }
 
 int gp_weight_sync_cost(gp_ctx* ctx, const int32_t* train, int32_t n_train, const int32_t* rollout,

@@ -187,56 +187,79 @@ __global__ void k4_level_scatter(MilpDims d, const long long* __restrict__ off,
   }
 }
 
-// Persistent cooperative kernel, one warp per state, lanes over the (type, devices) groups:
-// value = max_g best[s - delta_g] + hmax_g; choice = smallest config index c with
+// Lattice DP (k4_dp_multi below): one warp per state, lanes over the (type, devices)
+// groups: value = max_g best[s - delta_g] + hmax_g; choice = smallest config index c with
 // best[prev_g(c)] + h_c == value (src/rollout_milp.cpp:197-225). The lanes' partial
 // (max value, min index) pairs merge exactly in any order. A state at level l reads levels
 // <= l - n_min (n_min = fewest devices of any config), so `step` = n_min consecutive levels
 // form one phase between grid barriers.
-__global__ void __launch_bounds__(256) k4_dp_levels(MilpDims d, const Group* __restrict__ groups_g,
-                                                    int n_groups, const int* __restrict__ members_g,
-                                                    const double* __restrict__ h_g, int n_cfg, int step,
-                                                    const long long* __restrict__ off,
-                                                    const unsigned long long* __restrict__ order,
-                                                    double* __restrict__ best,
-                                                    int* __restrict__ choice) {
-  __shared__ Group groups[kMaxGroups];
-  __shared__ int members[kMaxCfg];
-  __shared__ double h[kMaxCfg];
-  __shared__ int shift[GP_MAX_TYPES];
-  __shared__ unsigned mask[GP_MAX_TYPES];
-  for (int i = threadIdx.x; i < n_groups; i += blockDim.x) groups[i] = groups_g[i];
-  for (int i = threadIdx.x; i < n_cfg; i += blockDim.x) {
-    members[i] = members_g[i];
-    h[i] = h_g[i];
-  }
-  if (threadIdx.x < d.T) {
-    shift[threadIdx.x] = d.off[threadIdx.x];
-    mask[threadIdx.x] = d.mask[threadIdx.x];
-  }
-  __syncthreads();
+// Several lattice tables in one cooperative launch: phase p runs levels
+// [p*step_t, (p+1)*step_t) of every table t (tables are independent), so a scheduler batch
+// pays max_t(phases_t) grid barriers instead of their sum; the tables' group data are read
+// through L1.
+struct DpTable {
+  MilpDims d;
+  int step, n_groups, phases, pad;
+  const Group* groups;
+  const int* members;
+  const double* h;
+  const long long* off;
+  const unsigned long long* order;
+  double* best;
+  int* choice;
+};
+constexpr int kDpMaxTables = 64;
+
+__global__ void __launch_bounds__(256) k4_dp_multi(const DpTable* __restrict__ tabs, int K, int max_phases) {
+  __shared__ long long pre[kDpMaxTables + 1];
+  __shared__ long long beg[kDpMaxTables];
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (int l = 0; l < d.levels; l += step) {
-    const long long e = off[min(l + step, d.levels)];
-    for (long long i = off[l] + warp; i < e; i += n_warps) {
-      const unsigned long long pk = order[i];
+  for (int ph = 0; ph < max_phases; ++ph) {
+    if (threadIdx.x < K) {
+      const DpTable& T = tabs[threadIdx.x];
+      const int l0 = ph * T.step;
+      long long b = 0, c = 0;
+      if (l0 < T.d.levels) {
+        const int l1 = min(l0 + T.step, T.d.levels);
+        b = T.off[l0];
+        c = T.off[l1] - b;
+      }
+      beg[threadIdx.x] = b;
+      pre[threadIdx.x + 1] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      pre[0] = 0;
+      for (int t = 0; t < K; ++t) pre[t + 1] += pre[t];
+    }
+    __syncthreads();
+    const long long total = pre[K];
+    for (long long w = warp; w < total; w += n_warps) {
+      int lo = 0, hi = K - 1;  // table of work item w: last t with pre[t] <= w
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (pre[mid] <= w) lo = mid;
+        else hi = mid - 1;
+      }
+      const DpTable& T = tabs[lo];
+      const unsigned long long pk = T.order[beg[lo] + (w - pre[lo])];
       long long s = 0;
-      for (int t = 0; t < d.T; ++t) s += (long long)((pk >> shift[t]) & mask[t]) * d.stride[t];
-      double m = 0.0;  // best[s] starts at 0.0; only a strictly larger candidate replaces it
+      for (int t = 0; t < T.d.T; ++t) s += (long long)((pk >> T.d.off[t]) & T.d.mask[t]) * T.d.stride[t];
+      double m = 0.0;
       int ch = -1;
-      for (int g = lane; g < n_groups; g += 32) {
-        const Group& G = groups[g];
-        if ((int)((pk >> shift[G.type]) & mask[G.type]) < G.n) continue;
-        const double bp = best[s - G.delta];
+      for (int g = lane; g < T.n_groups; g += 32) {
+        const Group G = T.groups[g];
+        if ((int)((pk >> T.d.off[G.type]) & T.d.mask[G.type]) < G.n) continue;
+        const double bp = T.best[s - G.delta];
         const double v = bp + G.hmax;
         if (v < m) continue;
-        int c = INT_MAX;  // first member (ascending index) reaching v
+        int c = INT_MAX;
         for (int k = 0; k < G.count; ++k) {
-          const int cc = members[G.first + k];
-          if (bp + h[cc] == v) {
+          const int cc = T.members[G.first + k];
+          if (bp + T.h[cc] == v) {
             c = cc;
             break;
           }
@@ -244,11 +267,10 @@ __global__ void __launch_bounds__(256) k4_dp_levels(MilpDims d, const Group* __r
         if (v > m) {
           m = v;
           ch = c;
-        } else if (c < ch) {  // tie with an earlier group: smallest config index wins
+        } else if (c < ch) {
           ch = c;
         }
       }
-      // (m, ch): ch == -1 exactly when m == 0, so the lexicographic merge is exact
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
@@ -259,8 +281,8 @@ __global__ void __launch_bounds__(256) k4_dp_levels(MilpDims d, const Group* __r
         }
       }
       if (lane == 0) {
-        best[s] = m;
-        choice[s] = ch;
+        T.best[s] = m;
+        T.choice[s] = ch;
       }
     }
     grid.sync();
@@ -545,19 +567,33 @@ int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opt
 struct MilpTable {
   std::vector<unsigned char> sig;  // configs + dims
   MilpDims d{};
-  void* buf = nullptr;             // best | choice
+  void* buf = nullptr;  // best | choice | order | level offsets/hist/cursor | groups | members | h
   size_t bytes = 0;
   double* best = nullptr;
   int* choice = nullptr;
+  unsigned long long* order = nullptr;
+  long long* off = nullptr;
+  Group* groups = nullptr;
+  int* members = nullptr;
+  double* h = nullptr;
+  int ng = 0, step = 1;
   long long last_use = 0;
+  long long pin = -1;  // milp batch epoch that uses it (not evictable within that batch)
+  long long pending_epoch = -1;  // batch whose DP launch will (re)compute it
   ~MilpTable() {
     if (buf) cudaFree(buf);
   }
 };
 
+// Lattice tables stay resident (B200: 180 GB HBM) up to kMilpCacheBytes, LRU beyond.
+constexpr size_t kMilpCacheBytes = (size_t)8 << 30;
+static const int kMilpCacheTables = 64;
+constexpr size_t kMilpPoolWarm = (size_t)2 << 30;
 struct MilpCache {
-  std::vector<std::unique_ptr<MilpTable>> tables;  // small LRU
-  long long clock = 0;
+  std::vector<std::unique_ptr<MilpTable>> tables;
+  long long clock = 0, epoch = 0;
+  size_t bytes = 0;
+  bool pool_ready = false;
 };
 
 // GPLAN_PROFILE=1: lattice tables built / reused, states tabulated, DP and backtrack wall time
@@ -604,10 +640,19 @@ static void set_dims(MilpDims& d, int dims, const int* caps) {
   d.levels = levels;
 }
 
+// Table key: the configs' fields (not their padding bytes) + dims.
 static std::vector<unsigned char> milp_sig(const gp_config* cfg, int nc, int dims) {
-  std::vector<unsigned char> sig(sizeof(gp_config) * nc + sizeof(int));
-  std::memcpy(sig.data(), cfg, sizeof(gp_config) * nc);
-  std::memcpy(sig.data() + sizeof(gp_config) * nc, &dims, sizeof(int));
+  std::vector<unsigned char> sig;
+  sig.reserve((size_t)nc * (GP_MAX_TYPES * 4 + 8) + 4);
+  auto put = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    sig.insert(sig.end(), b, b + n);
+  };
+  for (int c = 0; c < nc; ++c) {
+    put(cfg[c].type_counts, sizeof(int32_t) * dims);  // the DP reads counts and throughput only
+    put(&cfg[c].throughput, sizeof(double));
+  }
+  put(&dims, sizeof dims);
   return sig;
 }
 
@@ -630,30 +675,34 @@ static int milp_groups(const gp_config* cfg, int nc, int dims, std::vector<std::
   return GP_OK;
 }
 
-// A table for `cfg` covering `caps` (computes the lattice DP when no cached table does).
-static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, const int* caps, MilpTable** out) {
+// A table for `cfg` covering `caps`: a cached one, or a new one whose inputs and level
+// ordering are enqueued (its DP then runs in run_pending, batched with the others).
+static int plan_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, const int* caps, MilpTable** out,
+                      bool* pending) {
+  *pending = false;
   if (!ctx->milp_cache) ctx->milp_cache = new MilpCache();
   MilpCache& mc = *static_cast<MilpCache*>(ctx->milp_cache);
   const std::vector<unsigned char> sig = milp_sig(cfg, nc, dims);
   MilpTable* same = nullptr;
   for (auto& t : mc.tables) {
     if (t->sig != sig) continue;
-    same = t.get();
     bool covers = true;
     for (int u = 0; u < dims && covers; ++u) covers = caps[u] <= t->d.cap[u];
     if (covers) {
       t->last_use = ++mc.clock;
+      t->pin = mc.epoch;
       *out = t.get();
       g_milp_stats.reused++;
       return GP_OK;
     }
+    same = t.get();  // a same-config table: grown to the union lattice below (its DP reruns
+                     // before any backtrack of this batch, so its earlier users stay covered)
   }
-  const double t_start = now_s();
   std::vector<std::pair<long long, int>> key;
   int rc = milp_groups(cfg, nc, dims, key);
   if (rc) return rc;
-  // lattice to tabulate: the union with a cached table of the same configs when that
-  // grows the state count by at most 2x (a union of unlike lattices multiplies states)
+  // lattice to tabulate: the union with a cached table of the same configs when that grows
+  // the state count by at most 2x (a union of unlike lattices multiplies states)
   std::vector<int> lat(caps, caps + dims);
   if (same) {
     long long u = 1, own = 1;
@@ -665,18 +714,6 @@ static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, con
     }
     if (u <= 50000000 && u <= 2 * std::max(own, same->d.states)) lat = un;
     else same = nullptr;  // keep the cached table; tabulate this lattice separately
-  }
-  MilpTable* tab = same;
-  if (!tab) {
-    if (mc.tables.size() >= 4) {  // recycle the least recently used table (and its buffer)
-      auto lru = std::min_element(mc.tables.begin(), mc.tables.end(),
-                                  [](const auto& a, const auto& b) { return a->last_use < b->last_use; });
-      tab = lru->get();
-    } else {
-      mc.tables.push_back(std::make_unique<MilpTable>());
-      tab = mc.tables.back().get();
-    }
-    tab->sig = sig;
   }
   MilpDims d{};
   set_dims(d, dims, lat.data());
@@ -702,91 +739,160 @@ static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, con
   for (const Group& G : groups) step = std::min(step, G.n);
   std::vector<double> hs(nc);
   for (int c = 0; c < nc; ++c) hs[c] = cfg[c].throughput;
-  const size_t best_bytes = ((size_t)d.states * sizeof(double) + 255) & ~size_t(255);
-  const size_t tbytes = best_bytes + (size_t)d.states * sizeof(int) + 256;
-  GP_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (tbytes > tab->bytes) {  // grow-only, with headroom: tables of one run vary in size
-    if (tab->buf) cudaFree(tab->buf);
-    tab->buf = nullptr;
-    tab->bytes = 0;
-    const double t0 = now_s();
-    const size_t want = std::max(tbytes + tbytes / 2, (size_t)1 << 20);
-    GP_CUDA(cudaMalloc(&tab->buf, want));
-    tab->bytes = want;
-    g_milp_stats.mallocs++;
-    g_milp_stats.malloc_s += now_s() - t0;
-  }
-  tab->best = static_cast<double*>(tab->buf);
-  tab->choice = reinterpret_cast<int*>(static_cast<char*>(tab->buf) + best_bytes);
-  // scratch: groups, members, h, level tables, packed order
-  size_t bytes = 0;
-  auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+  size_t need = 0;
+  auto add = [&](size_t b) { need += ((b + 255) & ~size_t(255)) + 256; };
+  add(sizeof(double) * d.states);
+  add(sizeof(int) * d.states);
+  add(sizeof(unsigned long long) * d.states);
+  add(sizeof(long long) * (d.levels + 1));
+  add(sizeof(int) * d.levels);
+  add(sizeof(int) * d.levels);
+  add(sizeof(int));
   add(sizeof(Group) * ng);
   add(sizeof(int) * nc);
   add(sizeof(double) * nc);
-  add(sizeof(int) * d.levels);
-  add(sizeof(long long) * (d.levels + 1));
-  add(sizeof(int) * d.levels);
-  add(sizeof(int));
-  add(sizeof(unsigned long long) * d.states);
-  char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaRollout));
-  if (!base) return GP_CUDA_ERROR;
-  char* p = base;
-  Group* d_groups = carve2<Group>(p, ng);
-  int* d_members = carve2<int>(p, nc);
-  double* d_h = carve2<double>(p, nc);
+  MilpTable* tab = same;
+  if (!tab) {  // recycle the least recently used table outside this batch when over budget
+    MilpTable* lru = nullptr;
+    if (mc.bytes + need > kMilpCacheBytes || (int)mc.tables.size() >= kMilpCacheTables)
+      for (auto& t : mc.tables)
+        if (t->pin != mc.epoch && (!lru || t->last_use < lru->last_use)) lru = t.get();
+    if (lru) {
+      tab = lru;
+    } else {
+      mc.tables.push_back(std::make_unique<MilpTable>());
+      tab = mc.tables.back().get();
+    }
+    tab->sig = sig;
+  }
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));  // the pinned staging buffer is reused below
+  if (!mc.pool_ready) {  // stream-ordered allocations stay in the device pool between tables
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      void* warm = nullptr;  // map the table budget once; later tables sub-allocate from it
+      if (cudaMallocAsync(&warm, kMilpPoolWarm, ctx->stream) == cudaSuccess) cudaFreeAsync(warm, ctx->stream);
+      else cudaGetLastError();
+    }
+    mc.pool_ready = true;
+  }
+  if (need > tab->bytes) {  // grow-only, with headroom: tables of one run vary in size
+    if (tab->buf) GP_CUDA(cudaFreeAsync(tab->buf, ctx->stream));
+    mc.bytes -= tab->bytes;
+    tab->buf = nullptr;
+    tab->bytes = 0;
+    const double t0 = now_s();
+    const size_t want = std::max(need + need / 2, (size_t)1 << 20);
+    GP_CUDA(cudaMallocAsync(&tab->buf, want, ctx->stream));
+    tab->bytes = want;
+    mc.bytes += want;
+    g_milp_stats.mallocs++;
+    g_milp_stats.malloc_s += now_s() - t0;
+  }
+  char* p = static_cast<char*>(tab->buf);
+  tab->best = carve2<double>(p, d.states);
+  tab->choice = carve2<int>(p, d.states);
+  tab->order = carve2<unsigned long long>(p, d.states);
+  tab->off = carve2<long long>(p, d.levels + 1);
   int* d_hist = carve2<int>(p, d.levels);
-  long long* d_off = carve2<long long>(p, d.levels + 1);
   int* d_cursor = carve2<int>(p, d.levels);
   int* d_maxw = carve2<int>(p, 1);
-  unsigned long long* d_order = carve2<unsigned long long>(p, d.states);
-  const size_t in_bytes = (size_t)((char*)(d_h + nc) - (char*)d_groups);
+  tab->groups = carve2<Group>(p, ng);
+  tab->members = carve2<int>(p, nc);
+  tab->h = carve2<double>(p, nc);
+  const size_t in_bytes = (size_t)((char*)(tab->h + nc) - (char*)tab->groups);
   char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(in_bytes, (size_t)4096)));
   if (!hp) return GP_CUDA_ERROR;
   std::memcpy(hp, groups.data(), sizeof(Group) * ng);
-  std::memcpy(hp + ((char*)d_members - (char*)d_groups), members.data(), sizeof(int) * nc);
-  std::memcpy(hp + ((char*)d_h - (char*)d_groups), hs.data(), sizeof(double) * nc);
-  GP_CUDA(cudaMemcpyAsync(d_groups, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  std::memcpy(hp + ((char*)tab->members - (char*)tab->groups), members.data(), sizeof(int) * nc);
+  std::memcpy(hp + ((char*)tab->h - (char*)tab->groups), hs.data(), sizeof(double) * nc);
+  GP_CUDA(cudaMemcpyAsync(tab->groups, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h2d_bytes += (long long)in_bytes;
-  const double t_prep = now_s();
   GP_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int) * d.levels, ctx->stream));
   const int sweep_blocks = (int)std::min<long long>((d.states + 255) / 256, (long long)ctx->num_sms * 16);
   k4_level_hist<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_hist);
-  k4_level_scan<<<1, 32, 0, ctx->stream>>>(d_hist, d.levels, d_off, d_cursor, d_maxw);
-  k4_level_scatter<<<sweep_blocks, 256, 0, ctx->stream>>>(d, d_off, d_cursor, d_order);
+  k4_level_scan<<<1, 32, 0, ctx->stream>>>(d_hist, d.levels, tab->off, d_cursor, d_maxw);
+  k4_level_scatter<<<sweep_blocks, 256, 0, ctx->stream>>>(d, tab->off, d_cursor, tab->order);
   ctx->launches += 3;
-  const double t_kern = now_s();
-  g_milp_stats.prep_s += t_kern - t_prep;
-  g_milp_stats.levels += d.levels;
-  g_milp_stats.groups += ng;
-  static int occ = 0;
-  if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_dp_levels, 256, 0);
-    occ = std::max(1, occ);
-  }
-  // grid: about one warp per state of an average phase (2x for the wider middle levels),
-  // at most what is co-resident
-  const long long phases = (d.levels + step - 1) / step;
-  const long long warps = 2 * ((d.states + phases - 1) / phases);
-  int dp_blocks = (int)std::min<long long>((long long)ctx->num_sms * occ, (warps + 7) / 8);
-  dp_blocks = std::max(1, dp_blocks);
-  int ng_arg = ng, nc_arg = nc;
-  double* best = tab->best;
-  int* choice = tab->choice;
-  void* args[] = {&d, &d_groups, &ng_arg, &d_members, &d_h, &nc_arg, &step, &d_off, &d_order, &best, &choice};
-  GP_CUDA(cudaLaunchCooperativeKernel((void*)k4_dp_levels, dp_blocks, 256, args, 0, ctx->stream));
-  ctx->launches++;
   tab->d = d;
+  tab->ng = ng;
+  tab->step = step;
   tab->last_use = ++mc.clock;
+  tab->pin = mc.epoch;
   *out = tab;
+  *pending = tab->pending_epoch != mc.epoch;  // listed once per batch
+  tab->pending_epoch = mc.epoch;
   g_milp_stats.built++;
   g_milp_stats.states += d.states;
+  g_milp_stats.levels += d.levels;
+  g_milp_stats.groups += ng;
+  return GP_OK;
+}
+
+// The lattice DPs of the planned tables, kDpMaxTables per cooperative launch.
+static int run_pending(gp_ctx* ctx, const std::vector<MilpTable*>& pend) {
+  if (pend.empty()) return GP_OK;
+  const double t0 = now_s();
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_dp_multi, 256, 0);
+    occ = std::max(1, occ);
+  }
+  for (size_t c0 = 0; c0 < pend.size(); c0 += kDpMaxTables) {
+    const int K = (int)std::min<size_t>(kDpMaxTables, pend.size() - c0);
+    std::vector<DpTable> dt(K);
+    int max_phases = 0;
+    long long max_width = 1;
+    for (int k = 0; k < K; ++k) {
+      const MilpTable* t = pend[c0 + k];
+      DpTable& e = dt[k];
+      e.d = t->d;
+      e.step = t->step;
+      e.n_groups = t->ng;
+      e.phases = (t->d.levels + t->step - 1) / t->step;
+      e.pad = 0;
+      e.groups = t->groups;
+      e.members = t->members;
+      e.h = t->h;
+      e.off = t->off;
+      e.order = t->order;
+      e.best = t->best;
+      e.choice = t->choice;
+      max_phases = std::max(max_phases, e.phases);
+      max_width += 2 * ((t->d.states + e.phases - 1) / e.phases);
+    }
+    DpTable* d_dt = static_cast<DpTable*>(ctx_scratch(ctx, sizeof(DpTable) * K, kArenaRollout));
+    if (!d_dt) return GP_CUDA_ERROR;
+    GP_CUDA(cudaStreamSynchronize(ctx->stream));  // pinned staging + scratch reuse
+    char* hp = static_cast<char*>(ctx_pinned(ctx, sizeof(DpTable) * K + 256));
+    if (!hp) return GP_CUDA_ERROR;
+    std::memcpy(hp, dt.data(), sizeof(DpTable) * K);
+    GP_CUDA(cudaMemcpyAsync(d_dt, hp, sizeof(DpTable) * K, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->h2d_bytes += (long long)(sizeof(DpTable) * K);
+    // grid: about one warp per state of the widest phase sum, at most what is co-resident
+    int blocks = (int)std::min<long long>((long long)ctx->num_sms * occ, (max_width + 7) / 8);
+    blocks = std::max(1, blocks);
+    int K_arg = K;
+    void* args[] = {&d_dt, &K_arg, &max_phases};
+    GP_CUDA(cudaLaunchCooperativeKernel((void*)k4_dp_multi, blocks, 256, args, 0, ctx->stream));
+    ctx->launches++;
+  }
   if (std::getenv("GPLAN_PROFILE")) {
     cudaStreamSynchronize(ctx->stream);
-    g_milp_stats.dp_s += now_s() - t_start;
-    g_milp_stats.kern_s += now_s() - t_kern;
+    g_milp_stats.kern_s += now_s() - t0;
   }
   return GP_OK;
+}
+
+static int ensure_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, const int* caps, MilpTable** out) {
+  if (!ctx->milp_cache) ctx->milp_cache = new MilpCache();
+  static_cast<MilpCache*>(ctx->milp_cache)->epoch++;
+  bool pending = false;
+  int rc = plan_table(ctx, cfg, nc, dims, caps, out, &pending);
+  if (rc) return rc;
+  if (pending) rc = run_pending(ctx, {*out});
+  return rc;
 }
 
 // Backtracks q queries (caps, B, len) of the same configs from `tab` in one launch.
@@ -908,6 +1014,8 @@ int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs,
     if (milp_check(ncs[i], caps[i], dims)) rcs[i] = GP_INVALID;
   }
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sigs[a] < sigs[b]; });
+  std::vector<std::vector<int>> all_parts;  // queries per table, over all config lists
+  std::vector<std::vector<int>> all_caps;   // each table's lattice
   for (size_t g0 = 0; g0 < order.size();) {
     size_t g1 = g0;
     while (g1 < order.size() && sigs[order[g1]] == sigs[order[g0]]) ++g1;
@@ -942,12 +1050,34 @@ int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs,
         parts[hit].push_back(i);
       }
       for (size_t pidx = 0; pidx < parts.size(); ++pidx) {
-        const std::vector<int>& part = parts[pidx];
-        const std::vector<int>& pc = part_caps[pidx];
+        all_parts.push_back(parts[pidx]);
+        all_caps.push_back(part_caps[pidx]);
+      }
+    }
+    g0 = g1;
+  }
+  // every table of the batch planned first (cached or new), the new ones' DPs batched
+  if (!ctx->milp_cache) ctx->milp_cache = new MilpCache();
+  static_cast<MilpCache*>(ctx->milp_cache)->epoch++;
+  std::vector<MilpTable*> tabs(all_parts.size()), pend;
+  for (size_t pidx = 0; pidx < all_parts.size(); ++pidx) {
+    const int i0 = all_parts[pidx][0];
+    bool pending = false;
+    int rc = plan_table(ctx, cfgs[i0], ncs[i0], dims, all_caps[pidx].data(), &tabs[pidx], &pending);
+    if (rc) return rc;
+    if (pending) pend.push_back(tabs[pidx]);
+  }
+  {
+    int rc = run_pending(ctx, pend);
+    if (rc) return rc;
+  }
+  {
+    {
+      for (size_t pidx = 0; pidx < all_parts.size(); ++pidx) {
+        const std::vector<int>& part = all_parts[pidx];
         const int i0 = part[0];
-        MilpTable* tab = nullptr;
-        int rc = ensure_table(ctx, cfgs[i0], ncs[i0], dims, pc.data(), &tab);
-        if (rc) return rc;
+        MilpTable* tab = tabs[pidx];
+        int rc = GP_OK;
         std::vector<const int*> cp;
         std::vector<double> bb;
         std::vector<gp_rollout_result> ro(part.size());
@@ -969,7 +1099,6 @@ int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs,
         }
       }
     }
-    g0 = g1;
   }
   for (int i = 0; i < q; ++i)
     if (rcs[i] == -1) rcs[i] = GP_OK;

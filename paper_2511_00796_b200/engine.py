@@ -62,6 +62,9 @@ def lib() -> C.CDLL:
         _lib.gp_train_collect.argtypes = [vp, C.POINTER(abi.gp_train_result), abi.i32p]
         _lib.gp_ctx_set_timing.argtypes = [vp, C.c_int]
         _lib.gp_ctx_set_memo.argtypes = [vp, C.c_int]
+        _lib.gp_solve_milp_batch.argtypes = [vp, C.c_int32, C.POINTER(abi.gp_config), abi.i32p, abi.i32p,
+                                             C.c_int32, abi.f64p, C.c_double, C.POINTER(abi.gp_rollout_result),
+                                             C.POINTER(abi.gp_rollout_entry), abi.i32p]
         _lib.gp_train_timing.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]
         _lib.gp_ctx_io_bytes.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
                                          C.POINTER(C.c_double)]
@@ -216,6 +219,30 @@ class Engine:
         return {"feasible": bool(out.feasible), "objective": out.objective if out.feasible else None,
                 "train_set": ids[:out.n_train].tolist(), "partitions": out.partitions,
                 "train_candidates": out.train_candidates, "replica_vectors": out.replica_vectors}
+
+    def solve_milp_batch(self, queries, B, mean_len=None):
+        """queries: [(configs (list of gp_config), caps)] -> [(status, gp_rollout_result, entries)]."""
+        mean_len = self.problem.workload.mean_len if mean_len is None else mean_len
+        dims = len(self.problem.cluster.type_names)
+        off = [0]
+        for cfgs, _ in queries:
+            off.append(off[-1] + len(cfgs))
+        allc = (abi.gp_config * max(off[-1], 1))(*[c for cfgs, _ in queries for c in cfgs])
+        offs = np.array(off, dtype=np.int32)
+        caps = np.array([list(c) for _, c in queries], dtype=np.int32).reshape(-1)
+        Bs = np.full(len(queries), float(B))
+        out = (abi.gp_rollout_result * max(len(queries), 1))()
+        ent = (abi.gp_rollout_entry * max(off[-1], 1))()
+        st = np.zeros(max(len(queries), 1), dtype=np.int32)
+        _check(lib().gp_solve_milp_batch(self._h, len(queries), allc, offs.ctypes.data_as(abi.i32p),
+                                         caps.ctypes.data_as(abi.i32p), dims,
+                                         Bs.ctypes.data_as(abi.f64p), mean_len, out, ent,
+                                         st.ctypes.data_as(abi.i32p)))
+        res = []
+        for i in range(len(queries)):
+            n = out[i].n_entries if st[i] == 0 else 0
+            res.append((int(st[i]), out[i], [ent[off[i] + k] for k in range(n)]))
+        return res
 
     def set_memo(self, on: bool = True):
         """Enable (default) / disable + drop the window-independent constrained_search memo."""

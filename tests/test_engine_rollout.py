@@ -108,3 +108,38 @@ def test_milp_errors():
     assert res.n_entries == 0 and ent == []
     with pytest.raises(ValidationError):
         eng.enumerate_configs([])
+
+
+@pytest.mark.parametrize("name", ["c3_64gpu", "c4_256gpu", "c5_1024gpu"])
+def test_milp_batch_vs_oracle(name):
+    """gp_solve_milp_batch: many rollout sets (distinct config lists, nested and unrelated
+    lattices) solved in one call — the lattice DPs of all new tables in one launch — each
+    equal to the oracle's solve_milp."""
+    from paper_2511_00796_b200.engine import Engine
+    p = problem(name)
+    eng, orc = Engine(p), Oracle(p)
+    n = p.cluster.n
+    rng = random.Random(4040 + n)
+    queries, wants = [], []
+    B = float(p.workload.batch_rollouts * 3)
+    for train in random_train_sets(n, 40, seed=4040 + n):
+        roll = sorted(set(range(n)) - set(train))
+        if n > 256:
+            roll = sorted(rng.sample(range(n), rng.randint(40, 140)))
+        cfgs = eng.enumerate_configs(roll)
+        caps = eng.rollout_capacities(roll)
+        states = 1
+        for c in caps:
+            states *= c + 1
+        if not cfgs or states > 2_000_000:
+            continue
+        queries.append((cfgs, list(caps)))
+        wants.append(oracle_milp(orc, oracle_configs(orc, roll), caps, B, p.workload.mean_len))
+    assert len(queries) >= 8
+    got = eng.solve_milp_batch(queries, B)
+    for (st, res, ent), (rc, res_o, ent_o) in zip(got, wants):
+        assert (st == 0) == (rc == 0)
+        if rc == 0:
+            assert res.makespan == res_o.makespan and res.aggregate == res_o.aggregate
+            assert [(e.config, e.replicas, e.workload) for e in ent] == \
+                [(e.config, e.replicas, e.workload) for e in ent_o]
