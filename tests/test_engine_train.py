@@ -203,3 +203,29 @@ def test_device_level_links_path(monkeypatch):
         r, d = dev_level.constrained_search_raw(ids, 3)
         assert train_result_dict(r, d) == want, ids
         assert run(name, ids, 3) == want, ids
+
+
+def test_four_type_runs(monkeypatch):
+    """Four GPU types (the R = 4 instantiations of K1 and K1-fast): a 6.9e7-layout set —
+    fast == generic on the full range, slices == the oracle — and random subsets == oracle."""
+    name = "t4types_288gpu"
+    p = problem(name)
+    orc = Oracle(p)
+    ids = list(range(p.cluster.n))
+    total = engine(name).train_space(ids)
+    assert total == orc.train_space(ids) and total > 1 << 20
+    fast = run(name, ids, 3, lo=0, hi=total)
+    monkeypatch.setenv("GPLAN_K1_GENERIC", "1")
+    generic = run(name, ids, 3, lo=0, hi=total)
+    monkeypatch.delenv("GPLAN_K1_GENERIC")
+    assert fast == generic
+    for lo in (0, total // 5, total // 2, total - 30_000):
+        hi = min(total, lo + 30_000)
+        assert run(name, ids, 3, lo=lo, hi=hi) == orc.constrained_search(ids, 3, lo=lo, hi=hi)
+    checked = 0
+    for s in random_train_sets(p.cluster.n, 40, seed=4444, max_size=48):
+        if orc.train_space(s) > 150_000:
+            continue
+        assert run(name, s, 2) == orc.constrained_search(s, 2), s
+        checked += 1
+    assert checked >= 5
