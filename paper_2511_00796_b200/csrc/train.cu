@@ -142,20 +142,17 @@ __host__ __device__ __forceinline__ long long nm_winner(const NearMin& m, int wi
 
 // ---------------------------------------------------------------- K2a blocks
 // min_link_within_groups (src/cost_model.cpp:12-36), exact, for every option.
-__global__ void __launch_bounds__(256) k2a_block_stats(const int* __restrict__ ordered,
-                                                       const BlockMeta* __restrict__ meta,
-                                                       const int* __restrict__ pos,
-                                                       TrainTables tb, BlockRec* __restrict__ out,
-                                                       const int* __restrict__ dtype,
-                                                       const int* __restrict__ dmachine,
-                                                       const double* __restrict__ dflops,
-                                                       const double* __restrict__ dcap,
-                                                       const double* __restrict__ links, int N,
-                                                       int L, int mb, double* fd_coef,
-                                                       double2* __restrict__ blkf) {
+// CTA-cooperative body: block `bidx` of the set (also run by the fused small-set kernel).
+__device__ __forceinline__ void k2a_body(int bidx, const int* __restrict__ ordered,
+                                         const BlockMeta* __restrict__ meta, const int* __restrict__ pos,
+                                         const TrainTables& tb, BlockRec* __restrict__ out,
+                                         const int* __restrict__ dtype, const int* __restrict__ dmachine,
+                                         const double* __restrict__ dflops, const double* __restrict__ dcap,
+                                         const double* __restrict__ links, int N, int L, int mb,
+                                         double* fd_coef, double2* __restrict__ blkf) {
   __shared__ double red[32];
   __shared__ BlockRec rec;
-  const BlockMeta m = meta[blockIdx.x];
+  const BlockMeta m = meta[bidx];
   const int* P = pos + tb.pos_off[m.run];
   const int start = m.start_global + P[m.a];
   const int n = P[m.b] - P[m.a];
@@ -177,10 +174,9 @@ __global__ void __launch_bounds__(256) k2a_block_stats(const int* __restrict__ o
     rec.cap_front = dcap[dev[0]];
     for (int o = 0; o < 4; ++o) rec.beta_tp[o] = rec.beta_dp[o] = kInf;
   }
-  if (blockIdx.x == 0 && threadIdx.x < GP_MAX_STAGES + 1) {
-    const int S = threadIdx.x;
-    fd_coef[S] = S > 0 ? static_cast<double>(S - 1) / mb : 0.0;
-  }
+  if (bidx == 0)
+    for (int S = threadIdx.x; S <= GP_MAX_STAGES; S += blockDim.x)
+      fd_coef[S] = S > 0 ? static_cast<double>(S - 1) / mb : 0.0;
   __syncthreads();
   const int per_machine = rec.per_machine;
 #pragma unroll 1
@@ -262,24 +258,36 @@ __global__ void __launch_bounds__(256) k2a_block_stats(const int* __restrict__ o
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    out[blockIdx.x] = rec;
-    blkf[blockIdx.x] = make_double2(rec.flops, rec.lf_num);  // K1's (flops, L*f) view
+    out[bidx] = rec;
+    blkf[bidx] = make_double2(rec.flops, rec.lf_num);  // K1's (flops, L*f) view
   }
+  __syncthreads();  // rec is reused by the next block of a fused loop
+}
+
+__global__ void __launch_bounds__(256) k2a_block_stats(const int* __restrict__ ordered,
+                                                       const BlockMeta* __restrict__ meta,
+                                                       const int* __restrict__ pos,
+                                                       TrainTables tb, BlockRec* __restrict__ out,
+                                                       const int* __restrict__ dtype,
+                                                       const int* __restrict__ dmachine,
+                                                       const double* __restrict__ dflops,
+                                                       const double* __restrict__ dcap,
+                                                       const double* __restrict__ links, int N,
+                                                       int L, int mb, double* fd_coef,
+                                                       double2* __restrict__ blkf) {
+  k2a_body(blockIdx.x, ordered, meta, pos, tb, out, dtype, dmachine, dflops, dcap, links, N, L, mb, fd_coef, blkf);
 }
 
 // ------------------------------------------------------------ K2b transfers
 // min_link_between (src/cost_model.cpp:38-47) over adjacent blocks; one warp per item.
 // item = (run, a, b, c): within-run blocks [a,b) -> [b,c); c < 0 marks a cross-run item
 // (run r's block [a, nc+1) -> run r+1's block [0, -c)).
-__global__ void __launch_bounds__(256) k2b_transfers(const int* __restrict__ ordered,
-                                                     const int4* __restrict__ items, int n_items,
-                                                     const int* __restrict__ pos, TrainTables tb,
-                                                     TrainSpace sp, const int* __restrict__ run_start,
-                                                     const double* __restrict__ links, int N,
-                                                     double numer, double* tin, double* tx) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= n_items) return;
+// warp body: item `warp` of the set
+__device__ __forceinline__ void k2b_body(int warp, int lane, const int* __restrict__ ordered,
+                                         const int4* __restrict__ items, const int* __restrict__ pos,
+                                         const TrainTables& tb, const TrainSpace& sp,
+                                         const int* __restrict__ run_start, const double* __restrict__ links,
+                                         int N, double numer, double* tin, double* tx) {
   const int4 it = items[warp];
   const int r = it.x;
   const int* P = pos + tb.pos_off[r];
@@ -325,6 +333,17 @@ __global__ void __launch_bounds__(256) k2b_transfers(const int* __restrict__ ord
   }
 }
 
+__global__ void __launch_bounds__(256) k2b_transfers(const int* __restrict__ ordered,
+                                                     const int4* __restrict__ items, int n_items,
+                                                     const int* __restrict__ pos, TrainTables tb,
+                                                     TrainSpace sp, const int* __restrict__ run_start,
+                                                     const double* __restrict__ links, int N,
+                                                     double numer, double* tin, double* tx) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= n_items) return;
+  k2b_body(warp, threadIdx.x & 31, ordered, items, pos, tb, sp, run_start, links, N, numer, tin, tx);
+}
+
 // ------------------------------------------------------------ K2c stage table
 // Per (block, layer_count): the option loop of constrained_search
 // (src/train_search.cpp:289-315) with mem_cumsum_train and train_stage_cost.
@@ -362,12 +381,9 @@ __device__ __forceinline__ bool stage_option(const BlockRec& b, int lc, int o, c
 // mode 0 (constrained_search): per (block, layers) the comm-minimal memory-feasible option
 // (strict <, tp ascending). mode 1 (product space, enumerate_train_candidates): the option of
 // minimal TrainStageCost::total() — the value the product-space argmin reaches per stage.
-__global__ void __launch_bounds__(256) k2c_stage_table(const BlockRec* __restrict__ blk, int nblk,
-                                                       Scalars sc, const double* __restrict__ ceff,
-                                                       int mode, double2* __restrict__ stage,
-                                                       int8_t* __restrict__ opt) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)nblk * sc.L) return;
+__device__ __forceinline__ void k2c_body(long long idx, const BlockRec* __restrict__ blk, const Scalars& sc,
+                                         const double* __restrict__ ceff, int mode, double2* __restrict__ stage,
+                                         int8_t* __restrict__ opt) {
   const int bi = (int)(idx / sc.L);
   const int lc = (int)(idx - (long long)bi * sc.L) + 1;
   const BlockRec& b = blk[bi];
@@ -399,14 +415,21 @@ __global__ void __launch_bounds__(256) k2c_stage_table(const BlockRec* __restric
   opt[idx] = (int8_t)best_o;
 }
 
+__global__ void __launch_bounds__(256) k2c_stage_table(const BlockRec* __restrict__ blk, int nblk,
+                                                       Scalars sc, const double* __restrict__ ceff,
+                                                       int mode, double2* __restrict__ stage,
+                                                       int8_t* __restrict__ opt) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)nblk * sc.L) return;
+  k2c_body(idx, blk, sc, ceff, mode, stage, opt);
+}
+
 
 // --------------------------------------------------------- K2d suffix table
 // One entry per choice (k, cuts) of the LAST type run, in run_compositions order
 // (src/train_search.cpp:53-72, k ascending): block ids, internal transfers.
-__global__ void k2d_suffix_table(const int4* __restrict__ choices, int n, TrainSpace sp,
-                                 const double* __restrict__ tin, SufEnt* __restrict__ suf) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+__device__ __forceinline__ void k2d_body(int i, const int4* __restrict__ choices, const TrainSpace& sp,
+                                         const double* __restrict__ tin, SufEnt* __restrict__ suf) {
   const int r = sp.R - 1, nc = sp.nc[r], e = nc + 2;
   const int4 c = choices[i];  // (k, b1, b2, b3) position-index boundaries
   const int k = c.x;
@@ -421,6 +444,13 @@ __global__ void k2d_suffix_table(const int4* __restrict__ choices, int n, TrainS
   out.k = k;
   out.b1 = b[1];
   suf[i] = out;
+}
+
+__global__ void k2d_suffix_table(const int4* __restrict__ choices, int n, TrainSpace sp,
+                                 const double* __restrict__ tin, SufEnt* __restrict__ suf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  k2d_body(i, choices, sp, tin, suf);
 }
 
 // ------------------------------------------------------------- K1 layout scan
@@ -1084,22 +1114,18 @@ __device__ NearMin nm_block_reduce(NearMin m) {
   return m;
 }
 
+// The generic scan of work items warp, warp + n_warps, ... (prefix chunks) of a range;
+// returns the thread's summary. P/D: the warp's shared-memory prefix state.
 template <int R>
-__global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(TrainSpace sp, TrainTables tb,
-                                                      const double2* __restrict__ blkf, int L,
-                                                      ScanRange rg, NearMin* __restrict__ partial) {
+__device__ __forceinline__ NearMin k1_scan_warps(const TrainSpace& sp, const TrainTables& tb,
+                                                 const double2* __restrict__ blkf, int L, const ScanRange& rg,
+                                                 long long warp, long long n_warps, Prefix<R>& P,
+                                                 PrefixData<R>& D) {
   const int lane = threadIdx.x & 31;
-  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
   const long long n_suf = sp.n_suf;
   // thread summary in registers: NearMin {b0, k0..k2, feasible}
   long long b0 = kInfBits, k0 = LLONG_MAX, k1 = LLONG_MAX, k2 = LLONG_MAX, feasible = 0;
-  // the warp's current prefix lives in shared memory (lane 0 owns it; lanes read broadcasts)
-  __shared__ Prefix<R> sP[kK1Threads / 32];
-  __shared__ PrefixData<R> sD[kK1Threads / 32];
-  Prefix<R>& P = sP[threadIdx.x >> 5];
-  PrefixData<R>& D = sD[threadIdx.x >> 5];
   for (long long it = warp; it < n_items; it += n_warps) {
     long long p = rg.p_lo + it * rg.chunk;
     const long long p_end = min(p + rg.chunk, rg.p_lo + rg.n_pref);
@@ -1139,7 +1165,19 @@ __global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(Tra
       if (lane == 0 && p + 1 < p_end) prefix_advance<R>(sp, P);
     }
   }
-  NearMin nm{b0, {k0, k1, k2}, feasible};
+  return NearMin{b0, {k0, k1, k2}, feasible};
+}
+
+template <int R>
+__global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(TrainSpace sp, TrainTables tb,
+                                                      const double2* __restrict__ blkf, int L,
+                                                      ScanRange rg, NearMin* __restrict__ partial) {
+  // the warp's current prefix lives in shared memory (lane 0 owns it; lanes read broadcasts)
+  __shared__ Prefix<R> sP[kK1Threads / 32];
+  __shared__ PrefixData<R> sD[kK1Threads / 32];
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  NearMin nm = k1_scan_warps<R>(sp, tb, blkf, L, rg, warp, n_warps, sP[threadIdx.x >> 5], sD[threadIdx.x >> 5]);
   nm = nm_block_reduce(nm);
   if (threadIdx.x == 0) partial[blockIdx.x] = nm;
 }
@@ -1307,13 +1345,13 @@ __global__ void __launch_bounds__(kK1Threads) k1_deferred(TrainSpace sp, TrainTa
 
 // Merge CTA summaries, pick the window's winner and decode it (prefix, suffix) -> rank + plan.
 template <int R>
-__global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb,
-                                                   const double2* __restrict__ blkf,
-                                                   const BlockRec* __restrict__ blk, int L,
-                                                   int window, const NearMin* __restrict__ partial,
-                                                   int n_partial, TrainOut* __restrict__ out,
-                                                   const unsigned long long* __restrict__ slow_q,
-                                                   Scalars sc, const double* __restrict__ ceff, int mode) {
+__device__ __forceinline__ void k1_finalize_body(const TrainSpace& sp, const TrainTables& tb,
+                                                 const double2* __restrict__ blkf,
+                                                 const BlockRec* __restrict__ blk, int L, int window,
+                                                 const NearMin* __restrict__ partial, int n_partial,
+                                                 TrainOut* __restrict__ out,
+                                                 const unsigned long long* __restrict__ slow_q, const Scalars& sc,
+                                                 const double* __restrict__ ceff, int mode) {
   NearMin m;
   nm_init(m);
   for (int i = threadIdx.x; i < n_partial; i += blockDim.x) nm_merge(m, partial[i]);
@@ -1371,6 +1409,76 @@ __global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb
     ++n;
   }
   out->n_stages = n;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) k1_finalize(TrainSpace sp, TrainTables tb,
+                                                   const double2* __restrict__ blkf,
+                                                   const BlockRec* __restrict__ blk, int L,
+                                                   int window, const NearMin* __restrict__ partial,
+                                                   int n_partial, TrainOut* __restrict__ out,
+                                                   const unsigned long long* __restrict__ slow_q,
+                                                   Scalars sc, const double* __restrict__ ceff, int mode) {
+  k1_finalize_body<R>(sp, tb, blkf, blk, L, window, partial, n_partial, out, slow_q, sc, ceff, mode);
+}
+
+// ------------------------------------------------------- fused small-set path
+// A scheduler / exhaustive batch holds many train sets whose whole space is a few thousand
+// layouts; per-set launches of K2a..K2d, K1 and finalize would dominate. One CTA runs the
+// complete pipeline of one such set (the same bodies as the per-set kernels, phases
+// separated by CTA barriers), one launch per batch and type-run count.
+struct SmallSet {
+  TrainSpace sp;
+  TrainTables tb;
+  ScanRange rg;
+  const BlockMeta* meta;
+  const int* run_start;
+  const int4* items;
+  const int4* choices;
+  BlockRec* blk;
+  double2* blkf;
+  double2* stage;
+  int8_t* opt;
+  double* tin;
+  double* tx;
+  double* fd;
+  SufEnt* suf;
+  NearMin* partial;
+  TrainOut* out;
+  int nblk, n_items, n_choices, mode;
+};
+constexpr long long kSmallLayouts = 1 << 12;  // spaces up to this size take the fused path
+
+template <int R>
+__global__ void __launch_bounds__(kK1Threads) k_train_small(const SmallSet* __restrict__ sets, Scalars sc,
+                                                            const int* __restrict__ dtype,
+                                                            const int* __restrict__ dmachine,
+                                                            const double* __restrict__ dflops,
+                                                            const double* __restrict__ dcap,
+                                                            const double* __restrict__ links, int N,
+                                                            const double* __restrict__ ceff, double numer,
+                                                            int window) {
+  const SmallSet& S = sets[blockIdx.x];
+  const int L = sc.L;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int b = 0; b < S.nblk; ++b)  // K2a (CTA per block, sequentially)
+    k2a_body(b, S.tb.ordered, S.meta, S.tb.pos, S.tb, S.blk, dtype, dmachine, dflops, dcap, links, N, L, sc.mb,
+             S.fd, S.blkf);
+  for (int it = wid; it < S.n_items; it += nw)  // K2b (warp per item)
+    k2b_body(it, lane, S.tb.ordered, S.items, S.tb.pos, S.tb, S.sp, S.run_start, links, N, numer, S.tin, S.tx);
+  __syncthreads();
+  for (long long idx = threadIdx.x; idx < (long long)S.nblk * L; idx += blockDim.x)  // K2c
+    k2c_body(idx, S.blk, sc, ceff, S.mode, S.stage, S.opt);
+  for (int i = threadIdx.x; i < S.n_choices; i += blockDim.x)  // K2d
+    k2d_body(i, S.choices, S.sp, S.tin, S.suf);
+  __syncthreads();
+  __shared__ Prefix<R> sP[kK1Threads / 32];
+  __shared__ PrefixData<R> sD[kK1Threads / 32];
+  NearMin nm = k1_scan_warps<R>(S.sp, S.tb, S.blkf, L, S.rg, wid, nw, sP[wid], sD[wid]);
+  nm = nm_block_reduce(nm);
+  if (threadIdx.x == 0) S.partial[0] = nm;
+  __syncthreads();
+  k1_finalize_body<R>(S.sp, S.tb, S.blkf, S.blk, L, window, S.partial, 1, S.out, nullptr, sc, ceff, S.mode);
 }
 
 // ===================================================================== host
@@ -1954,19 +2062,8 @@ static double sum_stages(const HostSpace& h) {
   return h.total ? tot[0][0] : 0;
 }
 
-// Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
-static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long lo, long long hi,
-                           cudaStream_t stream, bool timing, bool force_generic = false, int lane = -1) {
-  const HostSpace& h = P.h;
-  if (lo < 0) lo = 0;
-  if (hi < 0 || hi > h.total) hi = h.total;
-  if (lo > hi) lo = hi;
-  P.lo = lo;
-  P.hi = hi;
-  P.window = window;
-  P.launched = true;
-  if (h.total == 0 || lo == hi) return GP_OK;  // std::nullopt
-  const int L = ctx->sc.L;
+// Device-side table view of a prepared train set.
+static TrainTables prepared_tables(const gp_ctx* ctx, const PreparedTrain& P) {
   TrainTables tb{};
   tb.ordered = P.d_ordered;
   tb.mgrp = P.d_mgrp;
@@ -1989,7 +2086,24 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   tb.sf_ms = P.d_sf_ms;
   tb.sf_st = P.d_sf_st;
   tb.nzs_max = P.d_nzs_max;
-  for (int r = 0; r < h.sp.R; ++r) tb.pos_off[r] = h.pos_off[r];
+  for (int r = 0; r < P.h.sp.R; ++r) tb.pos_off[r] = P.h.pos_off[r];
+  return tb;
+}
+
+// Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
+static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long lo, long long hi,
+                           cudaStream_t stream, bool timing, bool force_generic = false, int lane = -1) {
+  const HostSpace& h = P.h;
+  if (lo < 0) lo = 0;
+  if (hi < 0 || hi > h.total) hi = h.total;
+  if (lo > hi) lo = hi;
+  P.lo = lo;
+  P.hi = hi;
+  P.window = window;
+  P.launched = true;
+  if (h.total == 0 || lo == hi) return GP_OK;  // std::nullopt
+  const int L = ctx->sc.L;
+  const TrainTables tb = prepared_tables(ctx, P);
   const char* generic_env = std::getenv("GPLAN_K1_GENERIC");
   // (layer counts are tabulated as signed bytes: L <= 127)
   const int nlast = (h.sp.nc[h.sp.R - 1] + 2) * (h.sp.nc[h.sp.R - 1] + 1) / 2;
@@ -2266,8 +2380,73 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
   }
   GP_CUDA(cudaEventRecord(ctx->ev_lane[NL], ctx->stream));  // inputs are on the device
   for (int l = 0; l < NL; ++l) GP_CUDA(cudaStreamWaitEvent(ctx->lane[l], ctx->ev_lane[NL], 0));
+  // small spaces: the fused one-CTA-per-set kernel, one launch per type-run count
+  std::vector<int> small_of[GP_MAX_TYPES + 1];
   for (int i = 0; i < n_sets; ++i) {
-    const int l = i % NL;
+    const HostSpace& h = Ps[i].h;
+    if (h.total > 0 && h.total <= kSmallLayouts && h.sp.R >= 1 && h.sp.R <= 4) small_of[h.sp.R].push_back(i);
+  }
+  std::vector<char> is_small(n_sets, 0);
+  for (int R = 1; R <= 4; ++R) {
+    const int ns_ = (int)small_of[R].size();
+    if (ns_ == 0) continue;
+    std::vector<SmallSet> ss(ns_);
+    for (int j = 0; j < ns_; ++j) {
+      PreparedTrain& P = Ps[small_of[R][j]];
+      is_small[small_of[R][j]] = 1;
+      P.lo = 0;
+      P.hi = P.h.total;
+      P.window = window;
+      P.launched = true;
+      SmallSet& S = ss[j];
+      S.sp = P.h.sp;
+      S.tb = prepared_tables(ctx, P);
+      ScanRange rg{};
+      rank_split(P.h, 0, rg.p_lo, rg.s_lo);
+      rank_split(P.h, P.h.total, rg.p_hi, rg.s_hi);
+      rg.n_pref = rg.p_hi - rg.p_lo + (rg.s_hi > 0 ? 1 : 0);
+      rg.chunk = std::max(1LL, rg.n_pref / (2 * (kK1Threads / 32)));
+      S.rg = rg;
+      S.meta = P.d_meta;
+      S.run_start = P.d_run_start;
+      S.items = P.d_items;
+      S.choices = P.d_choices;
+      S.blk = P.d_blk;
+      S.blkf = P.d_blkf;
+      S.stage = P.d_stage;
+      S.opt = P.d_opt;
+      S.tin = P.d_tin;
+      S.tx = P.d_tx;
+      S.fd = P.d_fd;
+      S.suf = P.d_suf;
+      S.partial = P.d_partial;
+      S.out = P.d_out;
+      S.nblk = P.h.nblk;
+      S.n_items = (int)P.h.items.size();
+      S.n_choices = (int)P.h.choices.size();
+      S.mode = P.mode;
+    }
+    SmallSet* d_ss = nullptr;  // descriptors: stream-ordered allocation, freed after the launch
+    GP_CUDA(cudaMallocAsync(&d_ss, sizeof(SmallSet) * ns_, ctx->lane[R % NL]));
+    GP_CUDA(cudaMemcpyAsync(d_ss, ss.data(), sizeof(SmallSet) * ns_, cudaMemcpyHostToDevice, ctx->lane[R % NL]));
+    ctx->h2d_bytes += (long long)(sizeof(SmallSet) * ns_);
+    const double numer = ctx->sc.tokens > 0 ? ctx->sc.act_tok_h2 : 0.0;
+    auto launch = [&](auto kern) {
+      kern<<<ns_, kK1Threads, 0, ctx->lane[R % NL]>>>(d_ss, ctx->sc, ctx->d_type, ctx->d_machine, ctx->d_flops,
+                                                      ctx->d_hbm_cap, ctx->d_links, ctx->N, ctx->d_ceff, numer,
+                                                      window);
+    };
+    if (R == 1) launch(k_train_small<1>);
+    else if (R == 2) launch(k_train_small<2>);
+    else if (R == 3) launch(k_train_small<3>);
+    else launch(k_train_small<4>);
+    ctx->launches++;
+    GP_CUDA(cudaGetLastError());
+    GP_CUDA(cudaFreeAsync(d_ss, ctx->lane[R % NL]));  // (a pageable-source copy is staged on return)
+  }
+  for (int i = 0, k = 0; i < n_sets; ++i) {
+    if (is_small[i]) continue;
+    const int l = k++ % NL;
     int rc = launch_prepared(ctx, Ps[i], window, 0, -1, ctx->lane[l], false, false, l);
     if (rc) return rc;
   }
