@@ -107,7 +107,7 @@ struct TrainTables {
                           //   remainder order (desc, stage order among equals), 16 bits each
   const int2* sf_zb;      // [n_suf] zero-layer stage count at promotion b = 0..3 (bytes),
                           //   b = 4 (byte 0) | stage-would-exceed-L mask << 8
-  const double* sf_t;     // [3][n_suf] internal stage-transfer terms
+  const double* sf_t;     // [n_suf][4] internal stage-transfer terms (t0, t1, t2, 0)
   const signed char* sf_ms;  // [n_suf][kMsStride]: largest layer count at (b, d donations), -1: none
   const double2* sf_st;   // [5 * (kDonations + 1)][n_suf]: (max total, max compute) at (b, d)
   const int* nzs_max;     // suffix stats: [0] most zero-layer stages of any suffix choice,

@@ -815,7 +815,8 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
   for (int j = 0; j < k; ++j) rbs[rk[j]] = e.bi[j] - blk_off_last;
   sf_hot[i] = make_int4(fs, k | (e.b1 << 16), rbs[0] | (rbs[1] << 16), rbs[2] | (rbs[3] << 16));
 #pragma unroll
-  for (int j = 0; j < 3; ++j) sf_t[(size_t)j * n + i] = e.t[j];
+  for (int j = 0; j < 3; ++j) sf_t[(size_t)i * 4 + j] = e.t[j];
+  sf_t[(size_t)i * 4 + 3] = 0.0;
   unsigned nzs = 0, nz4 = 0, bad = 0;
   for (int b = 0; b <= 4; ++b) {
     int lay[4];
@@ -1016,14 +1017,16 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
   const int a_lo = max(0, L - fp_all - fs_max - 4), a_hi = min(kp, L - fp_all - fs_min);
   if (lane <= a_hi - a_lo) {
     const int a = a_lo + lane;
-    int lay[PrefixFast<R>::NQ];
+    int lay[PrefixFast<R>::NQ], top[PrefixFast<R>::NQ];  // layers; fl + 1 (-1: inactive slot)
     int nz = 0;
     bool over = false;
 #pragma unroll
-    for (int q = 0; q < NP; ++q) {
+    for (int q = 0; q < NP; ++q) {  // shared-memory reads hoisted out of the donation loop
       lay[q] = 0;
+      top[q] = -1;
       if (D.act[q]) {
-        lay[q] = F.fl[q] + (F.rk[q] < a ? 1 : 0);
+        top[q] = F.fl[q] + 1;
+        lay[q] = top[q] - 1 + (F.rk[q] < a ? 1 : 0);
         nz += lay[q] == 0;
         over |= lay[q] > L;
       }
@@ -1035,12 +1038,12 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
       double mt = 0, mc = 0;
 #pragma unroll
       for (int q = 0; q < NP; ++q) {
-        if (!D.act[q]) continue;
+        if (top[q] < 0) continue;
         if (lay[q] > 0 && lay[q] > mx) {
           mx = lay[q];
           qm = q;
         }
-        const int o = lay[q] == 0 ? DM + 2 : F.fl[q] + 1 - lay[q];
+        const int o = lay[q] == 0 ? DM + 2 : top[q] - lay[q];
         const double2 v = F.tc[q][o < 0 ? 0 : (o > DM + 2 ? DM + 2 : o)];
         if (v.x > mt) mt = v.x;
         if (v.y > mc) mc = v.y;
@@ -1202,6 +1205,7 @@ __global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace 
   const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
   const long long n_suf = sp.n_suf;
+  const int nsuf32 = sp.n_suf;
   long long b0 = kInfBits, k0 = LLONG_MAX, k1 = LLONG_MAX, k2 = LLONG_MAX, feasible = 0;
   unsigned n_tab = 0;
   __shared__ Prefix<R> sP[kK1Threads / 32];
@@ -1233,7 +1237,7 @@ __global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace 
       const long long ns = sp.cnt[R - 1][kp];
       const long long s0 = p == rg.p_lo ? rg.s_lo : 0;
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
-      for (long long s = s0 + lane; s < s1; s += 32) {
+      for (int s = (int)s0 + lane; s < (int)s1; s += 32) {  // (suffix indices fit 32 bits)
         const int4 A = __ldg(tb.sf_hot + s);  // fs, k|b1, rb01, rb23
         const int2 B = __ldg(tb.sf_zb + s);   // nzs0123, nzs4|bad
         const int fk = A.y & 0xffff;
@@ -1273,16 +1277,21 @@ __global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace 
         }
         ++n_tab;
         const double2 pa = F.pt[a][dP];
-        const double2 sb = tb.sf_st[(b * (kDonations + 1) + dS) * n_suf + s];
+        const double2 sb = tb.sf_st[(b * (kDonations + 1) + dS) * nsuf32 + s];
         double mt = pa.x, mc = pa.y;
         if (sb.x > mt) mt = sb.x;
         if (sb.y > mc) mc = sb.y;
         if (!(mt < __longlong_as_double(0x7ff0000000000000LL))) continue;  // memory-infeasible
         double tr = dtr;
         if (R > 1) tr += txs[(A.y >> 16) & 0xffff];
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          if (j + 1 < fk) tr += tb.sf_t[j * n_suf + s];
+        if (fk > 1) {  // internal transfers of the suffix, [s][4] (t0, t1, t2, 0)
+          const double2 t01 = __ldg(reinterpret_cast<const double2*>(tb.sf_t) + 2 * s);
+          tr += t01.x;
+          if (fk > 2) {
+            tr += t01.y;
+            if (fk > 3) tr += __ldg(tb.sf_t + 4 * s + 2);
+          }
+        }
         const double x = mt + fd[S] * mc + tr;
         ++feasible;
         const long long d = __double_as_longlong(x) - b0;
@@ -1994,7 +2003,7 @@ static size_t table_bytes(const HostSpace& h, int L, int max_blocks) {
   const size_t nsf = h.choices.size() + 1;
   add(sizeof(int4) * nsf);
   add(sizeof(int2) * nsf);
-  add(sizeof(double) * 3 * nsf);
+  add(sizeof(double) * 4 * nsf);
   add((size_t)kMsStride * nsf);
   add(sizeof(double2) * 5 * (kDonations + 1) * nsf);
   add(sizeof(int) * 3);
@@ -2039,7 +2048,7 @@ static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_bas
   const size_t nsf = h.choices.size() + 1;
   P.d_sf_hot = carve<int4>(tab, nsf);
   P.d_sf_zb = carve<int2>(tab, nsf);
-  P.d_sf_t = carve<double>(tab, 3 * nsf);
+  P.d_sf_t = carve<double>(tab, 4 * nsf);
   P.d_sf_ms = carve<signed char>(tab, (size_t)kMsStride * nsf);
   P.d_sf_st = carve<double2>(tab, 5 * (kDonations + 1) * nsf);
   P.d_nzs_max = carve<int>(tab, 3);
