@@ -29,6 +29,7 @@ def dump(name, obj):
 
 def main():
     shutil.copyfile(REF_PLAN, os.path.join(HERE, "desk_plan.json"))
+    shutil.copyfile(REF_PLAN.replace("plan.json", "explain.txt"), os.path.join(HERE, "desk_explain.txt"))
     # ---- full schedules (plan_to_json + trace)
     sched = {}
     for name, etas in (("c1_desk_mixed", [1, -1]), ("c2_16gpu", [-1]), ("c3_64gpu", [1, 2, 3, 4])):

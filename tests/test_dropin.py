@@ -30,3 +30,33 @@ def test_reference_scheduler_on_engine_matches_golden():
         assert line["plan"] == g["plan"], line["key"]
         assert line["trace"] == g["trace"], line["key"]
         assert line["engine_calls"] > 0
+
+
+CLI = os.path.join(ROOT, "oracle", "_ref", "rlsched_plan")
+
+
+@pytest.mark.skipif(not (os.path.exists(SHIM) and os.path.exists(CLI)),
+                    reason="libgplan_shim.so / rlsched_plan not built (need /root/reference at build time)")
+def test_cli_schedule_outputs_byte_identical(tmp_path):
+    """The reference CLI's `schedule` command (oracle/ref_cli.cpp over the unmodified
+    library) with and without the engine interposed: plan.json, explain.json, explain.txt
+    and stdout byte-identical; plan values and explain.txt equal the reference's committed
+    out/desk/ files."""
+    data = os.path.join(ROOT, "data")
+    args = [CLI, "--cluster", os.path.join(data, "clusters", "c1_desk_mixed.json"),
+            "--workload", os.path.join(data, "workloads", "c1_desk_mixed.json"),
+            "--calibration", os.path.join(data, "calibration", "c1_desk_mixed.json"), "--eta", "4"]
+    outs = {}
+    for label, env in (("cpu", dict(os.environ)), ("engine", dict(os.environ, LD_PRELOAD=SHIM, GPLAN_PROFILE="1"))):
+        d = tmp_path / label
+        r = subprocess.run(args + ["--out", str(d)], capture_output=True, env=env, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        if label == "engine":  # the shim's exit report: the seam calls went to the engine
+            assert b"gplan_shim constrained_search" in r.stderr and b"gplan_shim solve_milp" in r.stderr
+        outs[label] = {f: (d / f).read_bytes() for f in ("plan.json", "explain.json", "explain.txt")}
+        outs[label]["stdout"] = r.stdout
+    assert outs["engine"] == outs["cpu"]
+    plan = json.loads(outs["engine"]["plan.json"])
+    assert plan == golden("desk_plan.json")
+    with open(os.path.join(ROOT, "tests", "golden", "desk_explain.txt"), "rb") as f:
+        assert outs["engine"]["explain.txt"] == f.read()
