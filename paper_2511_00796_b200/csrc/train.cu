@@ -75,9 +75,6 @@ __device__ double block_min(double v, double* sm) {
   return r;
 }
 
-__device__ __forceinline__ bool better(double c1, long long r1, double c2, long long r2) {
-  return c1 < c2 || (c1 == c2 && r1 < r2);
-}
 
 // Window-independent argmin summary. The reference scores a layout by
 // cost = window * per_step (src/train_search.cpp, oracle/oracle.c:337) and keeps the first
