@@ -337,6 +337,42 @@ typedef struct {
  * train_ids: N ints. */
 int gp_exhaustive_optimum(gp_ctx* ctx, int32_t window, gp_exhaustive_result* out, int32_t* train_ids);
 
+/* ---- simulation of a scheduled plan ------------------------ */
+
+typedef struct {
+  int32_t window, staleness;          /* ScheduledPlan::window / ::staleness */
+  double c_train, c_update, c_reward; /* ScheduledPlan::costs (per window) */
+  int32_t n_entries;                  /* rollout_plan.entries */
+  const gp_config* configs;           /* entry configs (type_counts, n_stages, tp, throughput) */
+  const int32_t* replicas;            /* entry replica counts */
+  int32_t n_train, n_rollout;
+  const int32_t* train_ids;           /* partition.train_set (plan order) */
+  const int32_t* rollout_ids;         /* partition.rollout_set (plan order) */
+  const double* device_price;         /* $/hour per device id (cost reporting), n_devices */
+  int32_t n_buckets;                  /* workload length histogram (length, probability) */
+  const int32_t* bucket_len;
+  const double* bucket_prob;
+} gp_sim_plan;
+
+typedef struct {
+  int32_t steps_completed, pad;
+  double avg_step_time, avg_step_time_steady, throughput_tokens_per_s;
+  int64_t max_staleness_observed;
+  double rollout_stall_time, trainer_wait_time, rollout_busy_time, train_busy_time;
+  double sync_time_total, reward_time_total;
+  int64_t rollouts_produced, rollouts_consumed, rollouts_pending, rollouts_in_flight, tokens_consumed;
+  double total_time;
+  double dollar_cost_per_token;       /* NaN when the throughput is 0 (std::nullopt) */
+} gp_sim_report;
+
+/* simulate (src/simulator.cpp:381-403, events not recorded) for n_seeds seeds at once,
+ * one GPU thread per simulation (replica-parallel). used_devices (may be null): the
+ * concrete rollout device ids bound to replicas (same for every seed), n_rollout ints;
+ * n_used receives their count. GP_INVALID on the reference's ValidationErrors (no
+ * replicas, too few devices, deadlock), GP_CAPACITY when a queue exceeds its bound. */
+int gp_simulate(gp_ctx* ctx, const gp_sim_plan* plan, int32_t steps, int32_t sync_every, const uint64_t* seeds,
+                int32_t n_seeds, gp_sim_report* out, int32_t* used_devices, int32_t* n_used);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,7 @@
 #include "rlsched/plan_io.hpp"
 #include "rlsched/rollout_milp.hpp"
 #include "rlsched/scheduler.hpp"
+#include "rlsched/simulator.hpp"
 #include "rlsched/train_search.hpp"
 #include "rlsched/workload.hpp"
 
@@ -241,6 +242,43 @@ int ref_exhaustive_optimum(void* h, int window, char** out_json) {
     doc["objective"] = opt.objective;
     doc["train_set"] = opt.train_set;
     doc["seconds"] = secs;
+    *out_json = dup_string(doc.dump());
+  });
+}
+
+// simulate (src/simulator.cpp:381-403) of a plan document (plan_to_json form); the CLI's
+// simulate command applies the plan's staleness to the workload (src/cli.cpp:182-196).
+int ref_simulate(void* h, const char* plan_json, int steps, unsigned long long seed, int sync_every,
+                 char** out_json) {
+  return guarded([&] {
+    auto* ctx = static_cast<RefCtx*>(h);
+    ScheduledPlan plan = plan_from_json(plan_json);
+    WorkloadSpec work = ctx->work;
+    work.staleness = plan.staleness;
+    SimOptions opt;
+    opt.sync_every = sync_every;
+    opt.record_events = false;
+    SimReport r = simulate(plan, ctx->cluster, work, ctx->calib, steps, seed, opt);
+    ojson doc;
+    doc["steps_completed"] = r.steps_completed;
+    doc["avg_step_time"] = r.avg_step_time;
+    doc["avg_step_time_steady"] = r.avg_step_time_steady;
+    doc["throughput_tokens_per_s"] = r.throughput_tokens_per_s;
+    doc["max_staleness_observed"] = r.max_staleness_observed;
+    doc["rollout_stall_time"] = r.rollout_stall_time;
+    doc["trainer_wait_time"] = r.trainer_wait_time;
+    doc["rollout_busy_time"] = r.rollout_busy_time;
+    doc["train_busy_time"] = r.train_busy_time;
+    doc["sync_time_total"] = r.sync_time_total;
+    doc["reward_time_total"] = r.reward_time_total;
+    doc["rollouts_produced"] = r.rollouts_produced;
+    doc["rollouts_consumed"] = r.rollouts_consumed;
+    doc["rollouts_pending"] = r.rollouts_pending;
+    doc["rollouts_in_flight"] = r.rollouts_in_flight;
+    doc["tokens_consumed"] = r.tokens_consumed;
+    doc["total_time"] = r.total_time;
+    doc["dollar_cost_per_token"] = r.dollar_cost_per_token ? ojson(*r.dollar_cost_per_token) : ojson(nullptr);
+    doc["used_rollout_devices"] = r.used_rollout_devices;
     *out_json = dup_string(doc.dump());
   });
 }

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libgplan.so")
 
-SOURCES = ["capi.cu", "train.cu", "rollout.cu", "partition.cu", "schedule.cu", "exhaustive.cu"]
+SOURCES = ["capi.cu", "train.cu", "rollout.cu", "partition.cu", "schedule.cu", "exhaustive.cu", "simulate.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-prec-div=true", "-prec-sqrt=true",

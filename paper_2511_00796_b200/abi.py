@@ -107,6 +107,28 @@ class gp_exhaustive_result(C.Structure):
     ]
 
 
+class gp_sim_plan(C.Structure):
+    _fields_ = [
+        ("window", C.c_int32), ("staleness", C.c_int32), ("c_train", C.c_double), ("c_update", C.c_double),
+        ("c_reward", C.c_double), ("n_entries", C.c_int32), ("configs", C.POINTER(gp_config)),
+        ("replicas", i32p), ("n_train", C.c_int32), ("n_rollout", C.c_int32), ("train_ids", i32p),
+        ("rollout_ids", i32p), ("device_price", f64p), ("n_buckets", C.c_int32), ("bucket_len", i32p),
+        ("bucket_prob", f64p),
+    ]
+
+
+class gp_sim_report(C.Structure):
+    _fields_ = [
+        ("steps_completed", C.c_int32), ("pad", C.c_int32), ("avg_step_time", C.c_double),
+        ("avg_step_time_steady", C.c_double), ("throughput_tokens_per_s", C.c_double),
+        ("max_staleness_observed", C.c_int64), ("rollout_stall_time", C.c_double),
+        ("trainer_wait_time", C.c_double), ("rollout_busy_time", C.c_double), ("train_busy_time", C.c_double),
+        ("sync_time_total", C.c_double), ("reward_time_total", C.c_double), ("rollouts_produced", C.c_int64),
+        ("rollouts_consumed", C.c_int64), ("rollouts_pending", C.c_int64), ("rollouts_in_flight", C.c_int64),
+        ("tokens_consumed", C.c_int64), ("total_time", C.c_double), ("dollar_cost_per_token", C.c_double),
+    ]
+
+
 def default_train_opts() -> gp_train_opts:
     return gp_train_opts(4, 16)
 
@@ -145,6 +167,8 @@ def declare(lib: C.CDLL, prefix: str) -> None:
                                  C.c_int32, f64p],
             "train_candidates_search": [vp, i32p, C.c_int32, C.c_int32, P(gp_train_result), i32p],
             "exhaustive_optimum": [vp, C.c_int32, P(gp_exhaustive_result), i32p],
+            "simulate": [vp, P(gp_sim_plan), C.c_int32, C.c_int32, P(C.c_uint64), C.c_int32, P(gp_sim_report),
+                         i32p, i32p],
         })
     else:  # oracle: cluster/workload/calib pointers instead of a context
         cw = [P(gp_cluster), P(gp_workload)]

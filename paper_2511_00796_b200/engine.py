@@ -244,6 +244,49 @@ class Engine:
             res.append((int(st[i]), out[i], [ent[off[i] + k] for k in range(n)]))
         return res
 
+    def simulate(self, plan: dict, steps: int, seeds, sync_every: int = 1):
+        """simulate (src/simulator.cpp:381-403) of a plan document (plan_to_json form) under
+        this context's workload with the plan's staleness, one GPU thread per seed.
+        Returns ([report dict per seed], used rollout devices)."""
+        cl, w = self.problem.cluster, self.problem.workload
+        T = len(cl.type_names)
+        ents = plan["rollout_plan"]["entries"]
+        cfgs = (abi.gp_config * max(len(ents), 1))()
+        reps = np.zeros(max(len(ents), 1), dtype=np.int32)
+        for i, e in enumerate(ents):
+            for t in range(T):
+                cfgs[i].type_counts[t] = e["type_counts"][t]
+            cfgs[i].n_stages = len(e["tp_per_stage"])
+            for s, tp in enumerate(e["tp_per_stage"]):
+                cfgs[i].tp[s] = tp
+            cfgs[i].throughput = e["throughput_tps"]
+            reps[i] = e["replicas"]
+        train = _ids(plan["partition"]["train"])
+        roll = _ids(plan["partition"]["rollout"])
+        price = np.ascontiguousarray(cl.type_price[np.asarray(cl.device_type)], dtype=np.float64)
+        blen = np.array([int(l) for l, _ in w.histogram], dtype=np.int32)
+        bprob = np.array([float(p) for _, p in w.histogram], dtype=np.float64)
+        c = plan["costs"]
+        sp = abi.gp_sim_plan(int(plan["window_steps"]), int(plan["staleness"]), c["train_s"], c["update_s"],
+                             c["reward_s"], len(ents), cfgs, reps.ctypes.data_as(abi.i32p), len(train),
+                             len(roll), train.ctypes.data_as(abi.i32p), roll.ctypes.data_as(abi.i32p),
+                             price.ctypes.data_as(abi.f64p), len(blen), blen.ctypes.data_as(abi.i32p),
+                             bprob.ctypes.data_as(abi.f64p))
+        seeds = np.asarray(list(seeds), dtype=np.uint64)
+        out = (abi.gp_sim_report * max(len(seeds), 1))()
+        used = np.zeros(max(len(roll), 1), dtype=np.int32)
+        n_used = C.c_int32()
+        _check(lib().gp_simulate(self._h, C.byref(sp), steps, sync_every,
+                                 seeds.ctypes.data_as(C.POINTER(C.c_uint64)), len(seeds), out,
+                                 used.ctypes.data_as(abi.i32p), C.byref(n_used)))
+        reports = []
+        for i in range(len(seeds)):
+            r = {f: getattr(out[i], f) for f, _ in abi.gp_sim_report._fields_ if f != "pad"}
+            if r["dollar_cost_per_token"] != r["dollar_cost_per_token"]:
+                r["dollar_cost_per_token"] = None
+            reports.append(r)
+        return reports, used[:n_used.value].tolist()
+
     def set_memo(self, on: bool = True):
         """Enable (default) / disable + drop the window-independent constrained_search memo."""
         _check(lib().gp_ctx_set_memo(self._h, int(on)))

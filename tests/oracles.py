@@ -56,6 +56,7 @@ def ref_lib():
         _ref.ref_weight_sync.argtypes = [vp, abi.i32p, C.c_int, abi.i32p, C.c_int, C.c_int, cp,
                                          P(C.c_double)]
         _ref.ref_exhaustive_optimum.argtypes = [vp, C.c_int, P(vp)]
+        _ref.ref_simulate.argtypes = [vp, cp, C.c_int, C.c_ulonglong, C.c_int, P(vp)]
         _ref.ref_brute_milp.argtypes = [cp, abi.i32p, C.c_int, C.c_double, C.c_double, P(vp)]
         _ref.ref_partition_candidates.argtypes = [vp, C.c_double, C.c_double, C.c_double, C.c_double,
                                                   C.c_int, C.c_ulonglong, C.c_int, C.c_int, C.c_int,
@@ -122,6 +123,11 @@ class Ref:
     def exhaustive(self, window):
         out = C.c_void_p()
         return self._json(self.lib.ref_exhaustive_optimum(self.h, window, C.byref(out)), out)
+
+    def simulate(self, plan_json, steps, seed, sync_every=1):
+        out = C.c_void_p()
+        rc = self.lib.ref_simulate(self.h, plan_json.encode(), steps, seed, sync_every, C.byref(out))
+        return self._json(rc, out)
 
     def brute_milp(self, configs, caps, B, mean_len):
         caps = _ids(caps)
