@@ -311,7 +311,7 @@ static void score_layout_product(search_t* st) {
   const gp_workload* w = st->w;
   const int S = st->n_blocks;
   double f[GP_MAX_STAGES];
-  int layers[GP_MAX_STAGES], tps[GP_MAX_STAGES], dps[GP_MAX_STAGES];
+  int layers[GP_MAX_STAGES] = {0}, tps[GP_MAX_STAGES] = {0}, dps[GP_MAX_STAGES] = {0};
   int n_opt[GP_MAX_STAGES], opt_tp[GP_MAX_STAGES][4], pick[GP_MAX_STAGES];
   block_t blk[GP_MAX_STAGES];
   for (int s = 0; s < S; ++s) {
@@ -375,7 +375,7 @@ static void score_layout(search_t* st) {
   const gp_workload* w = st->w;
   const int S = st->n_blocks;
   double f[GP_MAX_STAGES];
-  int layers[GP_MAX_STAGES], tps[GP_MAX_STAGES], dps[GP_MAX_STAGES];
+  int layers[GP_MAX_STAGES] = {0}, tps[GP_MAX_STAGES] = {0}, dps[GP_MAX_STAGES] = {0};
   block_t blk[GP_MAX_STAGES];
   for (int s = 0; s < S; ++s) {
     blk[s].dev = st->sp->ordered + st->blk_start[s];
