@@ -1012,48 +1012,56 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
 #pragma unroll
   for (int q = 0; q < NP; ++q) fp_all += F.fl[q];
   const int a_lo = max(0, L - fp_all - fs_max - 4), a_hi = min(kp, L - fp_all - fs_min);
-  if (lane <= a_hi - a_lo) {
-    const int a = a_lo + lane;
-    int lay[PrefixFast<R>::NQ], top[PrefixFast<R>::NQ];  // layers; fl + 1 (-1: inactive slot)
-    int nz = 0;
-    bool over = false;
+  // One group of GS lanes per promotion count a, one lane per prefix stage slot: the
+  // per-stage values are reduced across the group (maxima of (total, compute), and the
+  // donor = the first slot with the most layers) for d = 0..dm water-filling donations.
+  constexpr int GS = NP <= 8 ? 8 : 16;
+  constexpr int GPW = 32 / GS;
+  const int grp = lane / GS, q = lane % GS;
+  const bool act = q < NP && D.act[q];
+  const int flq = act ? F.fl[q] : 0, rkq = act ? F.rk[q] : 0;
+  const double2* __restrict__ tcq = F.tc[q < NP ? q : 0];
+  const unsigned gmask = (GS == 32 ? 0xffffffffu : ((1u << GS) - 1u)) << (grp * GS);
+  for (int a0 = a_lo; a0 <= a_hi; a0 += GPW) {  // warp-uniform rounds
+    const int a = a0 + grp;
+    const bool ga = a <= a_hi;
+    int lay = act ? flq + (rkq < a ? 1 : 0) : 0;
+    int nz = (act && lay == 0) ? 1 : 0;
 #pragma unroll
-    for (int q = 0; q < NP; ++q) {  // shared-memory reads hoisted out of the donation loop
-      lay[q] = 0;
-      top[q] = -1;
-      if (D.act[q]) {
-        top[q] = F.fl[q] + 1;
-        lay[q] = top[q] - 1 + (F.rk[q] < a ? 1 : 0);
-        nz += lay[q] == 0;
-        over |= lay[q] > L;
-      }
-    }
+    for (int o = GS / 2; o >= 1; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    const bool over = (__ballot_sync(0xffffffffu, act && lay > L) & gmask) != 0;
     const int dm = min(DM, nz + nzs_max);
+    const int dm_w = __reduce_max_sync(0xffffffffu, ga ? dm : 0);
     bool live = true;
-    for (int d = 0; d <= dm; ++d) {
-      int mx = -1, qm = 0;
-      double mt = 0, mc = 0;
-#pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        if (top[q] < 0) continue;
-        if (lay[q] > 0 && lay[q] > mx) {
-          mx = lay[q];
-          qm = q;
-        }
-        const int o = lay[q] == 0 ? DM + 2 : top[q] - lay[q];
-        const double2 v = F.tc[q][o < 0 ? 0 : (o > DM + 2 ? DM + 2 : o)];
-        if (v.x > mt) mt = v.x;
-        if (v.y > mc) mc = v.y;
+    for (int d = 0; d <= dm_w; ++d) {
+      double vx = 0, vy = 0;  // an inactive slot adds nothing (the maxima start at 0)
+      if (act) {
+        const double2 v = tcq[lay == 0 ? DM + 2 : flq + 1 - lay];
+        vx = v.x > 0 ? v.x : 0.0;  // "if (v > m) m = v" from 0: NaN and non-positive values ignored
+        vy = v.y > 0 ? v.y : 0.0;
       }
-      F.pt[a][d] = make_double2(mt, mc);
-      F.mp[a][d] = (short)(live ? mx : -1);
-      if (mx < 2) live = false;  // a donor needs >= 2 layers (checked by the scan)
+      int key = (act && lay > 0) ? lay * 16 + (15 - q) : -1;  // most layers, then the first slot
 #pragma unroll
-      for (int q = 0; q < NP; ++q)
-        if (live && q == qm) lay[q]--;
+      for (int o = GS / 2; o >= 1; o >>= 1) {
+        const double ox = __shfl_xor_sync(0xffffffffu, vx, o), oy = __shfl_xor_sync(0xffffffffu, vy, o);
+        const int ok = __shfl_xor_sync(0xffffffffu, key, o);
+        if (ox > vx) vx = ox;
+        if (oy > vy) vy = oy;
+        key = max(key, ok);
+      }
+      const int mx = key < 0 ? -1 : key >> 4;
+      const int qm = key < 0 ? 0 : 15 - (key & 15);
+      if (ga && d <= dm && q == 0) {
+        F.pt[a][d] = make_double2(vx, vy);
+        F.mp[a][d] = (short)(live ? mx : -1);
+      }
+      if (mx < 2) live = false;  // a donor needs >= 2 layers (checked by the scan)
+      if (live && act && q == qm) --lay;
     }
-    F.nzp[a] = (unsigned char)nz;
-    if (over) atomicOr(&F.bad, 1 << a);
+    if (ga && q == 0) {
+      F.nzp[a] = (unsigned char)nz;
+      if (over) atomicOr(&F.bad, 1 << a);
+    }
   }
   if (lane == 0) {
     int fp = 0;
