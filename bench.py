@@ -351,7 +351,7 @@ def run_b200(args):
     return 0
 
 
-def time_to_best_plan(device, keys=("c3_64gpu/eta=1", "c4_256gpu/eta=2")):
+def time_to_best_plan(device, keys=("c3_64gpu/eta=1", "c4_256gpu/eta=2", "c5_1024gpu/eta=2")):
     """schedule() wall time (all window passes, up to the final plan) through the native
     batched driver (gp_schedule) on a freshly created context (context setup excluded,
     like the reference's input loading); the reference's own schedule() on one host core
@@ -381,6 +381,8 @@ def time_to_best_plan(device, keys=("c3_64gpu/eta=1", "c4_256gpu/eta=2")):
             row["plan_identical"] = ref == plan
         elif name == "c4_256gpu":
             row["reference_cpu_s"] = "did not finish in 25 min (SURVEY.md 6)"
+        elif name == "c5_1024gpu":
+            row["reference_cpu_s"] = "infeasible: materialises 4.3e11 layouts per pass (SURVEY.md 8a A5)"
         out[key] = row
     return out
 

@@ -863,6 +863,13 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
   atomicMax(nzs_max, zmax);
   atomicMax(nzs_max + 1, kFsBias - fs);  // suffix floor-sum range: min via the bias
   atomicMax(nzs_max + 2, fs);
+  // most zero-layer stages per (floor sum, promotion count): bounds the fix-ups a prefix
+  // promotion count can meet (a candidate with promotions a, b has fs = L - fp - a - b)
+  if (fs >= 0 && fs <= L)
+    for (int b = 0; b <= 4; ++b) {
+      const int z = b < 4 ? (int)((nzs >> (8 * b)) & 0xff) : (int)nz4;
+      if (z > 0) atomicMax(nzs_max + 3 + fs * 5 + b, z);
+    }
 }
 
 constexpr int kK1Threads = 128;
@@ -1030,7 +1037,13 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
 #pragma unroll
     for (int o = GS / 2; o >= 1; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
     const bool over = (__ballot_sync(0xffffffffu, act && lay > L) & gmask) != 0;
-    const int dm = min(DM, nz + nzs_max);
+    int zs = 0;  // most suffix zero-layer stages a candidate with promotion count a can meet
+    if (ga)
+      for (int b = 0; b <= 4; ++b) {
+        const int fs = L - fp_all - a - b;
+        if (fs >= 0 && fs <= L) zs = max(zs, tb.nzs_max[3 + fs * 5 + b]);
+      }
+    const int dm = min(DM, nz + min(zs, nzs_max));
     const int dm_w = __reduce_max_sync(0xffffffffu, ga ? dm : 0);
     bool live = true;
     for (int d = 0; d <= dm_w; ++d) {
@@ -2011,7 +2024,7 @@ static size_t table_bytes(const HostSpace& h, int L, int max_blocks) {
   add(sizeof(double) * 4 * nsf);
   add((size_t)kMsStride * nsf);
   add(sizeof(double2) * 5 * (kDonations + 1) * nsf);
-  add(sizeof(int) * 3);
+  add(sizeof(int) * (3 + 5 * (L + 1)));
   add(sizeof(NearMin) * (max_blocks + kDeferBlocks));
   return bytes;
 }
@@ -2056,7 +2069,7 @@ static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_bas
   P.d_sf_t = carve<double>(tab, 4 * nsf);
   P.d_sf_ms = carve<signed char>(tab, (size_t)kMsStride * nsf);
   P.d_sf_st = carve<double2>(tab, 5 * (kDonations + 1) * nsf);
-  P.d_nzs_max = carve<int>(tab, 3);
+  P.d_nzs_max = carve<int>(tab, 3 + 5 * (P.L + 1));
   P.d_partial = carve<NearMin>(tab, P.max_blocks + kDeferBlocks);
 }
 
@@ -2150,7 +2163,7 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
     ctx->launches += 2;
     if (fast) {
       k2e_block_shares<<<(h.nblk + 255) / 256, 256, 0, stream>>>(P.d_blkf, h.nblk, h.flops_total, P.d_blk_sh);
-      GP_CUDA(cudaMemsetAsync(P.d_nzs_max, 0, 3 * sizeof(int), stream));
+      GP_CUDA(cudaMemsetAsync(P.d_nzs_max, 0, (3 + 5 * (L + 1)) * sizeof(int), stream));
       k2f_suffix_fast<<<(ns + 127) / 128, 128, 0, stream>>>(P.d_suf, ns, P.d_blk_sh, P.d_stage, L,
                                                            h.sp.blk_off[h.sp.R - 1], P.d_sf_hot, P.d_sf_zb,
                                                            P.d_sf_t, P.d_sf_ms, P.d_sf_st, P.d_nzs_max);
