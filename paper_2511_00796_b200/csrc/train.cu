@@ -1101,6 +1101,7 @@ struct ScanRange {
   long long p_lo, s_lo, p_hi, s_hi;  // candidates (p, s) with (p_lo,s_lo) <= (p,s) < (p_hi,s_hi)
   long long n_pref;                  // prefixes touched
   long long chunk;                   // prefixes per warp work item
+  int defer_all;                     // test hook (GPLAN_K1_DEFER_ALL=1): K1-fast defers every candidate
 };
 
 constexpr int kDeferBlocks = 64;  // CTAs of k1_deferred (their partials follow K1-fast's)
@@ -1261,7 +1262,7 @@ __global__ void __launch_bounds__(kK1Threads, 8) k1_layout_scan_fast(TrainSpace 
         const int fk = A.y & 0xffff;
         const int S = kp + fk;
         const int extra = L - (fp + A.x);
-        bool slow = (unsigned)extra >= (unsigned)S;
+        bool slow = (unsigned)extra >= (unsigned)S || rg.defer_all;
         int a = 0, b = 0, dP = 0, dS = 0;
         if (!slow) {
           if (R > 1) {  // branch-free: unused stage slots hold block 0 and are masked
@@ -1733,6 +1734,8 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   ScanRange rg{};
   rank_split(h, lo, rg.p_lo, rg.s_lo);
   rank_split(h, hi, rg.p_hi, rg.s_hi);
+  const char* defer_env = std::getenv("GPLAN_K1_DEFER_ALL");
+  rg.defer_all = defer_env && defer_env[0] == '1';
   rg.n_pref = rg.p_hi - rg.p_lo + (rg.s_hi > 0 ? 1 : 0);
   const int threads = kK1Threads;
   static int occ_g = 0, occ_f = 0;

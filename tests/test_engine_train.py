@@ -229,3 +229,20 @@ def test_four_type_runs(monkeypatch):
         assert run(name, s, 2) == orc.constrained_search(s, 2), s
         checked += 1
     assert checked >= 5
+
+
+def test_deferred_and_overflow_paths(monkeypatch):
+    """K1-fast's generic fallback: with every candidate deferred (test hook), a range that
+    fits the device queue is scored by k1_deferred, a larger one overflows it and is rescanned
+    by the generic K1 — both equal to the normal scan."""
+    name = "c5_1024gpu"
+    p = problem(name)
+    ids = list(range(p.cluster.n))[:-1]
+    total = engine(name).train_space(ids)
+    for lo, hi in ((total // 4, total // 4 + 1_500_000), (total // 2, total // 2 + 3_000_000)):
+        want = run(name, ids, 3, lo=lo, hi=hi)
+        assert want["feasible"] > 0
+        monkeypatch.setenv("GPLAN_K1_DEFER_ALL", "1")
+        got = run(name, ids, 3, lo=lo, hi=hi)
+        monkeypatch.delenv("GPLAN_K1_DEFER_ALL")
+        assert got == want, (lo, hi)
