@@ -67,3 +67,20 @@ def test_exhaustive_optimum_beyond_reference_limit(name):
     want = Oracle(problem(name)).exhaustive(3)
     got = engine(name).exhaustive(3)
     assert got == want
+
+
+def test_product_space_large_set_fast_equals_generic(monkeypatch):
+    """Product-space search on a 3.4e6-layout C4 set: the K1-fast tables built from the
+    minimal-total stage table equal the generic scan (candidate count, cost, index, plan)."""
+    name = "c4_256gpu"
+    p = problem(name)
+    eng = engine(name)
+    ids = list(range(1, p.cluster.n))
+    res, devs = eng.train_candidates_search(ids, 3)
+    fast = train_result_dict(res, devs)
+    monkeypatch.setenv("GPLAN_K1_GENERIC", "1")
+    res, devs = eng.train_candidates_search(ids, 3)
+    generic = train_result_dict(res, devs)
+    monkeypatch.delenv("GPLAN_K1_GENERIC")
+    assert fast == generic
+    assert fast["found"] and fast["layouts"] > 3_000_000
