@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <vector>
 
 #include "gp_internal.h"
@@ -33,7 +34,7 @@ int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_tr
 int train_candidates_meta(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_result* res,
                           const int32_t* stage_devices, long long* count, long long* index);
 int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* ns, const gp_rollout_opts* o,
-                  std::vector<std::vector<gp_config>>& out);
+                  std::vector<std::vector<gp_config>>& out, std::vector<int>* uniq_of = nullptr);
 int weight_sync_batch(gp_ctx* ctx, int q, const int32_t* const* train, const int32_t* nt,
                       const int32_t* const* roll, const int32_t* nr, const int32_t* const* etype,
                       const int32_t* const* erep, const int32_t* ne, int window, double* out);
@@ -238,32 +239,47 @@ int exhaustive_optimum(gp_ctx* ctx, int window, gp_exhaustive_result* out, int32
     ph[1] += since(t0);
     t0 = now();
     std::vector<std::vector<gp_config>> cfgs;
-    rc = configs_batch(ctx, q, rp.data(), rn.data(), &ro, cfgs);
+    std::vector<int> cfg_class;
+    rc = configs_batch(ctx, q, rp.data(), rn.data(), &ro, cfgs, &cfg_class);
     if (rc) return rc;
     ph[2] += since(t0);
     t0 = now();
-    std::vector<int> live;
+    // The brute MILP depends only on (configs, capacities, B): sets sharing a config class
+    // and per-type capacities share one solve.
+    std::vector<int> live, job_of;
     std::vector<const std::vector<gp_config>*> bc;
     std::vector<std::vector<int32_t>> caps;
     std::vector<const int32_t*> capp;
     std::vector<double> Bs;
+    std::map<std::vector<int32_t>, int> job_index;
     for (int i = 0; i < q; ++i) {
       if (!tres[i].found || cfgs[i].empty()) continue;
       live.push_back(i);
     }
-    caps.resize(live.size());
+    std::vector<int32_t> key(T + 1);
     for (size_t j = 0; j < live.size(); ++j) {
       const int i = live[j];
-      caps[j].assign(T, 0);
-      for (int d : rl[i]) caps[j][ctx->h_type[d]]++;  // rollout_capacities (src/rollout_milp.cpp:113-120)
+      std::fill(key.begin(), key.end(), 0);
+      key[T] = cfg_class[i];
+      for (int d : rl[i]) key[ctx->h_type[d]]++;  // rollout_capacities (src/rollout_milp.cpp:113-120)
+      auto ins = job_index.emplace(key, (int)caps.size());
+      job_of.push_back(ins.first->second);
+      if (!ins.second) continue;
+      caps.emplace_back(key.begin(), key.begin() + T);
       bc.push_back(&cfgs[i]);
-      capp.push_back(caps[j].data());
       Bs.push_back(total_rollouts);
     }
-    std::vector<std::vector<int>> counts;
-    std::vector<BruteOut> bo;
-    rc = brute_batch(ctx, (int)live.size(), bc, capp, Bs, ctx->work.mean_len, counts, bo);
+    for (auto& c : caps) capp.push_back(c.data());
+    std::vector<std::vector<int>> jcounts;
+    std::vector<BruteOut> jbo;
+    rc = brute_batch(ctx, (int)caps.size(), bc, capp, Bs, ctx->work.mean_len, jcounts, jbo);
     if (rc) return rc;
+    std::vector<const std::vector<int>*> counts(live.size());
+    std::vector<BruteOut> bo(live.size());
+    for (size_t j = 0; j < live.size(); ++j) {
+      counts[j] = &jcounts[job_of[j]];
+      bo[j] = jbo[job_of[j]];
+    }
     ph[3] += since(t0);
     t0 = now();
     std::vector<int> wl;
@@ -274,12 +290,13 @@ int exhaustive_optimum(gp_ctx* ctx, int window, gp_exhaustive_result* out, int32
       out->replica_vectors += bo[j].vectors;
       if (!bo[j].feasible) continue;
       const int i = live[j];
-      for (size_t c = 0; c < counts[j].size(); ++c) {
-        if (counts[j][c] <= 0) continue;
+      const std::vector<int>& cj = *counts[j];
+      for (size_t c = 0; c < cj.size(); ++c) {
+        if (cj[c] <= 0) continue;
         int type = 0;  // ReplicaConfig::gpu_type
         while (type < T && cfgs[i][c].type_counts[type] == 0) ++type;
         et[j].push_back(type);
-        er[j].push_back(counts[j][c]);
+        er[j].push_back(cj[c]);
       }
       wl.push_back((int)j);
       wt.push_back(tp[i]);

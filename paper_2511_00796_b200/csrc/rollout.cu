@@ -23,6 +23,7 @@
 #include <climits>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <numeric>
 #include <vector>
@@ -446,15 +447,21 @@ int rollout_capacities(gp_ctx* ctx, const int32_t* ids, int n, int32_t* caps) {
 // host derives each set's per-type machine availability (enumeration metadata), one
 // K3 launch scores every (set, type, TP multiset) candidate, one copy brings them back.
 int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* ns, const gp_rollout_opts* o,
-                  std::vector<std::vector<gp_config>>& out) {
+                  std::vector<std::vector<gp_config>>& out, std::vector<int>* uniq_out) {
   out.assign(q, {});
   if (o->max_stages < 0 || o->max_stages > 4)
     return set_error(GP_INVALID, "rollout max_stages must lie in [0, 4] for the sm_100a kernel");
   const int T = ctx->T;
-  std::vector<int> avail((size_t)q * T * 4, 0), nm((size_t)q * T, 0);
+  // The configuration list of a set depends only on its per-type machine availability
+  // (the four largest per-machine device counts and the machine count of each type), so
+  // sets are deduplicated on that signature and K3 runs once per distinct signature.
+  std::vector<int> avail, nm;
+  std::vector<int> uniq_of(q, -1);
+  std::map<std::vector<int>, int> sig_index;
   std::vector<CfgCand> cands;
   std::vector<int> per_machine(ctx->M, 0), mtype(ctx->M, -1);
   std::vector<char> seen(ctx->N, 0);
+  std::vector<int> sig((size_t)T * 5);
   for (int si = 0; si < q; ++si) {
     const int32_t* id = ids[si];
     const int n = ns[si];
@@ -474,18 +481,27 @@ int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* 
     std::vector<std::vector<int>> by_type(T);
     for (int m = 0; m < ctx->M; ++m)
       if (per_machine[m]) by_type[mtype[m]].push_back(per_machine[m]);
+    std::fill(sig.begin(), sig.end(), 0);
     for (int t = 0; t < T; ++t) {
       auto& v = by_type[t];
       std::sort(v.rbegin(), v.rend());
-      nm[(size_t)si * T + t] = (int)v.size();
-      for (int k = 0; k < 4 && k < (int)v.size(); ++k) avail[((size_t)si * T + t) * 4 + k] = v[k];
-      if (v.empty()) continue;
+      sig[(size_t)t * 5] = (int)v.size();
+      for (int k = 0; k < 4 && k < (int)v.size(); ++k) sig[(size_t)t * 5 + 1 + k] = v[k];
+    }
+    auto ins = sig_index.emplace(sig, (int)sig_index.size());
+    uniq_of[si] = ins.first->second;
+    if (!ins.second) continue;
+    const int ui = ins.first->second;
+    for (int t = 0; t < T; ++t) {
+      nm.push_back(sig[(size_t)t * 5]);
+      for (int k = 0; k < 4; ++k) avail.push_back(sig[(size_t)t * 5 + 1 + k]);
+      if (by_type[t].empty()) continue;
       // candidates in reference order: stages, then tp_multisets over {8,4,2,1}
       for (int S = 1; S <= std::min(o->max_stages, 4); ++S) {
         int tp[4];
         std::function<void(int, int)> rec = [&](int d, int mx) {
           if (d == S) {
-            CfgCand c{t, S, {0, 0, 0, 0}, si};
+            CfgCand c{t, S, {0, 0, 0, 0}, ui};
             for (int u = 0; u < S; ++u) c.tp[u] = tp[u];
             cands.push_back(c);
             return;
@@ -501,7 +517,10 @@ int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* 
     }
   }
   const int nc = (int)cands.size();
-  if (nc == 0) return GP_OK;
+  if (nc == 0) {
+    if (uniq_out) *uniq_out = std::move(uniq_of);
+    return GP_OK;
+  }
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
   add(sizeof(CfgCand) * nc);
@@ -537,8 +556,11 @@ int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* 
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
   const gp_config* h_cfg = reinterpret_cast<const gp_config*>(hp);
   const int* h_keep = reinterpret_cast<const int*>(hp + ((char*)d_keep - (char*)d_out));
+  std::vector<std::vector<gp_config>> uniq(sig_index.size());
   for (int i = 0; i < nc; ++i)
-    if (h_keep[i]) out[cands[i].set].push_back(h_cfg[i]);
+    if (h_keep[i]) uniq[cands[i].set].push_back(h_cfg[i]);
+  for (int si = 0; si < q; ++si) out[si] = uniq[uniq_of[si]];
+  if (uniq_out) *uniq_out = std::move(uniq_of);
   return GP_OK;
 }
 
@@ -547,7 +569,7 @@ int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opt
   *n_out = 0;
   if (n <= 0) return set_error(GP_INVALID, "enumerate_configs requires a non-empty rollout set");
   std::vector<std::vector<gp_config>> res;
-  int rc = configs_batch(ctx, 1, &ids, &n, o, res);
+  int rc = configs_batch(ctx, 1, &ids, &n, o, res, nullptr);
   if (rc) return rc;
   const int k = (int)res[0].size();
   for (int i = 0; i < k && i < cap; ++i) out[i] = res[0][i];

@@ -26,7 +26,7 @@ namespace gp {
 int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
                 const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices, int mode = 0);
 int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* ns, const gp_rollout_opts* o,
-                  std::vector<std::vector<gp_config>>& out);
+                  std::vector<std::vector<gp_config>>& out, std::vector<int>* uniq_of = nullptr);
 int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs, const int32_t* const* caps,
                int dims, const double* Bs, double len, gp_rollout_result* outs, gp_rollout_entry* const* entries,
                int* rcs);

@@ -21,6 +21,7 @@
 // Every fp64 expression keeps the reference's association order; the library
 // is compiled with --fmad=false, so results are bit-identical to the CPU.
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -1965,6 +1966,7 @@ struct PreparedTrain {
 // GPLAN_PROFILE=1: memo hits / scanned sets / scanned layouts (stderr at exit)
 struct MemoStats {
   long long hits = 0, scans = 0, layouts = 0;
+  double ph[5] = {0, 0, 0, 0, 0};  // train_batch_run: build, carve+upload, launch, wait, fill
   unsigned long long fast_cnt[2] = {0, 0};
   void poll() {  // after a synchronisation
     if (!std::getenv("GPLAN_PROFILE")) return;
@@ -1978,8 +1980,9 @@ struct MemoStats {
       std::fprintf(stderr, "k1 fast: %llu candidates from tables, %llu by the generic fallback\n", fast_cnt[0],
                    fast_cnt[1]);
     if (std::getenv("GPLAN_PROFILE"))
-      std::fprintf(stderr, "train memo: %lld hits, %lld scanned sets, %lld scanned layouts\n", hits, scans,
-                   layouts);
+      std::fprintf(stderr, "train memo: %lld hits, %lld scanned sets, %lld scanned layouts; batch phases: "
+                   "build %.3f s, carve+upload %.3f s, launch %.3f s, wait %.3f s, fill %.3f s\n", hits, scans,
+                   layouts, ph[0], ph[1], ph[2], ph[3], ph[4]);
   }
 } g_memo_stats;
 
@@ -2377,6 +2380,12 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
   nms.assign(n_sets, {});
   ordered.assign(n_sets, {});
   if (n_sets <= 0) return GP_OK;
+  auto tick = std::chrono::steady_clock::now();
+  auto lap = [&](int k) {
+    const auto t = std::chrono::steady_clock::now();
+    g_memo_stats.ph[k] += std::chrono::duration<double>(t - tick).count();
+    tick = t;
+  };
   std::vector<PreparedTrain> Ps(n_sets);
   size_t ib = 0, tbytes = 0;
   for (int i = 0; i < n_sets; ++i) {
@@ -2389,6 +2398,7 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
     tbytes += table_bytes(Ps[i].h, Ps[i].L, Ps[i].max_blocks);
   }
   const size_t out_bytes = sizeof(TrainOut) * n_sets;
+  lap(0);
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
   char* base = static_cast<char*>(ctx_scratch(ctx, ib + tbytes + out_bytes + 1024, kArenaTrain));
   if (!base) return GP_CUDA_ERROR;
@@ -2402,6 +2412,7 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
   const size_t in_bytes = (size_t)(in - base);
   GP_CUDA(cudaMemcpyAsync(base, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h2d_bytes += (long long)in_bytes;
+  lap(1);
   // the sets run on kTrainLanes streams so that small sets overlap on the GPU
   constexpr int NL = gp_ctx::kTrainLanes;
   if (!ctx->lane[0]) {
@@ -2487,7 +2498,9 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
   TrainOut* ho = reinterpret_cast<TrainOut*>(hp);
   GP_CUDA(cudaMemcpyAsync(ho, d_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
   ctx->d2h_bytes += (long long)out_bytes;
+  lap(2);
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  lap(3);
   for (int i = 0; i < n_sets; ++i) {
     if (Ps[i].h.total > 0 && ho[i].overflow) {  // rescan with the generic K1
       int rc = launch_prepared(ctx, Ps[i], window, 0, -1, ctx->stream, false, true);
@@ -2504,6 +2517,7 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
     g_memo_stats.scans++;
     g_memo_stats.layouts += Ps[i].h.total;
   }
+  lap(4);
   g_memo_stats.poll();
   return GP_OK;
 }
