@@ -1020,24 +1020,39 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
 #pragma unroll
   for (int q = 0; q < NP; ++q) fp_all += F.fl[q];
   const int a_lo = max(0, L - fp_all - fs_max - 4), a_hi = min(kp, L - fp_all - fs_min);
-  // One group of GS lanes per promotion count a, one lane per prefix stage slot: the
-  // per-stage values are reduced across the group (maxima of (total, compute), and the
-  // donor = the first slot with the most layers) for d = 0..dm water-filling donations.
-  constexpr int GS = NP <= 8 ? 8 : 16;
+  // One group of GS = 4 lanes per promotion count a (eight per round), R - 1 prefix stage
+  // slots per lane (slot q = lane % 4 + 4 j): the per-stage values are reduced across the group
+  // (maxima of (total, compute), and the donor = the first slot with the most layers) for
+  // d = 0..dm water-filling donations.
+  constexpr int GS = 4;
+  constexpr int SPL = NP >= GS ? NP / GS : 1;  // = R - 1 (R = 1 returned above)
   constexpr int GPW = 32 / GS;
-  const int grp = lane / GS, q = lane % GS;
-  const bool act = q < NP && D.act[q];
-  const int flq = act ? F.fl[q] : 0, rkq = act ? F.rk[q] : 0;
-  const double2* __restrict__ tcq = F.tc[q < NP ? q : 0];
-  const unsigned gmask = (GS == 32 ? 0xffffffffu : ((1u << GS) - 1u)) << (grp * GS);
+  const int grp = lane / GS, ql = lane % GS;
+  bool actv[SPL];
+  int flv[SPL], rkv[SPL];
+#pragma unroll
+  for (int j = 0; j < SPL; ++j) {
+    const int q = ql + GS * j;
+    actv[j] = q < NP && D.act[q];
+    flv[j] = actv[j] ? F.fl[q] : 0;
+    rkv[j] = actv[j] ? F.rk[q] : 0;
+  }
+  const unsigned gmask = ((1u << GS) - 1u) << (grp * GS);
   for (int a0 = a_lo; a0 <= a_hi; a0 += GPW) {  // warp-uniform rounds
     const int a = a0 + grp;
     const bool ga = a <= a_hi;
-    int lay = act ? flq + (rkq < a ? 1 : 0) : 0;
-    int nz = (act && lay == 0) ? 1 : 0;
+    int lay[SPL];
+    int nz = 0;
+    bool ov = false;
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      lay[j] = actv[j] ? flv[j] + (rkv[j] < a ? 1 : 0) : 0;
+      nz += (actv[j] && lay[j] == 0) ? 1 : 0;
+      ov |= actv[j] && lay[j] > L;
+    }
 #pragma unroll
     for (int o = GS / 2; o >= 1; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
-    const bool over = (__ballot_sync(0xffffffffu, act && lay > L) & gmask) != 0;
+    const bool over = (__ballot_sync(0xffffffffu, ov) & gmask) != 0;
     int zs = 0;  // most suffix zero-layer stages a candidate with promotion count a can meet
     if (ga)
       for (int b = 0; b <= 4; ++b) {
@@ -1049,12 +1064,18 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
     bool live = true;
     for (int d = 0; d <= dm_w; ++d) {
       double vx = 0, vy = 0;  // an inactive slot adds nothing (the maxima start at 0)
-      if (act) {
-        const double2 v = tcq[lay == 0 ? DM + 2 : flq + 1 - lay];
-        vx = v.x > 0 ? v.x : 0.0;  // "if (v > m) m = v" from 0: NaN and non-positive values ignored
-        vy = v.y > 0 ? v.y : 0.0;
+      int key = -1;           // most layers, then the first slot
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) {
+        if (!actv[j]) continue;
+        const int q = ql + GS * j;
+        const double2 v = F.tc[q][lay[j] == 0 ? DM + 2 : flv[j] + 1 - lay[j]];
+        // "if (v > m) m = v" from 0: NaN and non-positive values ignored
+        const double tx = v.x > 0 ? v.x : 0.0, ty = v.y > 0 ? v.y : 0.0;
+        if (tx > vx) vx = tx;
+        if (ty > vy) vy = ty;
+        if (lay[j] > 0) key = max(key, lay[j] * 16 + (15 - q));
       }
-      int key = (act && lay > 0) ? lay * 16 + (15 - q) : -1;  // most layers, then the first slot
 #pragma unroll
       for (int o = GS / 2; o >= 1; o >>= 1) {
         const double ox = __shfl_xor_sync(0xffffffffu, vx, o), oy = __shfl_xor_sync(0xffffffffu, vy, o);
@@ -1064,15 +1085,19 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
         key = max(key, ok);
       }
       const int mx = key < 0 ? -1 : key >> 4;
-      const int qm = key < 0 ? 0 : 15 - (key & 15);
-      if (ga && d <= dm && q == 0) {
+      const int qm = key < 0 ? -1 : 15 - (key & 15);
+      if (ga && d <= dm && ql == 0) {
         F.pt[a][d] = make_double2(vx, vy);
         F.mp[a][d] = (short)(live ? mx : -1);
       }
       if (mx < 2) live = false;  // a donor needs >= 2 layers (checked by the scan)
-      if (live && act && q == qm) --lay;
+      if (live) {
+#pragma unroll
+        for (int j = 0; j < SPL; ++j)
+          if (actv[j] && ql + GS * j == qm) --lay[j];
+      }
     }
-    if (ga && q == 0) {
+    if (ga && ql == 0) {
       F.nzp[a] = (unsigned char)nz;
       if (over) atomicOr(&F.bad, 1 << a);
     }
