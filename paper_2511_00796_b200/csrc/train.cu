@@ -874,6 +874,7 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
 }
 
 constexpr int kK1Threads = 128;
+constexpr int kZsTable = 128;  // > L on the fast path
 constexpr int kMaxLastBlocks = 1024;  // last type run blocks with a per-prefix rank count (else generic K1)
 
 // Warp-uniform fast-path data of one prefix (shared memory).
@@ -953,7 +954,7 @@ __device__ __forceinline__ void prefix_data_warp(int lane, const TrainSpace& sp,
 template <int R>
 __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, const TrainTables& tb, int L,
                                             int3 sstat, PrefixData<R>& D, PrefixFast<R>& F,
-                                            unsigned char* cntb, double* txs) {
+                                            unsigned char* cntb, double* txs, const int* zst) {
   const int sp_nc_last = sp.nc[R - 1], blk_off_last = sp.blk_off[R - 1];
   constexpr int NP = PrefixData<R>::NP;
   constexpr int NPP = PrefixFast<R>::NPP;
@@ -1053,12 +1054,9 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
 #pragma unroll
     for (int o = GS / 2; o >= 1; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
     const bool over = (__ballot_sync(0xffffffffu, ov) & gmask) != 0;
-    int zs = 0;  // most suffix zero-layer stages a candidate with promotion count a can meet
-    if (ga)
-      for (int b = 0; b <= 4; ++b) {
-        const int fs = L - fp_all - a - b;
-        if (fs >= 0 && fs <= L) zs = max(zs, tb.nzs_max[3 + fs * 5 + b]);
-      }
+    // most suffix zero-layer stages a candidate with promotion count a can meet
+    const int za = fp_all + a;
+    const int zs = (ga && za < kZsTable) ? zst[za] : 0;
     const int dm = min(DM, nz + min(zs, nzs_max));
     const int dm_w = __reduce_max_sync(0xffffffffu, ga ? dm : 0);
     bool live = true;
@@ -1266,6 +1264,17 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
   unsigned char* const cntb = sL[threadIdx.x >> 5].cntb;
   double* const txs = sL[threadIdx.x >> 5].txs;
   for (int i = threadIdx.x; i <= GP_MAX_STAGES; i += blockDim.x) fd[i] = tb.fd_coef[i];
+  // zst[t]: most zero-layer suffix stages over the (floor sum, promotion count b) pairs a
+  // candidate whose prefix floors plus promotions total t can meet (fs = L - t - b)
+  __shared__ int zst[kZsTable];
+  for (int t = threadIdx.x; t < kZsTable; t += blockDim.x) {
+    int z = 0;
+    for (int b = 0; b <= 4; ++b) {
+      const int fs = L - t - b;
+      if (fs >= 0 && fs <= L) z = max(z, tb.nzs_max[3 + fs * 5 + b]);
+    }
+    zst[t] = z;
+  }
   __syncthreads();
   for (long long it = warp; it < n_items; it += n_warps) {
     long long p = rg.p_lo + it * rg.chunk;
@@ -1275,7 +1284,7 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
     for (; p < p_end; ++p) {
       __syncwarp();
       prefix_data_warp<R>(lane, sp, tb, P, D, F);
-      prefix_fast<R>(lane, sp, tb, L, sstat, D, F, cntb, txs);
+      prefix_fast<R>(lane, sp, tb, L, sstat, D, F, cntb, txs, zst);
       const int kp = D.u;
       const int fp = F.fp, pbad = F.bad;
       const double dtr = D.transfers;
