@@ -1327,8 +1327,8 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
             else ++dS;
           }
         }
-        const long long key = p * n_suf + s;
         if (slow) {
+          const long long key = p * n_suf + s;
           const unsigned long long at = atomicAdd(slow_q, 1ULL);
           if (at < (unsigned long long)kSlowQueue) slow_q[1 + at] = (unsigned long long)key;
           continue;
@@ -1353,7 +1353,8 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
         const double x = mt + fd[S] * mc + tr;
         ++feasible;
         const long long d = __double_as_longlong(x) - b0;
-        if (d < 3) {
+        if (d < 3) {  // (the key is formed only here and on the deferred path)
+          const long long key = p * n_suf + s;
           if (d < 0) {
             k2 = d == -1 ? k1 : d == -2 ? k0 : LLONG_MAX;
             k1 = d == -1 ? k0 : LLONG_MAX;
