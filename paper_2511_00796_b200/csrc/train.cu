@@ -1291,6 +1291,8 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
       const long long ns = sp.cnt[R - 1][kp];
       const long long s0 = p == rg.p_lo ? rg.s_lo : 0;
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
+      // table-scored count: every candidate of this lane, less the deferred ones (below)
+      if (s0 + lane < s1) n_tab += (unsigned)((s1 - s0 - lane + 31) >> 5);
 #pragma unroll 2  // (with 6 CTAs/SM: two candidates in flight per lane, measured +10%)
       for (int s = (int)s0 + lane; s < (int)s1; s += 32) {  // (suffix indices fit 32 bits)
         const int4 A = __ldg(tb.sf_hot + s);  // fs, k|b1, rb01, rb23
@@ -1331,9 +1333,9 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
           const long long key = p * n_suf + s;
           const unsigned long long at = atomicAdd(slow_q, 1ULL);
           if (at < (unsigned long long)kSlowQueue) slow_q[1 + at] = (unsigned long long)key;
+          --n_tab;
           continue;
         }
-        ++n_tab;
         const double2 pa = F.pt[a][dP];
         const double2 sb = tb.sf_st[(b * (kDonations + 1) + dS) * nsuf32 + s];
         double mt = pa.x, mc = pa.y;
