@@ -1317,8 +1317,8 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
           }
           a = extra - b;
           slow = ((pbad >> a) | (B.y >> (8 + b))) & 1;
-          const unsigned long long nzs = ((unsigned long long)(unsigned)B.y << 32) | (unsigned)B.x;
-          const int nz = F.nzp[a] + (int)((nzs >> (8 * b)) & 0xff);
+          // byte b of the 40-bit zero-count word {B.y:B.x} (b <= 4): one PRMT
+          const int nz = F.nzp[a] + (int)(__byte_perm((unsigned)B.x, (unsigned)B.y, (unsigned)b) & 0xff);
           if (nz > kDonations) slow = true;
           // zero-layer fix-up: each donation comes from the side holding the first maximum
           // (the prefix on ties: its stages come first); a donor must keep >= 1 layer
