@@ -1309,7 +1309,8 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
             // test holds (both sides < 128, so no borrow crosses a byte)
             const unsigned c0 = cntb[A.z & 0xffff], c1 = cntb[(unsigned)A.z >> 16];
             const unsigned c2 = cntb[A.w & 0xffff], c3 = cntb[(unsigned)A.w >> 16];
-            const unsigned w = (c0 | (c1 << 8) | (c2 << 16) | (c3 << 24)) + 0x04030201u;
+            const unsigned w = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410) +
+                               0x04030201u;  // bytes (c0, c1, c2, c3), each < 128
             const unsigned ge = ((unsigned)extra * 0x01010101u + 0x80808080u) - w;
             b = __popc(ge & (0x80808080u >> (32 - 8 * fk)));
           } else {
