@@ -41,8 +41,8 @@ WINDOW = 3
 METRIC = "candidate plans evaluated/sec"
 # from the committed ncu capture of K1-fast on this workload (profiles/r01/)
 K1_PROFILE = "profiles/r01/k1_layout_scan_fast_ncu_summary.txt"
-K1_WARP_INST_PER_CAND = 6.245   # smsp__inst_executed.sum / candidates (15,087,995,285 / 2,415,919,104)
-K1_DRAM_BYTES_PER_LAUNCH = 391424  # dram__bytes_read.sum + dram__bytes_write.sum (tables stay in L2)
+K1_WARP_INST_PER_CAND = 6.152   # smsp__inst_executed.sum / candidates (14,861,502,869 / 2,415,919,104)
+K1_DRAM_BYTES_PER_LAUNCH = 390400  # dram__bytes_read.sum + dram__bytes_write.sum (tables stay in L2)
 UNIT = "plans/s"
 
 
