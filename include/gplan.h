@@ -233,6 +233,15 @@ int gp_ctx_set_memo(gp_ctx* ctx, int on);
 int gp_train_timing(gp_ctx* ctx, float* k2_ms, float* k1_ms);
 void gp_ctx_io_bytes(gp_ctx* ctx, long long* h2d, long long* d2h, double* sum_stages);
 int gp_fp64_peak(gp_ctx* ctx, double* dadd_per_s);
+/* Test hook (parity of individual candidates, not a reference interface): per_step
+ * (train_cost_breakdown(...).per_step, src/cost_model.cpp:93-126) of every layout of
+ * ranks [lo, hi) of the train set, computed by the scan kernel itself (its DUMP
+ * instantiation), +inf for layouts without a memory-feasible option. path 0: the kernel
+ * constrained_search would use (K1-fast when eligible), 1: the generic K1, 2: K1-fast with
+ * every candidate deferred to its generic fallback. hi - lo <= 2^26. *fast_used (optional)
+ * is set to 1 when K1-fast scored the range. */
+int gp_debug_layout_costs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* opts,
+                          int64_t lo, int64_t hi, int32_t path, double* per_step, int32_t* fast_used);
 
 /* ---- rollout side: replaces enumerate_configs / rollout_capacities / solve_milp
  *      (src/rollout_milp.cpp:113-254) ------------------------------------- */

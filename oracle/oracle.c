@@ -261,6 +261,7 @@ typedef struct {
   int product;  /* enumerate_train_candidates product space instead of constrained_search */
   int64_t cand; /* product-space candidates visited */
   int err;
+  double* dump; /* optional: per_step of ranks [lo, hi) (+inf: no memory-feasible option) */
 } search_t;
 
 /* max_devices_per_machine (src/train_search.cpp:124-131). A block lies inside one
@@ -299,8 +300,7 @@ static double plan_step_cost(const search_t* st, const block_t* blk, int S, cons
       }
     }
   }
-  double per_step = max_stage + fill + transfers;
-  return st->window * per_step;
+  return max_stage + fill + transfers;  /* per_step; cost = window * per_step */
 }
 
 /* one block list of enumerate_train_candidates (src/train_search.cpp:179-216): every
@@ -344,7 +344,7 @@ static void score_layout_product(search_t* st) {
     }
     if (fits) {
       st->feasible++;
-      double cost = plan_step_cost(st, blk, S, layers, tps, dps);
+      double cost = st->window * plan_step_cost(st, blk, S, layers, tps, dps);
       if (!st->have_best || cost < st->best_cost) {
         st->have_best = 1;
         st->best_cost = cost;
@@ -406,10 +406,15 @@ static void score_layout(search_t* st) {
         dps[s] = dp;
       }
     }
-    if (best_comm < 0) return; /* dead layout */
+    if (best_comm < 0) { /* dead layout */
+      if (st->dump) st->dump[st->rank - st->lo] = HUGE_VAL;
+      return;
+    }
   }
   st->feasible++;
-  double cost = plan_step_cost(st, blk, S, layers, tps, dps);
+  double per_step = plan_step_cost(st, blk, S, layers, tps, dps);
+  if (st->dump) st->dump[st->rank - st->lo] = per_step;
+  double cost = st->window * per_step;
   if (!st->have_best || cost < st->best_cost) {
     st->have_best = 1;
     st->best_cost = cost;
@@ -514,9 +519,10 @@ int or_train_space(const gp_cluster* c, const gp_workload* w, const int32_t* ids
 }
 
 /* constrained_search (src/train_search.cpp:268-325), restricted to ranks [lo, hi). */
-int or_constrained_search(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
-                          const int32_t* ids, int32_t n, int32_t window, const gp_train_opts* opts,
-                          int64_t lo, int64_t hi, gp_train_result* out, int32_t* stage_devices) {
+static int constrained_search_impl(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                                   const int32_t* ids, int32_t n, int32_t window,
+                                   const gp_train_opts* opts, int64_t lo, int64_t hi,
+                                   gp_train_result* out, int32_t* stage_devices, double* dump) {
   memset(out, 0, sizeof *out);
   if (n <= 0) return fail(GP_INVALID, "constrained_search requires a non-empty train set");
   layout_space_t sp;
@@ -534,6 +540,7 @@ int or_constrained_search(const gp_cluster* c, const gp_workload* w, const gp_ca
   st.lo = lo;
   st.hi = hi;
   st.scoring = 1;
+  st.dump = dump;
   if (sp.max_stages >= sp.n_runs && lo < hi) recurse_runs(&st, 0, 0);
   out->layouts = hi > lo ? hi - lo : 0;
   out->feasible = st.feasible;
@@ -559,6 +566,24 @@ int or_constrained_search(const gp_cluster* c, const gp_workload* w, const gp_ca
   }
   space_free(&sp);
   return GP_OK;
+}
+
+int or_constrained_search(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                          const int32_t* ids, int32_t n, int32_t window, const gp_train_opts* opts,
+                          int64_t lo, int64_t hi, gp_train_result* out, int32_t* stage_devices) {
+  return constrained_search_impl(c, w, k, ids, n, window, opts, lo, hi, out, stage_devices, NULL);
+}
+
+/* per_step (train_cost_breakdown(...).per_step, src/cost_model.cpp:123) of every layout of
+ * ranks [lo, hi) in enumeration order, +inf for layouts without a memory-feasible option
+ * (src/train_search.cpp:260-266). hi must not exceed the space size. */
+int or_layout_costs(const gp_cluster* c, const gp_workload* w, const gp_calib* k, const int32_t* ids,
+                    int32_t n, const gp_train_opts* opts, int64_t lo, int64_t hi, double* per_step) {
+  gp_train_result res;
+  int32_t* devs = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  int rc = constrained_search_impl(c, w, k, ids, n, 1, opts, lo, hi, &res, devs, per_step);
+  free(devs);
+  return rc;
 }
 
 int or_train_candidates_search(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
@@ -1003,4 +1028,424 @@ int or_exhaustive_optimum(const gp_cluster* c, const gp_workload* w, const gp_ca
     for (int d = 0; d < n; ++d)
       if (m & (1u << d)) train_ids[out->n_train++] = d;
   return GP_OK;
+}
+
+/* ============================================ table-memoised constrained_search
+ * TEST INFRASTRUCTURE: the same restatement as or_constrained_search above, with the
+ * pure sub-results memoised so a full C5 train set (2.4e9 layouts) finishes on the host
+ * cores in minutes. Nothing is re-associated: each memo holds the value the plain
+ * restatement computes —
+ *   * min_link_within_groups per (block, tp option) and min_link_between per adjacent
+ *     block pair (src/cost_model.cpp:12-47; exact minima over the device-pair matrix);
+ *   * the per-stage option pick + train_stage_cost per (block, layer count)
+ *     (src/train_search.cpp:241-265, src/cost_model.cpp:57-91, total_layers == L);
+ *   * the block FLOPS left fold (src/train_search.cpp:229-232).
+ * Per layout it runs allocate_layers (src/train_search.cpp:146-177) and
+ * train_cost_breakdown's max / fill-drain / transfer fold (src/cost_model.cpp:93-126)
+ * exactly as above, and keeps the first rank of minimal window*per_step per window.
+ * Independent of every engine shortcut (constant allocation totals, promotion/donation
+ * tables, machine-pair link tables, near-minimum summaries). Rank ranges are split over
+ * pthreads; per-window (cost, rank) minima merge lexicographically. */
+#include <pthread.h>
+#include <stdatomic.h>
+
+typedef struct {
+  int start, n, type, per_machine;
+  double f, cap0;
+  double beta_tp[4], beta_dp[4];
+  double* tot;       /* [L] stage total of the comm-minimal memory-feasible option */
+  double* comp;      /* [L] compute */
+  signed char* ok;   /* [L] 0: no memory-feasible option */
+} tab_block_t;
+
+typedef struct {
+  layout_space_t* sp;
+  const gp_workload* w;
+  const gp_calib* k;
+  int L;
+  int n_pos[GP_MAX_TYPES];          /* cut positions incl. 0 and len: nc + 2 */
+  int* pos[GP_MAX_TYPES];
+  int blk_off[GP_MAX_TYPES];
+  tab_block_t* blk;                 /* per run: [i][j] for 0 <= i < j < n_pos */
+  double* tin[GP_MAX_TYPES];        /* [i][j][l]: beta between (i,j) and (j,l) of run r */
+  double* tx[GP_MAX_TYPES];         /* [i][l]: beta between (i, last) of run r and (0, l) of r+1 */
+  int n_windows;
+  const int32_t* windows;
+} tab_t;
+
+static int tab_bid(const tab_t* t, int r, int i, int j) {
+  return t->blk_off[r] + i * t->n_pos[r] + j;
+}
+
+static void tab_free(tab_t* t) {
+  for (int r = 0; r < t->sp->n_runs; ++r) {
+    free(t->pos[r]);
+    free(t->tin[r]);
+    free(t->tx[r]);
+  }
+  if (t->blk) {
+    int nb = t->blk_off[t->sp->n_runs];
+    for (int b = 0; b < nb; ++b) {
+      free(t->blk[b].tot);
+      free(t->blk[b].comp);
+      free(t->blk[b].ok);
+    }
+  }
+  free(t->blk);
+}
+
+static void tab_block_fill(tab_t* t, tab_block_t* b) {
+  const gp_cluster* c = t->sp->c;
+  const gp_workload* w = t->w;
+  const gp_calib* k = t->k;
+  const int32_t* dev = t->sp->ordered + b->start;
+  const int L = t->L;
+  double f = 0;
+  for (int i = 0; i < b->n; ++i) f += c->device_flops[dev[i]];
+  b->f = f;
+  b->type = c->device_type[dev[0]];
+  b->cap0 = c->device_hbm_cap[dev[0]];
+  b->per_machine = max_per_machine(c, dev, b->n);
+  static const int tp_opts[4] = {1, 2, 4, 8};
+  for (int o = 0; o < 4; ++o) {
+    b->beta_tp[o] = b->beta_dp[o] = K_INF;
+    int tp = tp_opts[o];
+    if (tp > b->per_machine || b->n % tp != 0) continue;
+    int dp = b->n / tp;
+    if (tp > 1) b->beta_tp[o] = min_link_groups(c, dev, b->n, tp, 0, 0);
+    if (dp > 1) b->beta_dp[o] = min_link_groups(c, dev, b->n, dp, 1, tp);
+  }
+  b->tot = (double*)malloc(sizeof(double) * (size_t)L);
+  b->comp = (double*)malloc(sizeof(double) * (size_t)L);
+  b->ok = (signed char*)malloc((size_t)L);
+  const double tokens = w_tokens(w);
+  for (int layers = 1; layers <= L; ++layers) {
+    double best_comm = -1, best_tot = 0, best_comp = 0;
+    for (int o = 0; o < 4; ++o) {
+      int tp = tp_opts[o];
+      if (tp > b->per_machine || b->n % tp != 0) continue;
+      int dp = b->n / tp;
+      double need_gb = mem_train_gb(w, k, tp, dp, layers);
+      if (need_gb * 1e9 > b->cap0) continue;
+      /* train_stage_cost (as above) with the memoised betas; total_layers == L */
+      stage_cost_t sc = {0, 0, 0};
+      double lf = (double)layers / L;
+      double need = 6.0 * w_params(w) * tokens * lf;
+      sc.compute = need / (k->compute_eff[b->type] * f);
+      if (tp > 1 && tokens > 0) {
+        double prt = tokens / dp;
+        double vol = k->tp_allreduce_coeff * layers * prt * w->hidden_dim * K_ACT_BYTES * 2.0 *
+                     (tp - 1) / tp;
+        sc.tp_comm = vol / b->beta_tp[o];
+      }
+      if (dp > 1) {
+        double shard = w_params(w) * lf * k->grad_bytes_per_param / tp;
+        double vol = 2.0 * shard * (dp - 1) / dp;
+        sc.dp_comm = vol / b->beta_dp[o];
+      }
+      double comm = sc.tp_comm + sc.dp_comm;
+      if (best_comm < 0 || comm < best_comm) {
+        best_comm = comm;
+        best_tot = sc.compute + sc.tp_comm + sc.dp_comm;  /* TrainStageCost::total() */
+        best_comp = sc.compute;
+      }
+    }
+    b->ok[layers - 1] = best_comm >= 0;
+    b->tot[layers - 1] = best_tot;
+    b->comp[layers - 1] = best_comp;
+  }
+}
+
+static double tab_between(const tab_t* t, int s0, int n0, int s1, int n1) {
+  block_t a = {t->sp->ordered + s0, n0}, b = {t->sp->ordered + s1, n1};
+  return min_link_between(t->sp->c, a, b);
+}
+
+static int tab_build(tab_t* t, layout_space_t* sp, const gp_workload* w, const gp_calib* k) {
+  memset(t, 0, sizeof *t);
+  t->sp = sp;
+  t->w = w;
+  t->k = k;
+  t->L = w->num_layers;
+  int nb = 0;
+  for (int r = 0; r < sp->n_runs; ++r) {
+    int np = sp->n_cuts[r] + 2;
+    t->n_pos[r] = np;
+    t->pos[r] = (int*)malloc(sizeof(int) * (size_t)np);
+    t->pos[r][0] = 0;
+    for (int i = 0; i < sp->n_cuts[r]; ++i) t->pos[r][i + 1] = sp->cuts[r][i];
+    t->pos[r][np - 1] = sp->run_len[r];
+    t->blk_off[r] = nb;
+    nb += np * np;
+  }
+  t->blk_off[sp->n_runs] = nb;
+  t->blk = (tab_block_t*)calloc((size_t)nb, sizeof(tab_block_t));
+  for (int r = 0; r < sp->n_runs; ++r) {
+    int np = t->n_pos[r];
+    for (int i = 0; i < np; ++i)
+      for (int j = i + 1; j < np; ++j) {
+        tab_block_t* b = &t->blk[tab_bid(t, r, i, j)];
+        b->start = sp->run_start[r] + t->pos[r][i];
+        b->n = t->pos[r][j] - t->pos[r][i];
+        tab_block_fill(t, b);
+      }
+    t->tin[r] = (double*)malloc(sizeof(double) * (size_t)np * np * np);
+    for (int i = 0; i < np; ++i)
+      for (int j = i + 1; j < np; ++j)
+        for (int l = j + 1; l < np; ++l) {
+          const tab_block_t* a = &t->blk[tab_bid(t, r, i, j)];
+          const tab_block_t* b = &t->blk[tab_bid(t, r, j, l)];
+          t->tin[r][((size_t)i * np + j) * np + l] = tab_between(t, a->start, a->n, b->start, b->n);
+        }
+    if (r + 1 < sp->n_runs) {
+      int np2 = sp->n_cuts[r + 1] + 2;
+      t->tx[r] = (double*)malloc(sizeof(double) * (size_t)np * np2);
+      for (int i = 0; i + 1 < np; ++i)
+        for (int l = 1; l < np2; ++l) {
+          int s0 = sp->run_start[r] + t->pos[r][i], n0 = sp->run_len[r] - t->pos[r][i];
+          int s1 = sp->run_start[r + 1], n1 = t->pos[r + 1][l];
+          t->tx[r][(size_t)i * np2 + l] = tab_between(t, s0, n0, s1, n1);
+        }
+    }
+  }
+  return 0;
+}
+
+#define TAB_MAX_WINDOWS 8
+typedef struct {
+  const tab_t* t;
+  int64_t rank, lo, hi, feasible;
+  int S;
+  int run_of[GP_MAX_STAGES], pi[GP_MAX_STAGES], pj[GP_MAX_STAGES];
+  int have[TAB_MAX_WINDOWS];
+  double best_cost[TAB_MAX_WINDOWS];
+  int64_t best_rank[TAB_MAX_WINDOWS];
+  double* dump;  /* per_step of ranks [lo, hi) (+inf: no memory-feasible option) */
+} tab_search_t;
+
+static void tab_score(tab_search_t* s) {
+  const tab_t* t = s->t;
+  const gp_workload* w = t->w;
+  const int S = s->S, L = t->L;
+  double f[GP_MAX_STAGES];
+  int layers[GP_MAX_STAGES];
+  const tab_block_t* blk[GP_MAX_STAGES];
+  for (int q = 0; q < S; ++q) {
+    blk[q] = &t->blk[tab_bid(t, s->run_of[q], s->pi[q], s->pj[q])];
+    f[q] = blk[q]->f;
+  }
+  allocate_layers(L, f, S, layers);
+  double max_stage = 0, max_compute = 0;
+  for (int q = 0; q < S; ++q) {
+    if (!blk[q]->ok[layers[q] - 1]) {
+      if (s->dump) s->dump[s->rank - s->lo] = HUGE_VAL;
+      return;
+    }
+    double tot = blk[q]->tot[layers[q] - 1], cmp = blk[q]->comp[layers[q] - 1];
+    if (tot > max_stage) max_stage = tot;
+    if (cmp > max_compute) max_compute = cmp;
+  }
+  double fill = 0, transfers = 0;
+  const double tokens = w_tokens(w);
+  if (S > 1) {
+    fill = (double)(S - 1) / w->micro_batches * max_compute;
+    if (tokens > 0) {
+      for (int q = 0; q + 1 < S; ++q) {
+        double beta;
+        int r = s->run_of[q];
+        if (s->run_of[q + 1] == r) {
+          int np = t->n_pos[r];
+          beta = t->tin[r][((size_t)s->pi[q] * np + s->pj[q]) * np + s->pj[q + 1]];
+        } else {
+          beta = t->tx[r][(size_t)s->pi[q] * t->n_pos[r + 1] + s->pj[q + 1]];
+        }
+        transfers += tokens * w->hidden_dim * K_ACT_BYTES / beta;
+      }
+    }
+  }
+  double per_step = max_stage + fill + transfers;
+  s->feasible++;
+  if (s->dump) s->dump[s->rank - s->lo] = per_step;
+  for (int i = 0; i < t->n_windows; ++i) {
+    double cost = t->windows[i] * per_step;
+    if (!s->have[i] || cost < s->best_cost[i]) {
+      s->have[i] = 1;
+      s->best_cost[i] = cost;
+      s->best_rank[i] = s->rank;
+    }
+  }
+}
+
+static void tab_runs(tab_search_t* s, int r, int used);
+
+static void tab_cuts(tab_search_t* s, int r, int used, int k, int chosen, int next, int prev_i) {
+  const layout_space_t* sp = s->t->sp;
+  if (chosen == k - 1) {
+    s->run_of[used + chosen] = r;
+    s->pi[used + chosen] = prev_i;
+    s->pj[used + chosen] = sp->n_cuts[r] + 1;
+    int64_t size = sp->cnt[r + 1][used + k];
+    if (s->rank + size <= s->lo || s->rank >= s->hi) {
+      s->rank += size;
+      return;
+    }
+    tab_runs(s, r + 1, used + k);
+    return;
+  }
+  int remaining = k - 1 - chosen;
+  for (int ci = next; ci + remaining <= sp->n_cuts[r]; ++ci) {
+    s->run_of[used + chosen] = r;
+    s->pi[used + chosen] = prev_i;
+    s->pj[used + chosen] = ci + 1;
+    tab_cuts(s, r, used, k, chosen + 1, ci + 1, ci + 1);
+  }
+}
+
+static void tab_runs(tab_search_t* s, int r, int used) {
+  const layout_space_t* sp = s->t->sp;
+  if (r == sp->n_runs) {
+    if (s->rank >= s->lo && s->rank < s->hi) {
+      s->S = used;
+      tab_score(s);
+    }
+    s->rank++;
+    return;
+  }
+  int remaining_runs = sp->n_runs - r - 1;
+  int kmax = sp->max_per_run < sp->run_len[r] ? sp->max_per_run : sp->run_len[r];
+  for (int k = 1; k <= kmax; ++k) {
+    if (used + k + remaining_runs > sp->max_stages) break;
+    tab_cuts(s, r, used, k, 0, 0, 0);
+  }
+}
+
+typedef struct {
+  const tab_t* t;
+  int64_t lo, hi, chunk;
+  atomic_llong next;
+  pthread_mutex_t mu;
+  tab_search_t acc;
+  double* dump;
+} tab_job_t;
+
+static void tab_merge(tab_search_t* into, const tab_search_t* s, int n_windows) {
+  into->feasible += s->feasible;
+  for (int i = 0; i < n_windows; ++i) {
+    if (!s->have[i]) continue;
+    if (!into->have[i] || s->best_cost[i] < into->best_cost[i] ||
+        (s->best_cost[i] == into->best_cost[i] && s->best_rank[i] < into->best_rank[i])) {
+      into->have[i] = 1;
+      into->best_cost[i] = s->best_cost[i];
+      into->best_rank[i] = s->best_rank[i];
+    }
+  }
+}
+
+static void* tab_worker(void* arg) {
+  tab_job_t* j = (tab_job_t*)arg;
+  tab_search_t loc;
+  memset(&loc, 0, sizeof loc);
+  for (;;) {
+    int64_t a = atomic_fetch_add(&j->next, j->chunk);
+    if (a >= j->hi) break;
+    int64_t b = a + j->chunk < j->hi ? a + j->chunk : j->hi;
+    tab_search_t s;
+    memset(&s, 0, sizeof s);
+    s.t = j->t;
+    s.lo = a;
+    s.hi = b;
+    s.dump = j->dump ? j->dump + (a - j->lo) : NULL;
+    tab_runs(&s, 0, 0);
+    tab_merge(&loc, &s, j->t->n_windows);
+  }
+  pthread_mutex_lock(&j->mu);
+  tab_merge(&j->acc, &loc, j->t->n_windows);
+  pthread_mutex_unlock(&j->mu);
+  return NULL;
+}
+
+/* constrained_search over ranks [lo, hi) for several windows at once (one scan):
+ * out_cost/out_rank[i] = the reference's (cost, rank) winner for windows[i]
+ * (out_rank = -1 when no layout is memory-feasible); *feasible = memory-feasible layouts;
+ * dump (optional, hi-lo doubles): per_step of every rank (+inf when infeasible). */
+int or_constrained_search_tab(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                              const int32_t* ids, int32_t n, const gp_train_opts* opts,
+                              const int32_t* windows, int32_t n_windows, int64_t lo, int64_t hi,
+                              int32_t threads, double* out_cost, int64_t* out_rank,
+                              int64_t* feasible, int64_t* layouts, double* dump) {
+  if (n <= 0) return fail(GP_INVALID, "constrained_search requires a non-empty train set");
+  if (n_windows < 1 || n_windows > TAB_MAX_WINDOWS) return fail(GP_INVALID, "1..8 windows");
+  layout_space_t sp;
+  int rc = space_build(&sp, c, w, ids, n, opts);
+  if (rc) return rc;
+  int64_t total = count_layouts(&sp);
+  if (hi < 0 || hi > total) hi = total;
+  if (lo < 0) lo = 0;
+  *layouts = total;
+  tab_t t;
+  tab_build(&t, &sp, w, k);
+  t.n_windows = n_windows;
+  t.windows = windows;
+  tab_job_t job;
+  memset(&job, 0, sizeof job);
+  job.t = &t;
+  job.lo = lo;
+  job.hi = hi;
+  job.dump = dump;
+  if (threads < 1) threads = 1;
+  int64_t span = hi > lo ? hi - lo : 0;
+  job.chunk = span / (threads * 64) + 1;
+  if (job.chunk < 4096) job.chunk = 4096;
+  atomic_init(&job.next, lo);
+  pthread_mutex_init(&job.mu, NULL);
+  if (sp.max_stages >= sp.n_runs && lo < hi) {
+    pthread_t th[256];
+    if (threads > 256) threads = 256;
+    for (int i = 0; i < threads; ++i) pthread_create(&th[i], NULL, tab_worker, &job);
+    for (int i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+  }
+  pthread_mutex_destroy(&job.mu);
+  *feasible = job.acc.feasible;
+  for (int i = 0; i < n_windows; ++i) {
+    out_cost[i] = job.acc.have[i] ? job.acc.best_cost[i] : 0.0;
+    out_rank[i] = job.acc.have[i] ? job.acc.best_rank[i] : -1;
+  }
+  tab_free(&t);
+  space_free(&sp);
+  return GP_OK;
+}
+
+/* per_step of the layouts of several rank ranges [lo[i], hi[i]) (concatenated into out),
+ * the memoised tables built once (as or_constrained_search_tab's dump). */
+int or_layout_costs_tab(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                        const int32_t* ids, int32_t n, const gp_train_opts* opts, int32_t n_ranges,
+                        const int64_t* lo, const int64_t* hi, double* out) {
+  if (n <= 0) return fail(GP_INVALID, "constrained_search requires a non-empty train set");
+  layout_space_t sp;
+  int rc = space_build(&sp, c, w, ids, n, opts);
+  if (rc) return rc;
+  int64_t total = count_layouts(&sp);
+  tab_t t;
+  tab_build(&t, &sp, w, k);
+  int32_t one = 1;
+  t.n_windows = 1;
+  t.windows = &one;
+  size_t off = 0;
+  for (int i = 0; i < n_ranges && !rc; ++i) {
+    if (lo[i] < 0 || hi[i] > total || lo[i] > hi[i]) {
+      rc = fail(GP_INVALID, "rank range outside the layout space");
+      break;
+    }
+    tab_search_t s;
+    memset(&s, 0, sizeof s);
+    s.t = &t;
+    s.lo = lo[i];
+    s.hi = hi[i];
+    s.dump = out + off;
+    if (sp.max_stages >= sp.n_runs && lo[i] < hi[i]) tab_runs(&s, 0, 0);
+    off += (size_t)(hi[i] - lo[i]);
+  }
+  tab_free(&t);
+  space_free(&sp);
+  return rc;
 }

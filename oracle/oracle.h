@@ -26,6 +26,23 @@ int or_constrained_search(const gp_cluster* c, const gp_workload* w, const gp_ca
                           const int32_t* ids, int32_t n, int32_t window, const gp_train_opts* opts,
                           int64_t lo, int64_t hi, gp_train_result* out, int32_t* stage_devices);
 
+/* per_step of every layout of ranks [lo, hi) (+inf: no memory-feasible option) */
+int or_layout_costs(const gp_cluster* c, const gp_workload* w, const gp_calib* k, const int32_t* ids,
+                    int32_t n, const gp_train_opts* opts, int64_t lo, int64_t hi, double* per_step);
+/* constrained_search over ranks [lo, hi) with memoised pure sub-results (min-links, stage
+ * picks, block FLOPS), several windows in one scan, pthreads over rank chunks. out_rank[i]
+ * = -1: nothing feasible. dump (optional): per_step of every rank, as or_layout_costs. */
+int or_constrained_search_tab(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                              const int32_t* ids, int32_t n, const gp_train_opts* opts,
+                              const int32_t* windows, int32_t n_windows, int64_t lo, int64_t hi,
+                              int32_t threads, double* out_cost, int64_t* out_rank,
+                              int64_t* feasible, int64_t* layouts, double* dump);
+
+/* per_step of several rank ranges [lo[i], hi[i]) concatenated into out (tables built once) */
+int or_layout_costs_tab(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
+                        const int32_t* ids, int32_t n, const gp_train_opts* opts, int32_t n_ranges,
+                        const int64_t* lo, const int64_t* hi, double* out);
+
 int or_enumerate_configs(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
                          const int32_t* ids, int32_t n, const gp_rollout_opts* opts,
                          gp_config* out, int32_t cap, int32_t* n_out);
@@ -51,6 +68,7 @@ typedef struct {
   int32_t restarts;
   int32_t expand_window;
   double band_widen_step;    /* 0.05 */
+  int32_t tab_threads;       /* > 0: large train sets via or_constrained_search_tab (threads) */
 } or_sched_opts;
 
 /* Writes a malloc'd JSON document with the plan_to_json fields (values only,

@@ -501,6 +501,7 @@ typedef struct {
   iter_t** memo;
   int n_memo, cap_memo;
   int err;
+  int tab_threads;  /* > 0: table-memoised constrained_search for spaces > 1e5 layouts */
 } search_phase_t;
 
 static int same_set(const int* a, int na, const int* b, int nb) {
@@ -523,7 +524,31 @@ static int evaluate_partition(search_phase_t* sp, const int* train, int nt, cons
   it->c_reward = w->reward_cost_const;
   gp_train_opts to = {4, 16};
   it->stage_dev = (int*)malloc(sizeof(int) * (size_t)(nt > 0 ? nt : 1));
-  int rc = or_constrained_search(c, w, sp->k, train, nt, sp->window, &to, 0, -1, &it->tr, it->stage_dev);
+  int rc;
+  int64_t space = 0;
+  if (sp->tab_threads > 0 && or_train_space(c, w, train, nt, &to, &space) == GP_OK && space > 100000) {
+    /* table-memoised scan for the winner's rank, then the plain restatement on that one rank
+     * for the plan (its cost is the same value) */
+    double cost;
+    int64_t rank, feasible, layouts;
+    int32_t win = sp->window;
+    rc = or_constrained_search_tab(c, w, sp->k, train, nt, &to, &win, 1, 0, -1, sp->tab_threads, &cost,
+                                   &rank, &feasible, &layouts, NULL);
+    if (rc) return rc;
+    if (rank >= 0) {
+      rc = or_constrained_search(c, w, sp->k, train, nt, sp->window, &to, rank, rank + 1, &it->tr,
+                                 it->stage_dev);
+      if (rc) return rc;
+      it->tr.rank = rank;
+      it->tr.cost = cost;
+    } else {
+      memset(&it->tr, 0, sizeof it->tr);
+    }
+    it->tr.layouts = layouts;
+    it->tr.feasible = feasible;
+  } else {
+    rc = or_constrained_search(c, w, sp->k, train, nt, sp->window, &to, 0, -1, &it->tr, it->stage_dev);
+  }
   if (rc) return rc;
   it->train_found = it->tr.found;
   double B = (double)w->batch_rollouts * sp->window;
@@ -859,6 +884,7 @@ int or_schedule(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
     sp.w = &eff;
     sp.k = k;
     sp.window = delta;
+    sp.tab_threads = o->tab_threads;
     free(run.trace);
     memset(&run, 0, sizeof run);
     int rc = run_two_phase(&sp, o, &run);

@@ -22,6 +22,8 @@ int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_tr
 int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int mode = 0);
 int train_launch(gp_ctx* ctx, int window, long long lo, long long hi);
 int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices);
+int train_layout_costs(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, long long lo,
+                       long long hi, int path, double* out, int* fast_used);
 void train_state_free(gp_ctx* ctx);
 void train_last_nm(gp_ctx* ctx, long long nm[4]);
 void train_nm_merge(long long a[4], const long long b[4]);
@@ -423,6 +425,17 @@ int gp_train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices) 
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return train_collect(ctx, out, stage_devices);
+}
+
+int gp_debug_layout_costs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* opts,
+                          int64_t lo, int64_t hi, int32_t path, double* per_step, int32_t* fast_used) {
+  if (!ctx || !per_step) return set_error(GP_INVALID, "null argument");
+  cudaSetDevice(ctx->device);
+  const gp_train_opts def{4, 16};
+  int f = 0;
+  const int rc = train_layout_costs(ctx, ids, n, opts ? opts : &def, lo, hi, path, per_step, &f);
+  if (fast_used) *fast_used = f;
+  return rc;
 }
 
 int gp_enumerate_configs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_rollout_opts* o,

@@ -1126,7 +1126,16 @@ struct ScanRange {
   long long n_pref;                  // prefixes touched
   long long chunk;                   // prefixes per warp work item
   int defer_all;                     // test hook (GPLAN_K1_DEFER_ALL=1): K1-fast defers every candidate
+  double* dump;                      // test hook (DUMP instantiations): per_step of rank r at dump[r - dump_lo]
+  long long dump_lo;
 };
+
+// DUMP instantiations (gp_debug_layout_costs): the rank of the prefix's first layout.
+template <int R>
+__device__ __forceinline__ long long dump_base(const TrainSpace& sp, long long p) {
+  Prefix<R> tmp;
+  return prefix_decode<R>(sp, p, tmp);
+}
 
 constexpr int kDeferBlocks = 64;  // CTAs of k1_deferred (their partials follow K1-fast's)
 
@@ -1162,7 +1171,7 @@ __device__ NearMin nm_block_reduce(NearMin m) {
 
 // The generic scan of work items warp, warp + n_warps, ... (prefix chunks) of a range;
 // returns the thread's summary. P/D: the warp's shared-memory prefix state.
-template <int R>
+template <int R, bool DUMP = false>
 __device__ __forceinline__ NearMin k1_scan_warps(const TrainSpace& sp, const TrainTables& tb,
                                                  const double2* __restrict__ blkf, int L, const ScanRange& rg,
                                                  long long warp, long long n_warps, Prefix<R>& P,
@@ -1184,10 +1193,13 @@ __device__ __forceinline__ NearMin k1_scan_warps(const TrainSpace& sp, const Tra
       const long long ns = sp.cnt[R - 1][D.u];
       const long long s0 = p == rg.p_lo ? rg.s_lo : 0;
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
+      const long long pbase = DUMP ? dump_base<R>(sp, p) - rg.dump_lo : 0;
       for (long long s = s0 + lane; s < s1; s += 32) {
         const SufEnt e = tb.suf[s];
         double x;
-        if (eval_layout<R, false>(sp, tb, blkf, L, D, e, x, nullptr, nullptr)) {
+        const bool ok = eval_layout<R, false>(sp, tb, blkf, L, D, e, x, nullptr, nullptr);
+        if (DUMP) rg.dump[pbase + s] = ok ? x : __longlong_as_double(0x7ff0000000000000LL);
+        if (ok) {
           ++feasible;
           // keys grow along a thread's walk: only a new minimum or a pattern within two
           // ulps of it can change the summary, and a pattern already held keeps its key
@@ -1214,7 +1226,7 @@ __device__ __forceinline__ NearMin k1_scan_warps(const TrainSpace& sp, const Tra
   return NearMin{b0, {k0, k1, k2}, feasible};
 }
 
-template <int R>
+template <int R, bool DUMP = false>
 __global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(TrainSpace sp, TrainTables tb,
                                                       const double2* __restrict__ blkf, int L,
                                                       ScanRange rg, NearMin* __restrict__ partial) {
@@ -1223,7 +1235,7 @@ __global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(Tra
   __shared__ PrefixData<R> sD[kK1Threads / 32];
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
-  NearMin nm = k1_scan_warps<R>(sp, tb, blkf, L, rg, warp, n_warps, sP[threadIdx.x >> 5], sD[threadIdx.x >> 5]);
+  NearMin nm = k1_scan_warps<R, DUMP>(sp, tb, blkf, L, rg, warp, n_warps, sP[threadIdx.x >> 5], sD[threadIdx.x >> 5]);
   nm = nm_block_reduce(nm);
   if (threadIdx.x == 0) partial[blockIdx.x] = nm;
 }
@@ -1238,7 +1250,7 @@ __device__ unsigned long long g_k1_fast_cnt[2];
 // outside [0, S), more than kDonations fix-ups, a donor left without layers) are queued
 // for k1_deferred, which scores them with the generic eval_layout — so every candidate's
 // per-step time is the one the reference computes.
-template <int R>
+template <int R, bool DUMP = false>
 __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace sp, TrainTables tb,
                                                       const double2* __restrict__ blkf, int L,
                                                       ScanRange rg, NearMin* __restrict__ partial,
@@ -1293,6 +1305,7 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
       // table-scored count: every candidate of this lane, less the deferred ones (below)
       if (s0 + lane < s1) n_tab += (unsigned)((s1 - s0 - lane + 31) >> 5);
+      const long long pbase = DUMP ? dump_base<R>(sp, p) - rg.dump_lo : 0;
 #pragma unroll 2  // (with 6 CTAs/SM: two candidates in flight per lane, measured +10%)
       for (int s = (int)s0 + lane; s < (int)s1; s += 32) {  // (suffix indices fit 32 bits)
         const int4 A = __ldg(tb.sf_hot + s);  // fs, k|b1, rb01, rb23
@@ -1342,7 +1355,10 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
         double mt = pa.x, mc = pa.y;
         if (sb.x > mt) mt = sb.x;
         if (sb.y > mc) mc = sb.y;
-        if (!(mt < __longlong_as_double(0x7ff0000000000000LL))) continue;  // memory-infeasible
+        if (!(mt < __longlong_as_double(0x7ff0000000000000LL))) {  // memory-infeasible
+          if (DUMP) rg.dump[pbase + s] = mt;
+          continue;
+        }
         double tr = dtr;
         if (R > 1) tr += txs[(A.y >> 16) & 0xffff];
         if (fk > 1) {  // internal transfers of the suffix, [s][4] (t0, t1, t2, 0)
@@ -1354,6 +1370,7 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
           }
         }
         const double x = mt + fd[S] * mc + tr;
+        if (DUMP) rg.dump[pbase + s] = x;
         ++feasible;
         const long long d = __double_as_longlong(x) - b0;
         if (d < 3) {  // (the key is formed only here and on the deferred path)
@@ -1383,11 +1400,11 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
 
 // The candidates K1-fast deferred, scored by the generic eval_layout (rare; keys arrive
 // in any order, so the summary merges them with nm_merge).
-template <int R>
+template <int R, bool DUMP = false>
 __global__ void __launch_bounds__(kK1Threads) k1_deferred(TrainSpace sp, TrainTables tb,
                                                          const double2* __restrict__ blkf, int L,
                                                          const unsigned long long* __restrict__ slow_q,
-                                                         NearMin* __restrict__ partial) {
+                                                         NearMin* __restrict__ partial, ScanRange rg) {
   const unsigned long long cnt = slow_q[0];
   const long long n = (long long)min(cnt, (unsigned long long)kSlowQueue);
   NearMin m;
@@ -1400,7 +1417,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_deferred(TrainSpace sp, TrainTa
     PrefixData<R> D;
     prefix_data<R>(sp, tb, blkf, P, D);
     double x;
-    if (eval_layout<R, false>(sp, tb, blkf, L, D, tb.suf[s], x, nullptr, nullptr)) {
+    const bool ok = eval_layout<R, false>(sp, tb, blkf, L, D, tb.suf[s], x, nullptr, nullptr);
+    if (DUMP) rg.dump[dump_base<R>(sp, p) - rg.dump_lo + s] = ok ? x : __longlong_as_double(0x7ff0000000000000LL);
+    if (ok) {
       NearMin o;
       o.b0 = __double_as_longlong(x);
       o.key[0] = key;
@@ -1773,12 +1792,14 @@ template <int R>
 int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const double2* blkf,
                 const BlockRec* blk, int window, long long lo, long long hi, NearMin* partial,
                 int max_blocks, TrainOut* d_out, cudaStream_t stream, bool fast, int mode,
-                unsigned long long* slow_q) {
+                unsigned long long* slow_q, double* dump = nullptr, bool defer_all = false) {
   ScanRange rg{};
+  rg.dump = dump;
+  rg.dump_lo = lo;
   rank_split(h, lo, rg.p_lo, rg.s_lo);
   rank_split(h, hi, rg.p_hi, rg.s_hi);
   const char* defer_env = std::getenv("GPLAN_K1_DEFER_ALL");
-  rg.defer_all = defer_env && defer_env[0] == '1';
+  rg.defer_all = defer_all || (defer_env && defer_env[0] == '1');
   rg.n_pref = rg.p_hi - rg.p_lo + (rg.s_hi > 0 ? 1 : 0);
   const int threads = kK1Threads;
   static int occ_g = 0, occ_f = 0;
@@ -1797,14 +1818,22 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   if (hi > lo) {
     if (fast) {
       GP_CUDA(cudaMemsetAsync(slow_q, 0, sizeof(unsigned long long), stream));
-      k1_layout_scan_fast<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial,
-                                                                  slow_q);
-      k1_deferred<R><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, slow_q,
-                                                            partial + blocks);
+      if (dump) {
+        k1_layout_scan_fast<R, true><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg,
+                                                                          partial, slow_q);
+        k1_deferred<R, true><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, slow_q,
+                                                                   partial + blocks, rg);
+      } else {
+        k1_layout_scan_fast<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial,
+                                                                    slow_q);
+        k1_deferred<R><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, slow_q,
+                                                              partial + blocks, rg);
+      }
       n_partial += kDeferBlocks;
       ctx->launches += 2;
     } else {
-      k1_layout_scan<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial);
+      if (dump) k1_layout_scan<R, true><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial);
+      else k1_layout_scan<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial);
       ctx->launches++;
     }
   } else {
@@ -2167,7 +2196,8 @@ static TrainTables prepared_tables(const gp_ctx* ctx, const PreparedTrain& P) {
 
 // Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
 static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long lo, long long hi,
-                           cudaStream_t stream, bool timing, bool force_generic = false, int lane = -1) {
+                           cudaStream_t stream, bool timing, bool force_generic = false, int lane = -1,
+                           double* dump = nullptr, bool* used_fast = nullptr, bool defer_all = false) {
   const HostSpace& h = P.h;
   if (lo < 0) lo = 0;
   if (hi < 0 || hi > h.total) hi = h.total;
@@ -2186,6 +2216,7 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   const bool fast = h.exact_total && h.total >= (1LL << 20) && ctx->sc.L <= 127 && nlast <= kMaxLastBlocks &&
                     h.sp.nc[h.sp.R - 1] + 2 <= kMaxJunction && !force_generic &&
                     !(generic_env && generic_env[0] == '1');
+  if (used_fast) *used_fast = fast;
   unsigned long long*& slow_q = lane < 0 ? ctx->d_slow : ctx->d_slow_lane[lane];
   if (fast && !slow_q) GP_CUDA(cudaMalloc(&slow_q, sizeof(unsigned long long) * (1 + kSlowQueue)));
   if (timing) GP_CUDA(cudaEventRecord(ctx->ev[0], stream));
@@ -2223,10 +2254,10 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   // ---- K1: layout scan over [lo, hi)
   const int R = h.sp.R;
   int rc;
-  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q);
-  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q);
-  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q);
-  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q);
+  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q, dump, defer_all);
+  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q, dump, defer_all);
+  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q, dump, defer_all);
+  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q, dump, defer_all);
   else rc = set_error(GP_INVALID, "train sets spanning more than 4 gpu types are not supported");
   if (!rc && timing) GP_CUDA(cudaEventRecord(ctx->ev[2], stream));
   return rc;
@@ -2281,6 +2312,33 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
   GP_CUDA(cudaMemcpyAsync(base, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h2d_bytes += (long long)in_bytes;
   ctx->sum_stages = sum_stages(P.h);
+  return GP_OK;
+}
+
+// Test hook (gp_debug_layout_costs): per_step of every layout of ranks [lo, hi) as the scan
+// kernels compute it (DUMP instantiations of the same code), +inf for memory-infeasible
+// layouts. path 0: the kernel the search would use (K1-fast when eligible); 1: generic K1;
+// 2: K1-fast with every candidate deferred to k1_deferred. *fast_used: K1-fast scored them.
+int train_layout_costs(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, long long lo,
+                       long long hi, int path, double* out, int* fast_used) {
+  int rc = train_prepare(ctx, ids, n, o, 0);
+  if (rc) return rc;
+  PreparedTrain& P = *prepared(ctx);
+  if (lo < 0 || hi > P.h.total || lo > hi) return set_error(GP_INVALID, "rank range outside the layout space");
+  if (hi - lo > (1LL << 26)) return set_error(GP_INVALID, "at most 2^26 ranks per call");
+  if (hi == lo) return GP_OK;
+  double* d = static_cast<double*>(ctx_scratch(ctx, sizeof(double) * (size_t)(hi - lo), kArenaMisc));
+  if (!d) return GP_CUDA_ERROR;
+  GP_CUDA(cudaMemsetAsync(d, 0xff, sizeof(double) * (size_t)(hi - lo), ctx->stream));  // NaN: unwritten
+  bool fast = false;
+  rc = launch_prepared(ctx, P, 1, lo, hi, ctx->stream, false, path == 1, -1, d, &fast, path == 2);
+  if (rc) return rc;
+  TrainOut* ho = reinterpret_cast<TrainOut*>(ctx_pinned(ctx, sizeof(TrainOut)));
+  GP_CUDA(cudaMemcpyAsync(ho, P.d_out, sizeof(TrainOut), cudaMemcpyDeviceToHost, ctx->stream));
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ho->overflow) return set_error(GP_INVALID, "deferred queue overflow: use a smaller range");
+  GP_CUDA(cudaMemcpy(out, d, sizeof(double) * (size_t)(hi - lo), cudaMemcpyDeviceToHost));
+  if (fast_used) *fast_used = fast;
   return GP_OK;
 }
 

@@ -181,6 +181,18 @@ class Engine:
             stages.append(Stage(devs[st.first:st.first + st.count].tolist(), st.tp, st.dp, st.layers))
         return TrainSearchResult(stages, res.cost, res.rank, res.layouts, res.feasible)
 
+    def debug_layout_costs(self, train_set, lo: int, hi: int, path: int = 0, opts=None):
+        """Test hook: per_step of every layout of ranks [lo, hi) as the scan kernel computes it
+        (+inf: memory-infeasible). path 0 = the kernel the search uses, 1 = generic K1,
+        2 = K1-fast with every candidate deferred. Returns (array, fast_used)."""
+        ids = _ids(train_set)
+        out = np.empty(max(hi - lo, 1), dtype=np.float64)
+        fast = C.c_int32()
+        _check(lib().gp_debug_layout_costs(self._h, ids.ctypes.data_as(abi.i32p), len(ids),
+                                           C.byref(opts or abi.default_train_opts()), lo, hi, path,
+                                           out.ctypes.data_as(abi.f64p), C.byref(fast)))
+        return out[:hi - lo], bool(fast.value)
+
     # ---- split form + measurement hooks (bench.py) -------------------------
     @property
     def stream_ptr(self) -> int:

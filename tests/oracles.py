@@ -30,6 +30,17 @@ def oracle_lib():
         _oracle.or_schedule.argtypes = [C.POINTER(abi.gp_cluster), C.POINTER(abi.gp_workload),
                                         C.POINTER(abi.gp_calib), C.c_void_p, C.POINTER(C.c_void_p)]
         _oracle.or_free.argtypes = [C.c_void_p]
+        P = C.POINTER
+        _oracle.or_layout_costs.argtypes = [P(abi.gp_cluster), P(abi.gp_workload), P(abi.gp_calib),
+                                            abi.i32p, C.c_int32, P(abi.gp_train_opts), C.c_int64,
+                                            C.c_int64, P(C.c_double)]
+        _oracle.or_layout_costs_tab.argtypes = [P(abi.gp_cluster), P(abi.gp_workload), P(abi.gp_calib),
+                                                abi.i32p, C.c_int32, P(abi.gp_train_opts), C.c_int32,
+                                                P(C.c_int64), P(C.c_int64), P(C.c_double)]
+        _oracle.or_constrained_search_tab.argtypes = [
+            P(abi.gp_cluster), P(abi.gp_workload), P(abi.gp_calib), abi.i32p, C.c_int32,
+            P(abi.gp_train_opts), abi.i32p, C.c_int32, C.c_int64, C.c_int64, C.c_int32,
+            P(C.c_double), P(C.c_int64), P(C.c_int64), P(C.c_int64), P(C.c_double)]
     return _oracle
 
 
@@ -203,6 +214,63 @@ class Oracle:
         res, devs = self.constrained_search_raw(ids, window, opts, lo, hi)
         return train_result_dict(res, devs)
 
+    def layout_costs(self, ids, lo, hi, opts=None):
+        """per_step of every layout of ranks [lo, hi) (+inf: no memory-feasible option)."""
+        ids = _ids(ids)
+        out = np.zeros(max(hi - lo, 1), dtype=np.float64)
+        rc = self.lib.or_layout_costs(C.byref(self.c), C.byref(self.w), C.byref(self.k),
+                                      ids.ctypes.data_as(abi.i32p), len(ids),
+                                      C.byref(opts or abi.default_train_opts()), lo, hi,
+                                      out.ctypes.data_as(C.POINTER(C.c_double)))
+        if rc:
+            self.err(rc)
+        return out[:hi - lo]
+
+    def layout_costs_tab(self, ids, ranges, opts=None):
+        """per_step of the layouts of several [lo, hi) rank ranges, concatenated."""
+        ids = _ids(ids)
+        lo = np.asarray([a for a, _ in ranges], dtype=np.int64)
+        hi = np.asarray([b for _, b in ranges], dtype=np.int64)
+        out = np.zeros(max(int((hi - lo).sum()), 1), dtype=np.float64)
+        rc = self.lib.or_layout_costs_tab(C.byref(self.c), C.byref(self.w), C.byref(self.k),
+                                          ids.ctypes.data_as(abi.i32p), len(ids),
+                                          C.byref(opts or abi.default_train_opts()), len(ranges),
+                                          lo.ctypes.data_as(C.POINTER(C.c_int64)),
+                                          hi.ctypes.data_as(C.POINTER(C.c_int64)),
+                                          out.ctypes.data_as(C.POINTER(C.c_double)))
+        if rc:
+            self.err(rc)
+        return out[:int((hi - lo).sum())]
+
+    def constrained_search_tab(self, ids, windows, lo=0, hi=-1, threads=None, dump=False, opts=None):
+        """Table-memoised restatement over ranks [lo, hi): {window: (cost, rank)}, feasible,
+        layouts (and the per_step dump when asked)."""
+        ids = _ids(ids)
+        windows = list(windows)
+        wa = np.asarray(windows, dtype=np.int32)
+        cost = np.zeros(len(windows), dtype=np.float64)
+        rank = np.zeros(len(windows), dtype=np.int64)
+        feas, lay = C.c_int64(), C.c_int64()
+        threads = threads or os.cpu_count() or 1
+        buf = None
+        if dump:
+            total = self.train_space(ids)
+            h = total if hi < 0 else min(hi, total)
+            buf = np.zeros(max(h - lo, 1), dtype=np.float64)
+        rc = self.lib.or_constrained_search_tab(
+            C.byref(self.c), C.byref(self.w), C.byref(self.k), ids.ctypes.data_as(abi.i32p), len(ids),
+            C.byref(opts or abi.default_train_opts()), wa.ctypes.data_as(abi.i32p), len(windows),
+            lo, hi, threads, cost.ctypes.data_as(C.POINTER(C.c_double)),
+            rank.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(feas), C.byref(lay),
+            buf.ctypes.data_as(C.POINTER(C.c_double)) if dump else None)
+        if rc:
+            self.err(rc)
+        out = {"windows": {w: (float(c), int(r)) for w, c, r in zip(windows, cost, rank)},
+               "feasible": feas.value, "layouts": lay.value}
+        if dump:
+            out["per_step"] = buf
+        return out
+
     def train_candidates_search(self, ids, window):
         ids = _ids(ids)
         res = abi.gp_train_result()
@@ -236,11 +304,12 @@ class Oracle:
             self.err(rc)
         return exhaustive_dict(out, ids)
 
-    def schedule(self, eta=-1, seed=4276115, expand=True, restarts=16):
+    def schedule(self, eta=-1, seed=4276115, expand=True, restarts=16, tab_threads=0):
         class SchedOpts(C.Structure):
             _fields_ = [("eta_override", C.c_int32), ("seed", C.c_uint64), ("restarts", C.c_int32),
-                        ("expand_window", C.c_int32), ("band_widen_step", C.c_double)]
-        o = SchedOpts(eta, seed, restarts, int(expand), 0.05)
+                        ("expand_window", C.c_int32), ("band_widen_step", C.c_double),
+                        ("tab_threads", C.c_int32)]
+        o = SchedOpts(eta, seed, restarts, int(expand), 0.05, tab_threads)
         out = C.c_void_p()
         rc = self.lib.or_schedule(C.byref(self.c), C.byref(self.w), C.byref(self.k), C.byref(o),
                                   C.byref(out))

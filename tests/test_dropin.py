@@ -60,3 +60,33 @@ def test_cli_schedule_outputs_byte_identical(tmp_path):
     assert plan == golden("desk_plan.json")
     with open(os.path.join(ROOT, "tests", "golden", "desk_explain.txt"), "rb") as f:
         assert outs["engine"]["explain.txt"] == f.read()
+
+
+def _strip(plan):
+    plan = dict(plan)
+    for k in ("format", "cluster_fingerprint", "calibration_fingerprint", "workload_fingerprint"):
+        plan.pop(k, None)
+    return plan
+
+
+@pytest.mark.skipif(not (os.path.exists(SHIM) and os.path.exists(REF)),
+                    reason="libgplan_shim.so / libref.so not built (need /root/reference at build time)")
+@pytest.mark.parametrize("key", ["c4_256gpu/eta=2", "c5_1024gpu/eta=2"])
+def test_native_driver_equals_reference_driver_at_scale(key):
+    """C4/C5: the native batched driver (gp_schedule) == the UNMODIFIED reference scheduler.cpp
+    (src/scheduler.cpp:122-292) with every seam call on the engine through the shim — plan
+    and iteration trace bit-equal. Pins the driver restatement (batching, memo, offer order)
+    where the reference's own leaf solvers cannot run."""
+    from common import problem
+    from paper_2511_00796_b200.engine import Engine
+    env = dict(os.environ, LD_PRELOAD=SHIM)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "dropin_driver.py"), key],
+                       capture_output=True, text=True, env=env, timeout=3000)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")][0]
+    assert line["engine_calls"] > 0
+    name, eta = key.split("/eta=")
+    with Engine(problem(name)) as eng:
+        plan, trace = eng.schedule(eta=int(eta), seed=4276115)
+    assert plan == _strip(line["plan"])
+    assert trace == line["trace"]

@@ -1,5 +1,7 @@
 """GPU: the native batched Algorithm-1 driver (gp_schedule) reproduces the reference's
-golden plans + traces exactly, and agrees with the drop-in path at C4 scale."""
+golden plans + traces exactly (C1-C3), and a multi-device context's plans equal the
+single-device ones. Its C4/C5 equality with the unmodified reference driver running on
+the engine's leaf solvers is tests/test_dropin.py::test_native_driver_equals_reference_driver_at_scale."""
 import pytest
 
 from common import golden, problem
@@ -30,3 +32,23 @@ def test_native_schedule_desk_golden():
     with Engine(problem("c1_desk_mixed")) as eng:
         plan, _ = eng.schedule(eta=-1, seed=4276115)
     assert plan == _strip(golden("desk_plan.json"))
+
+
+@pytest.mark.parametrize("key", ["c3_64gpu/eta=1", "c4_256gpu/eta=2"])
+def test_multi_device_context_schedule(key):
+    """gp_schedule on a multi-device context (every visible GPU, or two peer contexts on
+    device 0 of a one-GPU box): the iteration batches are split over the devices — and the
+    plan and trace equal the single-device run (and the reference golden where one exists)."""
+    import torch
+    from paper_2511_00796_b200.engine import Engine
+    n = torch.cuda.device_count()
+    name, eta = key.split("/eta=")
+    with Engine(problem(name)) as eng:
+        plan1, trace1 = eng.schedule(eta=int(eta), seed=4276115)
+    with Engine(problem(name), devices=list(range(n)) if n >= 2 else [0, 0]) as eng:
+        plan2, trace2 = eng.schedule(eta=int(eta), seed=4276115)
+    assert plan2 == plan1
+    assert trace2 == trace1
+    g = golden("schedules.json").get(key)
+    if g:
+        assert plan2 == _strip(g["plan"])

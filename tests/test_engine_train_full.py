@@ -1,0 +1,117 @@
+"""GPU: constrained_search at full C4/C5 scale against the independent CPU restatement.
+
+* Whole-space winners: every set of tests/golden/train_full.json (incl. the 2.42e9-layout
+  C5 bench set) — (cost, rank) for windows 1..8 and the memory-feasible count equal the
+  table-memoised C restatement's (oracle.c or_constrained_search_tab, pinned against the
+  reference goldens by tests/golden/make_golden_full.py and test_oracle.py).
+* K1-fast == generic K1 over the FULL bench set (every window, feasible count).
+* Per-candidate per_step (north_star: "per-candidate cost estimates match"): the scan
+  kernel's own value (DUMP instantiation, K1-fast path active) equals the oracle's
+  bit-for-bit on >= 1e5 random ranks per set, on the ranks around the bench winner and
+  around every golden window winner; the deferred (generic) fallback and the generic K1
+  agree on the same ranks.
+Reference: src/train_search.cpp:218-275, src/cost_model.cpp:93-126.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from common import golden, problem
+from oracles import Oracle
+
+pytestmark = pytest.mark.gpu
+
+FULL = golden("train_full.json")
+WINDOWS = list(range(1, 9))
+
+
+def _cases(name):
+    return [(name, i) for i in range(len(FULL[name]))]
+
+
+@pytest.fixture(scope="module")
+def engines():
+    from paper_2511_00796_b200.engine import Engine
+    out = {n: Engine(problem(n)) for n in ("c4_256gpu", "c5_1024gpu")}
+    yield out
+    for e in out.values():
+        e.close()
+
+
+@pytest.mark.parametrize("name,i", _cases("c4_256gpu") + _cases("c5_1024gpu"))
+def test_full_space_winner_matches_oracle(engines, name, i):
+    case = FULL[name][i]
+    eng = engines[name]
+    for w in WINDOWS:
+        res, _ = eng.constrained_search_raw(case["ids"], w)
+        want = case["windows"][str(w)]
+        assert res.layouts == case["layouts"]
+        assert res.feasible == case["feasible"]
+        if want["rank"] < 0:
+            assert not res.found
+        else:
+            assert (res.cost, res.rank) == (want["cost"], want["rank"]), (w, res.cost, res.rank, want)
+
+
+def test_fast_equals_generic_on_full_bench_set(engines):
+    eng = engines["c5_1024gpu"]
+    ids = FULL["c5_1024gpu"][0]["ids"]
+    assert len(ids) == 1023
+    eng.set_memo(False)
+    try:
+        fast = [eng.constrained_search_raw(ids, w, lo=0, hi=-1)[0] for w in (1, 3, 7)]
+        os.environ["GPLAN_K1_GENERIC"] = "1"
+        try:
+            gen = [eng.constrained_search_raw(ids, w, lo=0, hi=-1)[0] for w in (1, 3, 7)]
+        finally:
+            del os.environ["GPLAN_K1_GENERIC"]
+    finally:
+        eng.set_memo(True)
+    for a, b in zip(fast, gen):
+        assert (a.found, a.cost, a.rank, a.feasible, a.layouts) == (b.found, b.cost, b.rank, b.feasible, b.layouts)
+        assert a.layouts == 2_415_919_104
+
+
+def _ranges(total, rng, n_windows, width, anchors):
+    out = []
+    for a in anchors:
+        lo = max(0, min(total - width, a - width // 2))
+        out.append((lo, lo + width))
+    for lo in rng.integers(0, total - width, size=n_windows):
+        out.append((int(lo), int(lo) + width))
+    return sorted(set(out))
+
+
+@pytest.mark.parametrize("name,i", [("c5_1024gpu", 0), ("c5_1024gpu", 8), ("c4_256gpu", 0), ("c4_256gpu", 7)])
+def test_per_candidate_costs_vs_oracle(engines, name, i):
+    case = FULL[name][i]
+    eng, orc = engines[name], Oracle(problem(name))
+    ids, total = case["ids"], case["layouts"]
+    rng = np.random.default_rng(1234 + i)
+    anchors = sorted({v["rank"] for v in case["windows"].values() if v["rank"] >= 0})
+    rs = _ranges(total, rng, 400, 256, anchors)
+    want = orc.layout_costs_tab(ids, rs)
+    got = []
+    fast_all = True
+    for lo, hi in rs:
+        v, fast = eng.debug_layout_costs(ids, lo, hi, path=0)
+        got.append(v)
+        fast_all &= fast
+    got = np.concatenate(got)
+    assert fast_all  # K1-fast (constant allocation total) scored every range
+    assert got.size >= 100_000
+    assert not np.isnan(got).any()
+    np.testing.assert_array_equal(got.view(np.int64), want.view(np.int64))  # bitwise
+    assert np.isfinite(got).sum() > 0
+    # the plain (un-memoised) restatement on a subset
+    for lo, hi in rs[:6]:
+        plain = orc.layout_costs(ids, lo, hi)
+        tab = orc.layout_costs_tab(ids, [(lo, hi)])
+        np.testing.assert_array_equal(plain.view(np.int64), tab.view(np.int64))
+    # generic K1 and K1-fast's deferred (generic) fallback on the same ranks
+    sub = rs[:40]
+    want_sub = orc.layout_costs_tab(ids, sub)
+    for path in (1, 2):
+        g = np.concatenate([eng.debug_layout_costs(ids, lo, hi, path=path)[0] for lo, hi in sub])
+        np.testing.assert_array_equal(g.view(np.int64), want_sub.view(np.int64))

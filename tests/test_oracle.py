@@ -3,7 +3,7 @@ import json
 
 import pytest
 
-from common import CONFIGS, golden, problem
+from common import CONFIGS, golden, problem, random_train_sets
 from oracles import Oracle
 
 
@@ -119,3 +119,46 @@ def test_partition_matches_reference(name):
         got = oracle_partitions(orc, case["gamma_l"], case["gamma_h"], **kw)
         want = [(c["train"], c["objective"], c["compute_fraction"]) for c in case["candidates"]]
         assert got == want, (case["gamma_l"], case["gamma_h"], case["machine"])
+
+
+def test_table_oracle_vs_reference_goldens():
+    """or_constrained_search_tab (the memoised restatement behind train_full.json) reproduces
+    every reference constrained_search golden and the plain restatement's winner rank."""
+    for name in CONFIGS:
+        orc = Oracle(problem(name))
+        for case in golden("train_search.json")[name]:
+            r = orc.constrained_search_tab(case["ids"], [case["window"]], threads=4)
+            cost, rank = r["windows"][case["window"]]
+            assert r["layouts"] == case["layouts"]
+            if case["ref"]["found"]:
+                assert cost == case["ref"]["cost"]
+                if case["layouts"] <= 20_000:  # (the plain restatement is slow on big sets)
+                    assert rank == orc.constrained_search(case["ids"], case["window"])["rank"]
+            else:
+                assert rank == -1
+
+
+def test_table_oracle_per_layout_equals_plain():
+    """Per-layout per_step of the memoised restatement == the plain restatement, bitwise,
+    on slices of C3/C4/C5 train sets (incl. the 2.42e9-layout C5 bench set)."""
+    import numpy as np
+    for name in ("c3_64gpu", "c4_256gpu", "c5_1024gpu"):
+        p = problem(name)
+        orc = Oracle(p)
+        for ids in random_train_sets(p.cluster.n, 2, seed=5) + [list(range(p.cluster.n - 1))]:
+            total = orc.train_space(ids)
+            rs = [(lo, min(total, lo + 1500)) for lo in sorted({0, total // 3, max(0, total - 1500)})]
+            tab = orc.layout_costs_tab(ids, rs)
+            plain = np.concatenate([orc.layout_costs(ids, a, b) for a, b in rs])
+            np.testing.assert_array_equal(tab.view(np.int64), plain.view(np.int64))
+
+
+def test_full_golden_c4_recomputed():
+    """tests/golden/train_full.json's C4 entries recompute identically (the C5 entries take
+    minutes of host time and are recomputed by tests/golden/make_golden_full.py)."""
+    orc = Oracle(problem("c4_256gpu"))
+    for case in golden("train_full.json")["c4_256gpu"]:
+        r = orc.constrained_search_tab(case["ids"], list(range(1, 9)))
+        assert r["feasible"] == case["feasible"] and r["layouts"] == case["layouts"]
+        for w, (c, k) in r["windows"].items():
+            assert case["windows"][str(w)] == {"cost": c, "rank": k}
