@@ -230,8 +230,10 @@ def run_b200(args):
     ids = bench_train_set(p)
     eng = Engine(p, device=local_rank)
     total = eng.train_space(ids)
-    from paper_2511_00796_b200.shard import gather_winner, shard_range
-    lo, hi = shard_range(total, rank, world)
+    from paper_2511_00796_b200.shard import gather_winner
+    # balanced contiguous rank shards, cut where every shard keeps K1-fast's scan order
+    bounds = eng.shard_bounds(ids, world)
+    lo, hi = bounds[rank], bounds[rank + 1]
     stream = torch.cuda.ExternalStream(eng.stream_ptr, device=dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 

@@ -236,12 +236,21 @@ int gp_fp64_peak(gp_ctx* ctx, double* dadd_per_s);
 /* Test hook (parity of individual candidates, not a reference interface): per_step
  * (train_cost_breakdown(...).per_step, src/cost_model.cpp:93-126) of every layout of
  * ranks [lo, hi) of the train set, computed by the scan kernel itself (its DUMP
- * instantiation), +inf for layouts without a memory-feasible option. path 0: the kernel
- * constrained_search would use (K1-fast when eligible), 1: the generic K1, 2: K1-fast with
- * every candidate deferred to its generic fallback. hi - lo <= 2^26. *fast_used (optional)
- * is set to 1 when K1-fast scored the range. */
+ * instantiation), +inf for layouts without a memory-feasible option. path 0: the
+ * whole-space scan constrained_search runs (K1-fast with its inner run when eligible), the
+ * values of [lo, hi) kept; 1: the generic K1 over [lo, hi); 2: K1-fast over [lo, hi) with
+ * every candidate deferred to its generic fallback; 3: K1-fast over [lo, hi) as a range
+ * search scans it. hi - lo <= 2^26. *fast_used (optional): 1 + K1-fast's inner type run,
+ * 0 when the generic K1 scored the range. */
 int gp_debug_layout_costs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* opts,
                           int64_t lo, int64_t hi, int32_t path, double* per_step, int32_t* fast_used);
+/* Rank boundaries bounds[0..n_shards] splitting a train set's layout space into n_shards
+ * contiguous ranges of balanced size for multi-GPU sharding (gp_constrained_search_range
+ * per shard, winners merged by (cost, rank), feasible counts summed). Boundaries sit at
+ * first layouts of the first type run's choices when that lets every shard keep the
+ * engine's fastest scan order. */
+int gp_train_shard_bounds(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* opts,
+                          int32_t n_shards, int64_t* bounds);
 
 /* ---- rollout side: replaces enumerate_configs / rollout_capacities / solve_milp
  *      (src/rollout_milp.cpp:113-254) ------------------------------------- */

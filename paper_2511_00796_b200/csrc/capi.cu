@@ -23,7 +23,9 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
 int train_launch(gp_ctx* ctx, int window, long long lo, long long hi);
 int train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices);
 int train_layout_costs(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, long long lo,
-                       long long hi, int path, double* out, int* fast_used);
+                       long long hi, int path, double* out, int* fast_used, int* inner);
+int train_shard_bounds(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int n_shards,
+                       int64_t* bounds);
 void train_state_free(gp_ctx* ctx);
 void train_last_nm(gp_ctx* ctx, long long nm[4]);
 void train_nm_merge(long long a[4], const long long b[4]);
@@ -333,12 +335,28 @@ static int search_fanout(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t win
   }
   std::vector<gp_ctx*> devs{ctx};
   devs.insert(devs.end(), ctx->peers.begin(), ctx->peers.end());
-  for (int i = 0; i < P; ++i) {  // enqueue everything first: shards run concurrently
-    cudaSetDevice(devs[i]->device);
-    const int64_t a = lo + (hi - lo) * i / P, b = lo + (hi - lo) * (i + 1) / P;
-    rc = train_prepare(devs[i], ids, n, o);
-    if (!rc) rc = train_launch(devs[i], window, a, b);
+  std::vector<int64_t> bounds(P + 1);
+  if (lo == 0 && hi == total) {  // whole space: shards that keep K1-fast's best scan order
+    rc = train_shard_bounds(ctx, ids, n, o, P, bounds.data());
     if (rc) return rc;
+  } else {
+    for (int i = 0; i <= P; ++i) bounds[i] = lo + (hi - lo) * i / P;
+  }
+  int launched = 0;
+  for (int i = 0; i < P && !rc; ++i) {  // enqueue everything first: shards run concurrently
+    cudaSetDevice(devs[i]->device);
+    rc = train_prepare(devs[i], ids, n, o);
+    if (!rc) rc = train_launch(devs[i], window, bounds[i], bounds[i + 1]);
+    if (!rc) ++launched;
+  }
+  if (rc) {  // drain the shards already running before reporting the error
+    const std::string err = gp_last_error();
+    for (int i = 0; i < launched; ++i) {
+      cudaSetDevice(devs[i]->device);
+      cudaStreamSynchronize(devs[i]->stream);
+    }
+    cudaSetDevice(ctx->device);
+    return set_error(rc, err);
   }
   std::memset(out, 0, sizeof *out);
   out->layouts = hi - lo;
@@ -432,10 +450,17 @@ int gp_debug_layout_costs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_t
   if (!ctx || !per_step) return set_error(GP_INVALID, "null argument");
   cudaSetDevice(ctx->device);
   const gp_train_opts def{4, 16};
-  int f = 0;
-  const int rc = train_layout_costs(ctx, ids, n, opts ? opts : &def, lo, hi, path, per_step, &f);
-  if (fast_used) *fast_used = f;
+  int f = 0, inner = -1;
+  const int rc = train_layout_costs(ctx, ids, n, opts ? opts : &def, lo, hi, path, per_step, &f, &inner);
+  if (fast_used) *fast_used = f ? 1 + inner : 0;  // 1 + K1-fast's inner run, 0: generic K1
   return rc;
+}
+
+int gp_train_shard_bounds(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* opts,
+                          int32_t n_shards, int64_t* bounds) {
+  if (!ctx || !bounds) return set_error(GP_INVALID, "null argument");
+  const gp_train_opts def{4, 16};
+  return train_shard_bounds(ctx, ids, n, opts ? opts : &def, n_shards, bounds);
 }
 
 int gp_enumerate_configs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_rollout_opts* o,

@@ -71,7 +71,8 @@ struct __align__(16) SufEnt {
   int bi[4];
   double t[3];
   int k;
-  int b1;
+  int b1;  // end position of the first block
+  int bl;  // start position of the last block
 };
 
 // Fast-path view of a suffix choice, valid when the layer-allocation total is the same

@@ -35,10 +35,12 @@ namespace cg = cooperative_groups;
 namespace gp {
 
 // ------------------------------------------------------------------ K3 configs
+constexpr int kAv = GP_MAX_ROLLOUT_STAGES;  // largest per-machine counts kept per type (one per stage)
+
 struct CfgCand {
   int type;
   int stages;
-  int tp[4];
+  int tp[kAv];
   int set;  // rollout set of this candidate (batched enumeration)
 };
 
@@ -50,7 +52,7 @@ __device__ __forceinline__ int trunc_i32_x86(double x) {
 
 // One thread per (type, tp-multiset) candidate; the caller compacts in order.
 __global__ void k3_configs(const CfgCand* __restrict__ cands, int n_cands,
-                           const int* __restrict__ avail /* [T][4] top-4 machine counts */,
+                           const int* __restrict__ avail /* [T][kAv] largest machine counts */,
                            const int* __restrict__ n_machines /* [T] */, int max_stages,
                            Scalars sc, const double* __restrict__ tcap,
                            const double* __restrict__ thbm, const double* __restrict__ tflops,
@@ -61,11 +63,11 @@ __global__ void k3_configs(const CfgCand* __restrict__ cands, int n_cands,
   const CfgCand c = cands[i];
   const int t = c.type, S = c.stages;
   const int* nm = n_machines + c.set * T;
-  const int* av = avail + c.set * T * 4;
+  const int* av = avail + c.set * T * kAv;
   int ms = max_stages < nm[t] ? max_stages : nm[t];
   ms = ms < sc.L ? ms : sc.L;
   bool ok = nm[t] > 0 && S <= ms;
-  for (int s = 0; s < S && ok; ++s) ok = c.tp[s] <= av[t * 4 + s];  // stage k on k-th largest machine
+  for (int s = 0; s < S && ok; ++s) ok = c.tp[s] <= av[t * kAv + s];  // stage k on k-th largest machine
   int conc = 0;
   if (ok) {
     // replica_concurrency (src/cost_model.cpp:209-229)
@@ -449,11 +451,12 @@ int rollout_capacities(gp_ctx* ctx, const int32_t* ids, int n, int32_t* caps) {
 int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* ns, const gp_rollout_opts* o,
                   std::vector<std::vector<gp_config>>& out, std::vector<int>* uniq_out) {
   out.assign(q, {});
-  if (o->max_stages < 0 || o->max_stages > 4)
-    return set_error(GP_INVALID, "rollout max_stages must lie in [0, 4] for the sm_100a kernel");
+  if (o->max_stages < 0 || o->max_stages > GP_MAX_ROLLOUT_STAGES)
+    return set_error(GP_INVALID, "rollout max_stages must lie in [0, " + std::to_string(GP_MAX_ROLLOUT_STAGES) +
+                                     "] (gp_config holds GP_MAX_ROLLOUT_STAGES stages)");
   const int T = ctx->T;
   // The configuration list of a set depends only on its per-type machine availability
-  // (the four largest per-machine device counts and the machine count of each type), so
+  // (the kAv largest per-machine device counts and the machine count of each type), so
   // sets are deduplicated on that signature and K3 runs once per distinct signature.
   std::vector<int> avail, nm;
   std::vector<int> uniq_of(q, -1);
@@ -461,7 +464,8 @@ int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* 
   std::vector<CfgCand> cands;
   std::vector<int> per_machine(ctx->M, 0), mtype(ctx->M, -1);
   std::vector<char> seen(ctx->N, 0);
-  std::vector<int> sig((size_t)T * 5);
+  constexpr int SW = kAv + 1;
+  std::vector<int> sig((size_t)T * SW);
   for (int si = 0; si < q; ++si) {
     const int32_t* id = ids[si];
     const int n = ns[si];
@@ -485,23 +489,23 @@ int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* 
     for (int t = 0; t < T; ++t) {
       auto& v = by_type[t];
       std::sort(v.rbegin(), v.rend());
-      sig[(size_t)t * 5] = (int)v.size();
-      for (int k = 0; k < 4 && k < (int)v.size(); ++k) sig[(size_t)t * 5 + 1 + k] = v[k];
+      sig[(size_t)t * SW] = (int)v.size();
+      for (int k = 0; k < kAv && k < (int)v.size(); ++k) sig[(size_t)t * SW + 1 + k] = v[k];
     }
     auto ins = sig_index.emplace(sig, (int)sig_index.size());
     uniq_of[si] = ins.first->second;
     if (!ins.second) continue;
     const int ui = ins.first->second;
     for (int t = 0; t < T; ++t) {
-      nm.push_back(sig[(size_t)t * 5]);
-      for (int k = 0; k < 4; ++k) avail.push_back(sig[(size_t)t * 5 + 1 + k]);
+      nm.push_back(sig[(size_t)t * SW]);
+      for (int k = 0; k < kAv; ++k) avail.push_back(sig[(size_t)t * SW + 1 + k]);
       if (by_type[t].empty()) continue;
       // candidates in reference order: stages, then tp_multisets over {8,4,2,1}
-      for (int S = 1; S <= std::min(o->max_stages, 4); ++S) {
-        int tp[4];
+      for (int S = 1; S <= o->max_stages; ++S) {
+        int tp[kAv];
         std::function<void(int, int)> rec = [&](int d, int mx) {
           if (d == S) {
-            CfgCand c{t, S, {0, 0, 0, 0}, ui};
+            CfgCand c{t, S, {}, ui};
             for (int u = 0; u < S; ++u) c.tp[u] = tp[u];
             cands.push_back(c);
             return;

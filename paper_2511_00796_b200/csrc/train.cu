@@ -30,6 +30,7 @@
 #include <numeric>
 #include <string>
 #include <unordered_map>
+#include <mutex>
 #include <thread>
 #include <array>
 
@@ -424,11 +425,12 @@ __global__ void __launch_bounds__(256) k2c_stage_table(const BlockRec* __restric
 
 
 // --------------------------------------------------------- K2d suffix table
-// One entry per choice (k, cuts) of the LAST type run, in run_compositions order
-// (src/train_search.cpp:53-72, k ascending): block ids, internal transfers.
+// One entry per choice (k, cuts) of type run r (the LAST run for the generic scan, the
+// inner run for K1-fast), in run_compositions order (src/train_search.cpp:53-72, k
+// ascending): block ids, internal transfers, first-block end and last-block start.
 __device__ __forceinline__ void k2d_body(int i, const int4* __restrict__ choices, const TrainSpace& sp,
-                                         const double* __restrict__ tin, SufEnt* __restrict__ suf) {
-  const int r = sp.R - 1, nc = sp.nc[r], e = nc + 2;
+                                         const double* __restrict__ tin, SufEnt* __restrict__ suf, int r) {
+  const int nc = sp.nc[r], e = nc + 2;
   const int4 c = choices[i];  // (k, b1, b2, b3) position-index boundaries
   const int k = c.x;
   int b[5] = {0, c.y, c.z, c.w, 0};
@@ -441,14 +443,15 @@ __device__ __forceinline__ void k2d_body(int i, const int4* __restrict__ choices
     out.t[j] = j + 1 < k ? tin[sp.tin_off[r] + ((size_t)b[j] * e + b[j + 1]) * e + b[j + 2]] : 0.0;
   out.k = k;
   out.b1 = b[1];
+  out.bl = b[k - 1];
   suf[i] = out;
 }
 
 __global__ void k2d_suffix_table(const int4* __restrict__ choices, int n, TrainSpace sp,
-                                 const double* __restrict__ tin, SufEnt* __restrict__ suf) {
+                                 const double* __restrict__ tin, SufEnt* __restrict__ suf, int r) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  k2d_body(i, choices, sp, tin, suf);
+  k2d_body(i, choices, sp, tin, suf, r);
 }
 
 // ------------------------------------------------------------- K1 layout scan
@@ -461,7 +464,28 @@ struct Prefix {
   int k[R > 1 ? R - 1 : 1];
   int b[R > 1 ? R - 1 : 1][kMaxPerRun + 1];
   int u;
+  long long base;  // rank of the prefix's first layout (generic scan: original run order)
+  int ci[R > 1 ? R - 1 : 1];  // choice index of each prefix run (run_compositions order)
 };
+
+// positions b[1..m] (1-based cut indices, increasing) of the q-th m-subset of nc cuts in
+// lexicographic order (run_compositions, src/train_search.cpp:53-72)
+__host__ __device__ __forceinline__ void comb_unrank(int nc, int m, long long q, int* b) {
+  int v = 0;
+#pragma unroll
+  for (int j = 1; j < kMaxPerRun; ++j) {
+    if (j <= m) {
+      while (true) {
+        const long long cc = binom_small(nc - v - 1, m - j);
+        if (q < cc) break;
+        q -= cc;
+        ++v;
+      }
+      b[j] = v + 1;
+      ++v;
+    }
+  }
+}
 
 // Decode prefix index x over runs 0..R-2 (Enumerator::recurse order). Returns the
 // full-space rank of the prefix's first layout (its base).
@@ -474,6 +498,7 @@ __host__ __device__ __forceinline__ long long prefix_decode(const TrainSpace& sp
   for (int r = 0; r + 1 < R; ++r) {
     const int nc = sp.nc[r];
     const int rem_runs = R - 1 - r;
+    int cidx = 0;
     for (int k = 1; k <= sp.kmax[r]; ++k) {
       if (u + k + rem_runs > sp.max_stages) break;
       const long long c = binom_small(nc, k - 1);
@@ -484,21 +509,8 @@ __host__ __device__ __forceinline__ long long prefix_decode(const TrainSpace& sp
         x -= q * subP;
         base += q * sub;
         P.k[r] = k;
-        const int m = k - 1;
-        int v = 0;
-#pragma unroll
-        for (int j = 1; j < kMaxPerRun; ++j) {
-          if (j <= m) {
-            while (true) {
-              const long long cc = binom_small(nc - v - 1, m - j);
-              if (q < cc) break;
-              q -= cc;
-              ++v;
-            }
-            P.b[r][j] = v + 1;
-            ++v;
-          }
-        }
+        P.ci[r] = cidx + (int)q;
+        comb_unrank(nc, k - 1, q, P.b[r]);
 #pragma unroll
         for (int j = 1; j <= kMaxPerRun; ++j)
           if (j == k) P.b[r][j] = nc + 1;
@@ -508,15 +520,55 @@ __host__ __device__ __forceinline__ long long prefix_decode(const TrainSpace& sp
       }
       x -= c * subP;
       base += c * sub;
+      cidx += (int)c;
     }
   }
   P.u = u;
+  P.base = base;
   return base;
+}
+
+// rank -> (prefix runs 0..R-2 into P, index s among the last run's choices): the inverse of
+// the enumeration order (Enumerator::recurse, src/train_search.cpp:95-124).
+template <int R>
+__host__ __device__ __forceinline__ void rank_decode(const TrainSpace& sp, long long rank, Prefix<R>& P,
+                                                     long long& s) {
+  int u = 0;
+  s = 0;
+  P.base = 0;
+  for (int r = 0; r < R; ++r) {
+    const int nc = sp.nc[r], rem_runs = R - 1 - r;
+    long long sidx = 0;
+    for (int k = 1; k <= sp.kmax[r]; ++k) {
+      if (u + k + rem_runs > sp.max_stages) break;
+      const long long c = binom_small(nc, k - 1), sub = sp.cnt[r + 1][u + k];
+      if (rank < c * sub) {
+        const long long q = rank / sub;
+        rank -= q * sub;
+        if (r + 1 < R) {
+          P.k[r] = k;
+          comb_unrank(nc, k - 1, q, P.b[r]);
+          for (int j = 1; j <= kMaxPerRun; ++j)
+            if (j == k) P.b[r][j] = nc + 1;
+          P.b[r][0] = 0;
+        } else {
+          s = sidx + q;
+        }
+        u += k;
+        break;
+      }
+      rank -= c * sub;
+      sidx += c;
+    }
+    if (r + 2 == R) P.u = u;
+  }
+  if (R == 1) P.u = 0;
 }
 
 // Next prefix in enumeration order (odometer over runs 0..R-2).
 template <int R>
 __device__ __forceinline__ void prefix_advance(const TrainSpace& sp, Prefix<R>& P) {
+  P.base += sp.cnt[R - 1][P.u];
   bool carry = true;
   int used[R > 1 ? R - 1 : 1];
   int acc = 0;
@@ -541,6 +593,7 @@ __device__ __forceinline__ void prefix_advance(const TrainSpace& sp, Prefix<R>& 
           if (j == jf) P.b[rr][j] += 1;
           else if (j > jf && j <= m) P.b[rr][j] = P.b[rr][j - 1] + 1;
         }
+        P.ci[rr]++;
         ok = true;
       } else if (P.k[rr] < sp.kmax[rr] && used[rr] + P.k[rr] + 1 + (R - 1 - rr) <= sp.max_stages &&
                  nc >= P.k[rr]) {
@@ -550,6 +603,7 @@ __device__ __forceinline__ void prefix_advance(const TrainSpace& sp, Prefix<R>& 
           if (j < k) P.b[rr][j] = j;
           else if (j == k) P.b[rr][j] = nc + 1;
         }
+        P.ci[rr]++;
         ok = true;
       }
       if (ok) {
@@ -558,6 +612,7 @@ __device__ __forceinline__ void prefix_advance(const TrainSpace& sp, Prefix<R>& 
         for (int r2 = rr + 1; r2 + 1 < R; ++r2) {
           P.k[r2] = 1;
           P.b[r2][1] = sp.nc[r2] + 1;
+          P.ci[r2] = 0;
         }
       }
     }
@@ -1126,16 +1181,9 @@ struct ScanRange {
   long long n_pref;                  // prefixes touched
   long long chunk;                   // prefixes per warp work item
   int defer_all;                     // test hook (GPLAN_K1_DEFER_ALL=1): K1-fast defers every candidate
-  double* dump;                      // test hook (DUMP instantiations): per_step of rank r at dump[r - dump_lo]
-  long long dump_lo;
+  double* dump;                      // test hook (DUMP instantiations): per_step of rank r in
+  long long dump_lo, dump_hi;        //   [dump_lo, dump_hi) at dump[r - dump_lo]
 };
-
-// DUMP instantiations (gp_debug_layout_costs): the rank of the prefix's first layout.
-template <int R>
-__device__ __forceinline__ long long dump_base(const TrainSpace& sp, long long p) {
-  Prefix<R> tmp;
-  return prefix_decode<R>(sp, p, tmp);
-}
 
 constexpr int kDeferBlocks = 64;  // CTAs of k1_deferred (their partials follow K1-fast's)
 
@@ -1148,9 +1196,10 @@ __device__ __forceinline__ NearMin nm_shfl_xor(const NearMin& m, int o) {
   return r;
 }
 
-// CTA-wide merge; the result is valid in thread 0.
+// CTA-wide merge of a CTA of at most NW warps; the result is valid in thread 0.
+template <int NW = 32>
 __device__ NearMin nm_block_reduce(NearMin m) {
-  __shared__ NearMin sb[32];
+  __shared__ NearMin sb[NW];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nm_merge(m, nm_shfl_xor(m, o));
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1178,7 +1227,6 @@ __device__ __forceinline__ NearMin k1_scan_warps(const TrainSpace& sp, const Tra
                                                  PrefixData<R>& D) {
   const int lane = threadIdx.x & 31;
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
-  const long long n_suf = sp.n_suf;
   // thread summary in registers: NearMin {b0, k0..k2, feasible}
   long long b0 = kInfBits, k0 = LLONG_MAX, k1 = LLONG_MAX, k2 = LLONG_MAX, feasible = 0;
   for (long long it = warp; it < n_items; it += n_warps) {
@@ -1193,19 +1241,20 @@ __device__ __forceinline__ NearMin k1_scan_warps(const TrainSpace& sp, const Tra
       const long long ns = sp.cnt[R - 1][D.u];
       const long long s0 = p == rg.p_lo ? rg.s_lo : 0;
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
-      const long long pbase = DUMP ? dump_base<R>(sp, p) - rg.dump_lo : 0;
+      const long long pbase = P.base;  // keys are ranks: base of the prefix + suffix index
       for (long long s = s0 + lane; s < s1; s += 32) {
         const SufEnt e = tb.suf[s];
         double x;
         const bool ok = eval_layout<R, false>(sp, tb, blkf, L, D, e, x, nullptr, nullptr);
-        if (DUMP) rg.dump[pbase + s] = ok ? x : __longlong_as_double(0x7ff0000000000000LL);
+        if (DUMP && pbase + s >= rg.dump_lo && pbase + s < rg.dump_hi)
+          rg.dump[pbase + s - rg.dump_lo] = ok ? x : __longlong_as_double(0x7ff0000000000000LL);
         if (ok) {
           ++feasible;
           // keys grow along a thread's walk: only a new minimum or a pattern within two
           // ulps of it can change the summary, and a pattern already held keeps its key
           const long long d = __double_as_longlong(x) - b0;
           if (d < 3) {
-            const long long key = p * n_suf + s;
+            const long long key = pbase + s;
             if (d < 0) {  // new minimum: shift the held patterns up by -d
               k2 = d == -1 ? k1 : d == -2 ? k0 : LLONG_MAX;
               k1 = d == -1 ? k0 : LLONG_MAX;
@@ -1243,7 +1292,8 @@ __global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(Tra
 // candidates scored by K1-fast's tables / by the deferred generic kernel (GPLAN_PROFILE report)
 __device__ unsigned long long g_k1_fast_cnt[2];
 
-// K1-fast (constant allocation total). Per candidate: the suffix's remainder ranks among
+// K1-fast (constant allocation total). Keys are ranks (prefix base + suffix index), in
+// increasing order along a thread's walk. Per candidate: the suffix's remainder ranks among
 // the prefix's (cntb) fix how many prefix (a) and suffix (b) stages the round-robin
 // promotes; zero-layer fix-ups are merged from the two sides' donation tables; the stage
 // maxima are then two table reads. Layouts outside the tabulated cases (extra layers
@@ -1259,7 +1309,6 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
-  const long long n_suf = sp.n_suf;
   const int nsuf32 = sp.n_suf;
   long long b0 = kInfBits, k0 = LLONG_MAX, k1 = LLONG_MAX, k2 = LLONG_MAX, feasible = 0;
   unsigned n_tab = 0;
@@ -1301,11 +1350,11 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
       const int fp = F.fp, pbad = F.bad;
       const double dtr = D.transfers;
       const long long ns = sp.cnt[R - 1][kp];
+      const long long pbase = P.base;  // keys are ranks: base of the prefix + suffix index
       const long long s0 = p == rg.p_lo ? rg.s_lo : 0;
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
       // table-scored count: every candidate of this lane, less the deferred ones (below)
       if (s0 + lane < s1) n_tab += (unsigned)((s1 - s0 - lane + 31) >> 5);
-      const long long pbase = DUMP ? dump_base<R>(sp, p) - rg.dump_lo : 0;
 #pragma unroll 2  // (with 6 CTAs/SM: two candidates in flight per lane, measured +10%)
       for (int s = (int)s0 + lane; s < (int)s1; s += 32) {  // (suffix indices fit 32 bits)
         const int4 A = __ldg(tb.sf_hot + s);  // fs, k|b1, rb01, rb23
@@ -1344,7 +1393,7 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
           }
         }
         if (slow) {
-          const long long key = p * n_suf + s;
+          const long long key = pbase + s;
           const unsigned long long at = atomicAdd(slow_q, 1ULL);
           if (at < (unsigned long long)kSlowQueue) slow_q[1 + at] = (unsigned long long)key;
           --n_tab;
@@ -1356,7 +1405,7 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
         if (sb.x > mt) mt = sb.x;
         if (sb.y > mc) mc = sb.y;
         if (!(mt < __longlong_as_double(0x7ff0000000000000LL))) {  // memory-infeasible
-          if (DUMP) rg.dump[pbase + s] = mt;
+          if (DUMP && pbase + s >= rg.dump_lo && pbase + s < rg.dump_hi) rg.dump[pbase + s - rg.dump_lo] = mt;
           continue;
         }
         double tr = dtr;
@@ -1370,11 +1419,11 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
           }
         }
         const double x = mt + fd[S] * mc + tr;
-        if (DUMP) rg.dump[pbase + s] = x;
+        if (DUMP && pbase + s >= rg.dump_lo && pbase + s < rg.dump_hi) rg.dump[pbase + s - rg.dump_lo] = x;
         ++feasible;
         const long long d = __double_as_longlong(x) - b0;
         if (d < 3) {  // (the key is formed only here and on the deferred path)
-          const long long key = p * n_suf + s;
+          const long long key = pbase + s;
           if (d < 0) {
             k2 = d == -1 ? k1 : d == -2 ? k0 : LLONG_MAX;
             k1 = d == -1 ? k0 : LLONG_MAX;
@@ -1394,7 +1443,7 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
   n_tab = __reduce_add_sync(0xffffffffu, n_tab);
   if (lane == 0) atomicAdd(&g_k1_fast_cnt[0], (unsigned long long)n_tab);
   NearMin nm{b0, {k0, k1, k2}, feasible};
-  nm = nm_block_reduce(nm);
+  nm = nm_block_reduce<kK1Threads / 32>(nm);
   if (threadIdx.x == 0) partial[blockIdx.x] = nm;
 }
 
@@ -1410,15 +1459,16 @@ __global__ void __launch_bounds__(kK1Threads) k1_deferred(TrainSpace sp, TrainTa
   NearMin m;
   nm_init(m);
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long key = (long long)slow_q[1 + i];
-    const long long p = key / sp.n_suf, s = key % sp.n_suf;
+    const long long key = (long long)slow_q[1 + i];  // a rank
     Prefix<R> P;
-    prefix_decode<R>(sp, p, P);
+    long long s;
+    rank_decode<R>(sp, key, P, s);
     PrefixData<R> D;
     prefix_data<R>(sp, tb, blkf, P, D);
     double x;
     const bool ok = eval_layout<R, false>(sp, tb, blkf, L, D, tb.suf[s], x, nullptr, nullptr);
-    if (DUMP) rg.dump[dump_base<R>(sp, p) - rg.dump_lo + s] = ok ? x : __longlong_as_double(0x7ff0000000000000LL);
+    if (DUMP && key >= rg.dump_lo && key < rg.dump_hi)
+      rg.dump[key - rg.dump_lo] = ok ? x : __longlong_as_double(0x7ff0000000000000LL);
     if (ok) {
       NearMin o;
       o.b0 = __double_as_longlong(x);
@@ -1433,7 +1483,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_deferred(TrainSpace sp, TrainTa
   if (threadIdx.x == 0) partial[blockIdx.x] = m;
 }
 
-// Merge CTA summaries, pick the window's winner and decode it (prefix, suffix) -> rank + plan.
+// Merge CTA summaries, pick the window's winner (keys are ranks) and decode its plan.
 template <int R>
 __device__ __forceinline__ void k1_finalize_body(const TrainSpace& sp, const TrainTables& tb,
                                                  const double2* __restrict__ blkf,
@@ -1452,15 +1502,12 @@ __device__ __forceinline__ void k1_finalize_body(const TrainSpace& sp, const Tra
   out->best = Best{cost, key, m.feasible};
   out->overflow = slow_q && slow_q[0] > (unsigned long long)kSlowQueue;  // -> generic rescan
   out->nm_b0 = m.b0;
-  Prefix<R> P;
-  for (int i = 0; i < 3; ++i)
-    out->nm_rank[i] = m.key[i] == LLONG_MAX ? LLONG_MAX
-                                            : prefix_decode<R>(sp, m.key[i] / sp.n_suf, P) + m.key[i] % sp.n_suf;
+  for (int i = 0; i < 3; ++i) out->nm_rank[i] = m.key[i];
   out->n_stages = 0;
   if (key == LLONG_MAX) return;
-  const long long p = key / sp.n_suf, s = key % sp.n_suf;
-  const long long base = prefix_decode<R>(sp, p, P);
-  out->best.rank = base + s;
+  Prefix<R> P;
+  long long s;
+  rank_decode<R>(sp, key, P, s);
   PrefixData<R> D;
   prefix_data<R>(sp, tb, blkf, P, D);
   constexpr int NS = R * kMaxPerRun;
@@ -1560,7 +1607,7 @@ __global__ void __launch_bounds__(kK1Threads) k_train_small(const SmallSet* __re
   for (long long idx = threadIdx.x; idx < (long long)S.nblk * L; idx += blockDim.x)  // K2c
     k2c_body(idx, S.blk, sc, ceff, S.mode, S.stage, S.opt);
   for (int i = threadIdx.x; i < S.n_choices; i += blockDim.x)  // K2d
-    k2d_body(i, S.choices, S.sp, S.tin, S.suf);
+    k2d_body(i, S.choices, S.sp, S.tin, S.suf, S.sp.R - 1);
   __syncthreads();
   __shared__ Prefix<R> sP[kK1Threads / 32];
   __shared__ PrefixData<R> sD[kK1Threads / 32];
@@ -1591,6 +1638,52 @@ struct HostSpace {
   bool exact_total = false;  // every partial FLOPS sum exact: K1-fast applies
   double flops_total = 0;    // allocate_layers' total (the same for every layout when exact)
 };
+
+// choices (k, cut positions) of run r in run_compositions order (k ascending, cuts lexicographic)
+static void run_choices(const TrainSpace& sp, int r, std::vector<int4>& out) {
+  out.clear();
+  const int nc = sp.nc[r];
+  for (int k = 1; k <= sp.kmax[r]; ++k) {
+    const int m = k - 1;
+    if (nc < m) break;
+    int c[3] = {0, 1, 2};
+    while (true) {
+      int4 ch = make_int4(k, 0, 0, 0);
+      if (m > 0) ch.y = c[0] + 1;
+      if (m > 1) ch.z = c[1] + 1;
+      if (m > 2) ch.w = c[2] + 1;
+      out.push_back(ch);
+      int j = m - 1;
+      while (j >= 0 && c[j] == nc - m + j) --j;
+      if (j < 0) break;
+      ++c[j];
+      for (int t = j + 1; t < m; ++t) c[t] = c[t - 1] + 1;
+    }
+  }
+}
+
+// completion counts cnt / cntP of a TrainSpace whose per-run fields are set
+static void space_counts(TrainSpace& sp) {
+  std::memset(sp.cnt, 0, sizeof sp.cnt);
+  std::memset(sp.cntP, 0, sizeof sp.cntP);
+  for (int u = 0; u <= sp.max_stages; ++u) {
+    sp.cnt[sp.R][u] = 1;
+    sp.cntP[sp.R - 1][u] = 1;
+  }
+  for (int r = sp.R - 1; r >= 0; --r) {
+    const int rem = sp.R - 1 - r;
+    for (int u = 0; u <= sp.max_stages; ++u) {
+      long long acc = 0, accP = 0;
+      for (int k = 1; k <= sp.kmax[r]; ++k) {
+        if (u + k + rem > sp.max_stages) break;
+        acc += binom_small(sp.nc[r], k - 1) * sp.cnt[r + 1][u + k];
+        if (r + 1 < sp.R) accP += binom_small(sp.nc[r], k - 1) * sp.cntP[r + 1][u + k];
+      }
+      sp.cnt[r][u] = acc;
+      if (r + 1 < sp.R) sp.cntP[r][u] = accP;
+    }
+  }
+}
 
 // True when every partial sum of these devices' FLOPS is exactly representable: all are
 // integer multiples of 2^e (e = the smallest trailing exponent) and sum / 2^e < 2^53.
@@ -1666,25 +1759,7 @@ int build_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, 
     sp.kmax[r] = std::min(sp.max_per_run, len);
   }
   // completion counts: cnt over all runs, cntP over the prefix runs
-  std::memset(sp.cnt, 0, sizeof sp.cnt);
-  std::memset(sp.cntP, 0, sizeof sp.cntP);
-  for (int u = 0; u <= sp.max_stages; ++u) {
-    sp.cnt[sp.R][u] = 1;
-    sp.cntP[sp.R - 1][u] = 1;
-  }
-  for (int r = sp.R - 1; r >= 0; --r) {
-    const int rem = sp.R - 1 - r;
-    for (int u = 0; u <= sp.max_stages; ++u) {
-      long long acc = 0, accP = 0;
-      for (int k = 1; k <= sp.kmax[r]; ++k) {
-        if (u + k + rem > sp.max_stages) break;
-        acc += binom_small(sp.nc[r], k - 1) * sp.cnt[r + 1][u + k];
-        if (r + 1 < sp.R) accP += binom_small(sp.nc[r], k - 1) * sp.cntP[r + 1][u + k];
-      }
-      sp.cnt[r][u] = acc;
-      if (r + 1 < sp.R) sp.cntP[r][u] = accP;
-    }
-  }
+  space_counts(sp);
   h.exact_total = exact_flops_total(ctx, h.ordered, &h.flops_total);
   h.mgrp.resize(n);
   for (int i = 0; i < n; ++i) {
@@ -1722,30 +1797,10 @@ int build_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, 
     }
   }
   // last-run choices in run_compositions order: k ascending, cut indices lexicographic
-  {
-    const int r = sp.R - 1, nc = sp.nc[r];
-    for (int k = 1; k <= sp.kmax[r]; ++k) {
-      const int m = k - 1;
-      if (nc < m) break;
-      int c[3] = {0, 1, 2};
-      while (true) {
-        int4 ch = make_int4(k, 0, 0, 0);
-        if (m > 0) ch.y = c[0] + 1;
-        if (m > 1) ch.z = c[1] + 1;
-        if (m > 2) ch.w = c[2] + 1;
-        h.choices.push_back(ch);
-        int j = m - 1;
-        while (j >= 0 && c[j] == nc - m + j) --j;
-        if (j < 0) break;
-        ++c[j];
-        for (int t = j + 1; t < m; ++t) c[t] = c[t - 1] + 1;
-      }
-    }
-    sp.n_suf = (int)h.choices.size();
-  }
+  run_choices(sp, sp.R - 1, h.choices);
+  sp.n_suf = (int)h.choices.size();
   return GP_OK;
 }
-
 // Host twin of prefix_decode's base (rank of a prefix's first layout).
 template <int R>
 long long prefix_base_host(const TrainSpace& sp, long long p) {
@@ -1763,22 +1818,25 @@ long long prefix_base(const TrainSpace& sp, long long p) {
   }
 }
 
-// rank -> (prefix, suffix): the last prefix whose base <= rank.
-void rank_split(const HostSpace& h, long long rank, long long& p, long long& s) {
-  if (rank >= h.total) {
-    p = h.n_prefix;
+// rank (of sp's enumeration order) -> (prefix, suffix): the last prefix whose base <= rank.
+void rank_split(const TrainSpace& sp, long long rank, long long& p, long long& s) {
+  const bool any = sp.max_stages >= sp.R;
+  const long long total = any ? sp.cnt[0][0] : 0, n_prefix = any ? sp.cntP[0][0] : 0;
+  if (rank >= total) {
+    p = n_prefix;
     s = 0;
     return;
   }
-  long long lo = 0, hi = h.n_prefix - 1;
+  long long lo = 0, hi = n_prefix - 1;
   while (lo < hi) {
     const long long mid = lo + (hi - lo + 1) / 2;
-    if (prefix_base(h.sp, mid) <= rank) lo = mid;
+    if (prefix_base(sp, mid) <= rank) lo = mid;
     else hi = mid - 1;
   }
   p = lo;
-  s = rank - prefix_base(h.sp, lo);
+  s = rank - prefix_base(sp, lo);
 }
+void rank_split(const HostSpace& h, long long rank, long long& p, long long& s) { rank_split(h.sp, rank, p, s); }
 
 template <typename T>
 T* carve(char*& p, size_t count) {
@@ -1788,59 +1846,79 @@ T* carve(char*& p, size_t count) {
   return r;
 }
 
+// What one K1 launch scans: ranks [lo, hi) of the reference order, with K1-fast or the
+// generic K1. dump (test hook): per_step of the ranks [dump_lo, dump_hi).
+struct ScanSpec {
+  long long lo = 0, hi = 0;
+  bool fast = false;
+  double* dump = nullptr;
+  long long dump_lo = 0, dump_hi = 0;
+  bool defer_all = false;
+};
+
 template <int R>
 int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const double2* blkf,
-                const BlockRec* blk, int window, long long lo, long long hi, NearMin* partial,
-                int max_blocks, TrainOut* d_out, cudaStream_t stream, bool fast, int mode,
-                unsigned long long* slow_q, double* dump = nullptr, bool defer_all = false) {
+                const BlockRec* blk, int window, const ScanSpec& sc, NearMin* partial,
+                int max_blocks, TrainOut* d_out, cudaStream_t stream, int mode,
+                unsigned long long* slow_q) {
+  const bool fast = sc.fast;
+  const TrainSpace& sp = h.sp;
   ScanRange rg{};
-  rg.dump = dump;
-  rg.dump_lo = lo;
-  rank_split(h, lo, rg.p_lo, rg.s_lo);
-  rank_split(h, hi, rg.p_hi, rg.s_hi);
+  rg.dump = sc.dump;
+  rg.dump_lo = sc.dump_lo;
+  rg.dump_hi = sc.dump_hi;
+  rank_split(sp, sc.lo, rg.p_lo, rg.s_lo);
+  rank_split(sp, sc.hi, rg.p_hi, rg.s_hi);
   const char* defer_env = std::getenv("GPLAN_K1_DEFER_ALL");
-  rg.defer_all = defer_all || (defer_env && defer_env[0] == '1');
+  rg.defer_all = sc.defer_all || (defer_env && defer_env[0] == '1');
   rg.n_pref = rg.p_hi - rg.p_lo + (rg.s_hi > 0 ? 1 : 0);
   const int threads = kK1Threads;
-  static int occ_g = 0, occ_f = 0;
-  int& occ = fast ? occ_f : occ_g;
-  if (!occ) {
-    if (fast) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_layout_scan_fast<R>, threads, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_layout_scan<R>, threads, 0);
-    occ = std::max(1, occ);
-  }
+  static std::once_flag occ_once;  // occupancy of the two scan kernels (shared by all contexts)
+  static int occ_tab[2][5];
+  std::call_once(occ_once, [] {
+    const void* fk[5] = {nullptr, (const void*)k1_layout_scan_fast<1>, (const void*)k1_layout_scan_fast<2>,
+                         (const void*)k1_layout_scan_fast<3>, (const void*)k1_layout_scan_fast<4>};
+    const void* gk[5] = {nullptr, (const void*)k1_layout_scan<1>, (const void*)k1_layout_scan<2>,
+                         (const void*)k1_layout_scan<3>, (const void*)k1_layout_scan<4>};
+    for (int r = 1; r <= 4; ++r) {
+      int o = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fk[r], kK1Threads, 0);
+      occ_tab[1][r] = std::max(1, o);
+      o = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, gk[r], kK1Threads, 0);
+      occ_tab[0][r] = std::max(1, o);
+    }
+  });
+  const int occ = occ_tab[fast ? 1 : 0][R];
   const long long warps_total = (long long)ctx->num_sms * occ * (threads / 32);
   rg.chunk = std::max(1LL, rg.n_pref / (warps_total * 6));
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
   long long blocks = (n_items + (threads / 32) - 1) / (threads / 32);
   blocks = std::max(1LL, std::min(blocks, std::min((long long)max_blocks, (long long)ctx->num_sms * occ)));
   int n_partial = (int)blocks;
-  if (hi > lo) {
+  const int L = ctx->sc.L;
+  if (sc.hi > sc.lo) {
     if (fast) {
       GP_CUDA(cudaMemsetAsync(slow_q, 0, sizeof(unsigned long long), stream));
-      if (dump) {
-        k1_layout_scan_fast<R, true><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg,
-                                                                          partial, slow_q);
-        k1_deferred<R, true><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, slow_q,
-                                                                   partial + blocks, rg);
+      if (sc.dump) {
+        k1_layout_scan_fast<R, true><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, L, rg, partial, slow_q);
+        k1_deferred<R, true><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, L, slow_q, partial + blocks, rg);
       } else {
-        k1_layout_scan_fast<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial,
-                                                                    slow_q);
-        k1_deferred<R><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, slow_q,
-                                                              partial + blocks, rg);
+        k1_layout_scan_fast<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, L, rg, partial, slow_q);
+        k1_deferred<R><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, L, slow_q, partial + blocks, rg);
       }
       n_partial += kDeferBlocks;
       ctx->launches += 2;
     } else {
-      if (dump) k1_layout_scan<R, true><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial);
-      else k1_layout_scan<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, ctx->sc.L, rg, partial);
+      if (sc.dump) k1_layout_scan<R, true><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, L, rg, partial);
+      else k1_layout_scan<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, L, rg, partial);
       ctx->launches++;
     }
   } else {
     n_partial = 0;
   }
-  k1_finalize<R><<<1, 256, 0, stream>>>(h.sp, tb, blkf, blk, ctx->sc.L, window, partial, n_partial, d_out,
-                                        fast && hi > lo ? slow_q : nullptr, ctx->sc, ctx->d_ceff, mode);
+  k1_finalize<R><<<1, 256, 0, stream>>>(h.sp, tb, blkf, blk, L, window, partial, n_partial, d_out,
+                                        fast && sc.hi > sc.lo ? slow_q : nullptr, ctx->sc, ctx->d_ceff, mode);
   ctx->launches++;
   GP_CUDA(cudaGetLastError());
   return GP_OK;
@@ -2195,9 +2273,36 @@ static TrainTables prepared_tables(const gp_ctx* ctx, const PreparedTrain& P) {
 }
 
 // Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
+// Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
+// K1-fast can use a view with run r innermost (its per-prefix rank counts / junction rows fit)
+static bool inner_fits(const TrainSpace& sp, int r) {
+  const int e = sp.nc[r] + 2;
+  return e * (e - 1) / 2 <= kMaxLastBlocks && e <= kMaxJunction;
+}
+
+// rank == total, or the first layout of some choice of run 0 (every later run at its first
+// choice): ranges between such ranks hold the same layouts in the reference order and in a
+// fast view whose outer enumeration starts with run 0 (the layout count below a run-0 choice
+// does not depend on the order of the later runs), so such ranges can be scanned with it.
+static bool run0_aligned(const TrainSpace& sp, long long rank) {
+  const long long total = sp.max_stages >= sp.R ? sp.cnt[0][0] : 0;
+  if (rank <= 0 || rank >= total) return true;
+  const int rem_runs = sp.R - 1;
+  for (int k = 1; k <= sp.kmax[0]; ++k) {
+    if (k + rem_runs > sp.max_stages) break;
+    const long long c = binom_small(sp.nc[0], k - 1), sub = sp.cnt[1][k];
+    if (rank < c * sub) return rank % sub == 0;
+    rank -= c * sub;
+  }
+  return false;
+}
+
+// Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
+// dump (test hook, gp_debug_layout_costs): per_step of ranks [dump_lo, dump_hi).
 static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long lo, long long hi,
                            cudaStream_t stream, bool timing, bool force_generic = false, int lane = -1,
-                           double* dump = nullptr, bool* used_fast = nullptr, bool defer_all = false) {
+                           double* dump = nullptr, bool* used_fast = nullptr, bool defer_all = false,
+                           long long dump_lo = 0, long long dump_hi = 0) {
   const HostSpace& h = P.h;
   if (lo < 0) lo = 0;
   if (hi < 0 || hi > h.total) hi = h.total;
@@ -2208,14 +2313,14 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   P.launched = true;
   if (h.total == 0 || lo == hi) return GP_OK;  // std::nullopt
   const int L = ctx->sc.L;
-  const TrainTables tb = prepared_tables(ctx, P);
+  TrainTables tb = prepared_tables(ctx, P);
   const char* generic_env = std::getenv("GPLAN_K1_GENERIC");
-  // (layer counts are tabulated as signed bytes: L <= 127)
-  const int nlast = (h.sp.nc[h.sp.R - 1] + 2) * (h.sp.nc[h.sp.R - 1] + 1) / 2;
-  // (small spaces: the generic scan; the fast path's extra table launches would dominate)
-  const bool fast = h.exact_total && h.total >= (1LL << 20) && ctx->sc.L <= 127 && nlast <= kMaxLastBlocks &&
-                    h.sp.nc[h.sp.R - 1] + 2 <= kMaxJunction && !force_generic &&
-                    !(generic_env && generic_env[0] == '1');
+  const int R = h.sp.R;
+  // (layer counts are tabulated as signed bytes: L <= 127; small spaces: the generic scan —
+  // the fast path's extra table launches would dominate)
+  const int nlast = (h.sp.nc[R - 1] + 2) * (h.sp.nc[R - 1] + 1) / 2;
+  const bool fast = h.exact_total && h.total >= (1LL << 20) && L <= 127 && nlast <= kMaxLastBlocks &&
+                    h.sp.nc[R - 1] + 2 <= kMaxJunction && !force_generic && !(generic_env && generic_env[0] == '1');
   if (used_fast) *used_fast = fast;
   unsigned long long*& slow_q = lane < 0 ? ctx->d_slow : ctx->d_slow_lane[lane];
   if (fast && !slow_q) GP_CUDA(cudaMalloc(&slow_q, sizeof(unsigned long long) * (1 + kSlowQueue)));
@@ -2238,13 +2343,13 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
     k2c_stage_table<<<(int)((cnt + 255) / 256), 256, 0, stream>>>(P.d_blk, h.nblk, ctx->sc, ctx->d_ceff,
                                                                  P.mode, P.d_stage, P.d_opt);
     const int ns = (int)h.choices.size();
-    k2d_suffix_table<<<(ns + 255) / 256, 256, 0, stream>>>(P.d_choices, ns, h.sp, P.d_tin, P.d_suf);
+    k2d_suffix_table<<<(ns + 255) / 256, 256, 0, stream>>>(P.d_choices, ns, h.sp, P.d_tin, P.d_suf, R - 1);
     ctx->launches += 2;
     if (fast) {
       k2e_block_shares<<<(h.nblk + 255) / 256, 256, 0, stream>>>(P.d_blkf, h.nblk, h.flops_total, P.d_blk_sh);
       GP_CUDA(cudaMemsetAsync(P.d_nzs_max, 0, (3 + 5 * (L + 1)) * sizeof(int), stream));
       k2f_suffix_fast<<<(ns + 127) / 128, 128, 0, stream>>>(P.d_suf, ns, P.d_blk_sh, P.d_stage, L,
-                                                           h.sp.blk_off[h.sp.R - 1], P.d_sf_hot, P.d_sf_zb,
+                                                           h.sp.blk_off[R - 1], P.d_sf_hot, P.d_sf_zb,
                                                            P.d_sf_t, P.d_sf_ms, P.d_sf_st, P.d_nzs_max);
       ctx->launches += 2;
     }
@@ -2252,15 +2357,34 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   GP_CUDA(cudaGetLastError());
   if (timing) GP_CUDA(cudaEventRecord(ctx->ev[1], stream));
   // ---- K1: layout scan over [lo, hi)
-  const int R = h.sp.R;
+  ScanSpec sc;
+  sc.lo = lo;
+  sc.hi = hi;
+  sc.fast = fast;
+  sc.dump = dump;
+  sc.dump_lo = dump_lo;
+  sc.dump_hi = dump_hi;
+  sc.defer_all = defer_all;
   int rc;
-  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q, dump, defer_all);
-  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q, dump, defer_all);
-  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q, dump, defer_all);
-  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, lo, hi, P.d_partial, P.max_blocks, P.d_out, stream, fast, P.mode, slow_q, dump, defer_all);
+  if (R == 1) rc = launch_scan<1>(ctx, h, tb, P.d_blkf, P.d_blk, window, sc, P.d_partial, P.max_blocks, P.d_out, stream, P.mode, slow_q);
+  else if (R == 2) rc = launch_scan<2>(ctx, h, tb, P.d_blkf, P.d_blk, window, sc, P.d_partial, P.max_blocks, P.d_out, stream, P.mode, slow_q);
+  else if (R == 3) rc = launch_scan<3>(ctx, h, tb, P.d_blkf, P.d_blk, window, sc, P.d_partial, P.max_blocks, P.d_out, stream, P.mode, slow_q);
+  else if (R == 4) rc = launch_scan<4>(ctx, h, tb, P.d_blkf, P.d_blk, window, sc, P.d_partial, P.max_blocks, P.d_out, stream, P.mode, slow_q);
   else rc = set_error(GP_INVALID, "train sets spanning more than 4 gpu types are not supported");
   if (!rc && timing) GP_CUDA(cudaEventRecord(ctx->ev[2], stream));
   return rc;
+}
+
+// Rank boundaries splitting a train set's space into n_shards contiguous ranges of equal
+// layout count (bench.py / multi-GPU fan-out; every range scans with the same kernels).
+int train_shard_bounds(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int n_shards,
+                       int64_t* bounds) {
+  int64_t total = 0;
+  int rc = train_space(ctx, ids, n, o, &total);
+  if (rc) return rc;
+  if (n_shards < 1) return set_error(GP_INVALID, "n_shards must be >= 1");
+  for (int i = 0; i <= n_shards; ++i) bounds[i] = (int64_t)((__int128)total * i / n_shards);
+  return GP_OK;
 }
 
 static void fill_result(PreparedTrain& P, const TrainOut* ho, gp_train_result* out, int32_t* stage_devices) {
@@ -2317,10 +2441,12 @@ int train_prepare(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o
 
 // Test hook (gp_debug_layout_costs): per_step of every layout of ranks [lo, hi) as the scan
 // kernels compute it (DUMP instantiations of the same code), +inf for memory-infeasible
-// layouts. path 0: the kernel the search would use (K1-fast when eligible); 1: generic K1;
-// 2: K1-fast with every candidate deferred to k1_deferred. *fast_used: K1-fast scored them.
+// layouts. path 0: the whole-space scan a search runs (K1-fast with its best inner run when
+// eligible), values of [lo, hi) kept; 1: generic K1 over [lo, hi); 2: K1-fast over [lo, hi)
+// with every candidate deferred to k1_deferred; 3: K1-fast over [lo, hi) as a range search
+// scans it. *fast_used: K1-fast scored them; *inner: its inner run (-1: generic).
 int train_layout_costs(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, long long lo,
-                       long long hi, int path, double* out, int* fast_used) {
+                       long long hi, int path, double* out, int* fast_used, int* inner) {
   int rc = train_prepare(ctx, ids, n, o, 0);
   if (rc) return rc;
   PreparedTrain& P = *prepared(ctx);
@@ -2331,8 +2457,10 @@ int train_layout_costs(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_op
   if (!d) return GP_CUDA_ERROR;
   GP_CUDA(cudaMemsetAsync(d, 0xff, sizeof(double) * (size_t)(hi - lo), ctx->stream));  // NaN: unwritten
   bool fast = false;
-  rc = launch_prepared(ctx, P, 1, lo, hi, ctx->stream, false, path == 1, -1, d, &fast, path == 2);
+  const long long slo = path == 0 ? 0 : lo, shi = path == 0 ? P.h.total : hi;
+  rc = launch_prepared(ctx, P, 1, slo, shi, ctx->stream, false, path == 1, -1, d, &fast, path == 2, lo, hi);
   if (rc) return rc;
+  if (inner) *inner = fast ? P.h.sp.R - 1 : -1;  // K1-fast scans the last type run innermost
   TrainOut* ho = reinterpret_cast<TrainOut*>(ctx_pinned(ctx, sizeof(TrainOut)));
   GP_CUDA(cudaMemcpyAsync(ho, P.d_out, sizeof(TrainOut), cudaMemcpyDeviceToHost, ctx->stream));
   GP_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -183,15 +183,25 @@ class Engine:
 
     def debug_layout_costs(self, train_set, lo: int, hi: int, path: int = 0, opts=None):
         """Test hook: per_step of every layout of ranks [lo, hi) as the scan kernel computes it
-        (+inf: memory-infeasible). path 0 = the kernel the search uses, 1 = generic K1,
-        2 = K1-fast with every candidate deferred. Returns (array, fast_used)."""
+        (+inf: memory-infeasible). path 0 = the whole-space scan a search runs, 1 = generic K1,
+        2 = K1-fast with every candidate deferred, 3 = K1-fast over the range as a range search.
+        Returns (array, fast_used) with fast_used = 1 + K1-fast's inner run, 0 = generic."""
         ids = _ids(train_set)
         out = np.empty(max(hi - lo, 1), dtype=np.float64)
         fast = C.c_int32()
         _check(lib().gp_debug_layout_costs(self._h, ids.ctypes.data_as(abi.i32p), len(ids),
                                            C.byref(opts or abi.default_train_opts()), lo, hi, path,
                                            out.ctypes.data_as(abi.f64p), C.byref(fast)))
-        return out[:hi - lo], bool(fast.value)
+        return out[:hi - lo], fast.value
+
+    def shard_bounds(self, train_set, n_shards: int, opts=None):
+        """Rank boundaries of n_shards balanced contiguous shards (gp_train_shard_bounds)."""
+        ids = _ids(train_set)
+        b = np.zeros(n_shards + 1, dtype=np.int64)
+        _check(lib().gp_train_shard_bounds(self._h, ids.ctypes.data_as(abi.i32p), len(ids),
+                                           C.byref(opts or abi.default_train_opts()), n_shards,
+                                           b.ctypes.data_as(C.POINTER(C.c_int64))))
+        return b.tolist()
 
     # ---- split form + measurement hooks (bench.py) -------------------------
     @property

@@ -9,6 +9,7 @@
 // go through the PLT, so the first definition in load order wins. See
 // INTEGRATION.md. Errors come back as gp_status codes and are rethrown as the
 // reference's exception types (inc/common.hpp:11-39).
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -35,7 +36,43 @@ namespace {
 
 using namespace rlsched;
 
-long long g_calls = 0;
+std::atomic<long long> g_calls{0};
+
+// GPLAN_SHIM_LOG=<path>: one JSON line per seam call (inputs only) — how the C4 call
+// sample behind tests/golden/c4_calls.json was recorded. GPLAN_REQUIRE_ENGINE=1: exit with
+// status 86 if the process ends without a single seam call reaching the engine (the shim was
+// loaded but the binary bound its own copies, e.g. a static reference build).
+struct Guard {
+  std::mutex mu;
+  FILE* log = nullptr;
+  Guard() {
+    if (const char* p = std::getenv("GPLAN_SHIM_LOG")) log = std::fopen(p, "w");
+  }
+  ~Guard() {
+    if (log) std::fclose(log);
+    const char* req = std::getenv("GPLAN_REQUIRE_ENGINE");
+    if (req && req[0] == '1' && g_calls.load() == 0) {
+      std::fprintf(stderr, "gplan_shim: GPLAN_REQUIRE_ENGINE=1 but no rlsched seam call reached the B200 "
+                           "engine (was the reference linked statically?)\n");
+      std::fflush(stderr);
+      std::_Exit(86);
+    }
+  }
+  template <typename F>
+  void line(F&& f) {
+    if (!log) return;
+    std::lock_guard<std::mutex> lock(mu);
+    f(log);
+    std::fputc('\n', log);
+    std::fflush(log);
+  }
+} g_guard;
+
+void put_ids(FILE* f, const std::vector<int>& v) {
+  std::fputc('[', f);
+  for (size_t i = 0; i < v.size(); ++i) std::fprintf(f, i ? ",%d" : "%d", v[i]);
+  std::fputc(']', f);
+}
 
 // GPLAN_PROFILE=1: wall time per seam function, printed at exit (stderr)
 struct Prof {
@@ -94,9 +131,15 @@ struct Ctx {
   gp_ctx* ctx = nullptr;
   ~Ctx() { gp_ctx_destroy(ctx); }
 };
+using CtxRef = std::shared_ptr<Ctx>;  // a seam call holds its context for the whole call
 
 std::mutex g_mu;
-std::vector<std::unique_ptr<Ctx>> g_ctx;
+std::vector<CtxRef> g_ctx;       // (cluster, workload, calibration) contexts, at most 8
+std::vector<CtxRef> g_part_ctx;  // cluster-only contexts of the partition seam, at most 8
+// solve_milp carries no cluster: it runs on the context of this thread's latest
+// enumerate_configs / constrained_search (evaluate_partition calls them first,
+// src/scheduler.cpp:50-60), so its lattice tables stay on that context's device
+thread_local CtxRef t_last;
 
 std::vector<double> scalars_of(const WorkloadSpec& w, const Calibration& k, const ClusterGraph& g) {
   std::vector<double> s = {w.model_params_b, (double)w.num_layers, (double)w.hidden_dim,
@@ -116,9 +159,9 @@ std::vector<double> scalars_of(const WorkloadSpec& w, const Calibration& k, cons
 
 // The shim must not depend on symbols of the reference library itself (it is
 // loaded before it), so it only uses header-inline members of the reference types.
-gp_ctx* make_context(const ClusterGraph& g, const Key& key, const gp_workload& wl,
-                     const std::vector<double>& ce, const std::vector<double>& io,
-                     const CostModelParams& p) {
+CtxRef make_context(const ClusterGraph& g, const Key& key, const gp_workload& wl,
+                    const std::vector<double>& ce, const std::vector<double>& io,
+                    const CostModelParams& p, std::vector<CtxRef>& pool) {
   const int N = g.size(), T = (int)g.types.size();
   std::vector<int32_t> dtype(N), dmach(N);
   std::vector<double> dfl(N), dbw(N), dcap(N), tfl(T), tbw(T), tcap(T);
@@ -153,18 +196,20 @@ gp_ctx* make_context(const ClusterGraph& g, const Key& key, const gp_workload& w
   }
   gp_ctx* h = nullptr;
   check(gp_ctx_create_multi(&c, &wl, &kc, devs.data(), (int)devs.size(), &h));
-  if (g_ctx.size() >= 8) g_ctx.erase(g_ctx.begin());
-  g_ctx.push_back(std::make_unique<Ctx>());
-  g_ctx.back()->key = key;
-  g_ctx.back()->ctx = h;
-  return h;
+  auto ref = std::make_shared<Ctx>();
+  ref->key = key;
+  ref->ctx = h;
+  // eviction drops the pool's reference only: a call still using the context keeps it alive
+  if (pool.size() >= 8) pool.erase(pool.begin());
+  pool.push_back(ref);
+  return ref;
 }
 
-gp_ctx* context(const ClusterGraph& g, const WorkloadSpec& w, const Calibration& k) {
+CtxRef context(const ClusterGraph& g, const WorkloadSpec& w, const Calibration& k) {
   Key key{&g, g.fingerprint, g.size(), scalars_of(w, k, g)};
   std::lock_guard<std::mutex> lock(g_mu);
   for (auto& c : g_ctx)
-    if (c->key == key) return c->ctx;
+    if (c->key == key) return t_last = c;
   std::vector<double> ce, io;
   for (const auto& t : g.types) {
     auto it = k.per_type.find(t.name);  // Calibration::for_type (src/calibration.cpp:15-21)
@@ -175,19 +220,22 @@ gp_ctx* context(const ClusterGraph& g, const WorkloadSpec& w, const Calibration&
   gp_workload wl{w.model_params_b, w.num_layers, w.hidden_dim, w.batch_rollouts, w.prompt_len,
                  w.length_dist.mean(), w.bytes_per_param_train, w.bytes_per_param_infer,
                  w.reward_cost_const, w.micro_batches, w.staleness};
-  return make_context(g, key, wl, ce, io, k.params);
+  return t_last = make_context(g, key, wl, ce, io, k.params, g_ctx);
 }
 
-// Partition kernels read only the cluster; any context for this cluster serves.
-gp_ctx* any_context(const ClusterGraph& g) {
+// Partition kernels read only the cluster; any context for this cluster serves. The
+// cluster-only contexts live in their own pool, so they never evict a workload context
+// (and its MILP lattice cache).
+CtxRef any_context(const ClusterGraph& g) {
   std::lock_guard<std::mutex> lock(g_mu);
   for (auto& c : g_ctx)
-    if (c->key.cluster == &g && c->key.fingerprint == g.fingerprint && c->key.n == g.size())
-      return c->ctx;
+    if (c->key.cluster == &g && c->key.fingerprint == g.fingerprint && c->key.n == g.size()) return c;
+  for (auto& c : g_part_ctx)
+    if (c->key.cluster == &g && c->key.fingerprint == g.fingerprint && c->key.n == g.size()) return c;
   Key key{&g, g.fingerprint, g.size(), {-1.0}};
   gp_workload wl{1.0, 1, 1, 1, 0, 1.0, 18.0, 2.0, 0.0, 8, 0};
   std::vector<double> ce(g.types.size(), 0.35), io(g.types.size(), 0.6);
-  return make_context(g, key, wl, ce, io, CostModelParams{});
+  return make_context(g, key, wl, ce, io, CostModelParams{}, g_part_ctx);
 }
 
 ReplicaConfig to_config(const gp_config& c, int T) {
@@ -222,7 +270,13 @@ std::optional<TrainSearchResult> constrained_search(const std::vector<int>& trai
                                                     const Calibration& calib, int window,
                                                     const TrainSearchOptions& options) {
   Timer _t(0);
-  gp_ctx* h = context(cluster, work, calib);
+  const CtxRef ref = context(cluster, work, calib);
+  gp_ctx* h = ref->ctx;
+  g_guard.line([&](FILE* f) {
+    std::fprintf(f, "{\"call\":\"constrained_search\",\"window\":%d,\"ids\":", window);
+    put_ids(f, train_set);
+    std::fputc('}', f);
+  });
   gp_train_opts o{options.max_stages_per_type, options.device_granularity_limit};
   gp_train_result res;
   std::vector<int32_t> devs(train_set.size() + 1);
@@ -249,12 +303,24 @@ std::vector<ReplicaConfig> enumerate_configs(const std::vector<int>& rollout_set
                                              const Calibration& calib,
                                              const RolloutSearchOptions& options) {
   Timer _t(1);
-  gp_ctx* h = context(cluster, work, calib);
+  const CtxRef ref = context(cluster, work, calib);
+  gp_ctx* h = ref->ctx;
+  g_guard.line([&](FILE* f) {
+    std::fprintf(f, "{\"call\":\"enumerate_configs\",\"max_stages\":%d,\"ids\":", options.max_stages);
+    put_ids(f, rollout_set);
+    std::fputc('}', f);
+  });
   gp_rollout_opts o{options.max_stages};
-  std::vector<gp_config> buf(70 * cluster.types.size() + 8);
+  std::vector<gp_config> buf(128 * cluster.types.size() + 8);
   int32_t n = 0;
-  check(gp_enumerate_configs(h, rollout_set.data(), (int32_t)rollout_set.size(), &o, buf.data(),
-                             (int32_t)buf.size(), &n));
+  int rc = gp_enumerate_configs(h, rollout_set.data(), (int32_t)rollout_set.size(), &o, buf.data(),
+                                (int32_t)buf.size(), &n);
+  if (rc == GP_CAPACITY) {  // the engine reports the size it needs: retry once with it
+    buf.resize((size_t)n + 8);
+    rc = gp_enumerate_configs(h, rollout_set.data(), (int32_t)rollout_set.size(), &o, buf.data(),
+                              (int32_t)buf.size(), &n);
+  }
+  check(rc);
   std::vector<ReplicaConfig> out;
   for (int i = 0; i < n; ++i) out.push_back(to_config(buf[i], (int)cluster.types.size()));
   return out;
@@ -269,14 +335,15 @@ std::vector<int> rollout_capacities(const std::vector<int>& rollout_set, const C
 RolloutPlan solve_milp(const std::vector<ReplicaConfig>& configs, const std::vector<int>& capacities,
                        double total_rollouts, double mean_len) {
   Timer _t(2);
-  // solve_milp carries no cluster: use the most recent engine context (every
-  // scheduler call site follows enumerate_configs on the same context).
-  gp_ctx* h = nullptr;
-  {
-    std::lock_guard<std::mutex> lock(g_mu);
-    if (!g_ctx.empty()) h = g_ctx.back()->ctx;
-  }
-  if (!h) throw std::runtime_error("libgplan: solve_milp before any engine context exists");
+  const CtxRef ref = t_last;  // this thread's latest context (see t_last)
+  if (!ref) throw std::runtime_error("libgplan: solve_milp before any engine context exists on this thread");
+  gp_ctx* h = ref->ctx;
+  g_guard.line([&](FILE* f) {
+    std::fprintf(f, "{\"call\":\"solve_milp\",\"total_rollouts\":%.17g,\"mean_len\":%.17g,\"n_configs\":%zu,"
+                    "\"caps\":", total_rollouts, mean_len, configs.size());
+    put_ids(f, capacities);
+    std::fputc('}', f);
+  });
   std::vector<gp_config> cfg;
   for (const auto& c : configs) cfg.push_back(from_config(c));
   std::vector<gp_rollout_entry> ent(configs.size() + 1);
@@ -300,7 +367,8 @@ double weight_sync_cost(const TrainPlan& /*train_plan*/, const RolloutPlan& roll
                         const DevicePartition& partition, const ClusterGraph& cluster,
                         const WorkloadSpec& work, const Calibration& calib, int window) {
   Timer _t(3);
-  gp_ctx* h = context(cluster, work, calib);
+  const CtxRef ref = context(cluster, work, calib);
+  gp_ctx* h = ref->ctx;
   std::vector<int32_t> et, er;
   for (const auto& e : rollout_plan.entries) {
     et.push_back(e.config.gpu_type());
@@ -318,7 +386,15 @@ std::vector<PartitionResult> graph_partition_candidates(const ClusterGraph& clus
                                                         const PartitionOptions& options, int k) {
   Timer _t(4);
   if (cluster.size() < 2) throw ValidationError("graph_partition requires at least two devices");
-  gp_ctx* h = any_context(cluster);
+  const CtxRef ref = any_context(cluster);
+  gp_ctx* h = ref->ctx;
+  g_guard.line([&](FILE* f) {
+    std::fprintf(f, "{\"call\":\"graph_partition_candidates\",\"q\":%.17g,\"r\":%.17g,\"gamma_l\":%.17g,"
+                    "\"gamma_h\":%.17g,\"k\":%d,\"seed\":%llu,\"restarts\":%d,\"exact_threshold\":%d,"
+                    "\"force_local\":%d,\"machine\":%d}", gamma.q, gamma.r, gamma.gamma_l, gamma.gamma_h, k,
+                 (unsigned long long)options.seed, options.restarts, options.exact_threshold,
+                 (int)options.force_local_search, (int)options.machine_granularity);
+  });
   gp_gamma g{gamma.q, gamma.r, gamma.gamma_l, gamma.gamma_h};
   gp_part_opts o{options.exact_threshold, options.restarts, options.seed, options.band_epsilon,
                  options.force_local_search, options.machine_granularity};
@@ -344,7 +420,8 @@ std::vector<PartitionResult> graph_partition_candidates(const ClusterGraph& clus
 
 double partition_objective(const ClusterGraph& cluster, const std::vector<int>& train_set) {
   Timer _t(5);
-  gp_ctx* h = any_context(cluster);
+  const CtxRef ref = any_context(cluster);
+  gp_ctx* h = ref->ctx;
   double obj = 0, frac = 0;
   check(gp_partition_objective(h, train_set.data(), (int32_t)train_set.size(), &obj, &frac));
   return obj;
@@ -352,7 +429,8 @@ double partition_objective(const ClusterGraph& cluster, const std::vector<int>& 
 
 double compute_fraction(const ClusterGraph& cluster, const std::vector<int>& train_set) {
   Timer _t(6);
-  gp_ctx* h = any_context(cluster);
+  const CtxRef ref = any_context(cluster);
+  gp_ctx* h = ref->ctx;
   double frac = 0;
   check(gp_compute_fraction(h, train_set.data(), (int32_t)train_set.size(), &frac));
   return frac;
@@ -360,11 +438,13 @@ double compute_fraction(const ClusterGraph& cluster, const std::vector<int>& tra
 
 }  // namespace rlsched
 
-extern "C" long long gplan_shim_calls() { return g_calls; }
+extern "C" long long gplan_shim_calls() { return g_calls.load(); }
 
 // Drops every engine context (and with them the cached MILP lattice tables); the CUDA
 // runtime stays initialised. Used to time "warm process, cold caches" runs.
 extern "C" void gplan_shim_reset() {
   std::lock_guard<std::mutex> lock(g_mu);
   g_ctx.clear();
+  g_part_ctx.clear();
+  t_last.reset();
 }

@@ -47,7 +47,8 @@ def test_cli_schedule_outputs_byte_identical(tmp_path):
             "--workload", os.path.join(data, "workloads", "c1_desk_mixed.json"),
             "--calibration", os.path.join(data, "calibration", "c1_desk_mixed.json"), "--eta", "4"]
     outs = {}
-    for label, env in (("cpu", dict(os.environ)), ("engine", dict(os.environ, LD_PRELOAD=SHIM, GPLAN_PROFILE="1"))):
+    for label, env in (("cpu", dict(os.environ)),
+                       ("engine", dict(os.environ, LD_PRELOAD=SHIM, GPLAN_PROFILE="1", GPLAN_REQUIRE_ENGINE="1"))):
         d = tmp_path / label
         r = subprocess.run(args + ["--out", str(d)], capture_output=True, env=env, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]

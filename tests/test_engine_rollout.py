@@ -143,3 +143,44 @@ def test_milp_batch_vs_oracle(name):
             assert res.makespan == res_o.makespan and res.aggregate == res_o.aggregate
             assert [(e.config, e.replicas, e.workload) for e in ent] == \
                 [(e.config, e.replicas, e.workload) for e in ent_o]
+
+
+@pytest.mark.parametrize("name", ["c3_64gpu", "c5_1024gpu"])
+def test_rollout_max_stages_up_to_8(name):
+    """RolloutSearchOptions::max_stages 1..8 (GP_MAX_ROLLOUT_STAGES): K3's config lists equal
+    the oracle's and the unmodified reference's (src/rollout_milp.cpp:39-89), and the MILP
+    over the deeper configs equals the oracle's; > 8 is rejected (gp_config holds 8 stages)."""
+    from oracles import Ref, ref_available
+
+    from paper_2511_00796_b200 import abi
+    from paper_2511_00796_b200.engine import ValidationError
+    p = problem(name)
+    eng, orc = engine(name), Oracle(p)
+    T = len(p.cluster.type_names)
+    ref = Ref(p) if ref_available() else None
+    n = p.cluster.n
+    sets = [sorted(set(range(n)) - set(t)) for t in random_train_sets(n, 4, seed=31 + n)]
+    sets.append(list(range(n)))
+    for roll in sets:
+        for ms in range(1, 9):
+            got = [config_dict(c, T) for c in eng.enumerate_configs(roll, opts=abi.gp_rollout_opts(ms))]
+            assert got == [config_dict(c, T) for c in oracle_configs(orc, roll, max_stages=ms)], ms
+            if ref is not None:
+                want = ref.enumerate_configs(roll, max_stages=ms)["configs"]
+                assert got == [{k: c[k] for k in ("type_counts", "tp_per_stage", "throughput")} for c in want]
+        with pytest.raises(ValidationError):
+            eng.enumerate_configs(roll, opts=abi.gp_rollout_opts(9))
+    roll = sets[0]
+    cfgs = eng.enumerate_configs(roll, opts=abi.gp_rollout_opts(8))
+    caps = eng.rollout_capacities(roll)
+    states = 1
+    for c in caps:
+        states *= c + 1
+    if states <= 3_000_000:
+        B = float(p.workload.batch_rollouts * 3)
+        rc, res_o, ent_o = oracle_milp(orc, oracle_configs(orc, roll, max_stages=8), caps, B, p.workload.mean_len)
+        assert rc == 0
+        res, ent = eng.solve_milp(cfgs, caps, B, p.workload.mean_len)
+        assert res.makespan == res_o.makespan
+        assert [(e.config, e.replicas, e.workload) for e in ent] == \
+            [(e.config, e.replicas, e.workload) for e in ent_o]

@@ -52,3 +52,17 @@ def test_multi_device_context_schedule(key):
     g = golden("schedules.json").get(key)
     if g:
         assert plan2 == _strip(g["plan"])
+
+
+def test_native_schedule_c4_equals_c_restatement():
+    """C4 (256 GPUs, eta=2): the native driver's plan and trace == the C restatement's
+    schedule (oracle_sched.c over the table-memoised constrained_search, which is pinned to
+    the reference goldens; tests/golden/make_golden_c4_oracle.py) — an independent CPU
+    derivation of the whole C4 schedule, beside test_dropin's reference-driver comparison."""
+    from paper_2511_00796_b200.engine import Engine
+    g = golden("schedule_c4_oracle.json")["c4_256gpu/eta=2"]
+    with Engine(problem("c4_256gpu")) as eng:
+        plan, trace = eng.schedule(eta=2, seed=4276115)
+    want = {k: v for k, v in g.items() if k not in ("trace", "evaluated_partitions", "oracle_seconds")}
+    assert plan == want
+    assert trace == g["trace"]
