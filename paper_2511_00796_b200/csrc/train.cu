@@ -929,6 +929,23 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
 }
 
 constexpr int kK1Threads = 128;
+// K1-fast variant switches (A/B measurements with tools/build_variant.sh + k1_variants.sh);
+// the defaults are the product
+#ifndef GPV_GS
+#define GPV_GS 4     // lanes per promotion count in the per-prefix tables
+#endif
+#ifndef GPV_FC
+#define GPV_FC 0     // 1: 32-bit per-prefix feasible counter (measured +0.1 ms: off)
+#endif
+#ifndef GPV_NM
+#define GPV_NM 1     // 1: near-minimum test as one double compare against bits b0 + 2 (-0.27 ms)
+#endif
+#ifndef GPV_TR
+#define GPV_TR 1     // 1: suffix transfer terms added unconditionally (absent ones are exact zeros) (-0.9 ms)
+#endif
+#ifndef GPV_MERGE
+#define GPV_MERGE 1  // 1: zero-layer donors by the co-rank of the two donor sequences (no loop) (-0.4 ms)
+#endif
 constexpr int kZsTable = 128;  // > L on the fast path
 constexpr int kMaxLastBlocks = 1024;  // last type run blocks with a per-prefix rank count (else generic K1)
 
@@ -1080,8 +1097,8 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
   // slots per lane (slot q = lane % 4 + 4 j): the per-stage values are reduced across the group
   // (maxima of (total, compute), and the donor = the first slot with the most layers) for
   // d = 0..dm water-filling donations.
-  constexpr int GS = 4;
-  constexpr int SPL = NP >= GS ? NP / GS : 1;  // = R - 1 (R = 1 returned above)
+  constexpr int GS = GPV_GS;
+  constexpr int SPL = NP > 0 ? (NP + GS - 1) / GS : 1;  // outer slots per lane (R = 1 returned above)
   constexpr int GPW = 32 / GS;
   const int grp = lane / GS, ql = lane % GS;
   bool actv[SPL];
@@ -1311,6 +1328,9 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
   const int nsuf32 = sp.n_suf;
   long long b0 = kInfBits, k0 = LLONG_MAX, k1 = LLONG_MAX, k2 = LLONG_MAX, feasible = 0;
+#if GPV_NM
+  double xthr = __longlong_as_double(kInfBits);  // per-step times above bits b0 + 2 cannot matter
+#endif
   unsigned n_tab = 0;
   __shared__ Prefix<R> sP[kK1Threads / 32];
   __shared__ PrefixData<R> sD[kK1Threads / 32];
@@ -1355,6 +1375,9 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
       // table-scored count: every candidate of this lane, less the deferred ones (below)
       if (s0 + lane < s1) n_tab += (unsigned)((s1 - s0 - lane + 31) >> 5);
+#if GPV_FC
+      unsigned fc = 0;
+#endif
 #pragma unroll 2  // (with 6 CTAs/SM: two candidates in flight per lane, measured +10%)
       for (int s = (int)s0 + lane; s < (int)s1; s += 32) {  // (suffix indices fit 32 bits)
         const int4 A = __ldg(tb.sf_hot + s);  // fs, k|b1, rb01, rb23
@@ -1385,12 +1408,41 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
           if (nz > kDonations) slow = true;
           // zero-layer fix-up: each donation comes from the side holding the first maximum
           // (the prefix on ties: its stages come first); a donor must keep >= 1 layer
+#if GPV_MERGE
+          // the donors are the nz largest of the merge of the two non-increasing donor
+          // sequences (prefix first on ties): common cases "all from one side" first
+          if (nz > 0 && !slow) {
+            const signed char* __restrict__ msr = tb.sf_ms + s * kMsStride + b * (kDonations + 1);
+            const short* mpr = F.mp[a];
+            const int mpl = mpr[nz - 1], ms0 = __ldg(msr);
+            int last;
+            if (mpl >= ms0) {
+              dP = nz;
+              last = mpl;
+            } else {
+              const int msl = __ldg(msr + nz - 1), mp0 = mpr[0];
+              if (msl > mp0) {
+                dS = nz;
+                last = msl;
+              } else {
+#pragma unroll
+                for (int i = 1; i <= kDonations; ++i)
+                  if (i <= nz) dP += mpr[i - 1] >= __ldg(msr + nz - i) ? 1 : 0;
+                dS = nz - dP;
+                const int lp = dP > 0 ? mpr[dP - 1] : 127, ls = dS > 0 ? __ldg(msr + dS - 1) : 127;
+                last = lp < ls ? lp : ls;
+              }
+            }
+            if (last < 2) slow = true;
+          }
+#else
           for (int i = 0; i < nz && !slow; ++i) {
             const int mpv = F.mp[a][dP], msv = tb.sf_ms[s * kMsStride + b * (kDonations + 1) + dS];
             if ((mpv > msv ? mpv : msv) < 2) slow = true;
             if (mpv >= msv) ++dP;
             else ++dS;
           }
+#endif
         }
         if (slow) {
           const long long key = pbase + s;
@@ -1410,6 +1462,14 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
         }
         double tr = dtr;
         if (R > 1) tr += txs[(A.y >> 16) & 0xffff];
+#if GPV_TR
+        {  // internal transfers of the suffix, [s][4] (t0, t1, t2, 0): absent terms are 0.0
+          const double2 t01 = __ldg(reinterpret_cast<const double2*>(tb.sf_t) + 2 * s);
+          tr += t01.x;
+          tr += t01.y;
+          tr += __ldg(tb.sf_t + 4 * s + 2);
+        }
+#else
         if (fk > 1) {  // internal transfers of the suffix, [s][4] (t0, t1, t2, 0)
           const double2 t01 = __ldg(reinterpret_cast<const double2*>(tb.sf_t) + 2 * s);
           tr += t01.x;
@@ -1418,17 +1478,30 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
             if (fk > 3) tr += __ldg(tb.sf_t + 4 * s + 2);
           }
         }
+#endif
         const double x = mt + fd[S] * mc + tr;
         if (DUMP && pbase + s >= rg.dump_lo && pbase + s < rg.dump_hi) rg.dump[pbase + s - rg.dump_lo] = x;
+#if GPV_FC
+        ++fc;
+#else
         ++feasible;
+#endif
+#if GPV_NM
+        if (x <= xthr) {  // within two ulps of the smallest so far (the key is formed only here)
+          const long long d = __double_as_longlong(x) - b0;
+#else
         const long long d = __double_as_longlong(x) - b0;
         if (d < 3) {  // (the key is formed only here and on the deferred path)
+#endif
           const long long key = pbase + s;
           if (d < 0) {
             k2 = d == -1 ? k1 : d == -2 ? k0 : LLONG_MAX;
             k1 = d == -1 ? k0 : LLONG_MAX;
             k0 = key;
             b0 += d;
+#if GPV_NM
+            xthr = __longlong_as_double(b0 + 2);
+#endif
           } else if (d == 1) {
             k1 = min(k1, key);
           } else if (d == 2) {
@@ -1436,6 +1509,9 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
           }
         }
       }
+#if GPV_FC
+      feasible += fc;
+#endif
       __syncwarp();
       if (lane == 0 && p + 1 < p_end) prefix_advance<R>(sp, P);
     }
