@@ -119,7 +119,12 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- reference
-def ref_rate(p, sets, threads, window=WINDOW):
+def ref_threads():
+    """Host threads the --impl reference arm uses (one bounded set per thread per step)."""
+    return max(1, min(os.cpu_count() or 1, 32))
+
+
+def ref_rate(p, sets, threads, window=WINDOW, with_costs=False):
     import ctypes as C
 
     import numpy as np
@@ -130,15 +135,20 @@ def ref_rate(p, sets, threads, window=WINDOW):
     lib = ref.lib
     lib.ref_bench_constrained_search.argtypes = [C.c_void_p, C.POINTER(C.c_int32),
                                                  C.POINTER(C.c_int32), C.c_int, C.c_int, C.c_int,
-                                                 C.POINTER(C.c_double), C.POINTER(C.c_double)]
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                                 C.POINTER(C.c_double)]
     flat = np.ascontiguousarray(np.concatenate([np.asarray(s, dtype=np.int32) for s in sets]))
     lens = np.asarray([len(s) for s in sets], dtype=np.int32)
     secs, chk = C.c_double(), C.c_double()
+    costs = np.zeros(len(sets), dtype=np.float64)
     rc = lib.ref_bench_constrained_search(ref.h, flat.ctypes.data_as(C.POINTER(C.c_int32)),
                                           lens.ctypes.data_as(C.POINTER(C.c_int32)), len(sets),
-                                          window, threads, C.byref(secs), C.byref(chk))
+                                          window, threads, C.byref(secs), C.byref(chk),
+                                          costs.ctypes.data_as(C.POINTER(C.c_double)))
     if rc:
         raise RuntimeError(lib.ref_last_error().decode())
+    if with_costs:
+        return secs.value, costs.tolist()
     return secs.value
 
 
@@ -178,7 +188,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     p = problem()
-    threads = max(1, min(os.cpu_count() or 1, 32))
+    threads = ref_threads()
     sets = cpu_sample_sets(p, threads)
     from oracles import Oracle, ref_available
     orc = Oracle(p)
@@ -347,10 +357,160 @@ def run_b200(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(p)
+    if not args.no_units:
+        line["units"] = {"U1_same_workload": same_workload(local_rank, args.steps, args.warmup),
+                         "U2_milp": milp_rate(local_rank), "U3_partition": partition_rate(local_rank)}
     if not args.no_ttp:
         line["time_to_best_plan"] = time_to_best_plan(local_rank)
     print(json.dumps(line), flush=True)
     return 0
+
+
+def same_workload(device, steps, warmup):
+    """U1 like-for-like with the reference arm: the SAME bounded C5 train sets the
+    --impl reference arm scans on this host (one per host thread), through the public batched
+    entry point gp_constrained_search_batch (host buffers: one H2D, all sets in flight, one
+    D2H; memo off so every step scans), and the per-set costs checked against the
+    reference's own constrained_search on those sets."""
+    import torch
+
+    from paper_2511_00796_b200.engine import Engine
+    from oracles import Oracle, ref_available
+    p = problem()
+    sets = cpu_sample_sets(p, ref_threads())
+    layouts = sum(Oracle(p).train_space(s) for s in sets)
+    out = {"sets": len(sets), "layouts_per_step": layouts, "window": WINDOW,
+           "sample": f"{len(sets)} C5 train sets x 36,864 layouts (the --impl reference workload)"}
+    with Engine(p, device=device) as eng:
+        eng.set_memo(False)
+        secs = []
+        for i in range(warmup + steps):
+            torch.cuda.synchronize(device)
+            t = time.perf_counter()
+            res = eng.constrained_search_batch_raw(sets, WINDOW)
+            torch.cuda.synchronize(device)
+            if i >= warmup:
+                secs.append(time.perf_counter() - t)
+        launches = eng.launches
+    gpu_costs = [r.cost if r.found else -1.0 for r, _ in res]
+    out["b200_e2e"] = {"value": layouts / statistics.median(secs), "unit": UNIT,
+                       "ms_per_step": 1e3 * statistics.median(secs), "kernel_launches": launches}
+    if ref_available():
+        rsecs, rcosts = ref_rate(p, sets, ref_threads(), with_costs=True)
+        out["reference_cpu"] = {"value": layouts / rsecs, "unit": UNIT, "threads": ref_threads(),
+                                "seconds": rsecs}
+        out["speedup_e2e"] = out["b200_e2e"]["value"] / out["reference_cpu"]["value"]
+        out["costs_identical"] = gpu_costs == rcosts
+    return out
+
+
+def milp_rate(device):
+    """U2: MILP state x config relaxations/s of solve_milp (src/rollout_milp.cpp:115-142) on
+    a C5 rollout set with a 5e6-state capacity lattice (a fresh context: no cached lattice),
+    beside the reference's own solve_milp on a 1e6-state lattice on one host core. Work =
+    sum over configs c of the lattice states where c fits (one DADD + DSETP each)."""
+    import torch
+
+    from paper_2511_00796_b200.engine import Engine
+    from oracles import Ref, ref_available
+    p = problem()
+    cl = p.cluster
+
+    def rollout(per_type):
+        out = []
+        for t in range(len(cl.type_names)):
+            out += [d for d in range(cl.n) if cl.device_type[d] == t][:per_type]
+        return sorted(out)
+
+    def relax(cfgs, caps):
+        tot = 0
+        for c in cfgs:
+            v = [c["type_counts"][t] if isinstance(c, dict) else c.type_counts[t] for t in range(len(caps))]
+            prod = 1
+            for t, cap in enumerate(caps):
+                prod *= max(0, cap - v[t] + 1)
+            tot += prod
+        return tot
+
+    out = {}
+    roll = rollout(170)
+    B = float(p.workload.batch_rollouts * WINDOW)
+    secs = []
+    for _ in range(3):
+        with Engine(p, device=device) as eng:
+            cfgs = eng.enumerate_configs(roll)
+            caps = eng.rollout_capacities(roll)
+            eng.solve_milp(eng.enumerate_configs(rollout(20)), eng.rollout_capacities(rollout(20)), B,
+                           p.workload.mean_len)  # warm the context (another lattice)
+            torch.cuda.synchronize(device)
+            t = time.perf_counter()
+            res, _ = eng.solve_milp(cfgs, caps, B, p.workload.mean_len)
+            torch.cuda.synchronize(device)
+            secs.append(time.perf_counter() - t)
+    states = 1
+    for c in caps:
+        states *= c + 1
+    work = relax(cfgs, caps)
+    out["b200"] = {"value": work / min(secs), "unit": "relaxations/s", "lattice_states": states,
+                   "configs": len(cfgs), "relaxations": work, "seconds": min(secs),
+                   "makespan": res.makespan}
+    if ref_available():
+        ref = Ref(p)
+        small = rollout(100)
+        cfg = ref.enumerate_configs(small)
+        t = time.perf_counter()
+        ref.solve_milp(cfg["configs"], cfg["capacities"], B, p.workload.mean_len)
+        rs = time.perf_counter() - t
+        rstates = 1
+        for c in cfg["capacities"]:
+            rstates *= c + 1
+        rw = relax(cfg["configs"], cfg["capacities"])
+        out["reference_cpu"] = {"value": rw / rs, "unit": "relaxations/s", "lattice_states": rstates,
+                                "configs": len(cfg["configs"]), "seconds": rs, "threads": 1}
+        out["speedup"] = out["b200"]["value"] / out["reference_cpu"]["value"]
+    return out
+
+
+def partition_rate(device):
+    """U3: move/swap candidates examined per second by graph_partition_candidates
+    (src/partition.cpp:284-349, 16 restarts, top-8) at N = 1024 (band [0.45, 0.55]); the
+    work count comes from the C restatement's identical local search (or_partition_evals),
+    the result is checked against the reference's own call, timed on one host core."""
+    import torch
+
+    from paper_2511_00796_b200 import abi
+    from paper_2511_00796_b200.engine import Engine
+    from oracles import Oracle, Ref, oracle_partitions, ref_available
+    p = problem()
+    lo, hi, seed = 0.45, 0.55, 4276115
+    orc = Oracle(p)
+    orc.lib.or_partition_evals.restype = __import__("ctypes").c_int64
+    orc.lib.or_partition_evals(1)
+    want = oracle_partitions(orc, lo, hi, seed=seed)
+    evals = orc.lib.or_partition_evals(1)
+    o = abi.gp_part_opts(12, 16, seed, 1e-9, 0, 0)
+    with Engine(p, device=device) as eng:
+        eng.partition_candidates(0.2, 0.3, k=8, opts=o)  # unit tables, first launches
+        secs = []
+        for _ in range(3):
+            torch.cuda.synchronize(device)
+            t = time.perf_counter()
+            got = eng.partition_candidates(lo, hi, k=8, opts=o)
+            torch.cuda.synchronize(device)
+            secs.append(time.perf_counter() - t)
+    out = {"band": [lo, hi], "restarts": 16, "k": 8, "move_swap_evals": evals,
+           "b200": {"value": evals / min(secs), "unit": "move/swap gains/s", "seconds_per_call": min(secs)},
+           "matches_restatement": got == want}
+    if ref_available():
+        t = time.perf_counter()
+        r = Ref(p).partition_candidates(lo, hi, k=8, seed=seed)
+        rs = time.perf_counter() - t
+        out["reference_cpu"] = {"value": evals / rs, "unit": "move/swap gains/s", "seconds_per_call": rs,
+                                "threads": 1}
+        out["speedup"] = rs / min(secs)
+        out["matches_reference"] = got == [(c["train"], c["objective"], c["compute_fraction"])
+                                           for c in r["candidates"]]
+    return out
 
 
 def time_to_best_plan(device, keys=("c3_64gpu/eta=1", "c4_256gpu/eta=2", "c5_1024gpu/eta=2")):
@@ -397,6 +557,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttp", action="store_true", help="skip the time-to-best-plan runs")
+    ap.add_argument("--no-units", action="store_true",
+                    help="skip the same-workload / MILP / partition unit measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -213,6 +213,16 @@ int gp_constrained_search_range(gp_ctx* ctx, const int32_t* ids, int32_t n, int3
                                 const gp_train_opts* opts, int64_t lo, int64_t hi,
                                 gp_train_result* out, int32_t* stage_devices);
 
+/* Many constrained_search calls in one (the scheduler's evaluation batches, SURVEY 8f
+ * rank 1): set i is ids[off[i] .. off[i+1]) and its result goes to out[i] (its stage
+ * devices to stage_devices[off[i] ..]). All inputs travel in one H2D copy, every set's
+ * tables and scan are in flight together (small sets fused, one CTA each), results come
+ * back in one D2H copy; memoised like gp_constrained_search; split over the devices of a
+ * multi-device context by layout count. */
+int gp_constrained_search_batch(gp_ctx* ctx, int32_t n_sets, const int32_t* ids, const int32_t* off,
+                                int32_t window, const gp_train_opts* opts, gp_train_result* out,
+                                int32_t* stage_devices);
+
 /* Split form of gp_constrained_search_range for callers that overlap work or
  * time the device part alone (bench.py): prepare uploads the train set's
  * enumeration metadata (one H2D copy), launch enqueues the stage-table build

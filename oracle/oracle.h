@@ -58,6 +58,9 @@ int or_weight_sync_cost(const gp_cluster* c, const gp_workload* w, const gp_cali
 
 int or_partition_candidates(const gp_cluster* c, const gp_gamma* g, const gp_part_opts* opts,
                             int32_t k, gp_partition* out, int32_t* train_ids, int32_t* n_out);
+/* move/swap candidates examined by or_partition_candidates' local search since the last
+ * reset (the U3 work unit of SURVEY 8d) */
+int64_t or_partition_evals(int reset);
 int or_partition_objective(const gp_cluster* c, const int32_t* train, int32_t n_train,
                            double* objective, double* fraction);
 

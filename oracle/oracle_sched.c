@@ -325,6 +325,15 @@ static int cmp_score_desc_stable(const void* pa, const void* pb) {
 }
 
 /* local_search (src/partition.cpp:271-350) */
+/* move/swap candidates examined by local_search (the U3 work unit): per ascent
+ * step n moves + |train| * |rollout| swaps; test infrastructure, not thread-safe */
+static int64_t g_part_evals;
+int64_t or_partition_evals(int reset) {
+  const int64_t v = g_part_evals;
+  if (reset) g_part_evals = 0;
+  return v;
+}
+
 static void local_search(const units_t* u, band_t band, const gp_part_opts* o, topk_t* tk, int* buf) {
   int n = u->n;
   double* base = (double*)malloc(sizeof(double) * (size_t)n);
@@ -360,6 +369,7 @@ static void local_search(const units_t* u, band_t band, const gp_part_opts* o, t
     for (;;) {
       double cur = st_obj(&st);
       double best_gain = 1e-12;
+      g_part_evals += n + (int64_t)st.count * (n - st.count);
       int kind = -1, mi = 0, mj = 0;
       for (int i = 0; i < n; ++i) {
         int to_train = !st.in_train[i];

@@ -389,7 +389,8 @@ int ref_partition_objective(void* h, const int* train, int nt, double* objective
 // on train sets taken round-robin from `sets` (concatenated ids, set_len[i] each).
 // Returns wall seconds; layouts are counted by the caller.
 int ref_bench_constrained_search(void* h, const int* ids, const int* set_len, int n_sets,
-                                 int window, int threads, double* seconds, double* checksum) {
+                                 int window, int threads, double* seconds, double* checksum,
+                                 double* costs_out) {
   return guarded([&] {
     auto* ctx = static_cast<RefCtx*>(h);
     std::vector<std::vector<int>> sets;
@@ -414,6 +415,8 @@ int ref_bench_constrained_search(void* h, const int* ids, const int* set_len, in
     double cs = 0;
     for (double c : costs) cs += c;
     *checksum = cs;
+    if (costs_out)
+      for (size_t i = 0; i < costs.size(); ++i) costs_out[i] = costs[i];
   });
 }
 

@@ -169,6 +169,8 @@ def declare(lib: C.CDLL, prefix: str) -> None:
             "debug_layout_costs": [vp, i32p, C.c_int32, P(gp_train_opts), C.c_int64, C.c_int64, C.c_int32,
                                    f64p, P(C.c_int32)],
             "train_shard_bounds": [vp, i32p, C.c_int32, P(gp_train_opts), C.c_int32, P(C.c_int64)],
+            "constrained_search_batch": [vp, C.c_int32, i32p, i32p, C.c_int32, P(gp_train_opts),
+                                         P(gp_train_result), i32p],
             "exhaustive_optimum": [vp, C.c_int32, P(gp_exhaustive_result), i32p],
             "simulate": [vp, P(gp_sim_plan), C.c_int32, C.c_int32, P(C.c_uint64), C.c_int32, P(gp_sim_report),
                          i32p, i32p],

@@ -26,6 +26,8 @@ int train_layout_costs(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_op
                        long long hi, int path, double* out, int* fast_used, int* inner);
 int train_shard_bounds(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, int n_shards,
                        int64_t* bounds);
+int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
+                const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices, int mode);
 void train_state_free(gp_ctx* ctx);
 void train_last_nm(gp_ctx* ctx, long long nm[4]);
 void train_nm_merge(long long a[4], const long long b[4]);
@@ -431,6 +433,26 @@ int gp_train_prepare(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return train_prepare(ctx, ids, n, o);
+}
+
+int gp_constrained_search_batch(gp_ctx* ctx, int32_t n_sets, const int32_t* ids, const int32_t* off,
+                                int32_t window, const gp_train_opts* o, gp_train_result* out,
+                                int32_t* stage_devices) {
+  if (!ctx || !ids || !off || !out || n_sets < 0) return set_error(GP_INVALID, "null argument");
+  const gp_train_opts def{4, 16};
+  if (!o) o = &def;
+  std::vector<const int32_t*> p(n_sets);
+  std::vector<int32_t> ns(n_sets);
+  std::vector<int32_t*> sd(n_sets);
+  for (int i = 0; i < n_sets; ++i) {
+    if (off[i + 1] < off[i]) return set_error(GP_INVALID, "set offsets must be non-decreasing");
+    p[i] = ids + off[i];
+    ns[i] = off[i + 1] - off[i];
+    if (ns[i] <= 0) return set_error(GP_INVALID, "constrained_search requires a non-empty train set");
+    sd[i] = stage_devices ? stage_devices + off[i] : nullptr;
+  }
+  cudaSetDevice(ctx->device);
+  return train_batch(ctx, n_sets, p.data(), ns.data(), window, o, out, stage_devices ? sd.data() : nullptr, 0);
 }
 
 int gp_train_launch(gp_ctx* ctx, int32_t window, int64_t lo, int64_t hi) {

@@ -170,6 +170,22 @@ class Engine:
         _check(rc)
         return res, devs
 
+    def constrained_search_batch_raw(self, train_sets, window: int, opts=None):
+        """Many constrained_search calls in one (gp_constrained_search_batch): returns
+        [(gp_train_result, stage devices array)] in input order."""
+        off = np.zeros(len(train_sets) + 1, dtype=np.int32)
+        for i, t in enumerate(train_sets):
+            off[i + 1] = off[i] + len(t)
+        ids = np.ascontiguousarray(np.concatenate([np.asarray(t, dtype=np.int32) for t in train_sets])
+                                   if train_sets else np.zeros(1, dtype=np.int32))
+        res = (abi.gp_train_result * max(len(train_sets), 1))()
+        devs = np.zeros(max(int(off[-1]), 1), dtype=np.int32)
+        _check(lib().gp_constrained_search_batch(self._h, len(train_sets), ids.ctypes.data_as(abi.i32p),
+                                                 off.ctypes.data_as(abi.i32p), window,
+                                                 C.byref(opts or abi.default_train_opts()), res,
+                                                 devs.ctypes.data_as(abi.i32p)))
+        return [(res[i], devs[off[i]:off[i + 1]]) for i in range(len(train_sets))]
+
     def constrained_search(self, train_set, window: int, opts=None, lo: int = 0, hi: int = -1):
         """constrained_search (inc/train_search.hpp:29-33); None == std::nullopt."""
         res, devs = self.constrained_search_raw(train_set, window, opts, lo, hi)
