@@ -212,9 +212,11 @@ struct SState {
   int n_tr, n_ro;
 };
 
+// One CTA per (band, restart): blockIdx.x = band * restarts + r (a scheduler iteration's
+// bands run in one launch); band b's limits are bands[b] = (lo, hi).
 __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* __restrict__ tot,
                                                          const double* __restrict__ base_score,
-                                                         double lo, double hi, int restarts,
+                                                         const double2* __restrict__ bands, int restarts,
                                                          unsigned long long seed,
                                                          unsigned char* __restrict__ in_train_out,
                                                          RestartOut* __restrict__ out) {
@@ -232,7 +234,8 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
   __shared__ SState S;
   __shared__ Cand red[32];
   __shared__ int ired[32];
-  const int r = blockIdx.x;
+  const int r = blockIdx.x % restarts;
+  const double lo = bands[blockIdx.x / restarts].x, hi = bands[blockIdx.x / restarts].y;
   const Totals T = *tot;
   const int tid = threadIdx.x, nth = blockDim.x;
 
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
     }
   }
   __syncthreads();
-  for (int i = tid; i < n; i += nth) in_train_out[(size_t)r * n + i] = ok ? in_tr[i] : 0;
+  for (int i = tid; i < n; i += nth) in_train_out[(size_t)blockIdx.x * n + i] = ok ? in_tr[i] : 0;
   if (tid == 0) {
     RestartOut o;
     o.ok = ok;
@@ -457,7 +460,7 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
     o.steps = steps;
     o.obj = (T.link > 0 ? div_rn_recip2(S.link_train, T.link, T.y_link) : 0) +
             div_rn_recip2(T.hbm - S.hbm_train, T.hbm, T.y_hbm);
-    out[r] = o;
+    out[blockIdx.x] = o;
   }
 }
 
@@ -696,10 +699,20 @@ void part_cache_free(gp_ctx* ctx) {
   }
 }
 
-int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, int k, gp_partition* out,
-                         int32_t* train_ids, int32_t* n_out) {
-  *n_out = 0;
+// graph_partition_candidates (src/partition.cpp:369-406) for q bands in one go (the
+// scheduler's iteration-1 probes): unit tables once per context, the restarts of every band
+// in ONE k5_restart launch (q x restarts CTAs), the per-band offer / top-k kernels queued
+// back to back, one synchronisation and one D2H for all bands. Band i's candidates go to
+// out[i * k ..] with their train ids at train_ids[i * k * N ..]; rcs[i] = GP_OK or
+// GP_BAND_INFEASIBLE.
+int partition_candidates_batch(gp_ctx* ctx, int q, const gp_gamma* gs, const gp_part_opts* o, int k,
+                               gp_partition* out, int32_t* train_ids, int32_t* n_out, int* rcs) {
   const int N = ctx->N, M = ctx->M;
+  for (int i = 0; i < q; ++i) {
+    n_out[i] = 0;
+    rcs[i] = GP_OK;
+  }
+  if (q <= 0) return GP_OK;
   if (N < 2) return set_error(GP_INVALID, "graph_partition requires at least two devices");
   if (k < 1 || k > 64) return set_error(GP_INVALID, "k must lie in [1, 64]");
   if (o->restarts < 0) return set_error(GP_INVALID, "restarts must be >= 0");
@@ -722,7 +735,6 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
   mem_off.push_back((int)mem_ids.size());
   const int n = (int)mem_off.size() - 1;
   if (n > kMaxUnits) return set_error(GP_INVALID, "too many partition units for the sm_100a kernel");
-  const double lo = g->gamma_l - o->band_epsilon, hi = g->gamma_h + o->band_epsilon;
   const bool exact = !o->force_local_search && n <= o->exact_threshold && n <= 20;
   const int n_offers = exact ? (int)((1ull << n) - 2) : o->restarts;
   // ---- unit tables: built once per (context, granularity) — they depend only on the cluster
@@ -738,15 +750,15 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
     uadd(sizeof(double) * (size_t)n * n);
     uadd(sizeof(Totals));
     GP_CUDA(cudaMalloc(&pc->buf, ub));
-    char* q = static_cast<char*>(pc->buf);
-    pc->off = carve3<int>(q, n + 1);
-    pc->ids = carve3<int>(q, N);
-    pc->uf = carve3<double>(q, n);
-    pc->uh = carve3<double>(q, n);
-    pc->ui = carve3<double>(q, n);
-    pc->base = carve3<double>(q, n);
-    pc->cross = carve3<double>(q, (size_t)n * n);
-    pc->tot = carve3<Totals>(q, 1);
+    char* qp = static_cast<char*>(pc->buf);
+    pc->off = carve3<int>(qp, n + 1);
+    pc->ids = carve3<int>(qp, N);
+    pc->uf = carve3<double>(qp, n);
+    pc->uh = carve3<double>(qp, n);
+    pc->ui = carve3<double>(qp, n);
+    pc->base = carve3<double>(qp, n);
+    pc->cross = carve3<double>(qp, (size_t)n * n);
+    pc->tot = carve3<Totals>(qp, 1);
     const size_t in_bytes = (size_t)((char*)(pc->ids + N) - (char*)pc->off);
     char* hp0 = static_cast<char*>(ctx_pinned(ctx, in_bytes + 64));
     if (!hp0) return GP_CUDA_ERROR;
@@ -765,92 +777,119 @@ int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, 
   const Units u{n, pc->uf, pc->uh, pc->ui, pc->cross, pc->off, pc->ids};
   Totals* d_tot = pc->tot;
   double* d_base = pc->base;
-  // ---- per-call buffers
+  // ---- per-call buffers (q bands)
+  const int no1 = std::max(n_offers, 1);
+  // per-band result record: TopKOut, train ids, fractions (8-byte aligned), padded to 256 B
+  const size_t ids_end = sizeof(TopKOut) + sizeof(int) * (size_t)N * k;
+  const size_t frac_off = (ids_end + 7) & ~size_t(7);
+  const size_t out_band = (frac_off + sizeof(double) * k + 255) & ~size_t(255);
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
-  add(sizeof(Offer) * std::max(n_offers, 1));
-  add(sizeof(RestartOut) * std::max(o->restarts, 1));
-  add((size_t)std::max(n_offers, 1) * n);
-  add(sizeof(double) * std::max(n_offers, 1));
-  add(sizeof(int) * std::max(n_offers, 1));
-  add(sizeof(int) * (size_t)std::max(n_offers, 1) * N);  // train id lists per offer
-  add(sizeof(int) * (size_t)std::max(n_offers, 1));      // counts
-  add(sizeof(int) * (size_t)std::max(n_offers, 1) * M);  // footprints
-  add(sizeof(TopKOut));
-  add(sizeof(int) * (size_t)N * k);
-  add(sizeof(double) * k);
+  add(sizeof(double2) * q);
+  add(sizeof(Offer) * no1);
+  add(sizeof(RestartOut) * (size_t)q * std::max(o->restarts, 1));
+  add((size_t)q * no1 * n);
+  add(sizeof(double) * (size_t)q * no1);
+  add(sizeof(int) * (size_t)q * no1);
+  add(sizeof(int) * (size_t)q * no1 * N);  // train id lists per offer
+  add(sizeof(int) * (size_t)q * no1);      // counts
+  add(sizeof(int) * (size_t)q * no1 * M);  // footprints
+  add(out_band * q);                        // per band: TopKOut, train ids, fractions
   char* base = static_cast<char*>(ctx_scratch(ctx, bytes, kArenaPartition));
   if (!base) return GP_CUDA_ERROR;
   char* p = base;
-  Offer* d_offer = carve3<Offer>(p, std::max(n_offers, 1));
-  RestartOut* d_rout = carve3<RestartOut>(p, std::max(o->restarts, 1));
-  unsigned char* d_mask = carve3<unsigned char>(p, (size_t)std::max(n_offers, 1) * n);
-  double* d_objs = carve3<double>(p, std::max(n_offers, 1));
-  int* d_valid = carve3<int>(p, std::max(n_offers, 1));
-  int* d_lists = carve3<int>(p, (size_t)std::max(n_offers, 1) * N);
-  int* d_counts = carve3<int>(p, (size_t)std::max(n_offers, 1));
-  int* d_foot = carve3<int>(p, (size_t)std::max(n_offers, 1) * M);
-  TopKOut* d_tk = carve3<TopKOut>(p, 1);
-  int* d_tids = carve3<int>(p, (size_t)N * k);
-  double* d_frac = carve3<double>(p, k);
-  char* hp = static_cast<char*>(ctx_pinned(ctx, sizeof(TopKOut) + sizeof(int) * (size_t)N * k + sizeof(double) * k + 1024));
+  double2* d_bands = carve3<double2>(p, q);
+  Offer* d_offer = carve3<Offer>(p, no1);
+  RestartOut* d_rout = carve3<RestartOut>(p, (size_t)q * std::max(o->restarts, 1));
+  unsigned char* d_mask = carve3<unsigned char>(p, (size_t)q * no1 * n);
+  double* d_objs = carve3<double>(p, (size_t)q * no1);
+  int* d_valid = carve3<int>(p, (size_t)q * no1);
+  int* d_lists = carve3<int>(p, (size_t)q * no1 * N);
+  int* d_counts = carve3<int>(p, (size_t)q * no1);
+  int* d_foot = carve3<int>(p, (size_t)q * no1 * M);
+  char* d_res = carve3<char>(p, out_band * q);
+  const size_t mask_bytes = exact ? (size_t)no1 * n : 0;
+  const size_t hb_off = (std::max(out_band * q, mask_bytes) + 255) & ~size_t(255);
+  char* hp = static_cast<char*>(ctx_pinned(ctx, hb_off + sizeof(double2) * q + 1024));
   if (!hp) return GP_CUDA_ERROR;
+  GP_CUDA(cudaStreamSynchronize(ctx->stream));  // (the pinned staging buffer is reused)
+  double2* hb = reinterpret_cast<double2*>(hp + hb_off);
+  for (int i = 0; i < q; ++i) hb[i] = make_double2(gs[i].gamma_l - o->band_epsilon, gs[i].gamma_h + o->band_epsilon);
+  GP_CUDA(cudaMemcpyAsync(d_bands, hb, sizeof(double2) * q, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (long long)(sizeof(double2) * q);
   if (exact) {
-    k5_exact<<<(n_offers + 255) / 256, 256, 0, ctx->stream>>>(u, d_tot, lo, hi, d_offer);
-    ctx->launches++;
+    // masks 1..2^n-2 ascending; the unit membership of mask m is its bit pattern (shared by
+    // every band: only the in-band test differs)
+    for (int m = 0; m < n_offers; ++m)
+      for (int i = 0; i < n; ++i) hp[(size_t)m * n + i] = (char)(((m + 1) >> i) & 1);
+    for (int b = 0; b < q; ++b)
+      GP_CUDA(cudaMemcpyAsync(d_mask + (size_t)b * no1 * n, hp, mask_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->h2d_bytes += (long long)(mask_bytes * q);
   } else if (o->restarts > 0) {
     const size_t sm = sizeof(double) * 5 * n + sizeof(int) * (3 * n + 2) + n + 64;
     if (sm > 227 * 1024) return set_error(GP_INVALID, "partition units exceed shared memory");
     GP_CUDA(cudaFuncSetAttribute(k5_restart, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k5_restart<<<o->restarts, kK5Threads, sm, ctx->stream>>>(u, d_tot, d_base, lo, hi, o->restarts,
-                                                            o->seed, d_mask, d_rout);
+    k5_restart<<<q * o->restarts, kK5Threads, sm, ctx->stream>>>(u, d_tot, d_base, d_bands, o->restarts, o->seed,
+                                                                d_mask, d_rout);
     ctx->launches++;
   }
   GP_CUDA(cudaGetLastError());
-  // offers -> (mask rows, objective, valid) in the reference's offer order
-  if (exact) {
-    // masks 1..2^n-2 ascending; the unit membership of mask m is its bit pattern
-    std::vector<unsigned char> masks((size_t)n_offers * n);
-    for (int m = 0; m < n_offers; ++m)
-      for (int i = 0; i < n; ++i) masks[(size_t)m * n + i] = ((m + 1) >> i) & 1;
-    // stage through pinned memory in slices (small: <= 4094 x 12)
-    char* hp2 = static_cast<char*>(ctx_pinned(ctx, std::max(masks.size(), sizeof(TopKOut) + sizeof(int) * (size_t)N * k + sizeof(double) * k + 1024)));
-    if (!hp2) return GP_CUDA_ERROR;
-    GP_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::memcpy(hp2, masks.data(), masks.size());
-    GP_CUDA(cudaMemcpyAsync(d_mask, hp2, masks.size(), cudaMemcpyHostToDevice, ctx->stream));
-    ctx->h2d_bytes += (long long)masks.size();
+  for (int b = 0; b < q; ++b) {
+    const size_t ob = (size_t)b * no1;
+    char* rb = d_res + out_band * b;
+    TopKOut* d_tk = reinterpret_cast<TopKOut*>(rb);
+    int* d_tids = reinterpret_cast<int*>(rb + sizeof(TopKOut));
+    double* d_frac = reinterpret_cast<double*>(rb + frac_off);
+    if (exact) {
+      k5_exact<<<(n_offers + 255) / 256, 256, 0, ctx->stream>>>(u, d_tot, hb[b].x, hb[b].y, d_offer);
+      ctx->launches++;
+    }
+    k5_unpack_offers<<<(n_offers + 255) / 256, 256, 0, ctx->stream>>>(d_offer, d_rout + (size_t)b * o->restarts,
+                                                                      n_offers, exact, d_objs + ob, d_valid + ob);
+    k5_offer_lists<<<(n_offers + 7) / 8, 256, 0, ctx->stream>>>(u, d_mask + ob * n, d_valid + ob, n_offers,
+                                                                ctx->d_machine, M, N, d_lists + ob * N,
+                                                                d_counts + ob, d_foot + ob * M);
+    k5_topk<<<1, 32, 0, ctx->stream>>>(d_objs + ob, d_valid + ob, n_offers, k, M, N, d_lists + ob * N,
+                                       d_counts + ob, d_foot + ob * M, d_tk);
+    k5_emit<<<1, 1, 0, ctx->stream>>>(d_tk, d_lists + ob * N, N, ctx->d_flops, d_tids, d_frac);
+    ctx->launches += 4;
   }
-  k5_unpack_offers<<<(n_offers + 255) / 256, 256, 0, ctx->stream>>>(d_offer, d_rout, n_offers, exact, d_objs,
-                                                                    d_valid);
-  k5_offer_lists<<<(n_offers + 7) / 8, 256, 0, ctx->stream>>>(u, d_mask, d_valid, n_offers, ctx->d_machine, M, N,
-                                                              d_lists, d_counts, d_foot);
-  k5_topk<<<1, 32, 0, ctx->stream>>>(d_objs, d_valid, n_offers, k, M, N, d_lists, d_counts, d_foot, d_tk);
-  k5_emit<<<1, 1, 0, ctx->stream>>>(d_tk, d_lists, N, ctx->d_flops, d_tids, d_frac);
-  ctx->launches += 4;
   GP_CUDA(cudaGetLastError());
-  TopKOut* htk = reinterpret_cast<TopKOut*>(hp);
-  int* hids = reinterpret_cast<int*>(hp + sizeof(TopKOut));
-  double* hfrac = reinterpret_cast<double*>(hp + sizeof(TopKOut) + sizeof(int) * (size_t)N * k);
+  GP_CUDA(cudaMemcpyAsync(hp, d_res, out_band * q, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->d2h_bytes += (long long)(out_band * q);
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
-  GP_CUDA(cudaMemcpyAsync(htk, d_tk, sizeof(TopKOut), cudaMemcpyDeviceToHost, ctx->stream));
-  GP_CUDA(cudaMemcpyAsync(hids, d_tids, sizeof(int) * (size_t)N * k, cudaMemcpyDeviceToHost, ctx->stream));
-  GP_CUDA(cudaMemcpyAsync(hfrac, d_frac, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
-  ctx->d2h_bytes += (long long)(sizeof(TopKOut) + sizeof(int) * (size_t)N * k + sizeof(double) * k);
-  GP_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (htk->n_items == 0)
+  for (int b = 0; b < q; ++b) {
+    const char* rb = hp + out_band * b;
+    const TopKOut* htk = reinterpret_cast<const TopKOut*>(rb);
+    const int* hids = reinterpret_cast<const int*>(rb + sizeof(TopKOut));
+    const double* hfrac = reinterpret_cast<const double*>(rb + frac_off);
+    if (htk->n_items == 0) {
+      rcs[b] = GP_BAND_INFEASIBLE;
+      continue;
+    }
+    int off = 0;
+    for (int e = 0; e < htk->n_items; ++e) {
+      gp_partition& po = out[(size_t)b * k + e];
+      po.train_offset = off;
+      po.train_count = htk->item[e].count;
+      po.objective = htk->item[e].obj;
+      po.compute_fraction = hfrac[e];
+      std::memcpy(train_ids + (size_t)b * k * N + off, hids + off, sizeof(int32_t) * htk->item[e].count);
+      off += htk->item[e].count;
+    }
+    n_out[b] = htk->n_items;
+  }
+  return GP_OK;
+}
+
+int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, int k, gp_partition* out,
+                         int32_t* train_ids, int32_t* n_out) {
+  int rc_band = GP_OK;
+  const int rc = partition_candidates_batch(ctx, 1, g, o, k, out, train_ids, n_out, &rc_band);
+  if (rc) return rc;
+  if (rc_band)
     return set_error(GP_BAND_INFEASIBLE, "no bisection satisfies the compute-fraction band [" +
                                              std::to_string(g->gamma_l) + ", " + std::to_string(g->gamma_h) + "]");
-  int off = 0;
-  for (int e = 0; e < htk->n_items; ++e) {
-    out[e].train_offset = off;
-    out[e].train_count = htk->item[e].count;
-    out[e].objective = htk->item[e].obj;
-    out[e].compute_fraction = hfrac[e];
-    std::memcpy(train_ids + off, hids + off, sizeof(int32_t) * htk->item[e].count);
-    off += htk->item[e].count;
-  }
-  *n_out = htk->n_items;
   return GP_OK;
 }
 

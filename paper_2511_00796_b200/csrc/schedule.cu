@@ -35,6 +35,8 @@ int weight_sync_batch(gp_ctx* ctx, int q, const int32_t* const* train, const int
                       const int32_t* const* erep, const int32_t* ne, int window, double* out);
 int partition_candidates(gp_ctx* ctx, const gp_gamma* g, const gp_part_opts* o, int k, gp_partition* out,
                          int32_t* train_ids, int32_t* n_out);
+int partition_candidates_batch(gp_ctx* ctx, int q, const gp_gamma* gs, const gp_part_opts* o, int k,
+                               gp_partition* out, int32_t* train_ids, int32_t* n_out, int* rcs);
 
 namespace {
 
@@ -238,6 +240,53 @@ struct Driver {
 
   const Eval* get(const std::vector<int>& train) const { return memo.at(train).get(); }
 
+  // partition_with_widening for several gammas at once (iteration 1's probes): the
+  // unwidened bands of every gamma not yet cached in ONE batched partition call; a band that
+  // is infeasible continues with the sequential widening loop below (same result)
+  int widen_batch(const std::vector<Gamma>& gs, std::vector<std::vector<std::vector<int>>>& outs) {
+    outs.assign(gs.size(), {});
+    std::vector<int> todo;
+    for (size_t i = 0; i < gs.size(); ++i) {
+      auto it = part_cache.find(std::make_pair(gs[i].gl, gs[i].gh));
+      if (it != part_cache.end()) outs[i] = it->second;
+      else todo.push_back((int)i);
+    }
+    if (!todo.empty()) {
+      PhaseTimer pt(0);
+      const int k = std::max(1, o.candidate_width), q = (int)todo.size(), N = ctx->N;
+      gp_part_opts po{o.exact_threshold, o.restarts, o.seed, o.band_epsilon, o.force_local_search,
+                      o.machine_granularity};
+      std::vector<gp_gamma> gg(q);
+      for (int j = 0; j < q; ++j) {
+        const Gamma& g = gs[todo[j]];
+        gg[j] = gp_gamma{g.q, g.r, (0.0 < g.gl) ? g.gl : 0.0, (g.gh < 1.0) ? g.gh : 1.0};
+      }
+      std::vector<gp_partition> parts((size_t)q * k);
+      std::vector<int32_t> ids((size_t)q * k * N + 1);
+      std::vector<int32_t> nout(q);
+      std::vector<int> rcs(q);
+      int rc = partition_candidates_batch(ctx, q, gg.data(), &po, k, parts.data(), ids.data(), nout.data(),
+                                          rcs.data());
+      if (rc) return rc;
+      for (int j = 0; j < q; ++j) {
+        if (rcs[j] != GP_OK) continue;  // widened below
+        auto& res = outs[todo[j]];
+        const int32_t* idb = ids.data() + (size_t)j * k * N;
+        for (int e = 0; e < nout[j]; ++e) {
+          const gp_partition& pp = parts[(size_t)j * k + e];
+          res.emplace_back(idb + pp.train_offset, idb + pp.train_offset + pp.train_count);
+        }
+        part_cache[std::make_pair(gs[todo[j]].gl, gs[todo[j]].gh)] = res;
+      }
+    }
+    for (size_t i = 0; i < gs.size(); ++i)
+      if (outs[i].empty()) {
+        int rc = widen(gs[i], outs[i]);
+        if (rc) return rc;
+      }
+    return GP_OK;
+  }
+
   // partition_with_widening (src/scheduler.cpp:21-40) -> candidate train sets, best first
   int widen(const Gamma& g, std::vector<std::vector<int>>& out) {
     auto key = std::make_pair(g.gl, g.gh);
@@ -317,21 +366,28 @@ int run_two_phase(Driver& D, Run& run) {
       it = cached;
     } else {
       std::vector<std::vector<int>> cands;
-      int rc = D.widen(gamma, cands);
-      if (rc) return rc;
       std::vector<std::vector<std::vector<int>>> grid;
       std::vector<std::vector<int>> prefixes;
-      std::vector<std::vector<int>> batch = cands;
-      if (iter == 1) {
+      int rc;
+      if (iter == 1) {  // the main band and the grid probes: one batched partition call
+        std::vector<Gamma> gs{gamma};
         for (int p = 1; p <= o.grid_probes; ++p) {
           Gamma probe = gamma;
           probe.gl = probe.gh = static_cast<double>(p) / (o.grid_probes + 1);
-          std::vector<std::vector<int>> pc;
-          rc = D.widen(probe, pc);
-          if (rc) return rc;
-          batch.insert(batch.end(), pc.begin(), pc.end());
-          grid.push_back(std::move(pc));
+          gs.push_back(probe);
         }
+        std::vector<std::vector<std::vector<int>>> outs;
+        rc = D.widen_batch(gs, outs);
+        if (rc) return rc;
+        cands = std::move(outs[0]);
+        for (size_t i = 1; i < outs.size(); ++i) grid.push_back(std::move(outs[i]));
+      } else {
+        rc = D.widen(gamma, cands);
+        if (rc) return rc;
+      }
+      std::vector<std::vector<int>> batch = cands;
+      if (iter == 1) {
+        for (const auto& pc : grid) batch.insert(batch.end(), pc.begin(), pc.end());
         for (int lead = 0; lead < ctx->T; ++lead) {  // type-aligned prefix probes
           std::vector<int> order(N);
           for (int d = 0; d < N; ++d) order[d] = d;
