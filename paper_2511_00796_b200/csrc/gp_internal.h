@@ -4,12 +4,25 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
 #include "../../include/gplan.h"
 
 namespace gp {
+
+// A double updated from several host threads (GPLAN_PROFILE statistics: per-device threads of
+// the multi-GPU batches add to the same counters).
+struct AtomicD {
+  std::atomic<double> v{0.0};
+  void operator+=(double x) {
+    double cur = v.load(std::memory_order_relaxed);
+    while (!v.compare_exchange_weak(cur, cur + x, std::memory_order_relaxed)) {
+    }
+  }
+  operator double() const { return v.load(std::memory_order_relaxed); }
+};
 
 constexpr double kInf = 1e30;       // inc/common.hpp:41
 constexpr long long kSlowQueue = 1 << 21;  // deferred generic candidates per scan (overflow -> rescan)

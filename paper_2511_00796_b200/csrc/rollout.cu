@@ -25,7 +25,10 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <numeric>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "gp_internal.h"
@@ -623,18 +626,19 @@ struct MilpCache {
 };
 
 // GPLAN_PROFILE=1: lattice tables built / reused, states tabulated, DP and backtrack wall time
-struct MilpStats {
-  long long built = 0, reused = 0, states = 0, backtracks = 0, queries = 0, mallocs = 0;
-  double dp_s = 0, bt_s = 0, malloc_s = 0, prep_s = 0, kern_s = 0;
-  long long levels = 0, groups = 0;
+struct MilpStats {  // (updated from the per-device threads of milp_batch: atomics)
+  std::atomic<long long> built{0}, reused{0}, states{0}, backtracks{0}, queries{0}, mallocs{0};
+  AtomicD dp_s, bt_s, malloc_s, prep_s, kern_s;
+  std::atomic<long long> levels{0}, groups{0};
   ~MilpStats() {
     if (std::getenv("GPLAN_PROFILE"))
       std::fprintf(stderr,
                    "milp: %lld tables built (%lld states, %lld mallocs, %.3f s), %lld reused, %lld backtrack "
                    "launches for %lld queries (%.3f s); malloc %.3f s, level sort %.3f s, dp kernel %.3f s, "
                    "%lld levels, %lld groups\n",
-                   built, states, mallocs, dp_s, reused, backtracks, queries, bt_s, malloc_s, prep_s, kern_s,
-                   levels, groups);
+                   built.load(), states.load(), mallocs.load(), (double)dp_s, reused.load(), backtracks.load(),
+                   queries.load(), (double)bt_s, (double)malloc_s, (double)prep_s, (double)kern_s, levels.load(),
+                   groups.load());
   }
 } g_milp_stats;
 
@@ -860,11 +864,13 @@ static int plan_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, const
 static int run_pending(gp_ctx* ctx, const std::vector<MilpTable*>& pend) {
   if (pend.empty()) return GP_OK;
   const double t0 = now_s();
-  static int occ = 0;
-  if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_dp_multi, 256, 0);
-    occ = std::max(1, occ);
-  }
+  static std::once_flag occ_once;  // (run_pending is called from the per-device threads)
+  static int occ = 1;
+  std::call_once(occ_once, [] {
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k4_dp_multi, 256, 0);
+    occ = std::max(1, o);
+  });
   for (size_t c0 = 0; c0 < pend.size(); c0 += kDpMaxTables) {
     const int K = (int)std::min<size_t>(kDpMaxTables, pend.size() - c0);
     std::vector<DpTable> dt(K);
@@ -1023,9 +1029,9 @@ int solve_milp(gp_ctx* ctx, const gp_config* cfg, int nc, const int32_t* caps, i
 
 // Many MILPs (one scheduler evaluation batch). Results per query: GP_OK with a plan,
 // GP_INFEASIBLE (no configs / aggregate <= 0), or GP_INVALID (lattice > 5e7) in rcs[i].
-int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs, const int32_t* const* caps,
-               int dims, const double* Bs, double len, gp_rollout_result* outs, gp_rollout_entry* const* entries,
-               int* rcs) {
+static int milp_batch_one(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs,
+                          const int32_t* const* caps, int dims, const double* Bs, double len,
+                          gp_rollout_result* outs, gp_rollout_entry* const* entries, int* rcs) {
   // group queries with identical config lists
   std::vector<int> order(q);
   std::vector<std::vector<unsigned char>> sigs(q);
@@ -1242,6 +1248,68 @@ int weight_sync(gp_ctx* ctx, const int32_t* train, int nt, const int32_t* roll, 
   ctx->d2h_bytes += sizeof(double);
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
   *out = *ho;
+  return GP_OK;
+}
+
+}  // namespace gp
+
+namespace gp {
+
+// Many solve_milp instances (the scheduler's batches). On a multi-device context the queries
+// are split by configuration list — every list always goes to the same device, so its cached
+// lattice tables stay there across iterations — and the devices run their shares
+// concurrently (one host thread each); results land in the caller's arrays in query order.
+int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs, const int32_t* const* caps,
+               int dims, const double* Bs, double len, gp_rollout_result* outs, gp_rollout_entry* const* entries,
+               int* rcs) {
+  const int D = 1 + (int)ctx->peers.size();
+  if (D == 1 || q < 2) return milp_batch_one(ctx, q, cfgs, ncs, caps, dims, Bs, len, outs, entries, rcs);
+  std::vector<std::vector<int>> part(D);
+  for (int i = 0; i < q; ++i) {
+    const std::vector<unsigned char> sig = milp_sig(cfgs[i], ncs[i], dims);
+    unsigned long long h = 1469598103934665603ULL;  // FNV-1a of the configuration list
+    for (unsigned char c : sig) h = (h ^ c) * 1099511628211ULL;
+    part[h % D].push_back(i);
+  }
+  std::vector<int> rc_dev(D, GP_OK);
+  std::vector<std::string> err(D);
+  auto run = [&](int d) {
+    const std::vector<int>& pj = part[d];
+    if (pj.empty()) return;
+    gp_ctx* c = d == 0 ? ctx : ctx->peers[d - 1];
+    cudaSetDevice(c->device);
+    const int m = (int)pj.size();
+    std::vector<const gp_config*> cf(m);
+    std::vector<int> nc(m), rc(m);
+    std::vector<const int32_t*> cp(m);
+    std::vector<double> b(m);
+    std::vector<gp_rollout_result> o(m);
+    std::vector<gp_rollout_entry*> e(m);
+    for (int j = 0; j < m; ++j) {
+      cf[j] = cfgs[pj[j]];
+      nc[j] = ncs[pj[j]];
+      cp[j] = caps[pj[j]];
+      b[j] = Bs[pj[j]];
+      e[j] = entries[pj[j]];
+    }
+    rc_dev[d] = milp_batch_one(c, m, cf.data(), nc.data(), cp.data(), dims, b.data(), len, o.data(), e.data(),
+                               rc.data());
+    if (rc_dev[d]) {
+      err[d] = gp_last_error();
+      return;
+    }
+    for (int j = 0; j < m; ++j) {
+      outs[pj[j]] = o[j];
+      rcs[pj[j]] = rc[j];
+    }
+  };
+  std::vector<std::thread> th;
+  for (int d = 1; d < D; ++d) th.emplace_back(run, d);
+  run(0);
+  for (auto& t : th) t.join();
+  cudaSetDevice(ctx->device);
+  for (int d = 0; d < D; ++d)
+    if (rc_dev[d]) return set_error(rc_dev[d], err[d].empty() ? std::string("milp batch failed") : err[d]);
   return GP_OK;
 }
 

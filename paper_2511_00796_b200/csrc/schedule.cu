@@ -41,12 +41,12 @@ int partition_candidates_batch(gp_ctx* ctx, int q, const gp_gamma* gs, const gp_
 namespace {
 
 // GPLAN_PROFILE=1: host wall time per driver phase (stderr)
-struct Phase {
-  double sec[6] = {};
+struct Phase {  // (contexts may be driven from several host threads: atomics)
+  AtomicD sec[6];
   ~Phase() {
     if (!std::getenv("GPLAN_PROFILE")) return;
     static const char* n[6] = {"partition", "train_batch", "configs_batch", "milp_batch", "weight_sync", "host"};
-    for (int i = 0; i < 6; ++i) std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", n[i], sec[i]);
+    for (int i = 0; i < 6; ++i) std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", n[i], (double)sec[i]);
   }
 } g_phase;
 

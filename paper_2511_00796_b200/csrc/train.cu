@@ -2189,10 +2189,10 @@ struct PreparedTrain {
 };
 
 // GPLAN_PROFILE=1: memo hits / scanned sets / scanned layouts (stderr at exit)
-struct MemoStats {
-  long long hits = 0, scans = 0, layouts = 0;
-  double ph[5] = {0, 0, 0, 0, 0};  // train_batch_run: build, carve+upload, launch, wait, fill
-  unsigned long long fast_cnt[2] = {0, 0};
+struct MemoStats {  // (updated from the per-device threads of train_batch: atomics)
+  std::atomic<long long> hits{0}, scans{0}, layouts{0};
+  AtomicD ph[5];  // train_batch_run: build, carve+upload, launch, wait, fill
+  std::atomic<unsigned long long> fast_cnt[2] = {{0}, {0}};
   void poll() {  // after a synchronisation
     if (!std::getenv("GPLAN_PROFILE")) return;
     unsigned long long c[2] = {0, 0};
@@ -2202,12 +2202,13 @@ struct MemoStats {
   }
   ~MemoStats() {
     if (std::getenv("GPLAN_PROFILE"))
-      std::fprintf(stderr, "k1 fast: %llu candidates from tables, %llu by the generic fallback\n", fast_cnt[0],
-                   fast_cnt[1]);
+      std::fprintf(stderr, "k1 fast: %llu candidates from tables, %llu by the generic fallback\n",
+                   fast_cnt[0].load(), fast_cnt[1].load());
     if (std::getenv("GPLAN_PROFILE"))
       std::fprintf(stderr, "train memo: %lld hits, %lld scanned sets, %lld scanned layouts; batch phases: "
-                   "build %.3f s, carve+upload %.3f s, launch %.3f s, wait %.3f s, fill %.3f s\n", hits, scans,
-                   layouts, ph[0], ph[1], ph[2], ph[3], ph[4]);
+                   "build %.3f s, carve+upload %.3f s, launch %.3f s, wait %.3f s, fill %.3f s\n", hits.load(),
+                   scans.load(), layouts.load(), (double)ph[0], (double)ph[1], (double)ph[2], (double)ph[3],
+                   (double)ph[4]);
   }
 } g_memo_stats;
 
@@ -2346,31 +2347,6 @@ static TrainTables prepared_tables(const gp_ctx* ctx, const PreparedTrain& P) {
   tb.nzs_max = P.d_nzs_max;
   for (int r = 0; r < P.h.sp.R; ++r) tb.pos_off[r] = P.h.pos_off[r];
   return tb;
-}
-
-// Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
-// Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
-// K1-fast can use a view with run r innermost (its per-prefix rank counts / junction rows fit)
-static bool inner_fits(const TrainSpace& sp, int r) {
-  const int e = sp.nc[r] + 2;
-  return e * (e - 1) / 2 <= kMaxLastBlocks && e <= kMaxJunction;
-}
-
-// rank == total, or the first layout of some choice of run 0 (every later run at its first
-// choice): ranges between such ranks hold the same layouts in the reference order and in a
-// fast view whose outer enumeration starts with run 0 (the layout count below a run-0 choice
-// does not depend on the order of the later runs), so such ranges can be scanned with it.
-static bool run0_aligned(const TrainSpace& sp, long long rank) {
-  const long long total = sp.max_stages >= sp.R ? sp.cnt[0][0] : 0;
-  if (rank <= 0 || rank >= total) return true;
-  const int rem_runs = sp.R - 1;
-  for (int k = 1; k <= sp.kmax[0]; ++k) {
-    if (k + rem_runs > sp.max_stages) break;
-    const long long c = binom_small(sp.nc[0], k - 1), sub = sp.cnt[1][k];
-    if (rank < c * sub) return rank % sub == 0;
-    rank -= c * sub;
-  }
-  return false;
 }
 
 // Enqueues K2 + K1 + finalize for P over ranks [lo, hi) on `stream` (asynchronous).
