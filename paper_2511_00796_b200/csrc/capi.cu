@@ -388,6 +388,7 @@ static int search_fanout(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t win
 
 int gp_constrained_search(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
                           const gp_train_opts* o, gp_train_result* out, int32_t* stage_devices) {
+  NvtxRange nvtx("gp_constrained_search");
   if (!ctx) return set_error(GP_INVALID, "null context");
   std::string key;
   if (ids && o && n > 0) {
@@ -403,6 +404,7 @@ int gp_constrained_search(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t wi
 int gp_constrained_search_range(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t window,
                                 const gp_train_opts* o, int64_t lo, int64_t hi,
                                 gp_train_result* out, int32_t* stage_devices) {
+  NvtxRange nvtx("gp_constrained_search_range");
   if (!ctx) return set_error(GP_INVALID, "null context");
   long long nm[4];  // explicit ranges are never memoised: every call scans its range
   return search_fanout(ctx, ids, n, window, o, lo, hi, out, stage_devices, nm);
@@ -430,6 +432,7 @@ int gp_ctx_create_multi(const gp_cluster* c, const gp_workload* w, const gp_cali
 }
 
 int gp_train_prepare(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* o) {
+  NvtxRange nvtx("gp_train_prepare");
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return train_prepare(ctx, ids, n, o);
@@ -438,6 +441,7 @@ int gp_train_prepare(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_
 int gp_constrained_search_batch(gp_ctx* ctx, int32_t n_sets, const int32_t* ids, const int32_t* off,
                                 int32_t window, const gp_train_opts* o, gp_train_result* out,
                                 int32_t* stage_devices) {
+  NvtxRange nvtx("gp_constrained_search_batch");
   if (!ctx || !ids || !off || !out || n_sets < 0) return set_error(GP_INVALID, "null argument");
   const gp_train_opts def{4, 16};
   if (!o) o = &def;
@@ -456,12 +460,14 @@ int gp_constrained_search_batch(gp_ctx* ctx, int32_t n_sets, const int32_t* ids,
 }
 
 int gp_train_launch(gp_ctx* ctx, int32_t window, int64_t lo, int64_t hi) {
+  NvtxRange nvtx("gp_train_launch");
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return train_launch(ctx, window, lo, hi);
 }
 
 int gp_train_collect(gp_ctx* ctx, gp_train_result* out, int32_t* stage_devices) {
+  NvtxRange nvtx("gp_train_collect");
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return train_collect(ctx, out, stage_devices);
@@ -487,6 +493,7 @@ int gp_train_shard_bounds(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_t
 
 int gp_enumerate_configs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_rollout_opts* o,
                          gp_config* out, int32_t cap, int32_t* n_out) {
+  NvtxRange nvtx("gp_enumerate_configs");
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return rollout_configs(ctx, ids, n, o, out, cap, n_out);
@@ -500,6 +507,7 @@ int gp_rollout_capacities(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t* c
 int gp_solve_milp(gp_ctx* ctx, const gp_config* configs, int32_t n_configs, const int32_t* caps,
                   int32_t dims, double total_rollouts, double mean_len, gp_rollout_result* out,
                   gp_rollout_entry* entries) {
+  NvtxRange nvtx("gp_solve_milp");
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return solve_milp(ctx, configs, n_configs, caps, dims, total_rollouts, mean_len, out, entries);
@@ -508,6 +516,7 @@ int gp_solve_milp(gp_ctx* ctx, const gp_config* configs, int32_t n_configs, cons
 int gp_solve_milp_batch(gp_ctx* ctx, int32_t q, const gp_config* configs, const int32_t* cfg_off,
                         const int32_t* caps, int32_t dims, const double* total_rollouts, double mean_len,
                         gp_rollout_result* out, gp_rollout_entry* entries, int32_t* status) {
+  NvtxRange nvtx("gp_solve_milp_batch");
   if (!ctx) return set_error(GP_INVALID, "null context");
   if (q < 0 || (q > 0 && (!configs || !cfg_off || !caps || !total_rollouts || !out || !entries || !status)))
     return set_error(GP_INVALID, "null argument");
@@ -532,6 +541,7 @@ int gp_solve_milp_batch(gp_ctx* ctx, int32_t q, const gp_config* configs, const 
 int gp_weight_sync_cost(gp_ctx* ctx, const int32_t* train, int32_t n_train, const int32_t* rollout,
                         int32_t n_rollout, const int32_t* entry_types, const int32_t* entry_replicas,
                         int32_t n_entries, int32_t window, double* out) {
+  NvtxRange nvtx("gp_weight_sync_cost");
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return weight_sync(ctx, train, n_train, rollout, n_rollout, entry_types, entry_replicas, n_entries,
@@ -540,6 +550,7 @@ int gp_weight_sync_cost(gp_ctx* ctx, const int32_t* train, int32_t n_train, cons
 
 int gp_partition_candidates(gp_ctx* ctx, const gp_gamma* gamma, const gp_part_opts* opts, int32_t k,
                             gp_partition* out, int32_t* train_ids, int32_t* n_out) {
+  NvtxRange nvtx("gp_partition_candidates");
   if (!ctx) return set_error(GP_INVALID, "null context");
   cudaSetDevice(ctx->device);
   return partition_candidates(ctx, gamma, opts, k, out, train_ids, n_out);

@@ -2,7 +2,9 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <atomic>
 #include <string>
@@ -22,6 +24,33 @@ struct AtomicD {
     }
   }
   operator double() const { return v.load(std::memory_order_relaxed); }
+};
+
+// Debug builds (-DGP_DEBUG_CHECKS, tools/build_variant.sh checks): bounds / invariant checks
+// inside the kernels; a failing check prints its location and traps. (compute-sanitizer is
+// not available on the GPU pool this engine was developed on.)
+#ifdef GP_DEBUG_CHECKS
+#define GP_CHECK(cond)                                                                          \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("GP_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                                \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define GP_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
+// NVTX range for the lifetime of a scope (header-only NVTX 3: free unless a tool such as
+// Nsight Systems / ncu --nvtx is attached). Marks the driver phases and the C ABI calls.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 constexpr double kInf = 1e30;       // inc/common.hpp:41

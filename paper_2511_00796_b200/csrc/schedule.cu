@@ -53,7 +53,13 @@ struct Phase {  // (contexts may be driven from several host threads: atomics)
 struct PhaseTimer {
   int id;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  explicit PhaseTimer(int i) : id(i) {}
+  NvtxRange nvtx;
+  static const char* name(int i) {
+    static const char* n[6] = {"gp_schedule/partition", "gp_schedule/train_batch", "gp_schedule/configs_batch",
+                               "gp_schedule/milp_batch", "gp_schedule/weight_sync", "gp_schedule/host"};
+    return n[i];
+  }
+  explicit PhaseTimer(int i) : id(i), nvtx(name(i)) {}
   ~PhaseTimer() {
     g_phase.sec[id] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
@@ -462,6 +468,7 @@ int run_two_phase(Driver& D, Run& run) {
 int schedule(gp_ctx* ctx, const gp_sched_opts* o, gp_schedule_result* res, int32_t* train_ids,
              int32_t* rollout_ids, int32_t* stage_devices, gp_config* entry_configs, gp_rollout_entry* entries,
              int32_t entry_cap, double* trace) {
+  NvtxRange nvtx("gp_schedule");
   std::memset(res, 0, sizeof *res);
   if (ctx->N < 2) return set_error(GP_INFEASIBLE, "scheduling requires at least two devices");
   const int eta = o->eta_override >= 0 ? o->eta_override : ctx->work.staleness;
@@ -476,6 +483,7 @@ int schedule(gp_ctx* ctx, const gp_sched_opts* o, gp_schedule_result* res, int32
   std::map<std::pair<double, double>, std::vector<std::vector<int>>> parts;  // survives passes
   long long evaluated = 0, layouts = 0;
   while (true) {
+    NvtxRange pass_range("gp_schedule/window_pass");
     D = std::make_unique<Driver>(ctx, *o);  // fresh memo per pass (src/scheduler.cpp:129)
     D->window = delta;
     D->part_cache = parts;

@@ -778,6 +778,7 @@ __device__ __forceinline__ bool eval_layout(const TrainSpace& sp, const TrainTab
   for (int q = 0; q < NS; ++q) {
     if (act[q]) {
       const int b = q < NP ? vbi(q) : e.bi[q - NP];
+      GP_CHECK(lay[q] >= 1 && lay[q] <= L && b >= 0);
       const double2 st = stage[(unsigned)(b * L + (lay[q] - 1))];
       asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %2, %0;\n\t@p mov.b64 %0, %2;\n\t"
           "setp.gt.f64 p, %3, %1;\n\t@p mov.b64 %1, %3;\n\t}"
@@ -967,6 +968,10 @@ struct PrefixFast {
   unsigned char nzp[NP + 1];  // zero-layer prefix stages at promotion a
   int fp;                     // sum of the prefix floors
   int bad;                    // bit a: a promoted prefix stage would exceed L layers
+#ifdef GP_DEBUG_CHECKS
+  int a_lo, a_hi;             // the tabulated promotion counts
+  int dm[NP + 1];             // the tabulated donations per promotion count
+#endif
 };
 
 // K1-fast shared memory per warp beside PrefixFast: the rank count of every last-run
@@ -1093,6 +1098,12 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
 #pragma unroll
   for (int q = 0; q < NP; ++q) fp_all += F.fl[q];
   const int a_lo = max(0, L - fp_all - fs_max - 4), a_hi = min(kp, L - fp_all - fs_min);
+#ifdef GP_DEBUG_CHECKS
+  if (lane == 0) {
+    F.a_lo = a_lo;
+    F.a_hi = a_hi;
+  }
+#endif
   // One group of GS = 4 lanes per promotion count a (eight per round), R - 1 prefix stage
   // slots per lane (slot q = lane % 4 + 4 j): the per-stage values are reduced across the group
   // (maxima of (total, compute), and the donor = the first slot with the most layers) for
@@ -1168,6 +1179,9 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
       }
     }
     if (ga && ql == 0) {
+#ifdef GP_DEBUG_CHECKS
+      F.dm[a] = dm;
+#endif
       F.nzp[a] = (unsigned char)nz;
       if (over) atomicOr(&F.bad, 1 << a);
     }
@@ -1392,6 +1406,8 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
             // b = #{j < fk : cntb[rb_j] + j < extra}, the four tests as one byte-wise
             // subtraction: byte j of (extra + 128) - (cntb[rb_j] + j + 1) keeps bit 7 iff the
             // test holds (both sides < 128, so no borrow crosses a byte)
+            GP_CHECK((A.z & 0xffff) < kMaxLastBlocks && ((unsigned)A.z >> 16) < kMaxLastBlocks &&
+                     (A.w & 0xffff) < kMaxLastBlocks && ((unsigned)A.w >> 16) < kMaxLastBlocks);
             const unsigned c0 = cntb[A.z & 0xffff], c1 = cntb[(unsigned)A.z >> 16];
             const unsigned c2 = cntb[A.w & 0xffff], c3 = cntb[(unsigned)A.w >> 16];
             const unsigned w = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410) +
@@ -1404,6 +1420,10 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
           a = extra - b;
           slow = ((pbad >> a) | (B.y >> (8 + b))) & 1;
           // byte b of the 40-bit zero-count word {B.y:B.x} (b <= 4): one PRMT
+#ifdef GP_DEBUG_CHECKS
+          GP_CHECK(b >= 0 && b <= 4 && b <= fk);
+          if (!slow) GP_CHECK(a >= F.a_lo && a <= F.a_hi);  // the candidate's promotion count was tabulated
+#endif
           const int nz = F.nzp[a] + (int)(__byte_perm((unsigned)B.x, (unsigned)B.y, (unsigned)b) & 0xff);
           if (nz > kDonations) slow = true;
           // zero-layer fix-up: each donation comes from the side holding the first maximum
@@ -1451,6 +1471,9 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
           --n_tab;
           continue;
         }
+#ifdef GP_DEBUG_CHECKS
+        GP_CHECK(dP >= 0 && dP <= F.dm[a] && dS >= 0 && dS <= kDonations && S <= GP_MAX_STAGES);
+#endif
         const double2 pa = F.pt[a][dP];
         const double2 sb = tb.sf_st[(b * (kDonations + 1) + dS) * nsuf32 + s];
         double mt = pa.x, mc = pa.y;
@@ -1461,6 +1484,7 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
           continue;
         }
         double tr = dtr;
+        GP_CHECK(((A.y >> 16) & 0xffff) < kMaxJunction);
         if (R > 1) tr += txs[(A.y >> 16) & 0xffff];
 #if GPV_TR
         {  // internal transfers of the suffix, [s][4] (t0, t1, t2, 0): absent terms are 0.0
