@@ -3,8 +3,8 @@
  * Drop-in boundary for the hot path of the rlsched reference scheduler
  * (arXiv 2511.00796, /root/reference/proj). The reference has no plugin
  * registry: its seam is the C++ free-function API that
- * `evaluate_partition` / `partition_with_widening` call
- * (src/scheduler.cpp:77-131). Each entry point below replaces exactly one of
+ * `partition_with_widening` / `evaluate_partition` call (src/scheduler.cpp:21-40,
+ * 42-75). Each entry point below replaces exactly one of
  * those functions; the C++ shim in paper_2511_00796_b200/shim/ re-exposes them
  * under the reference signatures so the reference scheduler.cpp links
  * unchanged.
@@ -189,10 +189,10 @@ int gp_abi_version(void);
 /* Kernel launches issued by this context so far (diagnostics / bench claim). */
 long long gp_ctx_launches(gp_ctx* ctx);
 
-/* ---- training side: replaces constrained_search (src/train_search.cpp:268-325) */
+/* ---- training side: replaces constrained_search (src/train_search.cpp:218-275) */
 
 /* Number of layouts constrained_search would enumerate for `ids`
- * (enumerate_block_lists, src/train_search.cpp:176-192), without materialising. */
+ * (enumerate_block_lists, src/train_search.cpp:126-142), without materialising. */
 int gp_train_space(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* opts,
                    int64_t* layouts);
 
@@ -255,18 +255,19 @@ int gp_fp64_peak(gp_ctx* ctx, double* dadd_per_s);
 int gp_debug_layout_costs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* opts,
                           int64_t lo, int64_t hi, int32_t path, double* per_step, int32_t* fast_used);
 /* Rank boundaries bounds[0..n_shards] splitting a train set's layout space into n_shards
- * contiguous ranges of balanced size for multi-GPU sharding (gp_constrained_search_range
- * per shard, winners merged by (cost, rank), feasible counts summed). Boundaries sit at
- * first layouts of the first type run's choices when that lets every shard keep the
- * engine's fastest scan order. */
+ * contiguous ranges of equal size for multi-GPU sharding (gp_constrained_search_range per
+ * shard, winners merged by (cost, rank), feasible counts summed). */
 int gp_train_shard_bounds(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_train_opts* opts,
                           int32_t n_shards, int64_t* bounds);
 
 /* ---- rollout side: replaces enumerate_configs / rollout_capacities / solve_milp
- *      (src/rollout_milp.cpp:113-254) ------------------------------------- */
+ *      (src/rollout_milp.cpp:30-171) ------------------------------------- */
 
+/* enumerate_configs (inc/rollout_milp.hpp:22-25, src/rollout_milp.cpp:39-89); out holds cap
+ * records; GP_CAPACITY with *n_out = the count needed when cap is too small. */
 int gp_enumerate_configs(gp_ctx* ctx, const int32_t* ids, int32_t n, const gp_rollout_opts* opts,
                          gp_config* out, int32_t cap, int32_t* n_out);
+/* rollout_capacities (inc/rollout_milp.hpp:28-29, src/rollout_milp.cpp:30-37). */
 int gp_rollout_capacities(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t* caps);
 /* Many solve_milp instances in one call (the scheduler's evaluation batches): query i has
  * configs[cfg_off[i] .. cfg_off[i+1]), caps[i*dims ..], total_rollouts[i]; results in
@@ -275,24 +276,28 @@ int gp_rollout_capacities(gp_ctx* ctx, const int32_t* ids, int32_t n, int32_t* c
 int gp_solve_milp_batch(gp_ctx* ctx, int32_t q, const gp_config* configs, const int32_t* cfg_off,
                         const int32_t* caps, int32_t dims, const double* total_rollouts, double mean_len,
                         gp_rollout_result* out, gp_rollout_entry* entries, int32_t* status);
-/* Exact makespan DP. entries must hold n_configs records. B <= 0 -> empty plan. */
+/* solve_milp (inc/rollout_milp.hpp:35-37, src/rollout_milp.cpp:91-171): the exact makespan
+ * DP. entries must hold n_configs records. B <= 0 -> empty plan. */
 int gp_solve_milp(gp_ctx* ctx, const gp_config* configs, int32_t n_configs, const int32_t* caps,
                   int32_t dims, double total_rollouts, double mean_len, gp_rollout_result* out,
                   gp_rollout_entry* entries);
 
-/* ---- weight sync: replaces weight_sync_cost (src/cost_model.cpp:255-277) ---- */
+/* ---- weight sync: replaces weight_sync_cost (inc/cost_model.hpp:63-65,
+ *      src/cost_model.cpp:174-196) ---------------------------------------------- */
 int gp_weight_sync_cost(gp_ctx* ctx, const int32_t* train, int32_t n_train, const int32_t* rollout,
                         int32_t n_rollout, const int32_t* entry_types,
                         const int32_t* entry_replicas, int32_t n_entries, int32_t window,
                         double* out);
 
-/* ---- repartition: replaces graph_partition_candidates (src/partition.cpp:426-463) */
+/* ---- repartition: replaces graph_partition_candidates (inc/partition.hpp:53-55,
+ *      src/partition.cpp:369-406) -------------------------------------------- */
 /* out holds up to k records; train_ids holds up to k * n_devices ints. */
 int gp_partition_candidates(gp_ctx* ctx, const gp_gamma* gamma, const gp_part_opts* opts,
                             int32_t k, gp_partition* out, int32_t* train_ids, int32_t* n_out);
+/* partition_objective (inc/partition.hpp:40-42, src/partition.cpp:354-358). */
 int gp_partition_objective(gp_ctx* ctx, const int32_t* train, int32_t n_train, double* objective,
                            double* fraction);
-/* compute_fraction (src/partition.cpp:360-367). */
+/* compute_fraction (src/partition.cpp:361-367). */
 int gp_compute_fraction(gp_ctx* ctx, const int32_t* train, int32_t n_train, double* fraction);
 
 /* ---- Algorithm-1 driver on the engine: schedule() (src/scheduler.cpp:259-292) ----- */

@@ -264,7 +264,7 @@ typedef struct {
   double* dump; /* optional: per_step of ranks [lo, hi) (+inf: no memory-feasible option) */
 } search_t;
 
-/* max_devices_per_machine (src/train_search.cpp:124-131). A block lies inside one
+/* max_devices_per_machine (src/train_search.cpp:74-81). A block lies inside one
  * type run of the canonical order, so equal machine ids are contiguous. */
 static int max_per_machine(const gp_cluster* c, const int32_t* dev, int n) {
   int best = 0, run = 0;
@@ -369,7 +369,7 @@ static void score_layout_product(search_t* st) {
   }
 }
 
-/* one layout: constrained_search loop body (src/train_search.cpp:277-322) */
+/* one layout: constrained_search loop body (src/train_search.cpp:227-273) */
 static void score_layout(search_t* st) {
   const gp_cluster* c = st->sp->c;
   const gp_workload* w = st->w;
@@ -518,7 +518,7 @@ int or_train_space(const gp_cluster* c, const gp_workload* w, const int32_t* ids
   return GP_OK;
 }
 
-/* constrained_search (src/train_search.cpp:268-325), restricted to ranks [lo, hi). */
+/* constrained_search (src/train_search.cpp:218-275), restricted to ranks [lo, hi). */
 static int constrained_search_impl(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
                                    const int32_t* ids, int32_t n, int32_t window,
                                    const gp_train_opts* opts, int64_t lo, int64_t hi,
@@ -635,7 +635,7 @@ int or_train_candidates_search(const gp_cluster* c, const gp_workload* w, const 
 /* ================================================================ rollout */
 
 int or_rollout_capacities(const gp_cluster* c, const int32_t* ids, int32_t n, int32_t* caps) {
-  /* src/rollout_milp.cpp:113-120 */
+  /* src/rollout_milp.cpp:30-37 */
   for (int t = 0; t < c->n_types; ++t) caps[t] = 0;
   for (int i = 0; i < n; ++i) {
     if (ids[i] < 0 || ids[i] >= c->n_devices) return fail(GP_INVALID, "unknown device id %d", ids[i]);
@@ -743,7 +743,7 @@ static int cmp_desc_int(const void* a, const void* b) {
   return (x < y) - (x > y);
 }
 
-/* enumerate_configs (src/rollout_milp.cpp:122-172) */
+/* enumerate_configs (src/rollout_milp.cpp:39-89) */
 int or_enumerate_configs(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
                          const int32_t* ids, int32_t n, const gp_rollout_opts* opts,
                          gp_config* out, int32_t cap, int32_t* n_out) {
@@ -785,7 +785,7 @@ int or_enumerate_configs(const gp_cluster* c, const gp_workload* w, const gp_cal
   return GP_OK;
 }
 
-/* solve_milp (src/rollout_milp.cpp:174-254) */
+/* solve_milp (src/rollout_milp.cpp:91-171) */
 int or_solve_milp(const gp_config* cfg, int32_t nc, const int32_t* caps, int32_t dims, double B,
                   double len, gp_rollout_result* out, gp_rollout_entry* entries) {
   memset(out, 0, sizeof *out);
@@ -863,7 +863,7 @@ int or_solve_milp(const gp_config* cfg, int32_t nc, const int32_t* caps, int32_t
   return GP_OK;
 }
 
-/* weight_sync_cost (src/cost_model.cpp:255-277) */
+/* weight_sync_cost (src/cost_model.cpp:174-196) */
 int or_weight_sync_cost(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
                         const int32_t* train, int32_t nt, const int32_t* roll, int32_t nr,
                         const int32_t* etype, const int32_t* erep, int32_t ne, int32_t window,

@@ -64,7 +64,7 @@ int64_t or_partition_evals(int reset);
 int or_partition_objective(const gp_cluster* c, const int32_t* train, int32_t n_train,
                            double* objective, double* fraction);
 
-/* Algorithm 1 driver: schedule() (src/scheduler.cpp:315-348). */
+/* Algorithm 1 driver: schedule() (src/scheduler.cpp:259-292). */
 typedef struct {
   int32_t eta_override;      /* < 0: use workload staleness */
   uint64_t seed;

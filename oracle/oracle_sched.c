@@ -415,7 +415,7 @@ static void local_search(const units_t* u, band_t band, const gp_part_opts* o, t
   free(order);
 }
 
-/* compute_fraction (src/partition.cpp:360-367) */
+/* compute_fraction (src/partition.cpp:361-367) */
 static double compute_fraction(const gp_cluster* c, const int* train, int nt) {
   double total = 0, tr = 0;
   for (int d = 0; d < c->n_devices; ++d) total += c->device_flops[d];

@@ -261,7 +261,7 @@ int exhaustive_optimum(gp_ctx* ctx, int window, gp_exhaustive_result* out, int32
       const int i = live[j];
       std::fill(key.begin(), key.end(), 0);
       key[T] = cfg_class[i];
-      for (int d : rl[i]) key[ctx->h_type[d]]++;  // rollout_capacities (src/rollout_milp.cpp:113-120)
+      for (int d : rl[i]) key[ctx->h_type[d]]++;  // rollout_capacities (src/rollout_milp.cpp:30-37)
       auto ins = job_index.emplace(key, (int)caps.size());
       job_of.push_back(ins.first->second);
       if (!ins.second) continue;

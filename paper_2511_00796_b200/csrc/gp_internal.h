@@ -83,7 +83,7 @@ struct BlockRec {
   int n;            // devices
   int type;
   int per_machine;  // max_devices_per_machine
-  double flops;     // sequential fold of device flops (src/train_search.cpp:279-282)
+  double flops;     // sequential fold of device flops (src/train_search.cpp:229-232)
   double lf_num;    // num_layers * flops (allocate_layers numerator)
   double cap_front; // hbm_capacity of devices.front()
   double beta_tp[4];  // min link within TP groups for tp = 1,2,4,8 (index 0 unused)

@@ -547,7 +547,7 @@ __device__ bool warp_equal(const int* a, const int* b, int n) {
   return true;
 }
 
-// Replays TopK::offer (src/partition.cpp:183-201) in offer order with one warp:
+// Replays TopK::offer (src/partition.cpp:184-201) in offer order with one warp:
 // merge into an equivalent entry (|dobj| <= 1e-12 and same footprint) keeping the
 // lexicographically smaller train set (no re-sort), else push_back + sort + trim.
 __global__ void k5_topk(const double* __restrict__ objs, const int* __restrict__ valid, int n_offers, int k,
@@ -603,7 +603,7 @@ __global__ void k5_topk(const double* __restrict__ objs, const int* __restrict__
   }
 }
 
-// compute_fraction (src/partition.cpp:360-367) for each result + its train ids
+// compute_fraction (src/partition.cpp:361-367) for each result + its train ids
 __global__ void k5_emit(const TopKOut* __restrict__ tk, const int* __restrict__ ids, int N,
                         const double* __restrict__ dflops, int* __restrict__ ids_out,
                         double* __restrict__ frac_out) {
@@ -659,7 +659,7 @@ __global__ void k5_objective(const int* __restrict__ train, int nt, const double
   }
 }
 
-// compute_fraction (src/partition.cpp:360-367): two sequential folds
+// compute_fraction (src/partition.cpp:361-367): two sequential folds
 __global__ void k5_fraction(const int* __restrict__ train, int nt, const double* __restrict__ dflops, int N,
                             double* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;

@@ -1,9 +1,9 @@
 // rollout.cu — sm_100a kernels for the rollout side of the hot path:
 //   K3  enumerate_configs + replica_concurrency/replica_rate_at
-//       (src/rollout_milp.cpp:122-172, src/cost_model.cpp:209-253)
+//       (src/rollout_milp.cpp:39-89, src/cost_model.cpp:128-172)
 //   K4  solve_milp: exact unbounded-knapsack DP over the type-capacity lattice
-//       (src/rollout_milp.cpp:174-254), level-synchronous wavefront
-//   K6  weight_sync_cost (src/cost_model.cpp:255-277)
+//       (src/rollout_milp.cpp:91-171), level-synchronous wavefront
+//   K6  weight_sync_cost (src/cost_model.cpp:174-196)
 //
 // K4 design. best[s] = max_c best[s - v_c] + h_c with strict '>' in config order
 // (first maximal config wins). Every config is type-pure and uses >= 1 device,
@@ -73,7 +73,7 @@ __global__ void k3_configs(const CfgCand* __restrict__ cands, int n_cands,
   for (int s = 0; s < S && ok; ++s) ok = c.tp[s] <= av[t * kAv + s];  // stage k on k-th largest machine
   int conc = 0;
   if (ok) {
-    // replica_concurrency (src/cost_model.cpp:209-229)
+    // replica_concurrency (src/cost_model.cpp:128-148)
     int best = sc.max_conc;
     for (int s = 0; s < S; ++s) {
       const int layers = sc.L / S + (s < sc.L % S ? 1 : 0);  // layers_for_stage
@@ -105,7 +105,7 @@ __global__ void k3_configs(const CfgCand* __restrict__ cands, int n_cands,
   }
   cfg.type_counts[t] = n;
   cfg.n_stages = S;
-  // replica_rate_at (src/cost_model.cpp:231-246): only type t contributes
+  // replica_rate_at (src/cost_model.cpp:150-165): only type t contributes
   double agg_bw = 0, agg_flops = 0;
   for (int u = 0; u < T; ++u) {
     if (cfg.type_counts[u] == 0) continue;
@@ -195,7 +195,7 @@ __global__ void k4_level_scatter(MilpDims d, const long long* __restrict__ off,
 
 // Lattice DP (k4_dp_multi below): one warp per state, lanes over the (type, devices)
 // groups: value = max_g best[s - delta_g] + hmax_g; choice = smallest config index c with
-// best[prev_g(c)] + h_c == value (src/rollout_milp.cpp:197-225). The lanes' partial
+// best[prev_g(c)] + h_c == value (src/rollout_milp.cpp:115-143). The lanes' partial
 // (max value, min index) pairs merge exactly in any order. A state at level l reads levels
 // <= l - n_min (n_min = fewest devices of any config), so `step` = n_min consecutive levels
 // form one phase between grid barriers.
@@ -302,7 +302,7 @@ struct MilpOut {
   int pad;
 };
 
-// Backtracking + plan assembly, one thread per query (src/rollout_milp.cpp:227-253).
+// Backtracking + plan assembly, one thread per query (src/rollout_milp.cpp:145-170).
 __global__ void k4_backtrack(MilpDims d, int q, const long long* __restrict__ full_idx,
                              const gp_config* __restrict__ cfg, int n_cfg, const double* __restrict__ best,
                              const int* __restrict__ choice, const double* __restrict__ Bs, double len,
@@ -340,7 +340,7 @@ __global__ void k4_backtrack(MilpDims d, int q, const long long* __restrict__ fu
 
 // ------------------------------------------------------------ K6 weight sync
 // For each rollout entry type: max link from any train device into any rollout
-// device of that type; bottleneck = min over entries (src/cost_model.cpp:255-277).
+// device of that type; bottleneck = min over entries (src/cost_model.cpp:174-196).
 __global__ void k6_type_maxlink(const int* __restrict__ train, int nt, const int* __restrict__ roll,
                                 int nr, const int* __restrict__ dtype, const double* __restrict__ links,
                                 int N, double* __restrict__ type_max /* [T] */) {
@@ -448,7 +448,7 @@ int rollout_capacities(gp_ctx* ctx, const int32_t* ids, int n, int32_t* caps) {
   return GP_OK;
 }
 
-// enumerate_configs (src/rollout_milp.cpp:122-172), batched over rollout sets: the
+// enumerate_configs (src/rollout_milp.cpp:39-89), batched over rollout sets: the
 // host derives each set's per-type machine availability (enumeration metadata), one
 // K3 launch scores every (set, type, TP multiset) candidate, one copy brings them back.
 int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* ns, const gp_rollout_opts* o,
@@ -585,7 +585,7 @@ int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opt
   return GP_OK;
 }
 
-// solve_milp (src/rollout_milp.cpp:174-254)
+// solve_milp (src/rollout_milp.cpp:91-171)
 //
 // Lattice tables are cached per configuration list: best[s] and choice[s] depend only
 // on the state's coordinates and the configs (the recurrence never looks at the

@@ -175,7 +175,7 @@ struct Driver {
       if (rc) return rc;
       for (int j = 0; j < m; ++j) {
         const int i = mq[j];
-        if (rcs[j] == GP_INVALID)  // ValidationError escapes schedule() (src/rollout_milp.cpp:193-195)
+        if (rcs[j] == GP_INVALID)  // ValidationError escapes schedule() (src/rollout_milp.cpp:110-112)
           return set_error(GP_INVALID, "capacity lattice too large for the exact solver");
         if (rcs[j] != GP_OK) continue;  // InfeasibleError: caught, rollout = nullopt
         Eval& e = *ev[i];

@@ -350,7 +350,7 @@ __global__ void k8_simulate(int n_seeds, const unsigned long long* __restrict__ 
   out[t] = o;
 }
 
-// replica_concurrency (src/cost_model.cpp:209-229) of each entry config, as in K3.
+// replica_concurrency (src/cost_model.cpp:128-148) of each entry config, as in K3.
 __global__ void k8_concurrency(int n, const gp_config* __restrict__ cfg, Scalars sc, const double* __restrict__ tcap,
                                int T, int* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

@@ -1,6 +1,6 @@
 // train.cu — sm_100a kernels for the training-side hot loop:
-//   constrained_search (src/train_search.cpp:268-325) over the layout space of
-//   enumerate_block_lists (src/train_search.cpp:145-192), scored with
+//   constrained_search (src/train_search.cpp:218-275) over the layout space of
+//   enumerate_block_lists (src/train_search.cpp:126-142), scored with
 //   train_stage_cost / train_cost_breakdown / mem_cumsum_train
 //   (src/cost_model.cpp:57-126,198-207).
 //
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256) k2b_transfers(const int* __restrict__ ord
 
 // ------------------------------------------------------------ K2c stage table
 // Per (block, layer_count): the option loop of constrained_search
-// (src/train_search.cpp:289-315) with mem_cumsum_train and train_stage_cost.
+// (src/train_search.cpp:241-265) with mem_cumsum_train and train_stage_cost.
 // One (tp, dp) option of a stage with lc layers (src/train_search.cpp:241-258 with
 // tp_dp_options :74-93, mem_cumsum_train src/cost_model.cpp:198-207, train_stage_cost
 // :57-91). False when the option is not offered or exceeds the block's memory.
@@ -752,7 +752,7 @@ __device__ __forceinline__ bool eval_layout(const TrainSpace& sp, const TrainTab
         : "r"(pos[q]), "r"(ex_mod));
     zero |= act[q] && lay[q] == 0;
   }
-  if (zero) {  // every stage needs at least one layer (src/train_search.cpp:217-225)
+  if (zero) {  // every stage needs at least one layer (src/train_search.cpp:166-175)
 #pragma unroll
     for (int q = 0; q < NS; ++q) {
       if (act[q] && lay[q] == 0) {

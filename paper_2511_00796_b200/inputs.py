@@ -214,7 +214,7 @@ def length_mean(hist) -> float:
 
 
 def load_workload(doc) -> Workload:
-    """load_workload_json (src/workload.cpp:70-99)."""
+    """load_workload_json (src/workload.cpp:71-99)."""
     if isinstance(doc, str):
         doc = json.loads(doc)
     m = doc["model"]

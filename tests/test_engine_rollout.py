@@ -100,7 +100,7 @@ def test_milp_errors():
     eng = engine("c3_64gpu")
     p = problem("c3_64gpu")
     cfgs = eng.enumerate_configs(list(range(64)))
-    with pytest.raises(ValidationError):  # lattice > 5e7 (src/rollout_milp.cpp:193-195)
+    with pytest.raises(ValidationError):  # lattice > 5e7 (src/rollout_milp.cpp:110-112)
         eng.solve_milp(cfgs, [400, 400, 400], 64.0, p.workload.mean_len)
     with pytest.raises(InfeasibleError):  # no configs
         eng.solve_milp([], [8, 8, 8], 64.0, p.workload.mean_len)
