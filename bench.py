@@ -40,9 +40,9 @@ CONFIG = "c5_1024gpu"
 WINDOW = 3
 METRIC = "candidate plans evaluated/sec"
 # from the committed ncu capture of K1-fast on this workload (profiles/r01/)
-K1_PROFILE = "profiles/r01/k1_layout_scan_fast_ncu_summary.txt"
-K1_WARP_INST_PER_CAND = 6.152   # smsp__inst_executed.sum / candidates (14,861,502,869 / 2,415,919,104)
-K1_DRAM_BYTES_PER_LAUNCH = 390400  # dram__bytes_read.sum + dram__bytes_write.sum (tables stay in L2)
+K1_PROFILE = "profiles/r02/k1_layout_scan_fast_ncu_summary.txt"
+K1_WARP_INST_PER_CAND = 5.806   # smsp__inst_executed.sum / candidates (14,026,989,862 / 2,415,919,104)
+K1_DRAM_BYTES_PER_LAUNCH = 395776  # dram__bytes_read.sum + dram__bytes_write.sum (tables stay in L2)
 UNIT = "plans/s"
 
 
