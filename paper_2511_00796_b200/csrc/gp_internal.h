@@ -125,6 +125,21 @@ struct __align__(16) SufEnt {
 constexpr int kDonations = 4;  // fix-up donations tabulated (more -> generic fallback)
 constexpr int kMsStride = 32;  // bytes per suffix choice in TrainTables::sf_ms
 
+// K1-fast's per-choice tables of the MIDDLE run (the last of the prefix runs, R - 2): the
+// prefix tables of a combination (front runs 0..R-3, middle choice) are the merge of the
+// front's (built by the warp when the front changes) and this row (k2m_middle_rows).
+struct __align__(16) MidRow {  // (a multiple of 16 bytes: copied to shared memory in 16-byte chunks)
+  double2 pt[5][5];      // (max total, max compute) of its stages: top a1 promoted, d1 donations
+  double R[4];           // remainders in stable descending order (-1 pad)
+  double t[3];           // internal stage-transfer terms (0 for absent ones)
+  signed char mp[5][5];  // largest layer count after d1 donations (-1: no donor left; L <= 127)
+  unsigned char nz[5];   // zero-layer stages at promotion a1
+  unsigned char k, b1, bl;  // blocks, end of the first block, start of the last block
+  int fs;                // floor sum
+  int bad;               // bit a1: a promoted stage would exceed L layers
+};
+static_assert(sizeof(MidRow) == 512, "MidRow is copied in 32 16-byte chunks, one per lane");
+
 // Device-side training tables of one train set.
 struct TrainTables {
   const int* ordered;
@@ -155,6 +170,11 @@ struct TrainTables {
   const double2* sf_st;   // [5 * (kDonations + 1)][n_suf]: (max total, max compute) at (b, d)
   const int* nzs_max;     // suffix stats: [0] most zero-layer stages of any suffix choice,
                           //   [1] kFsBias - smallest floor sum, [2] largest floor sum
+  const MidRow* mid;       // [choices of run R - 2] middle-run rows (K1-fast, R >= 2)
+  const unsigned long long* cntb_mid;  // [choices of run R - 2][cw] rank counts of the last run's
+                                       //   blocks among the middle remainders (bytes, 8 per word)
+  int cw;                    // words per cntb_mid row
+  int n_mid;                 // rows of mid
   int pos_off[GP_MAX_TYPES];
 };
 

@@ -831,6 +831,105 @@ __global__ void k2e_block_shares(const double2* __restrict__ blkf, int nblk, dou
 
 constexpr int kFsBias = 1 << 20;  // suffix-stats encoding of the smallest floor sum
 
+// K2m: one thread per choice of the middle run (R - 2): its MidRow — the k2f tables for a
+// prefix side (promotion count a1 of its own stages, d1 water-filling donations taken from
+// them; zero-layer stages counted with the one layer the fix-up gives them) — and its rank
+// counts of the last run's blocks (#middle remainders >= x: prefix stages win ties).
+__global__ void k2m_middle_rows(const SufEnt* __restrict__ mch, int n, const double2* __restrict__ blk_sh,
+                                const double2* __restrict__ stage, int L, int blk_off_last, int nlast, int cw,
+                                MidRow* __restrict__ rows, unsigned long long* __restrict__ cntb_mid) {
+  constexpr int DM = kDonations;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const SufEnt e = mch[i];
+  const int k = e.k;
+  double rem[4];
+  int fl[4], rk[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    rem[j] = -1.0;
+    fl[j] = 0;
+    if (j < k) {
+      const double2 sh = blk_sh[e.bi[j]];
+      rem[j] = sh.x;
+      fl[j] = (int)sh.y;
+    }
+  }
+  MidRow row;
+  int fs = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    rk[j] = 0;
+#pragma unroll
+    for (int j2 = 0; j2 < 4; ++j2)
+      if (j2 < k && j2 != j) rk[j] += rem[j2] > rem[j] || (rem[j2] == rem[j] && j2 < j);
+    fs += fl[j];
+    row.R[j] = -1.0;
+  }
+  for (int j = 0; j < k; ++j) row.R[rk[j]] = rem[j];
+  for (int j = 0; j < 3; ++j) row.t[j] = e.t[j];
+  row.k = (unsigned char)k;
+  row.b1 = (unsigned char)e.b1;
+  row.bl = (unsigned char)e.bl;
+  row.fs = fs;
+  unsigned bad = 0;
+  for (int a = 0; a <= 4; ++a) {
+    int lay[4];
+    int nz = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      lay[j] = 0;
+      if (j < k) {
+        lay[j] = fl[j] + (rk[j] < a ? 1 : 0);
+        nz += lay[j] == 0;
+        if (lay[j] > L) bad |= 1u << a;
+      }
+    }
+    row.nz[a] = (unsigned char)nz;
+    bool live = true;
+    for (int d = 0; d <= DM; ++d) {
+      int mx = -1, jm = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < k && lay[j] > 0 && lay[j] > mx) {
+          mx = lay[j];
+          jm = j;
+        }
+      double mt = 0, mc = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= k) continue;
+        const int l1 = lay[j] == 0 ? 1 : lay[j];
+        if (l1 < 1 || l1 > L) continue;
+        const double2 st = stage[(unsigned)(e.bi[j] * L + (l1 - 1))];
+        if (st.x > mt) mt = st.x;
+        if (st.y > mc) mc = st.y;
+      }
+      row.mp[a][d] = (signed char)(live ? (mx > 127 ? 127 : mx) : -1);
+      row.pt[a][d] = make_double2(mt, mc);
+      if (mx < 2) live = false;  // a donor needs >= 2 layers
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (live && j == jm) lay[j]--;
+    }
+  }
+  row.bad = (int)bad;
+  rows[i] = row;
+  for (int w = 0; w < cw; ++w) {
+    unsigned long long v = 0;
+    for (int bq = 0; bq < 8; ++bq) {
+      const int x = 8 * w + bq;
+      if (x >= nlast) break;
+      const double xr = blk_sh[blk_off_last + x].x;
+      unsigned long long c = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c += (j < k && row.R[j] >= xr) ? 1u : 0u;
+      v |= c << (8 * bq);
+    }
+    cntb_mid[(size_t)i * cw + w] = v;
+  }
+}
+
 // Per suffix choice: the fast-path tables (TrainTables::sf_*) and, per promotion count b and
 // donation count d, the (max total, max compute) of its stages — zero-layer stages counted
 // with the one layer the fix-up gives them, donors with the layers they keep.
@@ -932,6 +1031,9 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
 constexpr int kK1Threads = 128;
 // K1-fast variant switches (A/B measurements with tools/build_variant.sh + k1_variants.sh);
 // the defaults are the product
+#ifndef GPV_CTAS
+#define GPV_CTAS 6   // K1-fast launch bounds: min CTAs per SM (6: 72 registers, 7 resident; 7: slower)
+#endif
 #ifndef GPV_GS
 #define GPV_GS 4     // lanes per promotion count in the per-prefix tables
 #endif
@@ -948,26 +1050,47 @@ constexpr int kK1Threads = 128;
 #define GPV_MERGE 1  // 1: zero-layer donors by the co-rank of the two donor sequences (no loop) (-0.4 ms)
 #endif
 constexpr int kZsTable = 128;  // > L on the fast path
-constexpr int kMaxLastBlocks = 1024;  // last type run blocks with a per-prefix rank count (else generic K1)
+// (the per-warp tables are kept small: the K1-fast CTAs' shared memory decides how much of the
+// SM's 256 KB stays L1 for the suffix tables, which every candidate reads)
+constexpr int kMaxLastBlocks = 256;  // last type run blocks with a per-prefix rank count (else generic K1)
 
-// Warp-uniform fast-path data of one prefix (shared memory).
+// Warp-uniform fast-path data of one prefix (shared memory): the tables the candidate loop
+// reads (pt, mp, nzp, fp, bad) and, for R >= 3, the FRONT runs' own tables (runs 0..R-3,
+// rebuilt only when the front combination changes), which the per-prefix merge combines
+// with the middle run's precomputed row (MidRow).
 template <int R>
 struct PrefixFast {
   static constexpr int NP = (R - 1) * kMaxPerRun;
-  static constexpr int NPP = NP < 4 ? 4 : (NP < 8 ? 8 : 16);  // > NP, power of two
-  static constexpr int NQ = NP > 0 ? NP : 1;
+  static constexpr int NPF = (R > 2 ? R - 2 : 0) * kMaxPerRun;  // front slots
+  static constexpr int NQF = NPF > 0 ? NPF : 1;
+  static constexpr int NPFP = NPF < 4 ? 4 : (NPF < 8 ? 8 : 16);  // > NPF, power of two
   static constexpr int DM = kDonations;
-  double srt[NPP];            // prefix remainders sorted (desc, stage order), padded with -1
+  // merged prefix tables (what the candidate loop reads)
   double2 pt[NP + 1][DM + 1]; // (max total, max compute) of the prefix stages: top a promoted, d donations
-  double2 tc[NQ][DM + 3];     // stage q's (total, compute) at fl+1-o layers (o <= DM+1), o = DM+2: 1 layer
-  double rem[NQ];
-  int fl[NQ];
-  int rk[NQ];
-  double term[NQ];            // per prefix slot: its stage-transfer term (0 if none)
   short mp[NP + 1][DM + 1];   // largest layer count after d donations (-1: none / invalid)
   unsigned char nzp[NP + 1];  // zero-layer prefix stages at promotion a
   int fp;                     // sum of the prefix floors
   int bad;                    // bit a: a promoted prefix stage would exceed L layers
+  // front tables (runs 0..R-3)
+  double srtf[NPFP];          // front remainders sorted (desc, stage order), padded with -1
+  double2 tcf[NQF][DM + 3];   // front stage q's (total, compute) at fl+1-o layers, o = DM+2: 1 layer
+  double remf[NQF];
+  int flf[NQF];
+  int rkf[NQF];
+  int bif[NQF];
+  double termf[NQF];          // per front slot: the stage-transfer term that follows it (0 if none)
+  bool actf[NQF];
+  double2 ptf[NPF + 1][DM + 1];
+  short mpf[NPF + 1][DM + 1];
+  unsigned char nzf[NPF + 1];
+  int kf, fpf, badf, a_lastf; // front stages, floor sum, over bits, start of the front's last block
+  double trf;                 // left fold of the front's stage transfers
+  long long fkey;             // front combination the front tables hold (-1: none)
+  MidRow mrow[2];             // the middle rows of this prefix and (prefetched by cp.async) the next
+  int mrow_c[2];              // middle choice held by each buffer (-1: none)
+  int mbuf;                   // buffer of the current prefix
+  int cnt1[NPFP];             // per sorted front entry: middle remainders strictly above it
+
 #ifdef GP_DEBUG_CHECKS
   int a_lo, a_hi;             // the tabulated promotion counts
   int dm[NP + 1];             // the tabulated donations per promotion count
@@ -976,16 +1099,17 @@ struct PrefixFast {
 
 // K1-fast shared memory per warp beside PrefixFast: the rank count of every last-run
 // block's remainder among the prefix's (cntb) and the prefix's junction-transfer row (txs).
-constexpr int kMaxJunction = 64;  // nc_last + 2 (else generic K1)
-struct PrefixLast {
-  unsigned char cntb[kMaxLastBlocks];
+constexpr int kMaxJunction = 32;  // nc_last + 2 (else generic K1)
+struct __align__(8) PrefixLast {
+  unsigned char cntb[kMaxLastBlocks];   // rank counts among all prefix remainders (merged)
+  unsigned char cntbf[kMaxLastBlocks];  // among the front's remainders only (rebuilt with the front)
   double txs[kMaxJunction];
 };
 
 // number of entries >= x in the descending, -1-padded srt (x >= 0)
 template <int R>
 __device__ __forceinline__ int count_ge(const double* srt, double x) {
-  constexpr int NPP = PrefixFast<R>::NPP;
+  constexpr int NPP = PrefixFast<R>::NPFP;
   int pos = 0;
 #pragma unroll
   for (int step = NPP / 2; step >= 1; step >>= 1)
@@ -993,14 +1117,76 @@ __device__ __forceinline__ int count_ge(const double* srt, double x) {
   return pos;
 }
 
-// All lanes: the K1-fast subset of prefix_data (slot activity, block ids, the junction
-// position) computed one slot per lane; the transfer terms go to F.term and are folded
-// in stage order by prefix_fast (adding the 0 terms of the other slots is exact).
+// 16-byte asynchronous global -> shared copies (LDGSTS): the next prefix's middle row is
+// fetched while the current prefix's candidates are scored.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// All lanes: start copying middle row c into buffer b (one 16-byte chunk per lane)
 template <int R>
-__device__ __forceinline__ void prefix_data_warp(int lane, const TrainSpace& sp, const TrainTables& tb,
-                                                 const Prefix<R>& P, PrefixData<R>& D, PrefixFast<R>& F) {
-  constexpr int NP = PrefixData<R>::NP;
-  if (lane < NP) {
+__device__ __forceinline__ void mid_fetch(int lane, const TrainTables& tb, PrefixFast<R>& F, int b, int c) {
+  static_assert(sizeof(MidRow) == 32 * 16, "one 16-byte chunk per lane");
+  const char* src = reinterpret_cast<const char*>(tb.mid + c);
+  char* dst = reinterpret_cast<char*>(&F.mrow[b]);
+  cp_async16(dst + 16 * lane, src + 16 * lane);
+  cp_async_commit();
+  if (lane == 0) F.mrow_c[b] = c;
+}
+
+// R == 1 (no prefix runs): empty prefix tables.
+template <int R>
+__device__ __forceinline__ void prefix_single(int lane, PrefixData<R>& D, PrefixFast<R>& F, unsigned char* cntb,
+                                              int nlast) {
+  constexpr int DM = kDonations;
+  if (lane <= DM) {
+    F.pt[0][lane] = make_double2(0.0, 0.0);
+    F.mp[0][lane] = -1;
+  }
+  if (lane == 0) {
+    F.fp = 0;
+    F.bad = 0;
+    F.nzp[0] = 0;
+    D.transfers = 0.0;
+    D.a_last = 0;
+    D.u = 0;
+  }
+  for (int i = lane; i < nlast; i += 32) cntb[i] = 0;
+  __syncwarp();
+}
+
+// All lanes: the front runs' (0..R-3) tables — slot data, remainder ranks, stage-time cache,
+// the full (promotion a0 in [0, kf], donation d0 <= kDonations) tables, the front transfer
+// fold and the rank counts of the last run's blocks among the front remainders. Rebuilt only
+// when the front combination changes (every ~#middle-choices prefixes).
+template <int R>
+__device__ __forceinline__ void front_fast(int lane, const TrainSpace& sp, const TrainTables& tb, int L,
+                                           const Prefix<R>& P, PrefixFast<R>& F, unsigned char* cntbf, int nlast) {
+  constexpr int NPF = PrefixFast<R>::NPF;
+  constexpr int NPFP = PrefixFast<R>::NPFP;
+  constexpr int DM = kDonations;
+  if (NPF == 0) {  // R == 2: no front
+    if (lane <= DM) {
+      F.ptf[0][lane] = make_double2(0.0, 0.0);
+      F.mpf[0][lane] = -1;
+    }
+    if (lane < NPFP) F.srtf[lane] = -1.0;
+    if (lane == 0) {
+      F.nzf[0] = 0;
+      F.kf = F.fpf = F.badf = F.a_lastf = 0;
+      F.trf = 0.0;
+    }
+    for (int i = lane; i < nlast; i += 32) cntbf[i] = 0;
+    __syncwarp();
+    return;
+  }
+  bool aq = false;
+  double rq = -1.0;
+  int fq = 0;
+  if (lane < NPF) {
     const int r = lane / kMaxPerRun, j = lane % kMaxPerRun;
     const bool act = j < P.k[r];
     int bi = 0;
@@ -1011,105 +1197,52 @@ __device__ __forceinline__ void prefix_data_warp(int lane, const TrainSpace& sp,
         const int e = sp.nc[r] + 2;
         t = tb.tin[sp.tin_off[r] + ((size_t)P.b[r][j] * e + P.b[r][j + 1]) * e +
                    P.b[r][j + 2 <= kMaxPerRun ? j + 2 : kMaxPerRun]];
-      } else if (r + 2 < R) {
+      } else if (r + 3 < R) {  // junction to the next front run
         const int e2 = sp.nc[r + 1] + 2;
         t = tb.tx[sp.tx_off[r] + (size_t)P.b[r][j] * e2 + P.b[r + 2 < R ? r + 1 : r][1]];
-      } else {
-        D.a_last = P.b[r][j];
+      } else {  // the front's last block: its junction to the middle run is per prefix
+        F.a_lastf = P.b[r][j];
       }
-    }
-    D.act[lane] = act;
-    D.bi[lane] = bi;
-    F.term[lane] = t;
-  }
-  if (lane == 0) D.u = P.u;
-  __syncwarp();
-}
-
-// All lanes: remainder ranks, floor sum, stage-time cache and the (promotion, donation)
-// tables of the warp's prefix.
-template <int R>
-__device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, const TrainTables& tb, int L,
-                                            int3 sstat, PrefixData<R>& D, PrefixFast<R>& F,
-                                            unsigned char* cntb, double* txs, const int* zst) {
-  const int sp_nc_last = sp.nc[R - 1], blk_off_last = sp.blk_off[R - 1];
-  constexpr int NP = PrefixData<R>::NP;
-  constexpr int NPP = PrefixFast<R>::NPP;
-  constexpr int DM = kDonations;
-  if (NP == 0) {
-    if (lane <= DM) {
-      F.pt[0][lane] = make_double2(0.0, 0.0);
-      F.mp[0][lane] = -1;
-    }
-    if (lane == 0) {
-      F.fp = 0;
-      F.bad = 0;
-      F.nzp[0] = 0;
-      D.transfers = 0.0;
-      D.a_last = 0;
-    }
-    __syncwarp();
-    return;
-  }
-  bool aq = false;
-  double rq = -1.0;
-  int fq = 0;
-  if (lane < NP) {
-    aq = D.act[lane];
-    if (aq) {
-      const double2 sh = tb.blk_sh[D.bi[lane]];
+      const double2 sh = tb.blk_sh[bi];
       rq = sh.x;
       fq = (int)sh.y;
     }
-    F.rem[lane] = rq;
-    F.fl[lane] = fq;
+    aq = act;
+    F.actf[lane] = act;
+    F.bif[lane] = bi;
+    F.termf[lane] = t;
+    F.remf[lane] = rq;
+    F.flf[lane] = fq;
   }
-  if (lane < NPP) F.srt[lane] = -1.0;
-  if (lane == 0) F.bad = 0;
+  if (lane < NPFP) F.srtf[lane] = -1.0;
+  if (lane == 0) F.badf = 0;
   __syncwarp();
-  if (lane < NP && aq) {
+  if (lane < NPF && aq) {
     int rk = 0;
 #pragma unroll
-    for (int q2 = 0; q2 < NP; ++q2) {
-      const double r2 = F.rem[q2];
-      rk += (D.act[q2] && (r2 > rq || (r2 == rq && q2 < lane))) ? 1 : 0;
+    for (int q2 = 0; q2 < NPF; ++q2) {
+      const double r2 = F.remf[q2];
+      rk += (F.actf[q2] && (r2 > rq || (r2 == rq && q2 < lane))) ? 1 : 0;
     }
-    F.rk[lane] = rk;
-    F.srt[rk] = rq;
+    F.rkf[lane] = rk;
+    F.srtf[rk] = rq;
   }
-  // stage-time cache: every layer count a prefix stage can end with
-  for (int idx = lane; idx < NP * (DM + 3); idx += 32) {
+  for (int idx = lane; idx < NPF * (DM + 3); idx += 32) {
     const int q = idx / (DM + 3), o = idx % (DM + 3);
-    if (!D.act[q]) continue;
-    const int lay = o == DM + 2 ? 1 : F.fl[q] + 1 - o;
+    if (!F.actf[q]) continue;
+    const int lay = o == DM + 2 ? 1 : F.flf[q] + 1 - o;
     double2 v = make_double2(kInf, kInf);
-    if (lay >= 1 && lay <= L) v = tb.stage[(unsigned)(D.bi[q] * L + (lay - 1))];
-    F.tc[q][o] = v;
+    if (lay >= 1 && lay <= L) v = tb.stage[(unsigned)(F.bif[q] * L + (lay - 1))];
+    F.tcf[q][o] = v;
   }
   __syncwarp();
-  // per promotion count a (one lane each): the layer counts, then up to dm water-filling
-  // donations (dm = the most fix-ups a candidate of this prefix can need), recording the
-  // stage maxima and the largest layer count of every state
-  // only the promotion counts a candidate can reach: extra = L - fp - fs with the suffix
-  // floor sum fs in [fs_min, fs_max] and a = extra - b, b in [0, 4]
-  const int kp = D.u;
-  const int nzs_max = sstat.x, fs_min = kFsBias - sstat.y, fs_max = sstat.z;
-  int fp_all = 0;
+  int kf = 0;
 #pragma unroll
-  for (int q = 0; q < NP; ++q) fp_all += F.fl[q];
-  const int a_lo = max(0, L - fp_all - fs_max - 4), a_hi = min(kp, L - fp_all - fs_min);
-#ifdef GP_DEBUG_CHECKS
-  if (lane == 0) {
-    F.a_lo = a_lo;
-    F.a_hi = a_hi;
-  }
-#endif
-  // One group of GS = 4 lanes per promotion count a (eight per round), R - 1 prefix stage
-  // slots per lane (slot q = lane % 4 + 4 j): the per-stage values are reduced across the group
-  // (maxima of (total, compute), and the donor = the first slot with the most layers) for
-  // d = 0..dm water-filling donations.
+  for (int r = 0; r + 2 < R; ++r) kf += P.k[r];
+  // One group of GS lanes per promotion count a0 in [0, kf], up to kDonations water-filling
+  // donations each (the first slot with the most layers donates).
   constexpr int GS = GPV_GS;
-  constexpr int SPL = NP > 0 ? (NP + GS - 1) / GS : 1;  // outer slots per lane (R = 1 returned above)
+  constexpr int SPL = NPF > 0 ? (NPF + GS - 1) / GS : 1;
   constexpr int GPW = 32 / GS;
   const int grp = lane / GS, ql = lane % GS;
   bool actv[SPL];
@@ -1117,14 +1250,14 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
 #pragma unroll
   for (int j = 0; j < SPL; ++j) {
     const int q = ql + GS * j;
-    actv[j] = q < NP && D.act[q];
-    flv[j] = actv[j] ? F.fl[q] : 0;
-    rkv[j] = actv[j] ? F.rk[q] : 0;
+    actv[j] = q < NPF && F.actf[q];
+    flv[j] = actv[j] ? F.flf[q] : 0;
+    rkv[j] = actv[j] ? F.rkf[q] : 0;
   }
   const unsigned gmask = ((1u << GS) - 1u) << (grp * GS);
-  for (int a0 = a_lo; a0 <= a_hi; a0 += GPW) {  // warp-uniform rounds
+  for (int a0 = 0; a0 <= kf; a0 += GPW) {
     const int a = a0 + grp;
-    const bool ga = a <= a_hi;
+    const bool ga = a <= kf;
     int lay[SPL];
     int nz = 0;
     bool ov = false;
@@ -1137,21 +1270,15 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
 #pragma unroll
     for (int o = GS / 2; o >= 1; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
     const bool over = (__ballot_sync(0xffffffffu, ov) & gmask) != 0;
-    // most suffix zero-layer stages a candidate with promotion count a can meet
-    const int za = fp_all + a;
-    const int zs = (ga && za < kZsTable) ? zst[za] : 0;
-    const int dm = min(DM, nz + min(zs, nzs_max));
-    const int dm_w = __reduce_max_sync(0xffffffffu, ga ? dm : 0);
     bool live = true;
-    for (int d = 0; d <= dm_w; ++d) {
+    for (int d = 0; d <= DM; ++d) {
       double vx = 0, vy = 0;  // an inactive slot adds nothing (the maxima start at 0)
       int key = -1;           // most layers, then the first slot
 #pragma unroll
       for (int j = 0; j < SPL; ++j) {
         if (!actv[j]) continue;
         const int q = ql + GS * j;
-        const double2 v = F.tc[q][lay[j] == 0 ? DM + 2 : flv[j] + 1 - lay[j]];
-        // "if (v > m) m = v" from 0: NaN and non-positive values ignored
+        const double2 v = F.tcf[q][lay[j] == 0 ? DM + 2 : flv[j] + 1 - lay[j]];
         const double tx = v.x > 0 ? v.x : 0.0, ty = v.y > 0 ? v.y : 0.0;
         if (tx > vx) vx = tx;
         if (ty > vy) vy = ty;
@@ -1167,11 +1294,11 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
       }
       const int mx = key < 0 ? -1 : key >> 4;
       const int qm = key < 0 ? -1 : 15 - (key & 15);
-      if (ga && d <= dm && ql == 0) {
-        F.pt[a][d] = make_double2(vx, vy);
-        F.mp[a][d] = (short)(live ? mx : -1);
+      if (ga && ql == 0) {
+        F.ptf[a][d] = make_double2(vx, vy);
+        F.mpf[a][d] = (short)(live ? mx : -1);
       }
-      if (mx < 2) live = false;  // a donor needs >= 2 layers (checked by the scan)
+      if (mx < 2) live = false;
       if (live) {
 #pragma unroll
         for (int j = 0; j < SPL; ++j)
@@ -1179,31 +1306,146 @@ __device__ __forceinline__ void prefix_fast(int lane, const TrainSpace& sp, cons
       }
     }
     if (ga && ql == 0) {
-#ifdef GP_DEBUG_CHECKS
-      F.dm[a] = dm;
-#endif
-      F.nzp[a] = (unsigned char)nz;
-      if (over) atomicOr(&F.bad, 1 << a);
+      F.nzf[a] = (unsigned char)nz;
+      if (over) atomicOr(&F.badf, 1 << a);
     }
   }
   if (lane == 0) {
     int fp = 0;
     double tr = 0.0;
 #pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      fp += F.fl[q];  // inactive slots hold 0
-      tr += F.term[q];
+    for (int q = 0; q < NPF; ++q) {
+      fp += F.flf[q];  // inactive slots hold 0
+      tr += F.termf[q];
     }
-    F.fp = fp;
-    D.transfers = tr;
+    F.kf = kf;
+    F.fpf = fp;
+    F.trf = tr;
   }
-  // rank count of every last-run block's remainder among the prefix remainders, and the
-  // junction-transfer row of the prefix's last block
-  const int e2 = sp_nc_last + 2;
-  const int nlast = e2 * (sp_nc_last + 1) / 2;
-  for (int i = lane; i < nlast; i += 32) cntb[i] = (unsigned char)count_ge<R>(F.srt, tb.blk_sh[blk_off_last + i].x);
+  for (int i = lane; i < nlast; i += 32)
+    cntbf[i] = (unsigned char)count_ge<R>(F.srtf, tb.blk_sh[sp.blk_off[R - 1] + i].x);
+  __syncwarp();
+}
+
+// All lanes: the prefix tables of (front combination, middle choice) — the merge of the
+// front tables and the middle run's MidRow. Promotions: the prefix's top-a stages by
+// remainder (ties: the earlier stage, i.e. the front) hold a0 front and a1 = a - a0 middle
+// stages; donations: the first stage with the most layers donates, so the d donors are the
+// d largest of the two non-increasing donor sequences (front first on ties, co-rank); the
+// maxima of a state are the maxima of the two sides' states. Then the transfer fold (front,
+// junction into the middle run, its internal terms), the merged rank counts and the
+// junction row to the last run.
+template <int R>
+__device__ __forceinline__ void prefix_merge(int lane, const TrainSpace& sp, const TrainTables& tb, int L,
+                                             int3 sstat, const Prefix<R>& P, PrefixData<R>& D, PrefixFast<R>& F,
+                                             PrefixLast& PL, const unsigned char* zst, int nlast) {
+  constexpr int NPF = PrefixFast<R>::NPF;
+  constexpr int DM = kDonations;
+  const int c1 = P.ci[R - 2];
+  // this prefix's middle row: normally prefetched into the other buffer during the previous
+  // prefix; else (chunk start, a front change) fetched now
+  int b = F.mbuf ^ 1;
+  if (F.mrow_c[b] != c1) {
+    b = F.mbuf;  // (the current buffer's row is no longer needed)
+    mid_fetch<R>(lane, tb, F, b, c1);
+  }
+  cp_async_wait_all();
+  __syncwarp();
+  if (lane == 0) F.mbuf = b;
+  const MidRow& M = F.mrow[b];
+  const int kf = F.kf, k1 = M.k;
+  if (lane < NPF) {
+    int c = 0;
+    const double rf = F.srtf[lane];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c += (j < k1 && M.R[j] > rf) ? 1 : 0;
+    F.cnt1[lane] = c;
+  }
+  if (lane == 0) {
+    F.bad = 0;
+    D.u = P.u;
+  }
+  __syncwarp();
+  const int fp_all = F.fpf + M.fs;
+  const int kp = kf + k1;
+  const int nzs_max = sstat.x, fs_min = kFsBias - sstat.y, fs_max = sstat.z;
+  const int a_lo = max(0, L - fp_all - fs_max - 4), a_hi = min(kp, L - fp_all - fs_min);
+#ifdef GP_DEBUG_CHECKS
+  if (lane == 0) {
+    F.a_lo = a_lo;
+    F.a_hi = a_hi;
+  }
+  GP_CHECK(kp == P.u);
+#endif
+  const int ncell = a_hi >= a_lo ? (a_hi - a_lo + 1) * (DM + 1) : 0;
+  for (int idx = lane; idx < ncell; idx += 32) {
+    const int a = a_lo + idx / (DM + 1), d = idx % (DM + 1);
+    int a0 = 0;
+#pragma unroll
+    for (int i = 0; i < NPF; ++i) a0 += (i < kf && i + F.cnt1[i] < a) ? 1 : 0;
+    const int a1 = a - a0;
+    GP_CHECK(a1 >= 0 && a1 <= k1 && a0 <= kf);
+    const int nz = F.nzf[a0] + M.nz[a1];
+    const int za = fp_all + a;
+    const int zs = za < kZsTable ? zst[za] : 0;
+    const int dm = min(DM, nz + min(zs, nzs_max));
+    if (d == 0) {
+      F.nzp[a] = (unsigned char)nz;
+      if (((F.badf >> a0) | (M.bad >> a1)) & 1) atomicOr(&F.bad, 1 << a);
+#ifdef GP_DEBUG_CHECKS
+      F.dm[a] = dm;
+#endif
+    }
+    if (d > dm) continue;
+    int d0 = 0;
+    if (d > 0) {  // common cases first: every donor from one side
+      if (F.mpf[a0][d - 1] >= M.mp[a1][0]) {
+        d0 = d;
+      } else if (M.mp[a1][d - 1] > F.mpf[a0][0]) {
+        d0 = 0;
+      } else {
+#pragma unroll
+        for (int i = 1; i <= DM; ++i)
+          if (i <= d) d0 += F.mpf[a0][i - 1] >= M.mp[a1][d - i] ? 1 : 0;
+      }
+    }
+    const int d1 = d - d0;
+    const double2 pf = F.ptf[a0][d0], pm = M.pt[a1][d1];
+    double2 v = pf;
+    if (pm.x > v.x) v.x = pm.x;
+    if (pm.y > v.y) v.y = pm.y;
+    bool live = true;
+    if (d > 0) {  // the donors so far: the smallest (last) one must have had >= 2 layers
+      const int lf = d0 > 0 ? F.mpf[a0][d0 - 1] : 0x7fff, lm = d1 > 0 ? M.mp[a1][d1 - 1] : 0x7fff;
+      live = (lf < lm ? lf : lm) >= 2;
+    }
+    const int mxf = F.mpf[a0][d0], mxm = M.mp[a1][d1];
+    F.pt[a][d] = v;
+    F.mp[a][d] = (short)(live ? (mxf > mxm ? mxf : mxm) : -1);
+  }
+  if (lane == 0) {
+    F.fp = fp_all;
+    double tr = F.trf;
+    if (R > 2) tr += tb.tx[sp.tx_off[R > 2 ? R - 3 : 0] + (size_t)F.a_lastf * (sp.nc[R - 2] + 2) + M.b1];
+    tr += M.t[0];  // (absent internal terms are exact zeros)
+    tr += M.t[1];
+    tr += M.t[2];
+    D.transfers = tr;
+    D.a_last = M.bl;
+  }
+  {
+    const int cw = tb.cw;
+    unsigned long long* __restrict__ dst = reinterpret_cast<unsigned long long*>(PL.cntb);
+    const unsigned long long* srcf = reinterpret_cast<const unsigned long long*>(PL.cntbf);
+    const unsigned long long* __restrict__ srcm = tb.cntb_mid + (size_t)c1 * cw;
+    for (int w = lane; w < cw; w += 32) dst[w] = srcf[w] + __ldg(srcm + w);  // bytes < 128: no carries
+  }
+  __syncwarp();
+  const int e2 = sp.nc[R - 1] + 2;
   const double* __restrict__ txrow = tb.tx + sp.tx_off[R > 1 ? R - 2 : 0] + (size_t)D.a_last * e2;
-  for (int i = lane; i < e2; i += 32) txs[i] = txrow[i];
+  for (int i = lane; i < e2; i += 32) PL.txs[i] = txrow[i];
+  // prefetch the next prefix's middle row (usually the next middle choice)
+  if (c1 + 1 < tb.n_mid) mid_fetch<R>(lane, tb, F, b ^ 1, c1 + 1);
   __syncwarp();
 }
 
@@ -1332,7 +1574,7 @@ __device__ unsigned long long g_k1_fast_cnt[2];
 // for k1_deferred, which scores them with the generic eval_layout — so every candidate's
 // per-step time is the one the reference computes.
 template <int R, bool DUMP = false>
-__global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace sp, TrainTables tb,
+__global__ void __launch_bounds__(kK1Threads, GPV_CTAS) k1_layout_scan_fast(TrainSpace sp, TrainTables tb,
                                                       const double2* __restrict__ blkf, int L,
                                                       ScanRange rg, NearMin* __restrict__ partial,
                                                       unsigned long long* __restrict__ slow_q) {
@@ -1361,14 +1603,20 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
   for (int i = threadIdx.x; i <= GP_MAX_STAGES; i += blockDim.x) fd[i] = tb.fd_coef[i];
   // zst[t]: most zero-layer suffix stages over the (floor sum, promotion count b) pairs a
   // candidate whose prefix floors plus promotions total t can meet (fs = L - t - b)
-  __shared__ int zst[kZsTable];
+  __shared__ unsigned char zst[kZsTable];
   for (int t = threadIdx.x; t < kZsTable; t += blockDim.x) {
     int z = 0;
     for (int b = 0; b <= 4; ++b) {
       const int fs = L - t - b;
       if (fs >= 0 && fs <= L) z = max(z, tb.nzs_max[3 + fs * 5 + b]);
     }
-    zst[t] = z;
+    zst[t] = (unsigned char)min(z, 255);
+  }
+  const int nlast = e2 * (e2 - 1) / 2;
+  if ((threadIdx.x & 31) == 0) {
+    F.fkey = -1;
+    F.mrow_c[0] = F.mrow_c[1] = -1;
+    F.mbuf = 0;
   }
   __syncthreads();
   for (long long it = warp; it < n_items; it += n_warps) {
@@ -1378,8 +1626,19 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
     if (lane == 0) prefix_decode<R>(sp, p, P);
     for (; p < p_end; ++p) {
       __syncwarp();
-      prefix_data_warp<R>(lane, sp, tb, P, D, F);
-      prefix_fast<R>(lane, sp, tb, L, sstat, D, F, cntb, txs, zst);
+      if constexpr (R == 1) {
+        prefix_single<R>(lane, D, F, cntb, nlast);
+      } else {
+        // the front runs' tables only when the front combination changed
+        long long fk = 0;
+#pragma unroll
+        for (int r = 0; r + 2 < R; ++r) fk = (fk << 21) | P.ci[r];
+        if (fk != F.fkey) {
+          front_fast<R>(lane, sp, tb, L, P, F, sL[threadIdx.x >> 5].cntbf, nlast);
+          if (lane == 0) F.fkey = fk;
+        }
+        prefix_merge<R>(lane, sp, tb, L, sstat, P, D, F, sL[threadIdx.x >> 5], zst, nlast);
+      }
       const int kp = D.u;
       const int fp = F.fp, pbad = F.bad;
       const double dtr = D.transfers;
@@ -1540,6 +1799,7 @@ __global__ void __launch_bounds__(kK1Threads, 6) k1_layout_scan_fast(TrainSpace 
       if (lane == 0 && p + 1 < p_end) prefix_advance<R>(sp, P);
     }
   }
+  cp_async_wait_all();  // (a last middle-row prefetch may still be in flight)
   n_tab = __reduce_add_sync(0xffffffffu, n_tab);
   if (lane == 0) atomicAdd(&g_k1_fast_cnt[0], (unsigned long long)n_tab);
   NearMin nm{b0, {k0, k1, k2}, feasible};
@@ -1737,6 +1997,7 @@ struct HostSpace {
   std::vector<int> mgrp, gstart, gmach;  // machine groups of the canonical order
   bool exact_total = false;  // every partial FLOPS sum exact: K1-fast applies
   double flops_total = 0;    // allocate_layers' total (the same for every layout when exact)
+  std::vector<int4> choices_m;  // choices of the middle run R - 2 (K1-fast's MidRow tables)
 };
 
 // choices (k, cut positions) of run r in run_compositions order (k ascending, cuts lexicographic)
@@ -1899,6 +2160,7 @@ int build_space(gp_ctx* ctx, const int32_t* ids, int n, const gp_train_opts* o, 
   // last-run choices in run_compositions order: k ascending, cut indices lexicographic
   run_choices(sp, sp.R - 1, h.choices);
   sp.n_suf = (int)h.choices.size();
+  if (sp.R >= 2) run_choices(sp, sp.R - 2, h.choices_m);
   return GP_OK;
 }
 // Host twin of prefix_decode's base (rank of a prefix's first layout).
@@ -2183,6 +2445,10 @@ struct PreparedTrain {
   BlockMeta* d_meta = nullptr;
   int4* d_items = nullptr;
   int4* d_choices = nullptr;
+  int4* d_choices_m = nullptr;  // middle-run choices (K1-fast)
+  SufEnt* d_sufm = nullptr;     // middle-run choice table
+  MidRow* d_mid = nullptr;
+  unsigned long long* d_cntb_mid = nullptr;
   int* d_mgrp = nullptr;
   int* d_gstart = nullptr;
   int* d_gmach = nullptr;
@@ -2245,6 +2511,12 @@ void train_state_free(gp_ctx* ctx) {
   prepared(ctx) = nullptr;
 }
 
+// words of one middle-run rank-count row: the last run's blocks, 8 per word
+static int cntb_words(const HostSpace& h) {
+  const int e = h.sp.nc[h.sp.R - 1] + 2;
+  return (e * (e - 1) / 2 + 7) / 8;
+}
+
 // ---- layout of one prepared train set in a device arena: the inputs section
 // (copied from host) first, then the tables the kernels build.
 static size_t input_bytes(const HostSpace& h) {
@@ -2256,6 +2528,7 @@ static size_t input_bytes(const HostSpace& h) {
   add(sizeof(BlockMeta) * h.meta.size());
   add(sizeof(int4) * h.items.size());
   add(sizeof(int4) * h.choices.size());
+  add(sizeof(int4) * h.choices_m.size());
   add(sizeof(int) * h.mgrp.size());
   add(sizeof(int) * h.gstart.size());
   add(sizeof(int) * h.gmach.size());
@@ -2273,6 +2546,9 @@ static size_t table_bytes(const HostSpace& h, int L, int max_blocks) {
   add(sizeof(double) * (h.tx_size + 1));
   add(sizeof(double) * (GP_MAX_STAGES + 1));
   add(sizeof(SufEnt) * (h.choices.size() + 1));
+  add(sizeof(SufEnt) * (h.choices_m.size() + 1));
+  add(sizeof(MidRow) * (h.choices_m.size() + 1));
+  add(sizeof(unsigned long long) * (h.choices_m.size() + 1) * cntb_words(h));
   add(sizeof(double2) * h.nblk);
   const size_t nsf = h.choices.size() + 1;
   add(sizeof(int4) * nsf);
@@ -2304,6 +2580,8 @@ static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_bas
   stage(h.items.data(), sizeof(int4) * h.items.size(), P.d_items);
   P.d_choices = carve<int4>(in, h.choices.size());
   stage(h.choices.data(), sizeof(int4) * h.choices.size(), P.d_choices);
+  P.d_choices_m = carve<int4>(in, h.choices_m.size());
+  stage(h.choices_m.data(), sizeof(int4) * h.choices_m.size(), P.d_choices_m);
   P.d_mgrp = carve<int>(in, h.mgrp.size());
   stage(h.mgrp.data(), sizeof(int) * h.mgrp.size(), P.d_mgrp);
   P.d_gstart = carve<int>(in, h.gstart.size());
@@ -2318,6 +2596,9 @@ static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_bas
   P.d_tx = carve<double>(tab, h.tx_size + 1);
   P.d_fd = carve<double>(tab, GP_MAX_STAGES + 1);
   P.d_suf = carve<SufEnt>(tab, h.choices.size() + 1);
+  P.d_sufm = carve<SufEnt>(tab, h.choices_m.size() + 1);
+  P.d_mid = carve<MidRow>(tab, h.choices_m.size() + 1);
+  P.d_cntb_mid = carve<unsigned long long>(tab, (h.choices_m.size() + 1) * cntb_words(h));
   P.d_blk_sh = carve<double2>(tab, h.nblk);
   const size_t nsf = h.choices.size() + 1;
   P.d_sf_hot = carve<int4>(tab, nsf);
@@ -2369,6 +2650,10 @@ static TrainTables prepared_tables(const gp_ctx* ctx, const PreparedTrain& P) {
   tb.sf_ms = P.d_sf_ms;
   tb.sf_st = P.d_sf_st;
   tb.nzs_max = P.d_nzs_max;
+  tb.mid = P.d_mid;
+  tb.cntb_mid = P.d_cntb_mid;
+  tb.cw = cntb_words(P.h);
+  tb.n_mid = (int)P.h.choices_m.size();
   for (int r = 0; r < P.h.sp.R; ++r) tb.pos_off[r] = P.h.pos_off[r];
   return tb;
 }
@@ -2427,6 +2712,15 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
       k2f_suffix_fast<<<(ns + 127) / 128, 128, 0, stream>>>(P.d_suf, ns, P.d_blk_sh, P.d_stage, L,
                                                            h.sp.blk_off[R - 1], P.d_sf_hot, P.d_sf_zb,
                                                            P.d_sf_t, P.d_sf_ms, P.d_sf_st, P.d_nzs_max);
+      if (R >= 2) {  // the middle run's rows (K2d on run R - 2, then K2m)
+        const int nm = (int)h.choices_m.size();
+        const int e_last = h.sp.nc[R - 1] + 2;
+        k2d_suffix_table<<<(nm + 255) / 256, 256, 0, stream>>>(P.d_choices_m, nm, h.sp, P.d_tin, P.d_sufm, R - 2);
+        k2m_middle_rows<<<(nm + 127) / 128, 128, 0, stream>>>(P.d_sufm, nm, P.d_blk_sh, P.d_stage, L,
+                                                             h.sp.blk_off[R - 1], e_last * (e_last - 1) / 2,
+                                                             cntb_words(h), P.d_mid, P.d_cntb_mid);
+        ctx->launches += 2;
+      }
       ctx->launches += 2;
     }
   }
