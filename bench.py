@@ -41,8 +41,8 @@ WINDOW = 3
 METRIC = "candidate plans evaluated/sec"
 # from the committed ncu capture of K1-fast on this workload (profiles/r01/)
 K1_PROFILE = "profiles/r02/k1_layout_scan_fast_ncu_summary.txt"
-K1_WARP_INST_PER_CAND = 4.663   # smsp__inst_executed.sum / candidates (11,265,218,259 / 2,415,919,104)
-K1_DRAM_BYTES_PER_LAUNCH = 1635328  # dram__bytes_read.sum + dram__bytes_write.sum (tables + middle rows, L2-resident)
+K1_WARP_INST_PER_CAND = 4.729   # smsp__inst_executed.sum / candidates (11,424,639,318 / 2,415,919,104)
+K1_DRAM_BYTES_PER_LAUNCH = 1634816  # dram__bytes_read.sum + dram__bytes_write.sum (tables + middle rows, L2-resident)
 UNIT = "plans/s"
 
 
@@ -360,8 +360,8 @@ def run_b200(args):
     if not args.no_units:
         line["units"] = {"U1_same_workload": same_workload(local_rank, args.steps, args.warmup),
                          "U2_milp": milp_rate(local_rank), "U3_partition": partition_rate(local_rank)}
-    if not args.no_ttp:
-        line["time_to_best_plan"] = time_to_best_plan(local_rank)
+    if not args.no_ttp:  # (at N > 1: rank 0 alone, one multi-GPU context over all N devices)
+        line["time_to_best_plan"] = time_to_best_plan(list(range(world)) if world > 1 else [local_rank])
     print(json.dumps(line), flush=True)
     return 0
 
@@ -513,11 +513,13 @@ def partition_rate(device):
     return out
 
 
-def time_to_best_plan(device, keys=("c3_64gpu/eta=1", "c4_256gpu/eta=2", "c5_1024gpu/eta=2")):
+def time_to_best_plan(devices, keys=("c3_64gpu/eta=1", "c4_256gpu/eta=2", "c5_1024gpu/eta=2")):
     """schedule() wall time (all window passes, up to the final plan) through the native
-    batched driver (gp_schedule) on a freshly created context (context setup excluded,
-    like the reference's input loading); the reference's own schedule() on one host core
-    for the configs it can finish, with the plans compared field by field."""
+    batched driver (gp_schedule) on a freshly created context over `devices` (one GPU, or
+    a multi-GPU context at N > 1: train batches split by layout count, MILP batches by
+    configuration list); context setup excluded, like the reference's input loading. The
+    reference's own schedule() on one host core for the configs it can finish (plans compared
+    field by field); the C4 plan is compared with the C restatement's whole-schedule fixture."""
     from common import problem as load
     from oracles import Ref, ref_available
 
@@ -526,13 +528,14 @@ def time_to_best_plan(device, keys=("c3_64gpu/eta=1", "c4_256gpu/eta=2", "c5_102
     for key in keys:
         name, eta = key.split("/eta=")
         prob = load(name)
-        with Engine(prob, device=device) as eng:  # warm-up run: CUDA module load, first allocations
+        kw = {"devices": list(devices)} if len(devices) > 1 else {"device": devices[0]}
+        with Engine(prob, **kw) as eng:  # warm-up run: CUDA module load, first allocations
             eng.schedule(eta=int(eta), seed=4276115)
-        with Engine(prob, device=device) as eng:
+        with Engine(prob, **kw) as eng:
             t = time.perf_counter()
             plan, _ = eng.schedule(eta=int(eta), seed=4276115)
             b200_s = time.perf_counter() - t
-        row = {"b200_s": b200_s, "window": plan["window_steps"],
+        row = {"b200_s": b200_s, "gpus": len(devices), "window": plan["window_steps"],
                "objective": max(plan["costs"]["train_s"], plan["costs"]["infer_total_s"])}
         if name in ("c1_desk_mixed", "c2_16gpu", "c3_64gpu") and ref_available():
             t = time.perf_counter()
@@ -542,7 +545,12 @@ def time_to_best_plan(device, keys=("c3_64gpu/eta=1", "c4_256gpu/eta=2", "c5_102
                 ref.pop(k, None)
             row["plan_identical"] = ref == plan
         elif name == "c4_256gpu":
+            from common import golden
             row["reference_cpu_s"] = "did not finish in 25 min (SURVEY.md 6)"
+            g = golden("schedule_c4_oracle.json")["c4_256gpu/eta=2"]
+            row["plan_identical_to_c_restatement"] = plan == {
+                k: v for k, v in g.items() if k not in ("trace", "evaluated_partitions", "oracle_seconds")}
+            row["c_restatement_cpu_s"] = g["oracle_seconds"]
         elif name == "c5_1024gpu":
             row["reference_cpu_s"] = "infeasible: materialises 4.3e11 layouts per pass (SURVEY.md 8a A5)"
         out[key] = row

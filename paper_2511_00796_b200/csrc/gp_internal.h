@@ -58,6 +58,8 @@ constexpr long long kSlowQueue = 1 << 21;  // deferred generic candidates per sc
 constexpr double kActBytes = 2.0;   // src/cost_model.cpp:10
 constexpr int kMaxPerRun = 4;       // K1 kernel instantiations support <= 4 blocks per type run
 constexpr long long kFanoutMinLayouts = 20000000;  // below this a search stays on one GPU
+constexpr long long kBatchSplitMinLayouts = 1000000000;  // a train batch below this stays on one GPU
+constexpr long long kMilpSplitMinStates = 20000000;      // a MILP batch below this stays on one GPU
 
 // Derived workload/calibration scalars, computed on the host exactly as the
 // reference's inline accessors do (inc/workload.hpp:51-58) and passed by value.

@@ -1263,7 +1263,14 @@ int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs,
                int dims, const double* Bs, double len, gp_rollout_result* outs, gp_rollout_entry* const* entries,
                int* rcs) {
   const int D = 1 + (int)ctx->peers.size();
-  if (D == 1 || q < 2) return milp_batch_one(ctx, q, cfgs, ncs, caps, dims, Bs, len, outs, entries, rcs);
+  long long states = 0;  // (lattice states of the batch: small batches stay on one device)
+  for (int i = 0; i < q && states < kMilpSplitMinStates; ++i) {
+    long long st = 1;
+    for (int t = 0; t < dims; ++t) st *= caps[i][t] + 1;
+    states += st;
+  }
+  if (D == 1 || q < 2 || states < kMilpSplitMinStates)
+    return milp_batch_one(ctx, q, cfgs, ncs, caps, dims, Bs, len, outs, entries, rcs);
   std::vector<std::vector<int>> part(D);
   for (int i = 0; i < q; ++i) {
     const std::vector<unsigned char> sig = milp_sig(cfgs[i], ncs[i], dims);

@@ -1034,6 +1034,9 @@ constexpr int kK1Threads = 128;
 #ifndef GPV_CTAS
 #define GPV_CTAS 6   // K1-fast launch bounds: min CTAs per SM (6: 72 registers, 7 resident; 7: slower)
 #endif
+#ifndef GPV_DYN
+#define GPV_DYN 1    // K1-fast: prefix chunks handed out by an atomic counter (finer, balanced)
+#endif
 #ifndef GPV_GS
 #define GPV_GS 4     // lanes per promotion count in the per-prefix tables
 #endif
@@ -1454,6 +1457,7 @@ struct ScanRange {
   long long n_pref;                  // prefixes touched
   long long chunk;                   // prefixes per warp work item
   int defer_all;                     // test hook (GPLAN_K1_DEFER_ALL=1): K1-fast defers every candidate
+  unsigned long long* work;          // K1-fast: next work item (zeroed per launch)
   double* dump;                      // test hook (DUMP instantiations): per_step of rank r in
   long long dump_lo, dump_hi;        //   [dump_lo, dump_hi) at dump[r - dump_lo]
 };
@@ -1619,7 +1623,12 @@ __global__ void __launch_bounds__(kK1Threads, GPV_CTAS) k1_layout_scan_fast(Trai
     F.mbuf = 0;
   }
   __syncthreads();
+  #if GPV_DYN
+  // the first item of each warp by its index, the next ones from the shared counter
+  for (long long it = warp; it < n_items;) {
+#else
   for (long long it = warp; it < n_items; it += n_warps) {
+#endif
     long long p = rg.p_lo + it * rg.chunk;
     const long long p_end = min(p + rg.chunk, rg.p_lo + rg.n_pref);
     __syncwarp();
@@ -1798,6 +1807,11 @@ __global__ void __launch_bounds__(kK1Threads, GPV_CTAS) k1_layout_scan_fast(Trai
       __syncwarp();
       if (lane == 0 && p + 1 < p_end) prefix_advance<R>(sp, P);
     }
+#if GPV_DYN
+    unsigned long long nx = 0;
+    if (lane == 0) nx = (unsigned long long)n_warps + atomicAdd(rg.work, 1ULL);
+    it = (long long)__shfl_sync(0xffffffffu, nx, 0);
+#endif
   }
   cp_async_wait_all();  // (a last middle-row prefetch may still be in flight)
   n_tab = __reduce_add_sync(0xffffffffu, n_tab);
@@ -2253,7 +2267,8 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   });
   const int occ = occ_tab[fast ? 1 : 0][R];
   const long long warps_total = (long long)ctx->num_sms * occ * (threads / 32);
-  rg.chunk = std::max(1LL, rg.n_pref / (warps_total * 6));
+  rg.chunk = std::max(1LL, rg.n_pref / (warps_total * (fast && GPV_DYN ? 24 : 6)));
+  rg.work = slow_q ? slow_q + 1 + kSlowQueue : nullptr;
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
   long long blocks = (n_items + (threads / 32) - 1) / (threads / 32);
   blocks = std::max(1LL, std::min(blocks, std::min((long long)max_blocks, (long long)ctx->num_sms * occ)));
@@ -2262,6 +2277,7 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   if (sc.hi > sc.lo) {
     if (fast) {
       GP_CUDA(cudaMemsetAsync(slow_q, 0, sizeof(unsigned long long), stream));
+      GP_CUDA(cudaMemsetAsync(slow_q + 1 + kSlowQueue, 0, sizeof(unsigned long long), stream));
       if (sc.dump) {
         k1_layout_scan_fast<R, true><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, L, rg, partial, slow_q);
         k1_deferred<R, true><<<kDeferBlocks, threads, 0, stream>>>(h.sp, tb, blkf, L, slow_q, partial + blocks, rg);
@@ -2684,7 +2700,7 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
                     h.sp.nc[R - 1] + 2 <= kMaxJunction && !force_generic && !(generic_env && generic_env[0] == '1');
   if (used_fast) *used_fast = fast;
   unsigned long long*& slow_q = lane < 0 ? ctx->d_slow : ctx->d_slow_lane[lane];
-  if (fast && !slow_q) GP_CUDA(cudaMalloc(&slow_q, sizeof(unsigned long long) * (1 + kSlowQueue)));
+  if (fast && !slow_q) GP_CUDA(cudaMalloc(&slow_q, sizeof(unsigned long long) * (2 + kSlowQueue)));
   if (timing) GP_CUDA(cudaEventRecord(ctx->ev[0], stream));
   // ---- K2: per-train-set tables
   k2a_block_stats<<<h.nblk, 256, 0, stream>>>(P.d_ordered, P.d_meta, P.d_pos, tb, P.d_blk, ctx->d_type,
@@ -3149,11 +3165,17 @@ int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_
       sz[j] = {(long long)total, j};
     }
     std::sort(sz.begin(), sz.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
-    std::vector<long long> load(D, 0);
-    for (const auto& e : sz) {
-      const int d = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-      dev_of[e.second] = d;
-      load[d] += e.first + 100000;  // + per-set fixed cost
+    long long all = 0;
+    for (const auto& e : sz) all += e.first;
+    // a batch worth well under a millisecond of scanning stays on one device: the per-device
+    // threads, uploads and synchronisations would cost more than they save
+    if (all >= kBatchSplitMinLayouts) {
+      std::vector<long long> load(D, 0);
+      for (const auto& e : sz) {
+        const int d = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        dev_of[e.second] = d;
+        load[d] += e.first + 100000;  // + per-set fixed cost
+      }
     }
   }
   std::vector<int> rcs(D, GP_OK);
