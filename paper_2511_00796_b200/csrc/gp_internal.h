@@ -163,11 +163,11 @@ struct TrainTables {
   // fast path (constant allocation total), structure-of-arrays over the suffix choices so
   // that a warp's 32 consecutive choices are read with coalesced loads (k2f_suffix_fast):
   const double2* blk_sh;  // [nblk] per block (remainder, floor) of its layer share
-  const int4* sf_hot;     // [n_suf] floor sum, k | b1 << 16, run-local block ids of the stages in
-                          //   remainder order (desc, stage order among equals), 16 bits each
-  const int2* sf_zb;      // [n_suf] zero-layer stage count at promotion b = 0..3 (bytes),
-                          //   b = 4 (byte 0) | stage-would-exceed-L mask << 8
-  const double* sf_t;     // [n_suf][4] internal stage-transfer terms (t0, t1, t2, 0)
+  const int4* sf_hot;     // [n_suf] floor sum; zero-layer stage count at promotion b = 4 | k << 8 |
+                          //   junction byte offset << 16; run-local block ids of the stages in
+                          //   remainder order (desc, stage order among equals), one byte each
+                          //   (255: none); zero-layer stage counts at b = 0..3, one byte each
+  const double* sf_t;     // internal stage-transfer terms: (t0, t1)[n_suf] as double2, then t2[n_suf]
   const signed char* sf_ms;  // [n_suf][kMsStride]: largest layer count at (b, d donations), -1: none
   const double2* sf_st;   // [5 * (kDonations + 1)][n_suf]: (max total, max compute) at (b, d)
   const int* nzs_max;     // suffix stats: [0] most zero-layer stages of any suffix choice,

@@ -933,9 +933,15 @@ __global__ void k2m_middle_rows(const SufEnt* __restrict__ mch, int n, const dou
 // Per suffix choice: the fast-path tables (TrainTables::sf_*) and, per promotion count b and
 // donation count d, the (max total, max compute) of its stages — zero-layer stages counted
 // with the one layer the fix-up gives them, donors with the layers they keep.
+constexpr int kMaxLastBlocks = 256;  // per-warp rank-count bytes; the fast path takes <= 255 last-run blocks (else generic K1)
+// suffix stage slots past k point at this rank-count entry, which holds kSentinelCount: its
+// promotion test (count + j < extra) never holds, so the scan needs no per-suffix slot mask
+constexpr int kSentinelBlock = 255;  // (byte ids: the fast path takes <= 255 last-run blocks)
+constexpr unsigned kSentinelCount = 124;  // + j + 1 <= 128 for j <= 3: no borrow between bytes
+
 __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const double2* __restrict__ blk_sh,
                                 const double2* __restrict__ stage, int L, int blk_off_last,
-                                int4* __restrict__ sf_hot, int2* __restrict__ sf_zb, double* __restrict__ sf_t,
+                                int4* __restrict__ sf_hot, double* __restrict__ sf_t,
                                 signed char* __restrict__ sf_ms, double2* __restrict__ sf_st,
                                 int* __restrict__ nzs_max) {
   constexpr int DM = kDonations;
@@ -956,7 +962,7 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
     }
   }
   int fs = 0;
-  int rbs[4] = {0, 0, 0, 0};
+  int rbs[4] = {kSentinelBlock, kSentinelBlock, kSentinelBlock, kSentinelBlock};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     rk[j] = 0;
@@ -966,10 +972,8 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
     fs += fl[j];
   }
   for (int j = 0; j < k; ++j) rbs[rk[j]] = e.bi[j] - blk_off_last;
-  sf_hot[i] = make_int4(fs, k | (e.b1 << 16), rbs[0] | (rbs[1] << 16), rbs[2] | (rbs[3] << 16));
-#pragma unroll
-  for (int j = 0; j < 3; ++j) sf_t[(size_t)i * 4 + j] = e.t[j];
-  sf_t[(size_t)i * 4 + 3] = 0.0;
+  reinterpret_cast<double2*>(sf_t)[i] = make_double2(e.t[0], e.t[1]);  // plane (t0, t1)[n]
+  sf_t[2 * (size_t)n + i] = e.t[2];                                     // plane t2[n]
   unsigned nzs = 0, nz4 = 0, bad = 0;
   for (int b = 0; b <= 4; ++b) {
     int lay[4];
@@ -1012,7 +1016,11 @@ __global__ void k2f_suffix_fast(const SufEnt* __restrict__ suf, int n, const dou
         if (live && j == jm) lay[j]--;
     }
   }
-  sf_zb[i] = make_int2((int)nzs, (int)(nz4 | (bad << 8)));
+  // (fs, nz4 | k << 8 | junction byte offset << 16, stage block ids in remainder order as bytes,
+  // zero-layer counts at b = 0..3 as bytes): with nz4 as byte 4, byte b of {y:w} is one PRMT
+  (void)bad;
+  sf_hot[i] = make_int4(fs, (int)nz4 | (k << 8) | ((e.b1 * 8) << 16),
+                        rbs[0] | (rbs[1] << 8) | (rbs[2] << 16) | (rbs[3] << 24), (int)nzs);
   int zmax = (int)nz4;
 #pragma unroll
   for (int b = 0; b < 4; ++b) zmax = max(zmax, (int)((nzs >> (8 * b)) & 0xff));
@@ -1040,22 +1048,12 @@ constexpr int kK1Threads = 128;
 #ifndef GPV_GS
 #define GPV_GS 4     // lanes per promotion count in the per-prefix tables
 #endif
-#ifndef GPV_FC
-#define GPV_FC 0     // 1: 32-bit per-prefix feasible counter (measured +0.1 ms: off)
-#endif
-#ifndef GPV_NM
-#define GPV_NM 1     // 1: near-minimum test as one double compare against bits b0 + 2 (-0.27 ms)
-#endif
-#ifndef GPV_TR
-#define GPV_TR 1     // 1: suffix transfer terms added unconditionally (absent ones are exact zeros) (-0.9 ms)
-#endif
 #ifndef GPV_MERGE
 #define GPV_MERGE 1  // 1: zero-layer donors by the co-rank of the two donor sequences (no loop) (-0.4 ms)
 #endif
 constexpr int kZsTable = 128;  // > L on the fast path
 // (the per-warp tables are kept small: the K1-fast CTAs' shared memory decides how much of the
 // SM's 256 KB stays L1 for the suffix tables, which every candidate reads)
-constexpr int kMaxLastBlocks = 256;  // last type run blocks with a per-prefix rank count (else generic K1)
 
 // Warp-uniform fast-path data of one prefix (shared memory): the tables the candidate loop
 // reads (pt, mp, nzp, fp, bad) and, for R >= 3, the FRONT runs' own tables (runs 0..R-3,
@@ -1104,9 +1102,10 @@ struct PrefixFast {
 // block's remainder among the prefix's (cntb) and the prefix's junction-transfer row (txs).
 constexpr int kMaxJunction = 32;  // nc_last + 2 (else generic K1)
 struct __align__(8) PrefixLast {
-  unsigned char cntb[kMaxLastBlocks];   // rank counts among all prefix remainders (merged)
-  unsigned char cntbf[kMaxLastBlocks];  // among the front's remainders only (rebuilt with the front)
+  unsigned char cntb[kMaxLastBlocks];      // rank counts among all prefix remainders (merged); [255]: sentinel
+  unsigned char cntbf[kMaxLastBlocks];     // among the front's remainders only (rebuilt with the front)
   double txs[kMaxJunction];
+  double fdk[8];                           // fill/drain coefficient of S = (prefix stages) + k stages
 };
 
 // number of entries >= x in the descending, -1-padded srt (x >= 0)
@@ -1394,8 +1393,8 @@ __device__ __forceinline__ void prefix_merge(int lane, const TrainSpace& sp, con
     const int dm = min(DM, nz + min(zs, nzs_max));
     if (d == 0) {
       F.nzp[a] = (unsigned char)nz;
-      if (((F.badf >> a0) | (M.bad >> a1)) & 1) atomicOr(&F.bad, 1 << a);
 #ifdef GP_DEBUG_CHECKS
+      if (((F.badf >> a0) | (M.bad >> a1)) & 1) atomicOr(&F.bad, 1 << a);
       F.dm[a] = dm;
 #endif
     }
@@ -1588,9 +1587,7 @@ __global__ void __launch_bounds__(kK1Threads, GPV_CTAS) k1_layout_scan_fast(Trai
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
   const int nsuf32 = sp.n_suf;
   long long b0 = kInfBits, k0 = LLONG_MAX, k1 = LLONG_MAX, k2 = LLONG_MAX, feasible = 0;
-#if GPV_NM
   double xthr = __longlong_as_double(kInfBits);  // per-step times above bits b0 + 2 cannot matter
-#endif
   unsigned n_tab = 0;
   __shared__ Prefix<R> sP[kK1Threads / 32];
   __shared__ PrefixData<R> sD[kK1Threads / 32];
@@ -1617,7 +1614,13 @@ __global__ void __launch_bounds__(kK1Threads, GPV_CTAS) k1_layout_scan_fast(Trai
     zst[t] = (unsigned char)min(z, 255);
   }
   const int nlast = e2 * (e2 - 1) / 2;
+  const int Lx = rg.defer_all ? -(1 << 20) : L;  // the test hook defers every candidate
+  double* const fdk = sL[threadIdx.x >> 5].fdk;
   if ((threadIdx.x & 31) == 0) {
+    // (per-prefix writes stop below the sentinel, or, with 249..255 blocks, add the middle
+    // row's zero padding byte to the front's sentinel)
+    cntb[kSentinelBlock] = (unsigned char)kSentinelCount;
+    sL[threadIdx.x >> 5].cntbf[kSentinelBlock] = (unsigned char)kSentinelCount;
     F.fkey = -1;
     F.mrow_c[0] = F.mrow_c[1] = -1;
     F.mbuf = 0;
@@ -1649,7 +1652,10 @@ __global__ void __launch_bounds__(kK1Threads, GPV_CTAS) k1_layout_scan_fast(Trai
         prefix_merge<R>(lane, sp, tb, L, sstat, P, D, F, sL[threadIdx.x >> 5], zst, nlast);
       }
       const int kp = D.u;
+      if (lane < 8) fdk[lane] = fd[min(kp + lane, GP_MAX_STAGES)];
+      __syncwarp();
       const int fp = F.fp, pbad = F.bad;
+      (void)pbad;  // (read by the debug checks)
       const double dtr = D.transfers;
       const long long ns = sp.cnt[R - 1][kp];
       const long long pbase = P.base;  // keys are ranks: base of the prefix + suffix index
@@ -1657,42 +1663,39 @@ __global__ void __launch_bounds__(kK1Threads, GPV_CTAS) k1_layout_scan_fast(Trai
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
       // table-scored count: every candidate of this lane, less the deferred ones (below)
       if (s0 + lane < s1) n_tab += (unsigned)((s1 - s0 - lane + 31) >> 5);
-#if GPV_FC
-      unsigned fc = 0;
-#endif
 #pragma unroll 2  // (with 6 CTAs/SM: two candidates in flight per lane, measured +10%)
-      for (int s = (int)s0 + lane; s < (int)s1; s += 32) {  // (suffix indices fit 32 bits)
-        const int4 A = __ldg(tb.sf_hot + s);  // fs, k|b1, rb01, rb23
-        const int2 B = __ldg(tb.sf_zb + s);   // nzs0123, nzs4|bad
-        const int fk = A.y & 0xffff;
+      for (unsigned s = (unsigned)s0 + lane; s < (unsigned)s1; s += 32) {  // (suffix indices fit 32 bits)
+        const int4 A = __ldg(tb.sf_hot + s);  // fs, nz4 | k << 8 | 8*b1 << 16, rb0..3, nzs0..3
+        const int fk = (int)__byte_perm((unsigned)A.y, 0u, 0x4441);
         const int S = kp + fk;
-        const int extra = L - (fp + A.x);
-        bool slow = (unsigned)extra >= (unsigned)S || rg.defer_all;
+        const int extra = Lx - (fp + A.x);
+        bool slow = (unsigned)extra >= (unsigned)S;  // (always under defer_all: Lx < 0)
         int a = 0, b = 0, dP = 0, dS = 0;
         if (!slow) {
-          if (R > 1) {  // branch-free: unused stage slots hold block 0 and are masked
+          if (R > 1) {  // branch-free: unused stage slots read the sentinel count
             // b = #{j < fk : cntb[rb_j] + j < extra}, the four tests as one byte-wise
             // subtraction: byte j of (extra + 128) - (cntb[rb_j] + j + 1) keeps bit 7 iff the
             // test holds (both sides < 128, so no borrow crosses a byte)
-            GP_CHECK((A.z & 0xffff) < kMaxLastBlocks && ((unsigned)A.z >> 16) < kMaxLastBlocks &&
-                     (A.w & 0xffff) < kMaxLastBlocks && ((unsigned)A.w >> 16) < kMaxLastBlocks);
-            const unsigned c0 = cntb[A.z & 0xffff], c1 = cntb[(unsigned)A.z >> 16];
-            const unsigned c2 = cntb[A.w & 0xffff], c3 = cntb[(unsigned)A.w >> 16];
+            // (bytes 1, 2 zero-extended by PRMT with a zero operand: one instruction each)
+            const unsigned c0 = cntb[A.z & 0xff], c1 = cntb[__byte_perm((unsigned)A.z, 0u, 0x4441)];
+            const unsigned c2 = cntb[__byte_perm((unsigned)A.z, 0u, 0x4442)], c3 = cntb[(unsigned)A.z >> 24];
             const unsigned w = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410) +
                                0x04030201u;  // bytes (c0, c1, c2, c3), each < 128
             const unsigned ge = ((unsigned)extra * 0x01010101u + 0x80808080u) - w;
-            b = __popc(ge & (0x80808080u >> (32 - 8 * fk)));
+            b = __popc(ge & 0x80808080u);  // (slots j >= fk read the sentinel count)
           } else {
             b = extra;
           }
           a = extra - b;
-          slow = ((pbad >> a) | (B.y >> (8 + b))) & 1;
-          // byte b of the 40-bit zero-count word {B.y:B.x} (b <= 4): one PRMT
+          // (no stage can exceed L layers here: every floor is <= L - extra, so the tables'
+          // over-L bits are never set for a candidate's own promotion counts)
+          GP_CHECK(!((pbad >> a) & 1));
+          // byte b of the 40-bit zero-count word {A.y:A.w} (b <= 4): one PRMT
 #ifdef GP_DEBUG_CHECKS
           GP_CHECK(b >= 0 && b <= 4 && b <= fk);
           if (!slow) GP_CHECK(a >= F.a_lo && a <= F.a_hi);  // the candidate's promotion count was tabulated
 #endif
-          const int nz = F.nzp[a] + (int)(__byte_perm((unsigned)B.x, (unsigned)B.y, (unsigned)b) & 0xff);
+          const int nz = F.nzp[a] + (int)(__byte_perm((unsigned)A.w, (unsigned)A.y, (unsigned)b) & 0xff);
           if (nz > kDonations) slow = true;
           // zero-layer fix-up: each donation comes from the side holding the first maximum
           // (the prefix on ties: its stages come first); a donor must keep >= 1 layer
@@ -1737,73 +1740,47 @@ __global__ void __launch_bounds__(kK1Threads, GPV_CTAS) k1_layout_scan_fast(Trai
           const unsigned long long at = atomicAdd(slow_q, 1ULL);
           if (at < (unsigned long long)kSlowQueue) slow_q[1 + at] = (unsigned long long)key;
           --n_tab;
-          continue;
-        }
+        } else {  // (no early exits: a flat if/else keeps the loop's reconvergence cheap)
 #ifdef GP_DEBUG_CHECKS
-        GP_CHECK(dP >= 0 && dP <= F.dm[a] && dS >= 0 && dS <= kDonations && S <= GP_MAX_STAGES);
+          GP_CHECK(dP >= 0 && dP <= F.dm[a] && dS >= 0 && dS <= kDonations && S <= GP_MAX_STAGES);
 #endif
-        const double2 pa = F.pt[a][dP];
-        const double2 sb = tb.sf_st[(b * (kDonations + 1) + dS) * nsuf32 + s];
-        double mt = pa.x, mc = pa.y;
-        if (sb.x > mt) mt = sb.x;
-        if (sb.y > mc) mc = sb.y;
-        if (!(mt < __longlong_as_double(0x7ff0000000000000LL))) {  // memory-infeasible
-          if (DUMP && pbase + s >= rg.dump_lo && pbase + s < rg.dump_hi) rg.dump[pbase + s - rg.dump_lo] = mt;
-          continue;
-        }
-        double tr = dtr;
-        GP_CHECK(((A.y >> 16) & 0xffff) < kMaxJunction);
-        if (R > 1) tr += txs[(A.y >> 16) & 0xffff];
-#if GPV_TR
-        {  // internal transfers of the suffix, [s][4] (t0, t1, t2, 0): absent terms are 0.0
-          const double2 t01 = __ldg(reinterpret_cast<const double2*>(tb.sf_t) + 2 * s);
-          tr += t01.x;
-          tr += t01.y;
-          tr += __ldg(tb.sf_t + 4 * s + 2);
-        }
-#else
-        if (fk > 1) {  // internal transfers of the suffix, [s][4] (t0, t1, t2, 0)
-          const double2 t01 = __ldg(reinterpret_cast<const double2*>(tb.sf_t) + 2 * s);
-          tr += t01.x;
-          if (fk > 2) {
+          const double2 pa = F.pt[a][dP];
+          const double2 sb = tb.sf_st[(b * (kDonations + 1) + dS) * nsuf32 + s];
+          double mt = pa.x, mc = pa.y;
+          if (sb.x > mt) mt = sb.x;
+          if (sb.y > mc) mc = sb.y;
+          if (mt < __longlong_as_double(0x7ff0000000000000LL)) {  // else memory-infeasible
+            double tr = dtr;
+            GP_CHECK(((unsigned)A.y >> 16) < 8 * kMaxJunction);
+            if (R > 1) tr += *reinterpret_cast<const double*>(reinterpret_cast<const char*>(txs) + ((unsigned)A.y >> 16));
+            // internal transfers of the suffix (t0, t1 | t2 planes, coalesced): absent terms are 0.0
+            const double2 t01 = __ldg(reinterpret_cast<const double2*>(tb.sf_t) + s);
+            tr += t01.x;
             tr += t01.y;
-            if (fk > 3) tr += __ldg(tb.sf_t + 4 * s + 2);
-          }
-        }
-#endif
-        const double x = mt + fd[S] * mc + tr;
-        if (DUMP && pbase + s >= rg.dump_lo && pbase + s < rg.dump_hi) rg.dump[pbase + s - rg.dump_lo] = x;
-#if GPV_FC
-        ++fc;
-#else
-        ++feasible;
-#endif
-#if GPV_NM
-        if (x <= xthr) {  // within two ulps of the smallest so far (the key is formed only here)
-          const long long d = __double_as_longlong(x) - b0;
-#else
-        const long long d = __double_as_longlong(x) - b0;
-        if (d < 3) {  // (the key is formed only here and on the deferred path)
-#endif
-          const long long key = pbase + s;
-          if (d < 0) {
-            k2 = d == -1 ? k1 : d == -2 ? k0 : LLONG_MAX;
-            k1 = d == -1 ? k0 : LLONG_MAX;
-            k0 = key;
-            b0 += d;
-#if GPV_NM
-            xthr = __longlong_as_double(b0 + 2);
-#endif
-          } else if (d == 1) {
-            k1 = min(k1, key);
-          } else if (d == 2) {
-            k2 = min(k2, key);
+            tr += __ldg(tb.sf_t + (2u * (unsigned)nsuf32 + s));
+            const double x = mt + fdk[fk] * mc + tr;  // fd[S], S = kp + fk
+            if (DUMP && pbase + s >= rg.dump_lo && pbase + s < rg.dump_hi) rg.dump[pbase + s - rg.dump_lo] = x;
+            ++feasible;
+            if (x <= xthr) {  // within two ulps of the smallest so far (the key is formed only here)
+              const long long d = __double_as_longlong(x) - b0;
+              const long long key = pbase + s;
+              if (d < 0) {
+                k2 = d == -1 ? k1 : d == -2 ? k0 : LLONG_MAX;
+                k1 = d == -1 ? k0 : LLONG_MAX;
+                k0 = key;
+                b0 += d;
+                xthr = __longlong_as_double(b0 + 2);
+              } else if (d == 1) {
+                k1 = min(k1, key);
+              } else if (d == 2) {
+                k2 = min(k2, key);
+              }
+            }
+          } else if (DUMP && pbase + s >= rg.dump_lo && pbase + s < rg.dump_hi) {
+            rg.dump[pbase + s - rg.dump_lo] = mt;
           }
         }
       }
-#if GPV_FC
-      feasible += fc;
-#endif
       __syncwarp();
       if (lane == 0 && p + 1 < p_end) prefix_advance<R>(sp, P);
     }
@@ -2478,7 +2455,6 @@ struct PreparedTrain {
   SufEnt* d_suf = nullptr;
   double2* d_blk_sh = nullptr;
   int4* d_sf_hot = nullptr;
-  int2* d_sf_zb = nullptr;
   double* d_sf_t = nullptr;
   signed char* d_sf_ms = nullptr;
   double2* d_sf_st = nullptr;
@@ -2568,7 +2544,6 @@ static size_t table_bytes(const HostSpace& h, int L, int max_blocks) {
   add(sizeof(double2) * h.nblk);
   const size_t nsf = h.choices.size() + 1;
   add(sizeof(int4) * nsf);
-  add(sizeof(int2) * nsf);
   add(sizeof(double) * 4 * nsf);
   add((size_t)kMsStride * nsf);
   add(sizeof(double2) * 5 * (kDonations + 1) * nsf);
@@ -2618,7 +2593,6 @@ static void carve_prepared(PreparedTrain& P, char*& in, char*& tab, char* in_bas
   P.d_blk_sh = carve<double2>(tab, h.nblk);
   const size_t nsf = h.choices.size() + 1;
   P.d_sf_hot = carve<int4>(tab, nsf);
-  P.d_sf_zb = carve<int2>(tab, nsf);
   P.d_sf_t = carve<double>(tab, 4 * nsf);
   P.d_sf_ms = carve<signed char>(tab, (size_t)kMsStride * nsf);
   P.d_sf_st = carve<double2>(tab, 5 * (kDonations + 1) * nsf);
@@ -2661,7 +2635,6 @@ static TrainTables prepared_tables(const gp_ctx* ctx, const PreparedTrain& P) {
   tb.suf = P.d_suf;
   tb.blk_sh = P.d_blk_sh;
   tb.sf_hot = P.d_sf_hot;
-  tb.sf_zb = P.d_sf_zb;
   tb.sf_t = P.d_sf_t;
   tb.sf_ms = P.d_sf_ms;
   tb.sf_st = P.d_sf_st;
@@ -2696,7 +2669,7 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   // (layer counts are tabulated as signed bytes: L <= 127; small spaces: the generic scan —
   // the fast path's extra table launches would dominate)
   const int nlast = (h.sp.nc[R - 1] + 2) * (h.sp.nc[R - 1] + 1) / 2;
-  const bool fast = h.exact_total && h.total >= (1LL << 20) && L <= 127 && nlast <= kMaxLastBlocks &&
+  const bool fast = h.exact_total && h.total >= (1LL << 20) && L <= 127 && nlast <= kSentinelBlock &&
                     h.sp.nc[R - 1] + 2 <= kMaxJunction && !force_generic && !(generic_env && generic_env[0] == '1');
   if (used_fast) *used_fast = fast;
   unsigned long long*& slow_q = lane < 0 ? ctx->d_slow : ctx->d_slow_lane[lane];
@@ -2726,7 +2699,7 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
       k2e_block_shares<<<(h.nblk + 255) / 256, 256, 0, stream>>>(P.d_blkf, h.nblk, h.flops_total, P.d_blk_sh);
       GP_CUDA(cudaMemsetAsync(P.d_nzs_max, 0, (3 + 5 * (L + 1)) * sizeof(int), stream));
       k2f_suffix_fast<<<(ns + 127) / 128, 128, 0, stream>>>(P.d_suf, ns, P.d_blk_sh, P.d_stage, L,
-                                                           h.sp.blk_off[R - 1], P.d_sf_hot, P.d_sf_zb,
+                                                           h.sp.blk_off[R - 1], P.d_sf_hot,
                                                            P.d_sf_t, P.d_sf_ms, P.d_sf_st, P.d_nzs_max);
       if (R >= 2) {  // the middle run's rows (K2d on run R - 2, then K2m)
         const int nm = (int)h.choices_m.size();
