@@ -5,19 +5,25 @@
 //
 // K5a units      unit folds (flops, hbm, internal link, cross matrix) — one CTA per unit row
 // K5b exact      one thread per bisection mask (n <= exact_threshold)
-// K5c restarts   one CTA per restart: SplitMix64-perturbed order (counter-based,
-//                parallel), CTA-wide stable sort, greedy seed, then the whole
-//                steepest-ascent loop on chip: every step scores all moves and all
-//                (train, rollout) swaps in parallel and reduces lexicographically on
-//                (gain desc, scan position asc) — the reference's first strict max.
+// K5c restarts   one thread-block cluster per restart (1..8 CTAs, as many as fill the
+//                GPU): SplitMix64-perturbed order (counter-based, parallel), CTA-wide
+//                stable sort, greedy seed, then the whole steepest-ascent loop on chip:
+//                every step scores all moves and all (train, rollout) swaps in parallel
+//                — the cluster's CTAs hold identical replicated state and each scores its
+//                share of the rows — and reduces lexicographically on (gain desc, scan
+//                position asc), the reference's first strict max, through distributed
+//                shared memory (one cluster barrier per step).
 // K5d topk       one thread replays TopK::offer in the reference's offer order.
 // Objective/fraction divisions by the fixed totals use a correctly rounded
 // reciprocal with one FMA residual correction (Markstein), identical to IEEE
 // division for these operands; every other fp operation keeps reference order.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "gp_internal.h"
 
@@ -212,14 +218,17 @@ struct SState {
   int n_tr, n_ro;
 };
 
-// One CTA per (band, restart): blockIdx.x = band * restarts + r (a scheduler iteration's
-// bands run in one launch); band b's limits are bands[b] = (lo, hi).
+// One cluster of csize CTAs per (band, restart): blockIdx.x / csize = band * restarts + r (a
+// scheduler iteration's bands run in one launch); band b's limits are bands[b] = (lo, hi).
+// Every CTA of a cluster runs the same seed and applies the same steps (replicated state);
+// the step scan is split by CTA rank and the winner is the lexicographic best of the CTAs'
+// winners, so the result is independent of csize (csize == 1: no cluster operations).
 __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* __restrict__ tot,
                                                          const double* __restrict__ base_score,
                                                          const double2* __restrict__ bands, int restarts,
                                                          unsigned long long seed,
                                                          unsigned char* __restrict__ in_train_out,
-                                                         RestartOut* __restrict__ out) {
+                                                         RestartOut* __restrict__ out, int csize) {
   extern __shared__ unsigned char smem[];
   const int n = u.n;
   double* ltt = reinterpret_cast<double*>(smem);
@@ -234,8 +243,10 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
   __shared__ SState S;
   __shared__ Cand red[32];
   __shared__ int ired[32];
-  const int r = blockIdx.x % restarts;
-  const double lo = bands[blockIdx.x / restarts].x, hi = bands[blockIdx.x / restarts].y;
+  __shared__ Cand cbest[2];  // this CTA's step winner (by step parity), read by the cluster
+  const int crank = blockIdx.x % csize, rid = blockIdx.x / csize;
+  const int r = rid % restarts;
+  const double lo = bands[rid / restarts].x, hi = bands[rid / restarts].y;
   const Totals T = *tot;
   const int tid = threadIdx.x, nth = blockDim.x;
 
@@ -376,6 +387,7 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
 
   // ---- steepest ascent (src/partition.cpp:302-347)
   unsigned long long steps = 0;
+  int par = 0;
   while (ok) {
     // ascending train / rollout unit lists (scan order of the swap loops)
     if (tid < 32) {
@@ -401,7 +413,7 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
     const double cur = (T.link > 0 ? div_rn_recip2(lt0, T.link, T.y_link) : 0) +
                        div_rn_recip2(T.hbm - hb0, T.hbm, T.y_hbm);
     Cand best{1e-12, INT_MAX};
-    for (int i = tid; i < n; i += nth) {  // single moves
+    for (int i = crank * nth + tid; i < n; i += nth * csize) {  // single moves (this CTA's share)
       const bool to_train = !in_tr[i];
       if (to_train && cnt + 1 == n) continue;
       if (!to_train && cnt == 1) continue;
@@ -422,7 +434,7 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
     for (int i = tid; i < n; i += nth) lb[i] = ltt[i] + ui[i];
     __syncthreads();
     const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
-    for (int ia = warp; ia < ntr; ia += nwarps) {
+    for (int ia = crank * nwarps + warp; ia < ntr; ia += nwarps * csize) {
       const int a = tr[ia];
       const double Fa = ft0 - uf[a];  // (flops_train - f[a]) + f[b]
       const double Xa = lt0 - lb[a];  // ((link_train - (ltt[a]+int[a])) + (ltt[b]+int[b])) - cross
@@ -439,7 +451,24 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
         if (c.gain > best.gain) best = c;
       }
     }
-    const Cand w = block_best(best, red);
+    Cand w = block_best(best, red);
+    if (csize > 1) {  // the cluster's best: each warp reads the CTAs' winners (lane k: rank k)
+      cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+      if (tid == 0) cbest[par] = w;
+      cl.sync();  // (a CTA rewrites cbest[par] two steps later, after the next barrier)
+      Cand c{-1e300, INT_MAX};
+      if (lane < csize) c = *cl.map_shared_rank(&cbest[par], lane);
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        Cand d;
+        d.gain = __shfl_xor_sync(0xffffffffu, c.gain, o);
+        d.pos = __shfl_xor_sync(0xffffffffu, c.pos, o);
+        if (cand_better(d, c)) c = d;
+      }
+      w.gain = __shfl_sync(0xffffffffu, c.gain, 0);
+      w.pos = __shfl_sync(0xffffffffu, c.pos, 0);
+      par ^= 1;
+    }
     if (w.pos == INT_MAX) break;
     ++steps;
     if (w.pos < n) {
@@ -452,7 +481,9 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
     }
   }
   __syncthreads();
-  for (int i = tid; i < n; i += nth) in_train_out[(size_t)blockIdx.x * n + i] = ok ? in_tr[i] : 0;
+  if (csize > 1) cooperative_groups::this_cluster().sync();  // no CTA leaves while its cbest may be read
+  if (crank != 0) return;
+  for (int i = tid; i < n; i += nth) in_train_out[(size_t)rid * n + i] = ok ? in_tr[i] : 0;
   if (tid == 0) {
     RestartOut o;
     o.ok = ok;
@@ -460,7 +491,7 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
     o.steps = steps;
     o.obj = (T.link > 0 ? div_rn_recip2(S.link_train, T.link, T.y_link) : 0) +
             div_rn_recip2(T.hbm - S.hbm_train, T.hbm, T.y_hbm);
-    out[blockIdx.x] = o;
+    out[rid] = o;
   }
 }
 
@@ -829,8 +860,27 @@ int partition_candidates_batch(gp_ctx* ctx, int q, const gp_gamma* gs, const gp_
     const size_t sm = sizeof(double) * 5 * n + sizeof(int) * (3 * n + 2) + n + 64;
     if (sm > 227 * 1024) return set_error(GP_INVALID, "partition units exceed shared memory");
     GP_CUDA(cudaFuncSetAttribute(k5_restart, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k5_restart<<<q * o->restarts, kK5Threads, sm, ctx->stream>>>(u, d_tot, d_base, d_bands, o->restarts, o->seed,
-                                                                d_mask, d_rout);
+    // cluster size: CTAs per restart so that the launch fills the SMs once (one 1024-thread
+    // CTA per SM), at most 8 (portable); GPLAN_K5_CLUSTER=c forces c (tests)
+    const int n_rs = q * o->restarts;
+    int csize = 1;
+    while (csize < 8 && (long long)n_rs * csize * 2 <= ctx->num_sms) csize *= 2;
+    if (const char* e = std::getenv("GPLAN_K5_CLUSTER")) csize = std::max(1, std::min(8, std::atoi(e)));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)(n_rs * csize));
+    lc.blockDim = dim3(kK5Threads);
+    lc.dynamicSmemBytes = sm;
+    lc.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    GP_CUDA(cudaLaunchKernelEx(&lc, k5_restart, u, (const Totals*)d_tot, (const double*)d_base,
+                               (const double2*)d_bands, o->restarts, (unsigned long long)o->seed, d_mask, d_rout,
+                               csize));
     ctx->launches++;
   }
   GP_CUDA(cudaGetLastError());

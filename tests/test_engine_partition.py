@@ -71,3 +71,21 @@ def test_partition_objective():
         assert orc.lib.or_partition_objective(C.byref(orc.c), ids.ctypes.data_as(C.POINTER(C.c_int32)),
                                               len(ids), C.byref(o), C.byref(f)) == 0
         assert eng.partition_objective(train) == (o.value, f.value)
+
+
+@pytest.mark.parametrize("csize", [1, 2, 4, 8])
+@pytest.mark.parametrize("name", ["c4_256gpu", "c5_1024gpu"])
+def test_restart_cluster_sizes_agree(name, csize, monkeypatch):
+    """K5 runs a restart on a cluster of 1..8 CTAs (replicated state, split step scan, DSMEM
+    winner exchange): every cluster size gives the C restatement's candidates. Single-band
+    calls (what the schedule's later iterations make) default to 8-CTA clusters."""
+    import random
+    rng = random.Random(7 + csize)
+    orc = Oracle(problem(name))
+    monkeypatch.setenv("GPLAN_K5_CLUSTER", str(csize))
+    for _ in range(3 if name == "c5_1024gpu" else 6):
+        lo = 0.2 + rng.random() * 0.5
+        hi = lo + 0.02 + rng.random() * 0.1
+        seed = rng.randrange(1 << 40)
+        want = oracle_partitions(orc, lo, hi, seed=seed)
+        assert run(name, lo, hi, seed=seed) == want, (lo, hi, seed, csize)
