@@ -18,6 +18,8 @@
 // reciprocal with one FMA residual correction (Markstein), identical to IEEE
 // division for these operands; every other fp operation keeps reference order.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -736,9 +738,25 @@ void part_cache_free(gp_ctx* ctx) {
 // back to back, one synchronisation and one D2H for all bands. Band i's candidates go to
 // out[i * k ..] with their train ids at train_ids[i * k * N ..]; rcs[i] = GP_OK or
 // GP_BAND_INFEASIBLE.
+// GPLAN_PROFILE=1: partition calls, bands, wall time and k5_restart device time (stderr)
+namespace {
+struct PartStats {  // (contexts may be driven from several host threads: atomics)
+  std::atomic<long long> calls{0}, bands{0};
+  AtomicD wall_s, restart_ms;
+  ~PartStats() {
+    if (std::getenv("GPLAN_PROFILE"))
+      std::fprintf(stderr, "partition: %lld calls, %lld bands, %.3f s wall, k5_restart %.3f s\n", calls.load(),
+                   bands.load(), (double)wall_s, (double)restart_ms / 1e3);
+  }
+} g_part_stats;
+}  // namespace
+
 int partition_candidates_batch(gp_ctx* ctx, int q, const gp_gamma* gs, const gp_part_opts* o, int k,
                                gp_partition* out, int32_t* train_ids, int32_t* n_out, int* rcs) {
   const int N = ctx->N, M = ctx->M;
+  static const bool prof = std::getenv("GPLAN_PROFILE") != nullptr;
+  const auto t_call = std::chrono::steady_clock::now();
+  cudaEvent_t pe[2] = {nullptr, nullptr};
   for (int i = 0; i < q; ++i) {
     n_out[i] = 0;
     rcs[i] = GP_OK;
@@ -878,9 +896,15 @@ int partition_candidates_batch(gp_ctx* ctx, int q, const gp_gamma* gs, const gp_
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
+    if (prof) {
+      cudaEventCreate(&pe[0]);
+      cudaEventCreate(&pe[1]);
+      cudaEventRecord(pe[0], ctx->stream);
+    }
     GP_CUDA(cudaLaunchKernelEx(&lc, k5_restart, u, (const Totals*)d_tot, (const double*)d_base,
                                (const double2*)d_bands, o->restarts, (unsigned long long)o->seed, d_mask, d_rout,
                                csize));
+    if (prof) cudaEventRecord(pe[1], ctx->stream);
     ctx->launches++;
   }
   GP_CUDA(cudaGetLastError());
@@ -908,6 +932,18 @@ int partition_candidates_batch(gp_ctx* ctx, int q, const gp_gamma* gs, const gp_
   GP_CUDA(cudaMemcpyAsync(hp, d_res, out_band * q, cudaMemcpyDeviceToHost, ctx->stream));
   ctx->d2h_bytes += (long long)(out_band * q);
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (prof) {
+    g_part_stats.calls++;
+    g_part_stats.bands += q;
+    if (pe[0]) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pe[0], pe[1]);
+      g_part_stats.restart_ms += ms;
+      cudaEventDestroy(pe[0]);
+      cudaEventDestroy(pe[1]);
+    }
+    g_part_stats.wall_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_call).count();
+  }
   for (int b = 0; b < q; ++b) {
     const char* rb = hp + out_band * b;
     const TopKOut* htk = reinterpret_cast<const TopKOut*>(rb);
