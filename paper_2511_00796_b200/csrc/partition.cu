@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
   __shared__ Cand red[32];
   __shared__ int ired[32];
   __shared__ Cand cbest[2];  // this CTA's step winner (by step parity), read by the cluster
+  __shared__ int lc_t[32], lc_r[32];
   const int crank = blockIdx.x % csize, rid = blockIdx.x / csize;
   const int r = rid % restarts;
   const double lo = bands[rid / restarts].x, hi = bands[rid / restarts].y;
@@ -315,6 +316,33 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
       S.hbm_train -= uh[i];
       S.flops_train -= uf[i];
       S.count--;
+    }
+    __syncthreads();
+  };
+  // remove(a) then add(b) in one pass: every element sees the same two roundings in the same
+  // order (ltt[j] - cross[a][j], then + cross[b][j]), and the totals the same sequence
+  auto swap_units = [&](int a, int b) {
+    __syncthreads();
+    if (tid == 0) {
+      const double la = ltt[a] + ui[a];                                  // remove: ltt[a] is not updated
+      const double lb2 = (ltt[b] - u.cross[(size_t)a * n + b]) + ui[b];  // add: ltt[b] after the removal
+      S.link_train -= la;
+      S.link_train += lb2;
+      S.hbm_train -= uh[a];
+      S.hbm_train += uh[b];
+      S.flops_train -= uf[a];
+      S.flops_train += uf[b];
+      in_tr[a] = 0;
+      in_tr[b] = 1;
+    }
+    __syncthreads();  // (thread 0 read ltt[a], ltt[b] before the update)
+    const double* ca = u.cross + (size_t)a * n;
+    const double* cb = u.cross + (size_t)b * n;
+    for (int j = tid; j < n; j += nth) {
+      double v = ltt[j];
+      if (j != a) v -= ca[j];
+      if (j != b) v += cb[j];
+      ltt[j] = v;
     }
     __syncthreads();
   };
@@ -391,22 +419,43 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
   unsigned long long steps = 0;
   int par = 0;
   while (ok) {
-    // ascending train / rollout unit lists (scan order of the swap loops)
-    if (tid < 32) {
-      int ctr = 0, cro = 0;
-      for (int base = 0; base < n; base += 32) {
-        const int i = base + tid;
-        const bool t = i < n && in_tr[i];
-        const bool rr = i < n && !in_tr[i];
+    {  // ascending train / rollout unit lists (scan order of the swap loops): every warp
+       // ballots 32 units, a per-round warp prefix places them
+      const int l_ = tid & 31, w_ = tid >> 5, nw_ = nth >> 5;
+      int bt = 0, br = 0;
+      for (int b0 = 0; b0 < n; b0 += nth) {
+        const int i = b0 + tid;
+        const bool t = i < n && in_tr[i], rr = i < n && !in_tr[i];
         const unsigned mt = __ballot_sync(0xffffffffu, t), mr = __ballot_sync(0xffffffffu, rr);
-        if (t) tr[ctr + __popc(mt & ((1u << tid) - 1))] = i;
-        if (rr) ro[cro + __popc(mr & ((1u << tid) - 1))] = i;
-        ctr += __popc(mt);
-        cro += __popc(mr);
+        if (l_ == 0) {
+          lc_t[w_] = __popc(mt);
+          lc_r[w_] = __popc(mr);
+        }
+        __syncthreads();
+        int pt = 0, pr = 0, at = 0, ar = 0;  // this warp's exclusive offsets, the round's totals
+        if (l_ < nw_) {
+          at = lc_t[l_];
+          ar = lc_r[l_];
+          pt = l_ < w_ ? at : 0;
+          pr = l_ < w_ ? ar : 0;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          pt += __shfl_xor_sync(0xffffffffu, pt, o);
+          pr += __shfl_xor_sync(0xffffffffu, pr, o);
+          at += __shfl_xor_sync(0xffffffffu, at, o);
+          ar += __shfl_xor_sync(0xffffffffu, ar, o);
+        }
+        const unsigned below = (1u << l_) - 1u;
+        if (t) tr[bt + pt + __popc(mt & below)] = i;
+        if (rr) ro[br + pr + __popc(mr & below)] = i;
+        bt += at;
+        br += ar;
+        __syncthreads();  // (lc_t / lc_r are rewritten by the next round)
       }
       if (tid == 0) {
-        S.n_tr = ctr;
-        S.n_ro = cro;
+        S.n_tr = bt;
+        S.n_ro = br;
       }
     }
     __syncthreads();
@@ -478,8 +527,7 @@ __global__ void __launch_bounds__(kK5Threads) k5_restart(Units u, const Totals* 
       else add(w.pos);
     } else {
       const int a = (w.pos - n) / n, b = (w.pos - n) % n;
-      remove(a);
-      add(b);
+      swap_units(a, b);
     }
   }
   __syncthreads();

@@ -2955,6 +2955,23 @@ int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_tr
   return rc;
 }
 
+// fn(i) for i < n on up to 16 host threads (inline below 64 items)
+template <typename F>
+static void parallel_sets(int n, F fn) {
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int nt = std::min({16, hw, n / 32});
+  if (nt <= 1) {
+    for (int i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (int i = t; i < n; i += nt) fn(i);
+    });
+  for (auto& x : th) x.join();
+}
+
 // Batched constrained_search over many train sets (the scheduler's evaluation batches):
 // every set's inputs travel in ONE H2D copy, all tables + scans are enqueued back to back,
 // the results come back in ONE D2H copy with ONE synchronisation.
@@ -2974,16 +2991,28 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
     tick = t;
   };
   std::vector<PreparedTrain> Ps(n_sets);
-  size_t ib = 0, tbytes = 0;
-  for (int i = 0; i < n_sets; ++i) {
-    int rc = build_space(ctx, ids[i], ns[i], o, Ps[i].h);
-    if (rc) return rc;
-    Ps[i].mode = mode;
-    Ps[i].L = ctx->sc.L;
-    Ps[i].max_blocks = std::min(ctx->num_sms * 8, (int)std::max<long long>(1, Ps[i].h.total / 4096));
-    ib += input_bytes(Ps[i].h);
-    tbytes += table_bytes(Ps[i].h, Ps[i].L, Ps[i].max_blocks);
+  std::vector<size_t> in_at(n_sets + 1, 0), tab_at(n_sets + 1, 0);  // per-set carve offsets
+  {  // host enumeration of every set's space, on several host threads for large batches
+    std::vector<int> rcs(n_sets, GP_OK);
+    std::vector<std::string> errs(n_sets);
+    parallel_sets(n_sets, [&](int i) {
+      rcs[i] = build_space(ctx, ids[i], ns[i], o, Ps[i].h);
+      if (rcs[i]) {
+        errs[i] = gp_last_error();  // (the message is thread-local)
+        return;
+      }
+      Ps[i].mode = mode;
+      Ps[i].L = ctx->sc.L;
+      Ps[i].max_blocks = std::min(ctx->num_sms * 8, (int)std::max<long long>(1, Ps[i].h.total / 4096));
+    });
+    for (int i = 0; i < n_sets; ++i)
+      if (rcs[i]) return set_error(rcs[i], errs[i]);
   }
+  for (int i = 0; i < n_sets; ++i) {
+    in_at[i + 1] = in_at[i] + input_bytes(Ps[i].h);
+    tab_at[i + 1] = tab_at[i] + table_bytes(Ps[i].h, Ps[i].L, Ps[i].max_blocks);
+  }
+  const size_t ib = in_at[n_sets], tbytes = tab_at[n_sets];
   const size_t out_bytes = sizeof(TrainOut) * n_sets;
   lap(0);
   GP_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -2991,12 +3020,16 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
   if (!base) return GP_CUDA_ERROR;
   char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(ib, out_bytes) + 1024));
   if (!hp) return GP_CUDA_ERROR;
-  char* in = base;
-  char* tab = base + ib;
-  for (int i = 0; i < n_sets; ++i) carve_prepared(Ps[i], in, tab, base, hp);
+  // (input_bytes / table_bytes bound what carve_prepared takes: the sets carve in parallel)
+  parallel_sets(n_sets, [&](int i) {
+    char* in_i = base + in_at[i];
+    char* tab_i = base + ib + tab_at[i];
+    carve_prepared(Ps[i], in_i, tab_i, base, hp);
+  });
+  char* tab = base + ib + tbytes;
   TrainOut* d_out = carve<TrainOut>(tab, n_sets);
   for (int i = 0; i < n_sets; ++i) Ps[i].d_out = d_out + i;
-  const size_t in_bytes = (size_t)(in - base);
+  const size_t in_bytes = ib;
   GP_CUDA(cudaMemcpyAsync(base, hp, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h2d_bytes += (long long)in_bytes;
   lap(1);
