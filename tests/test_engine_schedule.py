@@ -34,11 +34,12 @@ def test_native_schedule_desk_golden():
     assert plan == _strip(golden("desk_plan.json"))
 
 
-@pytest.mark.parametrize("key", ["c3_64gpu/eta=1", "c4_256gpu/eta=2"])
+@pytest.mark.parametrize("key", ["c3_64gpu/eta=1", "c4_256gpu/eta=2", "c5_1024gpu/eta=2"])
 def test_multi_device_context_schedule(key):
     """gp_schedule on a multi-device context (every visible GPU, or two peer contexts on
-    device 0 of a one-GPU box): the iteration batches are split over the devices — and the
-    plan and trace equal the single-device run (and the reference golden where one exists)."""
+    device 0 of a one-GPU box): the iteration batches are split over the devices and the next
+    iteration's candidate bands are partitioned speculatively on the auxiliary context — and
+    the plan and trace equal the single-device run (and the reference golden where one exists)."""
     import torch
     from paper_2511_00796_b200.engine import Engine
     n = torch.cuda.device_count()
