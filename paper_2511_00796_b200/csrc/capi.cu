@@ -71,12 +71,16 @@ void* ctx_scratch(gp_ctx* ctx, size_t bytes, int arena) {
   void*& buf = ctx->scratch_arena[arena];
   size_t& have = ctx->scratch_arena_bytes[arena];
   if (bytes > have) {
-    if (buf) cudaFree(buf);
+    // stream-ordered (the device's pool): a grown arena does not synchronise the whole device,
+    // which other host threads (peer / auxiliary contexts on the same GPU) may be using. Every
+    // API call ends with ctx->stream synchronised after its lane streams, so the old buffer
+    // is idle when it is released.
+    if (buf) cudaFreeAsync(buf, ctx->stream);
     buf = nullptr;
     // 1.5x headroom with a 4 MiB floor: the scheduler's batches vary in size and a
     // cudaMalloc/cudaFree pair costs more than the kernels of a small batch
     size_t want = std::max(bytes + bytes / 2, (size_t)4 << 20);
-    cudaError_t e = cudaMalloc(&buf, want);
+    cudaError_t e = cudaMallocAsync(&buf, want, ctx->stream);
     if (e != cudaSuccess) {
       have = 0;
       cuda_fail(e, "cudaMalloc(scratch)");
@@ -262,6 +266,14 @@ int gp_ctx_create(const gp_cluster* c, const gp_workload* w, const gp_calib* k, 
 #undef UP
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(set_error(GP_CUDA_ERROR, "cudaStreamCreate failed"));
+  {  // the scratch arenas and MILP tables are stream-ordered allocations: keep freed blocks
+     // in the device pool instead of returning them at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   // kernel-image probe: fails loudly if this build has no sm_100a code for the device
   int* flag = static_cast<int*>(ctx_scratch(ctx, 1 << 20));
   if (!flag) return fail(GP_CUDA_ERROR);
@@ -280,6 +292,8 @@ void gp_ctx_destroy(gp_ctx* ctx) {
   if (!ctx) return;
   for (gp_ctx* peer : ctx->peers) gp_ctx_destroy(peer);
   ctx->peers.clear();
+  gp_ctx_destroy(ctx->aux);
+  ctx->aux = nullptr;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* ptrs[] = {ctx->d_type, ctx->d_machine, ctx->d_flops, ctx->d_hbm_bw, ctx->d_hbm_cap,
@@ -425,6 +439,13 @@ int gp_ctx_create_multi(const gp_cluster* c, const gp_workload* w, const gp_cali
       return rc;
     }
     primary->peers.push_back(peer);
+  }
+  if (n_devices > 1) {  // the scheduler's speculative-partition context (last device)
+    rc = gp_ctx_create(c, w, k, devices[n_devices - 1], &primary->aux);
+    if (rc) {
+      gp_ctx_destroy(primary);
+      return rc;
+    }
   }
   cudaSetDevice(primary->device);
   *out = primary;

@@ -251,6 +251,10 @@ struct gp_ctx {
   bool memo = true;
   // peer contexts on other GPUs (gp_ctx_create_multi): constrained_search fans out over them
   std::vector<gp_ctx*> peers;
+  // multi-device contexts: an auxiliary context on the last device, on which the native
+  // driver computes the next iteration's candidate partitions while the current iteration's
+  // evaluation batch runs (schedule.cu)
+  gp_ctx* aux = nullptr;
   // optional device timing of the train phases (bench.py): events around K2 and K1
   bool timing = false;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};

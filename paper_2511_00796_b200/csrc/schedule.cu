@@ -16,7 +16,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include "gp_internal.h"
@@ -43,10 +45,16 @@ namespace {
 // GPLAN_PROFILE=1: host wall time per driver phase (stderr)
 struct Phase {  // (contexts may be driven from several host threads: atomics)
   AtomicD sec[6];
+  std::atomic<long long> spec_bands{0}, spec_kept{0}, widen_hits{0}, widen_calls{0};
   ~Phase() {
     if (!std::getenv("GPLAN_PROFILE")) return;
-    static const char* n[6] = {"partition", "train_batch", "configs_batch", "milp_batch", "weight_sync", "host"};
+    static const char* n[6] = {"partition", "train_batch", "configs_batch", "milp_batch", "weight_sync", "total"};
     for (int i = 0; i < 6; ++i) std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", n[i], (double)sec[i]);
+    double gpu = 0;
+    for (int i = 0; i < 5; ++i) gpu += (double)sec[i];
+    std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", "host (rest)", (double)sec[5] - gpu);
+    std::fprintf(stderr, "gp_schedule speculative bands %lld (kept %lld); widen %lld calls, %lld cache hits\n",
+                 spec_bands.load(), spec_kept.load(), widen_calls.load(), widen_hits.load());
   }
 } g_phase;
 
@@ -56,7 +64,7 @@ struct PhaseTimer {
   NvtxRange nvtx;
   static const char* name(int i) {
     static const char* n[6] = {"gp_schedule/partition", "gp_schedule/train_batch", "gp_schedule/configs_batch",
-                               "gp_schedule/milp_batch", "gp_schedule/weight_sync", "gp_schedule/host"};
+                               "gp_schedule/milp_batch", "gp_schedule/weight_sync", "gp_schedule"};
     return n[i];
   }
   explicit PhaseTimer(int i) : id(i), nvtx(name(i)) {}
@@ -257,15 +265,32 @@ struct Driver {
       if (it != part_cache.end()) outs[i] = it->second;
       else todo.push_back((int)i);
     }
-    if (!todo.empty()) {
-      PhaseTimer pt(0);
-      const int k = std::max(1, o.candidate_width), q = (int)todo.size(), N = ctx->N;
-      gp_part_opts po{o.exact_threshold, o.restarts, o.seed, o.band_epsilon, o.force_local_search,
-                      o.machine_granularity};
+    if (todo.empty()) return GP_OK;
+    PhaseTimer pt(0);
+    const int k = std::max(1, o.candidate_width), N = ctx->N;
+    gp_part_opts po{o.exact_threshold, o.restarts, o.seed, o.band_epsilon, o.force_local_search,
+                    o.machine_granularity};
+    // every band runs partition_with_widening's loop (widen() below); the bands still
+    // infeasible after a round move to their next widening together, one batched call per
+    // round — each band sees exactly the sequence of bands widen() would try
+    std::vector<double> w(todo.size(), 0.0);
+    std::vector<int> live(todo.size());
+    for (size_t j = 0; j < todo.size(); ++j) live[j] = (int)j;
+    for (bool first = true; !live.empty(); first = false) {
+      if (!first)
+        for (int j : live) {
+          const Gamma& g = gs[todo[j]];
+          const double lo = g.gl - w[j], hi = g.gh + w[j];  // the attempt that failed
+          if (!(0.0 < lo) && !(hi < 1.0))
+            return set_error(GP_INFEASIBLE, "no feasible bisection exists even with an unconstrained band");
+          w[j] += o.band_widen_step;
+        }
+      const int q = (int)live.size();
       std::vector<gp_gamma> gg(q);
-      for (int j = 0; j < q; ++j) {
-        const Gamma& g = gs[todo[j]];
-        gg[j] = gp_gamma{g.q, g.r, (0.0 < g.gl) ? g.gl : 0.0, (g.gh < 1.0) ? g.gh : 1.0};
+      for (int m = 0; m < q; ++m) {
+        const Gamma& g = gs[todo[live[m]]];
+        const double lo = g.gl - w[live[m]], hi = g.gh + w[live[m]];
+        gg[m] = gp_gamma{g.q, g.r, (0.0 < lo) ? lo : 0.0, (hi < 1.0) ? hi : 1.0};
       }
       std::vector<gp_partition> parts((size_t)q * k);
       std::vector<int32_t> ids((size_t)q * k * N + 1);
@@ -274,39 +299,85 @@ struct Driver {
       int rc = partition_candidates_batch(ctx, q, gg.data(), &po, k, parts.data(), ids.data(), nout.data(),
                                           rcs.data());
       if (rc) return rc;
-      for (int j = 0; j < q; ++j) {
-        if (rcs[j] != GP_OK) continue;  // widened below
-        auto& res = outs[todo[j]];
-        const int32_t* idb = ids.data() + (size_t)j * k * N;
-        for (int e = 0; e < nout[j]; ++e) {
-          const gp_partition& pp = parts[(size_t)j * k + e];
+      std::vector<int> still;
+      for (int m = 0; m < q; ++m) {
+        if (rcs[m] != GP_OK) {  // GP_BAND_INFEASIBLE: widened in the next round
+          still.push_back(live[m]);
+          continue;
+        }
+        auto& res = outs[todo[live[m]]];
+        const int32_t* idb = ids.data() + (size_t)m * k * N;
+        for (int e = 0; e < nout[m]; ++e) {
+          const gp_partition& pp = parts[(size_t)m * k + e];
           res.emplace_back(idb + pp.train_offset, idb + pp.train_offset + pp.train_count);
         }
-        part_cache[std::make_pair(gs[todo[j]].gl, gs[todo[j]].gh)] = res;
+        part_cache[std::make_pair(gs[todo[live[m]]].gl, gs[todo[live[m]]].gh)] = res;
       }
+      live.swap(still);
     }
-    for (size_t i = 0; i < gs.size(); ++i)
-      if (outs[i].empty()) {
-        int rc = widen(gs[i], outs[i]);
-        if (rc) return rc;
-      }
     return GP_OK;
+  }
+
+  // Speculative partitions (multi-device contexts): the bands the NEXT iteration can ask for
+  // (refine_gamma moves to one of two midpoints) are computed on the auxiliary context while
+  // this iteration's evaluation batch runs. graph_partition_candidates is a pure function of
+  // the band, so a band that was feasible unwidened enters part_cache exactly as widen()
+  // would have stored it; an infeasible one is left to widen().
+  struct Spec {
+    std::vector<Gamma> gs;
+    std::vector<std::vector<std::vector<int>>> outs;
+    std::vector<int> rcs;
+    std::thread th;
+  };
+  void spec_start(Spec& sp, const std::vector<Gamma>& next) {
+    gp_ctx* aux = ctx->aux;
+    if (!aux) return;
+    for (const Gamma& g : next)
+      if (!part_cache.count(std::make_pair(g.gl, g.gh))) sp.gs.push_back(g);
+    const int q = (int)sp.gs.size();
+    if (q == 0) return;
+    g_phase.spec_bands += q;
+    sp.outs.assign(q, {});
+    sp.rcs.assign(q, GP_OK);
+    sp.th = std::thread([this, &sp, aux, q] {
+      cudaSetDevice(aux->device);
+      for (int j = 0; j < q; ++j) sp.rcs[j] = widen_compute(aux, sp.gs[j], sp.outs[j]);
+    });
+  }
+  void spec_finish(Spec& sp) {
+    if (!sp.th.joinable()) return;
+    sp.th.join();
+    cudaSetDevice(ctx->device);
+    for (size_t j = 0; j < sp.gs.size(); ++j) {
+      if (sp.rcs[j] != GP_OK) continue;  // (speculation only: widen() recomputes what is missing)
+      part_cache[std::make_pair(sp.gs[j].gl, sp.gs[j].gh)] = std::move(sp.outs[j]);
+      g_phase.spec_kept++;
+    }
   }
 
   // partition_with_widening (src/scheduler.cpp:21-40) -> candidate train sets, best first
   int widen(const Gamma& g, std::vector<std::vector<int>>& out) {
     auto key = std::make_pair(g.gl, g.gh);
     auto it = part_cache.find(key);
+    g_phase.widen_calls++;
     if (it != part_cache.end()) {
+      g_phase.widen_hits++;
       out = it->second;
       return GP_OK;
     }
     PhaseTimer pt(0);
+    int rc = widen_compute(ctx, g, out);
+    if (rc == GP_OK) part_cache[key] = out;
+    return rc;
+  }
+
+  // the widening loop itself on context c (the driver's, or the auxiliary one), uncached
+  int widen_compute(gp_ctx* c, const Gamma& g, std::vector<std::vector<int>>& out) const {
     const int k = std::max(1, o.candidate_width);
     gp_part_opts po{o.exact_threshold, o.restarts, o.seed, o.band_epsilon, o.force_local_search,
                     o.machine_granularity};
     std::vector<gp_partition> parts(k);
-    std::vector<int32_t> ids((size_t)k * ctx->N + 1);
+    std::vector<int32_t> ids((size_t)k * c->N + 1);
     double w = 0;
     while (true) {
       gp_gamma gg{g.q, g.r, 0, 0};
@@ -314,13 +385,12 @@ struct Driver {
       gg.gamma_l = (0.0 < lo) ? lo : 0.0;  // std::max(0.0, ...)
       gg.gamma_h = (hi < 1.0) ? hi : 1.0;  // std::min(1.0, ...)
       int32_t n = 0;
-      int rc = partition_candidates(ctx, &gg, &po, k, parts.data(), ids.data(), &n);
+      int rc = partition_candidates(c, &gg, &po, k, parts.data(), ids.data(), &n);
       if (rc == GP_OK) {
         out.clear();
         for (int i = 0; i < n; ++i)
           out.emplace_back(ids.begin() + parts[i].train_offset,
                            ids.begin() + parts[i].train_offset + parts[i].train_count);
-        part_cache[key] = out;
         return GP_OK;
       }
       if (rc != GP_BAND_INFEASIBLE) return rc;
@@ -404,17 +474,38 @@ int run_two_phase(Driver& D, Run& run) {
             if (ta != tb) return ta < tb;
             return a < b;
           });
-          std::vector<int> t;
+          std::vector<int> s;  // the first m + 1 devices of `order`, ascending (ids are distinct)
+          s.reserve(N);
           for (int m = 0; m + 1 < N; ++m) {
-            t.push_back(order[m]);
-            std::vector<int> s = t;
-            std::sort(s.begin(), s.end());
+            s.insert(std::upper_bound(s.begin(), s.end(), order[m]), order[m]);
             prefixes.push_back(s);
           }
         }
         batch.insert(batch.end(), prefixes.begin(), prefixes.end());
       }
-      rc = D.eval_batch(batch);  // every evaluation of this iteration in one GPU batch
+      {
+        // the next iteration's possible bands, partitioned on the auxiliary context meanwhile
+        Driver::Spec spec;
+        if (!frozen && ctx->aux) {
+          std::vector<Gamma> next;
+          if (iter == 1) {
+            Gamma g = gamma;
+            g.gl = g.gh = (gamma.q + gamma.r) / 2;
+            next.push_back(g);
+          } else {
+            Gamma lo = gamma, hi = gamma;  // refine_gamma's two outcomes
+            lo.r = (gamma.q + gamma.r) / 2.0;
+            lo.gl = lo.gh = (lo.q + lo.r) / 2.0;
+            hi.q = (gamma.q + gamma.r) / 2.0;
+            hi.gl = hi.gh = (hi.q + hi.r) / 2.0;
+            next.push_back(lo);
+            next.push_back(hi);
+          }
+          D.spec_start(spec, next);
+        }
+        rc = D.eval_batch(batch);  // every evaluation of this iteration in one GPU batch
+        D.spec_finish(spec);
+      }
       if (rc) return rc;
       it = D.get(cands.front());
       for (size_t c = 1; c < cands.size(); ++c) best.offer(D.get(cands[c]));
@@ -468,7 +559,7 @@ int run_two_phase(Driver& D, Run& run) {
 int schedule(gp_ctx* ctx, const gp_sched_opts* o, gp_schedule_result* res, int32_t* train_ids,
              int32_t* rollout_ids, int32_t* stage_devices, gp_config* entry_configs, gp_rollout_entry* entries,
              int32_t entry_cap, double* trace) {
-  NvtxRange nvtx("gp_schedule");
+  PhaseTimer total(5);
   std::memset(res, 0, sizeof *res);
   if (ctx->N < 2) return set_error(GP_INFEASIBLE, "scheduling requires at least two devices");
   const int eta = o->eta_override >= 0 ? o->eta_override : ctx->work.staleness;

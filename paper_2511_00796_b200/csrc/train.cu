@@ -2955,11 +2955,10 @@ int train_search(gp_ctx* ctx, const int32_t* ids, int n, int window, const gp_tr
   return rc;
 }
 
-// fn(i) for i < n on up to 16 host threads (inline below 64 items)
+// fn(i) for i < n on up to max_threads host threads (inline below 64 items)
 template <typename F>
-static void parallel_sets(int n, F fn) {
-  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-  const int nt = std::min({16, hw, n / 32});
+static void parallel_sets(int n, int max_threads, F fn) {
+  const int nt = std::min(max_threads, n / 32);
   if (nt <= 1) {
     for (int i = 0; i < n; ++i) fn(i);
     return;
@@ -2980,7 +2979,7 @@ static void parallel_sets(int n, F fn) {
 static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
                            const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices,
                            int mode, std::vector<std::array<long long, 4>>& nms,
-                           std::vector<std::vector<int32_t>>& ordered) {
+                           std::vector<std::vector<int32_t>>& ordered, int host_threads) {
   nms.assign(n_sets, {});
   ordered.assign(n_sets, {});
   if (n_sets <= 0) return GP_OK;
@@ -2995,7 +2994,7 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
   {  // host enumeration of every set's space, on several host threads for large batches
     std::vector<int> rcs(n_sets, GP_OK);
     std::vector<std::string> errs(n_sets);
-    parallel_sets(n_sets, [&](int i) {
+    parallel_sets(n_sets, host_threads, [&](int i) {
       rcs[i] = build_space(ctx, ids[i], ns[i], o, Ps[i].h);
       if (rcs[i]) {
         errs[i] = gp_last_error();  // (the message is thread-local)
@@ -3021,7 +3020,7 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
   char* hp = static_cast<char*>(ctx_pinned(ctx, std::max(ib, out_bytes) + 1024));
   if (!hp) return GP_CUDA_ERROR;
   // (input_bytes / table_bytes bound what carve_prepared takes: the sets carve in parallel)
-  parallel_sets(n_sets, [&](int i) {
+  parallel_sets(n_sets, host_threads, [&](int i) {
     char* in_i = base + in_at[i];
     char* tab_i = base + ib + tab_at[i];
     carve_prepared(Ps[i], in_i, tab_i, base, hp);
@@ -3148,13 +3147,13 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
 int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
                 const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices, int mode) {
   if (n_sets <= 0) return GP_OK;
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
   std::vector<std::string> keys(n_sets);
+  parallel_sets(n_sets, std::min(16, hw), [&](int i) { keys[i] = train_memo_key(ids[i], ns[i], o, mode); });
   std::vector<int> todo;
-  for (int i = 0; i < n_sets; ++i) {
-    keys[i] = train_memo_key(ids[i], ns[i], o, mode);
+  for (int i = 0; i < n_sets; ++i)
     if (!train_memo_get(ctx, keys[i], window, outs + i, stage_devices ? stage_devices[i] : nullptr))
       todo.push_back(i);
-  }
   if (todo.empty()) return GP_OK;
   const int q = (int)todo.size();
   std::vector<std::array<long long, 4>> nms(q);
@@ -3164,12 +3163,16 @@ int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_
   const int D = 1 + (int)ctx->peers.size();
   if (D > 1 && q > 1) {  // longest-processing-time assignment by layout count
     std::vector<std::pair<long long, int>> sz(q);
-    for (int j = 0; j < q; ++j) {
+    std::vector<int> src(q, GP_OK);
+    std::vector<std::string> serr(q);
+    parallel_sets(q, std::min(16, hw), [&](int j) {
       int64_t total = 0;
-      int rc = train_space(ctx, ids[todo[j]], ns[todo[j]], o, &total);
-      if (rc) return rc;
+      src[j] = train_space(ctx, ids[todo[j]], ns[todo[j]], o, &total);
+      if (src[j]) serr[j] = gp_last_error();  // (thread-local)
       sz[j] = {(long long)total, j};
-    }
+    });
+    for (int j = 0; j < q; ++j)
+      if (src[j]) return set_error(src[j], serr[j]);
     std::sort(sz.begin(), sz.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
     long long all = 0;
     for (const auto& e : sz) all += e.first;
@@ -3188,6 +3191,9 @@ int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_
   std::vector<std::string> errs(D);
   std::vector<std::vector<int>> part(D);
   for (int j = 0; j < q; ++j) part[dev_of[j]].push_back(j);
+  int busy = 0;  // device threads of this batch share the host's cores for set preparation
+  for (int d = 0; d < D; ++d) busy += part[d].empty() ? 0 : 1;
+  const int host_threads = std::max(1, std::min(16, hw / std::max(1, busy)));
   auto run = [&](int d) {
     gp_ctx* c = d == 0 ? ctx : ctx->peers[d - 1];
     const std::vector<int>& pj = part[d];
@@ -3205,7 +3211,7 @@ int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_
     std::vector<std::array<long long, 4>> nm2;
     std::vector<std::vector<int32_t>> or2;
     rcs[d] = train_batch_run(c, (int)pj.size(), id2.data(), n2.data(), window, o, r2.data(),
-                             stage_devices ? sd2.data() : nullptr, mode, nm2, or2);
+                             stage_devices ? sd2.data() : nullptr, mode, nm2, or2, host_threads);
     if (rcs[d]) {
       errs[d] = gp_last_error();
       return;
