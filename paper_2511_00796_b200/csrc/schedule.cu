@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <atomic>
 #include <memory>
 #include <thread>
@@ -44,14 +45,16 @@ namespace {
 
 // GPLAN_PROFILE=1: host wall time per driver phase (stderr)
 struct Phase {  // (contexts may be driven from several host threads: atomics)
-  AtomicD sec[6];
+  AtomicD sec[9];
   std::atomic<long long> spec_bands{0}, spec_kept{0}, widen_hits{0}, widen_calls{0};
   ~Phase() {
     if (!std::getenv("GPLAN_PROFILE")) return;
-    static const char* n[6] = {"partition", "train_batch", "configs_batch", "milp_batch", "weight_sync", "total"};
-    for (int i = 0; i < 6; ++i) std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", n[i], (double)sec[i]);
+    static const char* n[9] = {"partition", "train_batch", "configs_batch", "milp_batch", "weight_sync", "total",
+                               "eval_prep", "eval_post", "probe_lists"};
+    for (int i = 0; i < 9; ++i) std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", n[i], (double)sec[i]);
     double gpu = 0;
     for (int i = 0; i < 5; ++i) gpu += (double)sec[i];
+    for (int i = 6; i < 9; ++i) gpu += (double)sec[i];
     std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", "host (rest)", (double)sec[5] - gpu);
     std::fprintf(stderr, "gp_schedule speculative bands %lld (kept %lld); widen %lld calls, %lld cache hits\n",
                  spec_bands.load(), spec_kept.load(), widen_calls.load(), widen_hits.load());
@@ -63,8 +66,9 @@ struct PhaseTimer {
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   NvtxRange nvtx;
   static const char* name(int i) {
-    static const char* n[6] = {"gp_schedule/partition", "gp_schedule/train_batch", "gp_schedule/configs_batch",
-                               "gp_schedule/milp_batch", "gp_schedule/weight_sync", "gp_schedule"};
+    static const char* n[9] = {"gp_schedule/partition", "gp_schedule/train_batch", "gp_schedule/configs_batch",
+                               "gp_schedule/milp_batch", "gp_schedule/weight_sync", "gp_schedule",
+                               "gp_schedule/eval_prep", "gp_schedule/eval_post", "gp_schedule/probe_lists"};
     return n[i];
   }
   explicit PhaseTimer(int i) : id(i), nvtx(name(i)) {}
@@ -112,17 +116,19 @@ struct Driver {
 
   // evaluate_partition (src/scheduler.cpp:42-75) for every not-yet-memoised train set
   int eval_batch(const std::vector<std::vector<int>>& trains) {
+    PhaseTimer* pt = new PhaseTimer(6);
     std::vector<const std::vector<int>*> todo;
     {
-      std::map<std::vector<int>, int> seen;
+      auto less = [](const std::vector<int>* a, const std::vector<int>* b) { return *a < *b; };
+      std::set<const std::vector<int>*, decltype(less)> seen(less);  // (no copies of the sets)
       for (const auto& t : trains)
-        if (!memo.count(t) && !seen.count(t)) {
-          seen[t] = 1;
-          todo.push_back(&t);
-        }
+        if (!memo.count(t) && seen.insert(&t).second) todo.push_back(&t);
     }
     const int q = (int)todo.size();
-    if (q == 0) return GP_OK;
+    if (q == 0) {
+      delete pt;
+      return GP_OK;
+    }
     std::vector<std::unique_ptr<Eval>> ev(q);
     std::vector<const int32_t*> tids(q), rids(q);
     std::vector<int32_t> tn(q), rn(q);
@@ -139,9 +145,10 @@ struct Driver {
       rn[i] = (int32_t)ev[i]->roll.size();
       sdev[i] = ev[i]->stage_dev.data();
     }
+    delete pt;
     // train side: constrained_search
     std::vector<gp_train_result> tr(q);
-    PhaseTimer* pt = new PhaseTimer(1);
+    pt = new PhaseTimer(1);
     int rc = train_batch(ctx, q, tids.data(), tn.data(), window, &o.train, tr.data(), sdev.data());
     delete pt;
     if (rc) return rc;
@@ -247,7 +254,12 @@ struct Driver {
         e.c_infer = e.c_rollout + e.c_reward + e.c_update;
       }
     }
-    for (int i = 0; i < q; ++i) memo[ev[i]->train] = std::move(ev[i]);
+    pt = new PhaseTimer(7);
+    for (int i = 0; i < q; ++i) {
+      const std::vector<int>& key = ev[i]->train;
+      memo.emplace(key, std::move(ev[i]));
+    }
+    delete pt;
     evaluated += q;
     return GP_OK;
   }
@@ -259,28 +271,44 @@ struct Driver {
   // is infeasible continues with the sequential widening loop below (same result)
   int widen_batch(const std::vector<Gamma>& gs, std::vector<std::vector<std::vector<int>>>& outs) {
     outs.assign(gs.size(), {});
+    std::vector<Gamma> todo_g;
     std::vector<int> todo;
     for (size_t i = 0; i < gs.size(); ++i) {
       auto it = part_cache.find(std::make_pair(gs[i].gl, gs[i].gh));
-      if (it != part_cache.end()) outs[i] = it->second;
-      else todo.push_back((int)i);
+      if (it != part_cache.end()) {
+        outs[i] = it->second;
+      } else {
+        todo.push_back((int)i);
+        todo_g.push_back(gs[i]);
+      }
     }
     if (todo.empty()) return GP_OK;
     PhaseTimer pt(0);
-    const int k = std::max(1, o.candidate_width), N = ctx->N;
+    std::vector<std::vector<std::vector<int>>> res;
+    int rc = widen_rounds(ctx, todo_g, res);
+    if (rc) return rc;
+    for (size_t j = 0; j < todo.size(); ++j) {
+      outs[todo[j]] = res[j];
+      part_cache[std::make_pair(todo_g[j].gl, todo_g[j].gh)] = std::move(res[j]);
+    }
+    return GP_OK;
+  }
+
+  // partition_with_widening (src/scheduler.cpp:21-40) for several bands on context c, uncached:
+  // the bands still infeasible after a round move to their next widening together, one
+  // batched call per round — each band sees exactly the sequence of bands widen() would try
+  int widen_rounds(gp_ctx* c, const std::vector<Gamma>& gs, std::vector<std::vector<std::vector<int>>>& outs) const {
+    outs.assign(gs.size(), {});
+    const int k = std::max(1, o.candidate_width), N = c->N;
     gp_part_opts po{o.exact_threshold, o.restarts, o.seed, o.band_epsilon, o.force_local_search,
                     o.machine_granularity};
-    // every band runs partition_with_widening's loop (widen() below); the bands still
-    // infeasible after a round move to their next widening together, one batched call per
-    // round — each band sees exactly the sequence of bands widen() would try
-    std::vector<double> w(todo.size(), 0.0);
-    std::vector<int> live(todo.size());
-    for (size_t j = 0; j < todo.size(); ++j) live[j] = (int)j;
+    std::vector<double> w(gs.size(), 0.0);
+    std::vector<int> live(gs.size());
+    for (size_t j = 0; j < gs.size(); ++j) live[j] = (int)j;
     for (bool first = true; !live.empty(); first = false) {
       if (!first)
         for (int j : live) {
-          const Gamma& g = gs[todo[j]];
-          const double lo = g.gl - w[j], hi = g.gh + w[j];  // the attempt that failed
+          const double lo = gs[j].gl - w[j], hi = gs[j].gh + w[j];  // the attempt that failed
           if (!(0.0 < lo) && !(hi < 1.0))
             return set_error(GP_INFEASIBLE, "no feasible bisection exists even with an unconstrained band");
           w[j] += o.band_widen_step;
@@ -288,7 +316,7 @@ struct Driver {
       const int q = (int)live.size();
       std::vector<gp_gamma> gg(q);
       for (int m = 0; m < q; ++m) {
-        const Gamma& g = gs[todo[live[m]]];
+        const Gamma& g = gs[live[m]];
         const double lo = g.gl - w[live[m]], hi = g.gh + w[live[m]];
         gg[m] = gp_gamma{g.q, g.r, (0.0 < lo) ? lo : 0.0, (hi < 1.0) ? hi : 1.0};
       }
@@ -296,7 +324,7 @@ struct Driver {
       std::vector<int32_t> ids((size_t)q * k * N + 1);
       std::vector<int32_t> nout(q);
       std::vector<int> rcs(q);
-      int rc = partition_candidates_batch(ctx, q, gg.data(), &po, k, parts.data(), ids.data(), nout.data(),
+      int rc = partition_candidates_batch(c, q, gg.data(), &po, k, parts.data(), ids.data(), nout.data(),
                                           rcs.data());
       if (rc) return rc;
       std::vector<int> still;
@@ -305,13 +333,12 @@ struct Driver {
           still.push_back(live[m]);
           continue;
         }
-        auto& res = outs[todo[live[m]]];
+        auto& res = outs[live[m]];
         const int32_t* idb = ids.data() + (size_t)m * k * N;
         for (int e = 0; e < nout[m]; ++e) {
           const gp_partition& pp = parts[(size_t)m * k + e];
           res.emplace_back(idb + pp.train_offset, idb + pp.train_offset + pp.train_count);
         }
-        part_cache[std::make_pair(gs[todo[live[m]]].gl, gs[todo[live[m]]].gh)] = res;
       }
       live.swap(still);
     }
@@ -326,7 +353,7 @@ struct Driver {
   struct Spec {
     std::vector<Gamma> gs;
     std::vector<std::vector<std::vector<int>>> outs;
-    std::vector<int> rcs;
+    int rc = GP_OK;
     std::thread th;
   };
   void spec_start(Spec& sp, const std::vector<Gamma>& next) {
@@ -337,19 +364,17 @@ struct Driver {
     const int q = (int)sp.gs.size();
     if (q == 0) return;
     g_phase.spec_bands += q;
-    sp.outs.assign(q, {});
-    sp.rcs.assign(q, GP_OK);
-    sp.th = std::thread([this, &sp, aux, q] {
+    sp.th = std::thread([this, &sp, aux] {
       cudaSetDevice(aux->device);
-      for (int j = 0; j < q; ++j) sp.rcs[j] = widen_compute(aux, sp.gs[j], sp.outs[j]);
+      sp.rc = widen_rounds(aux, sp.gs, sp.outs);
     });
   }
   void spec_finish(Spec& sp) {
     if (!sp.th.joinable()) return;
     sp.th.join();
     cudaSetDevice(ctx->device);
+    if (sp.rc != GP_OK) return;  // (speculation only: widen() computes what is missing)
     for (size_t j = 0; j < sp.gs.size(); ++j) {
-      if (sp.rcs[j] != GP_OK) continue;  // (speculation only: widen() recomputes what is missing)
       part_cache[std::make_pair(sp.gs[j].gl, sp.gs[j].gh)] = std::move(sp.outs[j]);
       g_phase.spec_kept++;
     }
@@ -366,39 +391,14 @@ struct Driver {
       return GP_OK;
     }
     PhaseTimer pt(0);
-    int rc = widen_compute(ctx, g, out);
-    if (rc == GP_OK) part_cache[key] = out;
-    return rc;
+    std::vector<std::vector<std::vector<int>>> res;
+    int rc = widen_rounds(ctx, {g}, res);
+    if (rc) return rc;
+    out = res[0];
+    part_cache[key] = std::move(res[0]);
+    return GP_OK;
   }
 
-  // the widening loop itself on context c (the driver's, or the auxiliary one), uncached
-  int widen_compute(gp_ctx* c, const Gamma& g, std::vector<std::vector<int>>& out) const {
-    const int k = std::max(1, o.candidate_width);
-    gp_part_opts po{o.exact_threshold, o.restarts, o.seed, o.band_epsilon, o.force_local_search,
-                    o.machine_granularity};
-    std::vector<gp_partition> parts(k);
-    std::vector<int32_t> ids((size_t)k * c->N + 1);
-    double w = 0;
-    while (true) {
-      gp_gamma gg{g.q, g.r, 0, 0};
-      const double lo = g.gl - w, hi = g.gh + w;
-      gg.gamma_l = (0.0 < lo) ? lo : 0.0;  // std::max(0.0, ...)
-      gg.gamma_h = (hi < 1.0) ? hi : 1.0;  // std::min(1.0, ...)
-      int32_t n = 0;
-      int rc = partition_candidates(c, &gg, &po, k, parts.data(), ids.data(), &n);
-      if (rc == GP_OK) {
-        out.clear();
-        for (int i = 0; i < n; ++i)
-          out.emplace_back(ids.begin() + parts[i].train_offset,
-                           ids.begin() + parts[i].train_offset + parts[i].train_count);
-        return GP_OK;
-      }
-      if (rc != GP_BAND_INFEASIBLE) return rc;
-      if (gg.gamma_l <= 0.0 && gg.gamma_h >= 1.0)
-        return set_error(GP_INFEASIBLE, "no feasible bisection exists even with an unconstrained band");
-      w += o.band_widen_step;
-    }
-  }
 };
 
 struct BestTracker {  // src/scheduler.cpp:77-95
@@ -461,6 +461,7 @@ int run_two_phase(Driver& D, Run& run) {
         rc = D.widen(gamma, cands);
         if (rc) return rc;
       }
+      PhaseTimer* pl = new PhaseTimer(8);
       std::vector<std::vector<int>> batch = cands;
       if (iter == 1) {
         for (const auto& pc : grid) batch.insert(batch.end(), pc.begin(), pc.end());
@@ -483,6 +484,7 @@ int run_two_phase(Driver& D, Run& run) {
         }
         batch.insert(batch.end(), prefixes.begin(), prefixes.end());
       }
+      delete pl;
       {
         // the next iteration's possible bands, partitioned on the auxiliary context meanwhile
         Driver::Spec spec;

@@ -2473,6 +2473,7 @@ struct PreparedTrain {
 // GPLAN_PROFILE=1: memo hits / scanned sets / scanned layouts (stderr at exit)
 struct MemoStats {  // (updated from the per-device threads of train_batch: atomics)
   std::atomic<long long> hits{0}, scans{0}, layouts{0};
+  std::atomic<long long> size_sets[12] = {}, size_layouts[12] = {};  // scanned sets by log10(layouts)
   AtomicD ph[5];  // train_batch_run: build, carve+upload, launch, wait, fill
   std::atomic<unsigned long long> fast_cnt[2] = {{0}, {0}};
   void poll() {  // after a synchronisation
@@ -2491,6 +2492,11 @@ struct MemoStats {  // (updated from the per-device threads of train_batch: atom
                    "build %.3f s, carve+upload %.3f s, launch %.3f s, wait %.3f s, fill %.3f s\n", hits.load(),
                    scans.load(), layouts.load(), (double)ph[0], (double)ph[1], (double)ph[2], (double)ph[3],
                    (double)ph[4]);
+    if (std::getenv("GPLAN_PROFILE"))
+      for (int b = 0; b < 12; ++b)
+        if (size_sets[b].load())
+          std::fprintf(stderr, "train sets of 1e%d..1e%d layouts: %lld sets, %lld layouts\n", b, b + 1,
+                       size_sets[b].load(), size_layouts[b].load());
   }
 } g_memo_stats;
 
@@ -3104,6 +3110,8 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
     GP_CUDA(cudaGetLastError());
     GP_CUDA(cudaFreeAsync(d_ss, ctx->lane[R % NL]));  // (a pageable-source copy is staged on return)
   }
+  // (measured: sending the sets that fill the GPU alone to one lane, the rest round-robin on
+  // the others, is no faster on the C5 schedule)
   for (int i = 0, k = 0; i < n_sets; ++i) {
     if (is_small[i]) continue;
     const int l = k++ % NL;
@@ -3135,6 +3143,12 @@ static int train_batch_run(gp_ctx* ctx, int n_sets, const int32_t* const* ids, c
     ordered[i] = Ps[i].h.ordered;
     g_memo_stats.scans++;
     g_memo_stats.layouts += Ps[i].h.total;
+    {
+      int b = 0;
+      for (long long t = Ps[i].h.total; t >= 10 && b < 11; t /= 10) ++b;
+      g_memo_stats.size_sets[b]++;
+      g_memo_stats.size_layouts[b] += Ps[i].h.total;
+    }
   }
   lap(4);
   g_memo_stats.poll();

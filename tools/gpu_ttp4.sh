@@ -7,3 +7,4 @@ CUDA_VISIBLE_DEVICES=0 python -m pytest tests/test_engine_schedule.py -x -q -k m
 python tools/ttp_native.py c5_1024gpu/eta=2 > gpurun_out/ttp_1dev.log 2>&1
 python tools/ttp_native.py c5_1024gpu/eta=2 --devices 0,1,2,3 > gpurun_out/ttp_4dev.log 2>&1
 GPLAN_PROFILE=1 python tools/ttp_native.py c5_1024gpu/eta=2 --devices 0,1,2,3 > gpurun_out/ttp_4dev_prof.log 2>&1
+GPLAN_PROFILE=1 python tools/ttp_native.py c5_1024gpu/eta=2 > gpurun_out/ttp_1dev_prof.log 2>&1
