@@ -933,6 +933,7 @@ __global__ void k2m_middle_rows(const SufEnt* __restrict__ mch, int n, const dou
 // Per suffix choice: the fast-path tables (TrainTables::sf_*) and, per promotion count b and
 // donation count d, the (max total, max compute) of its stages — zero-layer stages counted
 // with the one layer the fix-up gives them, donors with the layers they keep.
+constexpr long long kFastMinSuffixes = 32;  // K1-fast: least mean last-run choices per prefix
 constexpr int kMaxLastBlocks = 256;  // per-warp rank-count bytes; the fast path takes <= 255 last-run blocks (else generic K1)
 // suffix stage slots past k point at this rank-count entry, which holds kSentinelCount: its
 // promotion test (count + j < extra) never holds, so the scan needs no per-suffix slot mask
@@ -1561,6 +1562,81 @@ __global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan(Tra
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
   NearMin nm = k1_scan_warps<R, DUMP>(sp, tb, blkf, L, rg, warp, n_warps, sP[threadIdx.x >> 5], sD[threadIdx.x >> 5]);
+  nm = nm_block_reduce(nm);
+  if (threadIdx.x == 0) partial[blockIdx.x] = nm;
+}
+
+// The generic scan for spaces whose last type run has few choices (a last run of one or two
+// machines: a handful of suffixes per prefix, so a warp per prefix would leave most lanes idle
+// and pay the serial prefix tabulation per handful of candidates). Each warp splits into
+// G = 32 / GS groups of GS lanes; group g walks the g-th contiguous slice of the warp's chunk
+// (one decode, then the odometer), the G groups in lockstep — their leaders tabulate G
+// prefixes at once — and each group's lanes the prefix's suffixes. A thread's keys grow along
+// its walk.
+template <int R, int GS, bool DUMP = false>
+__global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan_grouped(TrainSpace sp, TrainTables tb,
+                                                      const double2* __restrict__ blkf, int L,
+                                                      ScanRange rg, NearMin* __restrict__ partial) {
+  constexpr int G = 32 / GS;
+  __shared__ Prefix<R> sP[kK1Threads / 32][G];
+  __shared__ PrefixData<R> sD[kK1Threads / 32][G];
+  const int lane = threadIdx.x & 31, g = lane / GS, gl = lane % GS;
+  Prefix<R>& P = sP[threadIdx.x >> 5][g];
+  PrefixData<R>& D = sD[threadIdx.x >> 5][g];
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
+  long long b0 = kInfBits, k0 = LLONG_MAX, k1 = LLONG_MAX, k2 = LLONG_MAX, feasible = 0;
+  for (long long it = warp; it < n_items; it += n_warps) {
+    // group g walks its own contiguous slice of the work item: one decode, then the odometer
+    const long long p0 = rg.p_lo + it * rg.chunk;
+    const long long p_end = min(p0 + rg.chunk, rg.p_lo + rg.n_pref);
+    const long long cl = (rg.chunk + G - 1) / G;
+    long long p = p0 + g * cl;
+    const long long q_end = min(p + cl, p_end);
+    __syncwarp();
+    if (gl == 0 && p < q_end) prefix_decode<R>(sp, p, P);
+    for (long long t = 0; t < cl; ++t, ++p) {
+      const bool has = p < q_end;
+      __syncwarp();
+      if (gl == 0 && has) prefix_data<R>(sp, tb, blkf, P, D);
+      __syncwarp();
+      long long s0 = 0, s1 = 0, pbase = 0;
+      if (has) {
+        const long long ns = sp.cnt[R - 1][D.u];
+        s0 = p == rg.p_lo ? rg.s_lo : 0;
+        s1 = p == rg.p_hi ? rg.s_hi : ns;
+        pbase = P.base;
+      }
+      for (long long s = s0 + gl; s < s1; s += GS) {
+        const SufEnt e = tb.suf[s];
+        double x;
+        const bool ok = eval_layout<R, false>(sp, tb, blkf, L, D, e, x, nullptr, nullptr);
+        if (DUMP && pbase + s >= rg.dump_lo && pbase + s < rg.dump_hi)
+          rg.dump[pbase + s - rg.dump_lo] = ok ? x : __longlong_as_double(0x7ff0000000000000LL);
+        if (ok) {
+          ++feasible;
+          const long long d = __double_as_longlong(x) - b0;
+          if (d < 3) {
+            const long long key = pbase + s;
+            if (d < 0) {
+              k2 = d == -1 ? k1 : d == -2 ? k0 : LLONG_MAX;
+              k1 = d == -1 ? k0 : LLONG_MAX;
+              k0 = key;
+              b0 += d;
+            } else if (d == 1) {
+              k1 = min(k1, key);
+            } else if (d == 2) {
+              k2 = min(k2, key);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (gl == 0 && p + 1 < q_end) prefix_advance<R>(sp, P);
+    }
+  }
+  NearMin nm{b0, {k0, k1, k2}, feasible};
   nm = nm_block_reduce(nm);
   if (threadIdx.x == 0) partial[blockIdx.x] = nm;
 }
@@ -2245,6 +2321,17 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   const int occ = occ_tab[fast ? 1 : 0][R];
   const long long warps_total = (long long)ctx->num_sms * occ * (threads / 32);
   rg.chunk = std::max(1LL, rg.n_pref / (warps_total * (fast && GPV_DYN ? 24 : 6)));
+  // generic scan of a space with fewer than 32 suffixes per prefix on average: one prefix per
+  // lane (gs = 1) — the serial prefix decode and tabulation then run on all 32 lanes at once,
+  // and a handful of suffixes per lane follows (gs = 32: one prefix per warp, lanes over its
+  // suffixes). GPLAN_K1_UNGROUPED=1 / GPLAN_K1_GROUP=4: the other layouts (tests, A/B).
+  int gs = 32;
+  if (!fast && R > 1 && !std::getenv("GPLAN_K1_UNGROUPED") && h.total < 32 * std::max(1LL, h.n_prefix)) {
+    const char* ge = std::getenv("GPLAN_K1_GROUP");
+    gs = ge && std::atoi(ge) == 4 ? 4 : 1;
+    const long long G = 32 / gs;
+    rg.chunk = (rg.chunk + G - 1) / G * G;
+  }
   rg.work = slow_q ? slow_q + 1 + kSlowQueue : nullptr;
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
   long long blocks = (n_items + (threads / 32) - 1) / (threads / 32);
@@ -2264,6 +2351,11 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
       }
       n_partial += kDeferBlocks;
       ctx->launches += 2;
+    } else if (gs < 32) {  // few suffixes per prefix: groups of gs lanes, G prefixes in lockstep
+      auto go = [&](auto kern) { kern<<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, L, rg, partial); };
+      if (gs == 1) sc.dump ? go(k1_layout_scan_grouped<R, 1, true>) : go(k1_layout_scan_grouped<R, 1>);
+      else sc.dump ? go(k1_layout_scan_grouped<R, 4, true>) : go(k1_layout_scan_grouped<R, 4>);
+      ctx->launches++;
     } else {
       if (sc.dump) k1_layout_scan<R, true><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, L, rg, partial);
       else k1_layout_scan<R><<<(int)blocks, threads, 0, stream>>>(h.sp, tb, blkf, L, rg, partial);
@@ -2674,9 +2766,13 @@ static int launch_prepared(gp_ctx* ctx, PreparedTrain& P, int window, long long 
   const int R = h.sp.R;
   // (layer counts are tabulated as signed bytes: L <= 127; small spaces: the generic scan —
   // the fast path's extra table launches would dominate)
+  // K1-fast puts the last run's choices on the lanes of a warp and pays a table merge per
+  // prefix: with fewer than kFastMinSuffixes last-run choices per prefix on average (a last
+  // type run of one or two machines) most lanes idle and the generic scan is faster
   const int nlast = (h.sp.nc[R - 1] + 2) * (h.sp.nc[R - 1] + 1) / 2;
   const bool fast = h.exact_total && h.total >= (1LL << 20) && L <= 127 && nlast <= kSentinelBlock &&
-                    h.sp.nc[R - 1] + 2 <= kMaxJunction && !force_generic && !(generic_env && generic_env[0] == '1');
+                    h.sp.nc[R - 1] + 2 <= kMaxJunction && h.total >= kFastMinSuffixes * h.n_prefix &&
+                    !force_generic && !(generic_env && generic_env[0] == '1');
   if (used_fast) *used_fast = fast;
   unsigned long long*& slow_q = lane < 0 ? ctx->d_slow : ctx->d_slow_lane[lane];
   if (fast && !slow_q) GP_CUDA(cudaMalloc(&slow_q, sizeof(unsigned long long) * (2 + kSlowQueue)));

@@ -137,3 +137,46 @@ def test_shards_recombine_to_the_whole_space(engines, n_shards):
                 best = (r.cost, r.rank)
         want = case["windows"][str(w)]
         assert best == (want["cost"], want["rank"]) and feas == case["feasible"]
+
+
+@pytest.mark.parametrize("lead,m", [(0, 780), (0, 800), (1, 790), (1, 830), (2, 790)])
+def test_small_last_run_sets_vs_oracle(engines, lead, m):
+    """Type-aligned prefix probes whose last type run is one to a few machines (a handful of
+    last-run choices per prefix): the generic scan with one prefix per lane
+    (k1_layout_scan_grouped<R, 1>) gives the restatement's winner for windows 1..4 and its
+    feasible count; 4-lane groups (GPLAN_K1_GROUP=4) and one prefix per warp
+    (GPLAN_K1_UNGROUPED=1) agree; per-candidate values through the grouped DUMP kernel equal
+    the oracle's on random ranges."""
+    from common import type_prefix_sets
+    p = problem("c5_1024gpu")
+    eng, orc = engines["c5_1024gpu"], Oracle(p)
+    ids = type_prefix_sets(p, lead, [m])[0]
+    wins = [1, 2, 3, 4]
+    o = orc.constrained_search_tab(ids, wins)
+    want, feas, lay = o["windows"], o["feasible"], o["layouts"]
+    eng.set_memo(False)
+    try:
+        got = {w: eng.constrained_search_raw(ids, w)[0] for w in wins}
+        os.environ["GPLAN_K1_UNGROUPED"] = "1"
+        try:
+            plain = {w: eng.constrained_search_raw(ids, w)[0] for w in wins}
+        finally:
+            del os.environ["GPLAN_K1_UNGROUPED"]
+        os.environ["GPLAN_K1_GROUP"] = "4"
+        try:
+            grp4 = {w: eng.constrained_search_raw(ids, w)[0] for w in wins}
+        finally:
+            del os.environ["GPLAN_K1_GROUP"]
+    finally:
+        eng.set_memo(True)
+    for w in wins:
+        r = got[w]
+        assert (r.layouts, r.feasible) == (lay, feas)
+        assert (r.cost, r.rank) == want[w], (w, r.cost, r.rank, want[w])
+        assert (plain[w].cost, plain[w].rank, plain[w].feasible) == (r.cost, r.rank, r.feasible)
+        assert (grp4[w].cost, grp4[w].rank, grp4[w].feasible) == (r.cost, r.rank, r.feasible)
+    rng = np.random.default_rng(m)
+    rs = _ranges(lay, rng, 8, 4096, [want[w][1] for w in wins if want[w][1] >= 0])
+    ref = orc.layout_costs_tab(ids, rs)
+    g = np.concatenate([eng.debug_layout_costs(ids, lo, hi, path=1)[0] for lo, hi in rs])
+    np.testing.assert_array_equal(g.view(np.int64), ref.view(np.int64))
