@@ -1578,11 +1578,17 @@ __global__ void __launch_bounds__(kK1Threads, R <= 3 ? 4 : 2) k1_layout_scan_gro
                                                       const double2* __restrict__ blkf, int L,
                                                       ScanRange rg, NearMin* __restrict__ partial) {
   constexpr int G = 32 / GS;
-  __shared__ Prefix<R> sP[kK1Threads / 32][G];
-  __shared__ PrefixData<R> sD[kK1Threads / 32][G];
+  // groups share their prefix through shared memory; with one lane per prefix (GS == 1) the
+  // lane keeps it in its own (local) memory: per-lane structs in shared memory would put every
+  // lane's same field in the same bank
+  constexpr int GSH = GS == 1 ? 1 : G;
+  __shared__ Prefix<R> sP[kK1Threads / 32][GSH];
+  __shared__ PrefixData<R> sD[kK1Threads / 32][GSH];
   const int lane = threadIdx.x & 31, g = lane / GS, gl = lane % GS;
-  Prefix<R>& P = sP[threadIdx.x >> 5][g];
-  PrefixData<R>& D = sD[threadIdx.x >> 5][g];
+  Prefix<R> Pl;
+  PrefixData<R> Dl;
+  Prefix<R>& P = GS == 1 ? Pl : sP[threadIdx.x >> 5][GS == 1 ? 0 : g];
+  PrefixData<R>& D = GS == 1 ? Dl : sD[threadIdx.x >> 5][GS == 1 ? 0 : g];
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long n_items = (rg.n_pref + rg.chunk - 1) / rg.chunk;
