@@ -41,8 +41,8 @@ WINDOW = 3
 METRIC = "candidate plans evaluated/sec"
 # from the committed ncu capture of K1-fast on this workload (profiles/r01/)
 K1_PROFILE = "profiles/r02/k1_layout_scan_fast_ncu_summary.txt"
-K1_WARP_INST_PER_CAND = 4.178   # smsp__inst_executed.sum / candidates (10,093,214,114 / 2,415,919,104)
-K1_DRAM_BYTES_PER_LAUNCH = 1950208  # dram__bytes_read.sum + dram__bytes_write.sum (tables + middle rows, L2-resident)
+K1_WARP_INST_PER_CAND = 4.160   # smsp__inst_executed.sum / candidates (10,050,744,126 / 2,415,919,104)
+K1_DRAM_BYTES_PER_LAUNCH = 1629440  # dram__bytes_read.sum + dram__bytes_write.sum (tables + middle rows, L2-resident)
 UNIT = "plans/s"
 
 

@@ -1381,11 +1381,16 @@ __device__ __forceinline__ void prefix_merge(int lane, const TrainSpace& sp, con
   GP_CHECK(kp == P.u);
 #endif
   const int ncell = a_hi >= a_lo ? (a_hi - a_lo + 1) * (DM + 1) : 0;
+  // a0(a) = #{front entries i < kf : i + cnt1[i] < a}, the keys held in registers (the cell
+  // loop's shared-memory stores would otherwise force a reload per cell)
+  int key[NPF > 0 ? NPF : 1];
+#pragma unroll
+  for (int i = 0; i < NPF; ++i) key[i] = i < kf ? i + F.cnt1[i] : (1 << 20);
   for (int idx = lane; idx < ncell; idx += 32) {
     const int a = a_lo + idx / (DM + 1), d = idx % (DM + 1);
     int a0 = 0;
 #pragma unroll
-    for (int i = 0; i < NPF; ++i) a0 += (i < kf && i + F.cnt1[i] < a) ? 1 : 0;
+    for (int i = 0; i < NPF; ++i) a0 += key[i] < a ? 1 : 0;
     const int a1 = a - a0;
     GP_CHECK(a1 >= 0 && a1 <= k1 && a0 <= kf);
     const int nz = F.nzf[a0] + M.nz[a1];
