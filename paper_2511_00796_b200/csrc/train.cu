@@ -1140,6 +1140,46 @@ __device__ __forceinline__ void mid_fetch(int lane, const TrainTables& tb, Prefi
   if (lane == 0) F.mrow_c[b] = c;
 }
 
+// K1-fast's prefix step (lane 0): the tables need only the middle run's choice index, the
+// prefix stage count (kf + the middle row's k) and the rank base, so while the middle run has
+// a next choice within the stage budget only those advance; the middle run's cut positions
+// and P.u are left stale. At the middle run's last choice they are restored and the full
+// odometer (prefix_advance) carries into the front runs and resets the middle run.
+template <int R>
+__device__ __forceinline__ void prefix_advance_fast(const TrainSpace& sp, Prefix<R>& P, int u_cur) {
+  if constexpr (R < 2) {
+    prefix_advance<R>(sp, P);
+  } else {
+    constexpr int rm = R - 2;
+    int used = 0;
+#pragma unroll
+    for (int r = 0; r < rm; ++r) used += P.k[r];
+    const int nc = sp.nc[rm];
+    // the middle run's largest stage count the odometer reaches (prefix_advance's growth test)
+    const int kallow = min(min(sp.kmax[rm], sp.max_stages - used - 1), nc + 1);
+    long long nallow = 0;  // its choices with 1..kallow stages (run_compositions order)
+#pragma unroll
+    for (int k = 1; k <= kMaxPerRun; ++k)
+      if (k <= kallow) nallow += binom_small(nc, k - 1);
+    if (P.ci[rm] + 1 < nallow) {
+      P.base += sp.cnt[R - 1][u_cur];
+      P.ci[rm]++;
+      return;
+    }
+    const int m = kallow - 1;  // the last choice: cut positions nc - m + 1 .. nc
+    P.k[rm] = kallow;
+    P.b[rm][0] = 0;
+#pragma unroll
+    for (int j = 1; j <= kMaxPerRun; ++j) {
+      if (j <= m) P.b[rm][j] = nc - (m - j);
+      else if (j == m + 1) P.b[rm][j] = nc + 1;
+    }
+    P.u = used + kallow;
+    GP_CHECK(P.u == u_cur);
+    prefix_advance<R>(sp, P);
+  }
+}
+
 // R == 1 (no prefix runs): empty prefix tables.
 template <int R>
 __device__ __forceinline__ void prefix_single(int lane, PrefixData<R>& D, PrefixFast<R>& F, unsigned char* cntb,
@@ -1366,7 +1406,7 @@ __device__ __forceinline__ void prefix_merge(int lane, const TrainSpace& sp, con
   }
   if (lane == 0) {
     F.bad = 0;
-    D.u = P.u;
+    D.u = kf + k1;  // (P.u is not maintained by prefix_advance_fast)
   }
   __syncwarp();
   const int fp_all = F.fpf + M.fs;
@@ -1378,7 +1418,6 @@ __device__ __forceinline__ void prefix_merge(int lane, const TrainSpace& sp, con
     F.a_lo = a_lo;
     F.a_hi = a_hi;
   }
-  GP_CHECK(kp == P.u);
 #endif
   const int ncell = a_hi >= a_lo ? (a_hi - a_lo + 1) * (DM + 1) : 0;
   // a0(a) = #{front entries i < kf : i + cnt1[i] < a}, the keys held in registers (the cell
@@ -1869,7 +1908,7 @@ __global__ void __launch_bounds__(kK1Threads, GPV_CTAS) k1_layout_scan_fast(Trai
         }
       }
       __syncwarp();
-      if (lane == 0 && p + 1 < p_end) prefix_advance<R>(sp, P);
+      if (lane == 0 && p + 1 < p_end) prefix_advance_fast<R>(sp, P, kp);
     }
 #if GPV_DYN
     unsigned long long nx = 0;
