@@ -595,6 +595,7 @@ int rollout_configs(gp_ctx* ctx, const int32_t* ids, int n, const gp_rollout_opt
 // agrees); each is then a backtrack from its own full state.
 struct MilpTable {
   std::vector<unsigned char> sig;  // configs + dims
+  unsigned long long sig_hash = 0;  // FNV-1a of sig (compared before the bytes)
   MilpDims d{};
   void* buf = nullptr;  // best | choice | order | level offsets/hist/cursor | groups | members | h
   size_t bytes = 0;
@@ -670,6 +671,12 @@ static void set_dims(MilpDims& d, int dims, const int* caps) {
   d.levels = levels;
 }
 
+static unsigned long long sig_hash(const std::vector<unsigned char>& v) {
+  unsigned long long h = 1469598103934665603ULL;
+  for (unsigned char c : v) h = (h ^ c) * 1099511628211ULL;
+  return h;
+}
+
 // Table key: the configs' fields (not their padding bytes) + dims.
 static std::vector<unsigned char> milp_sig(const gp_config* cfg, int nc, int dims) {
   std::vector<unsigned char> sig;
@@ -713,9 +720,10 @@ static int plan_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, const
   if (!ctx->milp_cache) ctx->milp_cache = new MilpCache();
   MilpCache& mc = *static_cast<MilpCache*>(ctx->milp_cache);
   const std::vector<unsigned char> sig = milp_sig(cfg, nc, dims);
+  const unsigned long long sh = sig_hash(sig);
   MilpTable* same = nullptr;
   for (auto& t : mc.tables) {
-    if (t->sig != sig) continue;
+    if (t->sig_hash != sh || t->sig != sig) continue;
     bool covers = true;
     for (int u = 0; u < dims && covers; ++u) covers = caps[u] <= t->d.cap[u];
     if (covers) {
@@ -794,6 +802,7 @@ static int plan_table(gp_ctx* ctx, const gp_config* cfg, int nc, int dims, const
       tab = mc.tables.back().get();
     }
     tab->sig = sig;
+    tab->sig_hash = sh;
   }
   GP_CUDA(cudaStreamSynchronize(ctx->stream));  // the pinned staging buffer is reused below
   if (!mc.pool_ready) {  // stream-ordered allocations stay in the device pool between tables
@@ -1045,12 +1054,16 @@ static int milp_batch_one(gp_ctx* ctx, int q, const gp_config* const* cfgs, cons
     if (ncs[i] == 0) { rcs[i] = GP_INFEASIBLE; continue; }
     if (milp_check(ncs[i], caps[i], dims)) rcs[i] = GP_INVALID;
   }
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sigs[a] < sigs[b]; });
+  std::vector<unsigned long long> hs(q);
+  for (int i = 0; i < q; ++i) hs[i] = sig_hash(sigs[i]);
+  // group equal config lists (hash first; the grouping order only decides table planning order)
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return hs[a] != hs[b] ? hs[a] < hs[b] : sigs[a] < sigs[b]; });
   std::vector<std::vector<int>> all_parts;  // queries per table, over all config lists
   std::vector<std::vector<int>> all_caps;   // each table's lattice
   for (size_t g0 = 0; g0 < order.size();) {
     size_t g1 = g0;
-    while (g1 < order.size() && sigs[order[g1]] == sigs[order[g0]]) ++g1;
+    while (g1 < order.size() && hs[order[g1]] == hs[order[g0]] && sigs[order[g1]] == sigs[order[g0]]) ++g1;
     std::vector<int> live;
     for (size_t j = g0; j < g1; ++j)
       if (rcs[order[j]] == GP_OK) live.push_back(order[j]);
