@@ -214,6 +214,8 @@ def test_four_type_runs(monkeypatch):
     ids = list(range(p.cluster.n))
     total = engine(name).train_space(ids)
     assert total == orc.train_space(ids) and total > 1 << 20
+    _, fast_used = engine(name).debug_layout_costs(ids, 0, 4096, path=0)
+    assert fast_used == 4  # K1-fast, the last of the 4 type runs innermost
     fast = run(name, ids, 3, lo=0, hi=total)
     monkeypatch.setenv("GPLAN_K1_GENERIC", "1")
     generic = run(name, ids, 3, lo=0, hi=total)
