@@ -629,17 +629,17 @@ struct MilpCache {
 // GPLAN_PROFILE=1: lattice tables built / reused, states tabulated, DP and backtrack wall time
 struct MilpStats {  // (updated from the per-device threads of milp_batch: atomics)
   std::atomic<long long> built{0}, reused{0}, states{0}, backtracks{0}, queries{0}, mallocs{0};
-  AtomicD dp_s, bt_s, malloc_s, prep_s, kern_s;
+  AtomicD dp_s, bt_s, malloc_s, prep_s, kern_s, sig_s, plan_s;
   std::atomic<long long> levels{0}, groups{0};
   ~MilpStats() {
     if (std::getenv("GPLAN_PROFILE"))
       std::fprintf(stderr,
                    "milp: %lld tables built (%lld states, %lld mallocs, %.3f s), %lld reused, %lld backtrack "
                    "launches for %lld queries (%.3f s); malloc %.3f s, level sort %.3f s, dp kernel %.3f s, "
-                   "%lld levels, %lld groups\n",
+                   "%lld levels, %lld groups; signatures %.3f s, table planning %.3f s\n",
                    built.load(), states.load(), mallocs.load(), (double)dp_s, reused.load(), backtracks.load(),
                    queries.load(), (double)bt_s, (double)malloc_s, (double)prep_s, (double)kern_s, levels.load(),
-                   groups.load());
+                   groups.load(), (double)sig_s, (double)plan_s);
   }
 } g_milp_stats;
 
@@ -1042,6 +1042,7 @@ static int milp_batch_one(gp_ctx* ctx, int q, const gp_config* const* cfgs, cons
                           const int32_t* const* caps, int dims, const double* Bs, double len,
                           gp_rollout_result* outs, gp_rollout_entry* const* entries, int* rcs) {
   // group queries with identical config lists
+  const double t_sig = now_s();
   std::vector<int> order(q);
   std::vector<std::vector<unsigned char>> sigs(q);
   for (int i = 0; i < q; ++i) {
@@ -1101,7 +1102,9 @@ static int milp_batch_one(gp_ctx* ctx, int q, const gp_config* const* cfgs, cons
     }
     g0 = g1;
   }
+  g_milp_stats.sig_s += now_s() - t_sig;
   // every table of the batch planned first (cached or new), the new ones' DPs batched
+  const double t_plan = now_s();
   if (!ctx->milp_cache) ctx->milp_cache = new MilpCache();
   static_cast<MilpCache*>(ctx->milp_cache)->epoch++;
   std::vector<MilpTable*> tabs(all_parts.size()), pend;
@@ -1112,6 +1115,7 @@ static int milp_batch_one(gp_ctx* ctx, int q, const gp_config* const* cfgs, cons
     if (rc) return rc;
     if (pending) pend.push_back(tabs[pidx]);
   }
+  g_milp_stats.plan_s += now_s() - t_plan;
   {
     int rc = run_pending(ctx, pend);
     if (rc) return rc;

@@ -1041,7 +1041,7 @@ constexpr int kK1Threads = 128;
 // K1-fast variant switches (A/B measurements with tools/build_variant.sh + k1_variants.sh);
 // the defaults are the product
 #ifndef GPV_CTAS
-#define GPV_CTAS 6   // K1-fast launch bounds: min CTAs per SM (6: 72 registers, 7 resident; 7: slower)
+#define GPV_CTAS 6   // K1-fast launch bounds: min CTAs per SM (6: 72 registers, 7 resident; 7: same, 5: -17%)
 #endif
 #ifndef GPV_DYN
 #define GPV_DYN 1    // K1-fast: prefix chunks handed out by an atomic counter (finer, balanced)
@@ -1049,6 +1049,11 @@ constexpr int kK1Threads = 128;
 #ifndef GPV_GS
 #define GPV_GS 4     // lanes per promotion count in the per-prefix tables
 #endif
+#ifndef GPV_UNROLL
+#define GPV_UNROLL 2  // K1-fast candidate loop unroll
+#endif
+#define GPV_PRAGMA_(x) _Pragma(#x)
+#define GPV_PRAGMA(x) GPV_PRAGMA_(x)
 #ifndef GPV_MERGE
 #define GPV_MERGE 1  // 1: zero-layer donors by the co-rank of the two donor sequences (no loop) (-0.4 ms)
 #endif
@@ -1789,7 +1794,7 @@ __global__ void __launch_bounds__(kK1Threads, GPV_CTAS) k1_layout_scan_fast(Trai
       const long long s1 = p == rg.p_hi ? rg.s_hi : ns;
       // table-scored count: every candidate of this lane, less the deferred ones (below)
       if (s0 + lane < s1) n_tab += (unsigned)((s1 - s0 - lane + 31) >> 5);
-#pragma unroll 2  // (with 6 CTAs/SM: two candidates in flight per lane, measured +10%)
+GPV_PRAGMA(unroll GPV_UNROLL)  // (2: two candidates in flight per lane; 1 measures the same, 3 slower)
       for (unsigned s = (unsigned)s0 + lane; s < (unsigned)s1; s += 32) {  // (suffix indices fit 32 bits)
         const int4 A = __ldg(tb.sf_hot + s);  // fs, nz4 | k << 8 | 8*b1 << 16, rb0..3, nzs0..3
         const int fk = (int)__byte_perm((unsigned)A.y, 0u, 0x4441);
