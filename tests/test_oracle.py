@@ -162,3 +162,13 @@ def test_full_golden_c4_recomputed():
         assert r["feasible"] == case["feasible"] and r["layouts"] == case["layouts"]
         for w, (c, k) in r["windows"].items():
             assert case["windows"][str(w)] == {"cost": c, "rank": k}
+
+
+def test_c4_schedule_restatement_equals_reference():
+    """The C restatement's whole C4 schedule fixture (schedule_c4_oracle.json) == the unmodified
+    reference's own C4 schedule (schedule_c4_reference.json): plan and trace."""
+    from common import golden
+    r = golden("schedule_c4_reference.json")["c4_256gpu/eta=2"]
+    o = golden("schedule_c4_oracle.json")["c4_256gpu/eta=2"]
+    assert {k: v for k, v in o.items() if k not in ("trace", "evaluated_partitions", "oracle_seconds")} == r["plan"]
+    assert o["trace"] == r["trace"]
