@@ -440,7 +440,8 @@ int gp_ctx_create_multi(const gp_cluster* c, const gp_workload* w, const gp_cali
     }
     primary->peers.push_back(peer);
   }
-  if (n_devices > 1) {  // the scheduler's speculative-partition context (last device)
+  const char* aux_env = std::getenv("GPLAN_AUX_SAME_DEVICE");  // (A/B: speculation on one GPU)
+  if (n_devices > 1 || (aux_env && aux_env[0] == '1')) {  // the scheduler's speculative-partition context (last device)
     rc = gp_ctx_create(c, w, k, devices[n_devices - 1], &primary->aux);
     if (rc) {
       gp_ctx_destroy(primary);
