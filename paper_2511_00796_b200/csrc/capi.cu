@@ -146,6 +146,21 @@ static int validate(const gp_cluster* c, const gp_workload* w, const gp_calib* k
   return GP_OK;
 }
 
+// An auxiliary context on ctx's device for the driver's speculative partitions (schedule.cu),
+// rebuilt from ctx's own copies of the inputs.
+int ctx_make_aux(gp_ctx* ctx) {
+  if (ctx->aux) return GP_OK;
+  std::vector<double> links((size_t)ctx->N * ctx->N);
+  GP_CUDA(cudaSetDevice(ctx->device));
+  GP_CUDA(cudaMemcpy(links.data(), ctx->d_links, sizeof(double) * links.size(), cudaMemcpyDeviceToHost));
+  gp_cluster c{ctx->N, ctx->T, ctx->M, ctx->h_type.data(), ctx->h_machine.data(), ctx->h_flops.data(),
+               ctx->h_hbm_bw.data(), ctx->h_hbm_cap.data(), ctx->h_tflops.data(), ctx->h_thbm.data(),
+               ctx->h_tcap.data(), links.data()};
+  gp_calib k = ctx->calib;
+  k.compute_eff = ctx->h_ceff.data();
+  k.io_eff = ctx->h_ioeff.data();
+  return gp_ctx_create(&c, &ctx->work, &k, ctx->device, &ctx->aux);
+}
 }  // namespace gp
 
 using namespace gp;
@@ -424,6 +439,7 @@ int gp_constrained_search_range(gp_ctx* ctx, const int32_t* ids, int32_t n, int3
   return search_fanout(ctx, ids, n, window, o, lo, hi, out, stage_devices, nm);
 }
 
+
 int gp_ctx_create_multi(const gp_cluster* c, const gp_workload* w, const gp_calib* k,
                         const int* devices, int n_devices, gp_ctx** out) {
   *out = nullptr;
@@ -440,8 +456,7 @@ int gp_ctx_create_multi(const gp_cluster* c, const gp_workload* w, const gp_cali
     }
     primary->peers.push_back(peer);
   }
-  const char* aux_env = std::getenv("GPLAN_AUX_SAME_DEVICE");  // (A/B: speculation on one GPU)
-  if (n_devices > 1 || (aux_env && aux_env[0] == '1')) {  // the scheduler's speculative-partition context (last device)
+  if (n_devices > 1) {  // the scheduler's speculative-partition context (last device)
     rc = gp_ctx_create(c, w, k, devices[n_devices - 1], &primary->aux);
     if (rc) {
       gp_ctx_destroy(primary);

@@ -28,6 +28,7 @@ namespace gp {
 
 int train_batch(gp_ctx* ctx, int n_sets, const int32_t* const* ids, const int32_t* ns, int window,
                 const gp_train_opts* o, gp_train_result* outs, int32_t* const* stage_devices, int mode = 0);
+int ctx_make_aux(gp_ctx* ctx);
 int configs_batch(gp_ctx* ctx, int q, const int32_t* const* ids, const int32_t* ns, const gp_rollout_opts* o,
                   std::vector<std::vector<gp_config>>& out, std::vector<int>* uniq_of = nullptr);
 int milp_batch(gp_ctx* ctx, int q, const gp_config* const* cfgs, const int* ncs, const int32_t* const* caps,
@@ -401,6 +402,14 @@ struct Driver {
 
 };
 
+static bool spec_off() {
+  static const bool off = [] {
+    const char* e = std::getenv("GPLAN_SPECULATE");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 struct BestTracker {  // src/scheduler.cpp:77-95
   const Eval* conforming = nullptr;
   const Eval* any = nullptr;
@@ -488,7 +497,7 @@ int run_two_phase(Driver& D, Run& run) {
       {
         // the next iteration's possible bands, partitioned on the auxiliary context meanwhile
         Driver::Spec spec;
-        if (!frozen && ctx->aux) {
+        if (!frozen && ctx->aux && !spec_off()) {
           std::vector<Gamma> next;
           if (iter == 1) {
             Gamma g = gamma;
@@ -564,6 +573,17 @@ int schedule(gp_ctx* ctx, const gp_sched_opts* o, gp_schedule_result* res, int32
   PhaseTimer total(5);
   std::memset(res, 0, sizeof *res);
   if (ctx->N < 2) return set_error(GP_INFEASIBLE, "scheduling requires at least two devices");
+  {  // speculative partitions: on multi-device contexts (their auxiliary context); on a one-GPU
+     // context only with GPLAN_SPECULATE=1 (an auxiliary context on the same GPU: measured
+     // within noise on C5, the partitions then compete with the train scans for the SMs);
+     // GPLAN_SPECULATE=0 turns them off
+    const char* e = std::getenv("GPLAN_SPECULATE");
+    const bool force = e && e[0] == '1';
+    if (!ctx->aux && ctx->peers.empty() && force) {
+      int rc = ctx_make_aux(ctx);
+      if (rc) return rc;
+    }
+  }
   const int eta = o->eta_override >= 0 ? o->eta_override : ctx->work.staleness;
   // WindowExpander (inc/rollout_milp.hpp:51-81)
   const int cap = o->delta_cap;
