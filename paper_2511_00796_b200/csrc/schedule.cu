@@ -46,16 +46,16 @@ namespace {
 
 // GPLAN_PROFILE=1: host wall time per driver phase (stderr)
 struct Phase {  // (contexts may be driven from several host threads: atomics)
-  AtomicD sec[9];
+  AtomicD sec[10];
   std::atomic<long long> spec_bands{0}, spec_kept{0}, widen_hits{0}, widen_calls{0};
   ~Phase() {
     if (!std::getenv("GPLAN_PROFILE")) return;
-    static const char* n[9] = {"partition", "train_batch", "configs_batch", "milp_batch", "weight_sync", "total",
-                               "eval_prep", "eval_post", "probe_lists"};
-    for (int i = 0; i < 9; ++i) std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", n[i], (double)sec[i]);
+    static const char* n[10] = {"partition", "train_batch", "configs_batch", "milp_batch", "weight_sync", "total",
+                               "eval_prep", "eval_post", "probe_lists", "spec_wait"};
+    for (int i = 0; i < 10; ++i) std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", n[i], (double)sec[i]);
     double gpu = 0;
     for (int i = 0; i < 5; ++i) gpu += (double)sec[i];
-    for (int i = 6; i < 9; ++i) gpu += (double)sec[i];
+    for (int i = 6; i < 10; ++i) gpu += (double)sec[i];
     std::fprintf(stderr, "gp_schedule %-14s %9.3f s\n", "host (rest)", (double)sec[5] - gpu);
     std::fprintf(stderr, "gp_schedule speculative bands %lld (kept %lld); widen %lld calls, %lld cache hits\n",
                  spec_bands.load(), spec_kept.load(), widen_calls.load(), widen_hits.load());
@@ -67,9 +67,10 @@ struct PhaseTimer {
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   NvtxRange nvtx;
   static const char* name(int i) {
-    static const char* n[9] = {"gp_schedule/partition", "gp_schedule/train_batch", "gp_schedule/configs_batch",
+    static const char* n[10] = {"gp_schedule/partition", "gp_schedule/train_batch", "gp_schedule/configs_batch",
                                "gp_schedule/milp_batch", "gp_schedule/weight_sync", "gp_schedule",
-                               "gp_schedule/eval_prep", "gp_schedule/eval_post", "gp_schedule/probe_lists"};
+                               "gp_schedule/eval_prep", "gp_schedule/eval_post", "gp_schedule/probe_lists",
+                               "gp_schedule/spec_wait"};
     return n[i];
   }
   explicit PhaseTimer(int i) : id(i), nvtx(name(i)) {}
@@ -372,7 +373,10 @@ struct Driver {
   }
   void spec_finish(Spec& sp) {
     if (!sp.th.joinable()) return;
-    sp.th.join();
+    {
+      PhaseTimer pt(9);  // (time the evaluation batch waited for the speculation)
+      sp.th.join();
+    }
     cudaSetDevice(ctx->device);
     if (sp.rc != GP_OK) return;  // (speculation only: widen() computes what is missing)
     for (size_t j = 0; j < sp.gs.size(); ++j) {
