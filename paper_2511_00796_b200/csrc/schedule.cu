@@ -135,7 +135,7 @@ struct Driver {
     std::vector<const int32_t*> tids(q), rids(q);
     std::vector<int32_t> tn(q), rn(q);
     std::vector<int32_t*> sdev(q);
-    for (int i = 0; i < q; ++i) {
+    auto make = [&](int i) {
       ev[i] = std::make_unique<Eval>();
       ev[i]->train = *todo[i];
       ev[i]->roll = complement(*todo[i]);
@@ -146,6 +146,19 @@ struct Driver {
       rids[i] = ev[i]->roll.data();
       rn[i] = (int32_t)ev[i]->roll.size();
       sdev[i] = ev[i]->stage_dev.data();
+    };
+    {  // (iteration 1: thousands of sets, built on several host threads)
+      const int nt = std::min({8, (int)std::max(1u, std::thread::hardware_concurrency()), q / 256});
+      if (nt <= 1) {
+        for (int i = 0; i < q; ++i) make(i);
+      } else {
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+          th.emplace_back([&, t] {
+            for (int i = t; i < q; i += nt) make(i);
+          });
+        for (auto& x : th) x.join();
+      }
     }
     delete pt;
     // train side: constrained_search
