@@ -1049,6 +1049,9 @@ constexpr int kK1Threads = 128;
 #ifndef GPV_GS
 #define GPV_GS 4     // lanes per promotion count in the per-prefix tables
 #endif
+#ifndef GPV_ITEMS
+#define GPV_ITEMS 24  // K1-fast: work items per warp (atomic-counter chunks; 12 and 48: -0.5 / -1 %)
+#endif
 #ifndef GPV_MINCHUNK
 #define GPV_MINCHUNK 16  // K1-fast: least prefixes per work item (1.5e8-layout set: 1.07 -> 0.81 ms; 64: 0.92)
 #endif
@@ -2378,7 +2381,7 @@ int launch_scan(gp_ctx* ctx, const HostSpace& h, const TrainTables& tb, const do
   });
   const int occ = occ_tab[fast ? 1 : 0][R];
   const long long warps_total = (long long)ctx->num_sms * occ * (threads / 32);
-  rg.chunk = std::max(1LL, rg.n_pref / (warps_total * (fast && GPV_DYN ? 24 : 6)));
+  rg.chunk = std::max(1LL, rg.n_pref / (warps_total * (fast && GPV_DYN ? GPV_ITEMS : 6)));
   // K1-fast: a work item starts with a prefix decode and, when its front differs from the
   // warp's last one, a front-table rebuild; keep items long enough to amortise both
   if (fast) rg.chunk = std::max<long long>(rg.chunk, GPV_MINCHUNK);
